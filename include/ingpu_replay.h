@@ -1,0 +1,219 @@
+/*
+ * include/ingpu_replay.h -- C-ABI of the B200-native in-GPU experience replay and its
+ * device-resident DQN / Double-DQN train step (Parr, "Deep In-GPU Experience Replay",
+ * arXiv 1801.03138).
+ *
+ * Citation keys: P:n = PAPER.md line n (section in brackets); S:n = SPEC.md line n;
+ * Qk = reading k of DESIGN.md "Readings of the paper".
+ *
+ * General conventions
+ *   - Every call returns an int status (RPL_OK = 0; > 0 informational; < 0 error).
+ *     Argument errors are detected on the host, returned synchronously and leave no
+ *     partial effect.  Errors detected on the device (corrupt terminal flag from
+ *     a device-sourced add, non-finite loss) set a sticky per-handle flag that the next
+ *     rpl_check() reports; rpl_last_error() gives a thread-local message.
+ *   - All work is enqueued asynchronously on the handle's CUDA stream (opts.cuda_stream /
+ *     cfg.cuda_stream; NULL = legacy default stream) except dqn_get_params,
+ *     dqn_debug_export and rpl_check, which synchronise that stream.
+ *   - A handle is used by one host thread at a time (external serialisation, S:164,
+ *     S:240).
+ *   - "device pointer" = memory on the handle's device (e.g. a torch CUDA tensor's
+ *     data_ptr()); "host pointer" = ordinary or pinned host memory.
+ *   - Nothing here falls back to the CPU: without a usable sm_100 device every call
+ *     that needs one returns RPL_ECUDA.
+ */
+#ifndef INGPU_REPLAY_H
+#define INGPU_REPLAY_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------------------ */
+enum {
+    RPL_OK = 0,
+    RPL_NOT_READY = 1,   /* replay size < burn_in: nothing done, counters unchanged */
+    RPL_EINVAL = -1,     /* invalid argument / config / dims / batch                        */
+    RPL_ENOMEM = -2,     /* device or pinned allocation failed (message: requested bytes)   */
+    RPL_ECORRUPT = -3,   /* terminal flag not in {0,1}                               */
+    RPL_ENUMERIC = -4,   /* non-finite loss: that step's update was skipped        */
+    RPL_ECUDA = -5,      /* CUDA runtime / launch error                                     */
+    RPL_ENCCL = -6,      /* NCCL unavailable or failed                                      */
+    RPL_ESTATE = -7      /* call not valid in the handle's state                           */
+};
+
+enum { RPL_HOST = 0, RPL_DEVICE = 1 };           /* where replay_add's inputs live        */
+enum { RPL_ONLINE = 0, RPL_TARGET = 1, RPL_GRAD = 2 };  /* which parameter vector          */
+
+typedef struct rpl_replay rpl_replay;   /* opaque */
+typedef struct rpl_dqn rpl_dqn;         /* opaque */
+
+/* ====================================================================================
+ * The replay (P:73 [Methods]: "The Experience Replay API has two methods: adding new
+ * experiences, and randomly sampling from the current experiences.")
+ * ==================================================================================== */
+typedef struct {
+    int32_t device;       /* CUDA device ordinal                                            */
+    void *cuda_stream;    /* cudaStream_t all work is enqueued on (NULL = default stream)   */
+    int64_t burn_in;      /* sampling / training allowed once size >= burn_in (>= 1)  */
+    uint64_t seed;        /* Philox key of the sampler (Q3)                                 */
+    uint32_t rank;        /* learner rank, < 2^24; selects an independent sampler stream    */
+    int64_t max_host_add; /* largest k accepted from host memory per replay_add (pinned
+                             staging size); 0 = 65536                                       */
+} rpl_replay_opts;
+
+/* Create an empty FIFO replay of `capacity` experiences whose states are `state_dim`
+ * fp32 values ("starts empty"; 1,000,000 x (27+27+3)).  Device layout: one
+ * 128-byte-aligned row per slot, [s | s' | a:i32 | r:f32 | terminal:u32 | pad], row
+ * stride round_up(2*state_dim+3, 32) floats (256 B for state_dim = 27).
+ * opts may be NULL (device 0, default stream, burn_in 1, seed 2, rank 0).
+ * Errors: EINVAL (capacity < 1, capacity >= 2^31, state_dim < 1, rank >= 2^24),
+ * ENOMEM, ECUDA.  *out owns the device ring until replay_destroy. */
+int replay_create(int64_t capacity, int32_t state_dim, const rpl_replay_opts *opts,
+                  rpl_replay **out);
+int replay_destroy(rpl_replay *replay);
+
+/* Insert k experiences, oldest evicted first: experience j goes to slot
+ * (cursor + j) mod capacity; afterwards cursor += k (mod capacity), size = min(size+k,
+ * capacity), total += k.  Inputs are SoA: s[k*state_dim], a[k], r[k],
+ * s_next[k*state_dim], done[k] in {0,1}.  mem = RPL_HOST: host pointers, copied into
+ * pinned staging before return (the caller may reuse them at once); one H2D copy of
+ * k*(8*state_dim+9) bytes is counted in replay_state's h2d_bytes -- the only PCIe
+ * traffic of the method.  mem = RPL_DEVICE: device pointers that must stay
+ * valid until the stream reaches the insert.
+ * Errors: EINVAL (k < 0, k > capacity, k > max_host_add for HOST, null pointer with
+ * k > 0), ECORRUPT (HOST done[j] > 1; nothing written).  k = 0 is a no-op.
+ * A device-sourced done[j] > 1 is written as 1 and raises the sticky ECORRUPT flag. */
+int replay_add(rpl_replay *replay, int64_t k, const float *s, const int32_t *a,
+               const float *r, const float *s_next, const uint8_t *done, int mem);
+
+/* Caller-owned DEVICE buffers receiving an unpacked batch ("unpacked into old
+ * state, new state, action, reward and is_terminal Tensors").  Any pointer may be NULL
+ * (that tensor is not written).  s, s_next: [B*state_dim] fp32 row-major; a: [B] i32;
+ * r: [B] fp32; done: [B] u8; idx: [B] i32 sampled slot indices. */
+typedef struct {
+    float *s;
+    float *s_next;
+    int32_t *a;
+    float *r;
+    uint8_t *done;
+    int32_t *idx;
+} rpl_batch;
+
+/* Sample B indices uniformly with replacement from [0, size) (Q1-Q3) and gather
+ * + unpack the rows into *out.  Index i of event E is
+ *   Philox4x32-10(ctr = (i/2, E_lo, E_hi, (1<<24)|rank), key = (seed_lo, seed_hi)),
+ *   u = words (x1:x0) for even i, (x3:x2) for odd i, idx = floor(u * size / 2^64).
+ * Consumes one sampler event (E += 1).  Returns RPL_NOT_READY (nothing done) while
+ * size < burn_in.  Errors: EINVAL (B < 1). */
+int replay_sample(rpl_replay *replay, int32_t batch, const rpl_batch *out);
+
+/* Gather + unpack the rows at the caller's DEVICE indices idx_dev[0..n) (each must be
+ * in [0, size); out-of-range indices are clamped and raise the sticky EINVAL flag).
+ * No sampler event is consumed.  Used for the gather-bandwidth measurement. */
+int replay_gather(rpl_replay *replay, int64_t n, const int32_t *idx_dev, const rpl_batch *out);
+
+/* Host mirror of the ring state; no synchronisation. */
+int replay_size(const rpl_replay *replay, int64_t *size);
+int replay_state(const rpl_replay *replay, int64_t *cursor, int64_t *size, uint64_t *total,
+                 uint64_t *events, uint64_t *h2d_bytes);
+
+/* ====================================================================================
+ * The DQN learner: the whole train step runs on the device with no input
+ * copied from the host.
+ * ==================================================================================== */
+typedef struct {
+    int32_t device;
+    void *cuda_stream;
+    int32_t state_dim;    /* D (27 for Melee)                                          */
+    int32_t n_actions;    /* |A| <= 32 (Q16)                                                 */
+    int32_t dueling;      /* 0: plain MLP head; 1: dueling V/A streams             */
+    int32_t n_hidden;     /* 1..4 shared hidden ReLU layers                                  */
+    int32_t hidden[4];    /* widths (<= 4096)                                                */
+    int32_t stream;       /* dueling: units per stream (512 in the paper)             */
+    int32_t double_dqn;   /* 0: y = r + g(1-d) max_a Q_t(s',a); 1: Double DQN (Q9)    */
+    float gamma;          /* discount in [0, 1]                                              */
+    float lr;             /* SGD step alpha                                           */
+    float huber_kappa;    /* Huber threshold (> 0); +INFINITY gives 1/2 delta^2 = P:90      */
+    int64_t sync_period;  /* target <- online after step t when t % period == 0;
+                             0 = only on sync_target()                                       */
+    int32_t max_batch;    /* largest batch dqn_train_step accepts (sizes the workspaces)    */
+} rpl_dqn_config;
+
+/* Number of fp32 parameters of the blob layout:
+ *   each shared layer l: W_l [N_l x K_l] row-major, then b_l [N_l];
+ *   plain head: W [A x N_last], b [A];
+ *   dueling: W_st [2S x N_last] (rows 0..S-1 V stream, S..2S-1 A stream), b_st [2S],
+ *            W_hd [(1+A) x S] (row 0 V head over V units, rows 1..A A head over A units),
+ *            b_hd [1+A].
+ * 140,297 for the paper's net (27 -> 128 -> 2 x 512 -> 1 + 8). */
+int dqn_param_count(const rpl_dqn_config *cfg, int64_t *n);
+
+/* Create a learner whose online AND target networks start equal to init_params_host
+ * (host blob of dqn_param_count floats).  Errors: EINVAL, ENOMEM, ECUDA. */
+int dqn_create(const rpl_dqn_config *cfg, const float *init_params_host, rpl_dqn **out);
+int dqn_destroy(rpl_dqn *dqn);
+
+/* One train step on `batch` experiences sampled from `replay` (which must live on the
+ * same device and stream):  burn-in gate -> Philox sample (event E of the replay)
+ * -> gather -> Q_online(s), Q_target(s') [, Q_online(s')] -> TD target, Huber loss ->
+ * backward through the online net -> SGD w -= lr * g -> step t += 1 -> target
+ * sync when t % sync_period == 0.  All in one cooperative kernel launch (plus an
+ * NCCL all-reduce and an SGD launch when attached to world > 1).  loss_dev (nullable,
+ * device fp32) receives the batch-mean Huber loss.  Returns RPL_NOT_READY (nothing
+ * enqueued, no counter advanced) while size < burn_in.  Errors: EINVAL (batch < 1 or >
+ * max_batch, dims differ from the replay's, different device), ECUDA. */
+int dqn_train_step(rpl_dqn *dqn, rpl_replay *replay, int32_t batch, float *loss_dev);
+
+/* target <- online (bit copy), enqueued on the stream. */
+int sync_target(rpl_dqn *dqn);
+
+/* Copy a parameter vector (RPL_ONLINE, RPL_TARGET, or RPL_GRAD = the last step's
+ * gradient, all-reduced if attached) to / from host memory (n must equal
+ * dqn_param_count).  get synchronises the stream. */
+int dqn_get_params(rpl_dqn *dqn, int which, float *host_out, int64_t n);
+int dqn_set_params(rpl_dqn *dqn, int which, const float *host_in, int64_t n);
+
+/* Executed train steps t (host mirror). */
+int dqn_step_count(const rpl_dqn *dqn, int64_t *steps);
+
+/* Debug export of the last train step's device intermediates (synchronises).  `what`:
+ *   RPL_DBG_IDX      [B] i32 sampled indices     RPL_DBG_S / RPL_DBG_S_NEXT [B*D] f32
+ *   RPL_DBG_A        [B] i32                     RPL_DBG_R [B] f32   RPL_DBG_DONE [B] u8
+ *   RPL_DBG_Q        [B*A] f32 Q_online(s)       RPL_DBG_QT_NEXT [B*A] f32 Q_target(s')
+ *   RPL_DBG_QO_NEXT  [B*A] f32 Q_online(s') (Double DQN only)
+ *   RPL_DBG_Y        [B] f32 TD targets          RPL_DBG_ASTAR [B] i32 (Double DQN)
+ *   RPL_DBG_H        [B*H] f32 online-net activations on s over the hidden-unit space
+ *                    (shared layers in order, then the stream units [V | A])
+ *   RPL_DBG_LOSS     [1] f32
+ * `bytes` must equal the size of that array for the last step's batch. */
+enum { RPL_DBG_IDX = 0, RPL_DBG_S, RPL_DBG_S_NEXT, RPL_DBG_A, RPL_DBG_R, RPL_DBG_DONE,
+       RPL_DBG_Q, RPL_DBG_QT_NEXT, RPL_DBG_QO_NEXT, RPL_DBG_Y, RPL_DBG_ASTAR, RPL_DBG_H,
+       RPL_DBG_LOSS };
+int dqn_debug_export(rpl_dqn *dqn, int what, void *host_out, int64_t bytes);
+
+/* ====================================================================================
+ * Data-parallel learners ("the agent's model would have to be synchronized every
+ * train step"): one process per GPU, each with its own replay shard; the gradient is
+ * averaged over ranks with NCCL (ncclAllReduce avg over NVLink/NVSwitch) before SGD.
+ * ==================================================================================== */
+/* Rank 0 creates an NCCL unique id (128 bytes) to broadcast (e.g. torch.distributed). */
+int rpl_nccl_unique_id(void *out128);
+/* Join the communicator; from then on dqn_train_step all-reduces the gradient. */
+int dqn_attach_nccl(rpl_dqn *dqn, int32_t rank, int32_t world, const void *id128);
+
+/* Synchronise the handle's stream and report (then clear) its sticky device error:
+ * RPL_OK, RPL_ECORRUPT, RPL_ENUMERIC or RPL_ECUDA.  handle = rpl_replay* or rpl_dqn*
+ * with kind = 0 (replay) or 1 (dqn). */
+int rpl_check(void *handle, int kind);
+const char *rpl_last_error(void);
+/* Number of kernels this library launched in the calling process (launch accounting). */
+uint64_t rpl_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INGPU_REPLAY_H */

@@ -199,6 +199,14 @@ class Ring:
         return lib().oracle_ring_add(C.byref(self._r), k, _ptr(s), _ptr(a), _ptr(r),
                                      _ptr(s_next), _ptr(done))
 
+    def add_many(self, e: dict, chunk: int = 65536) -> None:
+        n = len(e["a"])
+        chunk = min(chunk, self.capacity)
+        for i in range(0, n, chunk):
+            rc = self.add(**{k: v[i:i + chunk] for k, v in e.items()})
+            if rc != OK:
+                raise ValueError(f"oracle_ring_add rc={rc}")
+
     def gather(self, idx):
         idx = _c(idx, np.int32)
         B, D = idx.shape[0], self.state_dim

@@ -1,0 +1,1174 @@
+// dqn.cu -- the fused, device-resident DQN / Double-DQN train step (one cooperative launch).
+//
+// Paper: P:79-84 [Integration]: once the replay is on the GPU "all logic for a single train
+// step can be moved to the GPU" with "no inputs copied from the CPU"; P:88-94 [Deep Q-Network
+// Model]: dueling DQN (shared 128, V/A streams of 512, Q = V + A - mean A), target fixing,
+// the update rule w <- w + alpha (r + gamma max Q(s',a') - Q(s,a)) grad Q(s,a).
+//
+// B200 design: one persistent cooperative kernel, one CTA of 256
+// threads per SM, phases separated by a grid barrier:
+//   F0    Philox sample + gather ring rows + layer 0 of every needed forward (online(s),
+//         target(s'), [online(s')]) -- 32x64 FP32 register-tiled SIMT GEMM tiles
+//   F1.. remaining trunk layers (dueling: the 128 -> [V 512 | A 512] stream layer)
+//   Head  one warp per sample: V/A heads, dueling combine, max / argmax (warp shuffles), TD
+//         target, Huber, dQ, dueling backward, dZ of the last trunk layer
+//   Bl    backward of trunk layer l: dW_l (contraction over the batch, + bias row sums) and
+//         split-K partials of dH_{l-1}; head-weight gradients in the last layer's phase
+//   SGD   deterministic reduction of gradient partials, non-finite guard, w -= lr g,
+//         target sync on sync steps
+// All reductions run in a fixed order, so a step is bit-reproducible.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+#include "philox.cuh"
+
+namespace rpl {
+
+constexpr int NT = 256;   // threads per CTA
+constexpr int BM = 32;    // tile rows
+constexpr int BN = 64;    // tile cols
+constexpr int BK = 32;    // contraction chunk
+constexpr int MAXL = 5;   // trunk layers (4 shared + dueling stream layer)
+constexpr int MAXA = 32;  // actions (one warp)
+constexpr int MAXJ = MAXA + 1;
+
+struct TrainArgs {
+    // replay
+    const float *ring;
+    int rs, D;
+    int64_t size;
+    uint64_t seed, event;
+    uint32_t rank;
+    // network layout
+    int A, dueling, T, J, S, NH, nets, ddqn;
+    int N[MAXL], K[MAXL];
+    int64_t woff[MAXL], boff[MAXL], hw_off, hb_off, P;
+    // batch
+    int B;
+    float gamma, lr, kappa;
+    int kappa_inf;
+    // parameters
+    float *online, *target;
+    // workspaces
+    float *Xs, *Xs2, *r;
+    int32_t *a, *idx;
+    uint8_t *done;
+    float *H[MAXL];        // [nets][B][N_l]
+    float *dZlast;         // [B][NH]
+    float *dO;             // [B][J]
+    float *PdH[MAXL];      // layer l >= 1: [nsplit_n[l]][B][K_l]
+    int nsplit_n[MAXL];
+    float *gpart;          // [nsplit_b][P] (== grad when nsplit_b == 1)
+    int nsplit_b, bsplit;
+    float *grad;           // [P + 1] (grad[P] = batch-mean loss)
+    float *loss_part;      // [B]
+    float *Qs, *Qt2, *Qo2, *y;
+    int32_t *astar;
+    float *loss_out;
+    int apply_update, do_sync;
+    unsigned *bar;         // [0] arrivals, [1] generation
+    uint32_t *err;
+};
+
+struct __align__(16) TileSmem {
+    float As[BK][BM + 4];
+    float Bs[BK][BN + 4];
+    int idx[BM];
+    float red[NT / 32];
+    float head[NT / 32][MAXJ + 3];
+};
+
+// ------------------------------------------------------------------------------------------
+// grid barrier (all CTAs co-resident: cooperative launch)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned *bar)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned gen = ld_acquire(bar + 1);
+        __threadfence();
+        const unsigned arrived = atomicAdd(bar, 1u);
+        if (arrived == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (ld_acquire(bar + 1) == gen) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------------------------------
+// 32x64 register-tiled FP32 GEMM tile: C[m][n] = sum_{kk in [kb,ke)} A(m,kk) * B(n,kk).
+// Operand loaders return 0 outside their bounds.  Each thread owns a 2x4 block of C.
+// The next chunk is fetched into registers while the current one is multiplied.
+// If want_rowsum, rs(m, sum_kk A(m,kk)) is also produced (bias gradients).
+// ------------------------------------------------------------------------------------------
+template <class LA, class LB, class EPI, class RSUM>
+__device__ __forceinline__ void gemm_tile(const LA &la, const LB &lb, int m0, int n0, int kb,
+                                          int ke, const EPI &epi, bool want_rowsum,
+                                          const RSUM &rs, TileSmem &sm)
+{
+    const int tid = threadIdx.x, tn = tid & 15, tm = tid >> 4;
+    float acc[2][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    float rsum0 = 0.0f, rsum1 = 0.0f;
+    constexpr int NA = BM * BK / NT, NB = BN * BK / NT;
+    float ra[NA], rb[NB];
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+            const int e = i * NT + tid;
+            const int r = LA::kKContig ? e / BK : e % BM;
+            const int kk = LA::kKContig ? e % BK : e / BM;
+            ra[i] = la(m0 + r, k0 + kk);
+        }
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const int e = i * NT + tid;
+            const int r = LB::kKContig ? e / BK : e % BN;
+            const int kk = LB::kKContig ? e % BK : e / BN;
+            rb[i] = lb(n0 + r, k0 + kk);
+        }
+    };
+    auto stash = [&]() {
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+            const int e = i * NT + tid;
+            const int r = LA::kKContig ? e / BK : e % BM;
+            const int kk = LA::kKContig ? e % BK : e / BM;
+            sm.As[kk][r] = ra[i];
+        }
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const int e = i * NT + tid;
+            const int r = LB::kKContig ? e / BK : e % BN;
+            const int kk = LB::kKContig ? e % BK : e / BN;
+            sm.Bs[kk][r] = rb[i];
+        }
+    };
+    const int nchunks = (ke - kb + BK - 1) / BK;
+    if (nchunks > 0) {
+        fetch(kb);
+        stash();
+        __syncthreads();
+        for (int c = 0; c < nchunks; ++c) {
+            if (c + 1 < nchunks) fetch(kb + (c + 1) * BK);
+#pragma unroll 8
+            for (int k = 0; k < BK; ++k) {
+                const float2 av = *reinterpret_cast<const float2 *>(&sm.As[k][2 * tm]);
+                const float4 bv = *reinterpret_cast<const float4 *>(&sm.Bs[k][4 * tn]);
+                acc[0][0] = fmaf(av.x, bv.x, acc[0][0]);
+                acc[0][1] = fmaf(av.x, bv.y, acc[0][1]);
+                acc[0][2] = fmaf(av.x, bv.z, acc[0][2]);
+                acc[0][3] = fmaf(av.x, bv.w, acc[0][3]);
+                acc[1][0] = fmaf(av.y, bv.x, acc[1][0]);
+                acc[1][1] = fmaf(av.y, bv.y, acc[1][1]);
+                acc[1][2] = fmaf(av.y, bv.z, acc[1][2]);
+                acc[1][3] = fmaf(av.y, bv.w, acc[1][3]);
+            }
+            if (want_rowsum && tn == 0) {
+                for (int k = 0; k < BK; ++k) {
+                    rsum0 += sm.As[k][2 * tm];
+                    rsum1 += sm.As[k][2 * tm + 1];
+                }
+            }
+            __syncthreads();
+            if (c + 1 < nchunks) {
+                stash();
+                __syncthreads();
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) epi(m0 + 2 * tm + i, n0 + 4 * tn + j, acc[i][j]);
+    if (want_rowsum && tn == 0) {
+        rs(m0 + 2 * tm, rsum0);
+        rs(m0 + 2 * tm + 1, rsum1);
+    }
+}
+
+// ---- operand loaders --------------------------------------------------------------------
+// row-major [rows x ld] matrix, element (r, kk) = p[r*ld + kk], valid for r < R, kk < KE
+struct LdKMajor {
+    static constexpr bool kKContig = true;
+    const float *p;
+    int ld, R, KE;
+    __device__ float operator()(int r, int kk) const
+    {
+        return (r < R && kk < KE) ? __ldcg(p + (int64_t)r * ld + kk) : 0.0f;
+    }
+};
+// element (r, kk) = p[kk*ld + r] (contiguous along r), valid for r < R, kk in [KB, KE)
+struct LdRMajor {
+    static constexpr bool kKContig = false;
+    const float *p;
+    int ld, R, KB, KE;
+    __device__ float operator()(int r, int kk) const
+    {
+        return (r < R && kk >= KB && kk < KE) ? __ldcg(p + (int64_t)kk * ld + r) : 0.0f;
+    }
+};
+// gathered replay rows: element (m, k) = ring[idx[m - m0] * rs + col0 + k]
+struct LdRing {
+    static constexpr bool kKContig = true;
+    const float *ring;
+    const int *idx_s;
+    int m0, rs, col0, R, KE;
+    __device__ float operator()(int m, int k) const
+    {
+        return (m < R && k < KE) ? __ldg(ring + (int64_t)idx_s[m - m0] * rs + col0 + k) : 0.0f;
+    }
+};
+
+// dZ_l[b][n] of the online net: materialised for the last trunk layer, otherwise the
+// deterministic sum of the split-K partials of dH_l times the ReLU mask of layer l
+__device__ __forceinline__ float dz_val(const TrainArgs &p, int l, int b, int n)
+{
+    const int N = p.N[l];
+    if (l == p.T - 1) return __ldcg(p.dZlast + (int64_t)b * N + n);
+    const float *q = p.PdH[l + 1] + (int64_t)b * N + n;
+    const int64_t stride = (int64_t)p.B * N;
+    float s = 0.0f;
+    for (int i = 0; i < p.nsplit_n[l + 1]; ++i) s += __ldcg(q + i * stride);
+    const float h = __ldcg(p.H[l] + (int64_t)b * N + n);
+    return h > 0.0f ? s : 0.0f;
+}
+// (m = unit n, kk = sample b), contiguous along n (for dW)
+struct LdDzT {
+    static constexpr bool kKContig = false;
+    const TrainArgs *p;
+    int l, N, KB, KE;
+    __device__ float operator()(int n, int b) const
+    {
+        return (n < N && b >= KB && b < KE) ? dz_val(*p, l, b, n) : 0.0f;
+    }
+};
+// (m = sample b, kk = unit n), contiguous along n (for dH)
+struct LdDz {
+    static constexpr bool kKContig = true;
+    const TrainArgs *p;
+    int l, B, KB, KE;
+    __device__ float operator()(int b, int n) const
+    {
+        return (b < B && n >= KB && n < KE) ? dz_val(*p, l, b, n) : 0.0f;
+    }
+};
+
+struct NoRowsum {
+    __device__ void operator()(int, float) const {}
+};
+
+__device__ __forceinline__ float warp_sum(float v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ------------------------------------------------------------------------------------------
+// phases
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ const float *net_params(const TrainArgs &p, int net)
+{
+    return net == 1 ? p.target : p.online;
+}
+
+// F0 / Fl: forward of trunk layer l for every needed net
+__device__ void phase_forward(const TrainArgs &p, int l, TileSmem &sm)
+{
+    const int N = p.N[l], K = p.K[l], B = p.B;
+    const int mt = (B + BM - 1) / BM, nt = (N + BN - 1) / BN;
+    const int ntasks = p.nets * mt * nt;
+    for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+        const int net = t / (mt * nt), rem = t % (mt * nt);
+        const int m0 = (rem / nt) * BM, n0 = (rem % nt) * BN;
+        const float *theta = net_params(p, net);
+        const float *W = theta + p.woff[l];
+        const float *bias = theta + p.boff[l];
+        float *Hout = p.H[l] + (int64_t)net * B * N;
+        auto epi = [&](int m, int n, float v) {
+            if (m < B && n < N) {
+                v += __ldg(bias + n);
+                Hout[(int64_t)m * N + n] = v > 0.0f ? v : 0.0f;
+            }
+        };
+        LdKMajor lw{W, K, N, K};
+        if (l == 0) {
+            // sample (Philox, event E) + gather: the batch rows m0..m0+BM
+            __syncthreads();
+            if (threadIdx.x < BM / 2) {
+                const int pair = (m0 >> 1) + threadIdx.x;
+                int32_t i0, i1;
+                sample_pair(p.seed, p.rank, p.event, (uint32_t)pair, (uint64_t)p.size, i0, i1);
+                sm.idx[2 * threadIdx.x] = i0;
+                sm.idx[2 * threadIdx.x + 1] = i1;
+            }
+            __syncthreads();
+            const int col0 = (net == 0) ? 0 : p.D;   // s for online(s), s' for the others
+            LdRing lx{p.ring, sm.idx, m0, p.rs, col0, B, p.D};
+            // unpack the batch once (online(s) / target(s') tasks of the first column tile)
+            if (n0 == 0 && net <= 1) {
+                const int D = p.D;
+                for (int e = threadIdx.x; e < BM * D; e += NT) {
+                    const int r = e / D, c = e % D;
+                    if (m0 + r < B)
+                        (net == 0 ? p.Xs : p.Xs2)[(int64_t)(m0 + r) * D + c] =
+                            __ldg(p.ring + (int64_t)sm.idx[r] * p.rs + col0 + c);
+                }
+                if (net == 0 && threadIdx.x < BM && m0 + threadIdx.x < B) {
+                    const int r = threadIdx.x, b = m0 + r;
+                    const float *row = p.ring + (int64_t)sm.idx[r] * p.rs + 2 * D;
+                    p.idx[b] = sm.idx[r];
+                    p.a[b] = __float_as_int(__ldg(row));
+                    p.r[b] = __ldg(row + 1);
+                    p.done[b] = (uint8_t)(__float_as_uint(__ldg(row + 2)) != 0u);
+                }
+            }
+            gemm_tile(lx, lw, m0, n0, 0, K, epi, false, NoRowsum{}, sm);
+        } else {
+            LdKMajor lh{p.H[l - 1] + (int64_t)net * B * K, K, B, K};
+            gemm_tile(lh, lw, m0, n0, 0, K, epi, false, NoRowsum{}, sm);
+        }
+    }
+}
+
+__device__ __forceinline__ float huber(float d, float kappa, int kinf)
+{
+    const float ad = fabsf(d);
+    if (kinf || ad <= kappa) return 0.5f * d * d;
+    return kappa * (ad - 0.5f * kappa);
+}
+
+// Head: one warp per sample
+__device__ void phase_head(const TrainArgs &p, TileSmem &sm)
+{
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int nw = NT / 32;
+    const int A = p.A, J = p.J, S = p.S, NH = p.NH, B = p.B;
+    const int L = p.T - 1;
+    float *hs = sm.head[wib];
+    for (int b = blockIdx.x + gridDim.x * wib; b < B; b += gridDim.x * nw) {
+        float q0 = 0.0f, q1 = 0.0f, q2 = 0.0f;   // lane a < A holds Q_net(., a)
+        for (int net = 0; net < p.nets; ++net) {
+            const float *theta = net_params(p, net);
+            const float *Wh = theta + p.hw_off;
+            const float *bh = theta + p.hb_off;
+            const float *h = p.H[L] + ((int64_t)net * B + b) * NH;
+            for (int j = 0; j < J; ++j) {
+                float acc = 0.0f;
+                if (p.dueling) {
+                    const float *hh = h + (j == 0 ? 0 : S);
+                    for (int u = lane; u < S; u += 32) acc = fmaf(__ldg(Wh + (int64_t)j * S + u), __ldcg(hh + u), acc);
+                } else {
+                    for (int u = lane; u < NH; u += 32) acc = fmaf(__ldg(Wh + (int64_t)j * NH + u), __ldcg(h + u), acc);
+                }
+                acc = warp_sum(acc);
+                if (lane == 0) hs[j] = acc + __ldg(bh + j);
+            }
+            __syncwarp();
+            float qa = 0.0f;
+            if (p.dueling) {
+                // Q(s,a) = V(s) + A(s,a) - (1/|A|) sum_a' A(s,a')
+                float mean = 0.0f;
+                for (int a = 0; a < A; ++a) mean += hs[1 + a];
+                mean /= (float)A;
+                if (lane < A) qa = hs[0] + hs[1 + lane] - mean;
+            } else if (lane < A) {
+                qa = hs[lane];
+            }
+            if (net == 0) q0 = qa; else if (net == 1) q1 = qa; else q2 = qa;
+            __syncwarp();
+        }
+        // TD target (Q9): DQN max_a Q_t(s',a); DDQN Q_t(s', argmax_a Q_o(s',a))
+        float boot;
+        int astar = -1;
+        if (!p.ddqn) {
+            float m = lane < A ? q1 : -INFINITY;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            boot = m;
+        } else {
+            float v = lane < A ? q2 : -INFINITY;
+            int ix = lane;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, ix, o);
+                if (ov > v || (ov == v && oi < ix)) { v = ov; ix = oi; }   // ties: lowest index
+            }
+            astar = ix;
+            boot = __shfl_sync(0xffffffffu, q1, astar);
+        }
+        const int ab = p.a[b];
+        const float rb = p.r[b];
+        const float notdone = p.done[b] ? 0.0f : 1.0f;
+        const float yb = rb + p.gamma * notdone * boot;
+        // the enumerate-mask gather Q[i*A + a_i] is a register select here
+        const float qsel = __shfl_sync(0xffffffffu, q0, ab);
+        const float delta = qsel - yb;
+        const float g = (p.kappa_inf ? delta : fminf(fmaxf(delta, -p.kappa), p.kappa)) / (float)B;
+        // dL/dhead: plain dO_j = [j==a]g ; dueling dV = g, dA_j = [j==a]g - g/|A|
+        if (p.dueling) {
+            if (lane == 0) hs[0] = g;
+            if (lane < A) hs[1 + lane] = (lane == ab ? g : 0.0f) - g / (float)A;
+        } else if (lane < A) {
+            hs[lane] = lane == ab ? g : 0.0f;
+        }
+        __syncwarp();
+        for (int j = lane; j < J; j += 32) p.dO[(int64_t)b * J + j] = hs[j];
+        if (lane < A) {
+            p.Qs[(int64_t)b * A + lane] = q0;
+            p.Qt2[(int64_t)b * A + lane] = q1;
+            if (p.ddqn) p.Qo2[(int64_t)b * A + lane] = q2;
+        }
+        if (lane == 0) {
+            p.y[b] = yb;
+            p.loss_part[b] = huber(delta, p.kappa, p.kappa_inf);
+            if (p.ddqn) p.astar[b] = astar;
+        }
+        // dZ of the last trunk layer: (dO . W_head) * ReLU'(z)
+        const float *Wh = p.online + p.hw_off;
+        const float *h0 = p.H[L] + (int64_t)b * NH;
+        for (int u = lane; u < NH; u += 32) {
+            float dh = 0.0f;
+            if (p.dueling) {
+                if (u < S) {
+                    dh = hs[0] * __ldg(Wh + u);
+                } else {
+                    for (int a = 0; a < A; ++a) dh = fmaf(hs[1 + a], __ldg(Wh + (int64_t)(1 + a) * S + (u - S)), dh);
+                }
+            } else {
+                for (int a = 0; a < A; ++a) dh = fmaf(hs[a], __ldg(Wh + (int64_t)a * NH + u), dh);
+            }
+            p.dZlast[(int64_t)b * NH + u] = __ldcg(h0 + u) > 0.0f ? dh : 0.0f;
+        }
+        __syncwarp();
+    }
+}
+
+// backward of trunk layer l (+ the head weights when l == T-1)
+__device__ void phase_backward(const TrainArgs &p, int l, TileSmem &sm)
+{
+    const int N = p.N[l], K = p.K[l], B = p.B;
+    // (i) dW_l tiles: M = N units, N-dim = K inputs, contraction over the b-split
+    const int wmt = (N + BM - 1) / BM, wnt = (K + BN - 1) / BN;
+    const int n_w = wmt * wnt * p.nsplit_b;
+    // (ii) dH_{l-1} split-K partials: M = B, N-dim = K, contraction over units
+    const int hmt = (B + BM - 1) / BM, hnt = (K + BN - 1) / BN;
+    const int n_h = l > 0 ? hmt * hnt * p.nsplit_n[l] : 0;
+    // (iii) head weight gradients (l == T-1): 256 head-input units per task, per b-split
+    const int hu = (p.dueling ? p.S : p.NH);
+    const int n_hd_u = (l == p.T - 1) ? ((p.dueling ? 2 * hu : hu) + NT - 1) / NT : 0;
+    const int n_hd = (l == p.T - 1) ? (n_hd_u + 1) * p.nsplit_b : 0;
+    const float *Hprev = (l == 0) ? p.Xs : p.H[l - 1];
+    const int ntasks = n_w + n_h + n_hd;
+    for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+        if (t < n_w) {
+            const int s = t / (wmt * wnt), rem = t % (wmt * wnt);
+            const int m0 = (rem / wnt) * BM, n0 = (rem % wnt) * BN;
+            const int kb = s * p.bsplit, ke = min(B, kb + p.bsplit);
+            float *gp = p.gpart + (int64_t)s * p.P;
+            LdDzT la{&p, l, N, kb, ke};
+            LdRMajor lb{Hprev, K, K, kb, ke};
+            auto epi = [&](int m, int n, float v) {
+                if (m < N && n < K) gp[p.woff[l] + (int64_t)m * K + n] = v;
+            };
+            auto rs = [&](int m, float v) {
+                if (m < N) gp[p.boff[l] + m] = v;
+            };
+            gemm_tile(la, lb, m0, n0, kb, ke, epi, n0 == 0, rs, sm);
+        } else if (t < n_w + n_h) {
+            const int u = t - n_w;
+            const int s = u / (hmt * hnt), rem = u % (hmt * hnt);
+            const int m0 = (rem / hnt) * BM, n0 = (rem % hnt) * BN;
+            const int chunk = (N + p.nsplit_n[l] - 1) / p.nsplit_n[l];
+            const int kb = s * chunk, ke = min(N, kb + chunk);
+            float *out = p.PdH[l] + (int64_t)s * B * K;
+            LdDz la{&p, l, B, kb, ke};
+            LdRMajor lb{p.online + p.woff[l], K, K, kb, ke};
+            auto epi = [&](int m, int n, float v) {
+                if (m < B && n < K) out[(int64_t)m * K + n] = v;
+            };
+            gemm_tile(la, lb, m0, n0, kb, ke, epi, false, NoRowsum{}, sm);
+        } else {
+            // head gradients: g_Wh[j][u] = sum_b dO[b][j] h[b][u]; g_bh[j] = sum_b dO[b][j]
+            const int u = t - n_w - n_h;
+            const int s = u / (n_hd_u + 1), c = u % (n_hd_u + 1);
+            const int kb = s * p.bsplit, ke = min(B, kb + p.bsplit);
+            float *gp = p.gpart + (int64_t)s * p.P;
+            const int J = p.J, NH = p.NH;
+            const float *h = p.H[p.T - 1];   // online net on s
+            if (c < n_hd_u) {
+                const int unit = c * NT + threadIdx.x;   // index into the head-input units
+                if (unit < NH) {
+                    if (p.dueling) {
+                        const int S = p.S;
+                        if (unit < S) {
+                            float acc = 0.0f;
+                            for (int b = kb; b < ke; ++b) acc = fmaf(__ldcg(p.dO + (int64_t)b * J), __ldcg(h + (int64_t)b * NH + unit), acc);
+                            gp[p.hw_off + unit] = acc;
+                        } else {
+                            float acc[MAXA];
+#pragma unroll
+                            for (int a = 0; a < MAXA; ++a) acc[a] = 0.0f;
+                            for (int b = kb; b < ke; ++b) {
+                                const float hv = __ldcg(h + (int64_t)b * NH + unit);
+#pragma unroll
+                                for (int a = 0; a < MAXA; ++a)
+                                    if (a < p.A) acc[a] = fmaf(__ldcg(p.dO + (int64_t)b * J + 1 + a), hv, acc[a]);
+                            }
+#pragma unroll
+                            for (int a = 0; a < MAXA; ++a)
+                                if (a < p.A) gp[p.hw_off + (int64_t)(1 + a) * S + (unit - S)] = acc[a];
+                        }
+                    } else {
+                        float acc[MAXA];
+#pragma unroll
+                        for (int a = 0; a < MAXA; ++a) acc[a] = 0.0f;
+                        for (int b = kb; b < ke; ++b) {
+                            const float hv = __ldcg(h + (int64_t)b * NH + unit);
+#pragma unroll
+                            for (int a = 0; a < MAXA; ++a)
+                                if (a < p.A) acc[a] = fmaf(__ldcg(p.dO + (int64_t)b * J + a), hv, acc[a]);
+                        }
+#pragma unroll
+                        for (int a = 0; a < MAXA; ++a)
+                            if (a < p.A) gp[p.hw_off + (int64_t)a * NH + unit] = acc[a];
+                    }
+                }
+            } else if (threadIdx.x < J) {
+                float acc = 0.0f;
+                for (int b = kb; b < ke; ++b) acc += __ldcg(p.dO + (int64_t)b * J + threadIdx.x);
+                gp[p.hb_off + threadIdx.x] = acc;
+            }
+        }
+    }
+}
+
+__device__ float block_sum_fixed(float v, TileSmem &sm)
+{
+    v = warp_sum(v);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sm.red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    float s = 0.0f;
+    for (int w = 0; w < NT / 32; ++w) s += sm.red[w];   // same order in every thread/CTA
+    return s;
+}
+
+// SGD: deterministic reduction of the b-split partials, non-finite guard,
+// w -= lr g, target sync on sync steps
+__device__ void phase_sgd(const TrainArgs &p, TileSmem &sm)
+{
+    float ls = 0.0f;
+    for (int b = threadIdx.x; b < p.B; b += NT) ls += __ldcg(p.loss_part + b);
+    const float loss = block_sum_fixed(ls, sm) / (float)p.B;
+    const bool ok = isfinite(loss);
+    const int64_t stride = (int64_t)gridDim.x * NT;
+    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < p.P; i += stride) {
+        float g;
+        if (p.nsplit_b == 1) {
+            g = __ldcg(p.grad + i);
+        } else {
+            g = 0.0f;
+            for (int s = 0; s < p.nsplit_b; ++s) g += __ldcg(p.gpart + (int64_t)s * p.P + i);
+            p.grad[i] = g;
+        }
+        if (p.apply_update && ok) {
+            const float w = p.online[i] - p.lr * g;
+            p.online[i] = w;
+            if (p.do_sync) p.target[i] = w;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        p.grad[p.P] = loss;
+        if (p.loss_out) *p.loss_out = loss;
+        if (!ok) atomicOr(p.err, ERRBIT_NUMERIC);
+    }
+}
+
+__global__ void __launch_bounds__(NT, 1) train_step_kernel(const __grid_constant__ TrainArgs p)
+{
+    __shared__ TileSmem sm;
+    for (int l = 0; l < p.T; ++l) {
+        phase_forward(p, l, sm);
+        grid_barrier(p.bar);
+    }
+    phase_head(p, sm);
+    grid_barrier(p.bar);
+    for (int l = p.T - 1; l >= 0; --l) {
+        phase_backward(p, l, sm);
+        grid_barrier(p.bar);
+    }
+    phase_sgd(p, sm);
+}
+
+// SGD after an NCCL all-reduce (world > 1): grad[P] holds the rank-averaged loss
+__global__ void __launch_bounds__(256) sgd_kernel(float *online, float *target, const float *grad,
+                                                  int64_t P, float lr, int do_sync, uint32_t *err)
+{
+    const float loss = grad[P];
+    const bool ok = isfinite(loss);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (ok) {
+            const float w = online[i] - lr * grad[i];
+            online[i] = w;
+            if (do_sync) target[i] = w;
+        }
+    }
+    if (!ok && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(err, ERRBIT_NUMERIC);
+}
+
+// ------------------------------------------------------------------------------------------
+// NCCL (dlopen of the process's libnccl.so.2 -- the one torch loaded)
+// ------------------------------------------------------------------------------------------
+typedef struct { char internal[128]; } nccl_uid;
+typedef int (*fn_get_uid)(nccl_uid *);
+typedef int (*fn_init_rank)(void **, int, nccl_uid, int);
+typedef int (*fn_allreduce)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+typedef int (*fn_destroy)(void *);
+typedef const char *(*fn_errstr)(int);
+struct NcclApi {
+    bool loaded = false;
+    fn_get_uid get_uid = nullptr;
+    fn_init_rank init_rank = nullptr;
+    fn_allreduce allreduce = nullptr;
+    fn_destroy destroy = nullptr;
+    fn_errstr errstr = nullptr;
+};
+static NcclApi g_nccl;
+static int nccl_load()
+{
+    if (g_nccl.loaded) return RPL_OK;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        set_error("NCCL: dlopen(libnccl.so.2) failed: %s", dlerror());
+        return RPL_ENCCL;
+    }
+    g_nccl.get_uid = (fn_get_uid)dlsym(h, "ncclGetUniqueId");
+    g_nccl.init_rank = (fn_init_rank)dlsym(h, "ncclCommInitRank");
+    g_nccl.allreduce = (fn_allreduce)dlsym(h, "ncclAllReduce");
+    g_nccl.destroy = (fn_destroy)dlsym(h, "ncclCommDestroy");
+    g_nccl.errstr = (fn_errstr)dlsym(h, "ncclGetErrorString");
+    if (!g_nccl.get_uid || !g_nccl.init_rank || !g_nccl.allreduce || !g_nccl.destroy) {
+        set_error("NCCL: missing symbols in libnccl.so.2");
+        return RPL_ENCCL;
+    }
+    g_nccl.loaded = true;
+    return RPL_OK;
+}
+constexpr int kNcclFloat = 7;   // ncclFloat32
+constexpr int kNcclAvg = 4;     // ncclAvg
+
+}  // namespace rpl
+
+using namespace rpl;
+
+// ==========================================================================================
+// learner handle + C-ABI
+// ==========================================================================================
+struct rpl_dqn {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    rpl_dqn_config cfg{};
+    // layout
+    int T = 0, J = 0, NH = 0;
+    int N[MAXL] = {}, K[MAXL] = {};
+    int64_t woff[MAXL] = {}, boff[MAXL] = {}, hw_off = 0, hb_off = 0, P = 0, Htot = 0;
+    int sms = 148;
+    // device memory
+    float *online = nullptr, *target = nullptr, *grad = nullptr, *gpart = nullptr;
+    float *Xs = nullptr, *Xs2 = nullptr, *r = nullptr;
+    int32_t *a = nullptr, *idx = nullptr, *astar = nullptr;
+    uint8_t *done = nullptr;
+    float *H[MAXL] = {}, *dZlast = nullptr, *dO = nullptr, *PdH[MAXL] = {};
+    float *loss_part = nullptr, *Qs = nullptr, *Qt2 = nullptr, *Qo2 = nullptr, *y = nullptr;
+    float *loss_dev = nullptr;
+    unsigned *bar = nullptr;
+    uint32_t *err = nullptr;
+    int64_t gpart_elems = 0, pdh_elems[MAXL] = {};
+    int64_t steps = 0;
+    int last_B = 0;
+    // data parallel
+    void *comm = nullptr;
+    int rank = 0, world = 1;
+    std::vector<void *> allocs;
+};
+
+static int config_layout(const rpl_dqn_config *c, rpl_dqn *d)
+{
+    if (!c || c->state_dim < 1 || c->n_actions < 1 || c->n_actions > MAXA || c->n_hidden < 1 ||
+        c->n_hidden > 4 || !(c->gamma >= 0.0f && c->gamma <= 1.0f) || !(c->lr >= 0.0f) ||
+        !(c->huber_kappa > 0.0f) || c->sync_period < 0 || c->max_batch < 1 ||
+        c->max_batch > (1 << 20) || (c->dueling && (c->stream < 1 || c->stream > 4096)))
+        return RPL_EINVAL;
+    for (int l = 0; l < c->n_hidden; ++l)
+        if (c->hidden[l] < 1 || c->hidden[l] > 4096) return RPL_EINVAL;
+    int64_t P = 0;
+    int K = c->state_dim, T = 0;
+    for (int l = 0; l < c->n_hidden; ++l, ++T) {
+        d->N[T] = c->hidden[l];
+        d->K[T] = K;
+        d->woff[T] = P;
+        d->boff[T] = P + (int64_t)d->N[T] * K;
+        P += (int64_t)d->N[T] * K + d->N[T];
+        K = d->N[T];
+    }
+    if (c->dueling) {
+        d->N[T] = 2 * c->stream;
+        d->K[T] = K;
+        d->woff[T] = P;
+        d->boff[T] = P + (int64_t)d->N[T] * K;
+        P += (int64_t)d->N[T] * K + d->N[T];
+        ++T;
+        d->J = 1 + c->n_actions;
+        d->NH = 2 * c->stream;
+        d->hw_off = P;
+        d->hb_off = P + (int64_t)d->J * c->stream;
+        P += (int64_t)d->J * c->stream + d->J;
+    } else {
+        d->J = c->n_actions;
+        d->NH = K;
+        d->hw_off = P;
+        d->hb_off = P + (int64_t)d->J * K;
+        P += (int64_t)d->J * K + d->J;
+    }
+    d->T = T;
+    d->P = P;
+    d->Htot = 0;
+    for (int l = 0; l < T; ++l) d->Htot += d->N[l];
+    return RPL_OK;
+}
+
+extern "C" int dqn_param_count(const rpl_dqn_config *cfg, int64_t *n)
+{
+    rpl_dqn tmp;
+    if (!n || config_layout(cfg, &tmp) != RPL_OK) {
+        set_error("dqn_param_count: invalid config");
+        return RPL_EINVAL;
+    }
+    *n = tmp.P;
+    return RPL_OK;
+}
+
+// split choices (host): b-split of 256 samples for weight gradients; split-K of dH so a
+// phase has about one task per SM
+static int nsplit_b_for(int B) { return (B + 255) / 256; }
+static int nsplit_n_for(const rpl_dqn *d, int l, int B)
+{
+    const int tiles = ((B + BM - 1) / BM) * ((d->K[l] + BN - 1) / BN);
+    int ns = (d->sms + tiles - 1) / tiles;
+    const int maxs = (d->N[l] + BK - 1) / BK;
+    if (ns > maxs) ns = maxs;
+    if (ns < 1) ns = 1;
+    return ns;
+}
+
+template <class T>
+static bool dalloc(rpl_dqn *d, T **p, size_t n)
+{
+    void *q = nullptr;
+    if (cudaMalloc(&q, n * sizeof(T) + 16) != cudaSuccess) return false;
+    d->allocs.push_back(q);
+    *p = (T *)q;
+    return true;
+}
+
+extern "C" int dqn_destroy(rpl_dqn *d)
+{
+    if (!d) return RPL_OK;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(d->device);
+    cudaStreamSynchronize(d->stream);
+    if (d->comm && g_nccl.destroy) g_nccl.destroy(d->comm);
+    for (void *p : d->allocs) cudaFree(p);
+    delete d;
+    if (prev >= 0) cudaSetDevice(prev);
+    return RPL_OK;
+}
+
+extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn **out)
+{
+    if (!out || !init) {
+        set_error("dqn_create: null argument");
+        return RPL_EINVAL;
+    }
+    *out = nullptr;
+    rpl_dqn *d = new rpl_dqn();
+    if (config_layout(cfg, d) != RPL_OK) {
+        delete d;
+        set_error("dqn_create: invalid config");
+        return RPL_EINVAL;
+    }
+    d->cfg = *cfg;
+    d->device = cfg->device;
+    d->stream = (cudaStream_t)cfg->cuda_stream;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || d->device < 0 || d->device >= ndev) {
+        delete d;
+        set_error("dqn_create: no CUDA device %d", cfg->device);
+        return RPL_ECUDA;
+    }
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(d->device);
+    cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, d->device);
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, d->device);
+    const int Bm = cfg->max_batch, D = cfg->state_dim, A = cfg->n_actions;
+    const int nets = cfg->double_dqn ? 3 : 2;
+    bool ok = coop != 0;
+    ok = ok && dalloc(d, &d->online, d->P) && dalloc(d, &d->target, d->P) &&
+         dalloc(d, &d->grad, d->P + 1);
+    d->gpart_elems = (int64_t)nsplit_b_for(Bm) * d->P;
+    ok = ok && (nsplit_b_for(Bm) == 1 || dalloc(d, &d->gpart, d->gpart_elems));
+    ok = ok && dalloc(d, &d->Xs, (size_t)Bm * D) && dalloc(d, &d->Xs2, (size_t)Bm * D) &&
+         dalloc(d, &d->r, Bm) && dalloc(d, &d->a, Bm) && dalloc(d, &d->idx, Bm) &&
+         dalloc(d, &d->astar, Bm) && dalloc(d, &d->done, Bm) && dalloc(d, &d->dZlast, (size_t)Bm * d->NH) &&
+         dalloc(d, &d->dO, (size_t)Bm * d->J) && dalloc(d, &d->loss_part, Bm) &&
+         dalloc(d, &d->Qs, (size_t)Bm * A) && dalloc(d, &d->Qt2, (size_t)Bm * A) &&
+         dalloc(d, &d->Qo2, (size_t)Bm * A) && dalloc(d, &d->y, Bm) && dalloc(d, &d->loss_dev, 1) &&
+         dalloc(d, &d->bar, 2) && dalloc(d, &d->err, 1);
+    for (int l = 0; l < d->T && ok; ++l) {
+        ok = dalloc(d, &d->H[l], (size_t)nets * Bm * d->N[l]);
+        if (ok && l > 0) {
+            // nsplit_n * B <= (sms / tiles + 1) * B with tiles >= B / BM, so
+            // nsplit_n * B <= sms * BM + B for every batch size B <= max_batch
+            d->pdh_elems[l] = ((int64_t)d->sms * BM + Bm) * d->K[l];
+            ok = dalloc(d, &d->PdH[l], d->pdh_elems[l]);
+        }
+    }
+    if (!ok) {
+        if (!coop) set_error("dqn_create: device %d lacks cooperative launch", d->device);
+        else set_error("dqn_create: device allocation failed");
+        dqn_destroy(d);
+        if (prev >= 0) cudaSetDevice(prev);
+        return coop ? RPL_ENOMEM : RPL_ECUDA;
+    }
+    const size_t pb = (size_t)d->P * sizeof(float);
+    cudaError_t e = cudaMemcpyAsync(d->online, init, pb, cudaMemcpyHostToDevice, d->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d->target, init, pb, cudaMemcpyHostToDevice, d->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d->bar, 0, 2 * sizeof(unsigned) + 16, d->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d->err, 0, sizeof(uint32_t), d->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d->grad, 0, (d->P + 1) * sizeof(float), d->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(d->stream);
+    if (prev >= 0) cudaSetDevice(prev);
+    if (e != cudaSuccess) {
+        int rc = cuda_fail(e, "dqn_create init copies");
+        dqn_destroy(d);
+        return rc;
+    }
+    *out = d;
+    return RPL_OK;
+}
+
+static void fill_args(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int apply, int do_sync,
+                      TrainArgs &p)
+{
+    memset(&p, 0, sizeof p);
+    p.ring = rp->ring.rows;
+    p.rs = rp->ring.rs;
+    p.D = rp->ring.D;
+    p.size = rp->size;
+    p.seed = rp->seed;
+    p.event = rp->events;
+    p.rank = rp->rank;
+    const rpl_dqn_config &c = d->cfg;
+    p.A = c.n_actions;
+    p.dueling = c.dueling;
+    p.T = d->T;
+    p.J = d->J;
+    p.S = c.dueling ? c.stream : 0;
+    p.NH = d->NH;
+    p.nets = c.double_dqn ? 3 : 2;
+    p.ddqn = c.double_dqn;
+    for (int l = 0; l < d->T; ++l) {
+        p.N[l] = d->N[l];
+        p.K[l] = d->K[l];
+        p.woff[l] = d->woff[l];
+        p.boff[l] = d->boff[l];
+        p.H[l] = d->H[l];
+        p.PdH[l] = d->PdH[l];
+        p.nsplit_n[l] = l > 0 ? nsplit_n_for(d, l, B) : 1;
+    }
+    p.hw_off = d->hw_off;
+    p.hb_off = d->hb_off;
+    p.P = d->P;
+    p.B = B;
+    p.gamma = c.gamma;
+    p.lr = c.lr;
+    p.kappa_inf = std::isinf(c.huber_kappa) ? 1 : 0;
+    p.kappa = p.kappa_inf ? 0.0f : c.huber_kappa;
+    p.online = d->online;
+    p.target = d->target;
+    p.Xs = d->Xs;
+    p.Xs2 = d->Xs2;
+    p.r = d->r;
+    p.a = d->a;
+    p.idx = d->idx;
+    p.done = d->done;
+    p.dZlast = d->dZlast;
+    p.dO = d->dO;
+    p.nsplit_b = nsplit_b_for(B);
+    p.bsplit = 256;
+    p.gpart = p.nsplit_b == 1 ? d->grad : d->gpart;
+    p.grad = d->grad;
+    p.loss_part = d->loss_part;
+    p.Qs = d->Qs;
+    p.Qt2 = d->Qt2;
+    p.Qo2 = d->Qo2;
+    p.y = d->y;
+    p.astar = d->astar;
+    p.loss_out = loss_dev ? loss_dev : d->loss_dev;
+    p.apply_update = apply;
+    p.do_sync = do_sync;
+    p.bar = d->bar;
+    p.err = d->err;
+}
+
+static int grid_for(const rpl_dqn *d, const TrainArgs &p)
+{
+    // the largest phase task count, capped at one CTA per SM
+    int64_t mx = 1;
+    for (int l = 0; l < p.T; ++l) {
+        const int64_t f = (int64_t)p.nets * ((p.B + BM - 1) / BM) * ((p.N[l] + BN - 1) / BN);
+        const int64_t w = (int64_t)((p.N[l] + BM - 1) / BM) * ((p.K[l] + BN - 1) / BN) * p.nsplit_b;
+        const int64_t h = l > 0 ? (int64_t)((p.B + BM - 1) / BM) * ((p.K[l] + BN - 1) / BN) * p.nsplit_n[l] : 0;
+        mx = std::max(mx, std::max(f, w + h));
+    }
+    mx = std::max<int64_t>(mx, (p.B + NT / 32 - 1) / (NT / 32));
+    mx = std::max<int64_t>(mx, (p.P + NT - 1) / NT);
+    return (int)std::min<int64_t>(mx, d->sms);
+}
+
+extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *loss_dev)
+{
+    if (!d || !rp || batch < 1 || batch > d->cfg.max_batch || rp->ring.D != d->cfg.state_dim ||
+        rp->device != d->device) {
+        set_error("dqn_train_step: invalid argument (batch=%d max=%d)", batch,
+                  d ? d->cfg.max_batch : 0);
+        return RPL_EINVAL;
+    }
+    if (rp->size < rp->burn_in || rp->size < 1) return RPL_NOT_READY;   // P:44, nothing advances
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(d->device);
+    const int64_t t = d->steps + 1;
+    const int do_sync = d->cfg.sync_period > 0 && t % d->cfg.sync_period == 0;
+    const bool dp = d->comm != nullptr && d->world > 1;
+    TrainArgs p;
+    fill_args(d, rp, batch, loss_dev, dp ? 0 : 1, do_sync, p);
+    const int grid = grid_for(d, p);
+    void *args[] = {&p};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void *)train_step_kernel, dim3(grid),
+                                                dim3(NT), args, 0, d->stream);
+    if (e != cudaSuccess) {
+        if (prev >= 0) cudaSetDevice(prev);
+        return cuda_fail(e, "cudaLaunchCooperativeKernel(train_step_kernel)");
+    }
+    g_launches.fetch_add(1);
+    if (dp) {
+        int nr = g_nccl.allreduce(d->grad, d->grad, (size_t)d->P + 1, kNcclFloat, kNcclAvg,
+                                  d->comm, d->stream);
+        if (nr != 0) {
+            set_error("ncclAllReduce failed: %s", g_nccl.errstr ? g_nccl.errstr(nr) : "?");
+            if (prev >= 0) cudaSetDevice(prev);
+            return RPL_ENCCL;
+        }
+        sgd_kernel<<<(unsigned)d->sms, 256, 0, d->stream>>>(d->online, d->target, d->grad, d->P,
+                                                             d->cfg.lr, do_sync, d->err);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            if (prev >= 0) cudaSetDevice(prev);
+            return cuda_fail(e, "sgd_kernel");
+        }
+        g_launches.fetch_add(1);
+        if (loss_dev) cudaMemcpyAsync(loss_dev, d->grad + d->P, sizeof(float), cudaMemcpyDeviceToDevice, d->stream);
+    }
+    if (prev >= 0) cudaSetDevice(prev);
+    rp->events += 1;
+    d->steps = t;
+    d->last_B = batch;
+    return RPL_OK;
+}
+
+extern "C" int sync_target(rpl_dqn *d)
+{
+    if (!d) return RPL_EINVAL;
+    RPL_CUDA(cudaMemcpyAsync(d->target, d->online, (size_t)d->P * sizeof(float),
+                             cudaMemcpyDeviceToDevice, d->stream));
+    return RPL_OK;
+}
+
+static float *which_ptr(rpl_dqn *d, int which)
+{
+    return which == RPL_ONLINE ? d->online : which == RPL_TARGET ? d->target
+                                           : which == RPL_GRAD ? d->grad : nullptr;
+}
+
+extern "C" int dqn_get_params(rpl_dqn *d, int which, float *host_out, int64_t n)
+{
+    if (!d || !host_out || n != d->P || !which_ptr(d, which)) {
+        set_error("dqn_get_params: invalid argument");
+        return RPL_EINVAL;
+    }
+    RPL_CUDA(cudaMemcpyAsync(host_out, which_ptr(d, which), (size_t)n * sizeof(float),
+                             cudaMemcpyDeviceToHost, d->stream));
+    RPL_CUDA(cudaStreamSynchronize(d->stream));
+    return RPL_OK;
+}
+
+extern "C" int dqn_set_params(rpl_dqn *d, int which, const float *host_in, int64_t n)
+{
+    if (!d || !host_in || n != d->P || (which != RPL_ONLINE && which != RPL_TARGET)) {
+        set_error("dqn_set_params: invalid argument");
+        return RPL_EINVAL;
+    }
+    RPL_CUDA(cudaMemcpyAsync(which_ptr(d, which), host_in, (size_t)n * sizeof(float),
+                             cudaMemcpyHostToDevice, d->stream));
+    RPL_CUDA(cudaStreamSynchronize(d->stream));
+    return RPL_OK;
+}
+
+extern "C" int dqn_step_count(const rpl_dqn *d, int64_t *steps)
+{
+    if (!d || !steps) return RPL_EINVAL;
+    *steps = d->steps;
+    return RPL_OK;
+}
+
+extern "C" int dqn_debug_export(rpl_dqn *d, int what, void *host_out, int64_t bytes)
+{
+    if (!d || !host_out || d->last_B < 1) {
+        set_error("dqn_debug_export: no step executed yet");
+        return RPL_ESTATE;
+    }
+    const int64_t B = d->last_B, D = d->cfg.state_dim, A = d->cfg.n_actions;
+    const void *src = nullptr;
+    int64_t need = 0;
+    switch (what) {
+    case RPL_DBG_IDX: src = d->idx; need = B * 4; break;
+    case RPL_DBG_S: src = d->Xs; need = B * D * 4; break;
+    case RPL_DBG_S_NEXT: src = d->Xs2; need = B * D * 4; break;
+    case RPL_DBG_A: src = d->a; need = B * 4; break;
+    case RPL_DBG_R: src = d->r; need = B * 4; break;
+    case RPL_DBG_DONE: src = d->done; need = B; break;
+    case RPL_DBG_Q: src = d->Qs; need = B * A * 4; break;
+    case RPL_DBG_QT_NEXT: src = d->Qt2; need = B * A * 4; break;
+    case RPL_DBG_QO_NEXT: src = d->Qo2; need = B * A * 4; break;
+    case RPL_DBG_Y: src = d->y; need = B * 4; break;
+    case RPL_DBG_ASTAR: src = d->astar; need = B * 4; break;
+    case RPL_DBG_LOSS: src = d->grad + d->P; need = 4; break;
+    case RPL_DBG_H: need = B * d->Htot * 4; break;
+    default: set_error("dqn_debug_export: unknown item %d", what); return RPL_EINVAL;
+    }
+    if (bytes != need) {
+        set_error("dqn_debug_export: item %d needs %lld bytes, got %lld", what, (long long)need,
+                  (long long)bytes);
+        return RPL_EINVAL;
+    }
+    if (what == RPL_DBG_H) {
+        // hidden-unit space per sample: layer 0 units, layer 1 units, ... (online net on s)
+        std::vector<float> tmp;
+        int64_t off = 0;
+        float *o = (float *)host_out;
+        for (int l = 0; l < d->T; ++l) {
+            tmp.resize((size_t)B * d->N[l]);
+            RPL_CUDA(cudaMemcpyAsync(tmp.data(), d->H[l], tmp.size() * 4, cudaMemcpyDeviceToHost, d->stream));
+            RPL_CUDA(cudaStreamSynchronize(d->stream));
+            for (int64_t b = 0; b < B; ++b)
+                memcpy(o + b * d->Htot + off, tmp.data() + b * d->N[l], (size_t)d->N[l] * 4);
+            off += d->N[l];
+        }
+        return RPL_OK;
+    }
+    RPL_CUDA(cudaMemcpyAsync(host_out, src, (size_t)need, cudaMemcpyDeviceToHost, d->stream));
+    RPL_CUDA(cudaStreamSynchronize(d->stream));
+    return RPL_OK;
+}
+
+extern "C" int rpl_nccl_unique_id(void *out128)
+{
+    if (!out128) return RPL_EINVAL;
+    int rc = nccl_load();
+    if (rc != RPL_OK) return rc;
+    nccl_uid id;
+    int nr = g_nccl.get_uid(&id);
+    if (nr != 0) {
+        set_error("ncclGetUniqueId failed (%d)", nr);
+        return RPL_ENCCL;
+    }
+    memcpy(out128, &id, sizeof id);
+    return RPL_OK;
+}
+
+extern "C" int dqn_attach_nccl(rpl_dqn *d, int32_t rank, int32_t world, const void *id128)
+{
+    if (!d || !id128 || world < 1 || rank < 0 || rank >= world) return RPL_EINVAL;
+    if (d->comm) {
+        set_error("dqn_attach_nccl: already attached");
+        return RPL_ESTATE;
+    }
+    if (world == 1) return RPL_OK;
+    int rc = nccl_load();
+    if (rc != RPL_OK) return rc;
+    nccl_uid id;
+    memcpy(&id, id128, sizeof id);
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(d->device);
+    int nr = g_nccl.init_rank(&d->comm, world, id, rank);
+    if (prev >= 0) cudaSetDevice(prev);
+    if (nr != 0) {
+        d->comm = nullptr;
+        set_error("ncclCommInitRank failed: %s", g_nccl.errstr ? g_nccl.errstr(nr) : "?");
+        return RPL_ENCCL;
+    }
+    d->rank = rank;
+    d->world = world;
+    return RPL_OK;
+}
+
+extern "C" int rpl_check(void *handle, int kind)
+{
+    if (!handle || (kind != 0 && kind != 1)) return RPL_EINVAL;
+    cudaStream_t st;
+    uint32_t *err;
+    if (kind == 0) {
+        st = ((rpl_replay *)handle)->stream;
+        err = ((rpl_replay *)handle)->err_dev;
+    } else {
+        st = ((rpl_dqn *)handle)->stream;
+        err = ((rpl_dqn *)handle)->err;
+    }
+    RPL_CUDA(cudaStreamSynchronize(st));
+    uint32_t h = 0;
+    RPL_CUDA(cudaMemcpy(&h, err, sizeof h, cudaMemcpyDeviceToHost));
+    if (h) RPL_CUDA(cudaMemset(err, 0, sizeof h));
+    if (h & ERRBIT_CORRUPT) { set_error("corrupt terminal flag in a device-sourced add"); return RPL_ECORRUPT; }
+    if (h & ERRBIT_NUMERIC) { set_error("non-finite loss: update skipped"); return RPL_ENUMERIC; }
+    if (h & ERRBIT_RANGE) { set_error("gather index out of range (clamped)"); return RPL_EINVAL; }
+    return RPL_OK;
+}

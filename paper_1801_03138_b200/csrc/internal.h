@@ -1,0 +1,79 @@
+// internal.h -- shared internals of the CUDA path (NOT part of the C-ABI).
+//
+// The oracle never includes this file and this file never includes the oracle's.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "../../include/ingpu_replay.h"
+
+namespace rpl {
+
+// ---- error reporting -------------------------------------------------------------------
+void set_error(const char *fmt, ...);
+int cuda_fail(cudaError_t e, const char *what);   // records the message, returns RPL_ECUDA
+extern std::atomic<uint64_t> g_launches;            // kernels launched by this library
+
+#define RPL_CUDA(call)                                            \
+    do {                                                          \
+        cudaError_t _e = (call);                                  \
+        if (_e != cudaSuccess) return ::rpl::cuda_fail(_e, #call); \
+    } while (0)
+
+#define RPL_LAUNCHED()                                                   \
+    do {                                                                 \
+        cudaError_t _e = cudaGetLastError();                             \
+        if (_e != cudaSuccess) return ::rpl::cuda_fail(_e, "kernel launch"); \
+        ::rpl::g_launches.fetch_add(1, std::memory_order_relaxed);        \
+    } while (0)
+
+// sticky device-side error bits (written by kernels with atomicOr)
+enum : uint32_t { ERRBIT_CORRUPT = 1u, ERRBIT_NUMERIC = 2u, ERRBIT_RANGE = 4u };
+
+// Philox counter word 3 = (TAG << 24) | rank  (reading Q3)
+constexpr uint32_t TAG_SAMPLE = 1u;
+
+// ---- the replay ring ---------------------------------------------------------------------
+// Device row layout: row stride RS floats (multiple of 32,
+// i.e. 128-byte aligned rows):  [ s (D f32) | s' (D f32) | a (i32) | r (f32) | done (u32) | 0 ]
+struct Ring {
+    float *rows = nullptr;     // capacity * rs floats
+    int64_t capacity = 0;
+    int32_t D = 0;
+    int32_t rs = 0;            // row stride in floats
+};
+
+inline int32_t ring_row_stride(int32_t D) { return ((2 * D + 3) + 31) / 32 * 32; }
+
+}  // namespace rpl
+
+struct rpl_replay {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    rpl::Ring ring;
+    int64_t burn_in = 1;
+    uint64_t seed = 2;
+    uint32_t rank = 0;
+    // host mirror of the ring state (exact: every add is host-initiated with a known k)
+    int64_t cursor = 0, size = 0;
+    uint64_t total = 0, events = 0, h2d_bytes = 0;
+    // pinned host staging + device staging for RPL_HOST adds (double-buffered)
+    int64_t max_host_add = 65536;
+    void *pinned[2] = {nullptr, nullptr};
+    void *dstage[2] = {nullptr, nullptr};
+    cudaEvent_t staged[2] = {nullptr, nullptr};
+    int stage_slot = 0;
+    uint32_t *err_dev = nullptr;   // sticky device error word
+};
+
+namespace rpl {
+// launch helpers implemented in replay.cu, used by dqn.cu
+int launch_gather(const rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t event,
+                  int use_sampler, const rpl_batch *out);
+}  // namespace rpl

@@ -1,0 +1,413 @@
+// replay.cu -- the device FIFO ring of experiences: insert (replay_add), Philox sample +
+// gather + unpack (replay_sample / replay_gather), and the library's error plumbing.
+//
+// Paper: P:71-75 [Methods] (packed 1,000,000 x 57 Variable, block inserts, uniform integer
+// sampling + gather + unpack), P:44 (FIFO, burn-in).  B200 design: DESIGN.md "Kernels".
+#include <cstdarg>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "internal.h"
+#include "philox.cuh"
+
+namespace rpl {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string t_err;
+
+void set_error(const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_err = buf;
+}
+
+int cuda_fail(cudaError_t e, const char *what)
+{
+    set_error("CUDA error %d (%s) in %s", (int)e, cudaGetErrorString(e), what);
+    return RPL_ECUDA;
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev)
+    {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// ------------------------------------------------------------------------------------------
+// K1: insert.  One warp per experience; the warp writes the whole 128B-aligned row (one or
+// more fully coalesced 128-byte stores per 32 floats).  Slot = (cursor + j) mod capacity.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) insert_kernel(float *__restrict__ rows, int rs, int D,
+                                                     int64_t capacity, int64_t cursor, int64_t k,
+                                                     const float *__restrict__ s,
+                                                     const int32_t *__restrict__ a,
+                                                     const float *__restrict__ r,
+                                                     const float *__restrict__ s2,
+                                                     const uint8_t *__restrict__ done,
+                                                     uint32_t *err)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k;
+         j += nwarps) {
+        int64_t slot = cursor + j;
+        if (slot >= capacity) slot -= capacity;   // k <= capacity, cursor < capacity
+        float *row = rows + slot * rs;
+        for (int c = lane; c < rs; c += 32) {
+            float v = 0.0f;
+            if (c < D) {
+                v = s[j * D + c];
+            } else if (c < 2 * D) {
+                v = s2[j * D + (c - D)];
+            } else if (c == 2 * D) {
+                v = __int_as_float(a[j]);
+            } else if (c == 2 * D + 1) {
+                v = r[j];
+            } else if (c == 2 * D + 2) {
+                uint32_t d = done[j];
+                if (d > 1u) {
+                    atomicOr(err, ERRBIT_CORRUPT);
+                    d = 1u;
+                }
+                v = __uint_as_float(d);
+            }
+            row[c] = v;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K2+K3: Philox sample (or caller indices) + gather + unpack.  A warp owns groups of 64
+// consecutive batch entries: lane l draws entries (2l, 2l+1) with ONE Philox call (call j =
+// group/2 + l), then each half-warp gathers one row per iteration with 16-byte loads, 8 rows
+// per half-warp in flight, and scatters the fields into the five SoA outputs.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void store_field(int c, float v, int64_t i, int D, float *s,
+                                            float *s2, int32_t *a, float *r, uint8_t *done)
+{
+    if (c < D) {
+        if (s) s[i * D + c] = v;
+    } else if (c < 2 * D) {
+        if (s2) s2[i * D + (c - D)] = v;
+    } else if (c == 2 * D) {
+        if (a) a[i] = __float_as_int(v);
+    } else if (c == 2 * D + 1) {
+        if (r) r[i] = v;
+    } else if (c == 2 * D + 2) {
+        if (done) done[i] = (uint8_t)(__float_as_uint(v) != 0u);
+    }
+}
+
+template <bool kRow64>
+__global__ void __launch_bounds__(256) gather_kernel(const float *__restrict__ rows, int rs, int D,
+                                                     int64_t size, int64_t n,
+                                                     const int32_t *__restrict__ idx_in,
+                                                     uint64_t seed, uint32_t rank, uint64_t event,
+                                                     float *s, float *s2, int32_t *a, float *r,
+                                                     uint8_t *done, int32_t *idx_out, uint32_t *err)
+{
+    const int lane = threadIdx.x & 31;
+    const int half = lane >> 4, p = lane & 15;
+    const int64_t ngroups = (n + 63) / 64;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < ngroups;
+         g += nwarps) {
+        const int64_t base = g * 64;
+        int32_t i0, i1;
+        const int64_t e0 = base + 2 * lane;
+        if (idx_in == nullptr) {
+            sample_pair(seed, rank, event, (uint32_t)(g * 32 + lane), (uint64_t)size, i0, i1);
+        } else {
+            i0 = e0 < n ? idx_in[e0] : 0;
+            i1 = e0 + 1 < n ? idx_in[e0 + 1] : 0;
+            if (i0 < 0 || i0 >= size || i1 < 0 || i1 >= size) {
+                if (e0 < n) atomicOr(err, ERRBIT_RANGE);
+                i0 = min(max(i0, 0), (int32_t)size - 1);
+                i1 = min(max(i1, 0), (int32_t)size - 1);
+            }
+        }
+        if (idx_out) {
+            if (e0 < n) idx_out[e0] = i0;
+            if (e0 + 1 < n) idx_out[e0 + 1] = i1;
+        }
+        if (kRow64) {
+#pragma unroll
+            for (int u0 = 0; u0 < 32; u0 += 8) {
+                float4 v[8];
+                int64_t ent[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int32_t iA = __shfl_sync(0xffffffffu, i0, u0 + q);
+                    const int32_t iB = __shfl_sync(0xffffffffu, i1, u0 + q);
+                    const int32_t row = half ? iB : iA;
+                    ent[q] = base + 2 * (u0 + q) + half;
+                    if (ent[q] < n)
+                        v[q] = __ldg(reinterpret_cast<const float4 *>(rows + (int64_t)row * 64) + p);
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (ent[q] < n) {
+                        store_field(4 * p + 0, v[q].x, ent[q], D, s, s2, a, r, done);
+                        store_field(4 * p + 1, v[q].y, ent[q], D, s, s2, a, r, done);
+                        store_field(4 * p + 2, v[q].z, ent[q], D, s, s2, a, r, done);
+                        store_field(4 * p + 3, v[q].w, ent[q], D, s, s2, a, r, done);
+                    }
+                }
+            }
+        } else {
+            for (int u = 0; u < 32; ++u) {
+                const int32_t iA = __shfl_sync(0xffffffffu, i0, u);
+                const int32_t iB = __shfl_sync(0xffffffffu, i1, u);
+                const int32_t row = half ? iB : iA;
+                const int64_t ent = base + 2 * u + half;
+                if (ent >= n) continue;
+                const float4 *src = reinterpret_cast<const float4 *>(rows + (int64_t)row * rs);
+                for (int c4 = p; c4 < rs / 4; c4 += 16) {
+                    const float4 v = __ldg(src + c4);
+                    store_field(4 * c4 + 0, v.x, ent, D, s, s2, a, r, done);
+                    store_field(4 * c4 + 1, v.y, ent, D, s, s2, a, r, done);
+                    store_field(4 * c4 + 2, v.z, ent, D, s, s2, a, r, done);
+                    store_field(4 * c4 + 3, v.w, ent, D, s, s2, a, r, done);
+                }
+            }
+        }
+    }
+}
+
+int launch_gather(const rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t event,
+                  int use_sampler, const rpl_batch *out)
+{
+    const int64_t groups = (n + 63) / 64;
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, rp->device);
+    const int64_t warps_per_block = 8;
+    int64_t blocks = (groups + warps_per_block - 1) / warps_per_block;
+    const int64_t max_blocks = (int64_t)dev_sms * 8;
+    if (blocks > max_blocks) blocks = max_blocks;
+    if (blocks < 1) blocks = 1;
+    const rpl::Ring &R = rp->ring;
+    if (R.rs == 64) {
+        gather_kernel<true><<<(unsigned)blocks, 256, 0, rp->stream>>>(
+            R.rows, R.rs, R.D, rp->size, n, use_sampler ? nullptr : idx_dev, rp->seed, rp->rank,
+            event, out->s, out->s_next, out->a, out->r, out->done, out->idx, rp->err_dev);
+    } else {
+        gather_kernel<false><<<(unsigned)blocks, 256, 0, rp->stream>>>(
+            R.rows, R.rs, R.D, rp->size, n, use_sampler ? nullptr : idx_dev, rp->seed, rp->rank,
+            event, out->s, out->s_next, out->a, out->r, out->done, out->idx, rp->err_dev);
+    }
+    RPL_LAUNCHED();
+    return RPL_OK;
+}
+
+}  // namespace rpl
+
+using namespace rpl;
+
+// ==========================================================================================
+// C-ABI
+// ==========================================================================================
+extern "C" const char *rpl_last_error(void) { return rpl::t_err.c_str(); }
+extern "C" uint64_t rpl_kernel_launches(void) { return rpl::g_launches.load(); }
+
+static size_t host_add_bytes(int64_t k, int32_t D)
+{
+    return (size_t)k * (8 * (size_t)D + 4 + 4 + 1);
+}
+
+extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_replay_opts *opts,
+                             rpl_replay **out)
+{
+    if (!out) { set_error("replay_create: out is NULL"); return RPL_EINVAL; }
+    *out = nullptr;
+    rpl_replay_opts o{};
+    o.device = 0; o.cuda_stream = nullptr; o.burn_in = 1; o.seed = 2; o.rank = 0;
+    o.max_host_add = 0;
+    if (opts) o = *opts;
+    if (capacity < 1 || capacity >= (int64_t(1) << 31) || state_dim < 1 || state_dim > 1 << 20 ||
+        o.rank >= (1u << 24) || o.burn_in < 1 || o.max_host_add < 0) {
+        set_error("replay_create: invalid argument (capacity=%lld state_dim=%d rank=%u burn_in=%lld)",
+                  (long long)capacity, state_dim, o.rank, (long long)o.burn_in);
+        return RPL_EINVAL;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || o.device < 0 || o.device >= ndev) {
+        set_error("replay_create: no CUDA device %d (count %d)", o.device, ndev);
+        return RPL_ECUDA;
+    }
+    DeviceGuard g(o.device);
+    rpl_replay *rp = new rpl_replay();
+    rp->device = o.device;
+    rp->stream = (cudaStream_t)o.cuda_stream;
+    rp->burn_in = o.burn_in;
+    rp->seed = o.seed;
+    rp->rank = o.rank;
+    rp->max_host_add = o.max_host_add ? o.max_host_add : 65536;
+    if (rp->max_host_add > capacity) rp->max_host_add = capacity;
+    rp->ring.capacity = capacity;
+    rp->ring.D = state_dim;
+    rp->ring.rs = ring_row_stride(state_dim);
+    const size_t ring_bytes = (size_t)capacity * rp->ring.rs * sizeof(float);
+    cudaError_t e = cudaMalloc(&rp->ring.rows, ring_bytes);
+    if (e != cudaSuccess) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        set_error("replay_create: cudaMalloc of %zu ring bytes failed (%zu free)", ring_bytes, fr);
+        delete rp;
+        return RPL_ENOMEM;
+    }
+    const size_t st = host_add_bytes(rp->max_host_add, state_dim) + 64;
+    bool ok = cudaMalloc(&rp->err_dev, sizeof(uint32_t)) == cudaSuccess;
+    for (int i = 0; i < 2 && ok; ++i) {
+        ok = cudaHostAlloc(&rp->pinned[i], st, cudaHostAllocDefault) == cudaSuccess &&
+             cudaMalloc(&rp->dstage[i], st) == cudaSuccess &&
+             cudaEventCreateWithFlags(&rp->staged[i], cudaEventDisableTiming) == cudaSuccess;
+    }
+    if (!ok || cudaMemsetAsync(rp->err_dev, 0, sizeof(uint32_t), rp->stream) != cudaSuccess ||
+        cudaMemsetAsync(rp->ring.rows, 0, ring_bytes, rp->stream) != cudaSuccess) {
+        set_error("replay_create: staging allocation of %zu bytes failed", st);
+        replay_destroy(rp);
+        return RPL_ENOMEM;
+    }
+    *out = rp;
+    return RPL_OK;
+}
+
+extern "C" int replay_destroy(rpl_replay *rp)
+{
+    if (!rp) return RPL_OK;
+    DeviceGuard g(rp->device);
+    cudaStreamSynchronize(rp->stream);
+    for (int i = 0; i < 2; ++i) {
+        if (rp->staged[i]) cudaEventDestroy(rp->staged[i]);
+        if (rp->pinned[i]) cudaFreeHost(rp->pinned[i]);
+        if (rp->dstage[i]) cudaFree(rp->dstage[i]);
+    }
+    if (rp->err_dev) cudaFree(rp->err_dev);
+    if (rp->ring.rows) cudaFree(rp->ring.rows);
+    delete rp;
+    return RPL_OK;
+}
+
+extern "C" int replay_add(rpl_replay *rp, int64_t k, const float *s, const int32_t *a,
+                          const float *r, const float *s_next, const uint8_t *done, int mem)
+{
+    if (!rp) { set_error("replay_add: null handle"); return RPL_EINVAL; }
+    const int32_t D = rp->ring.D;
+    if (k < 0 || k > rp->ring.capacity || (mem != RPL_HOST && mem != RPL_DEVICE)) {
+        set_error("replay_add: invalid k=%lld (capacity %lld) or mem=%d", (long long)k,
+                  (long long)rp->ring.capacity, mem);
+        return RPL_EINVAL;
+    }
+    if (k == 0) return RPL_OK;
+    if (!s || !a || !r || !s_next || !done) {
+        set_error("replay_add: null input pointer");
+        return RPL_EINVAL;
+    }
+    DeviceGuard g(rp->device);
+    const float *ds = s, *dr = r, *ds2 = s_next;
+    const int32_t *da = a;
+    const uint8_t *dd = done;
+    if (mem == RPL_HOST) {
+        if (k > rp->max_host_add) {
+            set_error("replay_add: k=%lld exceeds max_host_add=%lld", (long long)k,
+                      (long long)rp->max_host_add);
+            return RPL_EINVAL;
+        }
+        for (int64_t j = 0; j < k; ++j)
+            if (done[j] > 1) {
+                set_error("replay_add: done[%lld]=%u not in {0,1}", (long long)j, done[j]);
+                return RPL_ECORRUPT;
+            }
+        const int slot = rp->stage_slot;
+        rp->stage_slot ^= 1;
+        // the pinned slot may still be read by the previous H2D copy from it
+        RPL_CUDA(cudaEventSynchronize(rp->staged[slot]));
+        char *hp = (char *)rp->pinned[slot];
+        char *dp = (char *)rp->dstage[slot];
+        const size_t bs = (size_t)k * D * sizeof(float);
+        size_t off = 0;
+        memcpy(hp + off, s, bs); ds = (const float *)(dp + off); off += bs;
+        memcpy(hp + off, s_next, bs); ds2 = (const float *)(dp + off); off += bs;
+        memcpy(hp + off, r, (size_t)k * 4); dr = (const float *)(dp + off); off += (size_t)k * 4;
+        memcpy(hp + off, a, (size_t)k * 4); da = (const int32_t *)(dp + off); off += (size_t)k * 4;
+        memcpy(hp + off, done, (size_t)k); dd = (const uint8_t *)(dp + off); off += (size_t)k;
+        RPL_CUDA(cudaMemcpyAsync(dp, hp, off, cudaMemcpyHostToDevice, rp->stream));
+        RPL_CUDA(cudaEventRecord(rp->staged[slot], rp->stream));
+        rp->h2d_bytes += off;
+    }
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, rp->device);
+    int64_t blocks = (k + 7) / 8;
+    if (blocks > (int64_t)dev_sms * 8) blocks = (int64_t)dev_sms * 8;
+    insert_kernel<<<(unsigned)blocks, 256, 0, rp->stream>>>(rp->ring.rows, rp->ring.rs, D,
+                                                            rp->ring.capacity, rp->cursor, k, ds,
+                                                            da, dr, ds2, dd, rp->err_dev);
+    RPL_LAUNCHED();
+    rp->cursor = (rp->cursor + k) % rp->ring.capacity;
+    rp->size = rp->size + k < rp->ring.capacity ? rp->size + k : rp->ring.capacity;
+    rp->total += (uint64_t)k;
+    return RPL_OK;
+}
+
+extern "C" int replay_sample(rpl_replay *rp, int32_t batch, const rpl_batch *out)
+{
+    if (!rp || !out || batch < 1) {
+        set_error("replay_sample: invalid argument (batch=%d)", batch);
+        return RPL_EINVAL;
+    }
+    if (rp->size < rp->burn_in) return RPL_NOT_READY;
+    DeviceGuard g(rp->device);
+    int rc = launch_gather(rp, batch, nullptr, rp->events, 1, out);
+    if (rc != RPL_OK) return rc;
+    rp->events += 1;
+    return RPL_OK;
+}
+
+extern "C" int replay_gather(rpl_replay *rp, int64_t n, const int32_t *idx_dev,
+                             const rpl_batch *out)
+{
+    if (!rp || !out || n < 0 || (n > 0 && !idx_dev)) {
+        set_error("replay_gather: invalid argument");
+        return RPL_EINVAL;
+    }
+    if (n == 0) return RPL_OK;
+    if (rp->size < 1) {
+        set_error("replay_gather: empty replay");
+        return RPL_ESTATE;
+    }
+    DeviceGuard g(rp->device);
+    return launch_gather(rp, n, idx_dev, 0, 0, out);
+}
+
+extern "C" int replay_size(const rpl_replay *rp, int64_t *size)
+{
+    if (!rp || !size) return RPL_EINVAL;
+    *size = rp->size;
+    return RPL_OK;
+}
+
+extern "C" int replay_state(const rpl_replay *rp, int64_t *cursor, int64_t *size,
+                            uint64_t *total, uint64_t *events, uint64_t *h2d_bytes)
+{
+    if (!rp) return RPL_EINVAL;
+    if (cursor) *cursor = rp->cursor;
+    if (size) *size = rp->size;
+    if (total) *total = rp->total;
+    if (events) *events = rp->events;
+    if (h2d_bytes) *h2d_bytes = rp->h2d_bytes;
+    return RPL_OK;
+}

@@ -1,0 +1,200 @@
+"""GPU parity of the fused train step (dqn_train_step through the C-ABI) against the oracle.
+
+Teacher-forced per step (tests/parity.py): idx and gathered batch bit-exact; Q, y, loss,
+gradients and new weights within 1e-5 normwise in FP32 (BASELINE north star); bit-exact in
+the dyadic exact-input mode.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from inputs import experiences, init_params
+from parity import f32, normwise, oracle_net, step_and_compare
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def b():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_1801_03138_b200.binding as binding
+    return binding
+
+
+def _cfg(b, **kw):
+    base = dict(state_dim=27, n_actions=8, dueling=True, hidden=(128,), stream=512,
+                double_dqn=False, gamma=0.99, lr=1e-3, huber_kappa=1.0, sync_period=0,
+                max_batch=4096)
+    base.update(kw)
+    return b.DQNConfig(**base)
+
+
+def _params(cfg, seed=3, dyadic=False):
+    return init_params(cfg.state_dim, cfg.n_actions, cfg.hidden, cfg.dueling, cfg.stream,
+                       seed=seed, dyadic=dyadic)
+
+
+@pytest.mark.parametrize("ddqn", [False, True], ids=["dqn", "ddqn"])
+def test_c1_200_steps_teacher_forced(b, ddqn):
+    # BASELINE configs[0]: capacity 1000, D=27, 8 actions, B=32, 2x64 MLP, burn-in 100,
+    # 200 executed train steps; 7 adds per iteration (the ring wraps in iteration 143);
+    # target sync every 50 steps
+    cfg = _cfg(b, dueling=False, hidden=(64, 64), double_dqn=ddqn, sync_period=50, max_batch=32)
+    p0 = _params(cfg)
+    rp = b.Replay(1000, 27, burn_in=100, seed=2)
+    dqn = b.DQN(cfg, p0)
+    orc = oracle.Ring(1000, 27)
+    e = experiences(214 * 7, seed=1)
+    stats = {}
+    ln = oracle.Learner(oracle_net(cfg), p0, gamma=f32(cfg.gamma), kappa=f32(cfg.huber_kappa),
+                        lr=f32(cfg.lr), double_dqn=ddqn, burn_in=100, sync_period=50, seed=2)
+    free_ring = oracle.Ring(1000, 27)
+    executed = 0
+    for it in range(1, 215):
+        part = {k: v[(it - 1) * 7:it * 7] for k, v in e.items()}
+        rp.add(**part)
+        orc.add(**part)
+        free_ring.add(**part)
+        out = step_and_compare(b, cfg, dqn, rp, orc, 32, seed=2, burn_in=100, stats=stats)
+        ln.step(free_ring, 32)
+        if out is None:
+            assert it <= 14
+            continue
+        executed += 1
+        t = executed
+        tgt = dqn.get_params(b.RPL_TARGET)
+        if t % 50 == 0:
+            assert np.array_equal(tgt, dqn.get_params(b.RPL_ONLINE))   # P:88 sync
+        else:
+            assert np.array_equal(tgt, out["target_before"])            # frozen
+    assert executed == 200 and dqn.steps == 200
+    # free-running drift of the fp32 device learner vs the fp64-arithmetic oracle learner
+    drift = normwise(dqn.get_params(b.RPL_ONLINE), ln.online, 1e-3, "200-step drift")
+    print(f"\nC1 {'DDQN' if ddqn else 'DQN'}: 200 steps, mask flips replayed {stats['mask_flips']},"
+          f" free-running drift {drift:.2e}")
+    assert dqn.check() == b.RPL_OK
+
+
+@pytest.mark.parametrize("ddqn", [False, True], ids=["dqn", "ddqn"])
+def test_paper_dueling_1m_ring_b128(b, ddqn):
+    # BASELINE configs[1]/[2]: 1,000,000-slot ring, 27-float states, batch 128, the paper's
+    # dueling net (27 -> 128 -> V 512 / A 512 -> 1 + 8); sampled steps at full size
+    cfg = _cfg(b, double_dqn=ddqn, lr=1e-3, max_batch=128, sync_period=2)
+    rp = b.Replay(1_000_000, 27, seed=2)
+    orc = oracle.Ring(1_000_000, 27)
+    e = experiences(1_000_000, seed=1)
+    rp.add_many(e)
+    orc.add_many(e)
+    dqn = b.DQN(cfg, _params(cfg))
+    for _ in range(4):
+        step_and_compare(b, cfg, dqn, rp, orc, 128, seed=2)
+    assert np.array_equal(dqn.get_params(b.RPL_TARGET), dqn.get_params(b.RPL_ONLINE))
+
+
+@pytest.mark.parametrize("batch", [1, 3, 33, 257, 1000, 4096])
+def test_batch_sweep_ddqn(b, batch):
+    # BASELINE configs[2]: Double DQN batch sweep 32..4096 plus ragged edge sizes
+    cfg = _cfg(b, double_dqn=True, max_batch=4096)
+    rp = b.Replay(50_000, 27, seed=5, rank=1)
+    orc = oracle.Ring(50_000, 27)
+    e = experiences(60_000, seed=6, done_prob=0.1)
+    rp.add_many(e)
+    orc.add_many(e)
+    dqn = b.DQN(cfg, _params(cfg, seed=7))
+    step_and_compare(b, cfg, dqn, rp, orc, batch, seed=5, rank=1)
+
+
+@pytest.mark.parametrize("net", [dict(dueling=False, hidden=(64, 64)),
+                                 dict(dueling=False, hidden=(50, 33, 17)),
+                                 dict(dueling=True, hidden=(48, 40), stream=72, n_actions=5),
+                                 dict(dueling=True, hidden=(128,), stream=512, n_actions=31)],
+                         ids=["2x64", "3layer-ragged", "dueling-small", "dueling-A31"])
+@pytest.mark.parametrize("kappa", [1.0, math.inf, 0.01])
+def test_other_nets_and_kappas(b, net, kappa):
+    cfg = _cfg(b, huber_kappa=kappa, double_dqn=True, max_batch=300, **net)
+    rp = b.Replay(5000, 27, seed=11)
+    orc = oracle.Ring(5000, 27)
+    e = experiences(5000, n_actions=cfg.n_actions, seed=12)
+    rp.add_many(e)
+    orc.add_many(e)
+    dqn = b.DQN(cfg, _params(cfg, seed=13))
+    for batch in (300, 77):
+        step_and_compare(b, cfg, dqn, rp, orc, batch, seed=11)
+
+
+@pytest.mark.parametrize("dueling", [False, True])
+def test_exact_input_mode_bitwise(b, dueling):
+    # dyadic states/weights/rewards and gamma = 0.5: every forward activation, Q, argmax and
+    # y (hence delta) is exact in fp32, so GPU == oracle bit for bit; the loss
+    # (delta^2 needs > 24 bits) and gradients are checked at the FP32 tolerance
+    cfg = _cfg(b, dueling=dueling, hidden=(128,) if dueling else (64, 64), gamma=0.5,
+               double_dqn=True, max_batch=128)
+    rp = b.Replay(4096, 27, seed=21)
+    orc = oracle.Ring(4096, 27)
+    e = experiences(4096, seed=22, dyadic=True)
+    rp.add_many(e)
+    orc.add_many(e)
+    dqn = b.DQN(cfg, _params(cfg, seed=23, dyadic=True))
+    dqn.set_params(_params(cfg, seed=24, dyadic=True), b.RPL_TARGET)
+    step_and_compare(b, cfg, dqn, rp, orc, 128, seed=21, exact=True)
+
+
+def test_burn_in_and_determinism_and_zero_h2d(b):
+    cfg = _cfg(b, max_batch=64, sync_period=3)
+    p0 = _params(cfg)
+    runs = []
+    for rep in range(2):
+        rp = b.Replay(1000, 27, burn_in=200, seed=31)
+        dqn = b.DQN(cfg, p0)
+        e = experiences(600, seed=32)
+        rp.add(**{k: v[:150] for k, v in e.items()})
+        # during burn-in nothing is enqueued and no counter advances
+        assert dqn.train_step(rp, 64) == b.RPL_NOT_READY
+        assert rp.state()["events"] == 0 and dqn.steps == 0
+        assert np.array_equal(dqn.get_params(b.RPL_ONLINE), p0)
+        rp.add(**{k: v[150:] for k, v in e.items()})
+        h2d = rp.state()["h2d_bytes"]
+        for _ in range(10):
+            assert dqn.train_step(rp, 64) == b.RPL_OK
+        # a train step copies nothing from the host
+        assert rp.state()["h2d_bytes"] == h2d == 600 * (8 * 27 + 9)
+        runs.append(dqn.get_params(b.RPL_ONLINE).tobytes() + dqn.get_params(b.RPL_TARGET).tobytes())
+    assert runs[0] == runs[1]   # same seeds -> byte-identical parameters
+
+
+def test_nonfinite_loss_skips_update(b):
+    import torch
+    cfg = _cfg(b, max_batch=64, sync_period=1)
+    rp = b.Replay(100, 27, seed=41)
+    e = experiences(100, seed=42)
+    e["r"][:] = np.nan
+    rp.add(**e)
+    dqn = b.DQN(cfg, _params(cfg))
+    p_before = dqn.get_params(b.RPL_ONLINE)
+    t_before = dqn.get_params(b.RPL_TARGET)
+    loss = torch.zeros(1, device="cuda")
+    assert dqn.train_step(rp, 64, loss) == b.RPL_OK
+    assert dqn.check() == b.RPL_ENUMERIC
+    assert np.isnan(loss.item())
+    assert np.array_equal(dqn.get_params(b.RPL_ONLINE), p_before)
+    assert np.array_equal(dqn.get_params(b.RPL_TARGET), t_before)
+
+
+def test_explicit_sync_target_and_set_get(b):
+    cfg = _cfg(b, max_batch=32)
+    rp = b.Replay(500, 27, seed=51)
+    rp.add(**experiences(500, seed=52))
+    dqn = b.DQN(cfg, _params(cfg))
+    for _ in range(3):
+        dqn.train_step(rp, 32)
+    assert not np.array_equal(dqn.get_params(b.RPL_TARGET), dqn.get_params(b.RPL_ONLINE))
+    dqn.sync_target()
+    assert np.array_equal(dqn.get_params(b.RPL_TARGET), dqn.get_params(b.RPL_ONLINE))
+    with pytest.raises(b.RplError):
+        dqn.train_step(rp, 33)   # > max_batch
+    with pytest.raises(b.RplError):
+        dqn.set_params(np.zeros(5, np.float32))
