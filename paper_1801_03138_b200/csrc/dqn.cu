@@ -20,18 +20,17 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "internal.h"
 #include "philox.cuh"
+#include "simt_gemm.cuh"
+#include "train_fast.cuh"
 
 namespace rpl {
 
-constexpr int NT = 256;   // threads per CTA
-constexpr int BM = 32;    // tile rows
-constexpr int BN = 64;    // tile cols
-constexpr int BK = 32;    // contraction chunk
 constexpr int MAXL = 5;   // trunk layers (4 shared + dueling stream layer)
 constexpr int MAXA = 32;  // actions (one warp)
 constexpr int MAXJ = MAXA + 1;
@@ -72,11 +71,12 @@ struct TrainArgs {
     int apply_update, do_sync;
     unsigned *bar;         // [0] arrivals, [1] generation
     uint32_t *err;
+    uint64_t *rctrl;       // replay control block: [0] events, [1] size
+    int64_t *step_dev;
+    int32_t *sync_flag;
 };
 
-struct __align__(16) TileSmem {
-    float As[BK][BM + 4];
-    float Bs[BK][BN + 4];
+struct __align__(16) TileSmem : GemmSmem {
     int idx[BM];
     float red[NT / 32];
     float head[NT / 32][MAXJ + 3];
@@ -112,136 +112,6 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar)
     __syncthreads();
 }
 
-// ------------------------------------------------------------------------------------------
-// 32x64 register-tiled FP32 GEMM tile: C[m][n] = sum_{kk in [kb,ke)} A(m,kk) * B(n,kk).
-// Operand loaders return 0 outside their bounds.  Each thread owns a 2x4 block of C.
-// The next chunk is fetched into registers while the current one is multiplied.
-// If want_rowsum, rs(m, sum_kk A(m,kk)) is also produced (bias gradients).
-// ------------------------------------------------------------------------------------------
-template <class LA, class LB, class EPI, class RSUM>
-__device__ __forceinline__ void gemm_tile(const LA &la, const LB &lb, int m0, int n0, int kb,
-                                          int ke, const EPI &epi, bool want_rowsum,
-                                          const RSUM &rs, TileSmem &sm)
-{
-    const int tid = threadIdx.x, tn = tid & 15, tm = tid >> 4;
-    float acc[2][4];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
-    float rsum0 = 0.0f, rsum1 = 0.0f;
-    constexpr int NA = BM * BK / NT, NB = BN * BK / NT;
-    float ra[NA], rb[NB];
-    auto fetch = [&](int k0) {
-#pragma unroll
-        for (int i = 0; i < NA; ++i) {
-            const int e = i * NT + tid;
-            const int r = LA::kKContig ? e / BK : e % BM;
-            const int kk = LA::kKContig ? e % BK : e / BM;
-            ra[i] = la(m0 + r, k0 + kk);
-        }
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            const int e = i * NT + tid;
-            const int r = LB::kKContig ? e / BK : e % BN;
-            const int kk = LB::kKContig ? e % BK : e / BN;
-            rb[i] = lb(n0 + r, k0 + kk);
-        }
-    };
-    auto stash = [&]() {
-#pragma unroll
-        for (int i = 0; i < NA; ++i) {
-            const int e = i * NT + tid;
-            const int r = LA::kKContig ? e / BK : e % BM;
-            const int kk = LA::kKContig ? e % BK : e / BM;
-            sm.As[kk][r] = ra[i];
-        }
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            const int e = i * NT + tid;
-            const int r = LB::kKContig ? e / BK : e % BN;
-            const int kk = LB::kKContig ? e % BK : e / BN;
-            sm.Bs[kk][r] = rb[i];
-        }
-    };
-    const int nchunks = (ke - kb + BK - 1) / BK;
-    if (nchunks > 0) {
-        fetch(kb);
-        stash();
-        __syncthreads();
-        for (int c = 0; c < nchunks; ++c) {
-            if (c + 1 < nchunks) fetch(kb + (c + 1) * BK);
-#pragma unroll 8
-            for (int k = 0; k < BK; ++k) {
-                const float2 av = *reinterpret_cast<const float2 *>(&sm.As[k][2 * tm]);
-                const float4 bv = *reinterpret_cast<const float4 *>(&sm.Bs[k][4 * tn]);
-                acc[0][0] = fmaf(av.x, bv.x, acc[0][0]);
-                acc[0][1] = fmaf(av.x, bv.y, acc[0][1]);
-                acc[0][2] = fmaf(av.x, bv.z, acc[0][2]);
-                acc[0][3] = fmaf(av.x, bv.w, acc[0][3]);
-                acc[1][0] = fmaf(av.y, bv.x, acc[1][0]);
-                acc[1][1] = fmaf(av.y, bv.y, acc[1][1]);
-                acc[1][2] = fmaf(av.y, bv.z, acc[1][2]);
-                acc[1][3] = fmaf(av.y, bv.w, acc[1][3]);
-            }
-            if (want_rowsum && tn == 0) {
-                for (int k = 0; k < BK; ++k) {
-                    rsum0 += sm.As[k][2 * tm];
-                    rsum1 += sm.As[k][2 * tm + 1];
-                }
-            }
-            __syncthreads();
-            if (c + 1 < nchunks) {
-                stash();
-                __syncthreads();
-            }
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) epi(m0 + 2 * tm + i, n0 + 4 * tn + j, acc[i][j]);
-    if (want_rowsum && tn == 0) {
-        rs(m0 + 2 * tm, rsum0);
-        rs(m0 + 2 * tm + 1, rsum1);
-    }
-}
-
-// ---- operand loaders --------------------------------------------------------------------
-// row-major [rows x ld] matrix, element (r, kk) = p[r*ld + kk], valid for r < R, kk < KE
-struct LdKMajor {
-    static constexpr bool kKContig = true;
-    const float *p;
-    int ld, R, KE;
-    __device__ float operator()(int r, int kk) const
-    {
-        return (r < R && kk < KE) ? __ldcg(p + (int64_t)r * ld + kk) : 0.0f;
-    }
-};
-// element (r, kk) = p[kk*ld + r] (contiguous along r), valid for r < R, kk in [KB, KE)
-struct LdRMajor {
-    static constexpr bool kKContig = false;
-    const float *p;
-    int ld, R, KB, KE;
-    __device__ float operator()(int r, int kk) const
-    {
-        return (r < R && kk >= KB && kk < KE) ? __ldcg(p + (int64_t)kk * ld + r) : 0.0f;
-    }
-};
-// gathered replay rows: element (m, k) = ring[idx[m - m0] * rs + col0 + k]
-struct LdRing {
-    static constexpr bool kKContig = true;
-    const float *ring;
-    const int *idx_s;
-    int m0, rs, col0, R, KE;
-    __device__ float operator()(int m, int k) const
-    {
-        return (m < R && k < KE) ? __ldg(ring + (int64_t)idx_s[m - m0] * rs + col0 + k) : 0.0f;
-    }
-};
-
-// dZ_l[b][n] of the online net: materialised for the last trunk layer, otherwise the
-// deterministic sum of the split-K partials of dH_l times the ReLU mask of layer l
 __device__ __forceinline__ float dz_val(const TrainArgs &p, int l, int b, int n)
 {
     const int N = p.N[l];
@@ -273,17 +143,6 @@ struct LdDz {
         return (b < B && n >= KB && n < KE) ? dz_val(*p, l, b, n) : 0.0f;
     }
 };
-
-struct NoRowsum {
-    __device__ void operator()(int, float) const {}
-};
-
-__device__ __forceinline__ float warp_sum(float v)
-{
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
 
 // ------------------------------------------------------------------------------------------
 // phases
@@ -604,6 +463,9 @@ __device__ void phase_sgd(const TrainArgs &p, TileSmem &sm)
         p.grad[p.P] = loss;
         if (p.loss_out) *p.loss_out = loss;
         if (!ok) atomicOr(p.err, ERRBIT_NUMERIC);
+        p.rctrl[0] = p.event + 1;
+        *p.step_dev += 1;
+        *p.sync_flag = p.do_sync;
     }
 }
 
@@ -625,8 +487,10 @@ __global__ void __launch_bounds__(NT, 1) train_step_kernel(const __grid_constant
 
 // SGD after an NCCL all-reduce (world > 1): grad[P] holds the rank-averaged loss
 __global__ void __launch_bounds__(256) sgd_kernel(float *online, float *target, const float *grad,
-                                                  int64_t P, float lr, int do_sync, uint32_t *err)
+                                                  int64_t P, float lr, const int32_t *sync_flag,
+                                                  uint32_t *err)
 {
+    const int do_sync = *sync_flag;
     const float loss = grad[P];
     const bool ok = isfinite(loss);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
@@ -710,6 +574,21 @@ struct rpl_dqn {
     int64_t gpart_elems = 0, pdh_elems[MAXL] = {};
     int64_t steps = 0;
     int last_B = 0;
+    // fast path (two trunk layers): head partials, dH0 split-K partials, device counters
+    bool fast = false;
+    float *part = nullptr, *dH0p = nullptr;
+    int64_t part_elems = 0, dh0p_elems = 0;
+    int64_t *step_dev = nullptr;
+    int32_t *sync_flag = nullptr;
+    cudaStream_t cap_stream = nullptr;
+    struct GraphEntry {
+        const rpl_replay *rp;
+        int B;
+        float *loss;
+        cudaGraphExec_t exec;
+    };
+    std::vector<GraphEntry> graphs;
+    bool use_graphs = true;
     // data parallel
     void *comm = nullptr;
     int rank = 0, world = 1;
@@ -795,6 +674,31 @@ static bool dalloc(rpl_dqn *d, T **p, size_t n)
     return true;
 }
 
+// ---- fast-path sizing (host) ---------------------------------------------------------------
+static int fast_ut(int N1) { return N1 > 64 ? 128 : (N1 > 32 ? 64 : 32); }
+static size_t fast_fwd_smem(const rpl_dqn *d, int ut)
+{
+    const FwdLayout L(d->cfg.state_dim, d->N[0], ut, d->J);
+    return (size_t)L.total * sizeof(float);
+}
+// split-K count of dH0 = dZ1 W1 so that K3 has about one task per SM
+static int fast_ns(const rpl_dqn *d, int B)
+{
+    const int n_w = ((d->N[1] + BM - 1) / BM) * ((d->N[0] + BN - 1) / BN) * ((B + 511) / 512);
+    const int tiles = ((B + BM - 1) / BM) * ((d->N[0] + BN - 1) / BN);
+    int want = (d->sms - n_w) / tiles;
+    int ns = 1;
+    while (ns * 2 <= want && ns * 2 * 32 <= d->N[1]) ns *= 2;
+    return ns;
+}
+static int fast_max_ns(const rpl_dqn *d)
+{
+    int m = 1;
+    for (int B = 1; B <= d->cfg.max_batch; B = B < d->cfg.max_batch ? std::min(2 * B, d->cfg.max_batch) : B + 1)
+        m = std::max(m, fast_ns(d, B));
+    return std::max(m, fast_ns(d, 1));
+}
+
 extern "C" int dqn_destroy(rpl_dqn *d)
 {
     if (!d) return RPL_OK;
@@ -803,6 +707,8 @@ extern "C" int dqn_destroy(rpl_dqn *d)
     cudaSetDevice(d->device);
     cudaStreamSynchronize(d->stream);
     if (d->comm && g_nccl.destroy) g_nccl.destroy(d->comm);
+    for (auto &g : d->graphs) cudaGraphExecDestroy(g.exec);
+    if (d->cap_stream) cudaStreamDestroy(d->cap_stream);
     for (void *p : d->allocs) cudaFree(p);
     delete d;
     if (prev >= 0) cudaSetDevice(prev);
@@ -860,6 +766,27 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
             ok = dalloc(d, &d->PdH[l], d->pdh_elems[l]);
         }
     }
+    // fast path: two trunk layers (dueling with one shared layer, or a plain 2-hidden-layer MLP)
+    const char *path = getenv("RPL_PATH");
+    d->fast = d->T == 2 && d->N[0] % 4 == 0 && d->N[0] <= 256 && D <= 64 && d->J <= F_MAXJ &&
+              d->woff[1] % 4 == 0 && !(path && strcmp(path, "generic") == 0);
+    const char *ng = getenv("RPL_NO_GRAPH");
+    d->use_graphs = !(ng && ng[0] == '1');
+    ok = ok && dalloc(d, &d->step_dev, 1) && dalloc(d, &d->sync_flag, 1);
+    if (ok && d->fast) {
+        const int ut = fast_ut(d->N[1]);
+        const int nut = (d->N[1] + ut - 1) / ut;
+        d->part_elems = (int64_t)nets * nut * Bm * d->J;
+        d->dh0p_elems = (int64_t)fast_max_ns(d) * Bm * d->N[0];
+        ok = dalloc(d, &d->part, d->part_elems) && dalloc(d, &d->dH0p, d->dh0p_elems);
+        ok = ok && cudaStreamCreateWithFlags(&d->cap_stream, cudaStreamNonBlocking) == cudaSuccess;
+        ok = ok && cudaFuncSetAttribute(fast_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        fast_fwd_smem(d, 128)) == cudaSuccess;
+        ok = ok && cudaFuncSetAttribute(fast_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        fast_fwd_smem(d, 64)) == cudaSuccess;
+        ok = ok && cudaFuncSetAttribute(fast_fwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        fast_fwd_smem(d, 32)) == cudaSuccess;
+    }
     if (!ok) {
         if (!coop) set_error("dqn_create: device %d lacks cooperative launch", d->device);
         else set_error("dqn_create: device allocation failed");
@@ -873,6 +800,8 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
     if (e == cudaSuccess) e = cudaMemsetAsync(d->bar, 0, 2 * sizeof(unsigned) + 16, d->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(d->err, 0, sizeof(uint32_t), d->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(d->grad, 0, (d->P + 1) * sizeof(float), d->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d->step_dev, 0, sizeof(int64_t), d->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d->sync_flag, 0, sizeof(int32_t), d->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(d->stream);
     if (prev >= 0) cudaSetDevice(prev);
     if (e != cudaSuccess) {
@@ -946,6 +875,97 @@ static void fill_args(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.do_sync = do_sync;
     p.bar = d->bar;
     p.err = d->err;
+    p.rctrl = rp->ctrl_dev;
+    p.step_dev = d->step_dev;
+    p.sync_flag = d->sync_flag;
+}
+
+static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int apply, FastArgs &p)
+{
+    memset(&p, 0, sizeof p);
+    const rpl_dqn_config &c = d->cfg;
+    p.ring = rp->ring.rows;
+    p.rs = rp->ring.rs;
+    p.D = rp->ring.D;
+    p.rctrl = rp->ctrl_dev;
+    p.seed = rp->seed;
+    p.rank = rp->rank;
+    p.A = c.n_actions;
+    p.dueling = c.dueling;
+    p.J = d->J;
+    p.S = c.dueling ? c.stream : 0;
+    p.N0 = d->N[0];
+    p.N1 = d->N[1];
+    p.nets = c.double_dqn ? 3 : 2;
+    p.ddqn = c.double_dqn;
+    p.w0 = d->woff[0];
+    p.b0 = d->boff[0];
+    p.w1 = d->woff[1];
+    p.b1 = d->boff[1];
+    p.wh = d->hw_off;
+    p.bh = d->hb_off;
+    p.P = d->P;
+    p.B = B;
+    p.gamma = c.gamma;
+    p.lr = c.lr;
+    p.kinf = std::isinf(c.huber_kappa) ? 1 : 0;
+    p.kappa = p.kinf ? 0.0f : c.huber_kappa;
+    p.sync_period = c.sync_period;
+    p.online = d->online;
+    p.target = d->target;
+    p.Xs = d->Xs;
+    p.Xs2 = d->Xs2;
+    p.r = d->r;
+    p.a = d->a;
+    p.idx = d->idx;
+    p.done = d->done;
+    p.H0 = d->H[0];
+    p.H1 = d->H[1];
+    p.part = d->part;
+    p.UT = fast_ut(p.N1);
+    p.nut = (p.N1 + p.UT - 1) / p.UT;
+    p.dHead = d->dO;
+    p.dZ1 = d->dZlast;
+    p.dH0p = d->dH0p;
+    p.NS = fast_ns(d, B);
+    p.nsb = (B + 511) / 512;
+    p.bsplit = 512;
+    p.gpart = p.nsb == 1 ? d->grad : d->gpart;
+    p.grad = d->grad;
+    p.loss_part = d->loss_part;
+    p.Qs = d->Qs;
+    p.Qt2 = d->Qt2;
+    p.Qo2 = d->Qo2;
+    p.y = d->y;
+    p.astar = d->astar;
+    p.loss_out = loss_dev ? loss_dev : d->loss_dev;
+    p.step_dev = d->step_dev;
+    p.sync_flag = d->sync_flag;
+    p.apply_update = apply;
+    p.err = d->err;
+}
+
+// the four fast-path kernels, enqueued on `st`
+static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
+{
+    const int nbt = (p.B + F_BT - 1) / F_BT;
+    const int k1_tasks = p.nets * nbt * p.nut;
+    const int g1 = std::min(k1_tasks, 2 * d->sms);
+    const size_t sm1 = fast_fwd_smem(d, p.UT);
+    if (p.UT == 128) fast_fwd_kernel<128><<<g1, NT, sm1, st>>>(p);
+    else if (p.UT == 64) fast_fwd_kernel<64><<<g1, NT, sm1, st>>>(p);
+    else fast_fwd_kernel<32><<<g1, NT, sm1, st>>>(p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    fast_td_kernel<<<std::min(p.B, 4 * d->sms), NT, 0, st>>>(p);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const int n_w = ((p.N1 + BM - 1) / BM) * ((p.N0 + BN - 1) / BN) * p.nsb;
+    const int n_h = ((p.B + BM - 1) / BM) * ((p.N0 + BN - 1) / BN) * p.NS;
+    const int n_hd = ((p.N1 + NT - 1) / NT + 1) * p.nsb;
+    fast_bwd1_kernel<<<std::min(n_w + n_h + n_hd, 4 * d->sms), NT, 0, st>>>(p);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    fast_bwd0_sgd_kernel<<<std::max(std::min(p.N0, 4 * d->sms), d->sms), NT, 0, st>>>(p);
+    return cudaGetLastError();
 }
 
 static int grid_for(const rpl_dqn *d, const TrainArgs &p)
@@ -978,17 +998,55 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
     const int64_t t = d->steps + 1;
     const int do_sync = d->cfg.sync_period > 0 && t % d->cfg.sync_period == 0;
     const bool dp = d->comm != nullptr && d->world > 1;
-    TrainArgs p;
-    fill_args(d, rp, batch, loss_dev, dp ? 0 : 1, do_sync, p);
-    const int grid = grid_for(d, p);
-    void *args[] = {&p};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void *)train_step_kernel, dim3(grid),
-                                                dim3(NT), args, 0, d->stream);
-    if (e != cudaSuccess) {
-        if (prev >= 0) cudaSetDevice(prev);
-        return cuda_fail(e, "cudaLaunchCooperativeKernel(train_step_kernel)");
+    cudaError_t e = cudaSuccess;
+    if (d->fast) {
+        FastArgs fp;
+        fill_fast(d, rp, batch, dp ? nullptr : loss_dev, dp ? 0 : 1, fp);
+        if (d->use_graphs) {
+            cudaGraphExec_t exec = nullptr;
+            float *lkey = dp ? nullptr : loss_dev;
+            for (auto &g : d->graphs)
+                if (g.rp == rp && g.B == batch && g.loss == lkey) exec = g.exec;
+            if (!exec) {
+                cudaGraph_t graph = nullptr;
+                e = cudaStreamBeginCapture(d->cap_stream, cudaStreamCaptureModeThreadLocal);
+                if (e == cudaSuccess) {
+                    cudaError_t e2 = fast_enqueue(d, fp, d->cap_stream);
+                    e = cudaStreamEndCapture(d->cap_stream, &graph);
+                    if (e2 != cudaSuccess) e = e2;
+                }
+                if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+                if (graph) cudaGraphDestroy(graph);
+                if (e == cudaSuccess) {
+                    if (d->graphs.size() >= 16) {
+                        cudaGraphExecDestroy(d->graphs.front().exec);
+                        d->graphs.erase(d->graphs.begin());
+                    }
+                    d->graphs.push_back({rp, batch, lkey, exec});
+                }
+            }
+            if (e == cudaSuccess) e = cudaGraphLaunch(exec, d->stream);
+        } else {
+            e = fast_enqueue(d, fp, d->stream);
+        }
+        if (e != cudaSuccess) {
+            if (prev >= 0) cudaSetDevice(prev);
+            return cuda_fail(e, "fast train step");
+        }
+        g_launches.fetch_add(4);
+    } else {
+        TrainArgs p;
+        fill_args(d, rp, batch, loss_dev, dp ? 0 : 1, do_sync, p);
+        const int grid = grid_for(d, p);
+        void *args[] = {&p};
+        e = cudaLaunchCooperativeKernel((const void *)train_step_kernel, dim3(grid), dim3(NT), args,
+                                        0, d->stream);
+        if (e != cudaSuccess) {
+            if (prev >= 0) cudaSetDevice(prev);
+            return cuda_fail(e, "cudaLaunchCooperativeKernel(train_step_kernel)");
+        }
+        g_launches.fetch_add(1);
     }
-    g_launches.fetch_add(1);
     if (dp) {
         int nr = g_nccl.allreduce(d->grad, d->grad, (size_t)d->P + 1, kNcclFloat, kNcclAvg,
                                   d->comm, d->stream);
@@ -998,7 +1056,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             return RPL_ENCCL;
         }
         sgd_kernel<<<(unsigned)d->sms, 256, 0, d->stream>>>(d->online, d->target, d->grad, d->P,
-                                                             d->cfg.lr, do_sync, d->err);
+                                                             d->cfg.lr, d->sync_flag, d->err);
         e = cudaGetLastError();
         if (e != cudaSuccess) {
             if (prev >= 0) cudaSetDevice(prev);
@@ -1007,6 +1065,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
         g_launches.fetch_add(1);
         if (loss_dev) cudaMemcpyAsync(loss_dev, d->grad + d->P, sizeof(float), cudaMemcpyDeviceToDevice, d->stream);
     }
+    (void)do_sync;
     if (prev >= 0) cudaSetDevice(prev);
     rp->events += 1;
     d->steps = t;

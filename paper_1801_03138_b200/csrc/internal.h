@@ -70,6 +70,9 @@ struct rpl_replay {
     cudaEvent_t staged[2] = {nullptr, nullptr};
     int stage_slot = 0;
     uint32_t *err_dev = nullptr;   // sticky device error word
+    // device control block read by graph-replayed train steps: [0] sampler events consumed,
+    // [1] filled size (kept equal to the host mirror by the kernels that change them)
+    uint64_t *ctrl_dev = nullptr;
 };
 
 namespace rpl {

@@ -58,9 +58,10 @@ __global__ void __launch_bounds__(256) insert_kernel(float *__restrict__ rows, i
                                                      const float *__restrict__ r,
                                                      const float *__restrict__ s2,
                                                      const uint8_t *__restrict__ done,
-                                                     uint32_t *err)
+                                                     uint32_t *err, uint64_t *ctrl, int64_t new_size)
 {
     const int lane = threadIdx.x & 31;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctrl[1] = (uint64_t)new_size;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k;
          j += nwarps) {
@@ -118,8 +119,10 @@ __global__ void __launch_bounds__(256) gather_kernel(const float *__restrict__ r
                                                      const int32_t *__restrict__ idx_in,
                                                      uint64_t seed, uint32_t rank, uint64_t event,
                                                      float *s, float *s2, int32_t *a, float *r,
-                                                     uint8_t *done, int32_t *idx_out, uint32_t *err)
+                                                     uint8_t *done, int32_t *idx_out, uint32_t *err,
+                                                     uint64_t *ctrl)
 {
+    if (idx_in == nullptr && ctrl && blockIdx.x == 0 && threadIdx.x == 0) ctrl[0] = event + 1;
     const int lane = threadIdx.x & 31;
     const int half = lane >> 4, p = lane & 15;
     const int64_t ngroups = (n + 63) / 64;
@@ -203,11 +206,13 @@ int launch_gather(const rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint6
     if (R.rs == 64) {
         gather_kernel<true><<<(unsigned)blocks, 256, 0, rp->stream>>>(
             R.rows, R.rs, R.D, rp->size, n, use_sampler ? nullptr : idx_dev, rp->seed, rp->rank,
-            event, out->s, out->s_next, out->a, out->r, out->done, out->idx, rp->err_dev);
+            event, out->s, out->s_next, out->a, out->r, out->done, out->idx, rp->err_dev,
+            rp->ctrl_dev);
     } else {
         gather_kernel<false><<<(unsigned)blocks, 256, 0, rp->stream>>>(
             R.rows, R.rs, R.D, rp->size, n, use_sampler ? nullptr : idx_dev, rp->seed, rp->rank,
-            event, out->s, out->s_next, out->a, out->r, out->done, out->idx, rp->err_dev);
+            event, out->s, out->s_next, out->a, out->r, out->done, out->idx, rp->err_dev,
+            rp->ctrl_dev);
     }
     RPL_LAUNCHED();
     return RPL_OK;
@@ -270,7 +275,9 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
         return RPL_ENOMEM;
     }
     const size_t st = host_add_bytes(rp->max_host_add, state_dim) + 64;
-    bool ok = cudaMalloc(&rp->err_dev, sizeof(uint32_t)) == cudaSuccess;
+    bool ok = cudaMalloc(&rp->err_dev, sizeof(uint32_t)) == cudaSuccess &&
+              cudaMalloc(&rp->ctrl_dev, 2 * sizeof(uint64_t)) == cudaSuccess &&
+              cudaMemsetAsync(rp->ctrl_dev, 0, 2 * sizeof(uint64_t), rp->stream) == cudaSuccess;
     for (int i = 0; i < 2 && ok; ++i) {
         ok = cudaHostAlloc(&rp->pinned[i], st, cudaHostAllocDefault) == cudaSuccess &&
              cudaMalloc(&rp->dstage[i], st) == cudaSuccess &&
@@ -297,6 +304,7 @@ extern "C" int replay_destroy(rpl_replay *rp)
         if (rp->dstage[i]) cudaFree(rp->dstage[i]);
     }
     if (rp->err_dev) cudaFree(rp->err_dev);
+    if (rp->ctrl_dev) cudaFree(rp->ctrl_dev);
     if (rp->ring.rows) cudaFree(rp->ring.rows);
     delete rp;
     return RPL_OK;
@@ -353,12 +361,14 @@ extern "C" int replay_add(rpl_replay *rp, int64_t k, const float *s, const int32
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, rp->device);
     int64_t blocks = (k + 7) / 8;
     if (blocks > (int64_t)dev_sms * 8) blocks = (int64_t)dev_sms * 8;
+    const int64_t new_size = rp->size + k < rp->ring.capacity ? rp->size + k : rp->ring.capacity;
     insert_kernel<<<(unsigned)blocks, 256, 0, rp->stream>>>(rp->ring.rows, rp->ring.rs, D,
                                                             rp->ring.capacity, rp->cursor, k, ds,
-                                                            da, dr, ds2, dd, rp->err_dev);
+                                                            da, dr, ds2, dd, rp->err_dev,
+                                                            rp->ctrl_dev, new_size);
     RPL_LAUNCHED();
     rp->cursor = (rp->cursor + k) % rp->ring.capacity;
-    rp->size = rp->size + k < rp->ring.capacity ? rp->size + k : rp->ring.capacity;
+    rp->size = new_size;
     rp->total += (uint64_t)k;
     return RPL_OK;
 }
