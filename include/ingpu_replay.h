@@ -189,10 +189,13 @@ int dqn_step_count(const rpl_dqn *dqn, int64_t *steps);
  *   RPL_DBG_H        [B*H] f32 online-net activations on s over the hidden-unit space
  *                    (shared layers in order, then the stream units [V | A])
  *   RPL_DBG_LOSS     [1] f32
+ *   RPL_DBG_TRACE    [4 x 2048 x 8] u64 per-CTA %globaltimer (ns) marks of the four fast-path
+ *                    kernels of the last step: [0] start, [1] end, [2..7] phase marks (only
+ *                    with env RPL_TRACE=1)
  * `bytes` must equal the size of that array for the last step's batch. */
 enum { RPL_DBG_IDX = 0, RPL_DBG_S, RPL_DBG_S_NEXT, RPL_DBG_A, RPL_DBG_R, RPL_DBG_DONE,
        RPL_DBG_Q, RPL_DBG_QT_NEXT, RPL_DBG_QO_NEXT, RPL_DBG_Y, RPL_DBG_ASTAR, RPL_DBG_H,
-       RPL_DBG_LOSS };
+       RPL_DBG_LOSS, RPL_DBG_TRACE };
 int dqn_debug_export(rpl_dqn *dqn, int what, void *host_out, int64_t bytes);
 
 /* ====================================================================================

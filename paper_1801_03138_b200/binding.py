@@ -26,7 +26,8 @@ RPL_ECUDA, RPL_ENCCL, RPL_ESTATE = -5, -6, -7
 RPL_HOST, RPL_DEVICE = 0, 1
 RPL_ONLINE, RPL_TARGET, RPL_GRAD = 0, 1, 2
 (RPL_DBG_IDX, RPL_DBG_S, RPL_DBG_S_NEXT, RPL_DBG_A, RPL_DBG_R, RPL_DBG_DONE, RPL_DBG_Q,
- RPL_DBG_QT_NEXT, RPL_DBG_QO_NEXT, RPL_DBG_Y, RPL_DBG_ASTAR, RPL_DBG_H, RPL_DBG_LOSS) = range(13)
+ RPL_DBG_QT_NEXT, RPL_DBG_QO_NEXT, RPL_DBG_Y, RPL_DBG_ASTAR, RPL_DBG_H, RPL_DBG_LOSS,
+ RPL_DBG_TRACE) = range(14)
 
 EXPORTS = [
     "replay_create", "replay_destroy", "replay_add", "replay_sample", "replay_gather",
@@ -331,7 +332,8 @@ class DQN:
                 RPL_DBG_QO_NEXT: (np.float32, (batch, A)), RPL_DBG_Y: (np.float32, (batch,)),
                 RPL_DBG_ASTAR: (np.int32, (batch,)),
                 RPL_DBG_H: (np.float32, (batch, hidden_units)),
-                RPL_DBG_LOSS: (np.float32, (1,))}[what]
+                RPL_DBG_LOSS: (np.float32, (1,)),
+                RPL_DBG_TRACE: (np.uint64, (4, 2048, 8))}[what]
         out = np.empty(spec[1], spec[0])
         _ok(_L.dqn_debug_export(self._h, what, out.ctypes.data_as(C.c_void_p), out.nbytes))
         return out

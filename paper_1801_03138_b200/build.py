@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libingpu_replay.so")
 SOURCES = ["replay.cu", "dqn.cu"]
-HEADERS = ["internal.h", "philox.cuh", "simt_gemm.cuh", "train_fast.cuh"]
+HEADERS = ["internal.h", "philox.cuh", "simt_gemm.cuh", "train_fast.cuh", "mma_tf32.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

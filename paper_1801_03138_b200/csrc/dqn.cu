@@ -589,6 +589,7 @@ struct rpl_dqn {
     };
     std::vector<GraphEntry> graphs;
     bool use_graphs = true;
+    unsigned long long *trace = nullptr;   // RPL_TRACE=1: per-CTA timestamps of the fast kernels
     // data parallel
     void *comm = nullptr;
     int rank = 0, world = 1;
@@ -675,11 +676,36 @@ static bool dalloc(rpl_dqn *d, T **p, size_t n)
 }
 
 // ---- fast-path sizing (host) ---------------------------------------------------------------
-static int fast_ut(int N1) { return N1 > 64 ? 128 : (N1 > 32 ? 64 : 32); }
+// layer-1 unit tile of K1: the largest of 128 / 64 / 32 that keeps every tile inside one
+// dueling stream (S % UT == 0); 0 = no valid tile (the generic kernel runs instead)
+static int fast_ut_cfg(const rpl_dqn_config &c, int N1)
+{
+    for (int ut : {128, 64, 32}) {
+        if (c.dueling ? (c.stream % ut == 0) : (ut == 32 || N1 > ut / 2)) return ut;
+    }
+    return 0;
+}
+static int fast_ut(const rpl_dqn *d) { return fast_ut_cfg(d->cfg, d->N[1]); }
+typedef void (*fwd_fn)(FastArgs);
+// K1 instantiation: compile-time dims for the paper's dueling net and configs[0]'s MLP
+static fwd_fn fast_fwd_fn(const rpl_dqn *d)
+{
+    const int ut = fast_ut(d), D = d->cfg.state_dim, N0 = d->N[0], J = d->J;
+    if (ut == 128 && D == 27 && N0 == 128 && J == 9) return fast_fwd_kernel<128, 27, 128, 9>;
+    if (ut == 64 && D == 27 && N0 == 64 && J == 8) return fast_fwd_kernel<64, 27, 64, 8>;
+    if (ut == 128) return fast_fwd_kernel<128, 0, 0, 0>;
+    if (ut == 64) return fast_fwd_kernel<64, 0, 0, 0>;
+    return fast_fwd_kernel<32, 0, 0, 0>;
+}
 static size_t fast_fwd_smem(const rpl_dqn *d, int ut)
 {
     const FwdLayout L(d->cfg.state_dim, d->N[0], ut, d->J);
     return (size_t)L.total * sizeof(float);
+}
+static size_t fast_td_smem(const rpl_dqn *d)
+{
+    const int hs = d->cfg.dueling ? d->cfg.stream : d->N[1];
+    return ((size_t)d->J * hs + d->N[1]) * sizeof(float);
 }
 // split-K count of dH0 = dZ1 W1 so that K3 has about one task per SM
 static int fast_ns(const rpl_dqn *d, int B)
@@ -769,23 +795,42 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
     // fast path: two trunk layers (dueling with one shared layer, or a plain 2-hidden-layer MLP)
     const char *path = getenv("RPL_PATH");
     d->fast = d->T == 2 && d->N[0] % 4 == 0 && d->N[0] <= 256 && D <= 64 && d->J <= F_MAXJ &&
+              d->N[1] % 4 == 0 && (!cfg->dueling || cfg->stream % 4 == 0) && fast_ut_cfg(*cfg, d->N[1]) > 0 &&
               d->woff[1] % 4 == 0 && !(path && strcmp(path, "generic") == 0);
     const char *ng = getenv("RPL_NO_GRAPH");
     d->use_graphs = !(ng && ng[0] == '1');
     ok = ok && dalloc(d, &d->step_dev, 1) && dalloc(d, &d->sync_flag, 1);
+    const char *tr = getenv("RPL_TRACE");
+    if (ok && tr && tr[0] == '1') {
+        ok = dalloc(d, &d->trace, 4 * 2048 * 8);
+        if (ok) cudaMemset(d->trace, 0, 4 * 2048 * 8 * sizeof(unsigned long long));
+    }
     if (ok && d->fast) {
-        const int ut = fast_ut(d->N[1]);
+        const int ut = fast_ut(d);
         const int nut = (d->N[1] + ut - 1) / ut;
         d->part_elems = (int64_t)nets * nut * Bm * d->J;
         d->dh0p_elems = (int64_t)fast_max_ns(d) * Bm * d->N[0];
         ok = dalloc(d, &d->part, d->part_elems) && dalloc(d, &d->dH0p, d->dh0p_elems);
         ok = ok && cudaStreamCreateWithFlags(&d->cap_stream, cudaStreamNonBlocking) == cudaSuccess;
-        ok = ok && cudaFuncSetAttribute(fast_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        fast_fwd_smem(d, 128)) == cudaSuccess;
-        ok = ok && cudaFuncSetAttribute(fast_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        fast_fwd_smem(d, 64)) == cudaSuccess;
-        ok = ok && cudaFuncSetAttribute(fast_fwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        fast_fwd_smem(d, 32)) == cudaSuccess;
+        ok = ok && cudaFuncSetAttribute(fast_fwd_fn(d), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        fast_fwd_smem(d, ut)) == cudaSuccess;
+        ok = ok && cudaFuncSetAttribute(fast_bwd0_sgd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        NT * D * sizeof(float)) == cudaSuccess;
+        ok = ok && cudaFuncSetAttribute(fast_bwd1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        K3_SMEM_FLOATS * sizeof(float)) == cudaSuccess;
+        // one shared-memory carveout for every kernel of the step: no L1/shared
+        // reconfiguration between consecutive kernels
+        if (ok) {
+            const void *fns[] = {(const void *)fast_fwd_fn(d), (const void *)fast_td_kernel,
+                                 (const void *)fast_bwd1_kernel, (const void *)fast_bwd0_sgd_kernel,
+                                 (const void *)insert_kernel_ptr()};
+            for (const void *f : fns)
+                ok = ok && cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                cudaSharedmemCarveoutMaxShared) == cudaSuccess;
+        }
+        ok = ok && fast_td_smem(d) <= 200 * 1024 &&
+             cudaFuncSetAttribute(fast_td_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  fast_td_smem(d)) == cudaSuccess;
     }
     if (!ok) {
         if (!coop) set_error("dqn_create: device %d lacks cooperative launch", d->device);
@@ -922,7 +967,7 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.H0 = d->H[0];
     p.H1 = d->H[1];
     p.part = d->part;
-    p.UT = fast_ut(p.N1);
+    p.UT = fast_ut(d);
     p.nut = (p.N1 + p.UT - 1) / p.UT;
     p.dHead = d->dO;
     p.dZ1 = d->dZlast;
@@ -943,6 +988,7 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.sync_flag = d->sync_flag;
     p.apply_update = apply;
     p.err = d->err;
+    p.trace = d->trace;
 }
 
 // the four fast-path kernels, enqueued on `st`
@@ -950,21 +996,21 @@ static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
 {
     const int nbt = (p.B + F_BT - 1) / F_BT;
     const int k1_tasks = p.nets * nbt * p.nut;
-    const int g1 = std::min(k1_tasks, 2 * d->sms);
+    const int g1 = std::min(k1_tasks, d->sms);
     const size_t sm1 = fast_fwd_smem(d, p.UT);
-    if (p.UT == 128) fast_fwd_kernel<128><<<g1, NT, sm1, st>>>(p);
-    else if (p.UT == 64) fast_fwd_kernel<64><<<g1, NT, sm1, st>>>(p);
-    else fast_fwd_kernel<32><<<g1, NT, sm1, st>>>(p);
+    fast_fwd_fn(d)<<<g1, F_NT1, sm1, st>>>(p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    fast_td_kernel<<<std::min(p.B, 4 * d->sms), NT, 0, st>>>(p);
+    fast_td_kernel<<<std::min(p.B, 4 * d->sms), NT, fast_td_smem(d), st>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const int n_w = ((p.N1 + BM - 1) / BM) * ((p.N0 + BN - 1) / BN) * p.nsb;
     const int n_h = ((p.B + BM - 1) / BM) * ((p.N0 + BN - 1) / BN) * p.NS;
-    const int n_hd = ((p.N1 + NT - 1) / NT + 1) * p.nsb;
-    fast_bwd1_kernel<<<std::min(n_w + n_h + n_hd, 4 * d->sms), NT, 0, st>>>(p);
+    const int hd_passes = p.dueling ? (p.A + 7) / 8 : (p.J + 7) / 8;
+    const int n_hd = (((p.N1 + F_G3 - 1) / F_G3) * hd_passes + 1) * p.nsb;
+    fast_bwd1_kernel<<<std::min(n_w + n_h + n_hd, 4 * d->sms), F_NT3, K3_SMEM_FLOATS * sizeof(float), st>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    fast_bwd0_sgd_kernel<<<std::max(std::min(p.N0, 4 * d->sms), d->sms), NT, 0, st>>>(p);
+    fast_bwd0_sgd_kernel<<<std::max(std::min(p.N0, 4 * d->sms), d->sms), NT,
+                           (size_t)std::min(p.B, NT) * p.D * sizeof(float), st>>>(p);
     return cudaGetLastError();
 }
 
@@ -1141,6 +1187,9 @@ extern "C" int dqn_debug_export(rpl_dqn *d, int what, void *host_out, int64_t by
     case RPL_DBG_ASTAR: src = d->astar; need = B * 4; break;
     case RPL_DBG_LOSS: src = d->grad + d->P; need = 4; break;
     case RPL_DBG_H: need = B * d->Htot * 4; break;
+    case RPL_DBG_TRACE:
+        if (!d->trace) { set_error("dqn_debug_export: tracing is off (set RPL_TRACE=1)"); return RPL_ESTATE; }
+        src = d->trace; need = 4 * 2048 * 8 * 8; break;
     default: set_error("dqn_debug_export: unknown item %d", what); return RPL_EINVAL;
     }
     if (bytes != need) {

@@ -79,4 +79,5 @@ namespace rpl {
 // launch helpers implemented in replay.cu, used by dqn.cu
 int launch_gather(const rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t event,
                   int use_sampler, const rpl_batch *out);
+const void *insert_kernel_ptr();
 }  // namespace rpl

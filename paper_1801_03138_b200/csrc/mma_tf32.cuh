@@ -1,0 +1,49 @@
+// mma_tf32.cuh -- FP32-accurate warp-level tensor-core products for the small 16-row tiles of
+// the fast path: "3xTF32" on mma.sync.m16n8k8 (CUDA path only).
+//
+// x = hi + lo with hi = tf32(x), lo = tf32(x - hi); a.b ~= hi_a hi_b + hi_a lo_b + lo_a hi_b
+// (the dropped lo_a lo_b term is ~2^-22 relative), accumulated in FP32.  Small terms are
+// accumulated first.  The error is at FP32 round-off level, which keeps the 1e-5 normwise
+// parity of the FP32 path (BASELINE north star); tests/test_gpu_train.py checks it.
+//
+// Fragment layouts of m16n8k8.row.col.f32.tf32.tf32.f32 (g = lane / 4, t = lane % 4):
+//   A 16x8 : a0 (g, t)   a1 (g+8, t)   a2 (g, t+4)   a3 (g+8, t+4)
+//   B 8x8  : b0 (k=t, n=g)             b1 (k=t+4, n=g)
+//   C 16x8 : c0 (g, 2t)  c1 (g, 2t+1)  c2 (g+8, 2t)  c3 (g+8, 2t+1)
+#pragma once
+#include <stdint.h>
+
+namespace rpl {
+
+__device__ __forceinline__ uint32_t tf32_rna(float x)
+{
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void tf32_split(float x, uint32_t &hi, uint32_t &lo)
+{
+    hi = tf32_rna(x);
+    lo = tf32_rna(x - __uint_as_float(hi));
+}
+
+__device__ __forceinline__ void mma_tf32(float c[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1)
+{
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// c += A(16x8) B(8x8) with both operands given as hi/lo pairs
+__device__ __forceinline__ void mma_3xtf32(float c[4], const uint32_t ah[4], const uint32_t al[4],
+                                           const uint32_t bh[2], const uint32_t bl[2])
+{
+    mma_tf32(c, al[0], al[1], al[2], al[3], bh[0], bh[1]);
+    mma_tf32(c, ah[0], ah[1], ah[2], ah[3], bl[0], bl[1]);
+    mma_tf32(c, ah[0], ah[1], ah[2], ah[3], bh[0], bh[1]);
+}
+
+}  // namespace rpl

@@ -191,6 +191,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const float *__restrict__ r
     }
 }
 
+const void *insert_kernel_ptr() { return (const void *)insert_kernel; }
+
 int launch_gather(const rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t event,
                   int use_sampler, const rpl_batch *out)
 {

@@ -3,15 +3,15 @@
 // 27 -> 64 -> 64 -> |A| MLP of configs[0]).  Four kernels, captured once per batch size into a
 // CUDA graph:
 //
-//   K1 fwd  : per (net, 16-row batch tile, 128-unit tile): Philox sample + gather the 16 rows,
-//             layer 0 for the tile's rows (recomputed per unit tile: 55 kMAC, cheaper than a
-//             grid-wide exchange), layer-1 units of the tile, and the tile's partial sums of the
-//             V/A heads.  Weight tiles stream into shared memory with cp.async while the gather
-//             is in flight.
+//   K1 fwd  : per (net, 16-row batch tile, unit tile of layer 1): Philox sample + gather the 16
+//             rows, layer 0 for those rows (recomputed per unit tile: 55 kMAC, cheaper than a
+//             grid-wide exchange), the tile's layer-1 units and its partial sums of the V/A
+//             heads.  All weights stream into shared memory with cp.async while the sampled
+//             rows are being gathered from HBM.
 //   K2 td   : per sample: reduce head partials, dueling combine, max / argmax (warp shuffles),
 //             TD target, Huber, dQ, dV/dA, and dZ1 = dHead . W_head (*) ReLU'(z1).
-//   K3 bwd1 : dW1 = dZ1^T H0 and split-K partials of dH0 = dZ1 W1 (32x64 SIMT GEMM tiles),
-//             head-weight gradients.
+//   K3 bwd1 : dW1 = dZ1^T H0 (+ db1) and split-K partials of dH0 = dZ1 W1 as 32x64 FP32 SIMT
+//             GEMM tiles (4x4 register blocking, float4 operand staging), head gradients.
 //   K4 bwd0 : dZ0 = (sum of dH0 partials) (*) ReLU'(z0), dW0 = dZ0^T X, then SGD of every
 //             parameter (non-finite guard), target sync, counters.
 //
@@ -20,11 +20,17 @@
 #pragma once
 #include "philox.cuh"
 #include "simt_gemm.cuh"
+#include "mma_tf32.cuh"
 
 namespace rpl {
 
 constexpr int F_BT = 16;          // batch rows per K1 task
 constexpr int F_MAXJ = 33;        // head outputs (1 + 32 actions)
+constexpr int F_JT = (F_MAXJ + 7) / 8;   // 8-wide MMA n-tiles of the head outputs
+constexpr int F_JP = 8 * F_JT;           // head outputs padded to the n-tiles
+constexpr int F_NT1 = 512;        // threads per K1 CTA
+constexpr int F_NT3 = 256;        // threads per K3 CTA (two 128-thread split-K groups)
+constexpr int F_G3 = 128;         // threads per K3 GEMM group
 
 struct FastArgs {
     // replay (rctrl[0] = sampler events consumed, rctrl[1] = filled size)
@@ -62,6 +68,31 @@ struct FastArgs {
     int32_t *sync_flag;  // written by K2 (step t+1 is a sync step), read by K4 / sgd_kernel
     int apply_update;
     uint32_t *err;
+    unsigned long long *trace;   // optional per-CTA [kernel][cta][start, end] %globaltimer (ns)
+};
+
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// records the CTA's start / end time when tracing is on (RPL_TRACE=1)
+struct CtaTrace {
+    unsigned long long *slot;
+    __device__ CtaTrace(unsigned long long *tr, int kernel)
+        : slot(tr && threadIdx.x == 0 ? tr + 8 * ((size_t)kernel * 2048 + blockIdx.x) : nullptr)
+    {
+        if (slot) slot[0] = gtimer();
+    }
+    __device__ ~CtaTrace()
+    {
+        if (slot) slot[1] = gtimer();
+    }
+    __device__ void mark(int i)
+    {
+        if (slot) slot[i] = gtimer();
+    }
 };
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
@@ -69,50 +100,71 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all()
 {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
+// n floats (n % 4 == 0, both pointers 16-byte aligned) global -> shared, 16-byte cp.async
+__device__ __forceinline__ void cp_async_row(float *dst, const float *src, int n, int tid, int nt)
+{
+    for (int c = tid; c < n / 4; c += nt) cp_async16(dst + 4 * c, src + 4 * c);
+}
 
-// shared-memory layout of K1 (floats); identical formula on the host (fast_fwd_smem_bytes)
+// shared-memory layout of K1 (32-bit words); the same formula sizes the launch on the host
 struct FwdLayout {
-    int DP, SW0, N0P, UT;
-    int oX, oW0, oH0, oW1, oH1, oWh, ob0, ob1, oidx, total;
+    int XP, N0P, UT, UTP;
+    int oW0, oX, oXh, oXl, oH0h, oH0l, oW1, oH1, oWh, ob0, ob1, oidx, ored, total;
     __host__ __device__ FwdLayout(int D, int N0, int UT_, int J)
     {
-        DP = (D + 3) & ~3;
-        SW0 = ((DP + 31) & ~31) + 4;     // row stride == 4 (mod 32): conflict-free LDS.128
-        N0P = ((N0 + 31) & ~31) + 4;
+        (void)J;
+        XP = ((D + 7) & ~7) + 4;         // X row stride: K padded to the MMA k-step, +4 words
+        N0P = ((N0 + 31) & ~31) + 4;     // row stride == 4 (mod 32): conflict-free fragments
         UT = UT_;
-        oX = 0;
-        oW0 = oX + F_BT * DP;
-        oH0 = oW0 + N0 * SW0;
-        oW1 = oH0 + F_BT * N0P;
-        oH1 = oW1 + UT * N0P;
-        oWh = oH1 + F_BT * (UT + 1);
-        ob0 = oWh + J * (UT + 1);
-        ob1 = ob0 + N0;
-        oidx = ob1 + UT;
-        total = oidx + F_BT;
+        UTP = UT + 4;
+        oW0 = 0;                         // W0 flat [N0 * D], 16-byte aligned
+        oX = (N0 * D + 3) & ~3;          // [BT][XP] fp32 gathered states
+        oXh = oX + F_BT * XP;            // [BT][XP] tf32 hi
+        oXl = oXh + F_BT * XP;           // [BT][XP] tf32 lo
+        oH0h = oXl + F_BT * XP;          // [BT][N0P] tf32 hi of H0
+        oH0l = oH0h + F_BT * N0P;        // [BT][N0P] tf32 lo of H0
+        oW1 = oH0l + F_BT * N0P;         // [UT][N0P] fp32 layer-1 weight tile
+        oH1 = oW1 + UT * N0P;            // [BT][UTP] fp32 H1 tile
+        oWh = oH1 + F_BT * UTP;          // [F_JP][UTP] fp32 head-weight tile (rows >= J zero)
+        ob0 = oWh + F_JP * UTP;          // [N0]
+        ob1 = ob0 + ((N0 + 3) & ~3);     // [UT]
+        oidx = ob1 + UT;                 // [BT]
+        ored = oidx + F_BT;              // [16 warps][16][F_JP] head partials
+        total = ored + 16 * 16 * F_JP;
     }
 };
 
 // ------------------------------------------------------------------------------------------
-// K1
+// K1.  512 threads = 16 warps; layer 0, layer 1 and the head partials are 16-row
+// tensor-core products (3xTF32 mma.sync.m16n8k8, FP32-accurate): warp w owns n-tiles
+// w, w+16, ... of 8 output units.  Compile-time dims (KD, KN0, KJ) for the paper's /
+// configs[0] nets; 0 = read at run time.
 // ------------------------------------------------------------------------------------------
-template <int UT>
-__global__ void __launch_bounds__(NT, 2) fast_fwd_kernel(const __grid_constant__ FastArgs p)
+template <int UT, int KD, int KN0, int KJ>
+__global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constant__ FastArgs p)
 {
+    CtaTrace trace_(p.trace, 0);
     extern __shared__ float4 smem4[];
     float *sm = reinterpret_cast<float *>(smem4);
-    constexpr int RPT = F_BT * UT / NT;   // rows per thread in layer 1
-    static_assert(RPT >= 1 && F_BT * UT == RPT * NT, "tile shape");
-    const int D = p.D, N0 = p.N0, N1 = p.N1, J = p.J, B = p.B;
+    constexpr int NW = F_NT1 / 32;
+    const int D = KD ? KD : p.D, N0 = KN0 ? KN0 : p.N0, J = KJ ? KJ : p.J;
+    const int N1 = p.N1, B = p.B;
     const FwdLayout L(D, N0, UT, J);
-    float *Xs = sm + L.oX, *W0s = sm + L.oW0, *H0s = sm + L.oH0, *W1s = sm + L.oW1;
-    float *H1s = sm + L.oH1, *Whs = sm + L.oWh, *b0s = sm + L.ob0, *b1s = sm + L.ob1;
+    float *W0f = sm + L.oW0, *Xs = sm + L.oX, *W1s = sm + L.oW1;
+    uint32_t *Xh = reinterpret_cast<uint32_t *>(sm + L.oXh), *Xl = reinterpret_cast<uint32_t *>(sm + L.oXl);
+    uint32_t *H0h = reinterpret_cast<uint32_t *>(sm + L.oH0h), *H0l = reinterpret_cast<uint32_t *>(sm + L.oH0l);
+    float *H1s = sm + L.oH1, *Whs = sm + L.oWh, *b0s = sm + L.ob0, *b1s = sm + L.ob1, *red = sm + L.ored;
     int *idxs = reinterpret_cast<int *>(sm + L.oidx);
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
     const int nbt = (B + F_BT - 1) / F_BT, nut = p.nut;
     const uint64_t event = p.rctrl[0];
     const uint64_t size = p.rctrl[1];
@@ -121,18 +173,38 @@ __global__ void __launch_bounds__(NT, 2) fast_fwd_kernel(const __grid_constant__
         const int net = task / (nbt * nut), rem = task % (nbt * nut);
         const int bt = rem / nut, ut = rem % nut;
         const int rb = bt * F_BT, u0 = ut * UT;
+        const int nu = min(UT, N1 - u0);   // valid units in this tile (multiple of 4)
         const float *theta = net == 1 ? p.target : p.online;
         __syncthreads();   // the previous task is done with shared memory
-        // (1) stream the layer-1 weight tile into shared memory (rows stride N0P)
+        // (1) weights -> shared memory, all 16-byte cp.async (no load waits on another)
         {
             const int c4 = N0 / 4;
-            for (int e = tid; e < UT * c4; e += NT) {
-                const int u = e / c4, c = e % c4;
+            for (int e = tid; e < UT * c4; e += F_NT1) {
+                const int u = e / c4, c = e - u * c4;
                 float *dst = W1s + u * L.N0P + 4 * c;
-                if (u0 + u < N1)
-                    cp_async16(dst, theta + p.w1 + (int64_t)(u0 + u) * N0 + 4 * c);
-                else
-                    *reinterpret_cast<float4 *>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (u < nu) cp_async16(dst, theta + p.w1 + (int64_t)(u0 + u) * N0 + 4 * c);
+                else *reinterpret_cast<float4 *>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        cp_async_row(W0f, theta + p.w0, N0 * D, tid, F_NT1);
+        cp_async_row(b0s, theta + p.b0, N0, tid, F_NT1);
+        cp_async_row(b1s, theta + p.b1 + u0, nu, tid, F_NT1);
+        for (int u = nu + tid; u < UT; u += F_NT1) b1s[u] = 0.0f;
+        {
+            // head weights of the tile's units: dueling V row (j = 0) over V units, A rows
+            // (j >= 1) over A units (a tile never straddles the streams: S % UT == 0)
+            const bool vtile = p.dueling && u0 < p.S;
+            for (int e = tid; e < F_JP * (UT / 4); e += F_NT1) {
+                const int j = e / (UT / 4), c = e - j * (UT / 4);
+                float *dst = Whs + j * L.UTP + 4 * c;
+                const float *src = nullptr;
+                if (j < J && 4 * c < nu) {
+                    if (!p.dueling) src = theta + p.wh + (int64_t)j * N1 + u0 + 4 * c;
+                    else if (vtile && j == 0) src = theta + p.wh + u0 + 4 * c;
+                    else if (!vtile && j > 0) src = theta + p.wh + (int64_t)j * p.S + (u0 - p.S) + 4 * c;
+                }
+                if (src) cp_async16(dst, src);
+                else *reinterpret_cast<float4 *>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
         // (2) Philox sample of the tile's rows (Q3)
@@ -142,101 +214,147 @@ __global__ void __launch_bounds__(NT, 2) fast_fwd_kernel(const __grid_constant__
             idxs[2 * tid] = i0;
             idxs[2 * tid + 1] = i1;
         }
-        // (3) layer-0 weights (transposed copy, zero-padded), biases, head-weight tile
-        for (int e = tid; e < N0 * L.DP; e += NT) {
-            const int n = e / L.DP, d = e % L.DP;
-            W0s[n * L.SW0 + d] = d < D ? __ldg(theta + p.w0 + (int64_t)n * D + d) : 0.0f;
-        }
-        for (int n = tid; n < N0; n += NT) b0s[n] = __ldg(theta + p.b0 + n);
-        for (int u = tid; u < UT; u += NT) b1s[u] = (u0 + u < N1) ? __ldg(theta + p.b1 + u0 + u) : 0.0f;
-        for (int e = tid; e < J * UT; e += NT) {
-            const int j = e / UT, u = e % UT, g = u0 + u;
-            float w = 0.0f;
-            if (g < N1) {
-                if (!p.dueling) w = __ldg(theta + p.wh + (int64_t)j * N1 + g);
-                else if (j == 0 && g < p.S) w = __ldg(theta + p.wh + g);
-                else if (j > 0 && g >= p.S) w = __ldg(theta + p.wh + (int64_t)j * p.S + (g - p.S));
-            }
-            Whs[j * (UT + 1) + u] = w;
-        }
         __syncthreads();
-        // (4) gather the 16 sampled rows: s for online(s), s' for target(s') / online(s')
+        // (3) gather the 16 sampled rows: s for online(s), s' for target(s') / online(s')
         const int col0 = net == 0 ? 0 : D;
-        for (int e = tid; e < F_BT * L.DP; e += NT) {
-            const int rr = e / L.DP, d = e % L.DP;
-            Xs[rr * L.DP + d] = d < D ? __ldg(p.ring + (int64_t)idxs[rr] * p.rs + col0 + d) : 0.0f;
+        for (int e = tid; e < F_BT * D; e += F_NT1) {
+            const int rr = e / D, d = e - rr * D;
+            cp_async4(Xs + rr * L.XP + d, p.ring + (int64_t)idxs[rr] * p.rs + col0 + d);
         }
-        if (ut == 0 && net <= 1) {
-            // unpack the batch once for the backward pass and the debug export
-            for (int e = tid; e < F_BT * D; e += NT) {
-                const int rr = e / D, d = e % D;
-                if (rb + rr < B)
-                    (net == 0 ? p.Xs : p.Xs2)[(int64_t)(rb + rr) * D + d] =
-                        __ldg(p.ring + (int64_t)idxs[rr] * p.rs + col0 + d);
-            }
-            if (net == 0 && tid < F_BT && rb + tid < B) {
-                const float *row = p.ring + (int64_t)idxs[tid] * p.rs + 2 * D;
-                p.idx[rb + tid] = idxs[tid];
-                p.a[rb + tid] = __float_as_int(__ldg(row));
-                p.r[rb + tid] = __ldg(row + 1);
-                p.done[rb + tid] = (uint8_t)(__float_as_uint(__ldg(row + 2)) != 0u);
-            }
+        int32_t ra_ = 0;
+        float rr_ = 0.0f;
+        uint32_t rd_ = 0;
+        const bool unpack_scalars = net == 0 && ut == 0 && tid < F_BT && rb + tid < B;
+        if (unpack_scalars) {
+            const float *row = p.ring + (int64_t)idxs[tid] * p.rs + 2 * D;
+            ra_ = __float_as_int(__ldg(row));
+            rr_ = __ldg(row + 1);
+            rd_ = __float_as_uint(__ldg(row + 2));
         }
-        __syncthreads();
-        // (5) layer 0 for the tile's rows: H0 = ReLU(X W0^T + b0)
-        for (int o = tid; o < F_BT * N0; o += NT) {
-            const int rr = o / N0, n = o % N0;
-            const float4 *x4 = reinterpret_cast<const float4 *>(Xs + rr * L.DP);
-            const float4 *w4 = reinterpret_cast<const float4 *>(W0s + n * L.SW0);
-            float acc = b0s[n];
-            for (int q = 0; q < L.DP / 4; ++q) {
-                const float4 x = x4[q], w = w4[q];
-                acc = fmaf(x.x, w.x, acc);
-                acc = fmaf(x.y, w.y, acc);
-                acc = fmaf(x.z, w.z, acc);
-                acc = fmaf(x.w, w.w, acc);
-            }
-            const float h = acc > 0.0f ? acc : 0.0f;
-            H0s[rr * L.N0P + n] = h;
-            if (net == 0 && ut == 0 && rb + rr < B) p.H0[(int64_t)(rb + rr) * N0 + n] = h;
-        }
+        trace_.mark(2);
         cp_async_wait_all();
         __syncthreads();
-        // (6) layer 1: thread (u, row group): RPT rows x 1 unit, float4 over k
-        {
-            const int u = tid % UT, r0 = (tid / UT) * RPT;
-            float acc[RPT];
-#pragma unroll
-            for (int i = 0; i < RPT; ++i) acc[i] = b1s[u];
-            const float4 *w4 = reinterpret_cast<const float4 *>(W1s + u * L.N0P);
-            for (int q = 0; q < N0 / 4; ++q) {
-                const float4 w = w4[q];
-#pragma unroll
-                for (int i = 0; i < RPT; ++i) {
-                    const float4 h = reinterpret_cast<const float4 *>(H0s + (r0 + i) * L.N0P)[q];
-                    acc[i] = fmaf(h.x, w.x, acc[i]);
-                    acc[i] = fmaf(h.y, w.y, acc[i]);
-                    acc[i] = fmaf(h.z, w.z, acc[i]);
-                    acc[i] = fmaf(h.w, w.w, acc[i]);
-                }
+        trace_.mark(3);
+        // split X into tf32 hi / lo (zero beyond D); unpack the batch once for the backward
+        // pass and the debug export
+        for (int e = tid; e < F_BT * L.XP; e += F_NT1) {
+            const int rr = e / L.XP, d = e - rr * L.XP;
+            const float x = d < D ? Xs[e] : 0.0f;
+            uint32_t hi, lo;
+            tf32_split(x, hi, lo);
+            Xh[e] = hi;
+            Xl[e] = lo;
+            if (ut == 0 && net <= 1 && d < D && rb + rr < B)
+                (net == 0 ? p.Xs : p.Xs2)[(int64_t)(rb + rr) * D + d] = x;
+        }
+        if (unpack_scalars) {
+            p.idx[rb + tid] = idxs[tid];
+            p.a[rb + tid] = ra_;
+            p.r[rb + tid] = rr_;
+            p.done[rb + tid] = (uint8_t)(rd_ != 0u);
+        }
+        __syncthreads();
+        // (4) layer 0: H0[16][N0] = ReLU(X W0^T + b0)
+        for (int nt = warp; nt < N0 / 8; nt += NW) {
+            const int n = nt * 8 + g;
+            float c[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int k0 = 0; k0 < D; k0 += 8) {
+                uint32_t ah[4], al[4], bh[2], bl[2];
+                ah[0] = Xh[g * L.XP + k0 + t];       al[0] = Xl[g * L.XP + k0 + t];
+                ah[1] = Xh[(g + 8) * L.XP + k0 + t]; al[1] = Xl[(g + 8) * L.XP + k0 + t];
+                ah[2] = Xh[g * L.XP + k0 + t + 4];   al[2] = Xl[g * L.XP + k0 + t + 4];
+                ah[3] = Xh[(g + 8) * L.XP + k0 + t + 4]; al[3] = Xl[(g + 8) * L.XP + k0 + t + 4];
+                const float w0 = k0 + t < D ? W0f[n * D + k0 + t] : 0.0f;
+                const float w1 = k0 + t + 4 < D ? W0f[n * D + k0 + t + 4] : 0.0f;
+                tf32_split(w0, bh[0], bl[0]);
+                tf32_split(w1, bh[1], bl[1]);
+                mma_3xtf32(c, ah, al, bh, bl);
             }
+            const int col = nt * 8 + 2 * t;
 #pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-                const float h = acc[i] > 0.0f ? acc[i] : 0.0f;
-                H1s[(r0 + i) * (UT + 1) + u] = h;
-                if (net == 0 && rb + r0 + i < B && u0 + u < N1)
-                    p.H1[(int64_t)(rb + r0 + i) * N1 + u0 + u] = h;
+            for (int q = 0; q < 4; ++q) {
+                const int rr = g + (q >> 1) * 8, cc = col + (q & 1);
+                float h = c[q] + b0s[cc];
+                h = h > 0.0f ? h : 0.0f;
+                uint32_t hi, lo;
+                tf32_split(h, hi, lo);
+                H0h[rr * L.N0P + cc] = hi;
+                H0l[rr * L.N0P + cc] = lo;
+                if (net == 0 && ut == 0 && rb + rr < B) p.H0[(int64_t)(rb + rr) * N0 + cc] = h;
             }
         }
         __syncthreads();
-        // (7) this tile's partial sums of the head outputs
-        for (int o = tid; o < F_BT * J; o += NT) {
-            const int rr = o / J, j = o % J;
-            const float *h = H1s + rr * (UT + 1);
-            const float *w = Whs + j * (UT + 1);
-            float acc = 0.0f;
-            for (int u = 0; u < UT; ++u) acc = fmaf(w[u], h[u], acc);
-            if (rb + rr < B) p.part[(((int64_t)net * nut + ut) * B + rb + rr) * J + j] = acc;
+        trace_.mark(4);
+        // (5) layer 1: H1[16][UT] = ReLU(H0 W1_tile^T + b1)
+        for (int nt = warp; nt < UT / 8; nt += NW) {
+            const float *wrow = W1s + (nt * 8 + g) * L.N0P;
+            float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+            for (int k0 = 0; k0 < N0; k0 += 8) {
+                uint32_t ah[4], al[4], bh[2], bl[2];
+                ah[0] = H0h[g * L.N0P + k0 + t];       al[0] = H0l[g * L.N0P + k0 + t];
+                ah[1] = H0h[(g + 8) * L.N0P + k0 + t]; al[1] = H0l[(g + 8) * L.N0P + k0 + t];
+                ah[2] = H0h[g * L.N0P + k0 + t + 4];   al[2] = H0l[g * L.N0P + k0 + t + 4];
+                ah[3] = H0h[(g + 8) * L.N0P + k0 + t + 4]; al[3] = H0l[(g + 8) * L.N0P + k0 + t + 4];
+                tf32_split(wrow[k0 + t], bh[0], bl[0]);
+                tf32_split(wrow[k0 + t + 4], bh[1], bl[1]);
+                mma_3xtf32(c, ah, al, bh, bl);
+            }
+            const int col = nt * 8 + 2 * t;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int rr = g + (q >> 1) * 8, cc = col + (q & 1);
+                float h = c[q] + b1s[cc];
+                h = h > 0.0f ? h : 0.0f;
+                H1s[rr * L.UTP + cc] = h;
+                if (net == 0 && rb + rr < B && cc < nu) p.H1[(int64_t)(rb + rr) * N1 + u0 + cc] = h;
+            }
+        }
+        __syncthreads();
+        trace_.mark(5);
+        // (6) head partials [16 rows][JP = 8 * ceil(J / 8)]: warp w takes k-steps w, w+16, ...
+        //     of the tile's units; the per-warp products are reduced in a fixed order
+        {
+            const int JT = (J + 7) / 8;
+            float c[F_JT][4];
+#pragma unroll
+            for (int jt = 0; jt < F_JT; ++jt)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) c[jt][q] = 0.0f;
+            for (int k0 = warp * 8; k0 < UT; k0 += NW * 8) {
+                uint32_t ah[4], al[4], bh[2], bl[2];
+                tf32_split(H1s[g * L.UTP + k0 + t], ah[0], al[0]);
+                tf32_split(H1s[(g + 8) * L.UTP + k0 + t], ah[1], al[1]);
+                tf32_split(H1s[g * L.UTP + k0 + t + 4], ah[2], al[2]);
+                tf32_split(H1s[(g + 8) * L.UTP + k0 + t + 4], ah[3], al[3]);
+#pragma unroll
+                for (int jt = 0; jt < F_JT; ++jt) {
+                    if (jt < JT) {
+                        tf32_split(Whs[(8 * jt + g) * L.UTP + k0 + t], bh[0], bl[0]);
+                        tf32_split(Whs[(8 * jt + g) * L.UTP + k0 + t + 4], bh[1], bl[1]);
+                        mma_3xtf32(c[jt], ah, al, bh, bl);
+                    }
+                }
+            }
+            float *rw = red + warp * (16 * F_JP);
+#pragma unroll
+            for (int jt = 0; jt < F_JT; ++jt) {
+                if (jt < JT) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int rr = g + (q >> 1) * 8, cc = 8 * jt + 2 * t + (q & 1);
+                        rw[rr * F_JP + cc] = c[jt][q];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        for (int o = tid; o < F_BT * J; o += F_NT1) {
+            const int rr = o / J, j = o - rr * J;
+            float v = 0.0f;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) v += red[w * (16 * F_JP) + rr * F_JP + j];
+            if (rb + rr < B) p.part[(((int64_t)net * nut + ut) * B + rb + rr) * J + j] = v;
         }
     }
 }
@@ -253,26 +371,50 @@ __device__ __forceinline__ float f_huber(float d, float kappa, int kinf)
 
 __global__ void __launch_bounds__(NT) fast_td_kernel(const __grid_constant__ FastArgs p)
 {
+    CtaTrace trace_(p.trace, 1);
+    extern __shared__ float4 smem4[];
+    const int A = p.A, J = p.J, B = p.B, N1 = p.N1, S = p.S;
+    const int HS = p.dueling ? S : N1;
+    float *Whs = reinterpret_cast<float *>(smem4);      // the online head weights (J x HS)
+    float *h1s = Whs + J * HS;                          // this sample's H1 row
     __shared__ float hs[3][F_MAXJ + 1];
     __shared__ float dhs[F_MAXJ + 1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int A = p.A, J = p.J, B = p.B, N1 = p.N1, S = p.S;
     if (blockIdx.x == 0 && tid == 0) {
         const int64_t t = *p.step_dev + 1;
         *p.sync_flag = (p.sync_period > 0 && t % p.sync_period == 0) ? 1 : 0;
     }
+    // the head weights are reused for every sample of this CTA: stream them in once
+    cp_async_row(Whs, p.online + p.wh, J * HS, tid, NT);
     for (int b = blockIdx.x; b < B; b += gridDim.x) {
         __syncthreads();
+        cp_async_row(h1s, p.H1 + (int64_t)b * N1, N1, tid, NT);
+        // the sample's action / reward / terminal, needed after the reduction (prefetched)
+        int ab = 0;
+        float rb = 0.0f;
+        uint8_t db = 0;
+        if (warp == 0) {
+            ab = p.a[b];
+            rb = p.r[b];
+            db = p.done[b];
+        }
         if (warp < p.nets) {
             const float *theta = warp == 1 ? p.target : p.online;
             for (int j = lane; j < J; j += 32) {
+                const float *src = p.part + ((int64_t)warp * p.nut * B + b) * J + j;
+                const int64_t stride = (int64_t)B * J;
+                float pv[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) pv[q] = q < p.nut ? __ldcg(src + q * stride) : 0.0f;
                 float v = __ldg(theta + p.bh + j);
-                for (int ut = 0; ut < p.nut; ++ut)
-                    v += __ldcg(p.part + (((int64_t)warp * p.nut + ut) * B + b) * J + j);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v += pv[q];
+                for (int q = 8; q < p.nut; ++q) v += __ldcg(src + q * stride);
                 hs[warp][j] = v;
             }
         }
         __syncthreads();
+        trace_.mark(2);
         if (warp == 0) {
             float q[3];
 #pragma unroll
@@ -311,15 +453,15 @@ __global__ void __launch_bounds__(NT) fast_td_kernel(const __grid_constant__ Fas
                 astar = ix;
                 boot = __shfl_sync(0xffffffffu, q[1], astar);
             }
-            const int ab = p.a[b];
-            const float notdone = p.done[b] ? 0.0f : 1.0f;
-            const float yb = p.r[b] + p.gamma * notdone * boot;
+            const float notdone = db ? 0.0f : 1.0f;
+            const float yb = rb + p.gamma * notdone * boot;
             const float qsel = __shfl_sync(0xffffffffu, q[0], ab);   // Q[i*A + a_i]
             const float delta = qsel - yb;
             const float g = (p.kinf ? delta : fminf(fmaxf(delta, -p.kappa), p.kappa)) / (float)B;
             if (p.dueling) {
-                if (lane == 0) dhs[0] = g;
+                // dV = sum_a dQ_a = g ; dA_a = dQ_a - (1/|A|) sum_a' dQ_a'
                 if (lane < A) dhs[1 + lane] = (lane == ab ? g : 0.0f) - g / (float)A;
+                if (lane == 0) dhs[0] = g;
             } else if (lane < A) {
                 dhs[lane] = lane == ab ? g : 0.0f;
             }
@@ -334,22 +476,188 @@ __global__ void __launch_bounds__(NT) fast_td_kernel(const __grid_constant__ Fas
                 if (p.ddqn) p.astar[b] = astar;
             }
         }
+        trace_.mark(3);
+        cp_async_wait_all();
         __syncthreads();
+        trace_.mark(4);
         for (int j = tid; j < J; j += NT) p.dHead[(int64_t)b * J + j] = dhs[j];
         // dZ1[b][u] = (dHead . W_head)[u] * ReLU'(z1[b][u])
-        const float *Wh = p.online + p.wh;
         for (int u = tid; u < N1; u += NT) {
             float dh = 0.0f;
             if (p.dueling) {
                 if (u < S) {
-                    dh = dhs[0] * __ldg(Wh + u);
+                    dh = dhs[0] * Whs[u];
                 } else {
-                    for (int k = 0; k < A; ++k) dh = fmaf(dhs[1 + k], __ldg(Wh + (int64_t)(1 + k) * S + (u - S)), dh);
+                    for (int k = 0; k < A; ++k) dh = fmaf(dhs[1 + k], Whs[(1 + k) * S + (u - S)], dh);
                 }
             } else {
-                for (int k = 0; k < A; ++k) dh = fmaf(dhs[k], __ldg(Wh + (int64_t)k * N1 + u), dh);
+                for (int k = 0; k < A; ++k) dh = fmaf(dhs[k], Whs[k * N1 + u], dh);
             }
-            p.dZ1[(int64_t)b * N1 + u] = __ldcg(p.H1 + (int64_t)b * N1 + u) > 0.0f ? dh : 0.0f;
+            p.dZ1[(int64_t)b * N1 + u] = h1s[u] > 0.0f ? dh : 0.0f;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K3 GEMM tile: C[32 x 64] = sum_{kk in [kb, ke)} A(m, kk) B(n, kk), 128 threads, 4x4 outputs
+// per thread, operands staged through registers (next chunk in flight while the current one
+// is multiplied).  Operand element (r, kk) is p[kk * ld + r] (kRc: contiguous along r) or
+// p[r * ld + kk]; interior, aligned tiles move as float4, edge tiles element by element.
+// ------------------------------------------------------------------------------------------
+struct Opnd {
+    const float *p;
+    int ld, R;
+};
+
+struct __align__(16) Gemm3Smem {
+    float As[BK][BM + 4];
+    float Bs[BK][BN + 4];
+};
+
+template <bool kRc, int TR>
+__device__ __forceinline__ void g3_fetch(const Opnd &o, int r0, int k0, int kb, int ke,
+                                         float4 *reg, int tid)
+{
+    constexpr int NV = TR * BK / 4 / F_G3;   // float4 per thread
+    const bool interior = (r0 + TR <= o.R) && (k0 >= kb) && (k0 + BK <= ke);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int e = i * F_G3 + tid;
+        if (kRc) {
+            const int kk = e / (TR / 4), r4 = e % (TR / 4);
+            const int r = r0 + 4 * r4, k = k0 + kk;
+            if (interior) {
+                reg[i] = __ldcg(reinterpret_cast<const float4 *>(o.p + (int64_t)k * o.ld + r));
+            } else {
+                float v[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    v[c] = (r + c < o.R && k >= kb && k < ke) ? __ldcg(o.p + (int64_t)k * o.ld + r + c) : 0.0f;
+                reg[i] = make_float4(v[0], v[1], v[2], v[3]);
+            }
+        } else {
+            const int r = e / (BK / 4), k4 = e % (BK / 4);
+            const int rr = r0 + r, k = k0 + 4 * k4;
+            if (interior) {
+                reg[i] = __ldcg(reinterpret_cast<const float4 *>(o.p + (int64_t)rr * o.ld + k));
+            } else {
+                float v[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    v[c] = (rr < o.R && k + c >= kb && k + c < ke) ? __ldcg(o.p + (int64_t)rr * o.ld + k + c) : 0.0f;
+                reg[i] = make_float4(v[0], v[1], v[2], v[3]);
+            }
+        }
+    }
+}
+
+template <bool kRc, int TR, int LDS>
+__device__ __forceinline__ void g3_stash(float (*S)[LDS], const float4 *reg, int tid)
+{
+    constexpr int NV = TR * BK / 4 / F_G3;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int e = i * F_G3 + tid;
+        if (kRc) {
+            const int kk = e / (TR / 4), r4 = e % (TR / 4);
+            *reinterpret_cast<float4 *>(&S[kk][4 * r4]) = reg[i];
+        } else {
+            const int r = e / (BK / 4), k4 = e % (BK / 4);
+            S[4 * k4 + 0][r] = reg[i].x;
+            S[4 * k4 + 1][r] = reg[i].y;
+            S[4 * k4 + 2][r] = reg[i].z;
+            S[4 * k4 + 3][r] = reg[i].w;
+        }
+    }
+}
+
+__device__ __forceinline__ void group_bar(int id)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(F_G3) : "memory");
+}
+
+// Two 128-thread groups split the contraction chunk-wise (group g takes chunks c = g mod 2),
+// each with its own staging buffers and named barrier; group 1 hands its partial tile to
+// group 0 through shared memory and group 0 runs the epilogue (fixed order: deterministic).
+template <bool kARc, bool kBRc, class EPI, class RSUM>
+__device__ __forceinline__ void gemm3_tile(const Opnd &a, const Opnd &b, int m0, int n0, int kb,
+                                           int ke, const EPI &epi, bool want_rowsum,
+                                           const RSUM &rs, Gemm3Smem *smg)
+{
+    const int grp = threadIdx.x / F_G3, tid = threadIdx.x % F_G3;
+    const int tn = tid & 15, tm = tid >> 4;
+    Gemm3Smem &sm = smg[grp];
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    float rsum[4] = {0.f, 0.f, 0.f, 0.f};
+    constexpr int NA = BM * BK / 4 / F_G3, NB = BN * BK / 4 / F_G3;
+    float4 ra[NA], rb[NB];
+    const int nchunks = (ke - kb + BK - 1) / BK;
+    const int mine = (nchunks - grp + 1) / 2;   // chunks grp, grp + 2, ...
+    __syncthreads();                             // the previous task is done with smem
+    if (mine > 0) {
+        g3_fetch<kARc, BM>(a, m0, kb + grp * BK, kb, ke, ra, tid);
+        g3_fetch<kBRc, BN>(b, n0, kb + grp * BK, kb, ke, rb, tid);
+        g3_stash<kARc, BM>(sm.As, ra, tid);
+        g3_stash<kBRc, BN>(sm.Bs, rb, tid);
+        group_bar(1 + grp);
+        for (int c = 0; c < mine; ++c) {
+            const int knext = kb + (grp + 2 * (c + 1)) * BK;
+            if (c + 1 < mine) {
+                g3_fetch<kARc, BM>(a, m0, knext, kb, ke, ra, tid);
+                g3_fetch<kBRc, BN>(b, n0, knext, kb, ke, rb, tid);
+            }
+#pragma unroll 8
+            for (int k = 0; k < BK; ++k) {
+                const float4 av = *reinterpret_cast<const float4 *>(&sm.As[k][4 * tm]);
+                const float4 bv = *reinterpret_cast<const float4 *>(&sm.Bs[k][4 * tn]);
+                const float ar[4] = {av.x, av.y, av.z, av.w};
+                const float br[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ar[i], br[j], acc[i][j]);
+            }
+            if (want_rowsum && tn == 0) {
+                for (int k = 0; k < BK; ++k) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) rsum[i] += sm.As[k][4 * tm + i];
+                }
+            }
+            group_bar(1 + grp);
+            if (c + 1 < mine) {
+                g3_stash<kARc, BM>(sm.As, ra, tid);
+                g3_stash<kBRc, BN>(sm.Bs, rb, tid);
+                group_bar(1 + grp);
+            }
+        }
+    }
+    // hand group 1's partial tile to group 0
+    float *xch = &smg[1].As[0][0];   // 16 floats x 128 threads + 4 rowsums x 16
+    __syncthreads();
+    if (grp == 1) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) xch[(i * 4 + j) * F_G3 + tid] = acc[i][j];
+        if (want_rowsum && tn == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) xch[16 * F_G3 + i * 8 + tm] = rsum[i];
+        }
+    }
+    __syncthreads();
+    if (grp == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                epi(m0 + 4 * tm + i, n0 + 4 * tn + j, acc[i][j] + xch[(i * 4 + j) * F_G3 + tid]);
+        if (want_rowsum && tn == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) rs(m0 + 4 * tm + i, rsum[i] + xch[16 * F_G3 + i * 8 + tm]);
         }
     }
 }
@@ -357,90 +665,125 @@ __global__ void __launch_bounds__(NT) fast_td_kernel(const __grid_constant__ Fas
 // ------------------------------------------------------------------------------------------
 // K3: dW1 / db1 tiles, dH0 split-K tiles, head-weight gradients
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) fast_bwd1_kernel(const __grid_constant__ FastArgs p)
+constexpr int K3_HD_FLOATS = 128 * F_G3 + 128 * F_MAXJ;   // head-gradient staging
+constexpr int K3_SMEM_FLOATS = (int)(2 * sizeof(Gemm3Smem) / 4) > K3_HD_FLOATS ? (int)(2 * sizeof(Gemm3Smem) / 4)
+                                                                             : K3_HD_FLOATS;
+
+__global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant__ FastArgs p)
 {
-    __shared__ GemmSmem sm;
-    __shared__ float dhs[128 * F_MAXJ];
+    CtaTrace trace_(p.trace, 2);
+    extern __shared__ float4 smem4[];
+    float *k3raw = reinterpret_cast<float *>(smem4);   // K3_SMEM_FLOATS
+    Gemm3Smem *sm = reinterpret_cast<Gemm3Smem *>(k3raw);   // one staging area per group
     const int N0 = p.N0, N1 = p.N1, B = p.B, J = p.J;
     const int wmt = (N1 + BM - 1) / BM, wnt = (N0 + BN - 1) / BN;
     const int n_w = wmt * wnt * p.nsb;
     const int hmt = (B + BM - 1) / BM, hnt = (N0 + BN - 1) / BN;
     const int n_h = hmt * hnt * p.NS;
-    const int hu_tasks = (N1 + NT - 1) / NT;
-    const int n_hd = (hu_tasks + 1) * p.nsb;
+    // head-weight gradient tasks: (128-unit tile) x (pass of <= 8 head rows), + 1 bias task
+    const int hd_passes = p.dueling ? (p.A + 7) / 8 : (J + 7) / 8;
+    const int hd_tasks = ((N1 + F_G3 - 1) / F_G3) * hd_passes;
+    const int n_hd = (hd_tasks + 1) * p.nsb;
     const int ntasks = n_w + n_h + n_hd;
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
         if (t < n_w) {
+            // dW1[u][k] = sum_b dZ1[b][u] H0[b][k]  (+ db1[u] = sum_b dZ1[b][u])
             const int s = t / (wmt * wnt), rem = t % (wmt * wnt);
             const int m0 = (rem / wnt) * BM, n0 = (rem % wnt) * BN;
             const int kb = s * p.bsplit, ke = min(B, kb + p.bsplit);
             float *gp = p.gpart + (int64_t)s * p.P;
-            LdRMajor la{p.dZ1, N1, N1, kb, ke};
-            LdRMajor lb{p.H0, N0, N0, kb, ke};
+            const Opnd a{p.dZ1, N1, N1}, bo{p.H0, N0, N0};
             auto epi = [&](int m, int n, float v) {
                 if (m < N1 && n < N0) gp[p.w1 + (int64_t)m * N0 + n] = v;
             };
             auto rs = [&](int m, float v) {
                 if (m < N1) gp[p.b1 + m] = v;
             };
-            gemm_tile(la, lb, m0, n0, kb, ke, epi, n0 == 0, rs, sm);
+            gemm3_tile<true, true>(a, bo, m0, n0, kb, ke, epi, n0 == 0, rs, sm);
+            trace_.mark(4);
         } else if (t < n_w + n_h) {
+            // dH0 partial [s][b][k] = sum_{u in split s} dZ1[b][u] W1[u][k]
             const int u = t - n_w;
             const int s = u / (hmt * hnt), rem = u % (hmt * hnt);
             const int m0 = (rem / hnt) * BM, n0 = (rem % hnt) * BN;
             const int chunk = (N1 + p.NS - 1) / p.NS;
             const int kb = s * chunk, ke = min(N1, kb + chunk);
             float *out = p.dH0p + (int64_t)s * B * N0;
-            LdKMajor la{p.dZ1, N1, B, ke};
-            LdRMajor lb{p.online + p.w1, N0, N0, kb, ke};
+            const Opnd a{p.dZ1, N1, B}, bo{p.online + p.w1, N0, N0};
             auto epi = [&](int m, int n, float v) {
                 if (m < B && n < N0) out[(int64_t)m * N0 + n] = v;
             };
-            gemm_tile(la, lb, m0, n0, kb, ke, epi, false, NoRowsum{}, sm);
+            gemm3_tile<false, true>(a, bo, m0, n0, kb, ke, epi, false, NoRowsum{}, sm);
         } else {
-            // g_Wh[j][u] = sum_b dHead[b][j] H1[b][u]; g_bh[j] = sum_b dHead[b][j]
+            // head-weight gradients g_Wh[j][u] = sum_b dHead[b][j] H1[b][u]: a task owns 128
+            // head-input units and a pass of up to 8 head rows j (dueling: the V row over V
+            // units, the A rows over A units); H1 / dHead chunks of 32 samples are staged in
+            // shared memory.  The last task of a b-split does the biases sum_b dHead[b][j].
             const int u = t - n_w - n_h;
-            const int s = u / (hu_tasks + 1), c = u % (hu_tasks + 1);
+            const int s = u / (hd_tasks + 1), c = u % (hd_tasks + 1);
             const int kb = s * p.bsplit, ke = min(B, kb + p.bsplit);
             float *gp = p.gpart + (int64_t)s * p.P;
-            const int unit = c * NT + threadIdx.x;
-            const bool is_bias = (c == hu_tasks);
-            float acc[F_MAXJ];
-#pragma unroll
-            for (int j = 0; j < F_MAXJ; ++j) acc[j] = 0.0f;
-            for (int c0 = kb; c0 < ke; c0 += 128) {
-                const int c1 = min(ke, c0 + 128);
-                __syncthreads();
-                for (int e = threadIdx.x; e < (c1 - c0) * J; e += NT)
-                    dhs[e] = __ldcg(p.dHead + (int64_t)c0 * J + e);
-                __syncthreads();
-                if (is_bias) {
-                    if (threadIdx.x < J)
-                        for (int bb = 0; bb < c1 - c0; ++bb) acc[0] += dhs[bb * J + threadIdx.x];
-                } else if (unit < N1) {
-                    int jlo = 0, jhi = J;
-                    if (p.dueling) {
-                        if (unit < p.S) jhi = 1;
-                        else jlo = 1;
+            if (c == hd_tasks) {
+                // warp w reduces head rows j = w, w + 4, ...: lanes stride the samples
+                const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+                for (int j = w; j < J; j += F_NT3 / 32) {
+                    float acc = 0.0f;
+                    for (int bb = kb + lane; bb < ke; bb += 32) acc += __ldcg(p.dHead + (int64_t)bb * J + j);
+                    acc = warp_sum(acc);
+                    if (lane == 0) gp[p.bh + j] = acc;
+                }
+            } else {
+                const int ut = c / hd_passes, pass = c % hd_passes;
+                const int u0 = ut * F_G3, unit = u0 + threadIdx.x;
+                int jlo, jn;   // head rows of this tile and pass
+                if (p.dueling) {
+                    if (u0 < p.S) { jlo = 0; jn = pass == 0 ? 1 : 0; }
+                    else { jlo = 1 + 8 * pass; jn = min(8, p.A - 8 * pass); }
+                } else {
+                    jlo = 8 * pass; jn = min(8, J - 8 * pass);
+                }
+                float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                float *hsm = k3raw;                    // [<=128][F_G3] (aliases the GEMM staging)
+                float *dsm = k3raw + 128 * F_G3;       // [<=128][J]
+                for (int c0 = kb; c0 < ke; c0 += 128) {
+                    const int cn = min(128, ke - c0);
+                    __syncthreads();
+                    if (u0 + F_G3 <= N1) {
+                        for (int e = threadIdx.x; e < cn * (F_G3 / 4); e += F_NT3) {
+                            const int bb = e / (F_G3 / 4), q = e % (F_G3 / 4);
+                            cp_async16(hsm + bb * F_G3 + 4 * q, p.H1 + (int64_t)(c0 + bb) * N1 + u0 + 4 * q);
+                        }
+                    } else {
+                        for (int e = threadIdx.x; e < cn * F_G3; e += F_NT3) {
+                            const int bb = e / F_G3, q = e % F_G3;
+                            hsm[e] = u0 + q < N1 ? __ldcg(p.H1 + (int64_t)(c0 + bb) * N1 + u0 + q) : 0.0f;
+                        }
                     }
-#pragma unroll 4
-                    for (int bb = 0; bb < c1 - c0; ++bb) {
-                        const float h = __ldcg(p.H1 + (int64_t)(c0 + bb) * N1 + unit);
+                    for (int e = threadIdx.x; e < cn * J; e += F_NT3) cp_async4(dsm + e, p.dHead + (int64_t)c0 * J + e);
+                    cp_async_wait_all();
+                    __syncthreads();
+                    if (c0 == kb) trace_.mark(2);
+                    if (threadIdx.x < F_G3) {
+                        for (int bb = 0; bb < cn; ++bb) {
+                            const float h = hsm[bb * F_G3 + threadIdx.x];
 #pragma unroll
-                        for (int j = 0; j < F_MAXJ; ++j)
-                            if (j >= jlo && j < jhi) acc[j] = fmaf(dhs[bb * J + j], h, acc[j]);
+                            for (int jj = 0; jj < 8; ++jj)
+                                if (jj < jn) acc[jj] = fmaf(dsm[bb * J + jlo + jj], h, acc[jj]);
+                        }
                     }
                 }
-            }
-            if (is_bias) {
-                if (threadIdx.x < J) gp[p.bh + threadIdx.x] = acc[0];
-            } else if (unit < N1) {
+                trace_.mark(3);
+                if (threadIdx.x < F_G3 && unit < N1) {
 #pragma unroll
-                for (int j = 0; j < F_MAXJ; ++j) {
-                    if (j >= J) break;
-                    if (!p.dueling) gp[p.wh + (int64_t)j * N1 + unit] = acc[j];
-                    else if (j == 0 && unit < p.S) gp[p.wh + unit] = acc[0];
-                    else if (j > 0 && unit >= p.S) gp[p.wh + (int64_t)j * p.S + (unit - p.S)] = acc[j];
+                    for (int jj = 0; jj < 8; ++jj) {
+                        if (jj >= jn) break;
+                        const int j = jlo + jj;
+                        int64_t dst;
+                        if (!p.dueling) dst = p.wh + (int64_t)j * N1 + unit;
+                        else if (j == 0) dst = p.wh + unit;
+                        else dst = p.wh + (int64_t)j * p.S + (unit - p.S);
+                        gp[dst] = acc[jj];
+                    }
                 }
             }
         }
@@ -452,6 +795,9 @@ __global__ void __launch_bounds__(NT) fast_bwd1_kernel(const __grid_constant__ F
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant__ FastArgs p)
 {
+    CtaTrace trace_(p.trace, 3);
+    extern __shared__ float4 smem4[];
+    float *Xsm = reinterpret_cast<float *>(smem4);   // [min(B, NT)][D] states of one b-chunk
     __shared__ float dzs[NT];
     __shared__ float red[NT];
     const int tid = threadIdx.x;
@@ -459,6 +805,7 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
     // batch-mean loss (fixed-order reduction, identical in every CTA)
     float ls = 0.0f;
     for (int b = tid; b < B; b += NT) ls += __ldcg(p.loss_part + b);
+    const bool do_sync = *p.sync_flag != 0;
     ls = warp_sum(ls);
     if ((tid & 31) == 0) red[tid >> 5] = ls;
     __syncthreads();
@@ -467,27 +814,45 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
     const float loss = lsum / (float)B;
     const bool ok = isfinite(loss);
     const bool upd = p.apply_update && ok;
-    const bool do_sync = *p.sync_flag != 0;
     __syncthreads();
+    trace_.mark(2);
     // (a) one CTA per layer-0 unit n: dZ0[:, n], dW0[n][:], db0[n], then its SGD
     for (int n = blockIdx.x; n < N0; n += gridDim.x) {
         // thread (d = tid % 32, group g = tid / 32) accumulates sum_b dZ0[b][n] X[b][d]
         const int d = tid & 31, grp = tid >> 5;
+        const float w_old = (tid < D) ? p.online[p.w0 + (int64_t)n * D + tid] : 0.0f;
+        const float b_old = (tid == 0) ? p.online[p.b0 + n] : 0.0f;
         float accw = 0.0f, accb = 0.0f;
         for (int c0 = 0; c0 < B; c0 += NT) {
+            const int cn = min(NT, B - c0);
+            __syncthreads();
+            // the chunk's states stream into shared memory while the dZ0 column is reduced
+            {
+                const int ne = cn * D, n4 = ne / 4;
+                const float *src = p.Xs + (int64_t)c0 * D;
+                for (int c = tid; c < n4; c += NT) cp_async16(Xsm + 4 * c, src + 4 * c);
+                for (int e = 4 * n4 + tid; e < ne; e += NT) cp_async4(Xsm + e, src + e);
+            }
             const int b = c0 + tid;
             float dz = 0.0f;
             if (b < B) {
-                for (int s = 0; s < p.NS; ++s) dz += __ldcg(p.dH0p + ((int64_t)s * B + b) * N0 + n);
-                dz = __ldcg(p.H0 + (int64_t)b * N0 + n) > 0.0f ? dz : 0.0f;
+                float part[8];
+                const int ns = p.NS;
+#pragma unroll
+                for (int s = 0; s < 8; ++s)
+                    part[s] = s < ns ? __ldcg(p.dH0p + ((int64_t)s * B + b) * N0 + n) : 0.0f;
+                const float h = __ldcg(p.H0 + (int64_t)b * N0 + n);
+#pragma unroll
+                for (int s = 0; s < 8; ++s) dz += part[s];
+                for (int s = 8; s < ns; ++s) dz += __ldcg(p.dH0p + ((int64_t)s * B + b) * N0 + n);
+                dz = h > 0.0f ? dz : 0.0f;
             }
-            __syncthreads();
             dzs[tid] = dz;
+            cp_async_wait_all();
             __syncthreads();
-            const int cn = min(NT, B - c0);
             for (int bb = grp; bb < cn; bb += NT / 32) {
                 const float z = dzs[bb];
-                if (d < D) accw = fmaf(z, __ldcg(p.Xs + (int64_t)(c0 + bb) * D + d), accw);
+                if (d < D) accw = fmaf(z, Xsm[bb * D + d], accw);
                 if (d == 0) accb += z;
             }
         }
@@ -501,7 +866,7 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
                 const int64_t i = p.w0 + (int64_t)n * D + tid;
                 p.grad[i] = s;
                 if (upd) {
-                    const float w = p.online[i] - p.lr * s;
+                    const float w = w_old - p.lr * s;
                     p.online[i] = w;
                     if (do_sync) p.target[i] = w;
                 }
@@ -516,16 +881,32 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
             const int64_t i = p.b0 + n;
             p.grad[i] = s;
             if (upd) {
-                const float w = p.online[i] - p.lr * s;
+                const float w = b_old - p.lr * s;
                 p.online[i] = w;
                 if (do_sync) p.target[i] = w;
             }
         }
         __syncthreads();
     }
-    // (b) every other parameter: [w1, P) (the blob stores W0, b0 first)
+    trace_.mark(3);
+    // (b) every other parameter: [w1, P) (the blob stores W0, b0 first), float4 where whole
     const int64_t lo = p.w1, n_el = p.P - p.w1;
-    for (int64_t e = (int64_t)blockIdx.x * NT + tid; e < n_el; e += (int64_t)gridDim.x * NT) {
+    const int64_t n4 = (p.nsb == 1) ? n_el / 4 : 0;
+    const int64_t stride = (int64_t)gridDim.x * NT;
+    for (int64_t e = (int64_t)blockIdx.x * NT + tid; e < n4; e += stride) {
+        const int64_t i = lo + 4 * e;
+        const float4 g = __ldcg(reinterpret_cast<const float4 *>(p.grad + i));
+        if (upd) {
+            float4 w = *reinterpret_cast<const float4 *>(p.online + i);
+            w.x -= p.lr * g.x;
+            w.y -= p.lr * g.y;
+            w.z -= p.lr * g.z;
+            w.w -= p.lr * g.w;
+            *reinterpret_cast<float4 *>(p.online + i) = w;
+            if (do_sync) *reinterpret_cast<float4 *>(p.target + i) = w;
+        }
+    }
+    for (int64_t e = 4 * n4 + (int64_t)blockIdx.x * NT + tid; e < n_el; e += stride) {
         const int64_t i = lo + e;
         float g;
         if (p.nsb == 1) {
