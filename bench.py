@@ -255,11 +255,8 @@ def run_ours(a, batch, first_line=True):
     dqn = binding.DQN(cfg, init_params(27, 8, cfg.hidden, cfg.dueling, cfg.stream, seed=3),
                       device=local)
     if world > 1:
-        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(binding.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        dqn.attach_nccl(rank, world, bytes(uid.cpu().numpy().tobytes()))
+        from paper_1801_03138_b200 import dp
+        dp.attach(dqn)   # NCCL gradient all-reduce inside every dqn_train_step
 
     K, W, k = a.steps, a.warmup, a.adds_per_step
     npool = max(k, 1) * 256
@@ -351,10 +348,13 @@ def run_ours(a, batch, first_line=True):
     traffic = load_traffic().get(f"train_step_b{batch}_{a.net}_{'ddqn' if a.ddqn else 'dqn'}")
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
                 "frac": achieved / peak_fp32, "traffic": traffic,
-                "kernel": "train_step_kernel (one cooperative launch per step)",
+                "kernel": "the train-step CUDA graph (fwd / td / bwd1 / bwd0+sgd kernels) timed as one "
+                          "unit with CUDA events around each dqn_train_step on the library stream",
                 "kernel_avg_us": kern_avg_ms * 1000.0, "flops_per_launch": flops,
                 "peak_note": "FP32 SIMT: 148 SMs x 128 FMA lanes x 2 FLOP x sm_max_mhz "
-                             f"{sm_mhz:.0f} MHz (derived, {peaks_kind} clock)"}
+                             f"{sm_mhz:.0f} MHz (derived, {peaks_kind} clock); the forward runs its "
+                             "products as 3xTF32 mma.sync, so this FP32 peak is the conservative "
+                             "denominator for an FP32-accurate step"}
 
     # ---- gather bandwidth (metric part 2): explicit-index gather from the 1M ring --------
     gather = None

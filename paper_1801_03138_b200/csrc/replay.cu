@@ -191,6 +191,93 @@ __global__ void __launch_bounds__(256) gather_kernel(const float *__restrict__ r
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Bandwidth-oriented gather for 256-byte rows (D <= 30): a warp owns 32 consecutive entries,
+// issues all 32 row loads (16 B per lane, 16 float4 in flight per lane) before using any, stages
+// the rows in shared memory, then writes every output tensor as full, coalesced lines (s and s'
+// as float4 runs of 32*D floats; a, r, done, idx as 32-wide vectors).
+// ------------------------------------------------------------------------------------------
+constexpr int GS_W = 8;   // warps per CTA
+template <int KD>
+__global__ void __launch_bounds__(GS_W * 32) gather_staged_kernel(
+    const float *__restrict__ rows, int64_t size, int64_t n, const int32_t *__restrict__ idx_in,
+    uint64_t seed, uint32_t rank, uint64_t event, float *s, float *s2, int32_t *a, float *r,
+    uint8_t *done, int32_t *idx_out, uint32_t *err, uint64_t *ctrl, int vec_ok)
+{
+    constexpr int RW = 2 * KD + 3;   // used words of a row: s | s' | a | r | done
+    constexpr int SP = RW + 1;       // staging row stride
+    extern __shared__ float4 gs_smem[];
+    float *st = reinterpret_cast<float *>(gs_smem) + (threadIdx.x >> 5) * 32 * SP;
+    if (idx_in == nullptr && ctrl && blockIdx.x == 0 && threadIdx.x == 0) ctrl[0] = event + 1;
+    const int lane = threadIdx.x & 31, half = lane >> 4, p = lane & 15;
+    const int64_t ngroups = (n + 31) / 32;
+    const int64_t nwarps = (int64_t)gridDim.x * GS_W;
+    for (int64_t grp = (int64_t)blockIdx.x * GS_W + (threadIdx.x >> 5); grp < ngroups; grp += nwarps) {
+        const int64_t base = grp * 32, e = base + lane;
+        int32_t ix;
+        if (idx_in == nullptr) {
+            int32_t i0, i1;
+            sample_pair(seed, rank, event, (uint32_t)(e >> 1), (uint64_t)size, i0, i1);
+            ix = (lane & 1) ? i1 : i0;
+        } else {
+            ix = e < n ? idx_in[e] : 0;
+            if (ix < 0 || ix >= size) {
+                if (e < n) atomicOr(err, ERRBIT_RANGE);
+                ix = min(max(ix, 0), (int32_t)size - 1);
+            }
+        }
+        if (idx_out && e < n) idx_out[e] = ix;
+        float4 v[16];
+#pragma unroll
+        for (int it = 0; it < 16; ++it) {
+            const int ent = 2 * it + half;
+            const int32_t rix = __shfl_sync(0xffffffffu, ix, ent);
+            v[it] = (base + ent < n) ? __ldg(reinterpret_cast<const float4 *>(rows + (int64_t)rix * 64) + p)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int it = 0; it < 16; ++it) {
+            const int ent = 2 * it + half;
+            float *dst = st + ent * SP;
+            const float c[4] = {v[it].x, v[it].y, v[it].z, v[it].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (4 * p + q < RW) dst[4 * p + q] = c[q];
+        }
+        __syncwarp();
+        const int cnt = (int)(n - base < 32 ? n - base : 32);
+        if (cnt == 32 && vec_ok) {
+            // 32 * KD floats per state tensor, 16-byte aligned (base % 32 == 0)
+            float4 *so = reinterpret_cast<float4 *>(s + base * KD);
+            float4 *s2o = reinterpret_cast<float4 *>(s2 + base * KD);
+            for (int q = lane; q < 8 * KD; q += 32) {
+                float w0[4], w1[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int el = 4 * q + k, rr = el / KD, cc = el - rr * KD;
+                    w0[k] = st[rr * SP + cc];
+                    w1[k] = st[rr * SP + KD + cc];
+                }
+                if (s) so[q] = make_float4(w0[0], w0[1], w0[2], w0[3]);
+                if (s2) s2o[q] = make_float4(w1[0], w1[1], w1[2], w1[3]);
+            }
+        } else {
+            for (int el = lane; el < cnt * KD; el += 32) {
+                const int rr = el / KD, cc = el - rr * KD;
+                if (s) s[base * KD + el] = st[rr * SP + cc];
+                if (s2) s2[base * KD + el] = st[rr * SP + KD + cc];
+            }
+        }
+        if (lane < cnt) {
+            const float *row = st + lane * SP + 2 * KD;
+            if (a) a[e] = __float_as_int(row[0]);
+            if (r) r[e] = row[1];
+            if (done) done[e] = (uint8_t)(__float_as_uint(row[2]) != 0u);
+        }
+        __syncwarp();
+    }
+}
+
 const void *insert_kernel_ptr() { return (const void *)insert_kernel; }
 
 int launch_gather(const rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t event,
@@ -205,7 +292,25 @@ int launch_gather(const rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint6
     if (blocks > max_blocks) blocks = max_blocks;
     if (blocks < 1) blocks = 1;
     const rpl::Ring &R = rp->ring;
-    if (R.rs == 64) {
+    if (R.rs == 64 && R.D == 27) {
+        // staged, line-coalesced writes (the Melee row: 27-float states)
+        constexpr int KD = 27;
+        const size_t smem = (size_t)GS_W * 32 * (2 * KD + 4) * sizeof(float);
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(gather_staged_kernel<KD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr_set = true;
+        }
+        const int64_t g32 = (n + 31) / 32;
+        int64_t nb = (g32 + GS_W - 1) / GS_W;
+        if (nb > (int64_t)dev_sms * 4) nb = (int64_t)dev_sms * 4;
+        if (nb < 1) nb = 1;
+        const int vec_ok = ((uintptr_t)out->s % 16 == 0) && ((uintptr_t)out->s_next % 16 == 0);
+        gather_staged_kernel<KD><<<(unsigned)nb, GS_W * 32, smem, rp->stream>>>(
+            R.rows, rp->size, n, use_sampler ? nullptr : idx_dev, rp->seed, rp->rank, event,
+            out->s, out->s_next, out->a, out->r, out->done, out->idx, rp->err_dev, rp->ctrl_dev,
+            vec_ok);
+    } else if (R.rs == 64) {
         gather_kernel<true><<<(unsigned)blocks, 256, 0, rp->stream>>>(
             R.rows, R.rs, R.D, rp->size, n, use_sampler ? nullptr : idx_dev, rp->seed, rp->rank,
             event, out->s, out->s_next, out->a, out->r, out->done, out->idx, rp->err_dev,

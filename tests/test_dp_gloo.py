@@ -1,0 +1,106 @@
+"""World-size-2 CPU (gloo) tests of the data-parallel host logic.
+
+The GPU path all-reduces the flat gradient with NCCL inside dqn_train_step; here the same
+protocol runs with the oracle as the per-rank learner and gloo as the transport:
+  * the 128-byte NCCL-id broadcast used by paper_1801_03138_b200.dp reaches every rank intact;
+  * replicas stay bit-identical step after step (mean of per-rank gradients, same SGD);
+  * world 2 with identical shards and a rank-independent stream equals one learner bit for
+    bit ((g + g) / 2 == g exactly);
+  * with distinct shards the averaged update equals the rank-order mean (O6 reading Q23).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from inputs import experiences, init_params
+
+NET = oracle.Net(27, 8, False, (64, 64))
+STEPS = 5
+B = 32
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _learner_steps(rank, world, same_shard, out):
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1801_03138_b200 import dp
+    # 1. unique-id broadcast
+    payload = bytes(range(128)) if rank == 0 else None
+    got = dp.broadcast_bytes(payload, 0)
+    assert got == bytes(range(128))
+    # 2. per-rank shard + sampler stream
+    data_rank = 0 if same_shard else rank
+    ring = oracle.Ring(500, 27)
+    ring.add(**experiences(500, seed=1, rank=data_rank))
+    w = init_params(27, 8, (64, 64), False, seed=3).astype(np.float64)
+    tg = w.copy()
+    for step in range(STEPS):
+        rc, batch = ring.sample(1, 2, data_rank, B)
+        assert rc == oracle.OK
+        o = oracle.dqn_loss_grad(NET, w.astype(np.float32), tg.astype(np.float32), batch, 0.99, 1.0, False)
+        g = torch.from_numpy(o["grad"].copy())
+        dist.all_reduce(g, op=dist.ReduceOp.SUM)
+        g = g.numpy() / world
+        w = oracle.sgd(w, g, 1e-2).astype(np.float32).astype(np.float64)
+        gathered = [torch.zeros_like(torch.from_numpy(w)) for _ in range(world)]
+        dist.all_gather(gathered, torch.from_numpy(w))
+        assert all(np.array_equal(x.numpy(), w) for x in gathered), "replicas diverged"
+    out[rank] = w
+    dist.destroy_process_group()
+
+
+def _run(world, same_shard):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_learner_steps, args=(world, same_shard, out), nprocs=world, join=True)
+        return {k: v for k, v in out.items()}
+
+
+def _single(data_rank):
+    ring = oracle.Ring(500, 27)
+    ring.add(**experiences(500, seed=1, rank=data_rank))
+    w = init_params(27, 8, (64, 64), False, seed=3).astype(np.float64)
+    tg = w.copy()
+    grads = []
+    for step in range(STEPS):
+        rc, batch = ring.sample(1, 2, data_rank, B)
+        o = oracle.dqn_loss_grad(NET, w.astype(np.float32), tg.astype(np.float32), batch, 0.99, 1.0, False)
+        w = oracle.sgd(w, o["grad"], 1e-2).astype(np.float32).astype(np.float64)
+        grads.append(o["grad"])
+    return w
+
+
+def test_world2_identical_shards_equals_single_learner():
+    out = _run(2, same_shard=True)
+    assert np.array_equal(out[0], out[1])
+    assert np.array_equal(out[0], _single(0))
+
+
+def test_world2_distinct_shards_replicas_identical_and_mean_rule():
+    out = _run(2, same_shard=False)
+    assert np.array_equal(out[0], out[1])
+    # the first averaged step equals the rank-order mean of the two per-rank gradients
+    w0 = init_params(27, 8, (64, 64), False, seed=3)
+    gs = []
+    for r in (0, 1):
+        ring = oracle.Ring(500, 27)
+        ring.add(**experiences(500, seed=1, rank=r))
+        rc, batch = ring.sample(1, 2, r, B)
+        gs.append(oracle.dqn_loss_grad(NET, w0, w0, batch, 0.99, 1.0, False)["grad"])
+    assert not np.array_equal(gs[0], gs[1])      # the shards really differ
+    assert not np.array_equal(out[0], _single(0))
