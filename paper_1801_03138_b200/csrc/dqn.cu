@@ -717,13 +717,6 @@ static int fast_ns(const rpl_dqn *d, int B)
     while (ns * 2 <= want && ns * 2 * 32 <= d->N[1]) ns *= 2;
     return ns;
 }
-static int fast_max_ns(const rpl_dqn *d)
-{
-    int m = 1;
-    for (int B = 1; B <= d->cfg.max_batch; B = B < d->cfg.max_batch ? std::min(2 * B, d->cfg.max_batch) : B + 1)
-        m = std::max(m, fast_ns(d, B));
-    return std::max(m, fast_ns(d, 1));
-}
 
 extern "C" int dqn_destroy(rpl_dqn *d)
 {
@@ -794,7 +787,7 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
     }
     // fast path: two trunk layers (dueling with one shared layer, or a plain 2-hidden-layer MLP)
     const char *path = getenv("RPL_PATH");
-    d->fast = d->T == 2 && d->N[0] % 4 == 0 && d->N[0] <= 256 && D <= 64 && d->J <= F_MAXJ &&
+    d->fast = d->T == 2 && d->N[0] % 4 == 0 && d->N[0] <= 256 && D <= 31 && d->J <= F_MAXJ &&
               d->N[1] % 4 == 0 && (!cfg->dueling || cfg->stream % 4 == 0) && fast_ut_cfg(*cfg, d->N[1]) > 0 &&
               d->woff[1] % 4 == 0 && !(path && strcmp(path, "generic") == 0);
     const char *ng = getenv("RPL_NO_GRAPH");
@@ -809,13 +802,16 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
         const int ut = fast_ut(d);
         const int nut = (d->N[1] + ut - 1) / ut;
         d->part_elems = (int64_t)nets * nut * Bm * d->J;
-        d->dh0p_elems = (int64_t)fast_max_ns(d) * Bm * d->N[0];
+        // dW0 / db0 partials: NS(B) x ceil(B / 32) x (N0 D + N0); NS(B) x tiles(B) <= sms
+        // with tiles(B) = ceil(B / 32) * ceil(N0 / 64) >= ceil(B / 32), so the product is
+        // bounded by sms + ceil(B / 32) for every B <= max_batch
+        const int64_t w0p = d->sms + (Bm + BM - 1) / BM;
+        d->dh0p_elems = w0p * (d->woff[1]);
         ok = dalloc(d, &d->part, d->part_elems) && dalloc(d, &d->dH0p, d->dh0p_elems);
         ok = ok && cudaStreamCreateWithFlags(&d->cap_stream, cudaStreamNonBlocking) == cudaSuccess;
         ok = ok && cudaFuncSetAttribute(fast_fwd_fn(d), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         fast_fwd_smem(d, ut)) == cudaSuccess;
-        ok = ok && cudaFuncSetAttribute(fast_bwd0_sgd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        NT * D * sizeof(float)) == cudaSuccess;
+
         ok = ok && cudaFuncSetAttribute(fast_bwd1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         K3_SMEM_FLOATS * sizeof(float)) == cudaSuccess;
         // one shared-memory carveout for every kernel of the step: no L1/shared
@@ -971,7 +967,7 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.nut = (p.N1 + p.UT - 1) / p.UT;
     p.dHead = d->dO;
     p.dZ1 = d->dZlast;
-    p.dH0p = d->dH0p;
+    p.w0part = d->dH0p;
     p.NS = fast_ns(d, B);
     p.nsb = (B + 511) / 512;
     p.bsplit = 512;
@@ -1006,11 +1002,10 @@ static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
     const int n_w = ((p.N1 + BM - 1) / BM) * ((p.N0 + BN - 1) / BN) * p.nsb;
     const int n_h = ((p.B + BM - 1) / BM) * ((p.N0 + BN - 1) / BN) * p.NS;
     const int hd_passes = p.dueling ? (p.A + 7) / 8 : (p.J + 7) / 8;
-    const int n_hd = (((p.N1 + F_G3 - 1) / F_G3) * hd_passes + 1) * p.nsb;
+    const int n_hd = (((p.N1 + HD_U - 1) / HD_U) * hd_passes + 1) * p.nsb;
     fast_bwd1_kernel<<<std::min(n_w + n_h + n_hd, 4 * d->sms), F_NT3, K3_SMEM_FLOATS * sizeof(float), st>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    fast_bwd0_sgd_kernel<<<std::max(std::min(p.N0, 4 * d->sms), d->sms), NT,
-                           (size_t)std::min(p.B, NT) * p.D * sizeof(float), st>>>(p);
+    fast_bwd0_sgd_kernel<<<d->sms, NT, 0, st>>>(p);
     return cudaGetLastError();
 }
 

@@ -56,7 +56,7 @@ struct FastArgs {
     int nut, UT;
     float *dHead;        // [B][J]
     float *dZ1;          // [B][N1]
-    float *dH0p;         // [NS][B][N0]
+    float *w0part;       // [NS][ceil(B/32)][N0*D + N0] dW0 / db0 partials (K3 -> K4)
     int NS;
     float *gpart;        // [nsb][P] (== grad when nsb == 1)
     int nsb, bsplit;
@@ -665,16 +665,135 @@ __device__ __forceinline__ void gemm3_tile(const Opnd &a, const Opnd &b, int m0,
 // ------------------------------------------------------------------------------------------
 // K3: dW1 / db1 tiles, dH0 split-K tiles, head-weight gradients
 // ------------------------------------------------------------------------------------------
-constexpr int K3_HD_FLOATS = 128 * F_G3 + 128 * F_MAXJ;   // head-gradient staging
-constexpr int K3_SMEM_FLOATS = (int)(2 * sizeof(Gemm3Smem) / 4) > K3_HD_FLOATS ? (int)(2 * sizeof(Gemm3Smem) / 4)
-                                                                             : K3_HD_FLOATS;
+// ------------------------------------------------------------------------------------------
+// K3 tensor-core tile: C[32 x 64] = sum_{kk in [kb, ke)} A(m, kk) B(n, kk) with 3xTF32
+// mma.sync.m16n8k8 (FP32-accurate), 256 threads = 8 warps as 2 (m16) x 4 (n16).  The whole
+// contraction range (up to MM_SK per pass) is copied global -> shared with 16-byte cp.async in
+// one go (one L2 round trip), stored k-major with row strides == 4 (mod 32) words so every
+// fragment load is conflict-free, and split into tf32 hi / lo while loading fragments.
+// Operand element (r, kk) is p[kk * ld + r] (kRc) or p[r * ld + kk]; r, kk multiples of 4 are
+// whole 16-byte chunks (all dims here are multiples of 4), missing chunks are zero-filled.
+// ------------------------------------------------------------------------------------------
+constexpr int MM_T = 256;
+constexpr int MM_SK = 128;                   // contraction per pass
+constexpr int MM_AS = BM + 4, MM_BS = BN + 4;
+constexpr int MM_FLOATS = MM_SK * (MM_AS + MM_BS);
+
+__device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, bool valid)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+
+// stage [k0, k0 + MM_SK) of an operand with TR rows into S[kk][r] (row stride LDS)
+template <bool kRc, int TR, int LDS>
+__device__ __forceinline__ void mm_stage(float *S, const Opnd &o, int r0, int k0, int kend, int tid)
+{
+    if (kRc) {
+        // source rows are kk: TR/4 chunks of 16 B per kk
+        for (int e = tid; e < MM_SK * (TR / 4); e += MM_T) {
+            const int kk = e / (TR / 4), r4 = e % (TR / 4);
+            const int r = r0 + 4 * r4, k = k0 + kk;
+            const bool v = r < o.R && k < kend;
+            cp_async16_zfill(S + kk * LDS + 4 * r4, v ? o.p + (int64_t)k * o.ld + r : o.p, v);
+        }
+    } else {
+        // source rows are r: 4 consecutive kk of one r per float4, transposed into shared
+        // memory; every load of the pass is issued before the first store
+        constexpr int NV = TR * (MM_SK / 4) / MM_T;
+        float4 v[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int e = i * MM_T + tid, r = e / (MM_SK / 4), k4 = e % (MM_SK / 4);
+            const int rr = r0 + r, k = k0 + 4 * k4;
+            v[i] = (rr < o.R && k < kend) ? __ldcg(reinterpret_cast<const float4 *>(o.p + (int64_t)rr * o.ld + k))
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int e = i * MM_T + tid, r = e / (MM_SK / 4), k4 = e % (MM_SK / 4);
+            S[(4 * k4 + 0) * LDS + r] = v[i].x;
+            S[(4 * k4 + 1) * LDS + r] = v[i].y;
+            S[(4 * k4 + 2) * LDS + r] = v[i].z;
+            S[(4 * k4 + 3) * LDS + r] = v[i].w;
+        }
+    }
+}
+
+template <bool kARc, bool kBRc, class EPI, class RSUM>
+__device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int m0, int n0, int kb, int ke,
+                                              const EPI &epi, bool want_rowsum, const RSUM &rs, float *smf)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3, wm = warp & 1, wn = warp >> 1;
+    float *As = smf, *Bs = smf + MM_SK * MM_AS;
+    // the MMA accumulates 32-deep partials (4 k-steps) that are added into round-to-nearest
+    // FP32 sums, so long contractions (K = 1024 at large batch) keep FP32-level accuracy
+    float c[2][4], cs[2][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c[i][q] = cs[i][q] = 0.0f;
+    float rsum = 0.0f;
+    for (int k0 = kb; k0 < ke; k0 += MM_SK) {
+        __syncthreads();   // the previous pass / task is done with the staging buffers
+        mm_stage<kARc, BM, MM_AS>(As, a, m0, k0, ke, tid);
+        mm_stage<kBRc, BN, MM_BS>(Bs, b, n0, k0, ke, tid);
+        cp_async_wait_all();
+        __syncthreads();
+        const int ksteps = (min(MM_SK, ke - k0) + 7) / 8;
+        const int mr = 16 * wm + g;
+        for (int ks = 0; ks < ksteps; ++ks) {
+            const int k = 8 * ks;
+            uint32_t ah[4], al[4];
+            tf32_split(As[(k + t) * MM_AS + mr], ah[0], al[0]);
+            tf32_split(As[(k + t) * MM_AS + mr + 8], ah[1], al[1]);
+            tf32_split(As[(k + t + 4) * MM_AS + mr], ah[2], al[2]);
+            tf32_split(As[(k + t + 4) * MM_AS + mr + 8], ah[3], al[3]);
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                const int nc = 16 * wn + 8 * nt + g;
+                uint32_t bh[2], bl[2];
+                tf32_split(Bs[(k + t) * MM_BS + nc], bh[0], bl[0]);
+                tf32_split(Bs[(k + t + 4) * MM_BS + nc], bh[1], bl[1]);
+                mma_3xtf32(c[nt], ah, al, bh, bl);
+            }
+            if ((ks & 3) == 3 || ks == ksteps - 1) {
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        cs[i][q] += c[i][q];
+                        c[i][q] = 0.0f;
+                    }
+            }
+        }
+        if (want_rowsum && tid < BM) {
+            const int kn = min(MM_SK, ke - k0);
+            for (int k = 0; k < kn; ++k) rsum += As[k * MM_AS + tid];
+        }
+    }
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            epi(m0 + 16 * wm + g + 8 * (q >> 1), n0 + 16 * wn + 8 * nt + 2 * t + (q & 1), cs[nt][q]);
+    if (want_rowsum && tid < BM) rs(m0 + tid, rsum);
+}
+
+constexpr int HD_U = 64;                                   // head-gradient unit tile
+constexpr int K3_HD_FLOATS = 128 * HD_U + 128 * F_MAXJ + 4 * HD_U * 8;   // head-gradient staging
+constexpr int K3_GEMM_FLOATS = MM_FLOATS;
+// + the dH0 tile and the batch tile's states (D <= 64)
+constexpr int K3_DH_FLOATS = K3_GEMM_FLOATS + BM * (BN + 4) + BM * 36 + BM * BN;
+constexpr int K3_SMEM_FLOATS = K3_DH_FLOATS > K3_HD_FLOATS ? K3_DH_FLOATS : K3_HD_FLOATS;
 
 __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant__ FastArgs p)
 {
     CtaTrace trace_(p.trace, 2);
     extern __shared__ float4 smem4[];
     float *k3raw = reinterpret_cast<float *>(smem4);   // K3_SMEM_FLOATS
-    Gemm3Smem *sm = reinterpret_cast<Gemm3Smem *>(k3raw);   // one staging area per group
     const int N0 = p.N0, N1 = p.N1, B = p.B, J = p.J;
     const int wmt = (N1 + BM - 1) / BM, wnt = (N0 + BN - 1) / BN;
     const int n_w = wmt * wnt * p.nsb;
@@ -682,7 +801,7 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
     const int n_h = hmt * hnt * p.NS;
     // head-weight gradient tasks: (128-unit tile) x (pass of <= 8 head rows), + 1 bias task
     const int hd_passes = p.dueling ? (p.A + 7) / 8 : (J + 7) / 8;
-    const int hd_tasks = ((N1 + F_G3 - 1) / F_G3) * hd_passes;
+    const int hd_tasks = ((N1 + HD_U - 1) / HD_U) * hd_passes;
     const int n_hd = (hd_tasks + 1) * p.nsb;
     const int ntasks = n_w + n_h + n_hd;
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
@@ -699,7 +818,7 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             auto rs = [&](int m, float v) {
                 if (m < N1) gp[p.b1 + m] = v;
             };
-            gemm3_tile<true, true>(a, bo, m0, n0, kb, ke, epi, n0 == 0, rs, sm);
+            gemm_mma_tile<true, true>(a, bo, m0, n0, kb, ke, epi, n0 == 0, rs, k3raw);
             trace_.mark(4);
         } else if (t < n_w + n_h) {
             // dH0 partial [s][b][k] = sum_{u in split s} dZ1[b][u] W1[u][k]
@@ -708,12 +827,78 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             const int m0 = (rem / hnt) * BM, n0 = (rem % hnt) * BN;
             const int chunk = (N1 + p.NS - 1) / p.NS;
             const int kb = s * chunk, ke = min(N1, kb + chunk);
-            float *out = p.dH0p + (int64_t)s * B * N0;
+            // the partial dH0 tile stays in shared memory; masked by ReLU'(z0) it gives this
+            // (split, batch tile)'s share of dW0 = dZ0^T X and db0 = sum_b dZ0 (the mask
+            // distributes over the split-K sum), reduced in K4 in a fixed order
+            float *tile = k3raw + K3_GEMM_FLOATS;          // [BM][BN + 4] partial dH0
+            float *xs = tile + BM * (BN + 4);              // [BM][XS] states, column D = 1
+            constexpr int XS = 36;
             const Opnd a{p.dZ1, N1, B}, bo{p.online + p.w1, N0, N0};
-            auto epi = [&](int m, int n, float v) {
-                if (m < B && n < N0) out[(int64_t)m * N0 + n] = v;
-            };
-            gemm3_tile<false, true>(a, bo, m0, n0, kb, ke, epi, false, NoRowsum{}, sm);
+            auto epi = [&](int m, int n, float v) { tile[(m - m0) * (BN + 4) + (n - n0)] = v; };
+            gemm_mma_tile<false, true>(a, bo, m0, n0, kb, ke, epi, false, NoRowsum{}, k3raw);
+            __syncthreads();
+            trace_.mark(5);
+            const int D = p.D, nb = min(BM, B - m0), nk = min(BN, N0 - n0);
+            float *h0t = xs + BM * XS;                     // [BM][BN] H0 of the tile (ReLU mask)
+            for (int e = threadIdx.x; e < nb * D; e += F_NT3) {
+                const int bb = e / D, d = e - bb * D;
+                cp_async4(xs + bb * XS + d, p.Xs + (int64_t)m0 * D + e);
+            }
+            for (int e = threadIdx.x; e < BM * (XS - D); e += F_NT3) {
+                const int bb = e / (XS - D), d = D + e % (XS - D);
+                xs[bb * XS + d] = (d == D && bb < nb) ? 1.0f : 0.0f;   // ones column -> db0
+            }
+            for (int e = threadIdx.x; e < nb * (nk / 4); e += F_NT3) {
+                const int bb = e / (nk / 4), q = e % (nk / 4);
+                cp_async16(h0t + bb * BN + 4 * q, p.H0 + (int64_t)(m0 + bb) * N0 + n0 + 4 * q);
+            }
+            cp_async_wait_all();
+            __syncthreads();
+            trace_.mark(6);
+            for (int e = threadIdx.x; e < BM * BN; e += F_NT3) {
+                const int bb = e / BN, kk = e % BN;
+                const bool on = bb < nb && kk < nk && h0t[bb * BN + kk] > 0.0f;
+                if (!on) tile[bb * (BN + 4) + kk] = 0.0f;
+            }
+            if (nb < BM)
+                for (int e = threadIdx.x; e < (BM - nb) * XS; e += F_NT3) xs[nb * XS + e] = 0.0f;
+            __syncthreads();
+            // dW0 / db0 share: C[unit k][d] = sum_b tile[b][k] xs[b][d] over the tile's rows;
+            // M = 64 units (4 m16 tiles), N = 32 (27 states + ones column), K = 32 rows
+            float *w0p = p.w0part + ((int64_t)s * ((B + BM - 1) / BM) + m0 / BM) * (p.b0 + N0);
+            {
+                const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+                const int mt = warp & 3, np = warp >> 2;   // m16 tile, pair of n8 tiles
+                float c2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+                for (int k = 0; k < BM; k += 8) {
+                    uint32_t ah[4], al[4];
+                    const int mr = 16 * mt + g;
+                    tf32_split(tile[(k + t) * (BN + 4) + mr], ah[0], al[0]);
+                    tf32_split(tile[(k + t) * (BN + 4) + mr + 8], ah[1], al[1]);
+                    tf32_split(tile[(k + t + 4) * (BN + 4) + mr], ah[2], al[2]);
+                    tf32_split(tile[(k + t + 4) * (BN + 4) + mr + 8], ah[3], al[3]);
+#pragma unroll
+                    for (int nt = 0; nt < 2; ++nt) {
+                        const int nc = 16 * np + 8 * nt + g;
+                        uint32_t bh[2], bl[2];
+                        tf32_split(xs[(k + t) * XS + nc], bh[0], bl[0]);
+                        tf32_split(xs[(k + t + 4) * XS + nc], bh[1], bl[1]);
+                        mma_3xtf32(c2[nt], ah, al, bh, bl);
+                    }
+                }
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int kk = 16 * mt + g + 8 * (q >> 1), d = 16 * np + 8 * nt + 2 * t + (q & 1);
+                        const int k = n0 + kk;
+                        if (kk >= nk) continue;
+                        if (d < D) w0p[p.w0 + (int64_t)k * D + d] = c2[nt][q];
+                        else if (d == D) w0p[p.b0 + k] = c2[nt][q];
+                    }
+            }
+            trace_.mark(7);
         } else {
             // head-weight gradients g_Wh[j][u] = sum_b dHead[b][j] H1[b][u]: a task owns 128
             // head-input units and a pass of up to 8 head rows j (dueling: the V row over V
@@ -733,8 +918,9 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
                     if (lane == 0) gp[p.bh + j] = acc;
                 }
             } else {
+                // 64-unit tile; thread = (unit, quarter of the samples); fixed-order reduction
                 const int ut = c / hd_passes, pass = c % hd_passes;
-                const int u0 = ut * F_G3, unit = u0 + threadIdx.x;
+                const int u0 = ut * HD_U, ul = threadIdx.x % HD_U, qtr = threadIdx.x / HD_U;
                 int jlo, jn;   // head rows of this tile and pass
                 if (p.dueling) {
                     if (u0 < p.S) { jlo = 0; jn = pass == 0 ? 1 : 0; }
@@ -743,19 +929,20 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
                     jlo = 8 * pass; jn = min(8, J - 8 * pass);
                 }
                 float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                float *hsm = k3raw;                    // [<=128][F_G3] (aliases the GEMM staging)
-                float *dsm = k3raw + 128 * F_G3;       // [<=128][J]
+                float *hsm = k3raw;                    // [<=128][HD_U]
+                float *dsm = k3raw + 128 * HD_U;       // [<=128][J]
+                float *red = dsm + 128 * F_MAXJ;       // [4][HD_U][8]
                 for (int c0 = kb; c0 < ke; c0 += 128) {
                     const int cn = min(128, ke - c0);
                     __syncthreads();
-                    if (u0 + F_G3 <= N1) {
-                        for (int e = threadIdx.x; e < cn * (F_G3 / 4); e += F_NT3) {
-                            const int bb = e / (F_G3 / 4), q = e % (F_G3 / 4);
-                            cp_async16(hsm + bb * F_G3 + 4 * q, p.H1 + (int64_t)(c0 + bb) * N1 + u0 + 4 * q);
+                    if (u0 + HD_U <= N1) {
+                        for (int e = threadIdx.x; e < cn * (HD_U / 4); e += F_NT3) {
+                            const int bb = e / (HD_U / 4), q = e % (HD_U / 4);
+                            cp_async16(hsm + bb * HD_U + 4 * q, p.H1 + (int64_t)(c0 + bb) * N1 + u0 + 4 * q);
                         }
                     } else {
-                        for (int e = threadIdx.x; e < cn * F_G3; e += F_NT3) {
-                            const int bb = e / F_G3, q = e % F_G3;
+                        for (int e = threadIdx.x; e < cn * HD_U; e += F_NT3) {
+                            const int bb = e / HD_U, q = e % HD_U;
                             hsm[e] = u0 + q < N1 ? __ldcg(p.H1 + (int64_t)(c0 + bb) * N1 + u0 + q) : 0.0f;
                         }
                     }
@@ -763,27 +950,30 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
                     cp_async_wait_all();
                     __syncthreads();
                     if (c0 == kb) trace_.mark(2);
-                    if (threadIdx.x < F_G3) {
-                        for (int bb = 0; bb < cn; ++bb) {
-                            const float h = hsm[bb * F_G3 + threadIdx.x];
+                    const int q0 = (cn * qtr) / 4, q1 = (cn * (qtr + 1)) / 4;
+                    for (int bb = q0; bb < q1; ++bb) {
+                        const float h = hsm[bb * HD_U + ul];
+                        const float *dr = dsm + bb * J + jlo;
 #pragma unroll
-                            for (int jj = 0; jj < 8; ++jj)
-                                if (jj < jn) acc[jj] = fmaf(dsm[bb * J + jlo + jj], h, acc[jj]);
-                        }
+                        for (int jj = 0; jj < 8; ++jj)
+                            if (jj < jn) acc[jj] = fmaf(dr[jj], h, acc[jj]);
                     }
                 }
-                trace_.mark(3);
-                if (threadIdx.x < F_G3 && unit < N1) {
 #pragma unroll
-                    for (int jj = 0; jj < 8; ++jj) {
-                        if (jj >= jn) break;
-                        const int j = jlo + jj;
-                        int64_t dst;
-                        if (!p.dueling) dst = p.wh + (int64_t)j * N1 + unit;
-                        else if (j == 0) dst = p.wh + unit;
-                        else dst = p.wh + (int64_t)j * p.S + (unit - p.S);
-                        gp[dst] = acc[jj];
-                    }
+                for (int jj = 0; jj < 8; ++jj) red[(qtr * HD_U + ul) * 8 + jj] = acc[jj];
+                __syncthreads();
+                trace_.mark(3);
+                for (int o = threadIdx.x; o < HD_U * 8; o += F_NT3) {
+                    const int uu = o / 8, jj = o % 8, unit = u0 + uu;
+                    if (jj >= jn || unit >= N1) continue;
+                    const float v = ((red[(0 * HD_U + uu) * 8 + jj] + red[(1 * HD_U + uu) * 8 + jj]) +
+                                     red[(2 * HD_U + uu) * 8 + jj]) + red[(3 * HD_U + uu) * 8 + jj];
+                    const int j = jlo + jj;
+                    int64_t dst;
+                    if (!p.dueling) dst = p.wh + (int64_t)j * N1 + unit;
+                    else if (j == 0) dst = p.wh + unit;
+                    else dst = p.wh + (int64_t)j * p.S + (unit - p.S);
+                    gp[dst] = v;
                 }
             }
         }
@@ -796,12 +986,9 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
 __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant__ FastArgs p)
 {
     CtaTrace trace_(p.trace, 3);
-    extern __shared__ float4 smem4[];
-    float *Xsm = reinterpret_cast<float *>(smem4);   // [min(B, NT)][D] states of one b-chunk
-    __shared__ float dzs[NT];
-    __shared__ float red[NT];
+    __shared__ float red[NT / 32];
     const int tid = threadIdx.x;
-    const int N0 = p.N0, D = p.D, B = p.B;
+    const int B = p.B;
     // batch-mean loss (fixed-order reduction, identical in every CTA)
     float ls = 0.0f;
     for (int b = tid; b < B; b += NT) ls += __ldcg(p.loss_part + b);
@@ -814,85 +1001,37 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
     const float loss = lsum / (float)B;
     const bool ok = isfinite(loss);
     const bool upd = p.apply_update && ok;
-    __syncthreads();
     trace_.mark(2);
-    // (a) one CTA per layer-0 unit n: dZ0[:, n], dW0[n][:], db0[n], then its SGD
-    for (int n = blockIdx.x; n < N0; n += gridDim.x) {
-        // thread (d = tid % 32, group g = tid / 32) accumulates sum_b dZ0[b][n] X[b][d]
-        const int d = tid & 31, grp = tid >> 5;
-        const float w_old = (tid < D) ? p.online[p.w0 + (int64_t)n * D + tid] : 0.0f;
-        const float b_old = (tid == 0) ? p.online[p.b0 + n] : 0.0f;
-        float accw = 0.0f, accb = 0.0f;
-        for (int c0 = 0; c0 < B; c0 += NT) {
-            const int cn = min(NT, B - c0);
-            __syncthreads();
-            // the chunk's states stream into shared memory while the dZ0 column is reduced
-            {
-                const int ne = cn * D, n4 = ne / 4;
-                const float *src = p.Xs + (int64_t)c0 * D;
-                for (int c = tid; c < n4; c += NT) cp_async16(Xsm + 4 * c, src + 4 * c);
-                for (int e = 4 * n4 + tid; e < ne; e += NT) cp_async4(Xsm + e, src + e);
-            }
-            const int b = c0 + tid;
-            float dz = 0.0f;
-            if (b < B) {
-                float part[8];
-                const int ns = p.NS;
+    const int64_t stride = (int64_t)gridDim.x * NT;
+    // (a) W0, b0: the fixed-order sum of the (split, batch tile) partials written by K3
+    const int64_t n0el = p.w1;                  // W0 and b0 lead the blob
+    const int nparts = p.NS * ((B + BM - 1) / BM);
+    for (int64_t i = (int64_t)blockIdx.x * NT + tid; i < n0el; i += stride) {
+        // compensated (Kahan) sum in a fixed order: up to NS * B / 32 partials
+        float g = 0.0f, comp = 0.0f;
+        for (int q0 = 0; q0 < nparts; q0 += 8) {
+            float v[8];
 #pragma unroll
-                for (int s = 0; s < 8; ++s)
-                    part[s] = s < ns ? __ldcg(p.dH0p + ((int64_t)s * B + b) * N0 + n) : 0.0f;
-                const float h = __ldcg(p.H0 + (int64_t)b * N0 + n);
+            for (int q = 0; q < 8; ++q) v[q] = q0 + q < nparts ? __ldcg(p.w0part + (int64_t)(q0 + q) * n0el + i) : 0.0f;
 #pragma unroll
-                for (int s = 0; s < 8; ++s) dz += part[s];
-                for (int s = 8; s < ns; ++s) dz += __ldcg(p.dH0p + ((int64_t)s * B + b) * N0 + n);
-                dz = h > 0.0f ? dz : 0.0f;
-            }
-            dzs[tid] = dz;
-            cp_async_wait_all();
-            __syncthreads();
-            for (int bb = grp; bb < cn; bb += NT / 32) {
-                const float z = dzs[bb];
-                if (d < D) accw = fmaf(z, Xsm[bb * D + d], accw);
-                if (d == 0) accb += z;
+            for (int q = 0; q < 8; ++q) {
+                const float yv = v[q] - comp;
+                const float tv = g + yv;
+                comp = (tv - g) - yv;
+                g = tv;
             }
         }
-        __syncthreads();
-        red[tid] = accw;
-        __syncthreads();
-        if (tid < 32) {
-            float s = 0.0f;
-            for (int g = 0; g < NT / 32; ++g) s += red[g * 32 + tid];
-            if (tid < D) {
-                const int64_t i = p.w0 + (int64_t)n * D + tid;
-                p.grad[i] = s;
-                if (upd) {
-                    const float w = w_old - p.lr * s;
-                    p.online[i] = w;
-                    if (do_sync) p.target[i] = w;
-                }
-            }
+        p.grad[i] = g;
+        if (upd) {
+            const float w = p.online[i] - p.lr * g;
+            p.online[i] = w;
+            if (do_sync) p.target[i] = w;
         }
-        __syncthreads();
-        red[tid] = accb;
-        __syncthreads();
-        if (tid == 0) {
-            float s = 0.0f;
-            for (int g = 0; g < NT / 32; ++g) s += red[g * 32];
-            const int64_t i = p.b0 + n;
-            p.grad[i] = s;
-            if (upd) {
-                const float w = b_old - p.lr * s;
-                p.online[i] = w;
-                if (do_sync) p.target[i] = w;
-            }
-        }
-        __syncthreads();
     }
     trace_.mark(3);
-    // (b) every other parameter: [w1, P) (the blob stores W0, b0 first), float4 where whole
+    // (b) every other parameter: [w1, P), float4 where whole
     const int64_t lo = p.w1, n_el = p.P - p.w1;
     const int64_t n4 = (p.nsb == 1) ? n_el / 4 : 0;
-    const int64_t stride = (int64_t)gridDim.x * NT;
     for (int64_t e = (int64_t)blockIdx.x * NT + tid; e < n4; e += stride) {
         const int64_t i = lo + 4 * e;
         const float4 g = __ldcg(reinterpret_cast<const float4 *>(p.grad + i));

@@ -81,10 +81,12 @@ def trace_main():
         dqn.train_step(rp, 128, loss)
     torch.cuda.synchronize()
     tr = dqn.debug(b.RPL_DBG_TRACE, 128).astype(np.int64)
-    t0 = min(tr[k][tr[k][:, 0] > 0][:, 0].min() for k in range(4))
-    names = ["K1 fwd", "K2 td", "K3 bwd1", "K4 bwd0+sgd"]
+    t0 = min(tr[k][tr[k][:, 0] > 0][:, 0].min() for k in range(4) if (tr[k][:, 0] > 0).any())
+    names = ["K1 fwd+td", "(unused)", "K3 bwd1", "K4 bwd0+sgd"]
     for k in range(4):
         m = tr[k][:, 0] > 0
+        if not m.any():
+            continue
         st, en = (tr[k][m, 0] - t0) / 1000.0, (tr[k][m, 1] - t0) / 1000.0
         dur = en - st
         print(f"{names[k]:12s} ctas={m.sum():4d} start [{st.min():6.2f},{st.max():6.2f}] end [{en.min():6.2f},"
