@@ -46,4 +46,16 @@ __device__ __forceinline__ void mma_3xtf32(float c[4], const uint32_t ah[4], con
     mma_tf32(c, ah[0], ah[1], ah[2], ah[3], bh[0], bh[1]);
 }
 
+// The three products into three independent accumulators (no dependent-HMMA chain inside a
+// k-step); combine small terms first with acc3_sum.
+__device__ __forceinline__ void mma_3xtf32_sep(float chh[4], float chl[4], float clh[4],
+                                               const uint32_t ah[4], const uint32_t al[4],
+                                               const uint32_t bh[2], const uint32_t bl[2])
+{
+    mma_tf32(clh, al[0], al[1], al[2], al[3], bh[0], bh[1]);
+    mma_tf32(chl, ah[0], ah[1], ah[2], ah[3], bl[0], bl[1]);
+    mma_tf32(chh, ah[0], ah[1], ah[2], ah[3], bh[0], bh[1]);
+}
+__device__ __forceinline__ float acc3_sum(float hh, float hl, float lh) { return (lh + hl) + hh; }
+
 }  // namespace rpl

@@ -730,11 +730,11 @@ __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int 
     float *As = smf, *Bs = smf + MM_SK * MM_AS;
     // the MMA accumulates 32-deep partials (4 k-steps) that are added into round-to-nearest
     // FP32 sums, so long contractions (K = 1024 at large batch) keep FP32-level accuracy
-    float c[2][4], cs[2][4];
+    float c[2][4], cl[2][4], cm[2][4], cs[2][4];   // hi*hi, hi*lo, lo*hi partials; sums
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) c[i][q] = cs[i][q] = 0.0f;
+        for (int q = 0; q < 4; ++q) c[i][q] = cl[i][q] = cm[i][q] = cs[i][q] = 0.0f;
     float rsum = 0.0f;
     for (int k0 = kb; k0 < ke; k0 += MM_SK) {
         __syncthreads();   // the previous pass / task is done with the staging buffers
@@ -757,15 +757,15 @@ __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int 
                 uint32_t bh[2], bl[2];
                 tf32_split(Bs[(k + t) * MM_BS + nc], bh[0], bl[0]);
                 tf32_split(Bs[(k + t + 4) * MM_BS + nc], bh[1], bl[1]);
-                mma_3xtf32(c[nt], ah, al, bh, bl);
+                mma_3xtf32_sep(c[nt], cl[nt], cm[nt], ah, al, bh, bl);
             }
             if ((ks & 3) == 3 || ks == ksteps - 1) {
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        cs[i][q] += c[i][q];
-                        c[i][q] = 0.0f;
+                        cs[i][q] += acc3_sum(c[i][q], cl[i][q], cm[i][q]);
+                        c[i][q] = cl[i][q] = cm[i][q] = 0.0f;
                     }
             }
         }
@@ -863,40 +863,31 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             if (nb < BM)
                 for (int e = threadIdx.x; e < (BM - nb) * XS; e += F_NT3) xs[nb * XS + e] = 0.0f;
             __syncthreads();
-            // dW0 / db0 share: C[unit k][d] = sum_b tile[b][k] xs[b][d] over the tile's rows;
-            // M = 64 units (4 m16 tiles), N = 32 (27 states + ones column), K = 32 rows
+            // dW0 / db0 share: C[unit k][d] = sum_b tile[b][k] xs[b][d] over the tile's rows
+            // (column D of xs is 1 -> db0); thread = (unit kk, 8 consecutive columns)
             float *w0p = p.w0part + ((int64_t)s * ((B + BM - 1) / BM) + m0 / BM) * (p.b0 + N0);
             {
-                const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
-                const int mt = warp & 3, np = warp >> 2;   // m16 tile, pair of n8 tiles
-                float c2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+                const int kk = threadIdx.x >> 2, d0 = 8 * (threadIdx.x & 3);
+                float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
+                for (int bb = 0; bb < BM; ++bb) {
+                    const float z = tile[bb * (BN + 4) + kk];
+                    const float4 x0 = *reinterpret_cast<const float4 *>(xs + bb * XS + d0);
+                    const float4 x1 = *reinterpret_cast<const float4 *>(xs + bb * XS + d0 + 4);
+                    acc[0] = fmaf(z, x0.x, acc[0]); acc[1] = fmaf(z, x0.y, acc[1]);
+                    acc[2] = fmaf(z, x0.z, acc[2]); acc[3] = fmaf(z, x0.w, acc[3]);
+                    acc[4] = fmaf(z, x1.x, acc[4]); acc[5] = fmaf(z, x1.y, acc[5]);
+                    acc[6] = fmaf(z, x1.z, acc[6]); acc[7] = fmaf(z, x1.w, acc[7]);
+                }
+                const int k = n0 + kk;
+                if (kk < nk) {
 #pragma unroll
-                for (int k = 0; k < BM; k += 8) {
-                    uint32_t ah[4], al[4];
-                    const int mr = 16 * mt + g;
-                    tf32_split(tile[(k + t) * (BN + 4) + mr], ah[0], al[0]);
-                    tf32_split(tile[(k + t) * (BN + 4) + mr + 8], ah[1], al[1]);
-                    tf32_split(tile[(k + t + 4) * (BN + 4) + mr], ah[2], al[2]);
-                    tf32_split(tile[(k + t + 4) * (BN + 4) + mr + 8], ah[3], al[3]);
-#pragma unroll
-                    for (int nt = 0; nt < 2; ++nt) {
-                        const int nc = 16 * np + 8 * nt + g;
-                        uint32_t bh[2], bl[2];
-                        tf32_split(xs[(k + t) * XS + nc], bh[0], bl[0]);
-                        tf32_split(xs[(k + t + 4) * XS + nc], bh[1], bl[1]);
-                        mma_3xtf32(c2[nt], ah, al, bh, bl);
+                    for (int q = 0; q < 8; ++q) {
+                        const int d = d0 + q;
+                        if (d < D) w0p[p.w0 + (int64_t)k * D + d] = acc[q];
+                        else if (d == D) w0p[p.b0 + k] = acc[q];
                     }
                 }
-#pragma unroll
-                for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int kk = 16 * mt + g + 8 * (q >> 1), d = 16 * np + 8 * nt + 2 * t + (q & 1);
-                        const int k = n0 + kk;
-                        if (kk >= nk) continue;
-                        if (d < D) w0p[p.w0 + (int64_t)k * D + d] = c2[nt][q];
-                        else if (d == D) w0p[p.b0 + k] = c2[nt][q];
-                    }
             }
             trace_.mark(7);
         } else {
@@ -1006,15 +997,15 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
     // (a) W0, b0: the fixed-order sum of the (split, batch tile) partials written by K3
     const int64_t n0el = p.w1;                  // W0 and b0 lead the blob
     const int nparts = p.NS * ((B + BM - 1) / BM);
-    for (int64_t i = (int64_t)blockIdx.x * NT + tid; i < n0el; i += stride) {
-        // compensated (Kahan) sum in a fixed order: up to NS * B / 32 partials
+    for (int64_t i = (int64_t)tid * gridDim.x + blockIdx.x; i < n0el; i += stride) {
+        // compensated (Kahan) sum in a fixed order: up to NS * B / 32 partials, 32 in flight
         float g = 0.0f, comp = 0.0f;
-        for (int q0 = 0; q0 < nparts; q0 += 8) {
-            float v[8];
+        for (int q0 = 0; q0 < nparts; q0 += 32) {
+            float v[32];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) v[q] = q0 + q < nparts ? __ldcg(p.w0part + (int64_t)(q0 + q) * n0el + i) : 0.0f;
+            for (int q = 0; q < 32; ++q) v[q] = q0 + q < nparts ? __ldcg(p.w0part + (int64_t)(q0 + q) * n0el + i) : 0.0f;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < 32; ++q) {
                 const float yv = v[q] - comp;
                 const float tv = g + yv;
                 comp = (tv - g) - yv;
