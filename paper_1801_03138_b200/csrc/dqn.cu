@@ -589,6 +589,7 @@ struct rpl_dqn {
     };
     std::vector<GraphEntry> graphs;
     bool use_graphs = true;
+    bool use_pdl = false;                  // programmatic dependent launch inside the graph
     unsigned long long *trace = nullptr;   // RPL_TRACE=1: per-CTA timestamps of the fast kernels
     // data parallel
     void *comm = nullptr;
@@ -792,6 +793,10 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
               d->woff[1] % 4 == 0 && !(path && strcmp(path, "generic") == 0);
     const char *ng = getenv("RPL_NO_GRAPH");
     d->use_graphs = !(ng && ng[0] == '1');
+    // programmatic dependent launch measured slower on this structure (dependent CTAs that
+    // start early compete for SM slots); opt in with RPL_PDL=1
+    const char *np = getenv("RPL_PDL");
+    d->use_pdl = np && np[0] == '1';
     ok = ok && dalloc(d, &d->step_dev, 1) && dalloc(d, &d->sync_flag, 1);
     const char *tr = getenv("RPL_TRACE");
     if (ok && tr && tr[0] == '1') {
@@ -988,25 +993,46 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
 }
 
 // the four fast-path kernels, enqueued on `st`
+// launch with programmatic dependent launch: the kernel may start while its predecessor is
+// finishing; it prefetches step-invariant data, then waits (griddepcontrol.wait) before
+// touching the predecessor's outputs
+template <class K>
+static cudaError_t launch_pdl(K kernel, int grid, int block, size_t smem, cudaStream_t st, bool pdl,
+                              const FastArgs &p)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, p);
+}
+
+// the fast-path kernels, enqueued on `st`
 static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
 {
     const int nbt = (p.B + F_BT - 1) / F_BT;
     const int k1_tasks = p.nets * nbt * p.nut;
     const int g1 = std::min(k1_tasks, d->sms);
     const size_t sm1 = fast_fwd_smem(d, p.UT);
-    fast_fwd_fn(d)<<<g1, F_NT1, sm1, st>>>(p);
-    cudaError_t e = cudaGetLastError();
+    const bool pdl = d->use_pdl;
+    cudaError_t e = launch_pdl(fast_fwd_fn(d), g1, F_NT1, sm1, st, false, p);
     if (e != cudaSuccess) return e;
-    fast_td_kernel<<<std::min(p.B, 4 * d->sms), NT, fast_td_smem(d), st>>>(p);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    e = launch_pdl(fast_td_kernel, std::min(p.B, 4 * d->sms), NT, fast_td_smem(d), st, pdl, p);
+    if (e != cudaSuccess) return e;
     const int n_w = ((p.N1 + BM - 1) / BM) * ((p.N0 + BN - 1) / BN) * p.nsb;
     const int n_h = ((p.B + BM - 1) / BM) * ((p.N0 + BN - 1) / BN) * p.NS;
     const int hd_passes = p.dueling ? (p.A + 7) / 8 : (p.J + 7) / 8;
     const int n_hd = (((p.N1 + HD_U - 1) / HD_U) * hd_passes + 1) * p.nsb;
-    fast_bwd1_kernel<<<std::min(n_w + n_h + n_hd, 4 * d->sms), F_NT3, K3_SMEM_FLOATS * sizeof(float), st>>>(p);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    fast_bwd0_sgd_kernel<<<d->sms, NT, 0, st>>>(p);
-    return cudaGetLastError();
+    e = launch_pdl(fast_bwd1_kernel, std::min(n_w + n_h + n_hd, 4 * d->sms), F_NT3,
+                   K3_SMEM_FLOATS * sizeof(float), st, pdl, p);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(fast_bwd0_sgd_kernel, d->sms, NT, 0, st, pdl, p);
 }
 
 static int grid_for(const rpl_dqn *d, const TrainArgs &p)

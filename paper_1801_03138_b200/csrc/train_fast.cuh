@@ -95,6 +95,11 @@ struct CtaTrace {
     }
 };
 
+// programmatic dependent launch: let the next kernel of the graph start early / wait for the
+// previous one's results (no-ops when the launch is not programmatic)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
 {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -153,6 +158,7 @@ template <int UT, int KD, int KN0, int KJ>
 __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constant__ FastArgs p)
 {
     CtaTrace trace_(p.trace, 0);
+    pdl_trigger();
     extern __shared__ float4 smem4[];
     float *sm = reinterpret_cast<float *>(smem4);
     constexpr int NW = F_NT1 / 32;
@@ -384,8 +390,11 @@ __global__ void __launch_bounds__(NT) fast_td_kernel(const __grid_constant__ Fas
         const int64_t t = *p.step_dev + 1;
         *p.sync_flag = (p.sync_period > 0 && t % p.sync_period == 0) ? 1 : 0;
     }
-    // the head weights are reused for every sample of this CTA: stream them in once
+    // the head weights are reused for every sample of this CTA: stream them in once (they are
+    // step-invariant, so before waiting for the forward kernel)
+    pdl_trigger();
     cp_async_row(Whs, p.online + p.wh, J * HS, tid, NT);
+    pdl_wait();
     for (int b = blockIdx.x; b < B; b += gridDim.x) {
         __syncthreads();
         cp_async_row(h1s, p.H1 + (int64_t)b * N1, N1, tid, NT);
@@ -791,6 +800,8 @@ constexpr int K3_SMEM_FLOATS = K3_DH_FLOATS > K3_HD_FLOATS ? K3_DH_FLOATS : K3_H
 
 __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant__ FastArgs p)
 {
+    pdl_trigger();
+    pdl_wait();
     CtaTrace trace_(p.trace, 2);
     extern __shared__ float4 smem4[];
     float *k3raw = reinterpret_cast<float *>(smem4);   // K3_SMEM_FLOATS
@@ -976,6 +987,7 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant__ FastArgs p)
 {
+    pdl_wait();
     CtaTrace trace_(p.trace, 3);
     __shared__ float red[NT / 32];
     const int tid = threadIdx.x;
@@ -997,7 +1009,7 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
     // (a) W0, b0: the fixed-order sum of the (split, batch tile) partials written by K3
     const int64_t n0el = p.w1;                  // W0 and b0 lead the blob
     const int nparts = p.NS * ((B + BM - 1) / BM);
-    for (int64_t i = (int64_t)tid * gridDim.x + blockIdx.x; i < n0el; i += stride) {
+    for (int64_t i = (int64_t)blockIdx.x * NT + tid; i < n0el; i += stride) {
         // compensated (Kahan) sum in a fixed order: up to NS * B / 32 partials, 32 in flight
         float g = 0.0f, comp = 0.0f;
         for (int q0 = 0; q0 < nparts; q0 += 32) {

@@ -37,9 +37,18 @@ def full(path):
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, data = rows[0], rows[1], rows[2:]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
+             "msecond": 1e6, "second": 1e9}
     res = []
     for r in data:
-        d = dict(zip(hdr, r))
+        d = {}
+        for h, u, v in zip(hdr, units, r):
+            if u in scale:
+                try:
+                    v = str(float(v.replace(",", "")) * scale[u])   # bytes / nanoseconds
+                except ValueError:
+                    pass
+            d[h] = v
         res.append(d)
     return res
 
