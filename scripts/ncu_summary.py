@@ -38,7 +38,8 @@ def full(path):
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
-             "msecond": 1e6, "second": 1e9}
+             "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9,
+             "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9, "Kbyte": 1e3}
     res = []
     for r in data:
         d = {}
@@ -72,6 +73,7 @@ def main():
                   f"{d.get('sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active', '-')} |")
             traffic.setdefault(name, []).append(rd + wr)
     json.dump({k: sum(v) / len(v) for k, v in traffic.items()}, open("/tmp/traffic_by_kernel.json", "w"), indent=1)
+    print("\n(DRAM bytes are per launch from `ncu --set full`, which flushes caches between kernels: cold)")
 
 
 if __name__ == "__main__":
