@@ -711,9 +711,10 @@ static size_t fast_td_smem(const rpl_dqn *d)
 // split-K count of dH0 = dZ1 W1 so that K3 has about one task per SM
 static int fast_ns(const rpl_dqn *d, int B)
 {
-    const int n_w = ((d->N[1] + BM - 1) / BM) * ((d->N[0] + BN - 1) / BN) * ((B + 511) / 512);
-    const int tiles = ((B + BM - 1) / BM) * ((d->N[0] + BN - 1) / BN);
-    int want = (d->sms - n_w) / tiles;
+    // K3 runs two CTAs per SM: aim at ~2 tasks per SM in total
+    const int n_w = ((d->N[1] + BM - 1) / BM) * ((d->N[0] + K3N - 1) / K3N) * ((B + 511) / 512);
+    const int tiles = ((B + BM - 1) / BM) * ((d->N[0] + K3N - 1) / K3N);
+    int want = (2 * d->sms - n_w) / tiles;
     int ns = 1;
     while (ns * 2 <= want && ns * 2 * 32 <= d->N[1]) ns *= 2;
     return ns;
@@ -1025,11 +1026,11 @@ static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
     if (e != cudaSuccess) return e;
     e = launch_pdl(fast_td_kernel, std::min(p.B, 4 * d->sms), NT, fast_td_smem(d), st, pdl, p);
     if (e != cudaSuccess) return e;
-    const int n_w = ((p.N1 + BM - 1) / BM) * ((p.N0 + BN - 1) / BN) * p.nsb;
-    const int n_h = ((p.B + BM - 1) / BM) * ((p.N0 + BN - 1) / BN) * p.NS;
+    const int n_w = ((p.N1 + BM - 1) / BM) * ((p.N0 + K3N - 1) / K3N) * p.nsb;
+    const int n_h = ((p.B + BM - 1) / BM) * ((p.N0 + K3N - 1) / K3N) * p.NS;
     const int hd_passes = p.dueling ? (p.A + 7) / 8 : (p.J + 7) / 8;
     const int n_hd = (((p.N1 + HD_U - 1) / HD_U) * hd_passes + 1) * p.nsb;
-    e = launch_pdl(fast_bwd1_kernel, std::min(n_w + n_h + n_hd, 4 * d->sms), F_NT3,
+    e = launch_pdl(fast_bwd1_kernel, std::min(n_w + n_h + n_hd, 2 * d->sms), F_NT3,
                    K3_SMEM_FLOATS * sizeof(float), st, pdl, p);
     if (e != cudaSuccess) return e;
     return launch_pdl(fast_bwd0_sgd_kernel, d->sms, NT, 0, st, pdl, p);

@@ -77,13 +77,18 @@ __device__ __forceinline__ unsigned long long gtimer()
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-// records the CTA's start / end time when tracing is on (RPL_TRACE=1)
+// records the CTA's start / end %globaltimer (ns) and phase marks as SM-clock cycles since
+// the CTA started when tracing is on (RPL_TRACE=1)
 struct CtaTrace {
     unsigned long long *slot;
+    long long c0;
     __device__ CtaTrace(unsigned long long *tr, int kernel)
-        : slot(tr && threadIdx.x == 0 ? tr + 8 * ((size_t)kernel * 2048 + blockIdx.x) : nullptr)
+        : slot(tr && threadIdx.x == 0 ? tr + 8 * ((size_t)kernel * 2048 + blockIdx.x) : nullptr), c0(0)
     {
-        if (slot) slot[0] = gtimer();
+        if (slot) {
+            slot[0] = gtimer();
+            c0 = clock64();
+        }
     }
     __device__ ~CtaTrace()
     {
@@ -91,7 +96,7 @@ struct CtaTrace {
     }
     __device__ void mark(int i)
     {
-        if (slot) slot[i] = gtimer();
+        if (slot) slot[i] = (unsigned long long)(clock64() - c0);
     }
 };
 
@@ -684,8 +689,9 @@ __device__ __forceinline__ void gemm3_tile(const Opnd &a, const Opnd &b, int m0,
 // whole 16-byte chunks (all dims here are multiples of 4), missing chunks are zero-filled.
 // ------------------------------------------------------------------------------------------
 constexpr int MM_T = 256;
+constexpr int K3N = 32;                      // K3 tile columns (32 x 32 tiles: 2 CTAs / SM)
 constexpr int MM_SK = 128;                   // contraction per pass
-constexpr int MM_AS = BM + 4, MM_BS = BN + 4;
+constexpr int MM_AS = BM + 4, MM_BS = K3N + 4;
 constexpr int MM_FLOATS = MM_SK * (MM_AS + MM_BS);
 
 __device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, bool valid)
@@ -739,16 +745,17 @@ __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int 
     float *As = smf, *Bs = smf + MM_SK * MM_AS;
     // the MMA accumulates 32-deep partials (4 k-steps) that are added into round-to-nearest
     // FP32 sums, so long contractions (K = 1024 at large batch) keep FP32-level accuracy
-    float c[2][4], cl[2][4], cm[2][4], cs[2][4];   // hi*hi, hi*lo, lo*hi partials; sums
+    constexpr int NT8 = K3N / 32;                 // n8 tiles per warp (warps: 2 m16 x 4 n)
+    float c[NT8][4], cl[NT8][4], cm[NT8][4], cs[NT8][4];   // hi*hi, hi*lo, lo*hi partials; sums
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < NT8; ++i)
 #pragma unroll
         for (int q = 0; q < 4; ++q) c[i][q] = cl[i][q] = cm[i][q] = cs[i][q] = 0.0f;
     float rsum = 0.0f;
     for (int k0 = kb; k0 < ke; k0 += MM_SK) {
         __syncthreads();   // the previous pass / task is done with the staging buffers
         mm_stage<kARc, BM, MM_AS>(As, a, m0, k0, ke, tid);
-        mm_stage<kBRc, BN, MM_BS>(Bs, b, n0, k0, ke, tid);
+        mm_stage<kBRc, K3N, MM_BS>(Bs, b, n0, k0, ke, tid);
         cp_async_wait_all();
         __syncthreads();
         const int ksteps = (min(MM_SK, ke - k0) + 7) / 8;
@@ -761,8 +768,8 @@ __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int 
             tf32_split(As[(k + t + 4) * MM_AS + mr], ah[2], al[2]);
             tf32_split(As[(k + t + 4) * MM_AS + mr + 8], ah[3], al[3]);
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                const int nc = 16 * wn + 8 * nt + g;
+            for (int nt = 0; nt < NT8; ++nt) {
+                const int nc = (K3N / 4) * wn + 8 * nt + g;
                 uint32_t bh[2], bl[2];
                 tf32_split(Bs[(k + t) * MM_BS + nc], bh[0], bl[0]);
                 tf32_split(Bs[(k + t + 4) * MM_BS + nc], bh[1], bl[1]);
@@ -770,7 +777,7 @@ __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int 
             }
             if ((ks & 3) == 3 || ks == ksteps - 1) {
 #pragma unroll
-                for (int i = 0; i < 2; ++i)
+                for (int i = 0; i < NT8; ++i)
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         cs[i][q] += acc3_sum(c[i][q], cl[i][q], cm[i][q]);
@@ -784,10 +791,10 @@ __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int 
         }
     }
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+    for (int nt = 0; nt < NT8; ++nt)
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            epi(m0 + 16 * wm + g + 8 * (q >> 1), n0 + 16 * wn + 8 * nt + 2 * t + (q & 1), cs[nt][q]);
+            epi(m0 + 16 * wm + g + 8 * (q >> 1), n0 + (K3N / 4) * wn + 8 * nt + 2 * t + (q & 1), cs[nt][q]);
     if (want_rowsum && tid < BM) rs(m0 + tid, rsum);
 }
 
@@ -795,7 +802,7 @@ constexpr int HD_U = 64;                                   // head-gradient unit
 constexpr int K3_HD_FLOATS = 128 * HD_U + 128 * F_MAXJ + 4 * HD_U * 8;   // head-gradient staging
 constexpr int K3_GEMM_FLOATS = MM_FLOATS;
 // + the dH0 tile and the batch tile's states (D <= 64)
-constexpr int K3_DH_FLOATS = K3_GEMM_FLOATS + BM * (BN + 4) + BM * 36 + BM * BN;
+constexpr int K3_DH_FLOATS = K3_GEMM_FLOATS + BM * (K3N + 4) + BM * 36 + BM * K3N;
 constexpr int K3_SMEM_FLOATS = K3_DH_FLOATS > K3_HD_FLOATS ? K3_DH_FLOATS : K3_HD_FLOATS;
 
 __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant__ FastArgs p)
@@ -806,9 +813,9 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
     extern __shared__ float4 smem4[];
     float *k3raw = reinterpret_cast<float *>(smem4);   // K3_SMEM_FLOATS
     const int N0 = p.N0, N1 = p.N1, B = p.B, J = p.J;
-    const int wmt = (N1 + BM - 1) / BM, wnt = (N0 + BN - 1) / BN;
+    const int wmt = (N1 + BM - 1) / BM, wnt = (N0 + K3N - 1) / K3N;
     const int n_w = wmt * wnt * p.nsb;
-    const int hmt = (B + BM - 1) / BM, hnt = (N0 + BN - 1) / BN;
+    const int hmt = (B + BM - 1) / BM, hnt = (N0 + K3N - 1) / K3N;
     const int n_h = hmt * hnt * p.NS;
     // head-weight gradient tasks: (128-unit tile) x (pass of <= 8 head rows), + 1 bias task
     const int hd_passes = p.dueling ? (p.A + 7) / 8 : (J + 7) / 8;
@@ -819,7 +826,7 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
         if (t < n_w) {
             // dW1[u][k] = sum_b dZ1[b][u] H0[b][k]  (+ db1[u] = sum_b dZ1[b][u])
             const int s = t / (wmt * wnt), rem = t % (wmt * wnt);
-            const int m0 = (rem / wnt) * BM, n0 = (rem % wnt) * BN;
+            const int m0 = (rem / wnt) * BM, n0 = (rem % wnt) * K3N;
             const int kb = s * p.bsplit, ke = min(B, kb + p.bsplit);
             float *gp = p.gpart + (int64_t)s * p.P;
             const Opnd a{p.dZ1, N1, N1}, bo{p.H0, N0, N0};
@@ -835,22 +842,22 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             // dH0 partial [s][b][k] = sum_{u in split s} dZ1[b][u] W1[u][k]
             const int u = t - n_w;
             const int s = u / (hmt * hnt), rem = u % (hmt * hnt);
-            const int m0 = (rem / hnt) * BM, n0 = (rem % hnt) * BN;
+            const int m0 = (rem / hnt) * BM, n0 = (rem % hnt) * K3N;
             const int chunk = (N1 + p.NS - 1) / p.NS;
             const int kb = s * chunk, ke = min(N1, kb + chunk);
             // the partial dH0 tile stays in shared memory; masked by ReLU'(z0) it gives this
             // (split, batch tile)'s share of dW0 = dZ0^T X and db0 = sum_b dZ0 (the mask
             // distributes over the split-K sum), reduced in K4 in a fixed order
-            float *tile = k3raw + K3_GEMM_FLOATS;          // [BM][BN + 4] partial dH0
-            float *xs = tile + BM * (BN + 4);              // [BM][XS] states, column D = 1
+            float *tile = k3raw + K3_GEMM_FLOATS;          // [BM][K3N + 4] partial dH0
+            float *xs = tile + BM * (K3N + 4);              // [BM][XS] states, column D = 1
             constexpr int XS = 36;
             const Opnd a{p.dZ1, N1, B}, bo{p.online + p.w1, N0, N0};
-            auto epi = [&](int m, int n, float v) { tile[(m - m0) * (BN + 4) + (n - n0)] = v; };
+            auto epi = [&](int m, int n, float v) { tile[(m - m0) * (K3N + 4) + (n - n0)] = v; };
             gemm_mma_tile<false, true>(a, bo, m0, n0, kb, ke, epi, false, NoRowsum{}, k3raw);
             __syncthreads();
             trace_.mark(5);
-            const int D = p.D, nb = min(BM, B - m0), nk = min(BN, N0 - n0);
-            float *h0t = xs + BM * XS;                     // [BM][BN] H0 of the tile (ReLU mask)
+            const int D = p.D, nb = min(BM, B - m0), nk = min(K3N, N0 - n0);
+            float *h0t = xs + BM * XS;                     // [BM][K3N] H0 of the tile (ReLU mask)
             for (int e = threadIdx.x; e < nb * D; e += F_NT3) {
                 const int bb = e / D, d = e - bb * D;
                 cp_async4(xs + bb * XS + d, p.Xs + (int64_t)m0 * D + e);
@@ -861,39 +868,39 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             }
             for (int e = threadIdx.x; e < nb * (nk / 4); e += F_NT3) {
                 const int bb = e / (nk / 4), q = e % (nk / 4);
-                cp_async16(h0t + bb * BN + 4 * q, p.H0 + (int64_t)(m0 + bb) * N0 + n0 + 4 * q);
+                cp_async16(h0t + bb * K3N + 4 * q, p.H0 + (int64_t)(m0 + bb) * N0 + n0 + 4 * q);
             }
             cp_async_wait_all();
             __syncthreads();
             trace_.mark(6);
-            for (int e = threadIdx.x; e < BM * BN; e += F_NT3) {
-                const int bb = e / BN, kk = e % BN;
-                const bool on = bb < nb && kk < nk && h0t[bb * BN + kk] > 0.0f;
-                if (!on) tile[bb * (BN + 4) + kk] = 0.0f;
+            for (int e = threadIdx.x; e < BM * K3N; e += F_NT3) {
+                const int bb = e / K3N, kk = e % K3N;
+                const bool on = bb < nb && kk < nk && h0t[bb * K3N + kk] > 0.0f;
+                if (!on) tile[bb * (K3N + 4) + kk] = 0.0f;
             }
             if (nb < BM)
                 for (int e = threadIdx.x; e < (BM - nb) * XS; e += F_NT3) xs[nb * XS + e] = 0.0f;
             __syncthreads();
+            trace_.mark(2);
             // dW0 / db0 share: C[unit k][d] = sum_b tile[b][k] xs[b][d] over the tile's rows
             // (column D of xs is 1 -> db0); thread = (unit kk, 8 consecutive columns)
             float *w0p = p.w0part + ((int64_t)s * ((B + BM - 1) / BM) + m0 / BM) * (p.b0 + N0);
             {
-                const int kk = threadIdx.x >> 2, d0 = 8 * (threadIdx.x & 3);
-                float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                // thread = (unit kk, 4 consecutive columns): 8 threads per unit
+                const int kk = threadIdx.x >> 3, d0 = 4 * (threadIdx.x & 7);
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 8
                 for (int bb = 0; bb < BM; ++bb) {
-                    const float z = tile[bb * (BN + 4) + kk];
+                    const float z = tile[bb * (K3N + 4) + kk];
                     const float4 x0 = *reinterpret_cast<const float4 *>(xs + bb * XS + d0);
-                    const float4 x1 = *reinterpret_cast<const float4 *>(xs + bb * XS + d0 + 4);
                     acc[0] = fmaf(z, x0.x, acc[0]); acc[1] = fmaf(z, x0.y, acc[1]);
                     acc[2] = fmaf(z, x0.z, acc[2]); acc[3] = fmaf(z, x0.w, acc[3]);
-                    acc[4] = fmaf(z, x1.x, acc[4]); acc[5] = fmaf(z, x1.y, acc[5]);
-                    acc[6] = fmaf(z, x1.z, acc[6]); acc[7] = fmaf(z, x1.w, acc[7]);
                 }
                 const int k = n0 + kk;
+                trace_.mark(3);
                 if (kk < nk) {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
+                    for (int q = 0; q < 4; ++q) {
                         const int d = d0 + q;
                         if (d < D) w0p[p.w0 + (int64_t)k * D + d] = acc[q];
                         else if (d == D) w0p[p.b0 + k] = acc[q];

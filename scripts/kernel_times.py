@@ -95,8 +95,8 @@ def trace_main():
         for ph in range(2, 8):
             mm = m & (tr[k][:, ph] > 0)
             if mm.any():
-                rel = (tr[k][mm, ph] - tr[k][mm, 0]) / 1000.0
-                print(f"    mark {ph}: {rel.mean():6.2f} us after CTA start (max {rel.max():6.2f})")
+                rel = tr[k][mm, ph] / 1965.0   # SM cycles -> us at the 1965 MHz max clock
+                print(f"    mark {ph}: {rel.mean():6.2f} us after CTA start (max {rel.max():6.2f}, n={mm.sum()})")
 
 
 if __name__ == "__main__":
