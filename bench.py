@@ -267,7 +267,7 @@ def run_ours(a, batch, first_line=True):
     def add_dev(i):
         if k:
             j = (i % 256) * k
-            rp.add(**{kk: v[j:j + k] for kk, v in pool_d.items()})
+            rp.add(**{kk: v[j:j + k] for kk, v in pool_d.items()}, defer=True)
 
     launches0 = binding.kernel_launches()
     for i in range(W):

@@ -45,7 +45,8 @@ enum {
     RPL_ESTATE = -7      /* call not valid in the handle's state                           */
 };
 
-enum { RPL_HOST = 0, RPL_DEVICE = 1 };           /* where replay_add's inputs live        */
+/* where replay_add's inputs live (RPL_DEVICE_DEFER: device, ring write may be deferred) */
+enum { RPL_HOST = 0, RPL_DEVICE = 1, RPL_DEVICE_DEFER = 2 };
 enum { RPL_ONLINE = 0, RPL_TARGET = 1, RPL_GRAD = 2 };  /* which parameter vector          */
 
 typedef struct rpl_replay rpl_replay;   /* opaque */
@@ -83,7 +84,15 @@ int replay_destroy(rpl_replay *replay);
  * pinned staging before return (the caller may reuse them at once); one H2D copy of
  * k*(8*state_dim+9) bytes is counted in replay_state's h2d_bytes -- the only PCIe
  * traffic of the method.  mem = RPL_DEVICE: device pointers that must stay
- * valid until the stream reaches the insert.
+ * valid until the stream reaches the insert.  mem = RPL_DEVICE_DEFER: device pointers
+ * whose contents must stay valid AND unchanged until the next call on this replay or the
+ * next dqn_train_step on it has been reached by the stream.
+ * Deferred insert (HOST and DEVICE_DEFER, k <= 4096): the ring write is not a separate
+ * kernel; the next fast-path dqn_train_step performs it inside its first kernel, which
+ * reads any sampled slot of this insert straight from its source ("read-through"), so
+ * the sampled batch is identical.  Any other call on the replay (add, sample, gather,
+ * rpl_check) first enqueues the write as an insert kernel.  Observable state (cursor,
+ * size, total, and every sample / gather) is the same as with an immediate insert.
  * Errors: EINVAL (k < 0, k > capacity, k > max_host_add for HOST, null pointer with
  * k > 0), ECORRUPT (HOST done[j] > 1; nothing written).  k = 0 is a no-op.
  * A device-sourced done[j] > 1 is written as 1 and raises the sticky ECORRUPT flag. */

@@ -23,7 +23,7 @@ LIB_PATH = os.path.join(_PKG, "lib", "libingpu_replay.so")
 RPL_OK, RPL_NOT_READY = 0, 1
 RPL_EINVAL, RPL_ENOMEM, RPL_ECORRUPT, RPL_ENUMERIC = -1, -2, -3, -4
 RPL_ECUDA, RPL_ENCCL, RPL_ESTATE = -5, -6, -7
-RPL_HOST, RPL_DEVICE = 0, 1
+RPL_HOST, RPL_DEVICE, RPL_DEVICE_DEFER = 0, 1, 2
 RPL_ONLINE, RPL_TARGET, RPL_GRAD = 0, 1, 2
 (RPL_DBG_IDX, RPL_DBG_S, RPL_DBG_S_NEXT, RPL_DBG_A, RPL_DBG_R, RPL_DBG_DONE, RPL_DBG_Q,
  RPL_DBG_QT_NEXT, RPL_DBG_QO_NEXT, RPL_DBG_Y, RPL_DBG_ASTAR, RPL_DBG_H, RPL_DBG_LOSS,
@@ -167,8 +167,10 @@ class Replay:
     def handle(self):
         return self._h
 
-    def add(self, s, a, r, s_next, done) -> int:
-        """replay_add: numpy / CPU tensors -> RPL_HOST; CUDA tensors -> RPL_DEVICE."""
+    def add(self, s, a, r, s_next, done, defer: bool = False) -> int:
+        """replay_add: numpy / CPU tensors -> RPL_HOST; CUDA tensors -> RPL_DEVICE, or
+        RPL_DEVICE_DEFER with defer=True (the tensors must stay unchanged until the next
+        call on this replay / the next train step on it; a reference is held until then)."""
         torch = _torch()
         if isinstance(s, torch.Tensor) and s.is_cuda:
             ts = [s.contiguous(), a.contiguous(), r.contiguous(), s_next.contiguous(),
@@ -176,7 +178,10 @@ class Replay:
             assert ts[0].dtype == torch.float32 and ts[1].dtype == torch.int32
             assert ts[2].dtype == torch.float32 and ts[4].dtype == torch.uint8
             k = ts[1].numel()
-            return _ok(_L.replay_add(self._h, k, *[_dptr(t) for t in ts], RPL_DEVICE))
+            rc = _ok(_L.replay_add(self._h, k, *[_dptr(t) for t in ts],
+                                   RPL_DEVICE_DEFER if defer else RPL_DEVICE))
+            self._deferred = ts if defer else None
+            return rc
         arrs = [np.ascontiguousarray(np.asarray(s), np.float32),
                 np.ascontiguousarray(np.asarray(a), np.int32),
                 np.ascontiguousarray(np.asarray(r), np.float32),

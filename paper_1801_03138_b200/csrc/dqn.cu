@@ -585,7 +585,10 @@ struct rpl_dqn {
         const rpl_replay *rp;
         int B;
         float *loss;
+        cudaGraph_t graph;          // kept alive: k1 is one of its nodes
         cudaGraphExec_t exec;
+        cudaGraphNode_t k1;         // K1's node (its args carry the deferred insert)
+        FastArgs k1args;            // the args K1's node currently holds
     };
     std::vector<GraphEntry> graphs;
     bool use_graphs = true;
@@ -728,7 +731,10 @@ extern "C" int dqn_destroy(rpl_dqn *d)
     cudaSetDevice(d->device);
     cudaStreamSynchronize(d->stream);
     if (d->comm && g_nccl.destroy) g_nccl.destroy(d->comm);
-    for (auto &g : d->graphs) cudaGraphExecDestroy(g.exec);
+    for (auto &g : d->graphs) {
+        cudaGraphExecDestroy(g.exec);
+        cudaGraphDestroy(g.graph);
+    }
     if (d->cap_stream) cudaStreamDestroy(d->cap_stream);
     for (void *p : d->allocs) cudaFree(p);
     delete d;
@@ -991,6 +997,19 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.apply_update = apply;
     p.err = d->err;
     p.trace = d->trace;
+    p.capacity = rp->ring.capacity;
+    const rpl_replay::Pending &q = rp->pend;
+    if (q.k > 0) {   // consumed by this step's K1 (dqn_train_step clears it)
+        p.pend_k = (int)q.k;
+        p.pend_cur = q.cursor;
+        p.pend_size = (uint64_t)q.new_size;
+        p.pend_s = q.s;
+        p.pend_s2 = q.s2;
+        p.pend_r = q.r;
+        p.pend_a = q.a;
+        p.pend_done = q.done;
+        p.pend_err = rp->err_dev;
+    }
 }
 
 // the four fast-path kernels, enqueued on `st`
@@ -1067,33 +1086,72 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
     const int do_sync = d->cfg.sync_period > 0 && t % d->cfg.sync_period == 0;
     const bool dp = d->comm != nullptr && d->world > 1;
     cudaError_t e = cudaSuccess;
+    // a deferred insert is consumed by the fast path's K1 on the shared stream; otherwise it
+    // is written now by the insert kernel
+    if (!d->fast || rp->stream != d->stream) {
+        if (int rc = replay_flush(rp)) {
+            if (prev >= 0) cudaSetDevice(prev);
+            return rc;
+        }
+    }
     if (d->fast) {
         FastArgs fp;
         fill_fast(d, rp, batch, dp ? nullptr : loss_dev, dp ? 0 : 1, fp);
+        rp->pend.k = 0;
         if (d->use_graphs) {
-            cudaGraphExec_t exec = nullptr;
+            rpl_dqn::GraphEntry *ge = nullptr;
             float *lkey = dp ? nullptr : loss_dev;
             for (auto &g : d->graphs)
-                if (g.rp == rp && g.B == batch && g.loss == lkey) exec = g.exec;
-            if (!exec) {
+                if (g.rp == rp && g.B == batch && g.loss == lkey) ge = &g;
+            if (!ge) {
                 cudaGraph_t graph = nullptr;
+                cudaGraphExec_t exec = nullptr;
+                cudaGraphNode_t k1 = nullptr;
                 e = cudaStreamBeginCapture(d->cap_stream, cudaStreamCaptureModeThreadLocal);
                 if (e == cudaSuccess) {
                     cudaError_t e2 = fast_enqueue(d, fp, d->cap_stream);
                     e = cudaStreamEndCapture(d->cap_stream, &graph);
                     if (e2 != cudaSuccess) e = e2;
                 }
+                if (e == cudaSuccess) {
+                    size_t n = 0;
+                    e = cudaGraphGetNodes(graph, nullptr, &n);
+                    std::vector<cudaGraphNode_t> nodes(n);
+                    if (e == cudaSuccess && n) e = cudaGraphGetNodes(graph, nodes.data(), &n);
+                    for (size_t i = 0; e == cudaSuccess && i < n && !k1; ++i) {
+                        cudaGraphNodeType ty;
+                        cudaKernelNodeParams kp = {};
+                        if (cudaGraphNodeGetType(nodes[i], &ty) == cudaSuccess &&
+                            ty == cudaGraphNodeTypeKernel &&
+                            cudaGraphKernelNodeGetParams(nodes[i], &kp) == cudaSuccess &&
+                            kp.func == (void *)fast_fwd_fn(d))
+                            k1 = nodes[i];
+                    }
+                    if (e == cudaSuccess && !k1) e = cudaErrorInvalidValue;
+                }
                 if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
-                if (graph) cudaGraphDestroy(graph);
                 if (e == cudaSuccess) {
                     if (d->graphs.size() >= 16) {
                         cudaGraphExecDestroy(d->graphs.front().exec);
+                        cudaGraphDestroy(d->graphs.front().graph);
                         d->graphs.erase(d->graphs.begin());
                     }
-                    d->graphs.push_back({rp, batch, lkey, exec});
+                    d->graphs.push_back({rp, batch, lkey, graph, exec, k1, fp});
+                    ge = &d->graphs.back();
+                } else if (graph) {
+                    cudaGraphDestroy(graph);
                 }
+            } else if (memcmp(&ge->k1args, &fp, sizeof fp) != 0) {
+                // only K1's args change between replays (the deferred insert)
+                cudaKernelNodeParams kp = {};
+                e = cudaGraphKernelNodeGetParams(ge->k1, &kp);
+                void *args[] = {&fp};
+                kp.kernelParams = args;
+                kp.extra = nullptr;
+                if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(ge->exec, ge->k1, &kp);
+                if (e == cudaSuccess) ge->k1args = fp;
             }
-            if (e == cudaSuccess) e = cudaGraphLaunch(exec, d->stream);
+            if (e == cudaSuccess) e = cudaGraphLaunch(ge->exec, d->stream);
         } else {
             e = fast_enqueue(d, fp, d->stream);
         }
@@ -1287,6 +1345,7 @@ extern "C" int rpl_check(void *handle, int kind)
     cudaStream_t st;
     uint32_t *err;
     if (kind == 0) {
+        if (int rc = replay_flush((rpl_replay *)handle)) return rc;
         st = ((rpl_replay *)handle)->stream;
         err = ((rpl_replay *)handle)->err_dev;
     } else {

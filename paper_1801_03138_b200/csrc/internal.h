@@ -73,11 +73,26 @@ struct rpl_replay {
     // device control block read by graph-replayed train steps: [0] sampler events consumed,
     // [1] filled size (kept equal to the host mirror by the kernels that change them)
     uint64_t *ctrl_dev = nullptr;
+    // At most one small insert whose ring write is deferred into the next fast train step's
+    // K1 (which reads sampled pending slots straight from these sources: "read-through").
+    // Any other operation on the replay first flushes it with the insert kernel.  The host
+    // mirror (cursor / size / total) already includes it.
+    struct Pending {
+        int64_t k = 0, cursor = 0, new_size = 0;
+        const float *s = nullptr, *s2 = nullptr, *r = nullptr;
+        const int32_t *a = nullptr;
+        const uint8_t *done = nullptr;
+    } pend;
+    bool no_defer = false;   // RPL_NO_DEFER=1: every insert is an immediate kernel
 };
 
 namespace rpl {
 // launch helpers implemented in replay.cu, used by dqn.cu
-int launch_gather(const rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t event,
+int launch_gather(rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t event,
                   int use_sampler, const rpl_batch *out);
 const void *insert_kernel_ptr();
+// enqueue the pending deferred insert (if any) as an insert-kernel launch
+int replay_flush(rpl_replay *rp);
+// largest insert that may be deferred into K1 (K1's CTAs write its rows)
+constexpr int64_t kMaxDeferredRows = 4096;
 }  // namespace rpl

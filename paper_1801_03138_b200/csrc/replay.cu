@@ -10,6 +10,7 @@
 
 #include "internal.h"
 #include "philox.cuh"
+#include "ring_row.cuh"
 
 namespace rpl {
 
@@ -67,27 +68,7 @@ __global__ void __launch_bounds__(256) insert_kernel(float *__restrict__ rows, i
          j += nwarps) {
         int64_t slot = cursor + j;
         if (slot >= capacity) slot -= capacity;   // k <= capacity, cursor < capacity
-        float *row = rows + slot * rs;
-        for (int c = lane; c < rs; c += 32) {
-            float v = 0.0f;
-            if (c < D) {
-                v = s[j * D + c];
-            } else if (c < 2 * D) {
-                v = s2[j * D + (c - D)];
-            } else if (c == 2 * D) {
-                v = __int_as_float(a[j]);
-            } else if (c == 2 * D + 1) {
-                v = r[j];
-            } else if (c == 2 * D + 2) {
-                uint32_t d = done[j];
-                if (d > 1u) {
-                    atomicOr(err, ERRBIT_CORRUPT);
-                    d = 1u;
-                }
-                v = __uint_as_float(d);
-            }
-            row[c] = v;
-        }
+        ring_write_row(rows + slot * rs, rs, D, lane, j, s, a, r, s2, done, err);
     }
 }
 
@@ -280,9 +261,28 @@ __global__ void __launch_bounds__(GS_W * 32) gather_staged_kernel(
 
 const void *insert_kernel_ptr() { return (const void *)insert_kernel; }
 
-int launch_gather(const rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t event,
+int replay_flush(rpl_replay *rp)
+{
+    rpl_replay::Pending &q = rp->pend;
+    if (q.k == 0) return RPL_OK;
+    const int64_t k = q.k;
+    q.k = 0;
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, rp->device);
+    int64_t blocks = (k + 7) / 8;
+    if (blocks > (int64_t)dev_sms * 8) blocks = (int64_t)dev_sms * 8;
+    insert_kernel<<<(unsigned)blocks, 256, 0, rp->stream>>>(rp->ring.rows, rp->ring.rs, rp->ring.D,
+                                                            rp->ring.capacity, q.cursor, k, q.s,
+                                                            q.a, q.r, q.s2, q.done, rp->err_dev,
+                                                            rp->ctrl_dev, q.new_size);
+    RPL_LAUNCHED();
+    return RPL_OK;
+}
+
+int launch_gather(rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t event,
                   int use_sampler, const rpl_batch *out)
 {
+    if (int rc = replay_flush(rp)) return rc;
     const int64_t groups = (n + 63) / 64;
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, rp->device);
@@ -367,6 +367,7 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
     rp->burn_in = o.burn_in;
     rp->seed = o.seed;
     rp->rank = o.rank;
+    if (const char *nd = getenv("RPL_NO_DEFER")) rp->no_defer = atoi(nd) != 0;
     rp->max_host_add = o.max_host_add ? o.max_host_add : 65536;
     if (rp->max_host_add > capacity) rp->max_host_add = capacity;
     rp->ring.capacity = capacity;
@@ -404,6 +405,7 @@ extern "C" int replay_destroy(rpl_replay *rp)
 {
     if (!rp) return RPL_OK;
     DeviceGuard g(rp->device);
+    rp->pend.k = 0;   // a never-consumed deferred insert is dropped with the ring
     cudaStreamSynchronize(rp->stream);
     for (int i = 0; i < 2; ++i) {
         if (rp->staged[i]) cudaEventDestroy(rp->staged[i]);
@@ -422,7 +424,8 @@ extern "C" int replay_add(rpl_replay *rp, int64_t k, const float *s, const int32
 {
     if (!rp) { set_error("replay_add: null handle"); return RPL_EINVAL; }
     const int32_t D = rp->ring.D;
-    if (k < 0 || k > rp->ring.capacity || (mem != RPL_HOST && mem != RPL_DEVICE)) {
+    if (k < 0 || k > rp->ring.capacity ||
+        (mem != RPL_HOST && mem != RPL_DEVICE && mem != RPL_DEVICE_DEFER)) {
         set_error("replay_add: invalid k=%lld (capacity %lld) or mem=%d", (long long)k,
                   (long long)rp->ring.capacity, mem);
         return RPL_EINVAL;
@@ -433,6 +436,7 @@ extern "C" int replay_add(rpl_replay *rp, int64_t k, const float *s, const int32
         return RPL_EINVAL;
     }
     DeviceGuard g(rp->device);
+    if (int rc = replay_flush(rp)) return rc;   // inserts stay in call order
     const float *ds = s, *dr = r, *ds2 = s_next;
     const int32_t *da = a;
     const uint8_t *dd = done;
@@ -464,16 +468,22 @@ extern "C" int replay_add(rpl_replay *rp, int64_t k, const float *s, const int32
         RPL_CUDA(cudaEventRecord(rp->staged[slot], rp->stream));
         rp->h2d_bytes += off;
     }
-    int dev_sms = 148;
-    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, rp->device);
-    int64_t blocks = (k + 7) / 8;
-    if (blocks > (int64_t)dev_sms * 8) blocks = (int64_t)dev_sms * 8;
     const int64_t new_size = rp->size + k < rp->ring.capacity ? rp->size + k : rp->ring.capacity;
-    insert_kernel<<<(unsigned)blocks, 256, 0, rp->stream>>>(rp->ring.rows, rp->ring.rs, D,
-                                                            rp->ring.capacity, rp->cursor, k, ds,
-                                                            da, dr, ds2, dd, rp->err_dev,
-                                                            rp->ctrl_dev, new_size);
-    RPL_LAUNCHED();
+    // Defer the ring write of a small insert into the next fast train step (its K1 reads
+    // sampled pending slots from the sources and writes the rows).  RPL_DEVICE inputs are
+    // only deferred on request (RPL_DEVICE_DEFER): the caller must keep them unchanged.
+    rpl_replay::Pending &q = rp->pend;
+    q.cursor = rp->cursor;
+    q.new_size = new_size;
+    q.s = ds;
+    q.s2 = ds2;
+    q.r = dr;
+    q.a = da;
+    q.done = dd;
+    q.k = k;
+    if (mem == RPL_DEVICE || k > kMaxDeferredRows || rp->no_defer) {
+        if (int rc = replay_flush(rp)) return rc;
+    }
     rp->cursor = (rp->cursor + k) % rp->ring.capacity;
     rp->size = new_size;
     rp->total += (uint64_t)k;

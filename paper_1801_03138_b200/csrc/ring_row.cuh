@@ -1,0 +1,43 @@
+// ring_row.cuh -- the one definition of a packed ring row write (CUDA path only), shared by
+// the insert kernel (replay.cu) and the deferred insert that K1 of the fast train step
+// performs (train_fast.cuh).  Row layout: [s (D) | s' (D) | a (i32 bits) |
+// r | done (u32 bits) | zero pad], rs words.  P:73: experience j goes to slot
+// (cursor + j) mod capacity.
+#pragma once
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace rpl {
+
+// warp-cooperative: lane c writes words c, c + 32, ... of experience j's row
+__device__ __forceinline__ void ring_write_row(float *row, int rs, int D, int lane, int64_t j,
+                                               const float *__restrict__ s,
+                                               const int32_t *__restrict__ a,
+                                               const float *__restrict__ r,
+                                               const float *__restrict__ s2,
+                                               const uint8_t *__restrict__ done, uint32_t *err)
+{
+    for (int c = lane; c < rs; c += 32) {
+        float v = 0.0f;
+        if (c < D) {
+            v = s[j * D + c];
+        } else if (c < 2 * D) {
+            v = s2[j * D + (c - D)];
+        } else if (c == 2 * D) {
+            v = __int_as_float(a[j]);
+        } else if (c == 2 * D + 1) {
+            v = r[j];
+        } else if (c == 2 * D + 2) {
+            uint32_t d = done[j];
+            if (d > 1u) {   // a device-sourced done > 1 is stored as 1 and flagged
+                atomicOr(err, ERRBIT_CORRUPT);
+                d = 1u;
+            }
+            v = __uint_as_float(d);
+        }
+        row[c] = v;
+    }
+}
+
+}  // namespace rpl

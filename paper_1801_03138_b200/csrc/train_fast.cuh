@@ -21,6 +21,7 @@
 #include "philox.cuh"
 #include "simt_gemm.cuh"
 #include "mma_tf32.cuh"
+#include "ring_row.cuh"
 
 namespace rpl {
 
@@ -34,11 +35,21 @@ constexpr int F_G3 = 128;         // threads per K3 GEMM group
 
 struct FastArgs {
     // replay (rctrl[0] = sampler events consumed, rctrl[1] = filled size)
-    const float *ring;
+    float *ring;
     int rs, D;
     uint64_t *rctrl;
     uint64_t seed;
     uint32_t rank;
+    // deferred insert (pend_k > 0, K1 only): experience j < pend_k belongs in slot
+    // (pend_cur + j) mod capacity; K1 reads sampled pending slots from these SoA sources,
+    // writes the rows and sets rctrl[1] = pend_size (replay.cu replay_add)
+    const float *pend_s, *pend_s2, *pend_r;
+    const int32_t *pend_a;
+    const uint8_t *pend_done;
+    uint32_t *pend_err;   // the replay's sticky error word (corrupt done)
+    int64_t pend_cur, capacity;
+    uint64_t pend_size;
+    int pend_k;
     // network
     int A, dueling, J, S, N0, N1, nets, ddqn;
     int64_t w0, b0, w1, b1, wh, bh, P;
@@ -128,7 +139,7 @@ __device__ __forceinline__ void cp_async_row(float *dst, const float *src, int n
 // shared-memory layout of K1 (32-bit words); the same formula sizes the launch on the host
 struct FwdLayout {
     int XP, N0P, UT, UTP;
-    int oW0, oX, oXh, oXl, oH0h, oH0l, oW1, oH1, oWh, ob0, ob1, oidx, ored, total;
+    int oW0, oX, oXh, oXl, oH0h, oH0l, oW1, oH1, oWh, ob0, ob1, oidx, opj, ored, total;
     __host__ __device__ FwdLayout(int D, int N0, int UT_, int J)
     {
         (void)J;
@@ -148,7 +159,8 @@ struct FwdLayout {
         ob0 = oWh + F_JP * UTP;          // [N0]
         ob1 = ob0 + ((N0 + 3) & ~3);     // [UT]
         oidx = ob1 + UT;                 // [BT]
-        ored = oidx + F_BT;              // [16 warps][16][F_JP] head partials
+        opj = oidx + F_BT;               // [BT] deferred-insert index j of the row, or -1
+        ored = opj + F_BT;               // [16 warps][16][F_JP] head partials
         total = ored + 16 * 16 * F_JP;
     }
 };
@@ -174,11 +186,12 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
     uint32_t *Xh = reinterpret_cast<uint32_t *>(sm + L.oXh), *Xl = reinterpret_cast<uint32_t *>(sm + L.oXl);
     uint32_t *H0h = reinterpret_cast<uint32_t *>(sm + L.oH0h), *H0l = reinterpret_cast<uint32_t *>(sm + L.oH0l);
     float *H1s = sm + L.oH1, *Whs = sm + L.oWh, *b0s = sm + L.ob0, *b1s = sm + L.ob1, *red = sm + L.ored;
-    int *idxs = reinterpret_cast<int *>(sm + L.oidx);
+    int *idxs = reinterpret_cast<int *>(sm + L.oidx), *pjs = reinterpret_cast<int *>(sm + L.opj);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
     const int nbt = (B + F_BT - 1) / F_BT, nut = p.nut;
     const uint64_t event = p.rctrl[0];
-    const uint64_t size = p.rctrl[1];
+    const uint64_t size = p.pend_k ? p.pend_size : p.rctrl[1];
+    if (p.pend_k && blockIdx.x == 0 && threadIdx.x == 0) p.rctrl[1] = p.pend_size;
     const int ntasks = p.nets * nbt * nut;
     for (int task = blockIdx.x; task < ntasks; task += gridDim.x) {
         const int net = task / (nbt * nut), rem = task % (nbt * nut);
@@ -224,23 +237,47 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
             sample_pair(p.seed, p.rank, event, (uint32_t)(rb / 2 + tid), size, i0, i1);
             idxs[2 * tid] = i0;
             idxs[2 * tid + 1] = i1;
+            int64_t j0 = (int64_t)i0 - p.pend_cur, j1 = (int64_t)i1 - p.pend_cur;
+            if (j0 < 0) j0 += p.capacity;
+            if (j1 < 0) j1 += p.capacity;
+            pjs[2 * tid] = j0 < p.pend_k ? (int)j0 : -1;
+            pjs[2 * tid + 1] = j1 < p.pend_k ? (int)j1 : -1;
         }
         __syncthreads();
         // (3) gather the 16 sampled rows: s for online(s), s' for target(s') / online(s')
         const int col0 = net == 0 ? 0 : D;
         for (int e = tid; e < F_BT * D; e += F_NT1) {
-            const int rr = e / D, d = e - rr * D;
-            cp_async4(Xs + rr * L.XP + d, p.ring + (int64_t)idxs[rr] * p.rs + col0 + d);
+            const int rr = e / D, d = e - rr * D, j = pjs[rr];
+            const float *src = j < 0 ? p.ring + (int64_t)idxs[rr] * p.rs + col0 + d
+                                     : (net == 0 ? p.pend_s : p.pend_s2) + (int64_t)j * D + d;
+            cp_async4(Xs + rr * L.XP + d, src);
         }
         int32_t ra_ = 0;
         float rr_ = 0.0f;
         uint32_t rd_ = 0;
         const bool unpack_scalars = net == 0 && ut == 0 && tid < F_BT && rb + tid < B;
         if (unpack_scalars) {
-            const float *row = p.ring + (int64_t)idxs[tid] * p.rs + 2 * D;
-            ra_ = __float_as_int(__ldg(row));
-            rr_ = __ldg(row + 1);
-            rd_ = __float_as_uint(__ldg(row + 2));
+            const int j = pjs[tid];
+            if (j < 0) {
+                const float *row = p.ring + (int64_t)idxs[tid] * p.rs + 2 * D;
+                ra_ = __float_as_int(__ldg(row));
+                rr_ = __ldg(row + 1);
+                rd_ = __float_as_uint(__ldg(row + 2));
+            } else {
+                ra_ = p.pend_a[j];
+                rr_ = p.pend_r[j];
+                rd_ = p.pend_done[j];
+            }
+        }
+        // the deferred insert's ring rows (no sampled row of this step reads them from the
+        // ring), overlapped with this CTA's first operand loads
+        if (p.pend_k && task == (int)blockIdx.x) {
+            for (int j = blockIdx.x * NW + warp; j < p.pend_k; j += gridDim.x * NW) {
+                int64_t slot = p.pend_cur + j;
+                if (slot >= p.capacity) slot -= p.capacity;
+                ring_write_row(p.ring + slot * p.rs, p.rs, D, lane, j, p.pend_s, p.pend_a,
+                               p.pend_r, p.pend_s2, p.pend_done, p.pend_err);
+            }
         }
         trace_.mark(2);
         cp_async_wait_all();
@@ -996,77 +1033,115 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
 {
     pdl_wait();
     CtaTrace trace_(p.trace, 3);
-    __shared__ float red[NT / 32];
-    const int tid = threadIdx.x;
+    constexpr int NWK4 = NT / 32;
+    __shared__ float red[NWK4];
+    __shared__ float wsum[NWK4][32];
+    const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
     const int B = p.B;
-    // batch-mean loss (fixed-order reduction, identical in every CTA)
+    const int64_t stride = (int64_t)gridDim.x * NT;
+    // Every load of the kernel's first round is issued before anything waits on one: the
+    // loss partials, the sync flag, this thread's first W0 partials and its first float4 of
+    // [w1, P) (grad + weights).
+    // (1) batch-mean loss (fixed-order reduction, identical in every CTA)
     float ls = 0.0f;
     for (int b = tid; b < B; b += NT) ls += __ldcg(p.loss_part + b);
-    const bool do_sync = *p.sync_flag != 0;
-    ls = warp_sum(ls);
-    if ((tid & 31) == 0) red[tid >> 5] = ls;
-    __syncthreads();
-    float lsum = 0.0f;
-    for (int w = 0; w < NT / 32; ++w) lsum += red[w];
-    const float loss = lsum / (float)B;
-    const bool ok = isfinite(loss);
-    const bool upd = p.apply_update && ok;
-    trace_.mark(2);
-    const int64_t stride = (int64_t)gridDim.x * NT;
-    // (a) W0, b0: the fixed-order sum of the (split, batch tile) partials written by K3
+    const int do_sync = __ldcg(p.sync_flag);
+    // (2) W0, b0: the fixed-order sum of the (split, batch tile) partials written by K3.  A
+    // CTA owns 32 consecutive elements; warp w sums partials q = w, w + 8, ... (compensated,
+    // in order; coalesced 128-B loads), then the 8 warp sums are added in warp order.
     const int64_t n0el = p.w1;                  // W0 and b0 lead the blob
     const int nparts = p.NS * ((B + BM - 1) / BM);
-    for (int64_t i = (int64_t)blockIdx.x * NT + tid; i < n0el; i += stride) {
-        // compensated (Kahan) sum in a fixed order: up to NS * B / 32 partials, 32 in flight
+    auto w0_partial = [&](int64_t i) {
         float g = 0.0f, comp = 0.0f;
-        for (int q0 = 0; q0 < nparts; q0 += 32) {
-            float v[32];
+        if (i >= n0el) return g;
+        for (int q0 = wq; q0 < nparts; q0 += 8 * NWK4) {
+            float v[8];
 #pragma unroll
-            for (int q = 0; q < 32; ++q) v[q] = q0 + q < nparts ? __ldcg(p.w0part + (int64_t)(q0 + q) * n0el + i) : 0.0f;
+            for (int q = 0; q < 8; ++q) {
+                const int qq = q0 + q * NWK4;
+                v[q] = qq < nparts ? __ldcg(p.w0part + (int64_t)qq * n0el + i) : 0.0f;
+            }
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
+            for (int q = 0; q < 8; ++q) {
                 const float yv = v[q] - comp;
                 const float tv = g + yv;
                 comp = (tv - g) - yv;
                 g = tv;
             }
         }
-        p.grad[i] = g;
+        return g;
+    };
+    // (3) first float4 of the elementwise SGD over [w1, P)
+    const int64_t lo = p.w1, n_el = p.P - p.w1;
+    const int64_t n4 = (p.nsb == 1) ? n_el / 4 : 0;
+    int64_t e4 = (int64_t)blockIdx.x * NT + tid;
+    float4 g4 = make_float4(0.f, 0.f, 0.f, 0.f), w4 = g4;
+    if (e4 < n4) {
+        g4 = __ldcg(reinterpret_cast<const float4 *>(p.grad + lo + 4 * e4));
+        w4 = *reinterpret_cast<const float4 *>(p.online + lo + 4 * e4);
+    }
+    int64_t i0 = (int64_t)blockIdx.x * 32;
+    float g = w0_partial(i0 + lane);
+    ls = warp_sum(ls);
+    if (lane == 0) red[wq] = ls;
+    wsum[wq][lane] = g;
+    __syncthreads();
+    float lsum = 0.0f;
+    for (int w = 0; w < NWK4; ++w) lsum += red[w];
+    const float loss = lsum / (float)B;
+    const bool ok = isfinite(loss);
+    const bool upd = p.apply_update && ok;
+    const float lr = p.lr;
+    trace_.mark(2);
+    auto w0_finish = [&](int64_t i) {
+        if (wq != 0 || i >= n0el) return;
+        float t = 0.0f;
+#pragma unroll
+        for (int w = 0; w < NWK4; ++w) t += wsum[w][lane];
+        p.grad[i] = t;
         if (upd) {
-            const float w = p.online[i] - p.lr * g;
+            const float w = p.online[i] - lr * t;
             p.online[i] = w;
             if (do_sync) p.target[i] = w;
         }
+    };
+    w0_finish(i0 + lane);
+    for (i0 += (int64_t)gridDim.x * 32; i0 < n0el; i0 += (int64_t)gridDim.x * 32) {
+        g = w0_partial(i0 + lane);
+        __syncthreads();   // wsum reuse
+        wsum[wq][lane] = g;
+        __syncthreads();
+        w0_finish(i0 + lane);
     }
     trace_.mark(3);
-    // (b) every other parameter: [w1, P), float4 where whole
-    const int64_t lo = p.w1, n_el = p.P - p.w1;
-    const int64_t n4 = (p.nsb == 1) ? n_el / 4 : 0;
-    for (int64_t e = (int64_t)blockIdx.x * NT + tid; e < n4; e += stride) {
-        const int64_t i = lo + 4 * e;
-        const float4 g = __ldcg(reinterpret_cast<const float4 *>(p.grad + i));
+    // (4) every other parameter: [w1, P), float4 where whole
+    for (; e4 < n4; e4 += stride) {
+        const int64_t i = lo + 4 * e4;
+        if (e4 != (int64_t)blockIdx.x * NT + tid) {
+            g4 = __ldcg(reinterpret_cast<const float4 *>(p.grad + i));
+            w4 = *reinterpret_cast<const float4 *>(p.online + i);
+        }
         if (upd) {
-            float4 w = *reinterpret_cast<const float4 *>(p.online + i);
-            w.x -= p.lr * g.x;
-            w.y -= p.lr * g.y;
-            w.z -= p.lr * g.z;
-            w.w -= p.lr * g.w;
-            *reinterpret_cast<float4 *>(p.online + i) = w;
-            if (do_sync) *reinterpret_cast<float4 *>(p.target + i) = w;
+            w4.x -= lr * g4.x;
+            w4.y -= lr * g4.y;
+            w4.z -= lr * g4.z;
+            w4.w -= lr * g4.w;
+            *reinterpret_cast<float4 *>(p.online + i) = w4;
+            if (do_sync) *reinterpret_cast<float4 *>(p.target + i) = w4;
         }
     }
     for (int64_t e = 4 * n4 + (int64_t)blockIdx.x * NT + tid; e < n_el; e += stride) {
         const int64_t i = lo + e;
-        float g;
+        float gs;
         if (p.nsb == 1) {
-            g = __ldcg(p.grad + i);
+            gs = __ldcg(p.grad + i);
         } else {
-            g = 0.0f;
-            for (int s = 0; s < p.nsb; ++s) g += __ldcg(p.gpart + (int64_t)s * p.P + i);
-            p.grad[i] = g;
+            gs = 0.0f;
+            for (int sb = 0; sb < p.nsb; ++sb) gs += __ldcg(p.gpart + (int64_t)sb * p.P + i);
+            p.grad[i] = gs;
         }
         if (upd) {
-            const float w = p.online[i] - p.lr * g;
+            const float w = p.online[i] - lr * gs;
             p.online[i] = w;
             if (do_sync) p.target[i] = w;
         }
@@ -1075,8 +1150,9 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
         p.grad[p.P] = loss;
         if (p.loss_out) *p.loss_out = loss;
         if (!ok) atomicOr(p.err, ERRBIT_NUMERIC);
-        p.rctrl[0] += 1;          // sampler event consumed
-        *p.step_dev += 1;         // executed train steps
+        // fire-and-forget reductions (no load round trip on the kernel's tail)
+        atomicAdd(reinterpret_cast<unsigned long long *>(p.rctrl), 1ull);   // sampler event consumed
+        atomicAdd(reinterpret_cast<unsigned long long *>(p.step_dev), 1ull); // executed train steps
     }
 }
 

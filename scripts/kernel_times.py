@@ -38,7 +38,7 @@ def main():
     def step(i):
         if a.adds:
             j = (i % 64) * a.adds
-            rp.add(**{k: v[j:j + a.adds] for k, v in pool.items()})
+            rp.add(**{k: v[j:j + a.adds] for k, v in pool.items()}, defer=True)
         dqn.train_step(rp, a.batch, loss)
 
     for i in range(50):

@@ -198,3 +198,67 @@ def test_explicit_sync_target_and_set_get(b):
         dqn.train_step(rp, 33)   # > max_batch
     with pytest.raises(b.RplError):
         dqn.set_params(np.zeros(5, np.float32))
+
+
+@pytest.mark.parametrize("mode", ["host", "device_defer", "mixed"])
+def test_deferred_insert_read_through(b, mode):
+    # replay_add's ring write deferred into the train step's first kernel (include/
+    # ingpu_replay.h, replay_add): with a 64-slot ring, 8 adds per step and batch 128 almost
+    # every step samples slots of the pending insert, which are read from its sources; the
+    # pending range wraps the ring end every 8th step.  Sampled batch bit-exact, the step
+    # within tolerance, and the ring contents exact afterwards.
+    import torch
+    cfg = _cfg(b, max_batch=128, double_dqn=True, sync_period=3)
+    C = 64
+    rp = b.Replay(C, 27, burn_in=16, seed=5)
+    orc = oracle.Ring(C, 27)
+    dqn = b.DQN(cfg, _params(cfg))
+    e = experiences(8 * 40, seed=11)
+    dev = {k: torch.from_numpy(v).cuda() for k, v in e.items()}
+    hits = 0
+    for it in range(40):
+        sl = slice(8 * it, 8 * it + 8)
+        if mode == "device_defer" or (mode == "mixed" and it % 2):
+            rp.add(**{k: v[sl] for k, v in dev.items()}, defer=True)
+        else:
+            rp.add(**{k: v[sl] for k, v in e.items()})
+        orc.add(**{k: v[sl] for k, v in e.items()})
+        if mode == "mixed" and it % 5 == 4 and it > 2:
+            # any other call on the replay writes the pending insert first
+            g = rp.sample(16)
+            rc, o = orc.sample(16, 5, 0, 16)
+            assert rc == oracle.OK
+            for k in ("idx", "s", "s_next", "a", "r", "done"):
+                assert np.array_equal(g[k].cpu().numpy(), o[k]), k
+        st = rp.state()
+        cur = st["cursor"]
+        out = step_and_compare(b, cfg, dqn, rp, orc, 128, seed=5, burn_in=16)
+        if out is not None:
+            idx = dqn.debug(b.RPL_DBG_IDX, 128).astype(np.int64)
+            hits += int(((idx - (cur - 8)) % C < 8).sum())
+    assert hits > 300   # ~16 of 128 rows per step
+    idx = torch.arange(C, dtype=torch.int32, device="cuda")
+    g = rp.gather(idx)
+    o = orc.gather(np.arange(C, dtype=np.int32))
+    for k in ("s", "s_next", "a", "r", "done"):
+        assert np.array_equal(g[k].cpu().numpy(), o[k]), k
+    assert rp.check() == b.RPL_OK and dqn.check() == b.RPL_OK
+
+
+def test_deferred_device_insert_corrupt_done(b):
+    # a device-sourced done > 1 is stored as 1 and raises the replay's sticky ECORRUPT,
+    # also when the deferred write happens inside the train step
+    import torch
+    cfg = _cfg(b, max_batch=32)
+    rp = b.Replay(50, 27, seed=61)
+    e = experiences(48, seed=62)
+    rp.add(**e)
+    dqn = b.DQN(cfg, _params(cfg))
+    bad = {k: torch.from_numpy(v[:2].copy()).cuda() for k, v in e.items()}
+    bad["done"][0] = 7
+    rp.add(**bad, defer=True)
+    assert dqn.train_step(rp, 32) == b.RPL_OK
+    assert dqn.check() == b.RPL_OK
+    assert rp.check() == b.RPL_ECORRUPT
+    g = rp.gather(torch.tensor([48, 49], dtype=torch.int32, device="cuda"))
+    assert g["done"].cpu().numpy().tolist() == [1, int(e["done"][1])]
