@@ -1,7 +1,7 @@
 // mma_tf32.cuh -- FP32-accurate warp-level tensor-core products for the small 16-row tiles of
 // the fast path: "3xTF32" on mma.sync.m16n8k8 (CUDA path only).
 //
-// x = hi + lo with hi = tf32(x), lo = tf32(x - hi); a.b ~= hi_a hi_b + hi_a lo_b + lo_a hi_b
+// x = hi + lo with hi = tf32(x), lo = x - hi (read as tf32 by the MMA); a.b ~= hi_a hi_b + hi_a lo_b + lo_a hi_b
 // (the dropped lo_a lo_b term is ~2^-22 relative), accumulated in FP32.  Small terms are
 // accumulated first.  The error is at FP32 round-off level, which keeps the 1e-5 normwise
 // parity of the FP32 path (BASELINE north star); tests/test_gpu_train.py checks it.
@@ -15,16 +15,14 @@
 
 namespace rpl {
 
-__device__ __forceinline__ uint32_t tf32_rna(float x)
-{
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
-}
+// hi = x rounded to tf32 (half away from zero: +half an ulp of the 10-bit mantissa, then
+// truncate; 2 integer ops instead of the multi-instruction cvt.rna.tf32 sequence sm_100a emits);
+// lo = x - hi is exact in fp32 and is passed raw: the MMA reads only its tf32 bits (the
+// dropped bits are ~2^-21 of x)
 __device__ __forceinline__ void tf32_split(float x, uint32_t &hi, uint32_t &lo)
 {
-    hi = tf32_rna(x);
-    lo = tf32_rna(x - __uint_as_float(hi));
+    hi = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
+    lo = __float_as_uint(x - __uint_as_float(hi));
 }
 
 __device__ __forceinline__ void mma_tf32(float c[4], uint32_t a0, uint32_t a1, uint32_t a2,

@@ -717,19 +717,23 @@ __device__ __forceinline__ void gemm3_tile(const Opnd &a, const Opnd &b, int m0,
 // K3: dW1 / db1 tiles, dH0 split-K tiles, head-weight gradients
 // ------------------------------------------------------------------------------------------
 // ------------------------------------------------------------------------------------------
-// K3 tensor-core tile: C[32 x 64] = sum_{kk in [kb, ke)} A(m, kk) B(n, kk) with 3xTF32
-// mma.sync.m16n8k8 (FP32-accurate), 256 threads = 8 warps as 2 (m16) x 4 (n16).  The whole
-// contraction range (up to MM_SK per pass) is copied global -> shared with 16-byte cp.async in
-// one go (one L2 round trip), stored k-major with row strides == 4 (mod 32) words so every
-// fragment load is conflict-free, and split into tf32 hi / lo while loading fragments.
+// K3 tensor-core tile: C[32 x K3N] = sum_{kk in [kb, ke)} A(m, kk) B(n, kk) with 3xTF32
+// mma.sync.m16n8k8 (FP32-accurate), 256 threads = 8 warps as 2 (m16) x 4 (n8 per K3N/4).  The
+// whole contraction range (up to MM_SK per pass) is copied global -> shared with 16-byte
+// cp.async in one go (one L2 round trip), in the source's own orientation: an operand whose
+// source rows are kk (kRc) is stored [kk][r] with row stride MM_KS == 8 (mod 32) words, one whose
+// source rows are r is stored [r][kk] with stride MM_RS == 4 (mod 32): both make every
+// fragment load conflict-free.  Values are split into tf32 hi / lo while loading fragments.
 // Operand element (r, kk) is p[kk * ld + r] (kRc) or p[r * ld + kk]; r, kk multiples of 4 are
 // whole 16-byte chunks (all dims here are multiples of 4), missing chunks are zero-filled.
 // ------------------------------------------------------------------------------------------
 constexpr int MM_T = 256;
 constexpr int K3N = 32;                      // K3 tile columns (32 x 32 tiles: 2 CTAs / SM)
 constexpr int MM_SK = 128;                   // contraction per pass
-constexpr int MM_AS = BM + 4, MM_BS = K3N + 4;
-constexpr int MM_FLOATS = MM_SK * (MM_AS + MM_BS);
+constexpr int MM_KS = 40;                    // [kk][r] stride (>= BM, K3N; == 8 mod 32)
+constexpr int MM_RS = MM_SK + 4;             // [r][kk] stride (== 4 mod 32)
+constexpr int MM_OPF = MM_SK * MM_KS > BM * MM_RS ? MM_SK * MM_KS : BM * MM_RS;   // one operand
+constexpr int MM_FLOATS = 2 * MM_OPF;
 
 __device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, bool valid)
 {
@@ -738,8 +742,8 @@ __device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, b
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
 }
 
-// stage [k0, k0 + MM_SK) of an operand with TR rows into S[kk][r] (row stride LDS)
-template <bool kRc, int TR, int LDS>
+// stage [k0, k0 + MM_SK) of an operand with TR rows: kRc -> S[kk][r], else S[r][kk]
+template <bool kRc, int TR>
 __device__ __forceinline__ void mm_stage(float *S, const Opnd &o, int r0, int k0, int kend, int tid)
 {
     if (kRc) {
@@ -748,38 +752,34 @@ __device__ __forceinline__ void mm_stage(float *S, const Opnd &o, int r0, int k0
             const int kk = e / (TR / 4), r4 = e % (TR / 4);
             const int r = r0 + 4 * r4, k = k0 + kk;
             const bool v = r < o.R && k < kend;
-            cp_async16_zfill(S + kk * LDS + 4 * r4, v ? o.p + (int64_t)k * o.ld + r : o.p, v);
+            cp_async16_zfill(S + kk * MM_KS + 4 * r4, v ? o.p + (int64_t)k * o.ld + r : o.p, v);
         }
     } else {
-        // source rows are r: 4 consecutive kk of one r per float4, transposed into shared
-        // memory; every load of the pass is issued before the first store
-        constexpr int NV = TR * (MM_SK / 4) / MM_T;
-        float4 v[NV];
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const int e = i * MM_T + tid, r = e / (MM_SK / 4), k4 = e % (MM_SK / 4);
+        // source rows are r: MM_SK/4 chunks of 16 B per r
+        for (int e = tid; e < TR * (MM_SK / 4); e += MM_T) {
+            const int r = e / (MM_SK / 4), k4 = e % (MM_SK / 4);
             const int rr = r0 + r, k = k0 + 4 * k4;
-            v[i] = (rr < o.R && k < kend) ? __ldcg(reinterpret_cast<const float4 *>(o.p + (int64_t)rr * o.ld + k))
-                                          : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const int e = i * MM_T + tid, r = e / (MM_SK / 4), k4 = e % (MM_SK / 4);
-            S[(4 * k4 + 0) * LDS + r] = v[i].x;
-            S[(4 * k4 + 1) * LDS + r] = v[i].y;
-            S[(4 * k4 + 2) * LDS + r] = v[i].z;
-            S[(4 * k4 + 3) * LDS + r] = v[i].w;
+            const bool v = rr < o.R && k < kend;
+            cp_async16_zfill(S + r * MM_RS + 4 * k4, v ? o.p + (int64_t)rr * o.ld + k : o.p, v);
         }
     }
 }
 
+// element (r, kk) of a staged operand
+template <bool kRc>
+__device__ __forceinline__ float mm_at(const float *S, int r, int kk)
+{
+    return kRc ? S[kk * MM_KS + r] : S[r * MM_RS + kk];
+}
+
 template <bool kARc, bool kBRc, class EPI, class RSUM>
 __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int m0, int n0, int kb, int ke,
-                                              const EPI &epi, bool want_rowsum, const RSUM &rs, float *smf)
+                                              const EPI &epi, bool want_rowsum, const RSUM &rs, float *smf,
+                                              CtaTrace *tr = nullptr, int mk = 0)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3, wm = warp & 1, wn = warp >> 1;
-    float *As = smf, *Bs = smf + MM_SK * MM_AS;
+    float *As = smf, *Bs = smf + MM_OPF;
     // the MMA accumulates 32-deep partials (4 k-steps) that are added into round-to-nearest
     // FP32 sums, so long contractions (K = 1024 at large batch) keep FP32-level accuracy
     constexpr int NT8 = K3N / 32;                 // n8 tiles per warp (warps: 2 m16 x 4 n)
@@ -791,25 +791,26 @@ __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int 
     float rsum = 0.0f;
     for (int k0 = kb; k0 < ke; k0 += MM_SK) {
         __syncthreads();   // the previous pass / task is done with the staging buffers
-        mm_stage<kARc, BM, MM_AS>(As, a, m0, k0, ke, tid);
-        mm_stage<kBRc, K3N, MM_BS>(Bs, b, n0, k0, ke, tid);
+        mm_stage<kARc, BM>(As, a, m0, k0, ke, tid);
+        mm_stage<kBRc, K3N>(Bs, b, n0, k0, ke, tid);
         cp_async_wait_all();
         __syncthreads();
+        if (tr && k0 == kb) tr->mark(mk);
         const int ksteps = (min(MM_SK, ke - k0) + 7) / 8;
         const int mr = 16 * wm + g;
         for (int ks = 0; ks < ksteps; ++ks) {
             const int k = 8 * ks;
             uint32_t ah[4], al[4];
-            tf32_split(As[(k + t) * MM_AS + mr], ah[0], al[0]);
-            tf32_split(As[(k + t) * MM_AS + mr + 8], ah[1], al[1]);
-            tf32_split(As[(k + t + 4) * MM_AS + mr], ah[2], al[2]);
-            tf32_split(As[(k + t + 4) * MM_AS + mr + 8], ah[3], al[3]);
+            tf32_split(mm_at<kARc>(As, mr, k + t), ah[0], al[0]);
+            tf32_split(mm_at<kARc>(As, mr + 8, k + t), ah[1], al[1]);
+            tf32_split(mm_at<kARc>(As, mr, k + t + 4), ah[2], al[2]);
+            tf32_split(mm_at<kARc>(As, mr + 8, k + t + 4), ah[3], al[3]);
 #pragma unroll
             for (int nt = 0; nt < NT8; ++nt) {
                 const int nc = (K3N / 4) * wn + 8 * nt + g;
                 uint32_t bh[2], bl[2];
-                tf32_split(Bs[(k + t) * MM_BS + nc], bh[0], bl[0]);
-                tf32_split(Bs[(k + t + 4) * MM_BS + nc], bh[1], bl[1]);
+                tf32_split(mm_at<kBRc>(Bs, nc, k + t), bh[0], bl[0]);
+                tf32_split(mm_at<kBRc>(Bs, nc, k + t + 4), bh[1], bl[1]);
                 mma_3xtf32_sep(c[nt], cl[nt], cm[nt], ah, al, bh, bl);
             }
             if ((ks & 3) == 3 || ks == ksteps - 1) {
@@ -824,9 +825,10 @@ __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int 
         }
         if (want_rowsum && tid < BM) {
             const int kn = min(MM_SK, ke - k0);
-            for (int k = 0; k < kn; ++k) rsum += As[k * MM_AS + tid];
+            for (int k = 0; k < kn; ++k) rsum += mm_at<kARc>(As, tid, k);
         }
     }
+    if (tr) tr->mark(mk + 1);
 #pragma unroll
     for (int nt = 0; nt < NT8; ++nt)
 #pragma unroll
@@ -873,7 +875,7 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             auto rs = [&](int m, float v) {
                 if (m < N1) gp[p.b1 + m] = v;
             };
-            gemm_mma_tile<true, true>(a, bo, m0, n0, kb, ke, epi, n0 == 0, rs, k3raw);
+            gemm_mma_tile<true, true>(a, bo, m0, n0, kb, ke, epi, n0 == 0, rs, k3raw, &trace_, 2);
             trace_.mark(4);
         } else if (t < n_w + n_h) {
             // dH0 partial [s][b][k] = sum_{u in split s} dZ1[b][u] W1[u][k]
@@ -890,9 +892,8 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             constexpr int XS = 36;
             const Opnd a{p.dZ1, N1, B}, bo{p.online + p.w1, N0, N0};
             auto epi = [&](int m, int n, float v) { tile[(m - m0) * (K3N + 4) + (n - n0)] = v; };
-            gemm_mma_tile<false, true>(a, bo, m0, n0, kb, ke, epi, false, NoRowsum{}, k3raw);
+            gemm_mma_tile<false, true>(a, bo, m0, n0, kb, ke, epi, false, NoRowsum{}, k3raw, &trace_, 5);
             __syncthreads();
-            trace_.mark(5);
             const int D = p.D, nb = min(BM, B - m0), nk = min(K3N, N0 - n0);
             float *h0t = xs + BM * XS;                     // [BM][K3N] H0 of the tile (ReLU mask)
             for (int e = threadIdx.x; e < nb * D; e += F_NT3) {
@@ -909,7 +910,6 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             }
             cp_async_wait_all();
             __syncthreads();
-            trace_.mark(6);
             for (int e = threadIdx.x; e < BM * K3N; e += F_NT3) {
                 const int bb = e / K3N, kk = e % K3N;
                 const bool on = bb < nb && kk < nk && h0t[bb * K3N + kk] > 0.0f;
@@ -918,7 +918,6 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             if (nb < BM)
                 for (int e = threadIdx.x; e < (BM - nb) * XS; e += F_NT3) xs[nb * XS + e] = 0.0f;
             __syncthreads();
-            trace_.mark(2);
             // dW0 / db0 share: C[unit k][d] = sum_b tile[b][k] xs[b][d] over the tile's rows
             // (column D of xs is 1 -> db0); thread = (unit kk, 8 consecutive columns)
             float *w0p = p.w0part + ((int64_t)s * ((B + BM - 1) / BM) + m0 / BM) * (p.b0 + N0);
@@ -934,7 +933,6 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
                     acc[2] = fmaf(z, x0.z, acc[2]); acc[3] = fmaf(z, x0.w, acc[3]);
                 }
                 const int k = n0 + kk;
-                trace_.mark(3);
                 if (kk < nk) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
@@ -995,7 +993,6 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
                     for (int e = threadIdx.x; e < cn * J; e += F_NT3) cp_async4(dsm + e, p.dHead + (int64_t)c0 * J + e);
                     cp_async_wait_all();
                     __syncthreads();
-                    if (c0 == kb) trace_.mark(2);
                     const int q0 = (cn * qtr) / 4, q1 = (cn * (qtr + 1)) / 4;
                     for (int bb = q0; bb < q1; ++bb) {
                         const float h = hsm[bb * HD_U + ul];
@@ -1008,7 +1005,6 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) red[(qtr * HD_U + ul) * 8 + jj] = acc[jj];
                 __syncthreads();
-                trace_.mark(3);
                 for (int o = threadIdx.x; o < HD_U * 8; o += F_NT3) {
                     const int uu = o / 8, jj = o % 8, unit = u0 + uu;
                     if (jj >= jn || unit >= N1) continue;

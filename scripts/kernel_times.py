@@ -44,6 +44,14 @@ def main():
     for i in range(50):
         step(i)
     torch.cuda.synchronize()
+    import time
+    t0 = time.perf_counter()
+    for i in range(400):
+        step(i)
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    print(f"host enqueue {1e6 * (t1 - t0) / 400:.2f} us/step, wall incl. drain {1e6 * (t2 - t0) / 400:.2f} us/step")
     with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
         for i in range(a.steps):
             step(i)

@@ -20,8 +20,8 @@ __global__ void __launch_bounds__(256) k_tile(const float *A, const float *B, fl
     for (int rep = 0; rep < reps; ++rep) {
         if (mode == 0) {
             __syncthreads();
-            mm_stage<true, BM, MM_AS>(smf, a, 0, 0, 128, threadIdx.x);
-            mm_stage<true, BN, MM_BS>(smf + MM_SK * MM_AS, b, 0, 0, 128, threadIdx.x);
+            mm_stage<true, BM>(smf, a, 0, 0, 128, threadIdx.x);
+            mm_stage<true, K3N>(smf + MM_OPF, b, 0, 0, 128, threadIdx.x);
             cp_async_wait_all();
             __syncthreads();
             sink += smf[threadIdx.x];
