@@ -136,6 +136,82 @@ __device__ __forceinline__ void cp_async_row(float *dst, const float *src, int n
     for (int c = tid; c < n / 4; c += nt) cp_async16(dst + 4 * c, src + 4 * c);
 }
 
+__device__ __forceinline__ float f_huber(float d, float kappa, int kinf)
+{
+    const float ad = fabsf(d);
+    if (kinf || ad <= kappa) return 0.5f * d * d;
+    return kappa * (ad - 0.5f * kappa);
+}
+
+// TD target, Huber loss and the head-output gradient of one sample, by one warp (lane j owns
+// head output j / action j).  hs[net * hsld + j]: head outputs (bias included) of the online
+// net on s (net 0), the target net on s' (1), the online net on s' (2, Double DQN).  Writes the
+// step's exported Q / y / loss / a* for sample b and dhs[0, J).
+__device__ __forceinline__ void td_warp(const FastArgs &p, const float *hs, int hsld, int ab, float rb,
+                                        uint8_t db, int b, int lane, float *dhs)
+{
+    const int A = p.A, B = p.B;
+    float q[3];
+#pragma unroll
+    for (int net = 0; net < 3; ++net) {
+        float qa = 0.0f;
+        if (net < p.nets) {
+            if (p.dueling) {
+                // Q(s,a) = V(s) + A(s,a) - (1/|A|) sum_a' A(s,a')
+                float mean = 0.0f;
+                for (int k = 0; k < A; ++k) mean += hs[net * hsld + 1 + k];
+                mean /= (float)A;
+                if (lane < A) qa = hs[net * hsld + 0] + hs[net * hsld + 1 + lane] - mean;
+            } else if (lane < A) {
+                qa = hs[net * hsld + lane];
+            }
+        }
+        q[net] = qa;
+    }
+    // TD target (Q9): DQN max_a Q_t(s',a); Double DQN Q_t(s', argmax_a Q_o(s',a))
+    float boot;
+    int astar = -1;
+    if (!p.ddqn) {
+        float m = lane < A ? q[1] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        boot = m;
+    } else {
+        float v = lane < A ? q[2] : -INFINITY;
+        int ix = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, ix, o);
+            if (ov > v || (ov == v && oi < ix)) { v = ov; ix = oi; }   // ties: lowest
+        }
+        astar = ix;
+        boot = __shfl_sync(0xffffffffu, q[1], astar);
+    }
+    const float notdone = db ? 0.0f : 1.0f;
+    const float yb = rb + p.gamma * notdone * boot;
+    const float qsel = __shfl_sync(0xffffffffu, q[0], ab);   // Q[i*A + a_i]
+    const float delta = qsel - yb;
+    const float g = (p.kinf ? delta : fminf(fmaxf(delta, -p.kappa), p.kappa)) / (float)B;
+    if (p.dueling) {
+        // dV = sum_a dQ_a = g ; dA_a = dQ_a - (1/|A|) sum_a' dQ_a'
+        if (lane < A) dhs[1 + lane] = (lane == ab ? g : 0.0f) - g / (float)A;
+        if (lane == 0) dhs[0] = g;
+    } else if (lane < A) {
+        dhs[lane] = lane == ab ? g : 0.0f;
+    }
+    if (lane < A) {
+        p.Qs[(int64_t)b * A + lane] = q[0];
+        p.Qt2[(int64_t)b * A + lane] = q[1];
+        if (p.ddqn) p.Qo2[(int64_t)b * A + lane] = q[2];
+    }
+    if (lane == 0) {
+        p.y[b] = yb;
+        p.loss_part[b] = f_huber(delta, p.kappa, p.kinf);
+        if (p.ddqn) p.astar[b] = astar;
+    }
+}
+
 // shared-memory layout of K1 (32-bit words); the same formula sizes the launch on the host
 struct FwdLayout {
     int XP, N0P, UT, UTP;
@@ -410,13 +486,6 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
 // ------------------------------------------------------------------------------------------
 // K2: one CTA per sample
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ float f_huber(float d, float kappa, int kinf)
-{
-    const float ad = fabsf(d);
-    if (kinf || ad <= kappa) return 0.5f * d * d;
-    return kappa * (ad - 0.5f * kappa);
-}
-
 __global__ void __launch_bounds__(NT) fast_td_kernel(const __grid_constant__ FastArgs p)
 {
     CtaTrace trace_(p.trace, 1);
@@ -466,67 +535,7 @@ __global__ void __launch_bounds__(NT) fast_td_kernel(const __grid_constant__ Fas
         }
         __syncthreads();
         trace_.mark(2);
-        if (warp == 0) {
-            float q[3];
-#pragma unroll
-            for (int net = 0; net < 3; ++net) {
-                float qa = 0.0f;
-                if (net < p.nets) {
-                    if (p.dueling) {
-                        // Q(s,a) = V(s) + A(s,a) - (1/|A|) sum_a' A(s,a')
-                        float mean = 0.0f;
-                        for (int k = 0; k < A; ++k) mean += hs[net][1 + k];
-                        mean /= (float)A;
-                        if (lane < A) qa = hs[net][0] + hs[net][1 + lane] - mean;
-                    } else if (lane < A) {
-                        qa = hs[net][lane];
-                    }
-                }
-                q[net] = qa;
-            }
-            // TD target (Q9): DQN max_a Q_t(s',a); Double DQN Q_t(s', argmax_a Q_o(s',a))
-            float boot;
-            int astar = -1;
-            if (!p.ddqn) {
-                float m = lane < A ? q[1] : -INFINITY;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-                boot = m;
-            } else {
-                float v = lane < A ? q[2] : -INFINITY;
-                int ix = lane;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const float ov = __shfl_xor_sync(0xffffffffu, v, o);
-                    const int oi = __shfl_xor_sync(0xffffffffu, ix, o);
-                    if (ov > v || (ov == v && oi < ix)) { v = ov; ix = oi; }   // ties: lowest
-                }
-                astar = ix;
-                boot = __shfl_sync(0xffffffffu, q[1], astar);
-            }
-            const float notdone = db ? 0.0f : 1.0f;
-            const float yb = rb + p.gamma * notdone * boot;
-            const float qsel = __shfl_sync(0xffffffffu, q[0], ab);   // Q[i*A + a_i]
-            const float delta = qsel - yb;
-            const float g = (p.kinf ? delta : fminf(fmaxf(delta, -p.kappa), p.kappa)) / (float)B;
-            if (p.dueling) {
-                // dV = sum_a dQ_a = g ; dA_a = dQ_a - (1/|A|) sum_a' dQ_a'
-                if (lane < A) dhs[1 + lane] = (lane == ab ? g : 0.0f) - g / (float)A;
-                if (lane == 0) dhs[0] = g;
-            } else if (lane < A) {
-                dhs[lane] = lane == ab ? g : 0.0f;
-            }
-            if (lane < A) {
-                p.Qs[(int64_t)b * A + lane] = q[0];
-                p.Qt2[(int64_t)b * A + lane] = q[1];
-                if (p.ddqn) p.Qo2[(int64_t)b * A + lane] = q[2];
-            }
-            if (lane == 0) {
-                p.y[b] = yb;
-                p.loss_part[b] = f_huber(delta, p.kappa, p.kinf);
-                if (p.ddqn) p.astar[b] = astar;
-            }
-        }
+        if (warp == 0) td_warp(p, &hs[0][0], F_MAXJ + 1, ab, rb, db, b, lane, dhs);
         trace_.mark(3);
         cp_async_wait_all();
         __syncthreads();
