@@ -786,18 +786,22 @@ __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int 
                                               const EPI &epi, bool want_rowsum, const RSUM &rs, float *smf,
                                               CtaTrace *tr = nullptr, int mk = 0)
 {
+    // 8 warps = 2 (m16 halves of the tile) x 4 (k-step residues): warp (wm, wk) computes rows
+    // 16 wm .. 16 wm + 15 x all K3N columns over the k-steps ks == wk (mod 4) of every pass --
+    // each A fragment feeds K3N / 8 MMAs and every staged word is read by one or two warps
+    // (shared-memory bandwidth, not the HMMA pipe, bounds this loop).  The four k-residue
+    // partials are added in a fixed order at the end.
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g = lane >> 2, t = lane & 3, wm = warp & 1, wn = warp >> 1;
+    const int g = lane >> 2, t = lane & 3, wm = warp & 1, wk = warp >> 1;
     float *As = smf, *Bs = smf + MM_OPF;
-    // the MMA accumulates 32-deep partials (4 k-steps) that are added into round-to-nearest
-    // FP32 sums, so long contractions (K = 1024 at large batch) keep FP32-level accuracy
-    constexpr int NT8 = K3N / 32;                 // n8 tiles per warp (warps: 2 m16 x 4 n)
+    constexpr int NT8 = K3N / 8;                  // n8 tiles per warp
     float c[NT8][4], cl[NT8][4], cm[NT8][4], cs[NT8][4];   // hi*hi, hi*lo, lo*hi partials; sums
 #pragma unroll
     for (int i = 0; i < NT8; ++i)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) c[i][q] = cl[i][q] = cm[i][q] = cs[i][q] = 0.0f;
+        for (int q = 0; q < 4; ++q) cs[i][q] = 0.0f;
     float rsum = 0.0f;
+    const int mr = 16 * wm + g;
     for (int k0 = kb; k0 < ke; k0 += MM_SK) {
         __syncthreads();   // the previous pass / task is done with the staging buffers
         mm_stage<kARc, BM>(As, a, m0, k0, ke, tid);
@@ -806,8 +810,13 @@ __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int 
         __syncthreads();
         if (tr && k0 == kb) tr->mark(mk);
         const int ksteps = (min(MM_SK, ke - k0) + 7) / 8;
-        const int mr = 16 * wm + g;
-        for (int ks = 0; ks < ksteps; ++ks) {
+#pragma unroll
+        for (int i = 0; i < NT8; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) c[i][q] = cl[i][q] = cm[i][q] = 0.0f;
+        // this warp's k-steps of the pass: at most MM_SK / 32 = 4, one 32-deep chunk of the
+        // round-to-nearest FP32 sums (long contractions keep FP32-level accuracy)
+        for (int ks = wk; ks < ksteps; ks += 4) {
             const int k = 8 * ks;
             uint32_t ah[4], al[4];
             tf32_split(mm_at<kARc>(As, mr, k + t), ah[0], al[0]);
@@ -816,33 +825,39 @@ __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int 
             tf32_split(mm_at<kARc>(As, mr + 8, k + t + 4), ah[3], al[3]);
 #pragma unroll
             for (int nt = 0; nt < NT8; ++nt) {
-                const int nc = (K3N / 4) * wn + 8 * nt + g;
+                const int nc = 8 * nt + g;
                 uint32_t bh[2], bl[2];
                 tf32_split(mm_at<kBRc>(Bs, nc, k + t), bh[0], bl[0]);
                 tf32_split(mm_at<kBRc>(Bs, nc, k + t + 4), bh[1], bl[1]);
                 mma_3xtf32_sep(c[nt], cl[nt], cm[nt], ah, al, bh, bl);
             }
-            if ((ks & 3) == 3 || ks == ksteps - 1) {
-#pragma unroll
-                for (int i = 0; i < NT8; ++i)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        cs[i][q] += acc3_sum(c[i][q], cl[i][q], cm[i][q]);
-                        c[i][q] = cl[i][q] = cm[i][q] = 0.0f;
-                    }
-            }
         }
+#pragma unroll
+        for (int i = 0; i < NT8; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cs[i][q] += acc3_sum(c[i][q], cl[i][q], cm[i][q]);
         if (want_rowsum && tid < BM) {
             const int kn = min(MM_SK, ke - k0);
             for (int k = 0; k < kn; ++k) rsum += mm_at<kARc>(As, tid, k);
         }
     }
     if (tr) tr->mark(mk + 1);
+    // k-residue partials -> shared memory (the staging buffers are free), fixed-order sum
+    __syncthreads();
+    float *red = smf;                                   // [4][BM][K3N + 1]
+    constexpr int RP = K3N + 1;
 #pragma unroll
     for (int nt = 0; nt < NT8; ++nt)
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            epi(m0 + 16 * wm + g + 8 * (q >> 1), n0 + (K3N / 4) * wn + 8 * nt + 2 * t + (q & 1), cs[nt][q]);
+            red[(wk * BM + 16 * wm + g + 8 * (q >> 1)) * RP + 8 * nt + 2 * t + (q & 1)] = cs[nt][q];
+    __syncthreads();
+    for (int e = tid; e < BM * K3N; e += MM_T) {
+        const int m = e / K3N, n = e - m * K3N;
+        const float v = ((red[(0 * BM + m) * RP + n] + red[(1 * BM + m) * RP + n]) +
+                         red[(2 * BM + m) * RP + n]) + red[(3 * BM + m) * RP + n];
+        epi(m0 + m, n0 + n, v);
+    }
     if (want_rowsum && tid < BM) rs(m0 + tid, rsum);
 }
 
@@ -884,8 +899,7 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             auto rs = [&](int m, float v) {
                 if (m < N1) gp[p.b1 + m] = v;
             };
-            gemm_mma_tile<true, true>(a, bo, m0, n0, kb, ke, epi, n0 == 0, rs, k3raw, &trace_, 2);
-            trace_.mark(4);
+            gemm_mma_tile<true, true>(a, bo, m0, n0, kb, ke, epi, n0 == 0, rs, k3raw);
         } else if (t < n_w + n_h) {
             // dH0 partial [s][b][k] = sum_{u in split s} dZ1[b][u] W1[u][k]
             const int u = t - n_w;
@@ -899,49 +913,45 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             float *tile = k3raw + K3_GEMM_FLOATS;          // [BM][K3N + 4] partial dH0
             float *xs = tile + BM * (K3N + 4);              // [BM][XS] states, column D = 1
             constexpr int XS = 36;
-            const Opnd a{p.dZ1, N1, B}, bo{p.online + p.w1, N0, N0};
-            auto epi = [&](int m, int n, float v) { tile[(m - m0) * (K3N + 4) + (n - n0)] = v; };
-            gemm_mma_tile<false, true>(a, bo, m0, n0, kb, ke, epi, false, NoRowsum{}, k3raw, &trace_, 5);
-            __syncthreads();
             const int D = p.D, nb = min(BM, B - m0), nk = min(K3N, N0 - n0);
             float *h0t = xs + BM * XS;                     // [BM][K3N] H0 of the tile (ReLU mask)
+            // the tile's states and H0 (ReLU mask) are requested first: they arrive with the
+            // GEMM operands (whose wait covers them)
+            __syncthreads();   // a previous task of this CTA is done with xs / h0t
             for (int e = threadIdx.x; e < nb * D; e += F_NT3) {
                 const int bb = e / D, d = e - bb * D;
                 cp_async4(xs + bb * XS + d, p.Xs + (int64_t)m0 * D + e);
-            }
-            for (int e = threadIdx.x; e < BM * (XS - D); e += F_NT3) {
-                const int bb = e / (XS - D), d = D + e % (XS - D);
-                xs[bb * XS + d] = (d == D && bb < nb) ? 1.0f : 0.0f;   // ones column -> db0
             }
             for (int e = threadIdx.x; e < nb * (nk / 4); e += F_NT3) {
                 const int bb = e / (nk / 4), q = e % (nk / 4);
                 cp_async16(h0t + bb * K3N + 4 * q, p.H0 + (int64_t)(m0 + bb) * N0 + n0 + 4 * q);
             }
-            cp_async_wait_all();
-            __syncthreads();
-            for (int e = threadIdx.x; e < BM * K3N; e += F_NT3) {
-                const int bb = e / K3N, kk = e % K3N;
-                const bool on = bb < nb && kk < nk && h0t[bb * K3N + kk] > 0.0f;
-                if (!on) tile[bb * (K3N + 4) + kk] = 0.0f;
+            for (int e = threadIdx.x; e < BM * XS; e += F_NT3) {
+                const int bb = e / XS, d = e - bb * XS;
+                if (bb >= nb || d >= D) xs[e] = (d == D && bb < nb) ? 1.0f : 0.0f;   // ones column -> db0
             }
-            if (nb < BM)
-                for (int e = threadIdx.x; e < (BM - nb) * XS; e += F_NT3) xs[nb * XS + e] = 0.0f;
+            for (int e = threadIdx.x; e < (BM - nb) * K3N; e += F_NT3) h0t[nb * K3N + e] = 0.0f;
+            const Opnd a{p.dZ1, N1, B}, bo{p.online + p.w1, N0, N0};
+            auto epi = [&](int m, int n, float v) { tile[(m - m0) * (K3N + 4) + (n - n0)] = v; };
+            gemm_mma_tile<false, true>(a, bo, m0, n0, kb, ke, epi, false, NoRowsum{}, k3raw, &trace_, 2);
             __syncthreads();
-            // dW0 / db0 share: C[unit k][d] = sum_b tile[b][k] xs[b][d] over the tile's rows
-            // (column D of xs is 1 -> db0); thread = (unit kk, 8 consecutive columns)
+            trace_.mark(4);
+            // dW0 / db0 share: C[unit k][d] = sum_b dZ0[b][k] xs[b][d] over the tile's rows with
+            // dZ0 = dH0 * ReLU'(z0) (column D of xs is 1 -> db0); thread = (unit kk, 4
+            // consecutive columns): 8 threads per unit
             float *w0p = p.w0part + ((int64_t)s * ((B + BM - 1) / BM) + m0 / BM) * (p.b0 + N0);
             {
-                // thread = (unit kk, 4 consecutive columns): 8 threads per unit
                 const int kk = threadIdx.x >> 3, d0 = 4 * (threadIdx.x & 7);
                 float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 8
                 for (int bb = 0; bb < BM; ++bb) {
-                    const float z = tile[bb * (K3N + 4) + kk];
+                    const float z = h0t[bb * K3N + kk] > 0.0f ? tile[bb * (K3N + 4) + kk] : 0.0f;
                     const float4 x0 = *reinterpret_cast<const float4 *>(xs + bb * XS + d0);
                     acc[0] = fmaf(z, x0.x, acc[0]); acc[1] = fmaf(z, x0.y, acc[1]);
                     acc[2] = fmaf(z, x0.z, acc[2]); acc[3] = fmaf(z, x0.w, acc[3]);
                 }
                 const int k = n0 + kk;
+                trace_.mark(6);
                 if (kk < nk) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
