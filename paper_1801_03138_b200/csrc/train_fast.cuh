@@ -157,11 +157,11 @@ __device__ __forceinline__ void td_warp(const FastArgs &p, const float *hs, int 
         float qa = 0.0f;
         if (net < p.nets) {
             if (p.dueling) {
-                // Q(s,a) = V(s) + A(s,a) - (1/|A|) sum_a' A(s,a')
-                float mean = 0.0f;
-                for (int k = 0; k < A; ++k) mean += hs[net * hsld + 1 + k];
-                mean /= (float)A;
-                if (lane < A) qa = hs[net * hsld + 0] + hs[net * hsld + 1 + lane] - mean;
+                // Q(s,a) = V(s) + A(s,a) - (1/|A|) sum_a' A(s,a'); the mean by a
+                // fixed shuffle tree over the lanes (A <= 32)
+                const float av = lane < A ? hs[net * hsld + 1 + lane] : 0.0f;
+                const float mean = warp_sum(av) / (float)A;
+                if (lane < A) qa = hs[net * hsld + 0] + av - mean;
             } else if (lane < A) {
                 qa = hs[net * hsld + lane];
             }
@@ -541,19 +541,30 @@ __global__ void __launch_bounds__(NT) fast_td_kernel(const __grid_constant__ Fas
         __syncthreads();
         trace_.mark(4);
         for (int j = tid; j < J; j += NT) p.dHead[(int64_t)b * J + j] = dhs[j];
-        // dZ1[b][u] = (dHead . W_head)[u] * ReLU'(z1[b][u])
-        for (int u = tid; u < N1; u += NT) {
-            float dh = 0.0f;
+        // dZ1[b][u] = (dHead . W_head)[u] * ReLU'(z1[b][u]), 4 consecutive units per thread
+        // (N1 % 4 == 0; a dueling stream boundary S % 4 == 0 never splits a group)
+        for (int u4 = tid; u4 < N1 / 4; u4 += NT) {
+            const int u = 4 * u4;
+            float4 dh = make_float4(0.f, 0.f, 0.f, 0.f);
+            auto acc = [&](float d, const float *w) {
+                const float4 wv = *reinterpret_cast<const float4 *>(w);
+                dh.x = fmaf(d, wv.x, dh.x); dh.y = fmaf(d, wv.y, dh.y);
+                dh.z = fmaf(d, wv.z, dh.z); dh.w = fmaf(d, wv.w, dh.w);
+            };
             if (p.dueling) {
                 if (u < S) {
-                    dh = dhs[0] * Whs[u];
+                    const float4 wv = *reinterpret_cast<const float4 *>(Whs + u);
+                    dh = make_float4(dhs[0] * wv.x, dhs[0] * wv.y, dhs[0] * wv.z, dhs[0] * wv.w);
                 } else {
-                    for (int k = 0; k < A; ++k) dh = fmaf(dhs[1 + k], Whs[(1 + k) * S + (u - S)], dh);
+                    for (int k = 0; k < A; ++k) acc(dhs[1 + k], Whs + (1 + k) * S + (u - S));
                 }
             } else {
-                for (int k = 0; k < A; ++k) dh = fmaf(dhs[k], Whs[k * N1 + u], dh);
+                for (int k = 0; k < A; ++k) acc(dhs[k], Whs + k * N1 + u);
             }
-            p.dZ1[(int64_t)b * N1 + u] = h1s[u] > 0.0f ? dh : 0.0f;
+            const float4 h = *reinterpret_cast<const float4 *>(h1s + u);
+            const float4 z = make_float4(h.x > 0.0f ? dh.x : 0.0f, h.y > 0.0f ? dh.y : 0.0f,
+                                         h.z > 0.0f ? dh.z : 0.0f, h.w > 0.0f ? dh.w : 0.0f);
+            *reinterpret_cast<float4 *>(p.dZ1 + (int64_t)b * N1 + u) = z;
         }
     }
 }

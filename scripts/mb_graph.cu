@@ -5,6 +5,8 @@
 #include <chrono>
 __global__ void k_spin(int ns, int *p)
 {
+    extern __shared__ float smem[];
+    if (ns < -1) smem[threadIdx.x] = 1.0f;
     const long long t0 = clock64();
     while (clock64() - t0 < ns) {}
     if (threadIdx.x == 0 && blockIdx.x == 0 && ns < 0) p[0] = 1;
@@ -15,12 +17,14 @@ int main()
     cudaMalloc(&p, 64);
     cudaStream_t st;
     cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-    for (unsigned flags : {0u, (unsigned)cudaGraphInstantiateFlagDeviceLaunch}) {
+    cudaFuncSetAttribute(k_spin, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024);
+    for (unsigned flags : {0u}) {
         for (int n : {1, 4}) {
             for (int spin : {0, 10000}) {
+              for (int smem : {0, 140 * 1024}) {
                 cudaGraph_t g;
                 cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
-                for (int i = 0; i < n; ++i) k_spin<<<148, 256, 0, st>>>(spin, p);
+                for (int i = 0; i < n; ++i) k_spin<<<148, 256, i == 0 ? smem : 0, st>>>(spin, p);
                 cudaStreamEndCapture(st, &g);
                 cudaGraphExec_t ge;
                 if (cudaGraphInstantiateWithFlags(&ge, g, flags) != cudaSuccess) { printf("inst fail\n"); continue; }
@@ -39,10 +43,11 @@ int main()
                 cudaEventSynchronize(b);
                 float ms;
                 cudaEventElapsedTime(&ms, a, b);
-                printf("flags %u graph of %d kernel(s) spin %5d cyc: %.2f us per launch on device (%.2f us host enqueue)\n", flags, n, spin,
+                printf("smem %6d graph of %d kernel(s) spin %5d cyc: %.2f us per launch on device (%.2f us host enqueue)\n", smem, n, spin,
                        1000.0 * ms / L, std::chrono::duration<double, std::micro>(h1 - h0).count() / L);
                 cudaGraphExecDestroy(ge);
                 cudaGraphDestroy(g);
+              }
             }
         }
     }
