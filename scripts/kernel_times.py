@@ -90,7 +90,7 @@ def trace_main():
     torch.cuda.synchronize()
     tr = dqn.debug(b.RPL_DBG_TRACE, 128).astype(np.int64)
     t0 = min(tr[k][tr[k][:, 0] > 0][:, 0].min() for k in range(4) if (tr[k][:, 0] > 0).any())
-    names = ["K1 fwd+td", "(unused)", "K3 bwd1", "K4 bwd0+sgd"]
+    names = ["K1 fwd", "K2 td", "K3 bwd1", "K4 bwd0+sgd"]
     for k in range(4):
         m = tr[k][:, 0] > 0
         if not m.any():
