@@ -48,6 +48,7 @@ enum {
 /* where replay_add's inputs live (RPL_DEVICE_DEFER: device, ring write may be deferred) */
 enum { RPL_HOST = 0, RPL_DEVICE = 1, RPL_DEVICE_DEFER = 2 };
 enum { RPL_ONLINE = 0, RPL_TARGET = 1, RPL_GRAD = 2 };  /* which parameter vector          */
+enum { RPL_F32 = 0, RPL_U8 = 1 };                        /* state element type of a replay  */
 
 typedef struct rpl_replay rpl_replay;   /* opaque */
 typedef struct rpl_dqn rpl_dqn;         /* opaque */
@@ -63,13 +64,18 @@ typedef struct {
     uint64_t seed;        /* Philox key of the sampler (Q3)                                 */
     uint32_t rank;        /* learner rank, < 2^24; selects an independent sampler stream    */
     int64_t max_host_add; /* largest k accepted from host memory per replay_add (pinned
-                             staging size); 0 = 65536                                       */
+                             staging size); 0 = 65536, capped at 256 MB of staging          */
+    int32_t state_dtype;  /* RPL_F32 (default, the paper's float states) or RPL_U8
+                             (Atari-shaped byte states; the network input is x = u8/255,
+                             SURVEY reading Q27)                                            */
 } rpl_replay_opts;
 
 /* Create an empty FIFO replay of `capacity` experiences whose states are `state_dim`
  * fp32 values ("starts empty"; 1,000,000 x (27+27+3)).  Device layout: one
  * 128-byte-aligned row per slot, [s | s' | a:i32 | r:f32 | terminal:u32 | pad], row
- * stride round_up(2*state_dim+3, 32) floats (256 B for state_dim = 27).
+ * stride round_up(2*state_dim+3, 32) floats (256 B for state_dim = 27).  RPL_U8 replays
+ * store [s u8 | s' u8 | pad to 16 B | a | r | terminal | pad], row stride
+ * round_up(round_up(2*state_dim, 16) + 12, 128) bytes (56,576 B for 84x84x4).
  * opts may be NULL (device 0, default stream, burn_in 1, seed 2, rank 0).
  * Errors: EINVAL (capacity < 1, capacity >= 2^31, state_dim < 1, rank >= 2^24),
  * ENOMEM, ECUDA.  *out owns the device ring until replay_destroy. */
@@ -80,7 +86,8 @@ int replay_destroy(rpl_replay *replay);
 /* Insert k experiences, oldest evicted first: experience j goes to slot
  * (cursor + j) mod capacity; afterwards cursor += k (mod capacity), size = min(size+k,
  * capacity), total += k.  Inputs are SoA: s[k*state_dim], a[k], r[k],
- * s_next[k*state_dim], done[k] in {0,1}.  mem = RPL_HOST: host pointers, copied into
+ * s_next[k*state_dim] (fp32, or u8 for RPL_U8 replays), done[k] in {0,1}.
+ * mem = RPL_HOST: host pointers, copied into
  * pinned staging before return (the caller may reuse them at once); one H2D copy of
  * k*(8*state_dim+9) bytes is counted in replay_state's h2d_bytes -- the only PCIe
  * traffic of the method.  mem = RPL_DEVICE: device pointers that must stay
@@ -96,16 +103,17 @@ int replay_destroy(rpl_replay *replay);
  * Errors: EINVAL (k < 0, k > capacity, k > max_host_add for HOST, null pointer with
  * k > 0), ECORRUPT (HOST done[j] > 1; nothing written).  k = 0 is a no-op.
  * A device-sourced done[j] > 1 is written as 1 and raises the sticky ECORRUPT flag. */
-int replay_add(rpl_replay *replay, int64_t k, const float *s, const int32_t *a,
-               const float *r, const float *s_next, const uint8_t *done, int mem);
+int replay_add(rpl_replay *replay, int64_t k, const void *s, const int32_t *a,
+               const float *r, const void *s_next, const uint8_t *done, int mem);
 
 /* Caller-owned DEVICE buffers receiving an unpacked batch ("unpacked into old
  * state, new state, action, reward and is_terminal Tensors").  Any pointer may be NULL
- * (that tensor is not written).  s, s_next: [B*state_dim] fp32 row-major; a: [B] i32;
- * r: [B] fp32; done: [B] u8; idx: [B] i32 sampled slot indices. */
+ * (that tensor is not written).  s, s_next: [B*state_dim] row-major in the replay's state
+ * type (fp32, or u8 for RPL_U8); a: [B] i32; r: [B] fp32; done: [B] u8; idx: [B] i32
+ * sampled slot indices. */
 typedef struct {
-    float *s;
-    float *s_next;
+    void *s;
+    void *s_next;
     int32_t *a;
     float *r;
     uint8_t *done;
@@ -190,7 +198,8 @@ int dqn_set_params(rpl_dqn *dqn, int which, const float *host_in, int64_t n);
 int dqn_step_count(const rpl_dqn *dqn, int64_t *steps);
 
 /* Debug export of the last train step's device intermediates (synchronises).  `what`:
- *   RPL_DBG_IDX      [B] i32 sampled indices     RPL_DBG_S / RPL_DBG_S_NEXT [B*D] f32
+ *   RPL_DBG_IDX      [B] i32 sampled indices     RPL_DBG_S / RPL_DBG_S_NEXT [B*D] in the
+ *                    replay's state type (f32, or u8 for RPL_U8)
  *   RPL_DBG_A        [B] i32                     RPL_DBG_R [B] f32   RPL_DBG_DONE [B] u8
  *   RPL_DBG_Q        [B*A] f32 Q_online(s)       RPL_DBG_QT_NEXT [B*A] f32 Q_target(s')
  *   RPL_DBG_QO_NEXT  [B*A] f32 Q_online(s') (Double DQN only)

@@ -47,6 +47,22 @@ def experiences(n: int, state_dim: int = 27, n_actions: int = 8, seed: int = 1, 
     return dict(s=s, a=a, r=r, s_next=s2, done=done)
 
 
+ATARI_STATE_DIM = 84 * 84 * 4   # SURVEY config 5: 84x84x4 uint8 frames stacked per state
+
+
+def experiences_u8(n: int, state_dim: int = ATARI_STATE_DIM, n_actions: int = 8, seed: int = 1,
+                   rank: int = 0, done_prob: float = 1.0 / 64.0) -> dict:
+    """n synthetic Atari-shaped experiences (SURVEY config 5): uint8 states uniform over
+    [0, 255], actions / rewards / terminals as in `experiences`."""
+    g = rng(seed, rank, PURPOSE_DATA)
+    s = g.integers(0, 256, size=(n, state_dim), dtype=np.uint8)
+    s2 = g.integers(0, 256, size=(n, state_dim), dtype=np.uint8)
+    r = g.uniform(-1.0, 1.0, size=n).astype(np.float32)
+    a = g.integers(0, n_actions, size=n).astype(np.int32)
+    done = (g.random(n) < done_prob).astype(np.uint8)
+    return dict(s=s, a=a, r=r, s_next=s2, done=done)
+
+
 def layer_shapes(state_dim: int, n_actions: int, hidden, dueling: bool, stream: int = 512):
     """(out, in) of every weight matrix of the parameter blob, in blob order
     (DESIGN.md "Parameter blob"); each W [out x in] is followed by its bias [out]."""

@@ -167,6 +167,95 @@ int oracle_ring_sample(oracle_ring *ring, int64_t burn_in, uint64_t seed, uint32
 }
 
 /* ------------------------------------------------------------------------------------
+ * Byte-state replay (SURVEY config 5: 84x84x4 uint8 Atari-shaped states; the paper's own
+ * rows are floats).  Same FIFO, sampler and gather as above over
+ * separate arrays; the network input is x = u8 / 255 (reading Q27, oracle_u8_input).
+ * ---------------------------------------------------------------------------------- */
+int oracle_ring_u8_init(oracle_ring_u8 *ring, int64_t capacity, int32_t state_dim)
+{
+    if (capacity < 1 || state_dim < 1) return ORACLE_EINVAL;
+    ring->capacity = capacity;
+    ring->state_dim = state_dim;
+    ring->s = (uint8_t *)calloc((size_t)capacity * (size_t)state_dim, 1);
+    ring->s_next = (uint8_t *)calloc((size_t)capacity * (size_t)state_dim, 1);
+    ring->a = (int32_t *)calloc((size_t)capacity, sizeof(int32_t));
+    ring->r = (float *)calloc((size_t)capacity, sizeof(float));
+    ring->done = (uint8_t *)calloc((size_t)capacity, 1);
+    ring->cursor = 0;
+    ring->size = 0;
+    ring->total = 0;
+    ring->events = 0;
+    if (!ring->s || !ring->s_next || !ring->a || !ring->r || !ring->done) {
+        oracle_ring_u8_free(ring);
+        return ORACLE_ENOMEM;
+    }
+    return ORACLE_OK;
+}
+
+void oracle_ring_u8_free(oracle_ring_u8 *ring)
+{
+    free(ring->s); free(ring->s_next); free(ring->a); free(ring->r); free(ring->done);
+    ring->s = ring->s_next = ring->done = NULL;
+    ring->a = NULL;
+    ring->r = NULL;
+}
+
+int oracle_ring_u8_add(oracle_ring_u8 *ring, int64_t k, const uint8_t *s, const int32_t *a,
+                       const float *r, const uint8_t *s_next, const uint8_t *done)
+{
+    const int64_t D = ring->state_dim;
+    if (k < 0 || k > ring->capacity) return ORACLE_EINVAL;
+    for (int64_t j = 0; j < k; ++j)
+        if (done[j] > 1) return ORACLE_ECORRUPT;
+    for (int64_t j = 0; j < k; ++j) {
+        const int64_t c = ring->cursor;
+        memcpy(ring->s + c * D, s + j * D, (size_t)D);
+        memcpy(ring->s_next + c * D, s_next + j * D, (size_t)D);
+        ring->a[c] = a[j];
+        ring->r[c] = r[j];
+        ring->done[c] = done[j];
+        ring->cursor = (ring->cursor + 1) % ring->capacity;
+        if (ring->size < ring->capacity) ring->size += 1;
+        ring->total += 1;
+    }
+    return ORACLE_OK;
+}
+
+int oracle_ring_u8_gather(const oracle_ring_u8 *ring, int32_t batch, const int32_t *idx,
+                          uint8_t *s, int32_t *a, float *r, uint8_t *s_next, uint8_t *done)
+{
+    const int64_t D = ring->state_dim;
+    for (int32_t i = 0; i < batch; ++i) {
+        if (idx[i] < 0 || idx[i] >= ring->size) return ORACLE_EINVAL;
+        const int64_t c = idx[i];
+        memcpy(s + (int64_t)i * D, ring->s + c * D, (size_t)D);
+        memcpy(s_next + (int64_t)i * D, ring->s_next + c * D, (size_t)D);
+        a[i] = ring->a[c];
+        r[i] = ring->r[c];
+        done[i] = ring->done[c];
+    }
+    return ORACLE_OK;
+}
+
+int oracle_ring_u8_sample(oracle_ring_u8 *ring, int64_t burn_in, uint64_t seed, uint32_t rank,
+                          int32_t batch, int32_t *idx, uint8_t *s, int32_t *a, float *r,
+                          uint8_t *s_next, uint8_t *done)
+{
+    if (ring->size < burn_in || ring->size < 1) return ORACLE_NOT_READY;
+    oracle_sample_indices(seed, rank, ring->events, ring->size, batch, idx);
+    ring->events += 1;
+    return oracle_ring_u8_gather(ring, batch, idx, s, a, r, s_next, done);
+}
+
+/* network input of a byte state: x = u8 / 255 (reading Q27), the fp32 nearest the exact
+ * quotient (the double quotient rounded once more cannot hit a float tie: u/255 has the
+ * non-terminating binary expansion 0.(u)(u)(u)... for 0 < u < 255) */
+void oracle_u8_input(int64_t n, const uint8_t *u, float *x)
+{
+    for (int64_t i = 0; i < n; ++i) x[i] = (float)((double)u[i] / 255.0);
+}
+
+/* ------------------------------------------------------------------------------------
  * The Q-network.  Plain MLP (the team's DQN) or the paper's Dueling DQN (P:88,
  * P:92-94 [Deep Q-Network Model]): shared hidden layers, then a V stream and an A stream
  * of `stream` units each, combined as Q(s,a) = V(s) + A(s,a) - (1/|A|) sum_a' A(s,a').

@@ -42,6 +42,29 @@ int oracle_ring_sample(oracle_ring *ring, int64_t burn_in, uint64_t seed, uint32
                        int32_t batch, int32_t *idx, float *s, int32_t *a, float *r,
                        float *s_next, uint8_t *done);
 
+/* byte-state replay (SURVEY config 5) */
+typedef struct {
+    int64_t capacity;
+    int32_t state_dim;
+    uint8_t *s, *s_next; /* capacity x state_dim */
+    int32_t *a;
+    float *r;
+    uint8_t *done;
+    int64_t cursor, size;
+    uint64_t total, events;
+} oracle_ring_u8;
+
+int oracle_ring_u8_init(oracle_ring_u8 *ring, int64_t capacity, int32_t state_dim);
+void oracle_ring_u8_free(oracle_ring_u8 *ring);
+int oracle_ring_u8_add(oracle_ring_u8 *ring, int64_t k, const uint8_t *s, const int32_t *a,
+                       const float *r, const uint8_t *s_next, const uint8_t *done);
+int oracle_ring_u8_gather(const oracle_ring_u8 *ring, int32_t batch, const int32_t *idx,
+                          uint8_t *s, int32_t *a, float *r, uint8_t *s_next, uint8_t *done);
+int oracle_ring_u8_sample(oracle_ring_u8 *ring, int64_t burn_in, uint64_t seed, uint32_t rank,
+                          int32_t batch, int32_t *idx, uint8_t *s, int32_t *a, float *r,
+                          uint8_t *s_next, uint8_t *done);
+void oracle_u8_input(int64_t n, const uint8_t *u, float *x);
+
 typedef struct {
     int32_t state_dim;
     int32_t n_actions;

@@ -56,6 +56,22 @@ class _Ring(C.Structure):
     ]
 
 
+class _RingU8(C.Structure):
+    _fields_ = [
+        ("capacity", C.c_int64),
+        ("state_dim", C.c_int32),
+        ("s", C.c_void_p),
+        ("s_next", C.c_void_p),
+        ("a", C.c_void_p),
+        ("r", C.c_void_p),
+        ("done", C.c_void_p),
+        ("cursor", C.c_int64),
+        ("size", C.c_int64),
+        ("total", C.c_uint64),
+        ("events", C.c_uint64),
+    ]
+
+
 class _Net(C.Structure):
     _fields_ = [
         ("state_dim", C.c_int32),
@@ -100,6 +116,17 @@ def _declare(L):
     L.oracle_ring_sample.argtypes = [C.POINTER(_Ring), C.c_int64, C.c_uint64, C.c_uint32,
                                      C.c_int32, _P, _P, _P, _P, _P, _P]
     L.oracle_ring_sample.restype = C.c_int
+    L.oracle_ring_u8_init.argtypes = [C.POINTER(_RingU8), C.c_int64, C.c_int32]
+    L.oracle_ring_u8_init.restype = C.c_int
+    L.oracle_ring_u8_free.argtypes = [C.POINTER(_RingU8)]
+    L.oracle_ring_u8_add.argtypes = [C.POINTER(_RingU8), C.c_int64, _P, _P, _P, _P, _P]
+    L.oracle_ring_u8_add.restype = C.c_int
+    L.oracle_ring_u8_gather.argtypes = [C.POINTER(_RingU8), C.c_int32, _P, _P, _P, _P, _P, _P]
+    L.oracle_ring_u8_gather.restype = C.c_int
+    L.oracle_ring_u8_sample.argtypes = [C.POINTER(_RingU8), C.c_int64, C.c_uint64, C.c_uint32,
+                                        C.c_int32, _P, _P, _P, _P, _P, _P]
+    L.oracle_ring_u8_sample.restype = C.c_int
+    L.oracle_u8_input.argtypes = [C.c_int64, _P, _P]
     L.oracle_param_count.argtypes = [C.POINTER(_Net)]
     L.oracle_param_count.restype = C.c_int64
     L.oracle_hidden_units.argtypes = [C.POINTER(_Net)]
@@ -231,6 +258,76 @@ class Ring:
                                       _ptr(out["idx"]), _ptr(out["s"]), _ptr(out["a"]),
                                       _ptr(out["r"]), _ptr(out["s_next"]), _ptr(out["done"]))
         return rc, (out if rc == OK else None)
+
+
+class RingU8:
+    """Byte-state replay (SURVEY config 5): oracle_ring_u8_* (same FIFO / sampler / gather
+    as Ring over uint8 states)."""
+
+    def __init__(self, capacity: int, state_dim: int):
+        self._r = _RingU8()
+        rc = lib().oracle_ring_u8_init(C.byref(self._r), capacity, state_dim)
+        if rc != OK:
+            raise ValueError(f"oracle_ring_u8_init rc={rc}")
+        self.state_dim = state_dim
+
+    def __del__(self):
+        if getattr(self, "_r", None) is not None and self._r.s:
+            lib().oracle_ring_u8_free(C.byref(self._r))
+
+    capacity = property(lambda self: self._r.capacity)
+    cursor = property(lambda self: self._r.cursor)
+    size = property(lambda self: self._r.size)
+    total = property(lambda self: self._r.total)
+
+    @property
+    def events(self):
+        return self._r.events
+
+    @events.setter
+    def events(self, v):
+        self._r.events = v
+
+    def add(self, s, a, r, s_next, done) -> int:
+        D = self.state_dim
+        s = _c(s, np.uint8).reshape(-1, D)
+        return lib().oracle_ring_u8_add(C.byref(self._r), s.shape[0], _ptr(s), _ptr(_c(a, np.int32)),
+                                        _ptr(_c(r, np.float32)),
+                                        _ptr(_c(s_next, np.uint8).reshape(-1, D)),
+                                        _ptr(_c(done, np.uint8)))
+
+    def _batch(self, B):
+        D = self.state_dim
+        return dict(idx=np.zeros(B, np.int32), s=np.zeros((B, D), np.uint8),
+                    a=np.zeros(B, np.int32), r=np.zeros(B, np.float32),
+                    s_next=np.zeros((B, D), np.uint8), done=np.zeros(B, np.uint8))
+
+    def gather(self, idx):
+        idx = _c(idx, np.int32)
+        out = self._batch(idx.shape[0])
+        rc = lib().oracle_ring_u8_gather(C.byref(self._r), idx.shape[0], _ptr(idx), _ptr(out["s"]),
+                                         _ptr(out["a"]), _ptr(out["r"]), _ptr(out["s_next"]),
+                                         _ptr(out["done"]))
+        if rc != OK:
+            raise ValueError(f"oracle_ring_u8_gather rc={rc}")
+        out["idx"] = idx
+        return out
+
+    def sample(self, burn_in: int, seed: int, rank: int, batch: int):
+        """Returns (rc, batch dict or None)."""
+        out = self._batch(batch)
+        rc = lib().oracle_ring_u8_sample(C.byref(self._r), burn_in, seed, rank, batch,
+                                         _ptr(out["idx"]), _ptr(out["s"]), _ptr(out["a"]),
+                                         _ptr(out["r"]), _ptr(out["s_next"]), _ptr(out["done"]))
+        return rc, (out if rc == OK else None)
+
+
+def u8_input(u) -> np.ndarray:
+    """oracle_u8_input: the network input x = u8 / 255 of byte states (reading Q27)."""
+    u = _c(u, np.uint8)
+    x = np.empty(u.shape, np.float32)
+    lib().oracle_u8_input(u.size, _ptr(u), _ptr(x))
+    return x
 
 
 # ------------------------------------------------------------------------------------

@@ -25,6 +25,7 @@ RPL_EINVAL, RPL_ENOMEM, RPL_ECORRUPT, RPL_ENUMERIC = -1, -2, -3, -4
 RPL_ECUDA, RPL_ENCCL, RPL_ESTATE = -5, -6, -7
 RPL_HOST, RPL_DEVICE, RPL_DEVICE_DEFER = 0, 1, 2
 RPL_ONLINE, RPL_TARGET, RPL_GRAD = 0, 1, 2
+RPL_F32, RPL_U8 = 0, 1
 (RPL_DBG_IDX, RPL_DBG_S, RPL_DBG_S_NEXT, RPL_DBG_A, RPL_DBG_R, RPL_DBG_DONE, RPL_DBG_Q,
  RPL_DBG_QT_NEXT, RPL_DBG_QO_NEXT, RPL_DBG_Y, RPL_DBG_ASTAR, RPL_DBG_H, RPL_DBG_LOSS,
  RPL_DBG_TRACE) = range(14)
@@ -46,7 +47,8 @@ class RplError(RuntimeError):
 
 class _ReplayOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("cuda_stream", C.c_void_p), ("burn_in", C.c_int64),
-                ("seed", C.c_uint64), ("rank", C.c_uint32), ("max_host_add", C.c_int64)]
+                ("seed", C.c_uint64), ("rank", C.c_uint32), ("max_host_add", C.c_int64),
+                ("state_dtype", C.c_int32)]
 
 
 class _Batch(C.Structure):
@@ -143,14 +145,19 @@ class Replay:
     """Handle of the device FIFO replay (``replay_create``)."""
 
     def __init__(self, capacity: int, state_dim: int, *, device: int = 0, stream=None,
-                 burn_in: int = 1, seed: int = 2, rank: int = 0, max_host_add: int = 0):
+                 burn_in: int = 1, seed: int = 2, rank: int = 0, max_host_add: int = 0,
+                 state_dtype: str = "f32"):
         torch = _torch()
         if not torch.cuda.is_available():
             raise RplError(RPL_ECUDA, "no CUDA device (the in-GPU replay has no CPU fallback)")
         self.device = device
+        self.u8 = state_dtype == "u8"
+        self.state_np = np.uint8 if self.u8 else np.float32
+        self.state_torch = torch.uint8 if self.u8 else torch.float32
         with torch.cuda.device(device):
             self._stream = _stream_handle(stream)
-        o = _ReplayOpts(device, self._stream, burn_in, seed, rank, max_host_add)
+        o = _ReplayOpts(device, self._stream, burn_in, seed, rank, max_host_add,
+                        RPL_U8 if self.u8 else RPL_F32)
         h = C.c_void_p()
         _ok(_L.replay_create(capacity, state_dim, C.byref(o), C.byref(h)))
         self._h = h
@@ -175,17 +182,18 @@ class Replay:
         if isinstance(s, torch.Tensor) and s.is_cuda:
             ts = [s.contiguous(), a.contiguous(), r.contiguous(), s_next.contiguous(),
                   done.contiguous()]
-            assert ts[0].dtype == torch.float32 and ts[1].dtype == torch.int32
+            assert ts[0].dtype == self.state_torch and ts[3].dtype == self.state_torch
+            assert ts[1].dtype == torch.int32
             assert ts[2].dtype == torch.float32 and ts[4].dtype == torch.uint8
             k = ts[1].numel()
             rc = _ok(_L.replay_add(self._h, k, *[_dptr(t) for t in ts],
                                    RPL_DEVICE_DEFER if defer else RPL_DEVICE))
             self._deferred = ts if defer else None
             return rc
-        arrs = [np.ascontiguousarray(np.asarray(s), np.float32),
+        arrs = [np.ascontiguousarray(np.asarray(s), self.state_np),
                 np.ascontiguousarray(np.asarray(a), np.int32),
                 np.ascontiguousarray(np.asarray(r), np.float32),
-                np.ascontiguousarray(np.asarray(s_next), np.float32),
+                np.ascontiguousarray(np.asarray(s_next), self.state_np),
                 np.ascontiguousarray(np.asarray(done), np.uint8)]
         k = arrs[1].size
         return _ok(_L.replay_add(self._h, k, *[x.ctypes.data_as(C.c_void_p) for x in arrs],
@@ -203,7 +211,9 @@ class Replay:
         if out is None:
             dev = torch.device("cuda", self.device)
             D = self.state_dim
-            out = dict(s=torch.empty(n, D, device=dev), s_next=torch.empty(n, D, device=dev),
+            st = self.state_torch
+            out = dict(s=torch.empty(n, D, dtype=st, device=dev),
+                       s_next=torch.empty(n, D, dtype=st, device=dev),
                        a=torch.empty(n, dtype=torch.int32, device=dev),
                        r=torch.empty(n, device=dev),
                        done=torch.empty(n, dtype=torch.uint8, device=dev),
@@ -307,8 +317,11 @@ class DQN:
 
     def train_step(self, replay: Replay, batch: int, loss_out=None) -> int:
         """dqn_train_step; returns RPL_OK or RPL_NOT_READY (burn-in)."""
-        return _ok(_L.dqn_train_step(self._h, replay._h, batch, _dptr(loss_out)),
-                   (RPL_OK, RPL_NOT_READY))
+        st = _ok(_L.dqn_train_step(self._h, replay._h, batch, _dptr(loss_out)),
+                 (RPL_OK, RPL_NOT_READY))
+        if st == RPL_OK:
+            self._last_u8 = replay.u8
+        return st
 
     def sync_target(self):
         _ok(_L.sync_target(self._h))
@@ -330,8 +343,9 @@ class DQN:
 
     def debug(self, what: int, batch: int, hidden_units: int = 0) -> np.ndarray:
         D, A = self.cfg.state_dim, self.cfg.n_actions
-        spec = {RPL_DBG_IDX: (np.int32, (batch,)), RPL_DBG_S: (np.float32, (batch, D)),
-                RPL_DBG_S_NEXT: (np.float32, (batch, D)), RPL_DBG_A: (np.int32, (batch,)),
+        sd = np.uint8 if getattr(self, "_last_u8", False) else np.float32
+        spec = {RPL_DBG_IDX: (np.int32, (batch,)), RPL_DBG_S: (sd, (batch, D)),
+                RPL_DBG_S_NEXT: (sd, (batch, D)), RPL_DBG_A: (np.int32, (batch,)),
                 RPL_DBG_R: (np.float32, (batch,)), RPL_DBG_DONE: (np.uint8, (batch,)),
                 RPL_DBG_Q: (np.float32, (batch, A)), RPL_DBG_QT_NEXT: (np.float32, (batch, A)),
                 RPL_DBG_QO_NEXT: (np.float32, (batch, A)), RPL_DBG_Y: (np.float32, (batch,)),

@@ -35,10 +35,14 @@ constexpr int MAXL = 5;   // trunk layers (4 shared + dueling stream layer)
 constexpr int MAXA = 32;  // actions (one warp)
 constexpr int MAXJ = MAXA + 1;
 
+constexpr int kWideInput = 1024;   // state_dim above which layer 0 is split-K (wide inputs)
+constexpr int kKs0Max = 16;        // layer-0 split-K chunks at most
+
 struct TrainArgs {
     // replay
     const float *ring;
     int rs, D;
+    int u8, so;            // byte states (x = u8 / 255, reading Q27); scalars at byte `so`
     int64_t size;
     uint64_t seed, event;
     uint32_t rank;
@@ -69,6 +73,8 @@ struct TrainArgs {
     int32_t *astar;
     float *loss_out;
     int apply_update, do_sync;
+    int ks0;               // split-K of the layer-0 forward (wide inputs): partials in PF0
+    float *PF0;            // [ks0][nets][B][N0]
     unsigned *bar;         // [0] arrivals, [1] generation
     uint32_t *err;
     uint64_t *rctrl;       // replay control block: [0] events, [1] size
@@ -144,6 +150,32 @@ struct LdDz {
     }
 };
 
+// byte-state operands (RPL_U8 replays): x = u8 / 255 (reading Q27), an exactly rounded fp32
+// quotient.  Gathered ring rows (m = sample, k = input), and the unpacked batch [B][D]
+// read as (r = input, kk = sample) for dW0.
+__device__ __forceinline__ float u8_input(uint8_t v) { return __fdiv_rn((float)v, 255.0f); }
+struct LdRingU8 {
+    static constexpr bool kKContig = true;
+    const uint8_t *ring;
+    const int *idx_s;
+    int m0;
+    int64_t rsb;
+    int col0, R, KE;
+    __device__ float operator()(int m, int k) const
+    {
+        return (m < R && k < KE) ? u8_input(__ldg(ring + (int64_t)idx_s[m - m0] * rsb + col0 + k)) : 0.0f;
+    }
+};
+struct LdRMajorU8 {
+    static constexpr bool kKContig = false;
+    const uint8_t *p;
+    int ld, R, KB, KE;
+    __device__ float operator()(int r, int kk) const
+    {
+        return (r < R && kk >= KB && kk < KE) ? u8_input(__ldcg(p + (int64_t)kk * ld + r)) : 0.0f;
+    }
+};
+
 // ------------------------------------------------------------------------------------------
 // phases
 // ------------------------------------------------------------------------------------------
@@ -152,26 +184,37 @@ __device__ __forceinline__ const float *net_params(const TrainArgs &p, int net)
     return net == 1 ? p.target : p.online;
 }
 
-// F0 / Fl: forward of trunk layer l for every needed net
+// F0 / Fl: forward of trunk layer l for every needed net.  Layer 0 samples + gathers its
+// rows; with a wide input (ks0 > 1) its contraction is split into ks0 chunks whose partial
+// sums go to PF0 and are reduced (+ bias, ReLU) by phase_l0_reduce after a grid barrier.
 __device__ void phase_forward(const TrainArgs &p, int l, TileSmem &sm)
 {
     const int N = p.N[l], K = p.K[l], B = p.B;
     const int mt = (B + BM - 1) / BM, nt = (N + BN - 1) / BN;
-    const int ntasks = p.nets * mt * nt;
+    const int ks = l == 0 ? p.ks0 : 1;
+    const int kchunk = ((K + ks - 1) / ks + BK - 1) / BK * BK;
+    const int ntasks = p.nets * mt * nt * ks;
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
-        const int net = t / (mt * nt), rem = t % (mt * nt);
+        const int kq = t / (p.nets * mt * nt), tt = t % (p.nets * mt * nt);
+        const int net = tt / (mt * nt), rem = tt % (mt * nt);
         const int m0 = (rem / nt) * BM, n0 = (rem % nt) * BN;
+        const int kb = kq * kchunk, ke = min(K, kb + kchunk);
         const float *theta = net_params(p, net);
         const float *W = theta + p.woff[l];
         const float *bias = theta + p.boff[l];
         float *Hout = p.H[l] + (int64_t)net * B * N;
+        float *Pout = ks > 1 ? p.PF0 + ((int64_t)kq * p.nets + net) * B * N : nullptr;
         auto epi = [&](int m, int n, float v) {
             if (m < B && n < N) {
-                v += __ldg(bias + n);
-                Hout[(int64_t)m * N + n] = v > 0.0f ? v : 0.0f;
+                if (Pout) {
+                    Pout[(int64_t)m * N + n] = v;
+                } else {
+                    v += __ldg(bias + n);
+                    Hout[(int64_t)m * N + n] = v > 0.0f ? v : 0.0f;
+                }
             }
         };
-        LdKMajor lw{W, K, N, K};
+        LdKMajor lw{W, K, N, ke};
         if (l == 0) {
             // sample (Philox, event E) + gather: the batch rows m0..m0+BM
             __syncthreads();
@@ -183,31 +226,65 @@ __device__ void phase_forward(const TrainArgs &p, int l, TileSmem &sm)
                 sm.idx[2 * threadIdx.x + 1] = i1;
             }
             __syncthreads();
-            const int col0 = (net == 0) ? 0 : p.D;   // s for online(s), s' for the others
-            LdRing lx{p.ring, sm.idx, m0, p.rs, col0, B, p.D};
+            const int D = p.D;
+            const int col0 = (net == 0) ? 0 : D;   // s for online(s), s' for the others
             // unpack the batch once (online(s) / target(s') tasks of the first column tile)
-            if (n0 == 0 && net <= 1) {
-                const int D = p.D;
-                for (int e = threadIdx.x; e < BM * D; e += NT) {
-                    const int r = e / D, c = e % D;
-                    if (m0 + r < B)
-                        (net == 0 ? p.Xs : p.Xs2)[(int64_t)(m0 + r) * D + c] =
-                            __ldg(p.ring + (int64_t)sm.idx[r] * p.rs + col0 + c);
+            if (n0 == 0 && net <= 1 && kq == 0) {
+                if (p.u8) {
+                    const uint8_t *rb = reinterpret_cast<const uint8_t *>(p.ring);
+                    uint8_t *xo = reinterpret_cast<uint8_t *>(net == 0 ? p.Xs : p.Xs2);
+                    for (int e = threadIdx.x; e < BM * D; e += NT) {
+                        const int r = e / D, c = e % D;
+                        if (m0 + r < B)
+                            xo[(int64_t)(m0 + r) * D + c] = __ldg(rb + (int64_t)sm.idx[r] * p.rs * 4 + col0 + c);
+                    }
+                } else {
+                    for (int e = threadIdx.x; e < BM * D; e += NT) {
+                        const int r = e / D, c = e % D;
+                        if (m0 + r < B)
+                            (net == 0 ? p.Xs : p.Xs2)[(int64_t)(m0 + r) * D + c] =
+                                __ldg(p.ring + (int64_t)sm.idx[r] * p.rs + col0 + c);
+                    }
                 }
                 if (net == 0 && threadIdx.x < BM && m0 + threadIdx.x < B) {
                     const int r = threadIdx.x, b = m0 + r;
-                    const float *row = p.ring + (int64_t)sm.idx[r] * p.rs + 2 * D;
+                    const float *row = p.u8 ? reinterpret_cast<const float *>(
+                                                  reinterpret_cast<const uint8_t *>(p.ring) +
+                                                  (int64_t)sm.idx[r] * p.rs * 4 + p.so)
+                                            : p.ring + (int64_t)sm.idx[r] * p.rs + 2 * D;
                     p.idx[b] = sm.idx[r];
                     p.a[b] = __float_as_int(__ldg(row));
                     p.r[b] = __ldg(row + 1);
                     p.done[b] = (uint8_t)(__float_as_uint(__ldg(row + 2)) != 0u);
                 }
             }
-            gemm_tile(lx, lw, m0, n0, 0, K, epi, false, NoRowsum{}, sm);
+            if (p.u8) {
+                LdRingU8 lx{reinterpret_cast<const uint8_t *>(p.ring), sm.idx, m0, (int64_t)p.rs * 4,
+                            col0, B, ke};
+                gemm_tile(lx, lw, m0, n0, kb, ke, epi, false, NoRowsum{}, sm);
+            } else {
+                LdRing lx{p.ring, sm.idx, m0, p.rs, col0, B, ke};
+                gemm_tile(lx, lw, m0, n0, kb, ke, epi, false, NoRowsum{}, sm);
+            }
         } else {
             LdKMajor lh{p.H[l - 1] + (int64_t)net * B * K, K, B, K};
             gemm_tile(lh, lw, m0, n0, 0, K, epi, false, NoRowsum{}, sm);
         }
+    }
+}
+
+// layer-0 split-K reduction: H0 = ReLU(sum_q PF0[q] + b0), partials added in chunk order
+__device__ void phase_l0_reduce(const TrainArgs &p)
+{
+    const int N = p.N[0], B = p.B;
+    const int64_t per_net = (int64_t)B * N, total = (int64_t)p.nets * per_net;
+    const int64_t stride = (int64_t)gridDim.x * NT;
+    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < total; i += stride) {
+        const int net = (int)(i / per_net), n = (int)(i % N);
+        float v = 0.0f;
+        for (int q = 0; q < p.ks0; ++q) v += __ldcg(p.PF0 + (int64_t)q * total + i);
+        v += __ldg(net_params(p, net) + p.boff[0] + n);
+        p.H[0][i] = v > 0.0f ? v : 0.0f;
     }
 }
 
@@ -348,14 +425,19 @@ __device__ void phase_backward(const TrainArgs &p, int l, TileSmem &sm)
             const int kb = s * p.bsplit, ke = min(B, kb + p.bsplit);
             float *gp = p.gpart + (int64_t)s * p.P;
             LdDzT la{&p, l, N, kb, ke};
-            LdRMajor lb{Hprev, K, K, kb, ke};
             auto epi = [&](int m, int n, float v) {
                 if (m < N && n < K) gp[p.woff[l] + (int64_t)m * K + n] = v;
             };
             auto rs = [&](int m, float v) {
                 if (m < N) gp[p.boff[l] + m] = v;
             };
-            gemm_tile(la, lb, m0, n0, kb, ke, epi, n0 == 0, rs, sm);
+            if (l == 0 && p.u8) {
+                LdRMajorU8 lb{reinterpret_cast<const uint8_t *>(Hprev), K, K, kb, ke};
+                gemm_tile(la, lb, m0, n0, kb, ke, epi, n0 == 0, rs, sm);
+            } else {
+                LdRMajor lb{Hprev, K, K, kb, ke};
+                gemm_tile(la, lb, m0, n0, kb, ke, epi, n0 == 0, rs, sm);
+            }
         } else if (t < n_w + n_h) {
             const int u = t - n_w;
             const int s = u / (hmt * hnt), rem = u % (hmt * hnt);
@@ -475,6 +557,10 @@ __global__ void __launch_bounds__(NT, 1) train_step_kernel(const __grid_constant
     for (int l = 0; l < p.T; ++l) {
         phase_forward(p, l, sm);
         grid_barrier(p.bar);
+        if (l == 0 && p.ks0 > 1) {
+            phase_l0_reduce(p);
+            grid_barrier(p.bar);
+        }
     }
     phase_head(p, sm);
     grid_barrier(p.bar);
@@ -574,6 +660,9 @@ struct rpl_dqn {
     int64_t gpart_elems = 0, pdh_elems[MAXL] = {};
     int64_t steps = 0;
     int last_B = 0;
+    int last_u8 = 0;                 // the last step's replay stores byte states
+    // wide inputs: layer-0 forward split-K partials [kKs0Max][nets][max_batch][N0]
+    float *PF0 = nullptr;
     // fast path (two trunk layers): head partials, dH0 split-K partials, device counters
     bool fast = false;
     float *part = nullptr, *dH0p = nullptr;
@@ -784,6 +873,8 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
          dalloc(d, &d->Qs, (size_t)Bm * A) && dalloc(d, &d->Qt2, (size_t)Bm * A) &&
          dalloc(d, &d->Qo2, (size_t)Bm * A) && dalloc(d, &d->y, Bm) && dalloc(d, &d->loss_dev, 1) &&
          dalloc(d, &d->bar, 2) && dalloc(d, &d->err, 1);
+    if (ok && D > kWideInput)
+        ok = dalloc(d, &d->PF0, (size_t)kKs0Max * nets * Bm * d->N[0]);
     for (int l = 0; l < d->T && ok; ++l) {
         ok = dalloc(d, &d->H[l], (size_t)nets * Bm * d->N[l]);
         if (ok && l > 0) {
@@ -866,6 +957,20 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
     return RPL_OK;
 }
 
+// split-K of the layer-0 forward for wide inputs: as many chunks as fill the grid in one
+// wave (the state_dim > kWideInput case, e.g. 84x84x4 byte states)
+static int ks0_for(const rpl_dqn *d, int B)
+{
+    if (d->cfg.state_dim <= kWideInput) return 1;
+    const int nets = d->cfg.double_dqn ? 3 : 2;
+    const int base = nets * ((B + BM - 1) / BM) * ((d->N[0] + BN - 1) / BN);
+    int ks = d->sms / base;
+    const int maxk = (d->cfg.state_dim + BK - 1) / BK;
+    if (ks > kKs0Max) ks = kKs0Max;
+    if (ks > maxk) ks = maxk;
+    return ks < 1 ? 1 : ks;
+}
+
 static void fill_args(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int apply, int do_sync,
                       TrainArgs &p)
 {
@@ -873,6 +978,8 @@ static void fill_args(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.ring = rp->ring.rows;
     p.rs = rp->ring.rs;
     p.D = rp->ring.D;
+    p.u8 = rp->ring.u8;
+    p.so = rp->ring.so;
     p.size = rp->size;
     p.seed = rp->seed;
     p.event = rp->events;
@@ -926,6 +1033,8 @@ static void fill_args(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.loss_out = loss_dev ? loss_dev : d->loss_dev;
     p.apply_update = apply;
     p.do_sync = do_sync;
+    p.ks0 = ks0_for(d, B);
+    p.PF0 = d->PF0;
     p.bar = d->bar;
     p.err = d->err;
     p.rctrl = rp->ctrl_dev;
@@ -1003,8 +1112,8 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
         p.pend_k = (int)q.k;
         p.pend_cur = q.cursor;
         p.pend_size = (uint64_t)q.new_size;
-        p.pend_s = q.s;
-        p.pend_s2 = q.s2;
+        p.pend_s = static_cast<const float *>(q.s);
+        p.pend_s2 = static_cast<const float *>(q.s2);
         p.pend_r = q.r;
         p.pend_a = q.a;
         p.pend_done = q.done;
@@ -1060,7 +1169,8 @@ static int grid_for(const rpl_dqn *d, const TrainArgs &p)
     // the largest phase task count, capped at one CTA per SM
     int64_t mx = 1;
     for (int l = 0; l < p.T; ++l) {
-        const int64_t f = (int64_t)p.nets * ((p.B + BM - 1) / BM) * ((p.N[l] + BN - 1) / BN);
+        const int64_t f = (int64_t)p.nets * ((p.B + BM - 1) / BM) * ((p.N[l] + BN - 1) / BN) *
+                          (l == 0 ? p.ks0 : 1);
         const int64_t w = (int64_t)((p.N[l] + BM - 1) / BM) * ((p.K[l] + BN - 1) / BN) * p.nsplit_b;
         const int64_t h = l > 0 ? (int64_t)((p.B + BM - 1) / BM) * ((p.K[l] + BN - 1) / BN) * p.nsplit_n[l] : 0;
         mx = std::max(mx, std::max(f, w + h));
@@ -1088,13 +1198,14 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
     cudaError_t e = cudaSuccess;
     // a deferred insert is consumed by the fast path's K1 on the shared stream; otherwise it
     // is written now by the insert kernel
-    if (!d->fast || rp->stream != d->stream) {
+    const bool fast = d->fast && !rp->ring.u8;   // the fast kernels read fp32 rows
+    if (!fast || rp->stream != d->stream) {
         if (int rc = replay_flush(rp)) {
             if (prev >= 0) cudaSetDevice(prev);
             return rc;
         }
     }
-    if (d->fast) {
+    if (fast) {
         FastArgs fp;
         fill_fast(d, rp, batch, dp ? nullptr : loss_dev, dp ? 0 : 1, fp);
         rp->pend.k = 0;
@@ -1196,6 +1307,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
     rp->events += 1;
     d->steps = t;
     d->last_B = batch;
+    d->last_u8 = rp->ring.u8;
     return RPL_OK;
 }
 
@@ -1255,8 +1367,8 @@ extern "C" int dqn_debug_export(rpl_dqn *d, int what, void *host_out, int64_t by
     int64_t need = 0;
     switch (what) {
     case RPL_DBG_IDX: src = d->idx; need = B * 4; break;
-    case RPL_DBG_S: src = d->Xs; need = B * D * 4; break;
-    case RPL_DBG_S_NEXT: src = d->Xs2; need = B * D * 4; break;
+    case RPL_DBG_S: src = d->Xs; need = B * D * (d->last_u8 ? 1 : 4); break;
+    case RPL_DBG_S_NEXT: src = d->Xs2; need = B * D * (d->last_u8 ? 1 : 4); break;
     case RPL_DBG_A: src = d->a; need = B * 4; break;
     case RPL_DBG_R: src = d->r; need = B * 4; break;
     case RPL_DBG_DONE: src = d->done; need = B; break;

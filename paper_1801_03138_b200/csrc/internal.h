@@ -42,14 +42,20 @@ constexpr uint32_t TAG_SAMPLE = 1u;
 // ---- the replay ring ---------------------------------------------------------------------
 // Device row layout: row stride RS floats (multiple of 32,
 // i.e. 128-byte aligned rows):  [ s (D f32) | s' (D f32) | a (i32) | r (f32) | done (u32) | 0 ]
+// RPL_U8 rings (byte states, SURVEY config 5): row = [s u8 (D) | s' u8 (D) | pad to 16 B |
+// a | r | done | pad], row stride a multiple of 128 B; `so` is the byte offset of a.
 struct Ring {
-    float *rows = nullptr;     // capacity * rs floats
+    float *rows = nullptr;     // capacity * rs words
     int64_t capacity = 0;
     int32_t D = 0;
-    int32_t rs = 0;            // row stride in floats
+    int32_t rs = 0;            // row stride in 4-byte words
+    int32_t u8 = 0;            // states stored as bytes
+    int32_t so = 0;            // u8 rings: byte offset of the scalars (a, r, done)
 };
 
 inline int32_t ring_row_stride(int32_t D) { return ((2 * D + 3) + 31) / 32 * 32; }
+inline int32_t ring_u8_scalar_offset(int32_t D) { return (2 * D + 15) / 16 * 16; }
+inline int32_t ring_u8_row_bytes(int32_t D) { return (ring_u8_scalar_offset(D) + 12 + 127) / 128 * 128; }
 
 }  // namespace rpl
 
@@ -79,7 +85,8 @@ struct rpl_replay {
     // mirror (cursor / size / total) already includes it.
     struct Pending {
         int64_t k = 0, cursor = 0, new_size = 0;
-        const float *s = nullptr, *s2 = nullptr, *r = nullptr;
+        const void *s = nullptr, *s2 = nullptr;   // fp32 (or u8) states
+        const float *r = nullptr;
         const int32_t *a = nullptr;
         const uint8_t *done = nullptr;
     } pend;

@@ -259,6 +259,106 @@ __global__ void __launch_bounds__(GS_W * 32) gather_staged_kernel(
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// RPL_U8 rings (Atari-shaped byte states, SURVEY config 5): rows of round_up(2D, 16) + 12
+// bytes padded to 128 B.  One CTA per experience: the states move as 16-byte vectors (four
+// loads in flight per thread before their stores) when both sides are 16-byte aligned.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void copy_bytes_cta(uint8_t *__restrict__ dst, const uint8_t *__restrict__ src,
+                                               int64_t nbytes)
+{
+    const int tid = threadIdx.x, nt = blockDim.x;
+    if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+        const int64_t n16 = nbytes >> 4;
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+        int64_t i = tid;
+        for (; i + 3 * nt < n16; i += 4 * nt) {
+            const uint4 v0 = __ldg(s4 + i), v1 = __ldg(s4 + i + nt), v2 = __ldg(s4 + i + 2 * nt),
+                        v3 = __ldg(s4 + i + 3 * nt);
+            d4[i] = v0;
+            d4[i + nt] = v1;
+            d4[i + 2 * nt] = v2;
+            d4[i + 3 * nt] = v3;
+        }
+        for (; i < n16; i += nt) d4[i] = __ldg(s4 + i);
+        for (int64_t b = (n16 << 4) + tid; b < nbytes; b += nt) dst[b] = src[b];
+    } else {
+        for (int64_t b = tid; b < nbytes; b += nt) dst[b] = src[b];
+    }
+}
+
+__global__ void __launch_bounds__(256) insert_u8_kernel(uint8_t *__restrict__ rows, int64_t rsb, int so,
+                                                        int D, int64_t capacity, int64_t cursor,
+                                                        int64_t k, const uint8_t *__restrict__ s,
+                                                        const int32_t *__restrict__ a,
+                                                        const float *__restrict__ r,
+                                                        const uint8_t *__restrict__ s2,
+                                                        const uint8_t *__restrict__ done, uint32_t *err,
+                                                        uint64_t *ctrl, int64_t new_size)
+{
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctrl[1] = (uint64_t)new_size;
+    for (int64_t j = blockIdx.x; j < k; j += gridDim.x) {
+        int64_t slot = cursor + j;
+        if (slot >= capacity) slot -= capacity;   // k <= capacity, cursor < capacity
+        uint8_t *row = rows + slot * rsb;
+        copy_bytes_cta(row, s + j * D, D);
+        copy_bytes_cta(row + D, s2 + j * D, D);
+        for (int b = 2 * D + threadIdx.x; b < so; b += blockDim.x) row[b] = 0;
+        if (threadIdx.x == 0) {
+            uint32_t d = done[j];
+            if (d > 1u) {   // a device-sourced done > 1 is stored as 1 and flagged
+                atomicOr(err, ERRBIT_CORRUPT);
+                d = 1u;
+            }
+            uint32_t *sc = reinterpret_cast<uint32_t *>(row + so);
+            sc[0] = (uint32_t)a[j];
+            sc[1] = __float_as_uint(r[j]);
+            sc[2] = d;
+        }
+    }
+}
+
+// Philox sample (or caller indices) + gather + unpack of byte-state rows: one CTA per entry
+__global__ void __launch_bounds__(256) gather_u8_kernel(const uint8_t *__restrict__ rows, int64_t rsb,
+                                                        int so, int D, int64_t size, int64_t n,
+                                                        const int32_t *__restrict__ idx_in,
+                                                        uint64_t seed, uint32_t rank, uint64_t event,
+                                                        uint8_t *s, uint8_t *s2, int32_t *a, float *r,
+                                                        uint8_t *done, int32_t *idx_out, uint32_t *err,
+                                                        uint64_t *ctrl)
+{
+    __shared__ int32_t ix_s;
+    if (idx_in == nullptr && ctrl && blockIdx.x == 0 && threadIdx.x == 0) ctrl[0] = event + 1;
+    for (int64_t e = blockIdx.x; e < n; e += gridDim.x) {
+        if (threadIdx.x == 0) {
+            int32_t ix;
+            if (idx_in == nullptr) {
+                int32_t i0, i1;
+                sample_pair(seed, rank, event, (uint32_t)(e >> 1), (uint64_t)size, i0, i1);
+                ix = (e & 1) ? i1 : i0;
+            } else {
+                ix = idx_in[e];
+                if (ix < 0 || ix >= size) {
+                    atomicOr(err, ERRBIT_RANGE);
+                    ix = min(max(ix, 0), (int32_t)size - 1);
+                }
+            }
+            ix_s = ix;
+            if (idx_out) idx_out[e] = ix;
+            const uint32_t *sc = reinterpret_cast<const uint32_t *>(rows + (int64_t)ix * rsb + so);
+            if (a) a[e] = (int32_t)__ldg(sc);
+            if (r) r[e] = __uint_as_float(__ldg(sc + 1));
+            if (done) done[e] = (uint8_t)(__ldg(sc + 2) != 0u);
+        }
+        __syncthreads();
+        const uint8_t *row = rows + (int64_t)ix_s * rsb;
+        if (s) copy_bytes_cta(s + e * D, row, D);
+        if (s2) copy_bytes_cta(s2 + e * D, row + D, D);
+        __syncthreads();   // ix_s reuse
+    }
+}
+
 const void *insert_kernel_ptr() { return (const void *)insert_kernel; }
 
 int replay_flush(rpl_replay *rp)
@@ -271,10 +371,19 @@ int replay_flush(rpl_replay *rp)
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, rp->device);
     int64_t blocks = (k + 7) / 8;
     if (blocks > (int64_t)dev_sms * 8) blocks = (int64_t)dev_sms * 8;
-    insert_kernel<<<(unsigned)blocks, 256, 0, rp->stream>>>(rp->ring.rows, rp->ring.rs, rp->ring.D,
-                                                            rp->ring.capacity, q.cursor, k, q.s,
-                                                            q.a, q.r, q.s2, q.done, rp->err_dev,
-                                                            rp->ctrl_dev, q.new_size);
+    if (rp->ring.u8) {
+        // one CTA per experience row (rows are ~56 KB for Atari-shaped states)
+        const int64_t ublocks = k < (int64_t)dev_sms * 16 ? k : (int64_t)dev_sms * 16;
+        insert_u8_kernel<<<(unsigned)ublocks, 256, 0, rp->stream>>>(
+            reinterpret_cast<uint8_t *>(rp->ring.rows), (int64_t)rp->ring.rs * 4, rp->ring.so,
+            rp->ring.D, rp->ring.capacity, q.cursor, k, static_cast<const uint8_t *>(q.s), q.a, q.r,
+            static_cast<const uint8_t *>(q.s2), q.done, rp->err_dev, rp->ctrl_dev, q.new_size);
+    } else {
+        insert_kernel<<<(unsigned)blocks, 256, 0, rp->stream>>>(
+            rp->ring.rows, rp->ring.rs, rp->ring.D, rp->ring.capacity, q.cursor, k,
+            static_cast<const float *>(q.s), q.a, q.r, static_cast<const float *>(q.s2), q.done,
+            rp->err_dev, rp->ctrl_dev, q.new_size);
+    }
     RPL_LAUNCHED();
     return RPL_OK;
 }
@@ -292,7 +401,16 @@ int launch_gather(rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t ev
     if (blocks > max_blocks) blocks = max_blocks;
     if (blocks < 1) blocks = 1;
     const rpl::Ring &R = rp->ring;
-    if (R.rs == 64 && R.D == 27) {
+    float *os = static_cast<float *>(out->s), *os2 = static_cast<float *>(out->s_next);
+    if (R.u8) {
+        int64_t nb = n < (int64_t)dev_sms * 8 ? n : (int64_t)dev_sms * 8;
+        if (nb < 1) nb = 1;
+        gather_u8_kernel<<<(unsigned)nb, 256, 0, rp->stream>>>(
+            reinterpret_cast<const uint8_t *>(R.rows), (int64_t)R.rs * 4, R.so, R.D, rp->size, n,
+            use_sampler ? nullptr : idx_dev, rp->seed, rp->rank, event,
+            static_cast<uint8_t *>(out->s), static_cast<uint8_t *>(out->s_next), out->a, out->r,
+            out->done, out->idx, rp->err_dev, rp->ctrl_dev);
+    } else if (R.rs == 64 && R.D == 27) {
         // staged, line-coalesced writes (the Melee row: 27-float states)
         constexpr int KD = 27;
         const size_t smem = (size_t)GS_W * 32 * (2 * KD + 4) * sizeof(float);
@@ -308,18 +426,15 @@ int launch_gather(rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t ev
         const int vec_ok = ((uintptr_t)out->s % 16 == 0) && ((uintptr_t)out->s_next % 16 == 0);
         gather_staged_kernel<KD><<<(unsigned)nb, GS_W * 32, smem, rp->stream>>>(
             R.rows, rp->size, n, use_sampler ? nullptr : idx_dev, rp->seed, rp->rank, event,
-            out->s, out->s_next, out->a, out->r, out->done, out->idx, rp->err_dev, rp->ctrl_dev,
-            vec_ok);
+            os, os2, out->a, out->r, out->done, out->idx, rp->err_dev, rp->ctrl_dev, vec_ok);
     } else if (R.rs == 64) {
         gather_kernel<true><<<(unsigned)blocks, 256, 0, rp->stream>>>(
             R.rows, R.rs, R.D, rp->size, n, use_sampler ? nullptr : idx_dev, rp->seed, rp->rank,
-            event, out->s, out->s_next, out->a, out->r, out->done, out->idx, rp->err_dev,
-            rp->ctrl_dev);
+            event, os, os2, out->a, out->r, out->done, out->idx, rp->err_dev, rp->ctrl_dev);
     } else {
         gather_kernel<false><<<(unsigned)blocks, 256, 0, rp->stream>>>(
             R.rows, R.rs, R.D, rp->size, n, use_sampler ? nullptr : idx_dev, rp->seed, rp->rank,
-            event, out->s, out->s_next, out->a, out->r, out->done, out->idx, rp->err_dev,
-            rp->ctrl_dev);
+            event, os, os2, out->a, out->r, out->done, out->idx, rp->err_dev, rp->ctrl_dev);
     }
     RPL_LAUNCHED();
     return RPL_OK;
@@ -335,9 +450,10 @@ using namespace rpl;
 extern "C" const char *rpl_last_error(void) { return rpl::t_err.c_str(); }
 extern "C" uint64_t rpl_kernel_launches(void) { return rpl::g_launches.load(); }
 
-static size_t host_add_bytes(int64_t k, int32_t D)
+// bytes of one host-sourced add of k experiences (the SoA inputs, copied once: P:32)
+static size_t host_add_bytes(int64_t k, int32_t D, bool u8)
 {
-    return (size_t)k * (8 * (size_t)D + 4 + 4 + 1);
+    return (size_t)k * (2 * (size_t)D * (u8 ? 1 : 4) + 4 + 4 + 1);
 }
 
 extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_replay_opts *opts,
@@ -350,7 +466,8 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
     o.max_host_add = 0;
     if (opts) o = *opts;
     if (capacity < 1 || capacity >= (int64_t(1) << 31) || state_dim < 1 || state_dim > 1 << 20 ||
-        o.rank >= (1u << 24) || o.burn_in < 1 || o.max_host_add < 0) {
+        o.rank >= (1u << 24) || o.burn_in < 1 || o.max_host_add < 0 ||
+        (o.state_dtype != RPL_F32 && o.state_dtype != RPL_U8)) {
         set_error("replay_create: invalid argument (capacity=%lld state_dim=%d rank=%u burn_in=%lld)",
                   (long long)capacity, state_dim, o.rank, (long long)o.burn_in);
         return RPL_EINVAL;
@@ -368,11 +485,18 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
     rp->seed = o.seed;
     rp->rank = o.rank;
     if (const char *nd = getenv("RPL_NO_DEFER")) rp->no_defer = atoi(nd) != 0;
+    const bool u8 = o.state_dtype == RPL_U8;
     rp->max_host_add = o.max_host_add ? o.max_host_add : 65536;
+    // pinned + device staging is two slots of max_host_add experiences: at most 256 MB each
+    const int64_t cap_rows = (int64_t)((256ull << 20) / host_add_bytes(1, state_dim, u8));
+    if (rp->max_host_add > cap_rows) rp->max_host_add = cap_rows > 0 ? cap_rows : 1;
     if (rp->max_host_add > capacity) rp->max_host_add = capacity;
     rp->ring.capacity = capacity;
     rp->ring.D = state_dim;
-    rp->ring.rs = ring_row_stride(state_dim);
+    rp->ring.u8 = u8 ? 1 : 0;
+    rp->ring.rs = u8 ? ring_u8_row_bytes(state_dim) / 4 : ring_row_stride(state_dim);
+    rp->ring.so = u8 ? ring_u8_scalar_offset(state_dim) : 0;
+    if (u8) rp->no_defer = true;   // deferral is a fast-path (fp32 states) feature
     const size_t ring_bytes = (size_t)capacity * rp->ring.rs * sizeof(float);
     cudaError_t e = cudaMalloc(&rp->ring.rows, ring_bytes);
     if (e != cudaSuccess) {
@@ -382,7 +506,7 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
         delete rp;
         return RPL_ENOMEM;
     }
-    const size_t st = host_add_bytes(rp->max_host_add, state_dim) + 64;
+    const size_t st = host_add_bytes(rp->max_host_add, state_dim, u8) + 64;
     bool ok = cudaMalloc(&rp->err_dev, sizeof(uint32_t)) == cudaSuccess &&
               cudaMalloc(&rp->ctrl_dev, 2 * sizeof(uint64_t)) == cudaSuccess &&
               cudaMemsetAsync(rp->ctrl_dev, 0, 2 * sizeof(uint64_t), rp->stream) == cudaSuccess;
@@ -419,8 +543,8 @@ extern "C" int replay_destroy(rpl_replay *rp)
     return RPL_OK;
 }
 
-extern "C" int replay_add(rpl_replay *rp, int64_t k, const float *s, const int32_t *a,
-                          const float *r, const float *s_next, const uint8_t *done, int mem)
+extern "C" int replay_add(rpl_replay *rp, int64_t k, const void *s, const int32_t *a,
+                          const float *r, const void *s_next, const uint8_t *done, int mem)
 {
     if (!rp) { set_error("replay_add: null handle"); return RPL_EINVAL; }
     const int32_t D = rp->ring.D;
@@ -437,7 +561,8 @@ extern "C" int replay_add(rpl_replay *rp, int64_t k, const float *s, const int32
     }
     DeviceGuard g(rp->device);
     if (int rc = replay_flush(rp)) return rc;   // inserts stay in call order
-    const float *ds = s, *dr = r, *ds2 = s_next;
+    const void *ds = s, *ds2 = s_next;
+    const float *dr = r;
     const int32_t *da = a;
     const uint8_t *dd = done;
     if (mem == RPL_HOST) {
@@ -457,12 +582,13 @@ extern "C" int replay_add(rpl_replay *rp, int64_t k, const float *s, const int32
         RPL_CUDA(cudaEventSynchronize(rp->staged[slot]));
         char *hp = (char *)rp->pinned[slot];
         char *dp = (char *)rp->dstage[slot];
-        const size_t bs = (size_t)k * D * sizeof(float);
+        // [r | a | s | s' | done]: the 4-byte fields first so every section stays aligned
+        const size_t bs = (size_t)k * D * (rp->ring.u8 ? 1 : sizeof(float));
         size_t off = 0;
-        memcpy(hp + off, s, bs); ds = (const float *)(dp + off); off += bs;
-        memcpy(hp + off, s_next, bs); ds2 = (const float *)(dp + off); off += bs;
         memcpy(hp + off, r, (size_t)k * 4); dr = (const float *)(dp + off); off += (size_t)k * 4;
         memcpy(hp + off, a, (size_t)k * 4); da = (const int32_t *)(dp + off); off += (size_t)k * 4;
+        memcpy(hp + off, s, bs); ds = dp + off; off += bs;
+        memcpy(hp + off, s_next, bs); ds2 = dp + off; off += bs;
         memcpy(hp + off, done, (size_t)k); dd = (const uint8_t *)(dp + off); off += (size_t)k;
         RPL_CUDA(cudaMemcpyAsync(dp, hp, off, cudaMemcpyHostToDevice, rp->stream));
         RPL_CUDA(cudaEventRecord(rp->staged[slot], rp->stream));

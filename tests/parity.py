@@ -68,6 +68,8 @@ def step_and_compare(b, cfg, dqn, rp, orc_ring, batch, *, seed, rank=0, burn_in=
         assert np.array_equal(g.view(np.uint8), np.ascontiguousarray(ob[key]).view(np.uint8)), key
     net = oracle_net(cfg)
     gamma, kappa = f32(cfg.gamma), (np.inf if np.isinf(cfg.huber_kappa) else f32(cfg.huber_kappa))
+    if ob["s"].dtype == np.uint8:   # byte states: the network input is u8 / 255 (Q27)
+        ob = dict(ob, s=oracle.u8_input(ob["s"]), s_next=oracle.u8_input(ob["s_next"]))
     out = oracle.dqn_loss_grad(net, online, target, ob, gamma, kappa, cfg.double_dqn)
     # decision replay (Q25)
     H = net.hidden_units
