@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-gather", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--sweep", default="", help="comma list of batch sizes: one JSON line each")
+    ap.add_argument("--config", choices=["c2", "c5"], default="c2",
+                    help="c2: BASELINE configs[1] (default); c5: configs[4] 84x84x4 uint8 states, "
+                         "batch 256 (other flags' defaults: --batch 256)")
     return ap.parse_args()
 
 
@@ -420,12 +423,224 @@ def run_ours(a, batch, first_line=True):
     return line
 
 
+# ------------------------------------------------------------------------------------------
+# config 5: 84x84x4 uint8 Atari-shaped states (BASELINE configs[4])
+# ------------------------------------------------------------------------------------------
+C5_D = 84 * 84 * 4
+C5_ROW_BYTES = 56576      # device row: round_up(round_up(2 * C5_D, 16) + 12, 128)
+
+
+def c5_cfg(binding, batch, ddqn):
+    return binding.DQNConfig(state_dim=C5_D, n_actions=8, dueling=True, hidden=(128,), stream=512,
+                             double_dqn=ddqn, gamma=0.99, lr=1e-4, huber_kappa=1.0,
+                             sync_period=10_000, max_batch=batch)
+
+
+def time_oracle_c5(batch, ddqn, seconds, pool):
+    """The oracle on a bounded sample of config 5: a 1,024-row byte ring (the 56 GB ring does
+    not fit in host RAM), its sampler + gather, u8 -> x, loss / gradient and SGD, composed
+    as they stand (never tuned), single thread, fp64."""
+    import oracle
+    from inputs import init_params
+    import paper_1801_03138_b200.binding as binding
+    cfg = c5_cfg(binding, batch, ddqn)
+    net = oracle_net_of(cfg)
+    ring = oracle.RingU8(1024, C5_D)
+    ring.add(**pool)
+    online = init_params(C5_D, 8, (128,), True, 512, seed=3)
+    target = online.copy()
+    n, t0 = 0, time.perf_counter()
+    while True:
+        rc, ob = ring.sample(1, 2, 0, batch)
+        ob = dict(ob, s=oracle.u8_input(ob["s"]), s_next=oracle.u8_input(ob["s_next"]))
+        out = oracle.dqn_loss_grad(net, online, target, ob, float(np.float32(0.99)), 1.0, ddqn)
+        online = oracle.sgd(online, out["grad"], float(np.float32(1e-4))).astype(np.float32)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds and n >= 2:
+            return n, el
+
+
+def run_c5(a):
+    import torch
+    import torch.distributed as dist
+    import paper_1801_03138_b200.binding as binding
+    from inputs import experiences_u8, init_params
+
+    rank, world, local = dist_env()
+    assert world == a.gpus, f"--gpus {a.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    peaks, peaks_kind = load_peaks()
+    batch = a.batch if a.batch != 128 else 256
+    cfg = c5_cfg(binding, batch, a.ddqn)
+    rp = binding.Replay(a.capacity, C5_D, device=local, burn_in=1, seed=2, rank=rank,
+                        state_dtype="u8")
+    # device-side pre-fill (startup, excluded from timings, P:117): a 1,024-experience pool of
+    # this rank's synthetic stream inserted round-robin until the ring is full
+    npool = 1024
+    pool_h = experiences_u8(npool, seed=1, rank=rank)
+    pool_d = {kk: torch.from_numpy(v).to(dev) for kk, v in pool_h.items()}
+    for i in range(0, a.capacity, npool):
+        m = min(npool, a.capacity - i)
+        rp.add(**{kk: v[:m] for kk, v in pool_d.items()})
+    dqn = binding.DQN(cfg, init_params(C5_D, 8, (128,), True, 512, seed=3), device=local)
+    if world > 1:
+        from paper_1801_03138_b200 import dp
+        dp.attach(dqn)
+    K, W, k = a.steps, a.warmup, a.adds_per_step
+    loss_dev = torch.zeros(1, device=dev)
+
+    def add_dev(i):
+        if k:
+            j = (i * k) % (npool - k)
+            rp.add(**{kk: v[j:j + k] for kk, v in pool_d.items()})
+
+    for i in range(W):
+        add_dev(i)
+        dqn.train_step(rp, batch, loss_dev)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches_w = binding.kernel_launches()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(K)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        start.record(stream)
+        for i in range(K):
+            add_dev(W + i)
+            ev[i][0].record(stream)
+            dqn.train_step(rp, batch, loss_dev)
+            ev[i][1].record(stream)
+        end.record(stream)
+        torch.cuda.synchronize()
+    launches = binding.kernel_launches() - launches_w
+    elapsed_ms = start.elapsed_time(end)
+    kern_ms = [s_.elapsed_time(e_) for s_, e_ in ev]
+    assert dqn.check() == binding.RPL_OK, binding.last_error()
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = t.item()
+    value = world * K / (elapsed_ms / 1000.0)
+
+    e2e = None
+    if not a.no_e2e:
+        loss_host = torch.zeros(K, dtype=torch.float32, pin_memory=True)
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h2d0 = rp.state()["h2d_bytes"]
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        s2.record(stream)
+        for i in range(K):
+            if k:
+                j = (i * k) % (npool - k)
+                rp.add(**{kk: v[j:j + k] for kk, v in pool_h.items()})
+            dqn.train_step(rp, batch, loss_dev)
+            loss_host[i:i + 1].copy_(loss_dev, non_blocking=True)
+        e2.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        e2e_ms = s2.elapsed_time(e2)
+        if world > 1:
+            t = torch.tensor([e2e_ms, wall * 1000.0], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms, wall = t[0].item(), t[1].item() / 1000.0
+        e2e = {"value": world * K / (max(e2e_ms / 1000.0, wall)), "unit": "train_steps/s",
+               "h2d_bytes_per_step": (rp.state()["h2d_bytes"] - h2d0) / K,
+               "d2h_bytes_per_step": 4,
+               "note": "replay_add(RPL_HOST) of byte states -> pinned staging -> H2D, "
+                       "dqn_train_step, loss D2H every step; slower of CUDA-event and wall time"}
+
+    flops = binding.step_flops(cfg, batch)
+    kern_avg_ms = float(np.mean(kern_ms))
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_fp32 = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+    achieved = flops / (kern_avg_ms / 1000.0) / 1e12
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
+                "frac": achieved / peak_fp32, "traffic": None,
+                "kernel": "train_step_kernel (cooperative wide-input path: split-K layer-0 forward "
+                          "over the 28,224 byte inputs, FP32 SIMT tiles) timed with CUDA events "
+                          "around each dqn_train_step",
+                "kernel_avg_us": kern_avg_ms * 1000.0, "flops_per_launch": flops,
+                "peak_note": f"FP32 SIMT: 148 SMs x 128 FMA lanes x 2 FLOP x {sm_mhz:.0f} MHz "
+                             f"({peaks_kind} clock)"}
+
+    gather = None
+    if not a.no_gather:
+        n_idx = 4096
+        idx = torch.randint(0, a.capacity, (n_idx,), dtype=torch.int32, device=dev)
+        out = {"s": torch.empty(n_idx, C5_D, dtype=torch.uint8, device=dev),
+               "s_next": torch.empty(n_idx, C5_D, dtype=torch.uint8, device=dev),
+               "a": torch.empty(n_idx, dtype=torch.int32, device=dev),
+               "r": torch.empty(n_idx, device=dev),
+               "done": torch.empty(n_idx, dtype=torch.uint8, device=dev),
+               "idx": torch.empty(n_idx, dtype=torch.int32, device=dev)}
+        for _ in range(3):
+            rp.gather(idx, out)
+        reps = 20
+        gs, ge = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        gs.record(stream)
+        for _ in range(reps):
+            rp.gather(idx, out)
+        ge.record(stream)
+        torch.cuda.synchronize()
+        g_ms = gs.elapsed_time(ge) / reps
+        per = (2 * C5_D + 12) + (2 * C5_D + 13)
+        gbs = n_idx * per / (g_ms / 1000.0) / 1e9
+        gather = {"indices_per_launch": n_idx, "us_per_launch": g_ms * 1000.0, "achieved_GBps": gbs,
+                  "peak_GBps": peaks["hbm_gbs"], "frac": gbs / peaks["hbm_gbs"], "bytes_per_index": per,
+                  "note": "replay_gather of 4,096 uniform indices from the byte ring (> L2): "
+                          "56,460 B row read + 56,461 B unpacked write (+ idx) per index"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        n, el = time_oracle_c5(batch, a.ddqn, a.cpu_seconds, pool_h)
+        cpu = {"value": n / el, "unit": "train_steps/s", "cores": 1, "kind": "oracle",
+               "sample": f"{n} oracle steps (sample + u8->x + loss/grad + SGD at B={batch}) from a "
+                         f"1,024-row host byte ring in {el:.1f} s, single thread, fp64",
+               "cpu": lscpu_model()}
+    line = {
+        "metric": "DQN train steps/s at batch 256, 84x84x4 uint8 states, 1M replay per GPU "
+                  "(BASELINE configs[4]); gather GB/s vs HBM peak",
+        "value": value, "unit": "train_steps/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"BASELINE configs[4]: {a.capacity:,}-slot replay of 84x84x4 uint8 "
+                               f"states ({a.capacity * C5_ROW_BYTES / 1e9:.1f} GB ring), "
+                               f"batch {batch}, dueling DQN 28224-128-[V512|A512]-1+8 on x = u8/255, "
+                               f"{'Double-DQN' if a.ddqn else 'DQN'} target, Huber, SGD, {k} "
+                               "inserts/step",
+                   "batch": batch, "capacity": a.capacity, "double_dqn": a.ddqn,
+                   "adds_per_step": k, "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2 (the byte ring is sampled uniformly)"},
+        "samples_per_s": value * batch, "gpu_launches": launches, "roofline": roofline,
+        "cpu_baseline": cpu, "e2e": e2e, "gather": gather, "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dqn.close()
+    rp.close()
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
         return
-    if a.sweep:
+    if a.config == "c5":
+        run_c5(a)
+    elif a.sweep:
         for i, bsz in enumerate(int(x) for x in a.sweep.split(",")):
             run_ours(a, bsz, first_line=(i == 0))
     else:
