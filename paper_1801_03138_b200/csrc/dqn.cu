@@ -122,6 +122,7 @@ __device__ __forceinline__ float dz_val(const TrainArgs &p, int l, int b, int n)
 {
     const int N = p.N[l];
     if (l == p.T - 1) return __ldcg(p.dZlast + (int64_t)b * N + n);
+    if (l == 0 && p.ks0 > 1) return __ldcg(p.PF0 + (int64_t)b * N + n);   // materialised dZ0
     const float *q = p.PdH[l + 1] + (int64_t)b * N + n;
     const int64_t stride = (int64_t)p.B * N;
     float s = 0.0f;
@@ -270,6 +271,20 @@ __device__ void phase_forward(const TrainArgs &p, int l, TileSmem &sm)
             LdKMajor lh{p.H[l - 1] + (int64_t)net * B * K, K, B, K};
             gemm_tile(lh, lw, m0, n0, 0, K, epi, false, NoRowsum{}, sm);
         }
+    }
+}
+
+// wide inputs: dZ0 = (sum of the dH0 split-K partials) * ReLU'(z0) materialised once in PF0
+// (free after the layer-0 reduction) for the many dW0 tiles, in dz_val's order
+__device__ void phase_dz0(const TrainArgs &p)
+{
+    const int N = p.N[0];
+    const int64_t total = (int64_t)p.B * N, stride = (int64_t)gridDim.x * NT;
+    const int64_t pstride = (int64_t)p.B * N;
+    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < total; i += stride) {
+        float s = 0.0f;
+        for (int q = 0; q < p.nsplit_n[1]; ++q) s += __ldcg(p.PdH[1] + q * pstride + i);
+        p.PF0[i] = __ldcg(p.H[0] + i) > 0.0f ? s : 0.0f;
     }
 }
 
@@ -565,6 +580,10 @@ __global__ void __launch_bounds__(NT, 1) train_step_kernel(const __grid_constant
     phase_head(p, sm);
     grid_barrier(p.bar);
     for (int l = p.T - 1; l >= 0; --l) {
+        if (l == 0 && p.ks0 > 1 && p.T > 1) {
+            phase_dz0(p);
+            grid_barrier(p.bar);
+        }
         phase_backward(p, l, sm);
         grid_barrier(p.bar);
     }
