@@ -28,6 +28,7 @@
 #include "philox.cuh"
 #include "simt_gemm.cuh"
 #include "train_fast.cuh"
+#include "wide.cuh"
 
 namespace rpl {
 
@@ -36,7 +37,7 @@ constexpr int MAXA = 32;  // actions (one warp)
 constexpr int MAXJ = MAXA + 1;
 
 constexpr int kWideInput = 1024;   // state_dim above which layer 0 is split-K (wide inputs)
-constexpr int kKs0Max = 16;        // layer-0 split-K chunks at most
+constexpr int kKs0Max = 80;        // layer-0 split-K chunks at most
 
 struct TrainArgs {
     // replay
@@ -73,6 +74,7 @@ struct TrainArgs {
     int32_t *astar;
     float *loss_out;
     int apply_update, do_sync;
+    int wide_tc;           // layer 0 (forward partials, dW0 + its SGD) runs in wide.cuh kernels
     int ks0;               // split-K of the layer-0 forward (wide inputs): partials in PF0
     float *PF0;            // [ks0][nets][B][N0]
     unsigned *bar;         // [0] arrivals, [1] generation
@@ -541,9 +543,17 @@ __device__ void phase_sgd(const TrainArgs &p, TileSmem &sm)
     const float loss = block_sum_fixed(ls, sm) / (float)p.B;
     const bool ok = isfinite(loss);
     const int64_t stride = (int64_t)gridDim.x * NT;
+    const int64_t w0b = p.woff[0], w0e = p.woff[0] + (int64_t)p.N[0] * p.K[0];
     for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < p.P; i += stride) {
         float g;
-        if (p.nsplit_b == 1) {
+        if (p.wide_tc && i >= w0b && i < w0e) continue;   // W0: wide_dw0_kernel
+        if (p.wide_tc && i >= p.boff[0] && i < p.boff[0] + p.N[0]) {
+            // db0 = sum_b dZ0[b][u] (dZ0 materialised in PF0), in sample order
+            const int u = (int)(i - p.boff[0]);
+            g = 0.0f;
+            for (int b = 0; b < p.B; ++b) g += __ldcg(p.PF0 + (int64_t)b * p.N[0] + u);
+            p.grad[i] = g;
+        } else if (p.nsplit_b == 1) {
             g = __ldcg(p.grad + i);
         } else {
             g = 0.0f;
@@ -570,8 +580,10 @@ __global__ void __launch_bounds__(NT, 1) train_step_kernel(const __grid_constant
 {
     __shared__ TileSmem sm;
     for (int l = 0; l < p.T; ++l) {
-        phase_forward(p, l, sm);
-        grid_barrier(p.bar);
+        if (!(l == 0 && p.wide_tc)) {   // wide_tc: sampled, gathered and multiplied already
+            phase_forward(p, l, sm);
+            grid_barrier(p.bar);
+        }
         if (l == 0 && p.ks0 > 1) {
             phase_l0_reduce(p);
             grid_barrier(p.bar);
@@ -584,6 +596,7 @@ __global__ void __launch_bounds__(NT, 1) train_step_kernel(const __grid_constant
             phase_dz0(p);
             grid_barrier(p.bar);
         }
+        if (l == 0 && p.wide_tc) break;   // dW0 and its SGD follow in wide_dw0_kernel
         phase_backward(p, l, sm);
         grid_barrier(p.bar);
     }
@@ -701,6 +714,7 @@ struct rpl_dqn {
     std::vector<GraphEntry> graphs;
     bool use_graphs = true;
     bool use_pdl = false;                  // programmatic dependent launch inside the graph
+    bool wide_tc = false;                  // byte-state wide inputs: layer 0 on tcgen05 (wide.cuh)
     unsigned long long *trace = nullptr;   // RPL_TRACE=1: per-CTA timestamps of the fast kernels
     // data parallel
     void *comm = nullptr;
@@ -894,6 +908,17 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
          dalloc(d, &d->bar, 2) && dalloc(d, &d->err, 1);
     if (ok && D > kWideInput)
         ok = dalloc(d, &d->PF0, (size_t)kKs0Max * nets * Bm * d->N[0]);
+    {
+        // tcgen05 layer 0 for byte-state replays (used when the replay is RPL_U8): 128 units,
+        // 16-byte input rows, batches up to 256 (RPL_NO_WIDE_TC=1 disables)
+        const char *nw = getenv("RPL_NO_WIDE_TC");
+        d->wide_tc = ok && D > kWideInput && D % 16 == 0 && d->N[0] == WD_M && d->T >= 2 &&
+                     !(nw && nw[0] == '1');
+        if (d->wide_tc) {
+            ok = cudaFuncSetAttribute(wide_l0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WD_SMEM) == cudaSuccess &&
+                 cudaFuncSetAttribute(wide_dw0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WD_SMEM) == cudaSuccess;
+        }
+    }
     for (int l = 0; l < d->T && ok; ++l) {
         ok = dalloc(d, &d->H[l], (size_t)nets * Bm * d->N[l]);
         if (ok && l > 0) {
@@ -1293,6 +1318,49 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
     } else {
         TrainArgs p;
         fill_args(d, rp, batch, loss_dev, dp ? 0 : 1, do_sync, p);
+        // byte states with a wide input: layer 0 on the tensor cores (wide.cuh) around the
+        // cooperative kernel, which then runs the layers above it
+        const bool wide = d->wide_tc && rp->ring.u8 && batch <= WD_MAXN;
+        WideArgs w{};
+        if (wide) {
+            const int nets = p.nets;
+            const int ks_max = std::max(1, std::min(kKs0Max, d->sms / nets));
+            w.D = p.D;
+            w.B = batch;
+            w.N0 = d->N[0];
+            w.nets = nets;
+            w.kchunk = ((p.D + ks_max - 1) / ks_max + WD_KS - 1) / WD_KS * WD_KS;
+            w.ks = (int)((p.D + w.kchunk - 1) / w.kchunk);
+            w.U0 = reinterpret_cast<const uint8_t *>(d->Xs);
+            w.U1 = reinterpret_cast<const uint8_t *>(d->Xs2);
+            w.online = d->online;
+            w.target = d->target;
+            w.w0 = d->woff[0];
+            w.PF0 = d->PF0;
+            w.dZ0 = d->PF0;
+            w.grad = d->grad;
+            w.P = d->P;
+            w.online_w = d->online;
+            w.target_w = d->target;
+            w.lr = d->cfg.lr;
+            w.apply_update = dp ? 0 : 1;
+            w.sync_flag = d->sync_flag;
+            p.wide_tc = 1;
+            p.ks0 = w.ks;
+            // (1) Philox sample + gather + unpack into the learner's batch buffers
+            rpl_batch bt{d->Xs, d->Xs2, d->a, d->r, d->done, d->idx};
+            if (int rc = launch_gather(rp, batch, nullptr, rp->events, 1, &bt)) {
+                if (prev >= 0) cudaSetDevice(prev);
+                return rc;
+            }
+            // (2) layer-0 forward partials of every net
+            wide_l0_kernel<<<nets * w.ks, WD_T, WD_SMEM, d->stream>>>(w);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) {
+                if (prev >= 0) cudaSetDevice(prev);
+                return cuda_fail(e, "wide_l0_kernel");
+            }
+        }
         const int grid = grid_for(d, p);
         void *args[] = {&p};
         e = cudaLaunchCooperativeKernel((const void *)train_step_kernel, dim3(grid), dim3(NT), args,
@@ -1302,6 +1370,16 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             return cuda_fail(e, "cudaLaunchCooperativeKernel(train_step_kernel)");
         }
         g_launches.fetch_add(1);
+        if (wide) {
+            // (4) dW0 = dZ0^T x per 256-input tile, then its SGD / target sync
+            wide_dw0_kernel<<<(unsigned)((p.D + WD_MAXN - 1) / WD_MAXN), WD_T, WD_SMEM, d->stream>>>(w);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) {
+                if (prev >= 0) cudaSetDevice(prev);
+                return cuda_fail(e, "wide_dw0_kernel");
+            }
+            g_launches.fetch_add(2);
+        }
     }
     if (dp) {
         int nr = g_nccl.allreduce(d->grad, d->grad, (size_t)d->P + 1, kNcclFloat, kNcclAvg,

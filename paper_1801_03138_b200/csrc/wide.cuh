@@ -1,0 +1,306 @@
+// wide.cuh -- the wide-input layer 0 of byte-state learners (SURVEY config 5: 84x84x4 uint8
+// states, 28,224 inputs) on the 5th-generation tensor cores (tcgen05, umma.cuh).  CUDA path only.
+//
+// The input x = u8 / 255 (reading Q27) is carried exactly as the integer u (0..255 is exact in
+// bf16) with the 1/255 applied to the fp32 result; every fp32 weight / gradient operand w is
+// split into three bf16 terms hi + mid + lo that hold all 24 of its significand bits
+// (umma::split3_bf16), so the three bf16 MMAs u*hi + u*mid + u*lo accumulate the exact
+// products in fp32 -- an FP32-accurate layer 0 (tests/test_gpu_u8.py checks it against the
+// fp64 oracle) at tensor-core rate.
+//
+//   wide_l0_kernel : Z0 partials.  CTA (net, k-chunk) computes D[128 units][B] =
+//                    W0_net[:, chunk] . U_net[:, chunk]^T (A = W0 K-major, B = U K-major) and
+//                    writes it to PF0[chunk][net][b][unit]; the cooperative train kernel adds
+//                    the chunks in order (+ bias, ReLU) -- the split-K layout of phase_l0_reduce.
+//   wide_dw0_kernel: dW0 tile [128 units][256 inputs] = dZ0^T U over the batch (A = dZ0^T
+//                    MN-major, B = U^T MN-major), then g = D / 255 -> grad, SGD (and the target
+//                    sync) of those W0 entries: layer 0's gradient never makes a round trip.
+// Both stage 64-deep K slices through two shared-memory buffers: the loads / conversions of
+// slice i + 1 overlap the MMAs of slice i (tcgen05.commit -> mbarrier per buffer).
+#pragma once
+#include <stdint.h>
+
+#include "umma.cuh"
+
+namespace rpl {
+
+constexpr int WD_M = 128;                 // units of layer 0 (the UMMA M)
+constexpr int WD_KS = 64;                 // K slice per stage
+constexpr int WD_T = 256;                 // threads
+constexpr int WD_MAXN = 256;              // UMMA N at most (batch for the forward, inputs for dW0)
+constexpr int WD_A_PLANE = WD_M * WD_KS * 2;            // bytes of one bf16 A plane
+constexpr int WD_B_BYTES = WD_MAXN * WD_KS * 2;         // bytes of the bf16 B slice
+constexpr int WD_STAGE = 3 * WD_A_PLANE + WD_B_BYTES;   // 80 KB
+constexpr int WD_SMEM = 2 * WD_STAGE + 1024;            // + alignment slack
+
+struct WideArgs {
+    int D, B, N0, nets, ks;          // inputs, batch, layer-0 units (== 128), nets, k-chunks
+    int64_t kchunk;                  // inputs per chunk (multiple of WD_KS)
+    const uint8_t *U0, *U1;          // gathered byte states s, s' [B][D]
+    const float *online, *target;
+    int64_t w0;                      // offset of W0 [N0][D] in the parameter blob
+    float *PF0;                      // [ks][nets][B][N0]
+    const float *dZ0;                // [B][N0] (materialised by the train kernel)
+    float *grad;                     // [P + 1] (grad[P] = batch-mean loss, set by the train kernel)
+    int64_t P;
+    float *online_w, *target_w;      // SGD targets (== online / target)
+    float lr;
+    int apply_update;
+    const int32_t *sync_flag;
+};
+
+// canonical no-swizzle offsets (umma.cuh): K-major rows x 64-deep slice, and MN-major
+__device__ __forceinline__ uint32_t wd_off_k(int r, int k) { return (r >> 3) * 1024 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2; }
+__device__ __forceinline__ uint32_t wd_off_mn(int r, int k, int R) { return (k >> 3) * (R / 8) * 128 + (r >> 3) * 128 + (k & 7) * 16 + (r & 7) * 2; }
+
+__device__ __forceinline__ uint32_t pack2(uint16_t a, uint16_t b) { return (uint32_t)a | ((uint32_t)b << 16); }
+__device__ __forceinline__ uint16_t u8_bf16(uint32_t v) { return __bfloat16_as_ushort(__uint2bfloat16_rn(v)); }
+
+// ------------------------------------------------------------------------------------------
+// layer-0 forward partials
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant__ WideArgs p)
+{
+    extern __shared__ uint8_t wd_raw[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>(((uintptr_t)wd_raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t mbar[2];
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int net = blockIdx.x / p.ks, kq = blockIdx.x % p.ks;
+    const int64_t kb = (int64_t)kq * p.kchunk;
+    const int64_t ke = kb + p.kchunk < p.D ? kb + p.kchunk : p.D;
+    const int nsl = (int)((ke - kb + WD_KS - 1) / WD_KS);
+    const int N = (p.B + 15) & ~15;                  // UMMA N: the batch rounded up to 16
+    const float *W0 = (net == 1 ? p.target : p.online) + p.w0;
+    const uint8_t *U = net == 0 ? p.U0 : p.U1;
+    if (warp == 0) umma::tmem_alloc(&tbase, 256);
+    if (tid == 0) {
+        umma::mbar_init(&mbar[0], 1);
+        umma::mbar_init(&mbar[1], 1);
+        umma::fence_mbar_init();
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tmem = tbase;
+    const uint32_t idesc = umma::idesc_bf16(WD_M, N, false, false);
+    for (int sl = 0; sl < nsl; ++sl) {
+        const int st = sl & 1;
+        uint8_t *A = sm + st * WD_STAGE, *Bs = A + 3 * WD_A_PLANE;
+        if (sl >= 2) umma::mbar_wait(&mbar[st], ((sl - 2) >> 1) & 1);   // MMAs of slice sl-2 done
+        const int64_t k0 = kb + (int64_t)sl * WD_KS;
+        // A: W0[u][k0 .. k0+63] fp32 -> hi / mid / lo bf16 planes (K-major)
+        for (int e = tid; e < WD_M * (WD_KS / 4); e += WD_T) {
+            const int u = e / (WD_KS / 4), k = 4 * (e % (WD_KS / 4));
+            float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (u < p.N0 && k0 + k + 3 < ke) {
+                w = __ldg(reinterpret_cast<const float4 *>(W0 + (int64_t)u * p.D + k0 + k));
+            } else if (u < p.N0) {
+                float t[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int q = 0; q < 4; ++q)
+                    if (k0 + k + q < ke) t[q] = __ldg(W0 + (int64_t)u * p.D + k0 + k + q);
+                w = make_float4(t[0], t[1], t[2], t[3]);
+            }
+            uint16_t h[4], m[4], l[4];
+            umma::split3_bf16(w.x, h[0], m[0], l[0]);
+            umma::split3_bf16(w.y, h[1], m[1], l[1]);
+            umma::split3_bf16(w.z, h[2], m[2], l[2]);
+            umma::split3_bf16(w.w, h[3], m[3], l[3]);
+            const uint32_t o = wd_off_k(u, k);
+            *reinterpret_cast<uint2 *>(A + o) = make_uint2(pack2(h[0], h[1]), pack2(h[2], h[3]));
+            *reinterpret_cast<uint2 *>(A + WD_A_PLANE + o) = make_uint2(pack2(m[0], m[1]), pack2(m[2], m[3]));
+            *reinterpret_cast<uint2 *>(A + 2 * WD_A_PLANE + o) = make_uint2(pack2(l[0], l[1]), pack2(l[2], l[3]));
+        }
+        // B: U[b][k0 .. k0+63] u8 -> bf16 (K-major), 16 bytes per thread-step
+        for (int e = tid; e < N * (WD_KS / 16); e += WD_T) {
+            const int b = e / (WD_KS / 16), k = 16 * (e % (WD_KS / 16));
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (b < p.B) {
+                const uint8_t *src = U + (int64_t)b * p.D + k0 + k;
+                if (k0 + k + 15 < ke && ((uintptr_t)src & 15) == 0) {
+                    v = __ldg(reinterpret_cast<const uint4 *>(src));
+                } else {
+                    uint8_t t[16];
+                    for (int q = 0; q < 16; ++q) t[q] = (k0 + k + q < ke) ? src[q] : 0;
+                    v = make_uint4(t[0] | t[1] << 8 | t[2] << 16 | (uint32_t)t[3] << 24,
+                                   t[4] | t[5] << 8 | t[6] << 16 | (uint32_t)t[7] << 24,
+                                   t[8] | t[9] << 8 | t[10] << 16 | (uint32_t)t[11] << 24,
+                                   t[12] | t[13] << 8 | t[14] << 16 | (uint32_t)t[15] << 24);
+                }
+            }
+            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+            uint32_t o8[8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                o8[2 * q] = pack2(u8_bf16(w4[q] & 0xFF), u8_bf16((w4[q] >> 8) & 0xFF));
+                o8[2 * q + 1] = pack2(u8_bf16((w4[q] >> 16) & 0xFF), u8_bf16(w4[q] >> 24));
+            }
+            *reinterpret_cast<uint4 *>(Bs + wd_off_k(b, k)) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
+            *reinterpret_cast<uint4 *>(Bs + wd_off_k(b, k + 8)) = make_uint4(o8[4], o8[5], o8[6], o8[7]);
+        }
+        umma::fence_async_smem();
+        umma::fence_before_sync();
+        __syncthreads();
+        if (tid == 0) {
+            umma::fence_after_sync();
+            for (int s = 0; s < WD_KS / 16; ++s) {
+                const uint64_t bd = umma::desc(Bs + 2 * s * 128, 128, 1024);
+#pragma unroll
+                for (int pl = 0; pl < 3; ++pl)
+                    umma::mma_bf16(tmem, umma::desc(A + pl * WD_A_PLANE + 2 * s * 128, 128, 1024), bd,
+                                   idesc, sl > 0 || s > 0 || pl > 0);
+            }
+            umma::commit(&mbar[st]);
+        }
+    }
+    // the last slice's commit covers every earlier MMA
+    {
+        const int last = nsl - 1;
+        umma::mbar_wait(&mbar[last & 1], (last >> 1) & 1);
+    }
+    umma::fence_after_sync();
+    // epilogue: warp w reads TMEM lanes (units) 32 (w % 4) .. + 31, columns (samples) of its half
+    {
+        const int q = warp & 3, half = warp >> 2, u = 32 * q + lane;
+        const int c0 = half * (N / 2), c1 = c0 + N / 2;
+        float *out = p.PF0 + ((int64_t)kq * p.nets + net) * p.B * p.N0;
+        for (int c = c0; c < c1; c += 8) {
+            float v[8];
+            umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + c, v);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (c + i < p.B && u < p.N0) out[(int64_t)(c + i) * p.N0 + u] = v[i] / 255.0f;
+        }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) umma::tmem_free(tmem, 256);
+}
+
+// ------------------------------------------------------------------------------------------
+// dW0 + SGD of W0
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant__ WideArgs p)
+{
+    extern __shared__ uint8_t wd_raw[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>(((uintptr_t)wd_raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t mbar[2];
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t n0 = (int64_t)blockIdx.x * WD_MAXN;                  // first input of the tile
+    const int nn = (int)(p.D - n0 < WD_MAXN ? p.D - n0 : WD_MAXN);    // inputs in the tile
+    const int N = (nn + 15) & ~15;
+    const int nsl = (p.B + WD_KS - 1) / WD_KS;
+    if (warp == 0) umma::tmem_alloc(&tbase, 256);
+    if (tid == 0) {
+        umma::mbar_init(&mbar[0], 1);
+        umma::mbar_init(&mbar[1], 1);
+        umma::fence_mbar_init();
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tmem = tbase;
+    const uint32_t idesc = umma::idesc_bf16(WD_M, N, true, true);
+    for (int sl = 0; sl < nsl; ++sl) {
+        const int st = sl & 1;
+        uint8_t *A = sm + st * WD_STAGE, *Bs = A + 3 * WD_A_PLANE;
+        if (sl >= 2) umma::mbar_wait(&mbar[st], ((sl - 2) >> 1) & 1);
+        const int b0 = sl * WD_KS;
+        // A = dZ0^T slice: element (unit u, sample b) = dZ0[b][u], MN-major (contiguous in u)
+        for (int e = tid; e < WD_KS * (WD_M / 4); e += WD_T) {
+            const int bb = e / (WD_M / 4), u = 4 * (e % (WD_M / 4));
+            float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (b0 + bb < p.B && u < p.N0)
+                z = __ldcg(reinterpret_cast<const float4 *>(p.dZ0 + (int64_t)(b0 + bb) * p.N0 + u));
+            uint16_t h[4], m[4], l[4];
+            umma::split3_bf16(z.x, h[0], m[0], l[0]);
+            umma::split3_bf16(z.y, h[1], m[1], l[1]);
+            umma::split3_bf16(z.z, h[2], m[2], l[2]);
+            umma::split3_bf16(z.w, h[3], m[3], l[3]);
+            const uint32_t o = wd_off_mn(u, bb, WD_M);
+            *reinterpret_cast<uint2 *>(A + o) = make_uint2(pack2(h[0], h[1]), pack2(h[2], h[3]));
+            *reinterpret_cast<uint2 *>(A + WD_A_PLANE + o) = make_uint2(pack2(m[0], m[1]), pack2(m[2], m[3]));
+            *reinterpret_cast<uint2 *>(A + 2 * WD_A_PLANE + o) = make_uint2(pack2(l[0], l[1]), pack2(l[2], l[3]));
+        }
+        // B = U^T slice: element (input n, sample b) = U[b][n0 + n], MN-major (contiguous in n)
+        for (int e = tid; e < WD_KS * (N / 16); e += WD_T) {
+            const int bb = e / (N / 16), n = 16 * (e % (N / 16));
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (b0 + bb < p.B) {
+                const uint8_t *src = p.U0 + (int64_t)(b0 + bb) * p.D + n0 + n;
+                if (n + 15 < nn && ((uintptr_t)src & 15) == 0) {
+                    v = __ldg(reinterpret_cast<const uint4 *>(src));
+                } else {
+                    uint8_t t[16];
+                    for (int q = 0; q < 16; ++q) t[q] = (n + q < nn) ? src[q] : 0;
+                    v = make_uint4(t[0] | t[1] << 8 | t[2] << 16 | (uint32_t)t[3] << 24,
+                                   t[4] | t[5] << 8 | t[6] << 16 | (uint32_t)t[7] << 24,
+                                   t[8] | t[9] << 8 | t[10] << 16 | (uint32_t)t[11] << 24,
+                                   t[12] | t[13] << 8 | t[14] << 16 | (uint32_t)t[15] << 24);
+                }
+            }
+            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+            uint32_t o8[8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                o8[2 * q] = pack2(u8_bf16(w4[q] & 0xFF), u8_bf16((w4[q] >> 8) & 0xFF));
+                o8[2 * q + 1] = pack2(u8_bf16((w4[q] >> 16) & 0xFF), u8_bf16(w4[q] >> 24));
+            }
+            *reinterpret_cast<uint4 *>(Bs + wd_off_mn(n, bb, N)) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
+            *reinterpret_cast<uint4 *>(Bs + wd_off_mn(n + 8, bb, N)) = make_uint4(o8[4], o8[5], o8[6], o8[7]);
+        }
+        umma::fence_async_smem();
+        umma::fence_before_sync();
+        __syncthreads();
+        if (tid == 0) {
+            umma::fence_after_sync();
+            const int ksteps = (min(WD_KS, p.B - b0) + 15) / 16;
+            for (int s = 0; s < ksteps; ++s) {
+                const uint64_t bd = umma::desc(Bs + 2 * s * (N / 8) * 128, (N / 8) * 128, 128);
+#pragma unroll
+                for (int pl = 0; pl < 3; ++pl)
+                    umma::mma_bf16(tmem, umma::desc(A + pl * WD_A_PLANE + 2 * s * (WD_M / 8) * 128,
+                                                    (WD_M / 8) * 128, 128),
+                                   bd, idesc, sl > 0 || s > 0 || pl > 0);
+            }
+            umma::commit(&mbar[st]);
+        }
+    }
+    {
+        const int last = nsl - 1;
+        umma::mbar_wait(&mbar[last & 1], (last >> 1) & 1);
+    }
+    umma::fence_after_sync();
+    // epilogue: g = D / 255 -> grad; w -= lr g (skipped on a non-finite loss); target
+    // sync on sync steps
+    {
+        const float loss = __ldcg(p.grad + p.P);
+        const bool upd = p.apply_update && isfinite(loss);
+        const bool sync = *p.sync_flag != 0;
+        const int q = warp & 3, half = warp >> 2, u = 32 * q + lane;
+        const int c0 = half * (N / 2), c1 = c0 + N / 2;
+        for (int c = c0; c < c1; c += 8) {
+            float v[8];
+            umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + c, v);
+            if (u >= p.N0) continue;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (c + i >= nn) continue;
+                const int64_t wi = p.w0 + (int64_t)u * p.D + n0 + c + i;
+                const float g = v[i] / 255.0f;
+                p.grad[wi] = g;
+                if (upd) {
+                    const float w = p.online_w[wi] - p.lr * g;
+                    p.online_w[wi] = w;
+                    if (sync) p.target_w[wi] = w;
+                }
+            }
+        }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) umma::tmem_free(tmem, 256);
+}
+
+}  // namespace rpl
