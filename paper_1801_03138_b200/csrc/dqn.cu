@@ -75,6 +75,7 @@ struct TrainArgs {
     float *loss_out;
     int apply_update, do_sync;
     int wide_tc;           // layer 0 (forward partials, dW0 + its SGD) runs in wide.cuh kernels
+    uint16_t *dZ0bf;       // wide_tc: bf16 hi / mid / lo planes of dZ0 [3][B][N0]
     int ks0;               // split-K of the layer-0 forward (wide inputs): partials in PF0
     float *PF0;            // [ks0][nets][B][N0]
     unsigned *bar;         // [0] arrivals, [1] generation
@@ -286,7 +287,15 @@ __device__ void phase_dz0(const TrainArgs &p)
     for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < total; i += stride) {
         float s = 0.0f;
         for (int q = 0; q < p.nsplit_n[1]; ++q) s += __ldcg(p.PdH[1] + q * pstride + i);
-        p.PF0[i] = __ldcg(p.H[0] + i) > 0.0f ? s : 0.0f;
+        const float z = __ldcg(p.H[0] + i) > 0.0f ? s : 0.0f;
+        p.PF0[i] = z;
+        if (p.wide_tc) {   // the dW0 kernel's tensor-core operand, split once
+            uint16_t h, m, l;
+            umma::split3_bf16(z, h, m, l);
+            p.dZ0bf[i] = h;
+            p.dZ0bf[total + i] = m;
+            p.dZ0bf[2 * total + i] = l;
+        }
     }
 }
 
@@ -715,6 +724,9 @@ struct rpl_dqn {
     bool use_graphs = true;
     bool use_pdl = false;                  // programmatic dependent launch inside the graph
     bool wide_tc = false;                  // byte-state wide inputs: layer 0 on tcgen05 (wide.cuh)
+    uint16_t *w0bf = nullptr;              // bf16 planes of W0 [online, target][3][N0 * D]
+    uint16_t *dz0bf = nullptr;             // bf16 planes of dZ0 [3][max_batch][N0]
+    bool w0bf_stale = true;                // planes to be re-split from the fp32 weights
     unsigned long long *trace = nullptr;   // RPL_TRACE=1: per-CTA timestamps of the fast kernels
     // data parallel
     void *comm = nullptr;
@@ -916,7 +928,9 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
                      !(nw && nw[0] == '1');
         if (d->wide_tc) {
             ok = cudaFuncSetAttribute(wide_l0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WD_SMEM) == cudaSuccess &&
-                 cudaFuncSetAttribute(wide_dw0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WD_SMEM) == cudaSuccess;
+                 cudaFuncSetAttribute(wide_dw0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WD_SMEM) == cudaSuccess &&
+                 dalloc(d, &d->w0bf, (size_t)6 * d->N[0] * D) &&
+                 dalloc(d, &d->dz0bf, (size_t)3 * Bm * d->N[0]);
         }
     }
     for (int l = 0; l < d->T && ok; ++l) {
@@ -1079,6 +1093,7 @@ static void fill_args(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.do_sync = do_sync;
     p.ks0 = ks0_for(d, B);
     p.PF0 = d->PF0;
+    p.dZ0bf = d->dz0bf;
     p.bar = d->bar;
     p.err = d->err;
     p.rctrl = rp->ctrl_dev;
@@ -1338,6 +1353,8 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             w.w0 = d->woff[0];
             w.PF0 = d->PF0;
             w.dZ0 = d->PF0;
+            w.dZ0bf = d->dz0bf;
+            w.W0bf = d->w0bf;
             w.grad = d->grad;
             w.P = d->P;
             w.online_w = d->online;
@@ -1347,6 +1364,18 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             w.sync_flag = d->sync_flag;
             p.wide_tc = 1;
             p.ks0 = w.ks;
+            if (d->w0bf_stale) {   // after create / set_params / sync_target / a DP step
+                const int64_t nd = (int64_t)d->N[0] * p.D;
+                wide_split_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->online + d->woff[0], d->w0bf, nd);
+                wide_split_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->target + d->woff[0], d->w0bf + 3 * nd, nd);
+                e = cudaGetLastError();
+                if (e != cudaSuccess) {
+                    if (prev >= 0) cudaSetDevice(prev);
+                    return cuda_fail(e, "wide_split_kernel");
+                }
+                g_launches.fetch_add(2);
+                d->w0bf_stale = false;
+            }
             // (1) Philox sample + gather + unpack into the learner's batch buffers
             rpl_batch bt{d->Xs, d->Xs2, d->a, d->r, d->done, d->idx};
             if (int rc = launch_gather(rp, batch, nullptr, rp->events, 1, &bt)) {
@@ -1389,6 +1418,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             if (prev >= 0) cudaSetDevice(prev);
             return RPL_ENCCL;
         }
+        d->w0bf_stale = true;   // the all-reduced update rewrote W0 without its planes
         sgd_kernel<<<(unsigned)d->sms, 256, 0, d->stream>>>(d->online, d->target, d->grad, d->P,
                                                              d->cfg.lr, d->sync_flag, d->err);
         e = cudaGetLastError();
@@ -1413,6 +1443,7 @@ extern "C" int sync_target(rpl_dqn *d)
     if (!d) return RPL_EINVAL;
     RPL_CUDA(cudaMemcpyAsync(d->target, d->online, (size_t)d->P * sizeof(float),
                              cudaMemcpyDeviceToDevice, d->stream));
+    d->w0bf_stale = true;
     return RPL_OK;
 }
 
@@ -1443,6 +1474,7 @@ extern "C" int dqn_set_params(rpl_dqn *d, int which, const float *host_in, int64
     RPL_CUDA(cudaMemcpyAsync(which_ptr(d, which), host_in, (size_t)n * sizeof(float),
                              cudaMemcpyHostToDevice, d->stream));
     RPL_CUDA(cudaStreamSynchronize(d->stream));
+    d->w0bf_stale = true;
     return RPL_OK;
 }
 

@@ -15,8 +15,12 @@
 //   wide_dw0_kernel: dW0 tile [128 units][256 inputs] = dZ0^T U over the batch (A = dZ0^T
 //                    MN-major, B = U^T MN-major), then g = D / 255 -> grad, SGD (and the target
 //                    sync) of those W0 entries: layer 0's gradient never makes a round trip.
-// Both stage 64-deep K slices through two shared-memory buffers: the loads / conversions of
-// slice i + 1 overlap the MMAs of slice i (tcgen05.commit -> mbarrier per buffer).
+// The fp32 operands are split once, not per CTA: W0's planes live next to the fp32 master
+// weights (rewritten by the dW0 epilogue's SGD, re-split by wide_split_kernel after any host
+// write or target sync) and dZ0's planes are written by the train kernel; the CTAs copy them
+// with 16-byte cp.async straight into the canonical layout.  Both kernels stage 64-deep K
+// slices through two shared-memory buffers: the loads of slice i + 1 overlap the MMAs of
+// slice i (tcgen05.commit -> mbarrier per buffer).
 #pragma once
 #include <stdint.h>
 
@@ -41,6 +45,8 @@ struct WideArgs {
     int64_t w0;                      // offset of W0 [N0][D] in the parameter blob
     float *PF0;                      // [ks][nets][B][N0]
     const float *dZ0;                // [B][N0] (materialised by the train kernel)
+    const uint16_t *dZ0bf;           // its bf16 hi / mid / lo planes [3][B][N0] (same kernel)
+    uint16_t *W0bf;                  // bf16 planes of W0: [net 0 online, 1 target][3][N0 * D]
     float *grad;                     // [P + 1] (grad[P] = batch-mean loss, set by the train kernel)
     int64_t P;
     float *online_w, *target_w;      // SGD targets (== online / target)
@@ -54,6 +60,25 @@ __device__ __forceinline__ uint32_t wd_off_k(int r, int k) { return (r >> 3) * 1
 __device__ __forceinline__ uint32_t wd_off_mn(int r, int k, int R) { return (k >> 3) * (R / 8) * 128 + (r >> 3) * 128 + (k & 7) * 16 + (r & 7) * 2; }
 
 __device__ __forceinline__ uint32_t pack2(uint16_t a, uint16_t b) { return (uint32_t)a | ((uint32_t)b << 16); }
+
+__device__ __forceinline__ void wd_cp16(void *smem, const void *gmem, bool valid)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void wd_cp_wait() { asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory"); }
+
+// planes[p][i] = split3(src[i])_p  (p = hi, mid, lo)
+__global__ void __launch_bounds__(256) wide_split_kernel(const float *__restrict__ src, uint16_t *planes, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint16_t h, m, l;
+        umma::split3_bf16(src[i], h, m, l);
+        planes[i] = h;
+        planes[n + i] = m;
+        planes[2 * n + i] = l;
+    }
+}
 __device__ __forceinline__ uint16_t u8_bf16(uint32_t v) { return __bfloat16_as_ushort(__uint2bfloat16_rn(v)); }
 
 // ------------------------------------------------------------------------------------------
@@ -71,7 +96,6 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
     const int64_t ke = kb + p.kchunk < p.D ? kb + p.kchunk : p.D;
     const int nsl = (int)((ke - kb + WD_KS - 1) / WD_KS);
     const int N = (p.B + 15) & ~15;                  // UMMA N: the batch rounded up to 16
-    const float *W0 = (net == 1 ? p.target : p.online) + p.w0;
     const uint8_t *U = net == 0 ? p.U0 : p.U1;
     if (warp == 0) umma::tmem_alloc(&tbase, 256);
     if (tid == 0) {
@@ -89,27 +113,16 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
         uint8_t *A = sm + st * WD_STAGE, *Bs = A + 3 * WD_A_PLANE;
         if (sl >= 2) umma::mbar_wait(&mbar[st], ((sl - 2) >> 1) & 1);   // MMAs of slice sl-2 done
         const int64_t k0 = kb + (int64_t)sl * WD_KS;
-        // A: W0[u][k0 .. k0+63] fp32 -> hi / mid / lo bf16 planes (K-major)
-        for (int e = tid; e < WD_M * (WD_KS / 4); e += WD_T) {
-            const int u = e / (WD_KS / 4), k = 4 * (e % (WD_KS / 4));
-            float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (u < p.N0 && k0 + k + 3 < ke) {
-                w = __ldg(reinterpret_cast<const float4 *>(W0 + (int64_t)u * p.D + k0 + k));
-            } else if (u < p.N0) {
-                float t[4] = {0.f, 0.f, 0.f, 0.f};
-                for (int q = 0; q < 4; ++q)
-                    if (k0 + k + q < ke) t[q] = __ldg(W0 + (int64_t)u * p.D + k0 + k + q);
-                w = make_float4(t[0], t[1], t[2], t[3]);
+        // A: the hi / mid / lo planes of W0[u][k0 .. k0+63] (K-major), 16-byte copies of 8 k
+        {
+            const int64_t nd = (int64_t)p.N0 * p.D;
+            const uint16_t *Wp = p.W0bf + (net == 1 ? 3 * nd : 0);
+            for (int e = tid; e < 3 * WD_M * (WD_KS / 8); e += WD_T) {
+                const int pl = e / (WD_M * (WD_KS / 8)), r = e % (WD_M * (WD_KS / 8));
+                const int u = r / (WD_KS / 8), k = 8 * (r % (WD_KS / 8));
+                const bool v = u < p.N0 && k0 + k < ke;
+                wd_cp16(A + pl * WD_A_PLANE + wd_off_k(u, k), v ? Wp + pl * nd + (int64_t)u * p.D + k0 + k : Wp, v);
             }
-            uint16_t h[4], m[4], l[4];
-            umma::split3_bf16(w.x, h[0], m[0], l[0]);
-            umma::split3_bf16(w.y, h[1], m[1], l[1]);
-            umma::split3_bf16(w.z, h[2], m[2], l[2]);
-            umma::split3_bf16(w.w, h[3], m[3], l[3]);
-            const uint32_t o = wd_off_k(u, k);
-            *reinterpret_cast<uint2 *>(A + o) = make_uint2(pack2(h[0], h[1]), pack2(h[2], h[3]));
-            *reinterpret_cast<uint2 *>(A + WD_A_PLANE + o) = make_uint2(pack2(m[0], m[1]), pack2(m[2], m[3]));
-            *reinterpret_cast<uint2 *>(A + 2 * WD_A_PLANE + o) = make_uint2(pack2(l[0], l[1]), pack2(l[2], l[3]));
         }
         // B: U[b][k0 .. k0+63] u8 -> bf16 (K-major), 16 bytes per thread-step
         for (int e = tid; e < N * (WD_KS / 16); e += WD_T) {
@@ -138,6 +151,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
             *reinterpret_cast<uint4 *>(Bs + wd_off_k(b, k)) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
             *reinterpret_cast<uint4 *>(Bs + wd_off_k(b, k + 8)) = make_uint4(o8[4], o8[5], o8[6], o8[7]);
         }
+        wd_cp_wait();
         umma::fence_async_smem();
         umma::fence_before_sync();
         __syncthreads();
@@ -207,21 +221,17 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
         uint8_t *A = sm + st * WD_STAGE, *Bs = A + 3 * WD_A_PLANE;
         if (sl >= 2) umma::mbar_wait(&mbar[st], ((sl - 2) >> 1) & 1);
         const int b0 = sl * WD_KS;
-        // A = dZ0^T slice: element (unit u, sample b) = dZ0[b][u], MN-major (contiguous in u)
-        for (int e = tid; e < WD_KS * (WD_M / 4); e += WD_T) {
-            const int bb = e / (WD_M / 4), u = 4 * (e % (WD_M / 4));
-            float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (b0 + bb < p.B && u < p.N0)
-                z = __ldcg(reinterpret_cast<const float4 *>(p.dZ0 + (int64_t)(b0 + bb) * p.N0 + u));
-            uint16_t h[4], m[4], l[4];
-            umma::split3_bf16(z.x, h[0], m[0], l[0]);
-            umma::split3_bf16(z.y, h[1], m[1], l[1]);
-            umma::split3_bf16(z.z, h[2], m[2], l[2]);
-            umma::split3_bf16(z.w, h[3], m[3], l[3]);
-            const uint32_t o = wd_off_mn(u, bb, WD_M);
-            *reinterpret_cast<uint2 *>(A + o) = make_uint2(pack2(h[0], h[1]), pack2(h[2], h[3]));
-            *reinterpret_cast<uint2 *>(A + WD_A_PLANE + o) = make_uint2(pack2(m[0], m[1]), pack2(m[2], m[3]));
-            *reinterpret_cast<uint2 *>(A + 2 * WD_A_PLANE + o) = make_uint2(pack2(l[0], l[1]), pack2(l[2], l[3]));
+        // A = dZ0^T slice: element (unit u, sample b) = dZ0[b][u], MN-major (contiguous in u):
+        // 16-byte copies of 8 units from the train kernel's bf16 planes
+        {
+            const int64_t pz = (int64_t)p.B * p.N0;
+            for (int e = tid; e < 3 * WD_KS * (WD_M / 8); e += WD_T) {
+                const int pl = e / (WD_KS * (WD_M / 8)), r = e % (WD_KS * (WD_M / 8));
+                const int bb = r / (WD_M / 8), u = 8 * (r % (WD_M / 8));
+                const bool v = b0 + bb < p.B && u < p.N0;
+                wd_cp16(A + pl * WD_A_PLANE + wd_off_mn(u, bb, WD_M),
+                        v ? p.dZ0bf + pl * pz + (int64_t)(b0 + bb) * p.N0 + u : p.dZ0bf, v);
+            }
         }
         // B = U^T slice: element (input n, sample b) = U[b][n0 + n], MN-major (contiguous in n)
         for (int e = tid; e < WD_KS * (N / 16); e += WD_T) {
@@ -250,6 +260,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
             *reinterpret_cast<uint4 *>(Bs + wd_off_mn(n, bb, N)) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
             *reinterpret_cast<uint4 *>(Bs + wd_off_mn(n + 8, bb, N)) = make_uint4(o8[4], o8[5], o8[6], o8[7]);
         }
+        wd_cp_wait();
         umma::fence_async_smem();
         umma::fence_before_sync();
         __syncthreads();
@@ -272,28 +283,60 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
         umma::mbar_wait(&mbar[last & 1], (last >> 1) & 1);
     }
     umma::fence_after_sync();
-    // epilogue: g = D / 255 -> grad; w -= lr g (skipped on a non-finite loss); target
-    // sync on sync steps
+    // epilogue: the accumulator tile goes TMEM -> registers -> shared memory (the staging
+    // buffers are free: every MMA has completed), then each warp walks whole W0 rows so the
+    // weight, gradient and plane accesses are coalesced: g = D / 255 -> grad; w -= lr g
+    // (skipped on a non-finite loss); the target copy on sync steps
+    constexpr int TS = WD_MAXN + 4;                 // tile row stride (floats)
+    float *T = reinterpret_cast<float *>(sm);       // [128][TS]
     {
-        const float loss = __ldcg(p.grad + p.P);
-        const bool upd = p.apply_update && isfinite(loss);
-        const bool sync = *p.sync_flag != 0;
         const int q = warp & 3, half = warp >> 2, u = 32 * q + lane;
         const int c0 = half * (N / 2), c1 = c0 + N / 2;
         for (int c = c0; c < c1; c += 8) {
             float v[8];
             umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + c, v);
-            if (u >= p.N0) continue;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                if (c + i >= nn) continue;
-                const int64_t wi = p.w0 + (int64_t)u * p.D + n0 + c + i;
-                const float g = v[i] / 255.0f;
-                p.grad[wi] = g;
-                if (upd) {
-                    const float w = p.online_w[wi] - p.lr * g;
-                    p.online_w[wi] = w;
-                    if (sync) p.target_w[wi] = w;
+            *reinterpret_cast<float4 *>(T + u * TS + c) = make_float4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<float4 *>(T + u * TS + c + 4) = make_float4(v[4], v[5], v[6], v[7]);
+        }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    {
+        const float loss = __ldcg(p.grad + p.P);
+        const bool upd = p.apply_update && isfinite(loss);
+        const bool sync = *p.sync_flag != 0;
+        const int64_t nd = (int64_t)p.N0 * p.D;
+        for (int u = warp; u < p.N0; u += WD_T / 32) {
+            for (int c = 4 * lane; c < nn; c += 128) {
+                const int64_t j = (int64_t)u * p.D + n0 + c;   // index within W0
+                const int64_t wi = p.w0 + j;
+                const float4 t = *reinterpret_cast<const float4 *>(T + u * TS + c);
+                const float4 g = make_float4(t.x / 255.0f, t.y / 255.0f, t.z / 255.0f, t.w / 255.0f);
+                *reinterpret_cast<float4 *>(p.grad + wi) = g;
+                if (!upd) continue;
+                float4 w = *reinterpret_cast<const float4 *>(p.online_w + wi);
+                w.x -= p.lr * g.x;
+                w.y -= p.lr * g.y;
+                w.z -= p.lr * g.z;
+                w.w -= p.lr * g.w;
+                *reinterpret_cast<float4 *>(p.online_w + wi) = w;
+                // the next step's forward operand: W0's bf16 planes, split once here
+                uint16_t h[4], m[4], l[4];
+                umma::split3_bf16(w.x, h[0], m[0], l[0]);
+                umma::split3_bf16(w.y, h[1], m[1], l[1]);
+                umma::split3_bf16(w.z, h[2], m[2], l[2]);
+                umma::split3_bf16(w.w, h[3], m[3], l[3]);
+                const uint2 ph = make_uint2(pack2(h[0], h[1]), pack2(h[2], h[3]));
+                const uint2 pm = make_uint2(pack2(m[0], m[1]), pack2(m[2], m[3]));
+                const uint2 pl = make_uint2(pack2(l[0], l[1]), pack2(l[2], l[3]));
+                *reinterpret_cast<uint2 *>(p.W0bf + j) = ph;
+                *reinterpret_cast<uint2 *>(p.W0bf + nd + j) = pm;
+                *reinterpret_cast<uint2 *>(p.W0bf + 2 * nd + j) = pl;
+                if (sync) {
+                    *reinterpret_cast<float4 *>(p.target_w + wi) = w;
+                    *reinterpret_cast<uint2 *>(p.W0bf + 3 * nd + j) = ph;
+                    *reinterpret_cast<uint2 *>(p.W0bf + 4 * nd + j) = pm;
+                    *reinterpret_cast<uint2 *>(p.W0bf + 5 * nd + j) = pl;
                 }
             }
         }
