@@ -76,6 +76,7 @@ struct TrainArgs {
     int apply_update, do_sync;
     int wide_tc;           // layer 0 (forward partials, dW0 + its SGD) runs in wide.cuh kernels
     uint16_t *dZ0bf;       // wide_tc: bf16 hi / mid / lo planes of dZ0 [3][B][N0]
+    unsigned long long *trace;   // RPL_TRACE=1: per-phase %globaltimer of CTA 0 (else null)
     int ks0;               // split-K of the layer-0 forward (wide inputs): partials in PF0
     float *PF0;            // [ks0][nets][B][N0]
     unsigned *bar;         // [0] arrivals, [1] generation
@@ -337,12 +338,41 @@ __device__ void phase_head(const TrainArgs &p, TileSmem &sm)
             const float *bh = theta + p.hb_off;
             const float *h = p.H[L] + ((int64_t)net * B + b) * NH;
             for (int j = 0; j < J; ++j) {
+                // head row j over its input units: dueling V row over the V units, A rows over
+                // the A units; float4 loads, four in flight per lane where aligned
+                const int len = p.dueling ? S : NH;
+                const float *w = Wh + (int64_t)j * len;
+                const float *hh = p.dueling ? h + (j == 0 ? 0 : S) : h;
                 float acc = 0.0f;
-                if (p.dueling) {
-                    const float *hh = h + (j == 0 ? 0 : S);
-                    for (int u = lane; u < S; u += 32) acc = fmaf(__ldg(Wh + (int64_t)j * S + u), __ldcg(hh + u), acc);
+                if ((len & 3) == 0 && (((uintptr_t)w | (uintptr_t)hh) & 15) == 0) {
+                    const float4 *w4 = reinterpret_cast<const float4 *>(w);
+                    const float4 *h4 = reinterpret_cast<const float4 *>(hh);
+                    const int n4 = len >> 2;
+                    int u = lane;
+                    for (; u + 96 < n4; u += 128) {
+                        float4 wv[4], hv[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            wv[q] = __ldg(w4 + u + 32 * q);
+                            hv[q] = __ldcg(h4 + u + 32 * q);
+                        }
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            acc = fmaf(wv[q].x, hv[q].x, acc);
+                            acc = fmaf(wv[q].y, hv[q].y, acc);
+                            acc = fmaf(wv[q].z, hv[q].z, acc);
+                            acc = fmaf(wv[q].w, hv[q].w, acc);
+                        }
+                    }
+                    for (; u < n4; u += 32) {
+                        const float4 wv = __ldg(w4 + u), hv = __ldcg(h4 + u);
+                        acc = fmaf(wv.x, hv.x, acc);
+                        acc = fmaf(wv.y, hv.y, acc);
+                        acc = fmaf(wv.z, hv.z, acc);
+                        acc = fmaf(wv.w, hv.w, acc);
+                    }
                 } else {
-                    for (int u = lane; u < NH; u += 32) acc = fmaf(__ldg(Wh + (int64_t)j * NH + u), __ldcg(h + u), acc);
+                    for (int u = lane; u < len; u += 32) acc = fmaf(__ldg(w + u), __ldcg(hh + u), acc);
                 }
                 acc = warp_sum(acc);
                 if (lane == 0) hs[j] = acc + __ldg(bh + j);
@@ -438,10 +468,10 @@ __device__ void phase_backward(const TrainArgs &p, int l, TileSmem &sm)
     // (ii) dH_{l-1} split-K partials: M = B, N-dim = K, contraction over units
     const int hmt = (B + BM - 1) / BM, hnt = (K + BN - 1) / BN;
     const int n_h = l > 0 ? hmt * hnt * p.nsplit_n[l] : 0;
-    // (iii) head weight gradients (l == T-1): 256 head-input units per task, per b-split
-    const int hu = (p.dueling ? p.S : p.NH);
-    const int n_hd_u = (l == p.T - 1) ? ((p.dueling ? 2 * hu : hu) + NT - 1) / NT : 0;
-    const int n_hd = (l == p.T - 1) ? (n_hd_u + 1) * p.nsplit_b : 0;
+    // (iii) head weight gradients (l == T-1) as GEMM tiles over (head row j, head-input unit u):
+    //       g_Wh[j][u] = sum_b dO[b][j] h[b][u], per b-split; the bias rows come with n0 == 0
+    const int hjt = (p.J + BM - 1) / BM, hut = (p.NH + BN - 1) / BN;
+    const int n_hd = (l == p.T - 1) ? hjt * hut * p.nsplit_b : 0;
     const float *Hprev = (l == 0) ? p.Xs : p.H[l - 1];
     const int ntasks = n_w + n_h + n_hd;
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
@@ -480,54 +510,23 @@ __device__ void phase_backward(const TrainArgs &p, int l, TileSmem &sm)
         } else {
             // head gradients: g_Wh[j][u] = sum_b dO[b][j] h[b][u]; g_bh[j] = sum_b dO[b][j]
             const int u = t - n_w - n_h;
-            const int s = u / (n_hd_u + 1), c = u % (n_hd_u + 1);
+            const int s = u / (hjt * hut), rem = u % (hjt * hut);
+            const int m0 = (rem / hut) * BM, n0 = (rem % hut) * BN;
             const int kb = s * p.bsplit, ke = min(B, kb + p.bsplit);
             float *gp = p.gpart + (int64_t)s * p.P;
-            const int J = p.J, NH = p.NH;
-            const float *h = p.H[p.T - 1];   // online net on s
-            if (c < n_hd_u) {
-                const int unit = c * NT + threadIdx.x;   // index into the head-input units
-                if (unit < NH) {
-                    if (p.dueling) {
-                        const int S = p.S;
-                        if (unit < S) {
-                            float acc = 0.0f;
-                            for (int b = kb; b < ke; ++b) acc = fmaf(__ldcg(p.dO + (int64_t)b * J), __ldcg(h + (int64_t)b * NH + unit), acc);
-                            gp[p.hw_off + unit] = acc;
-                        } else {
-                            float acc[MAXA];
-#pragma unroll
-                            for (int a = 0; a < MAXA; ++a) acc[a] = 0.0f;
-                            for (int b = kb; b < ke; ++b) {
-                                const float hv = __ldcg(h + (int64_t)b * NH + unit);
-#pragma unroll
-                                for (int a = 0; a < MAXA; ++a)
-                                    if (a < p.A) acc[a] = fmaf(__ldcg(p.dO + (int64_t)b * J + 1 + a), hv, acc[a]);
-                            }
-#pragma unroll
-                            for (int a = 0; a < MAXA; ++a)
-                                if (a < p.A) gp[p.hw_off + (int64_t)(1 + a) * S + (unit - S)] = acc[a];
-                        }
-                    } else {
-                        float acc[MAXA];
-#pragma unroll
-                        for (int a = 0; a < MAXA; ++a) acc[a] = 0.0f;
-                        for (int b = kb; b < ke; ++b) {
-                            const float hv = __ldcg(h + (int64_t)b * NH + unit);
-#pragma unroll
-                            for (int a = 0; a < MAXA; ++a)
-                                if (a < p.A) acc[a] = fmaf(__ldcg(p.dO + (int64_t)b * J + a), hv, acc[a]);
-                        }
-#pragma unroll
-                        for (int a = 0; a < MAXA; ++a)
-                            if (a < p.A) gp[p.hw_off + (int64_t)a * NH + unit] = acc[a];
-                    }
-                }
-            } else if (threadIdx.x < J) {
-                float acc = 0.0f;
-                for (int b = kb; b < ke; ++b) acc += __ldcg(p.dO + (int64_t)b * J + threadIdx.x);
-                gp[p.hb_off + threadIdx.x] = acc;
-            }
+            const int J = p.J, NH = p.NH, S = p.S;
+            LdRMajor la{p.dO, J, J, kb, ke};
+            LdRMajor lb{p.H[p.T - 1], NH, NH, kb, ke};   // online net on s
+            auto epi = [&](int j, int unit, float v) {
+                if (j >= J || unit >= NH) return;
+                if (!p.dueling) gp[p.hw_off + (int64_t)j * NH + unit] = v;
+                else if (j == 0 && unit < S) gp[p.hw_off + unit] = v;                          // V head
+                else if (j > 0 && unit >= S) gp[p.hw_off + (int64_t)j * S + (unit - S)] = v;   // A head
+            };
+            auto rs = [&](int j, float v) {
+                if (j < J) gp[p.hb_off + j] = v;
+            };
+            gemm_tile(la, lb, m0, n0, kb, ke, epi, n0 == 0, rs, sm);
         }
     }
 }
@@ -588,28 +587,45 @@ __device__ void phase_sgd(const TrainArgs &p, TileSmem &sm)
 __global__ void __launch_bounds__(NT, 1) train_step_kernel(const __grid_constant__ TrainArgs p)
 {
     __shared__ TileSmem sm;
+    // RPL_TRACE=1: %globaltimer after every phase (CTA 0), slots of kernel 0 in the trace
+    int mk = 0;
+    auto mark = [&]() {
+        if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            p.trace[mk] = t;
+        }
+        ++mk;
+    };
+    mark();
     for (int l = 0; l < p.T; ++l) {
         if (!(l == 0 && p.wide_tc)) {   // wide_tc: sampled, gathered and multiplied already
             phase_forward(p, l, sm);
             grid_barrier(p.bar);
         }
+        mark();
         if (l == 0 && p.ks0 > 1) {
             phase_l0_reduce(p);
             grid_barrier(p.bar);
         }
+        mark();
     }
     phase_head(p, sm);
     grid_barrier(p.bar);
+    mark();
     for (int l = p.T - 1; l >= 0; --l) {
         if (l == 0 && p.ks0 > 1 && p.T > 1) {
             phase_dz0(p);
             grid_barrier(p.bar);
         }
+        mark();
         if (l == 0 && p.wide_tc) break;   // dW0 and its SGD follow in wide_dw0_kernel
         phase_backward(p, l, sm);
         grid_barrier(p.bar);
+        mark();
     }
     phase_sgd(p, sm);
+    mark();
 }
 
 // SGD after an NCCL all-reduce (world > 1): grad[P] holds the rank-averaged loss
@@ -1094,6 +1110,7 @@ static void fill_args(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.ks0 = ks0_for(d, B);
     p.PF0 = d->PF0;
     p.dZ0bf = d->dz0bf;
+    p.trace = d->trace;
     p.bar = d->bar;
     p.err = d->err;
     p.rctrl = rp->ctrl_dev;
