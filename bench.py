@@ -388,6 +388,49 @@ def run_ours(a, batch, first_line=True):
                   "note": "replay_gather of 4M uniform indices from the 256 MB ring (> L2); algorithmic "
                           "bytes = 228 B packed row read + 229 B unpacked write per index; peak = "
                           f"{peaks_kind} HBM copy bandwidth"}
+        # the same gather across launch sizes (latency -> bandwidth bound)
+        sweep = []
+        for m in (128, 4096, 65536, 1 << 20, 1 << 22):
+            sub = {kk: v[:m] for kk, v in out.items()}
+            for _ in range(3):
+                rp.gather(idx[:m], sub)
+            reps_m = 50 if m <= 65536 else 10
+            gs.record(stream)
+            for _ in range(reps_m):
+                rp.gather(idx[:m], sub)
+            ge.record(stream)
+            torch.cuda.synchronize()
+            t_ms = gs.elapsed_time(ge) / reps_m
+            sweep.append({"indices": m, "us": t_ms * 1000.0,
+                          "GBps": m * (ROW_READ_BYTES + ROW_WRITE_BYTES) / (t_ms / 1000.0) / 1e9})
+        gather["sweep"] = sweep
+        rp.check()
+        # insert cost vs block size k (the B200 version of P:119-125, Fig. 3),
+        # host-sourced (one pinned H2D copy inside replay_add) and device-sourced
+        ins = []
+        big = experiences(10_000, seed=13, rank=rank)
+        big_d = {kk: torch.from_numpy(v).to(dev) for kk, v in big.items()}
+        for kk_ in (1, 10, 100, 2000, 10_000):
+            row = {"k": kk_}
+            for src, pool in (("host", big), ("device", big_d)):
+                part = {kx: v[:kk_] for kx, v in pool.items()}
+                for _ in range(3):
+                    rp.add(**part)
+                reps_i = 20
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                gs.record(stream)
+                for _ in range(reps_i):
+                    rp.add(**part)
+                ge.record(stream)
+                torch.cuda.synchronize()
+                wall = (time.perf_counter() - t0) / reps_i
+                dev_s = gs.elapsed_time(ge) / 1000.0 / reps_i
+                t = max(wall, dev_s)
+                row[f"{src}_us_per_experience"] = t * 1e6 / kk_
+                row[f"{src}_GBps"] = kk_ * EXP_INPUT_BYTES / t / 1e9
+            ins.append(row)
+        gather["insert_sweep"] = ins
         rp.check()
 
     # ---- CPU oracle baseline (rank 0, N=1 only) ------------------------------------------
