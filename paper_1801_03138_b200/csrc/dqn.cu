@@ -739,6 +739,7 @@ struct rpl_dqn {
     std::vector<GraphEntry> graphs;
     bool use_graphs = true;
     bool use_pdl = false;                  // programmatic dependent launch inside the graph
+    bool k3_pdl = true;                    // K3 alone programmatic after K2
     bool wide_tc = false;                  // byte-state wide inputs: layer 0 on tcgen05 (wide.cuh)
     uint16_t *w0bf = nullptr;              // bf16 planes of W0 [online, target][3][N0 * D]
     uint16_t *dz0bf = nullptr;             // bf16 planes of dZ0 [3][max_batch][N0]
@@ -969,6 +970,8 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
     // start early compete for SM slots); opt in with RPL_PDL=1
     const char *np = getenv("RPL_PDL");
     d->use_pdl = np && np[0] == '1';
+    const char *nk = getenv("RPL_NO_K3PDL");
+    d->k3_pdl = !(nk && nk[0] == '1');
     ok = ok && dalloc(d, &d->step_dev, 1) && dalloc(d, &d->sync_flag, 1);
     const char *tr = getenv("RPL_TRACE");
     if (ok && tr && tr[0] == '1') {
@@ -1234,8 +1237,10 @@ static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
     const int n_h = ((p.B + BM - 1) / BM) * ((p.N0 + K3N - 1) / K3N) * p.NS;
     const int hd_passes = p.dueling ? (p.A + 7) / 8 : (p.J + 7) / 8;
     const int n_hd = (((p.N1 + HD_U - 1) / HD_U) * hd_passes + 1) * p.nsb;
+    // K3 always programmatic: it stages K1's operands while K2 finishes (griddepcontrol.wait
+    // before K2's outputs); RPL_NO_K3PDL=1 serialises it
     e = launch_pdl(fast_bwd1_kernel, std::min(n_w + n_h + n_hd, 2 * d->sms), F_NT3,
-                   K3_SMEM_FLOATS * sizeof(float), st, pdl, p);
+                   K3_SMEM_FLOATS * sizeof(float), st, pdl || d->k3_pdl, p);
     if (e != cudaSuccess) return e;
     return launch_pdl(fast_bwd0_sgd_kernel, d->sms, NT, 0, st, pdl, p);
 }

@@ -815,8 +815,9 @@ __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int 
     const int mr = 16 * wm + g;
     for (int k0 = kb; k0 < ke; k0 += MM_SK) {
         __syncthreads();   // the previous pass / task is done with the staging buffers
-        mm_stage<kARc, BM>(As, a, m0, k0, ke, tid);
         mm_stage<kBRc, K3N>(Bs, b, n0, k0, ke, tid);
+        if (k0 == kb) pdl_wait();   // A is K2's dZ1 (no-op without a programmatic launch)
+        mm_stage<kARc, BM>(As, a, m0, k0, ke, tid);
         cp_async_wait_all();
         __syncthreads();
         if (tr && k0 == kb) tr->mark(mk);
@@ -881,8 +882,9 @@ constexpr int K3_SMEM_FLOATS = K3_DH_FLOATS > K3_HD_FLOATS ? K3_DH_FLOATS : K3_H
 
 __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant__ FastArgs p)
 {
-    pdl_trigger();
-    pdl_wait();
+    // K3 is launched programmatically after K2: every operand K1 (or an earlier step) wrote
+    // -- H0, H1, W1, the states -- is requested before griddepcontrol.wait, K2's dZ1 / dHead
+    // after it, so the weight / activation half of the staging overlaps K2
     CtaTrace trace_(p.trace, 2);
     extern __shared__ float4 smem4[];
     float *k3raw = reinterpret_cast<float *>(smem4);   // K3_SMEM_FLOATS
@@ -984,6 +986,7 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             float *gp = p.gpart + (int64_t)s * p.P;
             if (c == hd_tasks) {
                 // warp w reduces head rows j = w, w + 4, ...: lanes stride the samples
+                pdl_wait();
                 const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
                 for (int j = w; j < J; j += F_NT3 / 32) {
                     float acc = 0.0f;
@@ -1020,6 +1023,7 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
                             hsm[e] = u0 + q < N1 ? __ldcg(p.H1 + (int64_t)(c0 + bb) * N1 + u0 + q) : 0.0f;
                         }
                     }
+                    pdl_wait();   // dHead is K2's
                     for (int e = threadIdx.x; e < cn * J; e += F_NT3) cp_async4(dsm + e, p.dHead + (int64_t)c0 * J + e);
                     cp_async_wait_all();
                     __syncthreads();
