@@ -739,7 +739,8 @@ struct rpl_dqn {
     std::vector<GraphEntry> graphs;
     bool use_graphs = true;
     bool use_pdl = false;                  // programmatic dependent launch inside the graph
-    bool k3_pdl = true;                    // K3 alone programmatic after K2
+    bool k3_pdl = true;                    // K3 programmatic after K2
+    bool k2_pdl = false, k4_pdl = false;   // experiments: RPL_K2PDL=1, RPL_K4PDL=1
     bool wide_tc = false;                  // byte-state wide inputs: layer 0 on tcgen05 (wide.cuh)
     uint16_t *w0bf = nullptr;              // bf16 planes of W0 [online, target][3][N0 * D]
     uint16_t *dz0bf = nullptr;             // bf16 planes of dZ0 [3][max_batch][N0]
@@ -972,6 +973,9 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
     d->use_pdl = np && np[0] == '1';
     const char *nk = getenv("RPL_NO_K3PDL");
     d->k3_pdl = !(nk && nk[0] == '1');
+    const char *n2 = getenv("RPL_K2PDL"), *n4 = getenv("RPL_K4PDL");
+    d->k2_pdl = n2 && n2[0] == '1';
+    d->k4_pdl = n4 && n4[0] == '1';
     ok = ok && dalloc(d, &d->step_dev, 1) && dalloc(d, &d->sync_flag, 1);
     const char *tr = getenv("RPL_TRACE");
     if (ok && tr && tr[0] == '1') {
@@ -1231,7 +1235,8 @@ static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
     const bool pdl = d->use_pdl;
     cudaError_t e = launch_pdl(fast_fwd_fn(d), g1, F_NT1, sm1, st, false, p);
     if (e != cudaSuccess) return e;
-    e = launch_pdl(fast_td_kernel, std::min(p.B, 4 * d->sms), NT, fast_td_smem(d), st, pdl, p);
+    e = launch_pdl(fast_td_kernel, std::min(p.B, 4 * d->sms), NT, fast_td_smem(d), st,
+                   pdl || d->k2_pdl, p);
     if (e != cudaSuccess) return e;
     const int n_w = ((p.N1 + BM - 1) / BM) * ((p.N0 + K3N - 1) / K3N) * p.nsb;
     const int n_h = ((p.B + BM - 1) / BM) * ((p.N0 + K3N - 1) / K3N) * p.NS;
@@ -1242,7 +1247,7 @@ static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
     e = launch_pdl(fast_bwd1_kernel, std::min(n_w + n_h + n_hd, 2 * d->sms), F_NT3,
                    K3_SMEM_FLOATS * sizeof(float), st, pdl || d->k3_pdl, p);
     if (e != cudaSuccess) return e;
-    return launch_pdl(fast_bwd0_sgd_kernel, d->sms, NT, 0, st, pdl, p);
+    return launch_pdl(fast_bwd0_sgd_kernel, d->sms, NT, 0, st, pdl || d->k4_pdl, p);
 }
 
 static int grid_for(const rpl_dqn *d, const TrainArgs &p)
