@@ -1230,7 +1230,11 @@ static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
 {
     const int nbt = (p.B + F_BT - 1) / F_BT;
     const int k1_tasks = p.nets * nbt * p.nut;
-    const int g1 = std::min(k1_tasks, d->sms);
+    // large batches: a multiple of the nets x unit-tile combinations, so every CTA keeps one
+    // weight tile resident across its batch tiles
+    const int ncombo = p.nets * p.nut;
+    int g1 = std::min(k1_tasks, d->sms);
+    if (k1_tasks > d->sms && ncombo <= d->sms) g1 = (d->sms / ncombo) * ncombo;
     const size_t sm1 = fast_fwd_smem(d, p.UT);
     const bool pdl = d->use_pdl;
     cudaError_t e = launch_pdl(fast_fwd_fn(d), g1, F_NT1, sm1, st, false, p);

@@ -269,15 +269,21 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
     const uint64_t size = p.pend_k ? p.pend_size : p.rctrl[1];
     if (p.pend_k && blockIdx.x == 0 && threadIdx.x == 0) p.rctrl[1] = p.pend_size;
     const int ntasks = p.nets * nbt * nut;
+    // tasks are (net, unit tile)-major: with the grid a multiple of nets x nut (large batches),
+    // a CTA keeps one weight tile resident and walks batch tiles, loading the weights once
+    const int ncombo = p.nets * nut;
+    int loaded = -1;
     for (int task = blockIdx.x; task < ntasks; task += gridDim.x) {
-        const int net = task / (nbt * nut), rem = task % (nbt * nut);
-        const int bt = rem / nut, ut = rem % nut;
+        const int combo = task % ncombo, bt = task / ncombo;
+        const int net = combo / nut, ut = combo % nut;
         const int rb = bt * F_BT, u0 = ut * UT;
         const int nu = min(UT, N1 - u0);   // valid units in this tile (multiple of 4)
         const float *theta = net == 1 ? p.target : p.online;
+        const bool reload = combo != loaded;
+        loaded = combo;
         __syncthreads();   // the previous task is done with shared memory
         // (1) weights -> shared memory, all 16-byte cp.async (no load waits on another)
-        {
+        if (reload) {
             const int c4 = N0 / 4;
             for (int e = tid; e < UT * c4; e += F_NT1) {
                 const int u = e / c4, c = e - u * c4;
@@ -285,12 +291,12 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
                 if (u < nu) cp_async16(dst, theta + p.w1 + (int64_t)(u0 + u) * N0 + 4 * c);
                 else *reinterpret_cast<float4 *>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
             }
+            cp_async_row(W0f, theta + p.w0, N0 * D, tid, F_NT1);
+            cp_async_row(b0s, theta + p.b0, N0, tid, F_NT1);
+            cp_async_row(b1s, theta + p.b1 + u0, nu, tid, F_NT1);
+            for (int u = nu + tid; u < UT; u += F_NT1) b1s[u] = 0.0f;
         }
-        cp_async_row(W0f, theta + p.w0, N0 * D, tid, F_NT1);
-        cp_async_row(b0s, theta + p.b0, N0, tid, F_NT1);
-        cp_async_row(b1s, theta + p.b1 + u0, nu, tid, F_NT1);
-        for (int u = nu + tid; u < UT; u += F_NT1) b1s[u] = 0.0f;
-        {
+        if (reload) {
             // head weights of the tile's units: dueling V row (j = 0) over V units, A rows
             // (j >= 1) over A units (a tile never straddles the streams: S % UT == 0)
             const bool vtile = p.dueling && u0 < p.S;
