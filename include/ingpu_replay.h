@@ -49,6 +49,7 @@ enum {
 enum { RPL_HOST = 0, RPL_DEVICE = 1, RPL_DEVICE_DEFER = 2 };
 enum { RPL_ONLINE = 0, RPL_TARGET = 1, RPL_GRAD = 2 };  /* which parameter vector          */
 enum { RPL_F32 = 0, RPL_U8 = 1 };                        /* state element type of a replay  */
+enum { RPL_SAMPLE_UNIFORM = 0, RPL_SAMPLE_DISTINCT = 1 }; /* sampler of a replay            */
 
 typedef struct rpl_replay rpl_replay;   /* opaque */
 typedef struct rpl_dqn rpl_dqn;         /* opaque */
@@ -68,6 +69,9 @@ typedef struct {
     int32_t state_dtype;  /* RPL_F32 (default, the paper's float states) or RPL_U8
                              (Atari-shaped byte states; the network input is x = u8/255,
                              SURVEY reading Q27)                                            */
+    int32_t sampling;     /* RPL_SAMPLE_UNIFORM (default: uniform with replacement) or
+                             RPL_SAMPLE_DISTINCT (P:75's planned switch: the first B distinct
+                             values of the same index stream; needs size >= B, B <= 7168)    */
 } rpl_replay_opts;
 
 /* Create an empty FIFO replay of `capacity` experiences whose states are `state_dim`
@@ -124,8 +128,10 @@ typedef struct {
  * + unpack the rows into *out.  Index i of event E is
  *   Philox4x32-10(ctr = (i/2, E_lo, E_hi, (1<<24)|rank), key = (seed_lo, seed_hi)),
  *   u = words (x1:x0) for even i, (x3:x2) for odd i, idx = floor(u * size / 2^64).
- * Consumes one sampler event (E += 1).  Returns RPL_NOT_READY (nothing done) while
- * size < burn_in.  Errors: EINVAL (B < 1). */
+ * Consumes one sampler event (E += 1).  RPL_SAMPLE_DISTINCT replays take the first B
+ * distinct values of that index stream (position t = index t of the formula above), in
+ * stream order.  Returns RPL_NOT_READY (nothing done) while size < burn_in (or, distinct,
+ * size < B).  Errors: EINVAL (B < 1; distinct B > 7168). */
 int replay_sample(rpl_replay *replay, int32_t batch, const rpl_batch *out);
 
 /* Gather + unpack the rows at the caller's DEVICE indices idx_dev[0..n) (each must be

@@ -82,6 +82,30 @@ void oracle_sample_indices(uint64_t seed, uint32_t rank, uint64_t event, int64_t
     }
 }
 
+/* Distinct sampling ("I plan on switching back to sampling distinct integers", i.e.
+ * the in-RAM random.sample semantics): the first `batch` DISTINCT values
+ * of the same uniform index stream, in stream order (reading Q29).  Needs n >= batch. */
+int oracle_sample_distinct(uint64_t seed, uint32_t rank, uint64_t event, int64_t n,
+                           int32_t batch, int32_t *idx)
+{
+    if (n < batch) return ORACLE_EINVAL;
+    int32_t count = 0;
+    for (int64_t t = 0; count < batch; ++t) {
+        int32_t v;
+        uint32_t ctr[4] = {(uint32_t)(t / 2), (uint32_t)event, (uint32_t)(event >> 32),
+                           (ORACLE_TAG_SAMPLE << 24) | (rank & 0xFFFFFFu)};
+        uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+        uint32_t x[4];
+        oracle_philox4x32_10(ctr, key, x);
+        uint64_t u = (t % 2 == 0) ? (((uint64_t)x[1] << 32) | x[0]) : (((uint64_t)x[3] << 32) | x[2]);
+        v = (int32_t)(uint64_t)(((unsigned __int128)u * (unsigned __int128)(uint64_t)n) >> 64);
+        int seen = 0;
+        for (int32_t j = 0; j < count && !seen; ++j) seen = idx[j] == v;
+        if (!seen) idx[count++] = v;
+    }
+    return ORACLE_OK;
+}
+
 /* ------------------------------------------------------------------------------------
  * The replay: ONE packed array of C rows x (2D+3) floats, exactly the paper's layout
  * (P:71 [Methods]: "the experience replay Variable has shape 1,000,000 by 57"; action and
@@ -101,6 +125,7 @@ int oracle_ring_init(oracle_ring *ring, int64_t capacity, int32_t state_dim)
     ring->size = 0;
     ring->total = 0;
     ring->events = 0;
+    ring->distinct = 0;
     return ORACLE_OK;
 }
 
@@ -161,7 +186,12 @@ int oracle_ring_sample(oracle_ring *ring, int64_t burn_in, uint64_t seed, uint32
                        float *s_next, uint8_t *done)
 {
     if (ring->size < burn_in || ring->size < 1) return ORACLE_NOT_READY;
-    oracle_sample_indices(seed, rank, ring->events, ring->size, batch, idx);
+    if (ring->distinct) {
+        if (ring->size < batch) return ORACLE_NOT_READY;   /* reading Q29 */
+        oracle_sample_distinct(seed, rank, ring->events, ring->size, batch, idx);
+    } else {
+        oracle_sample_indices(seed, rank, ring->events, ring->size, batch, idx);
+    }
     ring->events += 1;
     return oracle_ring_gather(ring, batch, idx, s, a, r, s_next, done);
 }
@@ -185,6 +215,7 @@ int oracle_ring_u8_init(oracle_ring_u8 *ring, int64_t capacity, int32_t state_di
     ring->size = 0;
     ring->total = 0;
     ring->events = 0;
+    ring->distinct = 0;
     if (!ring->s || !ring->s_next || !ring->a || !ring->r || !ring->done) {
         oracle_ring_u8_free(ring);
         return ORACLE_ENOMEM;
@@ -242,7 +273,12 @@ int oracle_ring_u8_sample(oracle_ring_u8 *ring, int64_t burn_in, uint64_t seed, 
                           uint8_t *s_next, uint8_t *done)
 {
     if (ring->size < burn_in || ring->size < 1) return ORACLE_NOT_READY;
-    oracle_sample_indices(seed, rank, ring->events, ring->size, batch, idx);
+    if (ring->distinct) {
+        if (ring->size < batch) return ORACLE_NOT_READY;   /* reading Q29 */
+        oracle_sample_distinct(seed, rank, ring->events, ring->size, batch, idx);
+    } else {
+        oracle_sample_indices(seed, rank, ring->events, ring->size, batch, idx);
+    }
     ring->events += 1;
     return oracle_ring_u8_gather(ring, batch, idx, s, a, r, s_next, done);
 }

@@ -20,6 +20,8 @@ enum { ORACLE_TAG_SAMPLE = 1 };
 void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 void oracle_sample_indices(uint64_t seed, uint32_t rank, uint64_t event, int64_t n,
                            int32_t batch, int32_t *idx);
+int oracle_sample_distinct(uint64_t seed, uint32_t rank, uint64_t event, int64_t n,
+                           int32_t batch, int32_t *idx);
 
 typedef struct {
     int64_t capacity;
@@ -30,6 +32,7 @@ typedef struct {
     int64_t size;        /* filled slots, <= capacity */
     uint64_t total;      /* experiences ever added */
     uint64_t events;     /* sampler events consumed */
+    int32_t distinct;    /* 1: sample distinct indices (oracle_sample_distinct) */
 } oracle_ring;
 
 int oracle_ring_init(oracle_ring *ring, int64_t capacity, int32_t state_dim);
@@ -52,6 +55,7 @@ typedef struct {
     uint8_t *done;
     int64_t cursor, size;
     uint64_t total, events;
+    int32_t distinct;    /* 1: sample distinct indices (oracle_sample_distinct) */
 } oracle_ring_u8;
 
 int oracle_ring_u8_init(oracle_ring_u8 *ring, int64_t capacity, int32_t state_dim);

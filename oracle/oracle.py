@@ -53,6 +53,7 @@ class _Ring(C.Structure):
         ("size", C.c_int64),
         ("total", C.c_uint64),
         ("events", C.c_uint64),
+        ("distinct", C.c_int32),
     ]
 
 
@@ -69,6 +70,7 @@ class _RingU8(C.Structure):
         ("size", C.c_int64),
         ("total", C.c_uint64),
         ("events", C.c_uint64),
+        ("distinct", C.c_int32),
     ]
 
 
@@ -106,6 +108,8 @@ _P = C.c_void_p
 def _declare(L):
     L.oracle_philox4x32_10.argtypes = [_P, _P, _P]
     L.oracle_sample_indices.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_int64, C.c_int32, _P]
+    L.oracle_sample_distinct.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_int64, C.c_int32, _P]
+    L.oracle_sample_distinct.restype = C.c_int
     L.oracle_ring_init.argtypes = [C.POINTER(_Ring), C.c_int64, C.c_int32]
     L.oracle_ring_init.restype = C.c_int
     L.oracle_ring_free.argtypes = [C.POINTER(_Ring)]
@@ -170,15 +174,25 @@ def sample_indices(seed: int, rank: int, event: int, n: int, batch: int) -> np.n
     return idx
 
 
+def sample_distinct(seed: int, rank: int, event: int, n: int, batch: int) -> np.ndarray:
+    """oracle_sample_distinct: the first `batch` distinct values of the index stream."""
+    idx = np.zeros(batch, dtype=np.int32)
+    rc = lib().oracle_sample_distinct(seed, rank, event, n, batch, _ptr(idx))
+    if rc != OK:
+        raise ValueError(f"oracle_sample_distinct rc={rc}")
+    return idx
+
+
 # ------------------------------------------------------------------------------------
 # The replay ring (paper layout: packed 2D+3 floats per row, P:71)
 # ------------------------------------------------------------------------------------
 class Ring:
-    def __init__(self, capacity: int, state_dim: int):
+    def __init__(self, capacity: int, state_dim: int, distinct: bool = False):
         self._r = _Ring()
         rc = lib().oracle_ring_init(C.byref(self._r), capacity, state_dim)
         if rc != OK:
             raise ValueError(f"oracle_ring_init rc={rc}")
+        self._r.distinct = 1 if distinct else 0
         self.state_dim = state_dim
 
     def __del__(self):
@@ -264,11 +278,12 @@ class RingU8:
     """Byte-state replay (SURVEY config 5): oracle_ring_u8_* (same FIFO / sampler / gather
     as Ring over uint8 states)."""
 
-    def __init__(self, capacity: int, state_dim: int):
+    def __init__(self, capacity: int, state_dim: int, distinct: bool = False):
         self._r = _RingU8()
         rc = lib().oracle_ring_u8_init(C.byref(self._r), capacity, state_dim)
         if rc != OK:
             raise ValueError(f"oracle_ring_u8_init rc={rc}")
+        self._r.distinct = 1 if distinct else 0
         self.state_dim = state_dim
 
     def __del__(self):

@@ -48,7 +48,7 @@ class RplError(RuntimeError):
 class _ReplayOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("cuda_stream", C.c_void_p), ("burn_in", C.c_int64),
                 ("seed", C.c_uint64), ("rank", C.c_uint32), ("max_host_add", C.c_int64),
-                ("state_dtype", C.c_int32)]
+                ("state_dtype", C.c_int32), ("sampling", C.c_int32)]
 
 
 class _Batch(C.Structure):
@@ -146,7 +146,7 @@ class Replay:
 
     def __init__(self, capacity: int, state_dim: int, *, device: int = 0, stream=None,
                  burn_in: int = 1, seed: int = 2, rank: int = 0, max_host_add: int = 0,
-                 state_dtype: str = "f32"):
+                 state_dtype: str = "f32", sampling: str = "uniform"):
         torch = _torch()
         if not torch.cuda.is_available():
             raise RplError(RPL_ECUDA, "no CUDA device (the in-GPU replay has no CPU fallback)")
@@ -157,7 +157,7 @@ class Replay:
         with torch.cuda.device(device):
             self._stream = _stream_handle(stream)
         o = _ReplayOpts(device, self._stream, burn_in, seed, rank, max_host_add,
-                        RPL_U8 if self.u8 else RPL_F32)
+                        RPL_U8 if self.u8 else RPL_F32, 1 if sampling == "distinct" else 0)
         h = C.c_void_p()
         _ok(_L.replay_create(capacity, state_dim, C.byref(o), C.byref(h)))
         self._h = h

@@ -75,6 +75,7 @@ struct TrainArgs {
     float *loss_out;
     int apply_update, do_sync;
     int wide_tc;           // layer 0 (forward partials, dW0 + its SGD) runs in wide.cuh kernels
+    int distinct;          // batch indices precomputed by distinct_kernel into idx
     uint16_t *dZ0bf;       // wide_tc: bf16 hi / mid / lo planes of dZ0 [3][B][N0]
     unsigned long long *trace;   // RPL_TRACE=1: per-phase %globaltimer of CTA 0 (else null)
     int ks0;               // split-K of the layer-0 forward (wide inputs): partials in PF0
@@ -226,7 +227,12 @@ __device__ void phase_forward(const TrainArgs &p, int l, TileSmem &sm)
             if (threadIdx.x < BM / 2) {
                 const int pair = (m0 >> 1) + threadIdx.x;
                 int32_t i0, i1;
-                sample_pair(p.seed, p.rank, p.event, (uint32_t)pair, (uint64_t)p.size, i0, i1);
+                if (p.distinct) {
+                    i0 = 2 * pair < B ? p.idx[2 * pair] : 0;
+                    i1 = 2 * pair + 1 < B ? p.idx[2 * pair + 1] : 0;
+                } else {
+                    sample_pair(p.seed, p.rank, p.event, (uint32_t)pair, (uint64_t)p.size, i0, i1);
+                }
                 sm.idx[2 * threadIdx.x] = i0;
                 sm.idx[2 * threadIdx.x + 1] = i1;
             }
@@ -734,6 +740,7 @@ struct rpl_dqn {
         cudaGraph_t graph;          // kept alive: k1 is one of its nodes
         cudaGraphExec_t exec;
         cudaGraphNode_t k1;         // K1's node (its args carry the deferred insert)
+        cudaGraphNode_t ds;         // distinct sampler's node (same args) or null
         FastArgs k1args;            // the args K1's node currently holds
     };
     std::vector<GraphEntry> graphs;
@@ -971,6 +978,8 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
     // start early compete for SM slots); opt in with RPL_PDL=1
     const char *np = getenv("RPL_PDL");
     d->use_pdl = np && np[0] == '1';
+    ok = ok && cudaFuncSetAttribute(distinct_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)ds_smem_bytes(DS_MAXB)) == cudaSuccess;
     const char *nk = getenv("RPL_NO_K3PDL");
     d->k3_pdl = !(nk && nk[0] == '1');
     const char *n2 = getenv("RPL_K2PDL"), *n4 = getenv("RPL_K4PDL");
@@ -1115,6 +1124,7 @@ static void fill_args(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.apply_update = apply;
     p.do_sync = do_sync;
     p.ks0 = ks0_for(d, B);
+    p.distinct = rp->distinct ? 1 : 0;
     p.PF0 = d->PF0;
     p.dZ0bf = d->dz0bf;
     p.trace = d->trace;
@@ -1189,6 +1199,7 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.apply_update = apply;
     p.err = d->err;
     p.trace = d->trace;
+    p.distinct = rp->distinct ? 1 : 0;
     p.capacity = rp->ring.capacity;
     const rpl_replay::Pending &q = rp->pend;
     if (q.k > 0) {   // consumed by this step's K1 (dqn_train_step clears it)
@@ -1237,7 +1248,12 @@ static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
     if (k1_tasks > d->sms && ncombo <= d->sms) g1 = (d->sms / ncombo) * ncombo;
     const size_t sm1 = fast_fwd_smem(d, p.UT);
     const bool pdl = d->use_pdl;
-    cudaError_t e = launch_pdl(fast_fwd_fn(d), g1, F_NT1, sm1, st, false, p);
+    cudaError_t e;
+    if (p.distinct) {   // distinct batch indices first (distinct.cuh)
+        e = launch_pdl(distinct_fast_kernel, 1, DS_T, ds_smem_bytes(p.B), st, false, p);
+        if (e != cudaSuccess) return e;
+    }
+    e = launch_pdl(fast_fwd_fn(d), g1, F_NT1, sm1, st, false, p);
     if (e != cudaSuccess) return e;
     e = launch_pdl(fast_td_kernel, std::min(p.B, 4 * d->sms), NT, fast_td_smem(d), st,
                    pdl || d->k2_pdl, p);
@@ -1279,6 +1295,11 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
         return RPL_EINVAL;
     }
     if (rp->size < rp->burn_in || rp->size < 1) return RPL_NOT_READY;   // P:44, nothing advances
+    if (rp->distinct && rp->size < batch) return RPL_NOT_READY;          // reading Q29
+    if (rp->distinct && batch > DS_MAXB) {
+        set_error("dqn_train_step: distinct batch %d > %d", batch, DS_MAXB);
+        return RPL_EINVAL;
+    }
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(d->device);
@@ -1307,7 +1328,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             if (!ge) {
                 cudaGraph_t graph = nullptr;
                 cudaGraphExec_t exec = nullptr;
-                cudaGraphNode_t k1 = nullptr;
+                cudaGraphNode_t k1 = nullptr, ds = nullptr;
                 e = cudaStreamBeginCapture(d->cap_stream, cudaStreamCaptureModeThreadLocal);
                 if (e == cudaSuccess) {
                     cudaError_t e2 = fast_enqueue(d, fp, d->cap_stream);
@@ -1319,14 +1340,15 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                     e = cudaGraphGetNodes(graph, nullptr, &n);
                     std::vector<cudaGraphNode_t> nodes(n);
                     if (e == cudaSuccess && n) e = cudaGraphGetNodes(graph, nodes.data(), &n);
-                    for (size_t i = 0; e == cudaSuccess && i < n && !k1; ++i) {
+                    for (size_t i = 0; e == cudaSuccess && i < n; ++i) {
                         cudaGraphNodeType ty;
                         cudaKernelNodeParams kp = {};
                         if (cudaGraphNodeGetType(nodes[i], &ty) == cudaSuccess &&
                             ty == cudaGraphNodeTypeKernel &&
-                            cudaGraphKernelNodeGetParams(nodes[i], &kp) == cudaSuccess &&
-                            kp.func == (void *)fast_fwd_fn(d))
-                            k1 = nodes[i];
+                            cudaGraphKernelNodeGetParams(nodes[i], &kp) == cudaSuccess) {
+                            if (kp.func == (void *)fast_fwd_fn(d)) k1 = nodes[i];
+                            if (kp.func == (void *)distinct_fast_kernel) ds = nodes[i];
+                        }
                     }
                     if (e == cudaSuccess && !k1) e = cudaErrorInvalidValue;
                 }
@@ -1337,19 +1359,23 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                         cudaGraphDestroy(d->graphs.front().graph);
                         d->graphs.erase(d->graphs.begin());
                     }
-                    d->graphs.push_back({rp, batch, lkey, graph, exec, k1, fp});
+                    d->graphs.push_back({rp, batch, lkey, graph, exec, k1, ds, fp});
                     ge = &d->graphs.back();
                 } else if (graph) {
                     cudaGraphDestroy(graph);
                 }
             } else if (memcmp(&ge->k1args, &fp, sizeof fp) != 0) {
-                // only K1's args change between replays (the deferred insert)
-                cudaKernelNodeParams kp = {};
-                e = cudaGraphKernelNodeGetParams(ge->k1, &kp);
+                // only K1's (and the distinct sampler's) args change between replays: the
+                // deferred insert
                 void *args[] = {&fp};
-                kp.kernelParams = args;
-                kp.extra = nullptr;
-                if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(ge->exec, ge->k1, &kp);
+                for (cudaGraphNode_t nd : {ge->k1, ge->ds}) {
+                    if (!nd || e != cudaSuccess) continue;
+                    cudaKernelNodeParams kp = {};
+                    e = cudaGraphKernelNodeGetParams(nd, &kp);
+                    kp.kernelParams = args;
+                    kp.extra = nullptr;
+                    if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(ge->exec, nd, &kp);
+                }
                 if (e == cudaSuccess) ge->k1args = fp;
             }
             if (e == cudaSuccess) e = cudaGraphLaunch(ge->exec, d->stream);
@@ -1419,6 +1445,12 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             if (e != cudaSuccess) {
                 if (prev >= 0) cudaSetDevice(prev);
                 return cuda_fail(e, "wide_l0_kernel");
+            }
+        }
+        if (p.distinct && !wide) {   // distinct batch indices into d->idx (distinct.cuh)
+            if (int rc = launch_distinct(rp, batch, d->idx, d->err, nullptr, d->stream)) {
+                if (prev >= 0) cudaSetDevice(prev);
+                return rc;
             }
         }
         const int grid = grid_for(d, p);

@@ -91,6 +91,9 @@ struct rpl_replay {
         const uint8_t *done = nullptr;
     } pend;
     bool no_defer = false;   // RPL_NO_DEFER=1: every insert is an immediate kernel
+    bool distinct = false;   // RPL_SAMPLE_DISTINCT (distinct.cuh)
+    int32_t *ds_idx = nullptr;   // scratch indices of distinct replay_sample calls
+    int64_t ds_cap = 0;
 };
 
 namespace rpl {
@@ -98,6 +101,10 @@ namespace rpl {
 int launch_gather(rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t event,
                   int use_sampler, const rpl_batch *out);
 const void *insert_kernel_ptr();
+// distinct batch indices of the replay's current event into out[0..B) (distinct.cuh);
+// ctrl != null also advances the device event counter
+int launch_distinct(const rpl_replay *rp, int B, int32_t *out, uint32_t *err, uint64_t *ctrl,
+                    cudaStream_t st);
 // enqueue the pending deferred insert (if any) as an insert-kernel launch
 int replay_flush(rpl_replay *rp);
 // largest insert that may be deferred into K1 (K1's CTAs write its rows)

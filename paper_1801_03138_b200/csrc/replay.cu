@@ -11,6 +11,7 @@
 #include "internal.h"
 #include "philox.cuh"
 #include "ring_row.cuh"
+#include "distinct.cuh"
 
 namespace rpl {
 
@@ -359,6 +360,34 @@ __global__ void __launch_bounds__(256) gather_u8_kernel(const uint8_t *__restric
     }
 }
 
+// host-driven calls (replay_sample / replay_gather path, the generic train step)
+// (ctrl != null: the replay_sample path consumes the event: ctrl[0] = event + 1)
+__global__ void __launch_bounds__(DS_T, 1) distinct_kernel(uint64_t seed, uint32_t rank, uint64_t event,
+                                                           uint64_t n, int B, int32_t *out, uint32_t *err,
+                                                           uint64_t *ctrl)
+{
+    extern __shared__ int ds_smem[];
+    const int TS = ds_table_slots(B);
+    distinct_sample(seed, rank, event, n, B, out, err, ds_smem, ds_smem + TS);
+    if (ctrl && threadIdx.x == 0) ctrl[0] = event + 1;
+}
+
+// launcher for the other translation units (the generic train step)
+int launch_distinct(const rpl_replay *rp, int B, int32_t *out, uint32_t *err, uint64_t *ctrl,
+                    cudaStream_t st)
+{
+    static bool attr = false;
+    if (!attr) {
+        RPL_CUDA(cudaFuncSetAttribute(distinct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)ds_smem_bytes(DS_MAXB)));
+        attr = true;
+    }
+    distinct_kernel<<<1, DS_T, ds_smem_bytes(B), st>>>(rp->seed, rp->rank, rp->events,
+                                                       (uint64_t)rp->size, B, out, err, ctrl);
+    RPL_LAUNCHED();
+    return RPL_OK;
+}
+
 const void *insert_kernel_ptr() { return (const void *)insert_kernel; }
 
 int replay_flush(rpl_replay *rp)
@@ -392,6 +421,25 @@ int launch_gather(rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t ev
                   int use_sampler, const rpl_batch *out)
 {
     if (int rc = replay_flush(rp)) return rc;
+    if (use_sampler && rp->distinct) {
+        // distinct sampler (distinct.cuh) into the caller's idx (or scratch), then an
+        // explicit-index gather; the sampling kernel consumes the event
+        int32_t *buf = out->idx;
+        if (!buf) {
+            if (rp->ds_cap < n) {
+                if (rp->ds_idx) cudaFree(rp->ds_idx);
+                rp->ds_idx = nullptr;
+                rp->ds_cap = 0;
+                RPL_CUDA(cudaMalloc(&rp->ds_idx, (size_t)n * sizeof(int32_t)));
+                rp->ds_cap = n;
+            }
+            buf = rp->ds_idx;
+        }
+        (void)event;   // == rp->events on this path
+        if (int rc = launch_distinct(rp, (int)n, buf, rp->err_dev, rp->ctrl_dev, rp->stream)) return rc;
+        idx_dev = buf;
+        use_sampler = 0;
+    }
     const int64_t groups = (n + 63) / 64;
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, rp->device);
@@ -467,7 +515,8 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
     if (opts) o = *opts;
     if (capacity < 1 || capacity >= (int64_t(1) << 31) || state_dim < 1 || state_dim > 1 << 20 ||
         o.rank >= (1u << 24) || o.burn_in < 1 || o.max_host_add < 0 ||
-        (o.state_dtype != RPL_F32 && o.state_dtype != RPL_U8)) {
+        (o.state_dtype != RPL_F32 && o.state_dtype != RPL_U8) ||
+        (o.sampling != RPL_SAMPLE_UNIFORM && o.sampling != RPL_SAMPLE_DISTINCT)) {
         set_error("replay_create: invalid argument (capacity=%lld state_dim=%d rank=%u burn_in=%lld)",
                   (long long)capacity, state_dim, o.rank, (long long)o.burn_in);
         return RPL_EINVAL;
@@ -497,6 +546,7 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
     rp->ring.rs = u8 ? ring_u8_row_bytes(state_dim) / 4 : ring_row_stride(state_dim);
     rp->ring.so = u8 ? ring_u8_scalar_offset(state_dim) : 0;
     if (u8) rp->no_defer = true;   // deferral is a fast-path (fp32 states) feature
+    rp->distinct = o.sampling == RPL_SAMPLE_DISTINCT;
     const size_t ring_bytes = (size_t)capacity * rp->ring.rs * sizeof(float);
     cudaError_t e = cudaMalloc(&rp->ring.rows, ring_bytes);
     if (e != cudaSuccess) {
@@ -538,6 +588,7 @@ extern "C" int replay_destroy(rpl_replay *rp)
     }
     if (rp->err_dev) cudaFree(rp->err_dev);
     if (rp->ctrl_dev) cudaFree(rp->ctrl_dev);
+    if (rp->ds_idx) cudaFree(rp->ds_idx);
     if (rp->ring.rows) cudaFree(rp->ring.rows);
     delete rp;
     return RPL_OK;
@@ -622,7 +673,11 @@ extern "C" int replay_sample(rpl_replay *rp, int32_t batch, const rpl_batch *out
         set_error("replay_sample: invalid argument (batch=%d)", batch);
         return RPL_EINVAL;
     }
-    if (rp->size < rp->burn_in) return RPL_NOT_READY;
+    if (rp->distinct && batch > DS_MAXB) {
+        set_error("replay_sample: distinct batch %d > %d", batch, DS_MAXB);
+        return RPL_EINVAL;
+    }
+    if (rp->size < rp->burn_in || (rp->distinct && rp->size < batch)) return RPL_NOT_READY;
     DeviceGuard g(rp->device);
     int rc = launch_gather(rp, batch, nullptr, rp->events, 1, out);
     if (rc != RPL_OK) return rc;

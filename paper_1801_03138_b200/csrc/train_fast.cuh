@@ -22,6 +22,7 @@
 #include "simt_gemm.cuh"
 #include "mma_tf32.cuh"
 #include "ring_row.cuh"
+#include "distinct.cuh"
 
 namespace rpl {
 
@@ -78,6 +79,7 @@ struct FastArgs {
     int64_t *step_dev;
     int32_t *sync_flag;  // written by K2 (step t+1 is a sync step), read by K4 / sgd_kernel
     int apply_update;
+    int distinct;        // 1: the batch indices come from distinct_fast_kernel (in idx)
     uint32_t *err;
     unsigned long long *trace;   // optional per-CTA [kernel][cta][start, end] %globaltimer (ns)
 };
@@ -212,6 +214,17 @@ __device__ __forceinline__ void td_warp(const FastArgs &p, const float *hs, int 
     }
 }
 
+// the distinct sampler of the fast path (graph-replayed: event and filled size read on the
+// device, the deferred insert's size included) -> idx[B], read by K1
+__global__ void __launch_bounds__(DS_T, 1) distinct_fast_kernel(const __grid_constant__ FastArgs p)
+{
+    extern __shared__ int ds_smem[];
+    const uint64_t event = p.rctrl[0];
+    const uint64_t size = p.pend_k ? p.pend_size : p.rctrl[1];
+    distinct_sample(p.seed, p.rank, event, size, p.B, p.idx, p.err, ds_smem,
+                    ds_smem + ds_table_slots(p.B));
+}
+
 // shared-memory layout of K1 (32-bit words); the same formula sizes the launch on the host
 struct FwdLayout {
     int XP, N0P, UT, UTP;
@@ -316,7 +329,12 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
         // (2) Philox sample of the tile's rows (Q3)
         if (tid < F_BT / 2) {
             int32_t i0, i1;
-            sample_pair(p.seed, p.rank, event, (uint32_t)(rb / 2 + tid), size, i0, i1);
+            if (p.distinct) {   // written by distinct_fast_kernel (rows past B: any valid slot)
+                i0 = rb + 2 * tid < B ? p.idx[rb + 2 * tid] : 0;
+                i1 = rb + 2 * tid + 1 < B ? p.idx[rb + 2 * tid + 1] : 0;
+            } else {
+                sample_pair(p.seed, p.rank, event, (uint32_t)(rb / 2 + tid), size, i0, i1);
+            }
             idxs[2 * tid] = i0;
             idxs[2 * tid + 1] = i1;
             int64_t j0 = (int64_t)i0 - p.pend_cur, j1 = (int64_t)i1 - p.pend_cur;

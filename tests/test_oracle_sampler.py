@@ -93,3 +93,46 @@ def test_duplicate_rate_matches_paper():
     p = 1.0 - math.prod(1.0 - i / 1000 for i in range(32))
     se = math.sqrt(p * (1 - p) / n_ev)
     assert abs(d / n_ev - p) < 4 * se
+
+
+# ---- distinct sampling ("I plan on switching back to sampling distinct integers";
+# SURVEY 8(f) NEXT-4; reading Q29: the first B distinct values of the same index stream) ----
+
+def _stream(seed, rank, event, n, length):
+    # the uniform sampler's stream extended past B: position t is index t of a batch of `length`
+    return oracle.sample_indices(seed, rank, event, n, length)
+
+
+@pytest.mark.parametrize("n,B", [(1_000_000, 128), (200, 128), (128, 128), (37, 5), (1000, 999)])
+def test_distinct_is_first_distinct_of_stream(n, B):
+    idx = oracle.sample_distinct(2, 3, 7, n, B)
+    assert len(set(idx.tolist())) == B and idx.min() >= 0 and idx.max() < n
+    # brute force over a long enough prefix of the uniform stream
+    L = 64
+    while True:
+        st = _stream(2, 3, 7, n, L)
+        firsts = list(dict.fromkeys(st.tolist()))
+        if len(firsts) >= B:
+            break
+        L *= 2
+    assert idx.tolist() == firsts[:B]
+
+
+def test_distinct_equals_uniform_without_collisions():
+    # with no repeated index in the uniform batch the two samplers agree exactly
+    for ev in range(20):
+        u = oracle.sample_indices(2, 0, ev, 1_000_000, 64)
+        if len(set(u.tolist())) == 64:
+            assert np.array_equal(oracle.sample_distinct(2, 0, ev, 1_000_000, 64), u)
+
+
+def test_distinct_needs_enough_rows_and_ring_gate():
+    with pytest.raises(ValueError):
+        oracle.sample_distinct(2, 0, 0, 10, 11)
+    r = oracle.Ring(50, 3, distinct=True)
+    from inputs import experiences
+    r.add(**experiences(20, state_dim=3))
+    rc, _ = r.sample(1, 2, 0, 32)          # size 20 < B 32: not ready (Q29), nothing advances
+    assert rc == oracle.NOT_READY and r.events == 0
+    rc, b = r.sample(1, 2, 0, 20)          # B == size: a permutation of the ring
+    assert rc == oracle.OK and sorted(b["idx"].tolist()) == list(range(20))
