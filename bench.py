@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-gather", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--sweep", default="", help="comma list of batch sizes: one JSON line each")
+    ap.add_argument("--distinct", action="store_true",
+                    help="sample distinct indices (RPL_SAMPLE_DISTINCT, P:75's planned switch)")
     ap.add_argument("--config", choices=["c2", "c5"], default="c2",
                     help="c2: BASELINE configs[1] (default); c5: configs[4] 84x84x4 uint8 states, "
                          "batch 256 (other flags' defaults: --batch 256)")
@@ -252,7 +254,8 @@ def run_ours(a, batch, first_line=True):
     peaks, peaks_kind = load_peaks()
 
     cfg = make_cfg(a, binding, batch)
-    rp = binding.Replay(a.capacity, 27, device=local, burn_in=1, seed=2, rank=rank)
+    rp = binding.Replay(a.capacity, 27, device=local, burn_in=1, seed=2, rank=rank,
+                        sampling="distinct" if a.distinct else "uniform")
     # pre-fill the whole ring (startup excluded from timings); per-rank data stream
     rp.add_many(experiences(a.capacity, seed=1, rank=rank))
     dqn = binding.DQN(cfg, init_params(27, 8, cfg.hidden, cfg.dueling, cfg.stream, seed=3),
@@ -448,6 +451,7 @@ def run_ours(a, batch, first_line=True):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(a, batch), "batch": batch, "capacity": a.capacity,
                    "net": a.net, "double_dqn": a.ddqn, "adds_per_step": k,
+                   "sampling": "distinct" if a.distinct else "uniform (with replacement, P:75)",
                    "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2: the 256 MB ring (> 126 MB L2) is sampled uniformly;"
                          " the 0.56 MB weights stay L2-resident as in steady-state training"},

@@ -1386,7 +1386,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             if (prev >= 0) cudaSetDevice(prev);
             return cuda_fail(e, "fast train step");
         }
-        g_launches.fetch_add(4);
+        g_launches.fetch_add(fp.distinct ? 5 : 4);
     } else {
         TrainArgs p;
         fill_args(d, rp, batch, loss_dev, dp ? 0 : 1, do_sync, p);
