@@ -31,8 +31,7 @@ constexpr int F_MAXJ = 33;        // head outputs (1 + 32 actions)
 constexpr int F_JT = (F_MAXJ + 7) / 8;   // 8-wide MMA n-tiles of the head outputs
 constexpr int F_JP = 8 * F_JT;           // head outputs padded to the n-tiles
 constexpr int F_NT1 = 512;        // threads per K1 CTA
-constexpr int F_NT3 = 256;        // threads per K3 CTA (two 128-thread split-K groups)
-constexpr int F_G3 = 128;         // threads per K3 GEMM group
+constexpr int F_NT3 = 256;        // threads per K3 CTA
 
 struct FastArgs {
     // replay (rctrl[0] = sampler events consumed, rctrl[1] = filled size)
@@ -593,173 +592,12 @@ __global__ void __launch_bounds__(NT) fast_td_kernel(const __grid_constant__ Fas
     }
 }
 
-// ------------------------------------------------------------------------------------------
-// K3 GEMM tile: C[32 x 64] = sum_{kk in [kb, ke)} A(m, kk) B(n, kk), 128 threads, 4x4 outputs
-// per thread, operands staged through registers (next chunk in flight while the current one
-// is multiplied).  Operand element (r, kk) is p[kk * ld + r] (kRc: contiguous along r) or
-// p[r * ld + kk]; interior, aligned tiles move as float4, edge tiles element by element.
-// ------------------------------------------------------------------------------------------
+// K3 operand: element (r, kk) is p[kk * ld + r] (source rows are kk) or p[r * ld + kk]
 struct Opnd {
     const float *p;
     int ld, R;
 };
 
-struct __align__(16) Gemm3Smem {
-    float As[BK][BM + 4];
-    float Bs[BK][BN + 4];
-};
-
-template <bool kRc, int TR>
-__device__ __forceinline__ void g3_fetch(const Opnd &o, int r0, int k0, int kb, int ke,
-                                         float4 *reg, int tid)
-{
-    constexpr int NV = TR * BK / 4 / F_G3;   // float4 per thread
-    const bool interior = (r0 + TR <= o.R) && (k0 >= kb) && (k0 + BK <= ke);
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int e = i * F_G3 + tid;
-        if (kRc) {
-            const int kk = e / (TR / 4), r4 = e % (TR / 4);
-            const int r = r0 + 4 * r4, k = k0 + kk;
-            if (interior) {
-                reg[i] = __ldcg(reinterpret_cast<const float4 *>(o.p + (int64_t)k * o.ld + r));
-            } else {
-                float v[4];
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    v[c] = (r + c < o.R && k >= kb && k < ke) ? __ldcg(o.p + (int64_t)k * o.ld + r + c) : 0.0f;
-                reg[i] = make_float4(v[0], v[1], v[2], v[3]);
-            }
-        } else {
-            const int r = e / (BK / 4), k4 = e % (BK / 4);
-            const int rr = r0 + r, k = k0 + 4 * k4;
-            if (interior) {
-                reg[i] = __ldcg(reinterpret_cast<const float4 *>(o.p + (int64_t)rr * o.ld + k));
-            } else {
-                float v[4];
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    v[c] = (rr < o.R && k + c >= kb && k + c < ke) ? __ldcg(o.p + (int64_t)rr * o.ld + k + c) : 0.0f;
-                reg[i] = make_float4(v[0], v[1], v[2], v[3]);
-            }
-        }
-    }
-}
-
-template <bool kRc, int TR, int LDS>
-__device__ __forceinline__ void g3_stash(float (*S)[LDS], const float4 *reg, int tid)
-{
-    constexpr int NV = TR * BK / 4 / F_G3;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int e = i * F_G3 + tid;
-        if (kRc) {
-            const int kk = e / (TR / 4), r4 = e % (TR / 4);
-            *reinterpret_cast<float4 *>(&S[kk][4 * r4]) = reg[i];
-        } else {
-            const int r = e / (BK / 4), k4 = e % (BK / 4);
-            S[4 * k4 + 0][r] = reg[i].x;
-            S[4 * k4 + 1][r] = reg[i].y;
-            S[4 * k4 + 2][r] = reg[i].z;
-            S[4 * k4 + 3][r] = reg[i].w;
-        }
-    }
-}
-
-__device__ __forceinline__ void group_bar(int id)
-{
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(F_G3) : "memory");
-}
-
-// Two 128-thread groups split the contraction chunk-wise (group g takes chunks c = g mod 2),
-// each with its own staging buffers and named barrier; group 1 hands its partial tile to
-// group 0 through shared memory and group 0 runs the epilogue (fixed order: deterministic).
-template <bool kARc, bool kBRc, class EPI, class RSUM>
-__device__ __forceinline__ void gemm3_tile(const Opnd &a, const Opnd &b, int m0, int n0, int kb,
-                                           int ke, const EPI &epi, bool want_rowsum,
-                                           const RSUM &rs, Gemm3Smem *smg)
-{
-    const int grp = threadIdx.x / F_G3, tid = threadIdx.x % F_G3;
-    const int tn = tid & 15, tm = tid >> 4;
-    Gemm3Smem &sm = smg[grp];
-    float acc[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
-    float rsum[4] = {0.f, 0.f, 0.f, 0.f};
-    constexpr int NA = BM * BK / 4 / F_G3, NB = BN * BK / 4 / F_G3;
-    float4 ra[NA], rb[NB];
-    const int nchunks = (ke - kb + BK - 1) / BK;
-    const int mine = (nchunks - grp + 1) / 2;   // chunks grp, grp + 2, ...
-    __syncthreads();                             // the previous task is done with smem
-    if (mine > 0) {
-        g3_fetch<kARc, BM>(a, m0, kb + grp * BK, kb, ke, ra, tid);
-        g3_fetch<kBRc, BN>(b, n0, kb + grp * BK, kb, ke, rb, tid);
-        g3_stash<kARc, BM>(sm.As, ra, tid);
-        g3_stash<kBRc, BN>(sm.Bs, rb, tid);
-        group_bar(1 + grp);
-        for (int c = 0; c < mine; ++c) {
-            const int knext = kb + (grp + 2 * (c + 1)) * BK;
-            if (c + 1 < mine) {
-                g3_fetch<kARc, BM>(a, m0, knext, kb, ke, ra, tid);
-                g3_fetch<kBRc, BN>(b, n0, knext, kb, ke, rb, tid);
-            }
-#pragma unroll 8
-            for (int k = 0; k < BK; ++k) {
-                const float4 av = *reinterpret_cast<const float4 *>(&sm.As[k][4 * tm]);
-                const float4 bv = *reinterpret_cast<const float4 *>(&sm.Bs[k][4 * tn]);
-                const float ar[4] = {av.x, av.y, av.z, av.w};
-                const float br[4] = {bv.x, bv.y, bv.z, bv.w};
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ar[i], br[j], acc[i][j]);
-            }
-            if (want_rowsum && tn == 0) {
-                for (int k = 0; k < BK; ++k) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) rsum[i] += sm.As[k][4 * tm + i];
-                }
-            }
-            group_bar(1 + grp);
-            if (c + 1 < mine) {
-                g3_stash<kARc, BM>(sm.As, ra, tid);
-                g3_stash<kBRc, BN>(sm.Bs, rb, tid);
-                group_bar(1 + grp);
-            }
-        }
-    }
-    // hand group 1's partial tile to group 0
-    float *xch = &smg[1].As[0][0];   // 16 floats x 128 threads + 4 rowsums x 16
-    __syncthreads();
-    if (grp == 1) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) xch[(i * 4 + j) * F_G3 + tid] = acc[i][j];
-        if (want_rowsum && tn == 0) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) xch[16 * F_G3 + i * 8 + tm] = rsum[i];
-        }
-    }
-    __syncthreads();
-    if (grp == 0) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                epi(m0 + 4 * tm + i, n0 + 4 * tn + j, acc[i][j] + xch[(i * 4 + j) * F_G3 + tid]);
-        if (want_rowsum && tn == 0) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) rs(m0 + 4 * tm + i, rsum[i] + xch[16 * F_G3 + i * 8 + tm]);
-        }
-    }
-}
-
-// ------------------------------------------------------------------------------------------
-// K3: dW1 / db1 tiles, dH0 split-K tiles, head-weight gradients
-// ------------------------------------------------------------------------------------------
 // ------------------------------------------------------------------------------------------
 // K3 tensor-core tile: C[32 x K3N] = sum_{kk in [kb, ke)} A(m, kk) B(n, kk) with 3xTF32
 // mma.sync.m16n8k8 (FP32-accurate), 256 threads = 8 warps as 2 (m16) x 4 (n8 per K3N/4).  The
