@@ -72,6 +72,12 @@ typedef struct {
     int32_t sampling;     /* RPL_SAMPLE_UNIFORM (default: uniform with replacement) or
                              RPL_SAMPLE_DISTINCT (P:75's planned switch: the first B distinct
                              values of the same index stream; needs size >= B, B <= 7168)    */
+    int32_t state_sharing; /* 1: store one state per experience: the new state of the
+                             experience in slot i is the old state of slot i+1; rows hold
+                             [s | a | r | terminal] (half the bytes); replay_add ignores
+                             s_next (may be NULL); the sampler draws over the size - 1
+                             experiences whose successor is stored (all but the newest), at
+                             logical position u -> slot (oldest + u) mod capacity            */
 } rpl_replay_opts;
 
 /* Create an empty FIFO replay of `capacity` experiences whose states are `state_dim`

@@ -126,6 +126,21 @@ int oracle_ring_init(oracle_ring *ring, int64_t capacity, int32_t state_dim)
     ring->total = 0;
     ring->events = 0;
     ring->distinct = 0;
+    ring->shared = 0;
+    return ORACLE_OK;
+}
+
+/* Shared-state storage ("the new state of an experience is the old state of the next
+ * experience.  So, by only storing one state per experience, and modifying the sample
+ * operations, ..."; reading Q30): rows [s | a | r | terminal] (D+3
+ * floats), the new state of the experience in slot i is the old state of slot (i+1) mod C,
+ * and the sampler draws over the size-1 experiences whose successor is stored -- every one
+ * but the newest -- at logical position u, slot (oldest + u) mod C.  Only on an empty ring. */
+int oracle_ring_set_shared(oracle_ring *ring)
+{
+    if (ring->size != 0) return ORACLE_EINVAL;
+    ring->shared = 1;
+    ring->row_width = ring->state_dim + 3;
     return ORACLE_OK;
 }
 
@@ -144,13 +159,15 @@ int oracle_ring_add(oracle_ring *ring, int64_t k, const float *s, const int32_t 
     if (k < 0 || k > ring->capacity) return ORACLE_EINVAL;
     for (int64_t j = 0; j < k; ++j)
         if (done[j] > 1) return ORACLE_ECORRUPT;
+    const int32_t sc = ring->shared ? D : 2 * D;   /* first scalar column */
     for (int64_t j = 0; j < k; ++j) {
         float *row = ring->rows + ring->cursor * ring->row_width;
         for (int32_t d = 0; d < D; ++d) row[d] = s[j * D + d];
-        for (int32_t d = 0; d < D; ++d) row[D + d] = s_next[j * D + d];
-        row[2 * D] = (float)a[j];            /* "cast to floats when added" */
-        row[2 * D + 1] = r[j];
-        row[2 * D + 2] = done[j] ? 1.0f : 0.0f;
+        if (!ring->shared)   /* shared: the next experience's s is this one's s' */
+            for (int32_t d = 0; d < D; ++d) row[D + d] = s_next[j * D + d];
+        row[sc] = (float)a[j];               /* "cast to floats when added" */
+        row[sc + 1] = r[j];
+        row[sc + 2] = done[j] ? 1.0f : 0.0f;
         ring->cursor = (ring->cursor + 1) % ring->capacity;
         if (ring->size < ring->capacity) ring->size += 1;
         ring->total += 1;
@@ -165,14 +182,23 @@ int oracle_ring_gather(const oracle_ring *ring, int32_t batch, const int32_t *id
                        int32_t *a, float *r, float *s_next, uint8_t *done)
 {
     const int32_t D = ring->state_dim;
+    const int32_t sc = ring->shared ? D : 2 * D;
     for (int32_t i = 0; i < batch; ++i) {
         if (idx[i] < 0 || idx[i] >= ring->size) return ORACLE_EINVAL;
         const float *row = ring->rows + (int64_t)idx[i] * ring->row_width;
         for (int32_t d = 0; d < D; ++d) s[i * D + d] = row[d];
-        for (int32_t d = 0; d < D; ++d) s_next[i * D + d] = row[D + d];
-        a[i] = (int32_t)row[2 * D];          /* "cast back to their appropriate types" */
-        r[i] = row[2 * D + 1];
-        float t = row[2 * D + 2];
+        if (ring->shared) {
+            /* the experience must have a stored successor: not the newest slot */
+            const int64_t newest = (ring->cursor + ring->capacity - 1) % ring->capacity;
+            if (idx[i] == newest) return ORACLE_EINVAL;
+            const float *nxt = ring->rows + ((int64_t)idx[i] + 1) % ring->capacity * ring->row_width;
+            for (int32_t d = 0; d < D; ++d) s_next[i * D + d] = nxt[d];
+        } else {
+            for (int32_t d = 0; d < D; ++d) s_next[i * D + d] = row[D + d];
+        }
+        a[i] = (int32_t)row[sc];             /* "cast back to their appropriate types" */
+        r[i] = row[sc + 1];
+        float t = row[sc + 2];
         if (t != 0.0f && t != 1.0f) return ORACLE_ECORRUPT;
         done[i] = (uint8_t)(t == 1.0f);
     }
@@ -186,11 +212,18 @@ int oracle_ring_sample(oracle_ring *ring, int64_t burn_in, uint64_t seed, uint32
                        float *s_next, uint8_t *done)
 {
     if (ring->size < burn_in || ring->size < 1) return ORACLE_NOT_READY;
+    /* shared states: the newest experience has no stored successor yet (reading Q30) */
+    const int64_t n = ring->shared ? ring->size - 1 : ring->size;
+    if (n < 1) return ORACLE_NOT_READY;
     if (ring->distinct) {
-        if (ring->size < batch) return ORACLE_NOT_READY;   /* reading Q29 */
-        oracle_sample_distinct(seed, rank, ring->events, ring->size, batch, idx);
+        if (n < batch) return ORACLE_NOT_READY;   /* reading Q29 */
+        oracle_sample_distinct(seed, rank, ring->events, n, batch, idx);
     } else {
-        oracle_sample_indices(seed, rank, ring->events, ring->size, batch, idx);
+        oracle_sample_indices(seed, rank, ring->events, n, batch, idx);
+    }
+    if (ring->shared) {   /* logical position u -> slot (oldest + u) mod C */
+        const int64_t oldest = ring->size < ring->capacity ? 0 : ring->cursor;
+        for (int32_t i = 0; i < batch; ++i) idx[i] = (int32_t)((oldest + idx[i]) % ring->capacity);
     }
     ring->events += 1;
     return oracle_ring_gather(ring, batch, idx, s, a, r, s_next, done);
@@ -216,6 +249,7 @@ int oracle_ring_u8_init(oracle_ring_u8 *ring, int64_t capacity, int32_t state_di
     ring->total = 0;
     ring->events = 0;
     ring->distinct = 0;
+    ring->shared = 0;
     if (!ring->s || !ring->s_next || !ring->a || !ring->r || !ring->done) {
         oracle_ring_u8_free(ring);
         return ORACLE_ENOMEM;
@@ -241,7 +275,7 @@ int oracle_ring_u8_add(oracle_ring_u8 *ring, int64_t k, const uint8_t *s, const 
     for (int64_t j = 0; j < k; ++j) {
         const int64_t c = ring->cursor;
         memcpy(ring->s + c * D, s + j * D, (size_t)D);
-        memcpy(ring->s_next + c * D, s_next + j * D, (size_t)D);
+        if (!ring->shared) memcpy(ring->s_next + c * D, s_next + j * D, (size_t)D);
         ring->a[c] = a[j];
         ring->r[c] = r[j];
         ring->done[c] = done[j];
@@ -260,7 +294,12 @@ int oracle_ring_u8_gather(const oracle_ring_u8 *ring, int32_t batch, const int32
         if (idx[i] < 0 || idx[i] >= ring->size) return ORACLE_EINVAL;
         const int64_t c = idx[i];
         memcpy(s + (int64_t)i * D, ring->s + c * D, (size_t)D);
-        memcpy(s_next + (int64_t)i * D, ring->s_next + c * D, (size_t)D);
+        if (ring->shared) {   /* the next experience's old state (reading Q30) */
+            if (c == (ring->cursor + ring->capacity - 1) % ring->capacity) return ORACLE_EINVAL;
+            memcpy(s_next + (int64_t)i * D, ring->s + (c + 1) % ring->capacity * D, (size_t)D);
+        } else {
+            memcpy(s_next + (int64_t)i * D, ring->s_next + c * D, (size_t)D);
+        }
         a[i] = ring->a[c];
         r[i] = ring->r[c];
         done[i] = ring->done[c];
@@ -273,11 +312,17 @@ int oracle_ring_u8_sample(oracle_ring_u8 *ring, int64_t burn_in, uint64_t seed, 
                           uint8_t *s_next, uint8_t *done)
 {
     if (ring->size < burn_in || ring->size < 1) return ORACLE_NOT_READY;
+    const int64_t n = ring->shared ? ring->size - 1 : ring->size;   /* reading Q30 */
+    if (n < 1) return ORACLE_NOT_READY;
     if (ring->distinct) {
-        if (ring->size < batch) return ORACLE_NOT_READY;   /* reading Q29 */
-        oracle_sample_distinct(seed, rank, ring->events, ring->size, batch, idx);
+        if (n < batch) return ORACLE_NOT_READY;   /* reading Q29 */
+        oracle_sample_distinct(seed, rank, ring->events, n, batch, idx);
     } else {
-        oracle_sample_indices(seed, rank, ring->events, ring->size, batch, idx);
+        oracle_sample_indices(seed, rank, ring->events, n, batch, idx);
+    }
+    if (ring->shared) {
+        const int64_t oldest = ring->size < ring->capacity ? 0 : ring->cursor;
+        for (int32_t i = 0; i < batch; ++i) idx[i] = (int32_t)((oldest + idx[i]) % ring->capacity);
     }
     ring->events += 1;
     return oracle_ring_u8_gather(ring, batch, idx, s, a, r, s_next, done);

@@ -33,9 +33,11 @@ typedef struct {
     uint64_t total;      /* experiences ever added */
     uint64_t events;     /* sampler events consumed */
     int32_t distinct;    /* 1: sample distinct indices (oracle_sample_distinct) */
+    int32_t shared;      /* 1: shared-state rows [s | a | r | t] (oracle_ring_set_shared) */
 } oracle_ring;
 
 int oracle_ring_init(oracle_ring *ring, int64_t capacity, int32_t state_dim);
+int oracle_ring_set_shared(oracle_ring *ring);
 void oracle_ring_free(oracle_ring *ring);
 int oracle_ring_add(oracle_ring *ring, int64_t k, const float *s, const int32_t *a,
                     const float *r, const float *s_next, const uint8_t *done);
@@ -56,6 +58,7 @@ typedef struct {
     int64_t cursor, size;
     uint64_t total, events;
     int32_t distinct;    /* 1: sample distinct indices (oracle_sample_distinct) */
+    int32_t shared;      /* 1: s' = s of the next slot (set on an empty ring) */
 } oracle_ring_u8;
 
 int oracle_ring_u8_init(oracle_ring_u8 *ring, int64_t capacity, int32_t state_dim);

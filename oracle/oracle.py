@@ -54,6 +54,7 @@ class _Ring(C.Structure):
         ("total", C.c_uint64),
         ("events", C.c_uint64),
         ("distinct", C.c_int32),
+        ("shared", C.c_int32),
     ]
 
 
@@ -71,6 +72,7 @@ class _RingU8(C.Structure):
         ("total", C.c_uint64),
         ("events", C.c_uint64),
         ("distinct", C.c_int32),
+        ("shared", C.c_int32),
     ]
 
 
@@ -113,6 +115,8 @@ def _declare(L):
     L.oracle_ring_init.argtypes = [C.POINTER(_Ring), C.c_int64, C.c_int32]
     L.oracle_ring_init.restype = C.c_int
     L.oracle_ring_free.argtypes = [C.POINTER(_Ring)]
+    L.oracle_ring_set_shared.argtypes = [C.POINTER(_Ring)]
+    L.oracle_ring_set_shared.restype = C.c_int
     L.oracle_ring_add.argtypes = [C.POINTER(_Ring), C.c_int64, _P, _P, _P, _P, _P]
     L.oracle_ring_add.restype = C.c_int
     L.oracle_ring_gather.argtypes = [C.POINTER(_Ring), C.c_int32, _P, _P, _P, _P, _P, _P]
@@ -187,12 +191,15 @@ def sample_distinct(seed: int, rank: int, event: int, n: int, batch: int) -> np.
 # The replay ring (paper layout: packed 2D+3 floats per row)
 # ------------------------------------------------------------------------------------
 class Ring:
-    def __init__(self, capacity: int, state_dim: int, distinct: bool = False):
+    def __init__(self, capacity: int, state_dim: int, distinct: bool = False,
+                 shared: bool = False):
         self._r = _Ring()
         rc = lib().oracle_ring_init(C.byref(self._r), capacity, state_dim)
         if rc != OK:
             raise ValueError(f"oracle_ring_init rc={rc}")
         self._r.distinct = 1 if distinct else 0
+        if shared:
+            lib().oracle_ring_set_shared(C.byref(self._r))
         self.state_dim = state_dim
 
     def __del__(self):
@@ -235,7 +242,7 @@ class Ring:
         k = s.shape[0]
         a = _c(a, np.int32)
         r = _c(r, np.float32)
-        s_next = _c(s_next, np.float32).reshape(-1, D)
+        s_next = _c(s_next, np.float32).reshape(-1, D) if s_next is not None else None
         done = _c(done, np.uint8)
         return lib().oracle_ring_add(C.byref(self._r), k, _ptr(s), _ptr(a), _ptr(r),
                                      _ptr(s_next), _ptr(done))
@@ -278,12 +285,14 @@ class RingU8:
     """Byte-state replay (SURVEY config 5): oracle_ring_u8_* (same FIFO / sampler / gather
     as Ring over uint8 states)."""
 
-    def __init__(self, capacity: int, state_dim: int, distinct: bool = False):
+    def __init__(self, capacity: int, state_dim: int, distinct: bool = False,
+                 shared: bool = False):
         self._r = _RingU8()
         rc = lib().oracle_ring_u8_init(C.byref(self._r), capacity, state_dim)
         if rc != OK:
             raise ValueError(f"oracle_ring_u8_init rc={rc}")
         self._r.distinct = 1 if distinct else 0
+        self._r.shared = 1 if shared else 0
         self.state_dim = state_dim
 
     def __del__(self):
@@ -308,7 +317,7 @@ class RingU8:
         s = _c(s, np.uint8).reshape(-1, D)
         return lib().oracle_ring_u8_add(C.byref(self._r), s.shape[0], _ptr(s), _ptr(_c(a, np.int32)),
                                         _ptr(_c(r, np.float32)),
-                                        _ptr(_c(s_next, np.uint8).reshape(-1, D)),
+                                        _ptr(_c(s_next, np.uint8).reshape(-1, D)) if s_next is not None else None,
                                         _ptr(_c(done, np.uint8)))
 
     def _batch(self, B):

@@ -48,7 +48,7 @@ class RplError(RuntimeError):
 class _ReplayOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("cuda_stream", C.c_void_p), ("burn_in", C.c_int64),
                 ("seed", C.c_uint64), ("rank", C.c_uint32), ("max_host_add", C.c_int64),
-                ("state_dtype", C.c_int32), ("sampling", C.c_int32)]
+                ("state_dtype", C.c_int32), ("sampling", C.c_int32), ("state_sharing", C.c_int32)]
 
 
 class _Batch(C.Structure):
@@ -146,7 +146,7 @@ class Replay:
 
     def __init__(self, capacity: int, state_dim: int, *, device: int = 0, stream=None,
                  burn_in: int = 1, seed: int = 2, rank: int = 0, max_host_add: int = 0,
-                 state_dtype: str = "f32", sampling: str = "uniform"):
+                 state_dtype: str = "f32", sampling: str = "uniform", shared_state: bool = False):
         torch = _torch()
         if not torch.cuda.is_available():
             raise RplError(RPL_ECUDA, "no CUDA device (the in-GPU replay has no CPU fallback)")
@@ -157,7 +157,9 @@ class Replay:
         with torch.cuda.device(device):
             self._stream = _stream_handle(stream)
         o = _ReplayOpts(device, self._stream, burn_in, seed, rank, max_host_add,
-                        RPL_U8 if self.u8 else RPL_F32, 1 if sampling == "distinct" else 0)
+                        RPL_U8 if self.u8 else RPL_F32, 1 if sampling == "distinct" else 0,
+                        1 if shared_state else 0)
+        self.shared_state = shared_state
         h = C.c_void_p()
         _ok(_L.replay_create(capacity, state_dim, C.byref(o), C.byref(h)))
         self._h = h
@@ -180,24 +182,29 @@ class Replay:
         call on this replay / the next train step on it; a reference is held until then)."""
         torch = _torch()
         if isinstance(s, torch.Tensor) and s.is_cuda:
+            if s_next is None:   # shared-state replay: s' is the next experience's s
+                s_next = s[:0]
             ts = [s.contiguous(), a.contiguous(), r.contiguous(), s_next.contiguous(),
                   done.contiguous()]
             assert ts[0].dtype == self.state_torch and ts[3].dtype == self.state_torch
             assert ts[1].dtype == torch.int32
             assert ts[2].dtype == torch.float32 and ts[4].dtype == torch.uint8
             k = ts[1].numel()
-            rc = _ok(_L.replay_add(self._h, k, *[_dptr(t) for t in ts],
+            ptrs = [_dptr(t) for t in ts]
+            if ts[3].numel() == 0:
+                ptrs[3] = None
+            rc = _ok(_L.replay_add(self._h, k, *ptrs,
                                    RPL_DEVICE_DEFER if defer else RPL_DEVICE))
             self._deferred = ts if defer else None
             return rc
         arrs = [np.ascontiguousarray(np.asarray(s), self.state_np),
                 np.ascontiguousarray(np.asarray(a), np.int32),
                 np.ascontiguousarray(np.asarray(r), np.float32),
-                np.ascontiguousarray(np.asarray(s_next), self.state_np),
+                None if s_next is None else np.ascontiguousarray(np.asarray(s_next), self.state_np),
                 np.ascontiguousarray(np.asarray(done), np.uint8)]
         k = arrs[1].size
-        return _ok(_L.replay_add(self._h, k, *[x.ctypes.data_as(C.c_void_p) for x in arrs],
-                                 RPL_HOST))
+        return _ok(_L.replay_add(self._h, k, *[None if x is None else x.ctypes.data_as(C.c_void_p)
+                                              for x in arrs], RPL_HOST))
 
     def add_many(self, e: dict, chunk: int = 65536):
         n = len(e["a"])

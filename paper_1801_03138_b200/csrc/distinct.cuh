@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include "philox.cuh"
+#include "ring_row.cuh"
 
 namespace rpl {
 
@@ -29,8 +30,11 @@ __host__ __device__ inline int ds_table_slots(int B)
 }
 __host__ inline size_t ds_smem_bytes(int B) { return (size_t)ds_table_slots(B) * 8; }
 
+// out[i] = slot_of(i-th distinct logical position, oldest, capacity) (identity for a plain
+// ring: oldest = 0)
 __device__ inline void distinct_sample(uint64_t seed, uint32_t rank, uint64_t event, uint64_t n,
-                                       int B, int32_t *out, uint32_t *err, int *keys, int *pos)
+                                       int B, int32_t *out, uint32_t *err, int *keys, int *pos,
+                                       uint64_t oldest, int64_t capacity)
 {
     __shared__ int wsum[DS_T / 32];
     __shared__ int s_total;
@@ -81,7 +85,7 @@ __device__ inline void distinct_sample(uint64_t seed, uint32_t rank, uint64_t ev
         }
         __syncthreads();
         const int excl = (warp ? wsum[warp - 1] : 0) + excl_w;
-        if (first && count + excl < B) out[count + excl] = v;
+        if (first && count + excl < B) out[count + excl] = slot_of(v, oldest, capacity);
         count += s_total;
         __syncthreads();   // wsum / s_total reuse
     }

@@ -44,6 +44,8 @@ struct TrainArgs {
     const float *ring;
     int rs, D;
     int u8, so;            // byte states (x = u8 / 255, reading Q27); scalars at byte `so`
+    int shared, sw;        // shared states (s' = next slot's s); fp32 scalar word offset
+    int64_t cursor, capacity;
     int64_t size;
     uint64_t seed, event;
     uint32_t rank;
@@ -89,6 +91,7 @@ struct TrainArgs {
 
 struct __align__(16) TileSmem : GemmSmem {
     int idx[BM];
+    int idx2[BM];          // the s' row of each sampled slot (== idx unless shared states)
     float red[NT / 32];
     float head[NT / 32][MAXJ + 3];
 };
@@ -231,14 +234,24 @@ __device__ void phase_forward(const TrainArgs &p, int l, TileSmem &sm)
                     i0 = 2 * pair < B ? p.idx[2 * pair] : 0;
                     i1 = 2 * pair + 1 < B ? p.idx[2 * pair + 1] : 0;
                 } else {
-                    sample_pair(p.seed, p.rank, p.event, (uint32_t)pair, (uint64_t)p.size, i0, i1);
+                    // shared states: logical positions over all but the newest experience
+                    const int64_t nvalid = p.shared ? p.size - 1 : p.size;
+                    const uint64_t oldest = (p.shared && p.size == p.capacity) ? (uint64_t)p.cursor : 0;
+                    sample_pair(p.seed, p.rank, p.event, (uint32_t)pair, (uint64_t)nvalid, i0, i1);
+                    i0 = slot_of(i0, oldest, p.capacity);
+                    i1 = slot_of(i1, oldest, p.capacity);
                 }
                 sm.idx[2 * threadIdx.x] = i0;
                 sm.idx[2 * threadIdx.x + 1] = i1;
+                sm.idx2[2 * threadIdx.x] = p.shared ? (int)((i0 + 1) % p.capacity) : i0;
+                sm.idx2[2 * threadIdx.x + 1] = p.shared ? (int)((i1 + 1) % p.capacity) : i1;
             }
             __syncthreads();
             const int D = p.D;
-            const int col0 = (net == 0) ? 0 : D;   // s for online(s), s' for the others
+            // s for online(s), s' for the others: the same row's second state, or the next
+            // slot's state with shared states
+            const int col0 = (net == 0 || p.shared) ? 0 : D;
+            const int *rows_s = (net == 0) ? sm.idx : sm.idx2;
             // unpack the batch once (online(s) / target(s') tasks of the first column tile)
             if (n0 == 0 && net <= 1 && kq == 0) {
                 if (p.u8) {
@@ -247,14 +260,14 @@ __device__ void phase_forward(const TrainArgs &p, int l, TileSmem &sm)
                     for (int e = threadIdx.x; e < BM * D; e += NT) {
                         const int r = e / D, c = e % D;
                         if (m0 + r < B)
-                            xo[(int64_t)(m0 + r) * D + c] = __ldg(rb + (int64_t)sm.idx[r] * p.rs * 4 + col0 + c);
+                            xo[(int64_t)(m0 + r) * D + c] = __ldg(rb + (int64_t)rows_s[r] * p.rs * 4 + col0 + c);
                     }
                 } else {
                     for (int e = threadIdx.x; e < BM * D; e += NT) {
                         const int r = e / D, c = e % D;
                         if (m0 + r < B)
                             (net == 0 ? p.Xs : p.Xs2)[(int64_t)(m0 + r) * D + c] =
-                                __ldg(p.ring + (int64_t)sm.idx[r] * p.rs + col0 + c);
+                                __ldg(p.ring + (int64_t)rows_s[r] * p.rs + col0 + c);
                     }
                 }
                 if (net == 0 && threadIdx.x < BM && m0 + threadIdx.x < B) {
@@ -262,7 +275,7 @@ __device__ void phase_forward(const TrainArgs &p, int l, TileSmem &sm)
                     const float *row = p.u8 ? reinterpret_cast<const float *>(
                                                   reinterpret_cast<const uint8_t *>(p.ring) +
                                                   (int64_t)sm.idx[r] * p.rs * 4 + p.so)
-                                            : p.ring + (int64_t)sm.idx[r] * p.rs + 2 * D;
+                                            : p.ring + (int64_t)sm.idx[r] * p.rs + p.sw;
                     p.idx[b] = sm.idx[r];
                     p.a[b] = __float_as_int(__ldg(row));
                     p.r[b] = __ldg(row + 1);
@@ -270,11 +283,11 @@ __device__ void phase_forward(const TrainArgs &p, int l, TileSmem &sm)
                 }
             }
             if (p.u8) {
-                LdRingU8 lx{reinterpret_cast<const uint8_t *>(p.ring), sm.idx, m0, (int64_t)p.rs * 4,
+                LdRingU8 lx{reinterpret_cast<const uint8_t *>(p.ring), rows_s, m0, (int64_t)p.rs * 4,
                             col0, B, ke};
                 gemm_tile(lx, lw, m0, n0, kb, ke, epi, false, NoRowsum{}, sm);
             } else {
-                LdRing lx{p.ring, sm.idx, m0, p.rs, col0, B, ke};
+                LdRing lx{p.ring, rows_s, m0, p.rs, col0, B, ke};
                 gemm_tile(lx, lw, m0, n0, kb, ke, epi, false, NoRowsum{}, sm);
             }
         } else {
@@ -1070,6 +1083,10 @@ static void fill_args(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.D = rp->ring.D;
     p.u8 = rp->ring.u8;
     p.so = rp->ring.so;
+    p.shared = rp->ring.shared;
+    p.sw = rp->ring.sw;
+    p.cursor = rp->cursor;
+    p.capacity = rp->ring.capacity;
     p.size = rp->size;
     p.seed = rp->seed;
     p.event = rp->events;
@@ -1142,6 +1159,8 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.ring = rp->ring.rows;
     p.rs = rp->ring.rs;
     p.D = rp->ring.D;
+    p.shared = rp->ring.shared;
+    p.sw = rp->ring.sw;
     p.rctrl = rp->ctrl_dev;
     p.seed = rp->seed;
     p.rank = rp->rank;
@@ -1295,7 +1314,8 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
         return RPL_EINVAL;
     }
     if (rp->size < rp->burn_in || rp->size < 1) return RPL_NOT_READY;   // P:44, nothing advances
-    if (rp->distinct && rp->size < batch) return RPL_NOT_READY;          // reading Q29
+    if (sampleable(rp) < 1) return RPL_NOT_READY;                        // reading Q30
+    if (rp->distinct && sampleable(rp) < batch) return RPL_NOT_READY;    // reading Q29
     if (rp->distinct && batch > DS_MAXB) {
         set_error("dqn_train_step: distinct batch %d > %d", batch, DS_MAXB);
         return RPL_EINVAL;

@@ -51,11 +51,22 @@ struct Ring {
     int32_t rs = 0;            // row stride in 4-byte words
     int32_t u8 = 0;            // states stored as bytes
     int32_t so = 0;            // u8 rings: byte offset of the scalars (a, r, done)
+    int32_t shared = 0;        // shared states: s' of slot i = s of slot i + 1
+    int32_t sw = 0;            // fp32 rings: word offset of the scalars (2D, or D if shared)
 };
 
-inline int32_t ring_row_stride(int32_t D) { return ((2 * D + 3) + 31) / 32 * 32; }
-inline int32_t ring_u8_scalar_offset(int32_t D) { return (2 * D + 15) / 16 * 16; }
-inline int32_t ring_u8_row_bytes(int32_t D) { return (ring_u8_scalar_offset(D) + 12 + 127) / 128 * 128; }
+inline int32_t ring_row_stride(int32_t D, bool shared = false)
+{
+    return (((shared ? 1 : 2) * D + 3) + 31) / 32 * 32;
+}
+inline int32_t ring_u8_scalar_offset(int32_t D, bool shared = false)
+{
+    return ((shared ? 1 : 2) * D + 15) / 16 * 16;
+}
+inline int32_t ring_u8_row_bytes(int32_t D, bool shared = false)
+{
+    return (ring_u8_scalar_offset(D, shared) + 12 + 127) / 128 * 128;
+}
 
 }  // namespace rpl
 
@@ -77,7 +88,7 @@ struct rpl_replay {
     int stage_slot = 0;
     uint32_t *err_dev = nullptr;   // sticky device error word
     // device control block read by graph-replayed train steps: [0] sampler events consumed,
-    // [1] filled size (kept equal to the host mirror by the kernels that change them)
+    // [1] filled size, [2] cursor (kept equal to the host mirror by the kernels that change them)
     uint64_t *ctrl_dev = nullptr;
     // At most one small insert whose ring write is deferred into the next fast train step's
     // K1 (which reads sampled pending slots straight from these sources: "read-through").
@@ -105,6 +116,10 @@ const void *insert_kernel_ptr();
 // ctrl != null also advances the device event counter
 int launch_distinct(const rpl_replay *rp, int B, int32_t *out, uint32_t *err, uint64_t *ctrl,
                     cudaStream_t st);
+// experiences the sampler draws from (shared states: all but the newest, reading Q30) and the
+// slot of logical position 0 (shared states: the oldest experience; else 0, slot == u)
+int64_t sampleable(const rpl_replay *rp);
+uint64_t oldest_slot(const rpl_replay *rp);
 // enqueue the pending deferred insert (if any) as an insert-kernel launch
 int replay_flush(rpl_replay *rp);
 // largest insert that may be deferred into K1 (K1's CTAs write its rows)

@@ -53,7 +53,7 @@ struct DeviceGuard {
 // K1: insert.  One warp per experience; the warp writes the whole 128B-aligned row (one or
 // more fully coalesced 128-byte stores per 32 floats).  Slot = (cursor + j) mod capacity.
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) insert_kernel(float *__restrict__ rows, int rs, int D,
+__global__ void __launch_bounds__(256) insert_kernel(float *__restrict__ rows, int rs, int D, int sw,
                                                      int64_t capacity, int64_t cursor, int64_t k,
                                                      const float *__restrict__ s,
                                                      const int32_t *__restrict__ a,
@@ -63,13 +63,61 @@ __global__ void __launch_bounds__(256) insert_kernel(float *__restrict__ rows, i
                                                      uint32_t *err, uint64_t *ctrl, int64_t new_size)
 {
     const int lane = threadIdx.x & 31;
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctrl[1] = (uint64_t)new_size;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctrl[1] = (uint64_t)new_size;
+        ctrl[2] = (uint64_t)((cursor + k) % capacity);
+    }
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k;
          j += nwarps) {
         int64_t slot = cursor + j;
         if (slot >= capacity) slot -= capacity;   // k <= capacity, cursor < capacity
-        ring_write_row(rows + slot * rs, rs, D, lane, j, s, a, r, s2, done, err);
+        ring_write_row(rows + slot * rs, rs, D, sw, lane, j, s, a, r, s2, done, err);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Shared-state rows (reading Q30): sample over the experiences with a stored successor
+// (logical position u -> slot (oldest + u) mod C), the new state from the next slot's row.
+// One warp per entry.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) gather_shared_kernel(const float *__restrict__ rows, int rs, int D,
+                                                            int sw, int64_t capacity, int64_t nvalid,
+                                                            uint64_t oldest, int64_t size, int64_t n,
+                                                            const int32_t *__restrict__ idx_in,
+                                                            uint64_t seed, uint32_t rank, uint64_t event,
+                                                            float *s, float *s2, int32_t *a, float *r,
+                                                            uint8_t *done, int32_t *idx_out, uint32_t *err,
+                                                            uint64_t *ctrl)
+{
+    if (idx_in == nullptr && ctrl && blockIdx.x == 0 && threadIdx.x == 0) ctrl[0] = event + 1;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < n; e += nwarps) {
+        int32_t ix;
+        if (idx_in == nullptr) {
+            int32_t i0, i1;
+            sample_pair(seed, rank, event, (uint32_t)(e >> 1), (uint64_t)nvalid, i0, i1);
+            ix = slot_of((e & 1) ? i1 : i0, oldest, capacity);
+        } else {
+            ix = idx_in[e];
+            if (ix < 0 || ix >= size) {
+                if (lane == 0) atomicOr(err, ERRBIT_RANGE);
+                ix = min(max(ix, 0), (int32_t)size - 1);
+            }
+        }
+        const int64_t nx = (ix + 1) % capacity;
+        const float *row = rows + (int64_t)ix * rs, *nrow = rows + nx * rs;
+        for (int c = lane; c < D; c += 32) {
+            if (s) s[e * D + c] = __ldg(row + c);
+            if (s2) s2[e * D + c] = __ldg(nrow + c);
+        }
+        if (lane == 0) {
+            if (idx_out) idx_out[e] = ix;
+            if (a) a[e] = __float_as_int(__ldg(row + sw));
+            if (r) r[e] = __ldg(row + sw + 1);
+            if (done) done[e] = (uint8_t)(__float_as_uint(__ldg(row + sw + 2)) != 0u);
+        }
     }
 }
 
@@ -290,7 +338,7 @@ __device__ __forceinline__ void copy_bytes_cta(uint8_t *__restrict__ dst, const 
 }
 
 __global__ void __launch_bounds__(256) insert_u8_kernel(uint8_t *__restrict__ rows, int64_t rsb, int so,
-                                                        int D, int64_t capacity, int64_t cursor,
+                                                        int D, int shared, int64_t capacity, int64_t cursor,
                                                         int64_t k, const uint8_t *__restrict__ s,
                                                         const int32_t *__restrict__ a,
                                                         const float *__restrict__ r,
@@ -298,14 +346,17 @@ __global__ void __launch_bounds__(256) insert_u8_kernel(uint8_t *__restrict__ ro
                                                         const uint8_t *__restrict__ done, uint32_t *err,
                                                         uint64_t *ctrl, int64_t new_size)
 {
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctrl[1] = (uint64_t)new_size;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctrl[1] = (uint64_t)new_size;
+        ctrl[2] = (uint64_t)((cursor + k) % capacity);
+    }
     for (int64_t j = blockIdx.x; j < k; j += gridDim.x) {
         int64_t slot = cursor + j;
         if (slot >= capacity) slot -= capacity;   // k <= capacity, cursor < capacity
         uint8_t *row = rows + slot * rsb;
         copy_bytes_cta(row, s + j * D, D);
-        copy_bytes_cta(row + D, s2 + j * D, D);
-        for (int b = 2 * D + threadIdx.x; b < so; b += blockDim.x) row[b] = 0;
+        if (!shared) copy_bytes_cta(row + D, s2 + j * D, D);   // shared: s' is the next row's s
+        for (int b = (shared ? 1 : 2) * D + threadIdx.x; b < so; b += blockDim.x) row[b] = 0;
         if (threadIdx.x == 0) {
             uint32_t d = done[j];
             if (d > 1u) {   // a device-sourced done > 1 is stored as 1 and flagged
@@ -322,7 +373,8 @@ __global__ void __launch_bounds__(256) insert_u8_kernel(uint8_t *__restrict__ ro
 
 // Philox sample (or caller indices) + gather + unpack of byte-state rows: one CTA per entry
 __global__ void __launch_bounds__(256) gather_u8_kernel(const uint8_t *__restrict__ rows, int64_t rsb,
-                                                        int so, int D, int64_t size, int64_t n,
+                                                        int so, int D, int shared, int64_t capacity,
+                                                        uint64_t oldest, int64_t nvalid, int64_t size, int64_t n,
                                                         const int32_t *__restrict__ idx_in,
                                                         uint64_t seed, uint32_t rank, uint64_t event,
                                                         uint8_t *s, uint8_t *s2, int32_t *a, float *r,
@@ -336,8 +388,8 @@ __global__ void __launch_bounds__(256) gather_u8_kernel(const uint8_t *__restric
             int32_t ix;
             if (idx_in == nullptr) {
                 int32_t i0, i1;
-                sample_pair(seed, rank, event, (uint32_t)(e >> 1), (uint64_t)size, i0, i1);
-                ix = (e & 1) ? i1 : i0;
+                sample_pair(seed, rank, event, (uint32_t)(e >> 1), (uint64_t)nvalid, i0, i1);
+                ix = slot_of((e & 1) ? i1 : i0, oldest, capacity);
             } else {
                 ix = idx_in[e];
                 if (ix < 0 || ix >= size) {
@@ -355,7 +407,7 @@ __global__ void __launch_bounds__(256) gather_u8_kernel(const uint8_t *__restric
         __syncthreads();
         const uint8_t *row = rows + (int64_t)ix_s * rsb;
         if (s) copy_bytes_cta(s + e * D, row, D);
-        if (s2) copy_bytes_cta(s2 + e * D, row + D, D);
+        if (s2) copy_bytes_cta(s2 + e * D, shared ? rows + (int64_t)((ix_s + 1) % capacity) * rsb : row + D, D);
         __syncthreads();   // ix_s reuse
     }
 }
@@ -364,11 +416,11 @@ __global__ void __launch_bounds__(256) gather_u8_kernel(const uint8_t *__restric
 // (ctrl != null: the replay_sample path consumes the event: ctrl[0] = event + 1)
 __global__ void __launch_bounds__(DS_T, 1) distinct_kernel(uint64_t seed, uint32_t rank, uint64_t event,
                                                            uint64_t n, int B, int32_t *out, uint32_t *err,
-                                                           uint64_t *ctrl)
+                                                           uint64_t *ctrl, uint64_t oldest, int64_t capacity)
 {
     extern __shared__ int ds_smem[];
     const int TS = ds_table_slots(B);
-    distinct_sample(seed, rank, event, n, B, out, err, ds_smem, ds_smem + TS);
+    distinct_sample(seed, rank, event, n, B, out, err, ds_smem, ds_smem + TS, oldest, capacity);
     if (ctrl && threadIdx.x == 0) ctrl[0] = event + 1;
 }
 
@@ -383,12 +435,22 @@ int launch_distinct(const rpl_replay *rp, int B, int32_t *out, uint32_t *err, ui
         attr = true;
     }
     distinct_kernel<<<1, DS_T, ds_smem_bytes(B), st>>>(rp->seed, rp->rank, rp->events,
-                                                       (uint64_t)rp->size, B, out, err, ctrl);
+                                                       (uint64_t)sampleable(rp), B, out, err, ctrl,
+                                                       oldest_slot(rp), rp->ring.capacity);
     RPL_LAUNCHED();
     return RPL_OK;
 }
 
 const void *insert_kernel_ptr() { return (const void *)insert_kernel; }
+
+int64_t sampleable(const rpl_replay *rp)
+{
+    return rp->ring.shared ? (rp->size > 0 ? rp->size - 1 : 0) : rp->size;
+}
+uint64_t oldest_slot(const rpl_replay *rp)
+{
+    return (rp->ring.shared && rp->size == rp->ring.capacity) ? (uint64_t)rp->cursor : 0;
+}
 
 int replay_flush(rpl_replay *rp)
 {
@@ -405,11 +467,11 @@ int replay_flush(rpl_replay *rp)
         const int64_t ublocks = k < (int64_t)dev_sms * 16 ? k : (int64_t)dev_sms * 16;
         insert_u8_kernel<<<(unsigned)ublocks, 256, 0, rp->stream>>>(
             reinterpret_cast<uint8_t *>(rp->ring.rows), (int64_t)rp->ring.rs * 4, rp->ring.so,
-            rp->ring.D, rp->ring.capacity, q.cursor, k, static_cast<const uint8_t *>(q.s), q.a, q.r,
+            rp->ring.D, rp->ring.shared, rp->ring.capacity, q.cursor, k, static_cast<const uint8_t *>(q.s), q.a, q.r,
             static_cast<const uint8_t *>(q.s2), q.done, rp->err_dev, rp->ctrl_dev, q.new_size);
     } else {
         insert_kernel<<<(unsigned)blocks, 256, 0, rp->stream>>>(
-            rp->ring.rows, rp->ring.rs, rp->ring.D, rp->ring.capacity, q.cursor, k,
+            rp->ring.rows, rp->ring.rs, rp->ring.D, rp->ring.sw, rp->ring.capacity, q.cursor, k,
             static_cast<const float *>(q.s), q.a, q.r, static_cast<const float *>(q.s2), q.done,
             rp->err_dev, rp->ctrl_dev, q.new_size);
     }
@@ -450,13 +512,21 @@ int launch_gather(rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t ev
     if (blocks < 1) blocks = 1;
     const rpl::Ring &R = rp->ring;
     float *os = static_cast<float *>(out->s), *os2 = static_cast<float *>(out->s_next);
+    const int64_t nvalid = sampleable(rp);
+    const uint64_t oldest = oldest_slot(rp);
     if (R.u8) {
         int64_t nb = n < (int64_t)dev_sms * 8 ? n : (int64_t)dev_sms * 8;
         if (nb < 1) nb = 1;
         gather_u8_kernel<<<(unsigned)nb, 256, 0, rp->stream>>>(
-            reinterpret_cast<const uint8_t *>(R.rows), (int64_t)R.rs * 4, R.so, R.D, rp->size, n,
+            reinterpret_cast<const uint8_t *>(R.rows), (int64_t)R.rs * 4, R.so, R.D, R.shared,
+            R.capacity, oldest, nvalid, rp->size, n,
             use_sampler ? nullptr : idx_dev, rp->seed, rp->rank, event,
             static_cast<uint8_t *>(out->s), static_cast<uint8_t *>(out->s_next), out->a, out->r,
+            out->done, out->idx, rp->err_dev, rp->ctrl_dev);
+    } else if (R.shared) {
+        gather_shared_kernel<<<(unsigned)blocks, 256, 0, rp->stream>>>(
+            R.rows, R.rs, R.D, R.sw, R.capacity, nvalid, oldest, rp->size, n,
+            use_sampler ? nullptr : idx_dev, rp->seed, rp->rank, event, os, os2, out->a, out->r,
             out->done, out->idx, rp->err_dev, rp->ctrl_dev);
     } else if (R.rs == 64 && R.D == 27) {
         // staged, line-coalesced writes (the Melee row: 27-float states)
@@ -516,7 +586,8 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
     if (capacity < 1 || capacity >= (int64_t(1) << 31) || state_dim < 1 || state_dim > 1 << 20 ||
         o.rank >= (1u << 24) || o.burn_in < 1 || o.max_host_add < 0 ||
         (o.state_dtype != RPL_F32 && o.state_dtype != RPL_U8) ||
-        (o.sampling != RPL_SAMPLE_UNIFORM && o.sampling != RPL_SAMPLE_DISTINCT)) {
+        (o.sampling != RPL_SAMPLE_UNIFORM && o.sampling != RPL_SAMPLE_DISTINCT) ||
+        (o.state_sharing != 0 && o.state_sharing != 1)) {
         set_error("replay_create: invalid argument (capacity=%lld state_dim=%d rank=%u burn_in=%lld)",
                   (long long)capacity, state_dim, o.rank, (long long)o.burn_in);
         return RPL_EINVAL;
@@ -543,8 +614,11 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
     rp->ring.capacity = capacity;
     rp->ring.D = state_dim;
     rp->ring.u8 = u8 ? 1 : 0;
-    rp->ring.rs = u8 ? ring_u8_row_bytes(state_dim) / 4 : ring_row_stride(state_dim);
-    rp->ring.so = u8 ? ring_u8_scalar_offset(state_dim) : 0;
+    const bool sh = o.state_sharing != 0;
+    rp->ring.shared = sh ? 1 : 0;
+    rp->ring.rs = u8 ? ring_u8_row_bytes(state_dim, sh) / 4 : ring_row_stride(state_dim, sh);
+    rp->ring.so = u8 ? ring_u8_scalar_offset(state_dim, sh) : 0;
+    rp->ring.sw = sh ? state_dim : 2 * state_dim;
     if (u8) rp->no_defer = true;   // deferral is a fast-path (fp32 states) feature
     rp->distinct = o.sampling == RPL_SAMPLE_DISTINCT;
     const size_t ring_bytes = (size_t)capacity * rp->ring.rs * sizeof(float);
@@ -558,8 +632,8 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
     }
     const size_t st = host_add_bytes(rp->max_host_add, state_dim, u8) + 64;
     bool ok = cudaMalloc(&rp->err_dev, sizeof(uint32_t)) == cudaSuccess &&
-              cudaMalloc(&rp->ctrl_dev, 2 * sizeof(uint64_t)) == cudaSuccess &&
-              cudaMemsetAsync(rp->ctrl_dev, 0, 2 * sizeof(uint64_t), rp->stream) == cudaSuccess;
+              cudaMalloc(&rp->ctrl_dev, 3 * sizeof(uint64_t)) == cudaSuccess &&
+              cudaMemsetAsync(rp->ctrl_dev, 0, 3 * sizeof(uint64_t), rp->stream) == cudaSuccess;
     for (int i = 0; i < 2 && ok; ++i) {
         ok = cudaHostAlloc(&rp->pinned[i], st, cudaHostAllocDefault) == cudaSuccess &&
              cudaMalloc(&rp->dstage[i], st) == cudaSuccess &&
@@ -606,7 +680,7 @@ extern "C" int replay_add(rpl_replay *rp, int64_t k, const void *s, const int32_
         return RPL_EINVAL;
     }
     if (k == 0) return RPL_OK;
-    if (!s || !a || !r || !s_next || !done) {
+    if (!s || !a || !r || (!s_next && !rp->ring.shared) || !done) {
         set_error("replay_add: null input pointer");
         return RPL_EINVAL;
     }
@@ -639,7 +713,9 @@ extern "C" int replay_add(rpl_replay *rp, int64_t k, const void *s, const int32_
         memcpy(hp + off, r, (size_t)k * 4); dr = (const float *)(dp + off); off += (size_t)k * 4;
         memcpy(hp + off, a, (size_t)k * 4); da = (const int32_t *)(dp + off); off += (size_t)k * 4;
         memcpy(hp + off, s, bs); ds = dp + off; off += bs;
-        memcpy(hp + off, s_next, bs); ds2 = dp + off; off += bs;
+        if (!rp->ring.shared) {   // shared states: one state per experience crosses PCIe
+            memcpy(hp + off, s_next, bs); ds2 = dp + off; off += bs;
+        }
         memcpy(hp + off, done, (size_t)k); dd = (const uint8_t *)(dp + off); off += (size_t)k;
         RPL_CUDA(cudaMemcpyAsync(dp, hp, off, cudaMemcpyHostToDevice, rp->stream));
         RPL_CUDA(cudaEventRecord(rp->staged[slot], rp->stream));
@@ -677,7 +753,8 @@ extern "C" int replay_sample(rpl_replay *rp, int32_t batch, const rpl_batch *out
         set_error("replay_sample: distinct batch %d > %d", batch, DS_MAXB);
         return RPL_EINVAL;
     }
-    if (rp->size < rp->burn_in || (rp->distinct && rp->size < batch)) return RPL_NOT_READY;
+    const int64_t nvalid = sampleable(rp);
+    if (rp->size < rp->burn_in || nvalid < 1 || (rp->distinct && nvalid < batch)) return RPL_NOT_READY;
     DeviceGuard g(rp->device);
     int rc = launch_gather(rp, batch, nullptr, rp->events, 1, out);
     if (rc != RPL_OK) return rc;

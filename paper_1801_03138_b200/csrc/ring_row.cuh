@@ -1,8 +1,15 @@
 // ring_row.cuh -- the one definition of a packed ring row write (CUDA path only), shared by
 // the insert kernel (replay.cu) and the deferred insert that K1 of the fast train step
-// performs (train_fast.cuh).  Row layout (DESIGN.md §4): [s (D) | s' (D) | a (i32 bits) |
-// r | done (u32 bits) | zero pad], rs words.  P:73: experience j goes to slot
-// (cursor + j) mod capacity.
+// performs (train_fast.cuh).  Row layout (DESIGN.md §7): [s (D) | s' (D) | a (i32 bits) |
+// r | done (u32 bits) | zero pad], rs words, or [s | a | r | done | pad] with shared states.
+// experience j goes to slot (cursor + j) mod capacity.
+
+// sampler slot of logical position u: the uniform stream draws u over the n sampleable
+// experiences; with shared states the newest is excluded and u counts from the oldest
+__device__ __forceinline__ int32_t slot_of(int32_t u, uint64_t oldest, int64_t capacity)
+{
+    return (int32_t)((oldest + (uint64_t)u) % (uint64_t)capacity);
+}
 #pragma once
 #include <stdint.h>
 
@@ -10,8 +17,9 @@
 
 namespace rpl {
 
-// warp-cooperative: lane c writes words c, c + 32, ... of experience j's row
-__device__ __forceinline__ void ring_write_row(float *row, int rs, int D, int lane, int64_t j,
+// warp-cooperative: lane c writes words c, c + 32, ... of experience j's row.  sw = first
+// scalar word: 2D, or D for shared-state rows [s | a | r | done] (no s' stored)
+__device__ __forceinline__ void ring_write_row(float *row, int rs, int D, int sw, int lane, int64_t j,
                                                const float *__restrict__ s,
                                                const int32_t *__restrict__ a,
                                                const float *__restrict__ r,
@@ -22,13 +30,13 @@ __device__ __forceinline__ void ring_write_row(float *row, int rs, int D, int la
         float v = 0.0f;
         if (c < D) {
             v = s[j * D + c];
-        } else if (c < 2 * D) {
+        } else if (c < sw) {
             v = s2[j * D + (c - D)];
-        } else if (c == 2 * D) {
+        } else if (c == sw) {
             v = __int_as_float(a[j]);
-        } else if (c == 2 * D + 1) {
+        } else if (c == sw + 1) {
             v = r[j];
-        } else if (c == 2 * D + 2) {
+        } else if (c == sw + 2) {
             uint32_t d = done[j];
             if (d > 1u) {   // a device-sourced done > 1 is stored as 1 and flagged
                 atomicOr(err, ERRBIT_CORRUPT);

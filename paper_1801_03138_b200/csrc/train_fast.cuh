@@ -34,9 +34,10 @@ constexpr int F_NT1 = 512;        // threads per K1 CTA
 constexpr int F_NT3 = 256;        // threads per K3 CTA
 
 struct FastArgs {
-    // replay (rctrl[0] = sampler events consumed, rctrl[1] = filled size)
+    // replay (rctrl[0] = sampler events consumed, rctrl[1] = filled size, rctrl[2] = cursor)
     float *ring;
     int rs, D;
+    int shared, sw;      // shared states (s' = next slot's s); scalar word offset
     uint64_t *rctrl;
     uint64_t seed;
     uint32_t rank;
@@ -220,14 +221,17 @@ __global__ void __launch_bounds__(DS_T, 1) distinct_fast_kernel(const __grid_con
     extern __shared__ int ds_smem[];
     const uint64_t event = p.rctrl[0];
     const uint64_t size = p.pend_k ? p.pend_size : p.rctrl[1];
-    distinct_sample(p.seed, p.rank, event, size, p.B, p.idx, p.err, ds_smem,
-                    ds_smem + ds_table_slots(p.B));
+    const uint64_t cursor = p.pend_k ? (uint64_t)((p.pend_cur + p.pend_k) % p.capacity) : p.rctrl[2];
+    const uint64_t nvalid = p.shared ? size - 1 : size;
+    const uint64_t oldest = (p.shared && size == (uint64_t)p.capacity) ? cursor : 0;
+    distinct_sample(p.seed, p.rank, event, nvalid, p.B, p.idx, p.err, ds_smem,
+                    ds_smem + ds_table_slots(p.B), oldest, p.capacity);
 }
 
 // shared-memory layout of K1 (32-bit words); the same formula sizes the launch on the host
 struct FwdLayout {
     int XP, N0P, UT, UTP;
-    int oW0, oX, oXh, oXl, oH0h, oH0l, oW1, oH1, oWh, ob0, ob1, oidx, opj, ored, total;
+    int oW0, oX, oXh, oXl, oH0h, oH0l, oW1, oH1, oWh, ob0, ob1, oidx, opj, opj2, ored, total;
     __host__ __device__ FwdLayout(int D, int N0, int UT_, int J)
     {
         (void)J;
@@ -248,7 +252,8 @@ struct FwdLayout {
         ob1 = ob0 + ((N0 + 3) & ~3);     // [UT]
         oidx = ob1 + UT;                 // [BT]
         opj = oidx + F_BT;               // [BT] deferred-insert index j of the row, or -1
-        ored = opj + F_BT;               // [16 warps][16][F_JP] head partials
+        opj2 = opj + F_BT;               // [BT] the same for its s' row (shared states)
+        ored = opj2 + F_BT;              // [16 warps][16][F_JP] head partials
         total = ored + 16 * 16 * F_JP;
     }
 };
@@ -275,11 +280,19 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
     uint32_t *H0h = reinterpret_cast<uint32_t *>(sm + L.oH0h), *H0l = reinterpret_cast<uint32_t *>(sm + L.oH0l);
     float *H1s = sm + L.oH1, *Whs = sm + L.oWh, *b0s = sm + L.ob0, *b1s = sm + L.ob1, *red = sm + L.ored;
     int *idxs = reinterpret_cast<int *>(sm + L.oidx), *pjs = reinterpret_cast<int *>(sm + L.opj);
+    int *pjs2 = reinterpret_cast<int *>(sm + L.opj2);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
     const int nbt = (B + F_BT - 1) / F_BT, nut = p.nut;
     const uint64_t event = p.rctrl[0];
     const uint64_t size = p.pend_k ? p.pend_size : p.rctrl[1];
-    if (p.pend_k && blockIdx.x == 0 && threadIdx.x == 0) p.rctrl[1] = p.pend_size;
+    const uint64_t cursor = p.pend_k ? (uint64_t)((p.pend_cur + p.pend_k) % p.capacity) : p.rctrl[2];
+    // shared states: the newest experience has no stored successor (reading Q30)
+    const uint64_t nvalid = p.shared ? size - 1 : size;
+    const uint64_t oldest = (p.shared && size == (uint64_t)p.capacity) ? cursor : 0;
+    if (p.pend_k && blockIdx.x == 0 && threadIdx.x == 0) {
+        p.rctrl[1] = p.pend_size;
+        p.rctrl[2] = cursor;
+    }
     const int ntasks = p.nets * nbt * nut;
     // tasks are (net, unit tile)-major: with the grid a multiple of nets x nut (large batches),
     // a CTA keeps one weight tile resident and walks batch tiles, loading the weights once
@@ -332,23 +345,33 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
                 i0 = rb + 2 * tid < B ? p.idx[rb + 2 * tid] : 0;
                 i1 = rb + 2 * tid + 1 < B ? p.idx[rb + 2 * tid + 1] : 0;
             } else {
-                sample_pair(p.seed, p.rank, event, (uint32_t)(rb / 2 + tid), size, i0, i1);
+                sample_pair(p.seed, p.rank, event, (uint32_t)(rb / 2 + tid), nvalid, i0, i1);
+                i0 = slot_of(i0, oldest, p.capacity);
+                i1 = slot_of(i1, oldest, p.capacity);
             }
             idxs[2 * tid] = i0;
             idxs[2 * tid + 1] = i1;
-            int64_t j0 = (int64_t)i0 - p.pend_cur, j1 = (int64_t)i1 - p.pend_cur;
-            if (j0 < 0) j0 += p.capacity;
-            if (j1 < 0) j1 += p.capacity;
-            pjs[2 * tid] = j0 < p.pend_k ? (int)j0 : -1;
-            pjs[2 * tid + 1] = j1 < p.pend_k ? (int)j1 : -1;
+            // deferred-insert index of a slot (read-through), or -1
+            auto pend_j = [&](int64_t slot) {
+                int64_t j = slot - p.pend_cur;
+                if (j < 0) j += p.capacity;
+                return j < p.pend_k ? (int)j : -1;
+            };
+            pjs[2 * tid] = pend_j(i0);
+            pjs[2 * tid + 1] = pend_j(i1);
+            pjs2[2 * tid] = p.shared ? pend_j((i0 + 1) % p.capacity) : -1;
+            pjs2[2 * tid + 1] = p.shared ? pend_j((i1 + 1) % p.capacity) : -1;
         }
         __syncthreads();
         // (3) gather the 16 sampled rows: s for online(s), s' for target(s') / online(s')
-        const int col0 = net == 0 ? 0 : D;
+        // shared states: s' is the old state of the next slot
+        const bool nxt = net != 0 && p.shared;
+        const int col0 = net == 0 || p.shared ? 0 : D;
         for (int e = tid; e < F_BT * D; e += F_NT1) {
-            const int rr = e / D, d = e - rr * D, j = pjs[rr];
-            const float *src = j < 0 ? p.ring + (int64_t)idxs[rr] * p.rs + col0 + d
-                                     : (net == 0 ? p.pend_s : p.pend_s2) + (int64_t)j * D + d;
+            const int rr = e / D, d = e - rr * D, j = nxt ? pjs2[rr] : pjs[rr];
+            const int64_t slot = nxt ? (idxs[rr] + 1) % p.capacity : idxs[rr];
+            const float *src = j < 0 ? p.ring + slot * p.rs + col0 + d
+                                     : (net == 0 || p.shared ? p.pend_s : p.pend_s2) + (int64_t)j * D + d;
             cp_async4(Xs + rr * L.XP + d, src);
         }
         int32_t ra_ = 0;
@@ -358,7 +381,7 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
         if (unpack_scalars) {
             const int j = pjs[tid];
             if (j < 0) {
-                const float *row = p.ring + (int64_t)idxs[tid] * p.rs + 2 * D;
+                const float *row = p.ring + (int64_t)idxs[tid] * p.rs + p.sw;
                 ra_ = __float_as_int(__ldg(row));
                 rr_ = __ldg(row + 1);
                 rd_ = __float_as_uint(__ldg(row + 2));
@@ -374,7 +397,7 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
             for (int j = blockIdx.x * NW + warp; j < p.pend_k; j += gridDim.x * NW) {
                 int64_t slot = p.pend_cur + j;
                 if (slot >= p.capacity) slot -= p.capacity;
-                ring_write_row(p.ring + slot * p.rs, p.rs, D, lane, j, p.pend_s, p.pend_a,
+                ring_write_row(p.ring + slot * p.rs, p.rs, D, p.sw, lane, j, p.pend_s, p.pend_a,
                                p.pend_r, p.pend_s2, p.pend_done, p.pend_err);
             }
         }

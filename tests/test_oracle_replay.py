@@ -144,3 +144,50 @@ def test_sample_matches_sampler_then_gather():
     rc, b1 = r1.sample(burn_in=1, seed=1, rank=0, batch=4)
     assert rc == oracle.OK and np.all(b1["idx"] == 0)
     assert np.array_equal(b1["s"], np.repeat(e["s"][:1], 4, axis=0))
+
+
+# ---- shared-state storage ("by only storing one state per experience, and
+# modifying the sample operations"; reading Q30) ----
+
+def test_shared_state_rows_and_next_state():
+    # half-width rows [s | a | r | t]; s' of slot i is s of slot i+1; the newest slot has
+    # no successor and is never sampled
+    D, C = 3, 6
+    r = oracle.Ring(C, D, shared=True)
+    assert r.rows().shape[1] >= D + 3 and r._r.row_width == D + 3
+    e = _exp(4, D)
+    assert r.add(e["s"], e["a"], e["r"], None, e["done"]) == oracle.OK
+    g = r.gather([0, 1, 2])
+    assert np.array_equal(g["s"], e["s"][:3]) and np.array_equal(g["s_next"], e["s"][1:4])
+    with pytest.raises(ValueError):
+        r.gather([3])   # the newest experience: s' not stored yet
+
+
+@pytest.mark.parametrize("distinct", [False, True])
+def test_shared_state_sampler_brute_force(distinct):
+    # the sampler draws logical positions u over the size-1 experiences with a successor,
+    # slot = (oldest + u) mod C; checked by brute force against an explicit deque of the
+    # stream, before and after the ring wraps
+    D, C, B = 2, 40, 16
+    r = oracle.Ring(C, D, shared=True, distinct=distinct)
+    e = _exp(200, D, seed=3)
+    t = 0
+    for k in [10, 7, 13, 25, 31, 40, 3]:
+        part = {kk: v[t:t + k] for kk, v in e.items()}
+        assert r.add(part["s"], part["a"], part["r"], None, part["done"]) == oracle.OK
+        t += k
+        stream = list(range(max(0, t - C), t))        # experiences in the ring, oldest first
+        ev = r.events
+        rc, b = r.sample(1, 5, 0, B)
+        n = len(stream) - 1
+        if distinct and n < B:
+            assert rc == oracle.NOT_READY
+            continue
+        assert rc == oracle.OK
+        u = (oracle.sample_distinct if distinct else oracle.sample_indices)(5, 0, ev, n, B)
+        for i in range(B):
+            src = stream[u[i]]                          # logical position u -> experience
+            assert b["idx"][i] == src % C               # its slot (FIFO: t mod C)
+            assert np.array_equal(b["s"][i], e["s"][src])
+            assert np.array_equal(b["s_next"][i], e["s"][src + 1])   # the next experience's s
+            assert b["a"][i] == e["a"][src] and b["done"][i] == e["done"][src]
