@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-gather", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--sweep", default="", help="comma list of batch sizes: one JSON line each")
+    ap.add_argument("--shared-state", action="store_true",
+                    help="store one state per experience (P:141): s' = the next slot's s")
     ap.add_argument("--distinct", action="store_true",
                     help="sample distinct indices (RPL_SAMPLE_DISTINCT, P:75's planned switch)")
     ap.add_argument("--config", choices=["c2", "c5"], default="c2",
@@ -255,7 +257,8 @@ def run_ours(a, batch, first_line=True):
 
     cfg = make_cfg(a, binding, batch)
     rp = binding.Replay(a.capacity, 27, device=local, burn_in=1, seed=2, rank=rank,
-                        sampling="distinct" if a.distinct else "uniform")
+                        sampling="distinct" if a.distinct else "uniform",
+                        shared_state=a.shared_state)
     # pre-fill the whole ring (startup excluded from timings); per-rank data stream
     rp.add_many(experiences(a.capacity, seed=1, rank=rank))
     dqn = binding.DQN(cfg, init_params(27, 8, cfg.hidden, cfg.dueling, cfg.stream, seed=3),
@@ -452,6 +455,7 @@ def run_ours(a, batch, first_line=True):
         "config": {"workload": workload_name(a, batch), "batch": batch, "capacity": a.capacity,
                    "net": a.net, "double_dqn": a.ddqn, "adds_per_step": k,
                    "sampling": "distinct" if a.distinct else "uniform (with replacement, P:75)",
+                   "state_storage": "shared (s' = next slot's s, P:141)" if a.shared_state else "s and s' per row",
                    "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2: the 256 MB ring (> 126 MB L2) is sampled uniformly;"
                          " the 0.56 MB weights stay L2-resident as in steady-state training"},
@@ -475,6 +479,7 @@ def run_ours(a, batch, first_line=True):
 # ------------------------------------------------------------------------------------------
 C5_D = 84 * 84 * 4
 C5_ROW_BYTES = 56576      # device row: round_up(round_up(2 * C5_D, 16) + 12, 128)
+C5_ROW_BYTES_SHARED = 28288   # one state per row: round_up(round_up(C5_D, 16) + 12, 128)
 
 
 def c5_cfg(binding, batch, ddqn):
@@ -525,7 +530,8 @@ def run_c5(a):
     batch = a.batch if a.batch != 128 else 256
     cfg = c5_cfg(binding, batch, a.ddqn)
     rp = binding.Replay(a.capacity, C5_D, device=local, burn_in=1, seed=2, rank=rank,
-                        state_dtype="u8")
+                        state_dtype="u8", shared_state=a.shared_state,
+                        sampling="distinct" if a.distinct else "uniform")
     # device-side pre-fill (startup, excluded from timings): a 1,024-experience pool of
     # this rank's synthetic stream inserted round-robin until the ring is full
     npool = 1024
@@ -668,7 +674,8 @@ def run_c5(a):
         "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"BASELINE configs[4]: {a.capacity:,}-slot replay of 84x84x4 uint8 "
-                               f"states ({a.capacity * C5_ROW_BYTES / 1e9:.1f} GB ring), "
+                               f"states ({a.capacity * (C5_ROW_BYTES_SHARED if a.shared_state else C5_ROW_BYTES) / 1e9:.1f} GB ring"
+                               f"{', shared states' if a.shared_state else ''}), "
                                f"batch {batch}, dueling DQN 28224-128-[V512|A512]-1+8 on x = u8/255, "
                                f"{'Double-DQN' if a.ddqn else 'DQN'} target, Huber, SGD, {k} "
                                "inserts/step",
