@@ -124,32 +124,46 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
                 wd_cp16(A + pl * WD_A_PLANE + wd_off_k(u, k), v ? Wp + pl * nd + (int64_t)u * p.D + k0 + k : Wp, v);
             }
         }
-        // B: U[b][k0 .. k0+63] u8 -> bf16 (K-major), 16 bytes per thread-step
-        for (int e = tid; e < N * (WD_KS / 16); e += WD_T) {
-            const int b = e / (WD_KS / 16), k = 16 * (e % (WD_KS / 16));
-            uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            if (b < p.B) {
-                const uint8_t *src = U + (int64_t)b * p.D + k0 + k;
-                if (k0 + k + 15 < ke && ((uintptr_t)src & 15) == 0) {
-                    v = __ldg(reinterpret_cast<const uint4 *>(src));
-                } else {
-                    uint8_t t[16];
-                    for (int q = 0; q < 16; ++q) t[q] = (k0 + k + q < ke) ? src[q] : 0;
-                    v = make_uint4(t[0] | t[1] << 8 | t[2] << 16 | (uint32_t)t[3] << 24,
-                                   t[4] | t[5] << 8 | t[6] << 16 | (uint32_t)t[7] << 24,
-                                   t[8] | t[9] << 8 | t[10] << 16 | (uint32_t)t[11] << 24,
-                                   t[12] | t[13] << 8 | t[14] << 16 | (uint32_t)t[15] << 24);
-                }
-            }
-            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-            uint32_t o8[8];
+        // B: U[b][k0 .. k0+63] u8 -> bf16 (K-major), 16 bytes per thread-step; every load of
+        // the slice is issued before the first conversion (at most 4 per thread: N <= 256)
+        {
+            const int total = N * (WD_KS / 16);
+            uint4 v[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                o8[2 * q] = pack2(u8_bf16(w4[q] & 0xFF), u8_bf16((w4[q] >> 8) & 0xFF));
-                o8[2 * q + 1] = pack2(u8_bf16((w4[q] >> 16) & 0xFF), u8_bf16(w4[q] >> 24));
+                const int e = tid + q * WD_T;
+                v[q] = make_uint4(0u, 0u, 0u, 0u);
+                if (e >= total) continue;
+                const int b = e / (WD_KS / 16), k = 16 * (e % (WD_KS / 16));
+                if (b < p.B) {
+                    const uint8_t *src = U + (int64_t)b * p.D + k0 + k;
+                    if (k0 + k + 15 < ke && ((uintptr_t)src & 15) == 0) {
+                        v[q] = __ldg(reinterpret_cast<const uint4 *>(src));
+                    } else {
+                        uint8_t t[16];
+                        for (int i = 0; i < 16; ++i) t[i] = (k0 + k + i < ke) ? src[i] : 0;
+                        v[q] = make_uint4(t[0] | t[1] << 8 | t[2] << 16 | (uint32_t)t[3] << 24,
+                                          t[4] | t[5] << 8 | t[6] << 16 | (uint32_t)t[7] << 24,
+                                          t[8] | t[9] << 8 | t[10] << 16 | (uint32_t)t[11] << 24,
+                                          t[12] | t[13] << 8 | t[14] << 16 | (uint32_t)t[15] << 24);
+                    }
+                }
             }
-            *reinterpret_cast<uint4 *>(Bs + wd_off_k(b, k)) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
-            *reinterpret_cast<uint4 *>(Bs + wd_off_k(b, k + 8)) = make_uint4(o8[4], o8[5], o8[6], o8[7]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int e = tid + q * WD_T;
+                if (e >= total) continue;
+                const int b = e / (WD_KS / 16), k = 16 * (e % (WD_KS / 16));
+                const uint32_t w4[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+                uint32_t o8[8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    o8[2 * i] = pack2(u8_bf16(w4[i] & 0xFF), u8_bf16((w4[i] >> 8) & 0xFF));
+                    o8[2 * i + 1] = pack2(u8_bf16((w4[i] >> 16) & 0xFF), u8_bf16(w4[i] >> 24));
+                }
+                *reinterpret_cast<uint4 *>(Bs + wd_off_k(b, k)) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
+                *reinterpret_cast<uint4 *>(Bs + wd_off_k(b, k + 8)) = make_uint4(o8[4], o8[5], o8[6], o8[7]);
+            }
         }
         wd_cp_wait();
         umma::fence_async_smem();
@@ -233,32 +247,46 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
                         v ? p.dZ0bf + pl * pz + (int64_t)(b0 + bb) * p.N0 + u : p.dZ0bf, v);
             }
         }
-        // B = U^T slice: element (input n, sample b) = U[b][n0 + n], MN-major (contiguous in n)
-        for (int e = tid; e < WD_KS * (N / 16); e += WD_T) {
-            const int bb = e / (N / 16), n = 16 * (e % (N / 16));
-            uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            if (b0 + bb < p.B) {
-                const uint8_t *src = p.U0 + (int64_t)(b0 + bb) * p.D + n0 + n;
-                if (n + 15 < nn && ((uintptr_t)src & 15) == 0) {
-                    v = __ldg(reinterpret_cast<const uint4 *>(src));
-                } else {
-                    uint8_t t[16];
-                    for (int q = 0; q < 16; ++q) t[q] = (n + q < nn) ? src[q] : 0;
-                    v = make_uint4(t[0] | t[1] << 8 | t[2] << 16 | (uint32_t)t[3] << 24,
-                                   t[4] | t[5] << 8 | t[6] << 16 | (uint32_t)t[7] << 24,
-                                   t[8] | t[9] << 8 | t[10] << 16 | (uint32_t)t[11] << 24,
-                                   t[12] | t[13] << 8 | t[14] << 16 | (uint32_t)t[15] << 24);
-                }
-            }
-            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-            uint32_t o8[8];
+        // B = U^T slice: element (input n, sample b) = U[b][n0 + n], MN-major (contiguous in n);
+        // all loads first (at most 4 per thread), then the conversions
+        {
+            const int total = WD_KS * (N / 16);
+            uint4 v[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                o8[2 * q] = pack2(u8_bf16(w4[q] & 0xFF), u8_bf16((w4[q] >> 8) & 0xFF));
-                o8[2 * q + 1] = pack2(u8_bf16((w4[q] >> 16) & 0xFF), u8_bf16(w4[q] >> 24));
+                const int e = tid + q * WD_T;
+                v[q] = make_uint4(0u, 0u, 0u, 0u);
+                if (e >= total) continue;
+                const int bb = e / (N / 16), n = 16 * (e % (N / 16));
+                if (b0 + bb < p.B) {
+                    const uint8_t *src = p.U0 + (int64_t)(b0 + bb) * p.D + n0 + n;
+                    if (n + 15 < nn && ((uintptr_t)src & 15) == 0) {
+                        v[q] = __ldg(reinterpret_cast<const uint4 *>(src));
+                    } else {
+                        uint8_t t[16];
+                        for (int i = 0; i < 16; ++i) t[i] = (n + i < nn) ? src[i] : 0;
+                        v[q] = make_uint4(t[0] | t[1] << 8 | t[2] << 16 | (uint32_t)t[3] << 24,
+                                          t[4] | t[5] << 8 | t[6] << 16 | (uint32_t)t[7] << 24,
+                                          t[8] | t[9] << 8 | t[10] << 16 | (uint32_t)t[11] << 24,
+                                          t[12] | t[13] << 8 | t[14] << 16 | (uint32_t)t[15] << 24);
+                    }
+                }
             }
-            *reinterpret_cast<uint4 *>(Bs + wd_off_mn(n, bb, N)) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
-            *reinterpret_cast<uint4 *>(Bs + wd_off_mn(n + 8, bb, N)) = make_uint4(o8[4], o8[5], o8[6], o8[7]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int e = tid + q * WD_T;
+                if (e >= total) continue;
+                const int bb = e / (N / 16), n = 16 * (e % (N / 16));
+                const uint32_t w4[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+                uint32_t o8[8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    o8[2 * i] = pack2(u8_bf16(w4[i] & 0xFF), u8_bf16((w4[i] >> 8) & 0xFF));
+                    o8[2 * i + 1] = pack2(u8_bf16((w4[i] >> 16) & 0xFF), u8_bf16(w4[i] >> 24));
+                }
+                *reinterpret_cast<uint4 *>(Bs + wd_off_mn(n, bb, N)) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
+                *reinterpret_cast<uint4 *>(Bs + wd_off_mn(n + 8, bb, N)) = make_uint4(o8[4], o8[5], o8[6], o8[7]);
+            }
         }
         wd_cp_wait();
         umma::fence_async_smem();
