@@ -287,9 +287,7 @@ def run_ours(a, batch, first_line=True):
         dist.barrier()
     launches_w = binding.kernel_launches()
 
-    # ---- device-resident timed region ----------------------------------------------------
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(K)]
+    # ---- device-resident timed region (nothing but the steps between the two events) ------
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
@@ -298,13 +296,22 @@ def run_ours(a, batch, first_line=True):
         start.record(stream)
         for i in range(K):
             add_dev(W + i)
-            ev[i][0].record(stream)
             dqn.train_step(rp, batch, loss_dev)
-            ev[i][1].record(stream)
         end.record(stream)
         torch.cuda.synchronize()
     launches = binding.kernel_launches() - launches_w
     elapsed_ms = start.elapsed_time(end)
+    # per-launch duration of the step's kernels for the roofline: a separate pass with CUDA
+    # events around every dqn_train_step (the events add stream ops, so not the timed one)
+    kr = min(K, 1000)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(kr)]
+    for i in range(kr):
+        add_dev(W + K + i)
+        ev[i][0].record(stream)
+        dqn.train_step(rp, batch, loss_dev)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
     kern_ms = [s.elapsed_time(e) for s, e in ev]
     st = dqn.check()
     assert st == binding.RPL_OK, f"device error {st}: {binding.last_error()}"
@@ -330,8 +337,9 @@ def run_ours(a, batch, first_line=True):
             if k:
                 j = (i % 256) * k
                 rp.add(**{kk: v[j:j + k] for kk, v in pool_h.items()})
-            dqn.train_step(rp, batch, loss_dev)
-            loss_host[i:i + 1].copy_(loss_dev, non_blocking=True)
+            # the step's loss is stored by the last kernel straight into pinned host memory
+            # (a 4-byte device -> host write over PCIe; no copy op in the stream)
+            dqn.train_step(rp, batch, loss_host[i:i + 1])
         e2.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
@@ -344,9 +352,10 @@ def run_ours(a, batch, first_line=True):
         assert np.all(np.isfinite(loss_host.numpy()))
         e2e = {"value": world * K / (max(e2e_ms / 1000.0, wall)), "unit": "train_steps/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4,
-               "note": "replay_add(RPL_HOST) from pageable numpy -> library pinned staging -> "
-                       "H2D, dqn_train_step, loss D2H into pinned host memory, every step; "
-                       "slower of CUDA-event and wall time"}
+               "note": "replay_add(RPL_HOST) from pageable numpy -> library pinned staging (read "
+                       "by the device over PCIe when the step consumes the insert: zero-copy), "
+                       "dqn_train_step whose last kernel writes the loss into pinned host memory, "
+                       "every step; slower of CUDA-event and wall time"}
 
     # ---- roofline of the dominant kernel (the fused train step) --------------------------
     flops = binding.step_flops(cfg, batch)
@@ -559,8 +568,6 @@ def run_c5(a):
     if world > 1:
         dist.barrier()
     launches_w = binding.kernel_launches()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(K)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
@@ -569,13 +576,20 @@ def run_c5(a):
         start.record(stream)
         for i in range(K):
             add_dev(W + i)
-            ev[i][0].record(stream)
             dqn.train_step(rp, batch, loss_dev)
-            ev[i][1].record(stream)
         end.record(stream)
         torch.cuda.synchronize()
     launches = binding.kernel_launches() - launches_w
     elapsed_ms = start.elapsed_time(end)
+    kr = min(K, 200)   # per-step durations for the roofline, in a separate pass
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(kr)]
+    for i in range(kr):
+        add_dev(W + K + i)
+        ev[i][0].record(stream)
+        dqn.train_step(rp, batch, loss_dev)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
     kern_ms = [s_.elapsed_time(e_) for s_, e_ in ev]
     assert dqn.check() == binding.RPL_OK, binding.last_error()
     if world > 1:
@@ -598,8 +612,9 @@ def run_c5(a):
             if k:
                 j = (i * k) % (npool - k)
                 rp.add(**{kk: v[j:j + k] for kk, v in pool_h.items()})
-            dqn.train_step(rp, batch, loss_dev)
-            loss_host[i:i + 1].copy_(loss_dev, non_blocking=True)
+            # the step's loss is stored by the last kernel straight into pinned host memory
+            # (a 4-byte device -> host write over PCIe; no copy op in the stream)
+            dqn.train_step(rp, batch, loss_host[i:i + 1])
         e2.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0

@@ -100,7 +100,8 @@ int replay_destroy(rpl_replay *replay);
  * mem = RPL_HOST: host pointers, copied into
  * pinned staging before return (the caller may reuse them at once); one H2D copy of
  * k*(8*state_dim+9) bytes is counted in replay_state's h2d_bytes -- the only PCIe
- * traffic of the method.  mem = RPL_DEVICE: device pointers that must stay
+ * traffic of the method; a deferred host add is read by the device straight from
+ * the pinned staging (zero-copy) when the step consumes it.  mem = RPL_DEVICE: device pointers that must stay
  * valid until the stream reaches the insert.  mem = RPL_DEVICE_DEFER: device pointers
  * whose contents must stay valid AND unchanged until the next call on this replay or the
  * next dqn_train_step on it has been reached by the stream.
@@ -190,9 +191,11 @@ int dqn_destroy(rpl_dqn *dqn);
  * same device and stream):  burn-in gate -> Philox sample (event E of the replay)
  * -> gather -> Q_online(s), Q_target(s') [, Q_online(s')] -> TD target, Huber loss ->
  * backward through the online net -> SGD w -= lr * g -> step t += 1 -> target
- * sync when t % sync_period == 0.  All in one cooperative kernel launch (plus an
- * NCCL all-reduce and an SGD launch when attached to world > 1).  loss_dev (nullable,
- * device fp32) receives the batch-mean Huber loss.  Returns RPL_NOT_READY (nothing
+ * sync when t % sync_period == 0.  One CUDA-graph launch of the fast path's kernels
+ * (or one cooperative kernel for other shapes; byte-state wide inputs add their layer-0
+ * tensor-core kernels), plus an NCCL all-reduce and an SGD launch when attached to world > 1.  loss_dev (nullable, fp32,
+ * device memory or pinned host memory -- the latter is written by the device over PCIe, no
+ * copy op) receives the batch-mean Huber loss.  Returns RPL_NOT_READY (nothing
  * enqueued, no counter advanced) while size < burn_in.  Errors: EINVAL (batch < 1 or >
  * max_batch, dims differ from the replay's, different device), ECUDA. */
 int dqn_train_step(rpl_dqn *dqn, rpl_replay *replay, int32_t batch, float *loss_dev);

@@ -749,12 +749,14 @@ struct rpl_dqn {
     struct GraphEntry {
         const rpl_replay *rp;
         int B;
-        float *loss;
-        cudaGraph_t graph;          // kept alive: k1 is one of its nodes
+        int apply;                  // 0: data-parallel step (SGD after the all-reduce)
+        cudaGraph_t graph;          // kept alive: its nodes are updated in place
         cudaGraphExec_t exec;
-        cudaGraphNode_t k1;         // K1's node (its args carry the deferred insert)
-        cudaGraphNode_t ds;         // distinct sampler's node (same args) or null
-        FastArgs k1args;            // the args K1's node currently holds
+        // nodes whose args change between replays: K1 and the distinct sampler (deferred
+        // insert read-through, control block), K3 (the deferred insert's ring write), K4
+        // (the loss destination)
+        cudaGraphNode_t k1, ds, k3, k4;
+        FastArgs args;              // the args those nodes currently hold
     };
     std::vector<GraphEntry> graphs;
     bool use_graphs = true;
@@ -1339,16 +1341,18 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
     if (fast) {
         FastArgs fp;
         fill_fast(d, rp, batch, dp ? nullptr : loss_dev, dp ? 0 : 1, fp);
+        const int zslot = rp->pend.slot;   // zero-copy staging slot the insert reads (or -1)
         rp->pend.k = 0;
+        rp->pend.slot = -1;
         if (d->use_graphs) {
             rpl_dqn::GraphEntry *ge = nullptr;
-            float *lkey = dp ? nullptr : loss_dev;
+            const int apply = dp ? 0 : 1;
             for (auto &g : d->graphs)
-                if (g.rp == rp && g.B == batch && g.loss == lkey) ge = &g;
+                if (g.rp == rp && g.B == batch && g.apply == apply) ge = &g;
             if (!ge) {
                 cudaGraph_t graph = nullptr;
                 cudaGraphExec_t exec = nullptr;
-                cudaGraphNode_t k1 = nullptr, ds = nullptr;
+                cudaGraphNode_t k1 = nullptr, ds = nullptr, k3 = nullptr, k4 = nullptr;
                 e = cudaStreamBeginCapture(d->cap_stream, cudaStreamCaptureModeThreadLocal);
                 if (e == cudaSuccess) {
                     cudaError_t e2 = fast_enqueue(d, fp, d->cap_stream);
@@ -1368,9 +1372,11 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                             cudaGraphKernelNodeGetParams(nodes[i], &kp) == cudaSuccess) {
                             if (kp.func == (void *)fast_fwd_fn(d)) k1 = nodes[i];
                             if (kp.func == (void *)distinct_fast_kernel) ds = nodes[i];
+                            if (kp.func == (void *)fast_bwd1_kernel) k3 = nodes[i];
+                            if (kp.func == (void *)fast_bwd0_sgd_kernel) k4 = nodes[i];
                         }
                     }
-                    if (e == cudaSuccess && !k1) e = cudaErrorInvalidValue;
+                    if (e == cudaSuccess && (!k1 || !k3 || !k4)) e = cudaErrorInvalidValue;
                 }
                 if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
                 if (e == cudaSuccess) {
@@ -1379,28 +1385,58 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                         cudaGraphDestroy(d->graphs.front().graph);
                         d->graphs.erase(d->graphs.begin());
                     }
-                    d->graphs.push_back({rp, batch, lkey, graph, exec, k1, ds, fp});
+                    d->graphs.push_back({rp, batch, apply, graph, exec, k1, ds, k3, k4, fp});
                     ge = &d->graphs.back();
                 } else if (graph) {
                     cudaGraphDestroy(graph);
                 }
-            } else if (memcmp(&ge->k1args, &fp, sizeof fp) != 0) {
-                // only K1's (and the distinct sampler's) args change between replays: the
-                // deferred insert
+            } else if (memcmp(&ge->args, &fp, sizeof fp) != 0) {
+                // between replays only the deferred insert and the loss destination change:
+                // update the nodes that read them
+                const bool pend_changed = ge->args.pend_k != fp.pend_k || ge->args.pend_cur != fp.pend_cur ||
+                                          ge->args.pend_s != fp.pend_s || ge->args.pend_size != fp.pend_size ||
+                                          ge->args.pend_s2 != fp.pend_s2 || ge->args.pend_r != fp.pend_r ||
+                                          ge->args.pend_a != fp.pend_a || ge->args.pend_done != fp.pend_done;
+                const bool loss_changed = ge->args.loss_out != fp.loss_out;
+                FastArgs cmp = ge->args;
+                cmp.pend_k = fp.pend_k; cmp.pend_cur = fp.pend_cur; cmp.pend_s = fp.pend_s;
+                cmp.pend_s2 = fp.pend_s2; cmp.pend_r = fp.pend_r; cmp.pend_a = fp.pend_a;
+                cmp.pend_done = fp.pend_done; cmp.pend_size = fp.pend_size; cmp.pend_err = fp.pend_err;
+                cmp.loss_out = fp.loss_out;
                 void *args[] = {&fp};
-                for (cudaGraphNode_t nd : {ge->k1, ge->ds}) {
-                    if (!nd || e != cudaSuccess) continue;
+                auto update = [&](cudaGraphNode_t nd) {
+                    if (!nd || e != cudaSuccess) return;
                     cudaKernelNodeParams kp = {};
                     e = cudaGraphKernelNodeGetParams(nd, &kp);
                     kp.kernelParams = args;
                     kp.extra = nullptr;
                     if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(ge->exec, nd, &kp);
+                };
+                if (memcmp(&cmp, &fp, sizeof fp) != 0) {
+                    // anything else differs (not expected): every node of the step
+                    size_t n = 0;
+                    e = cudaGraphGetNodes(ge->graph, nullptr, &n);
+                    std::vector<cudaGraphNode_t> nodes(n);
+                    if (e == cudaSuccess && n) e = cudaGraphGetNodes(ge->graph, nodes.data(), &n);
+                    for (size_t i = 0; e == cudaSuccess && i < n; ++i) update(nodes[i]);
+                } else {
+                    if (pend_changed) {
+                        update(ge->k1);
+                        update(ge->ds);
+                        update(ge->k3);
+                    }
+                    if (loss_changed) update(ge->k4);
                 }
-                if (e == cudaSuccess) ge->k1args = fp;
+                if (e == cudaSuccess) ge->args = fp;
             }
             if (e == cudaSuccess) e = cudaGraphLaunch(ge->exec, d->stream);
         } else {
             e = fast_enqueue(d, fp, d->stream);
+        }
+        if (e == cudaSuccess) {
+            // the zero-copy staging slot may be rewritten once the stream passes this step
+            if (zslot >= 0 && cudaEventRecord(rp->staged[zslot], d->stream) != cudaSuccess)
+                e = cudaGetLastError();
         }
         if (e != cudaSuccess) {
             if (prev >= 0) cudaSetDevice(prev);

@@ -100,7 +100,9 @@ struct rpl_replay {
         const float *r = nullptr;
         const int32_t *a = nullptr;
         const uint8_t *done = nullptr;
+        int slot = -1;   // zero-copy host add: the pinned staging slot its sources live in
     } pend;
+    bool zero_copy = true;   // host adds read by the device from pinned memory (RPL_NO_ZC=1: H2D copy)
     bool no_defer = false;   // RPL_NO_DEFER=1: every insert is an immediate kernel
     bool distinct = false;   // RPL_SAMPLE_DISTINCT (distinct.cuh)
     int32_t *ds_idx = nullptr;   // scratch indices of distinct replay_sample calls
@@ -122,6 +124,9 @@ int64_t sampleable(const rpl_replay *rp);
 uint64_t oldest_slot(const rpl_replay *rp);
 // enqueue the pending deferred insert (if any) as an insert-kernel launch
 int replay_flush(rpl_replay *rp);
+// the pending insert was enqueued for consumption on `st`: a zero-copy staging slot may be
+// reused once the stream passes this point
+int replay_consumed(rpl_replay *rp, int slot, cudaStream_t st);
 // largest insert that may be deferred into K1 (K1's CTAs write its rows)
 constexpr int64_t kMaxDeferredRows = 4096;
 }  // namespace rpl

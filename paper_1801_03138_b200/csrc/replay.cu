@@ -452,12 +452,20 @@ uint64_t oldest_slot(const rpl_replay *rp)
     return (rp->ring.shared && rp->size == rp->ring.capacity) ? (uint64_t)rp->cursor : 0;
 }
 
+int replay_consumed(rpl_replay *rp, int slot, cudaStream_t st)
+{
+    if (slot >= 0) RPL_CUDA(cudaEventRecord(rp->staged[slot], st));
+    return RPL_OK;
+}
+
 int replay_flush(rpl_replay *rp)
 {
     rpl_replay::Pending &q = rp->pend;
     if (q.k == 0) return RPL_OK;
     const int64_t k = q.k;
     q.k = 0;
+    const int zslot = q.slot;
+    q.slot = -1;
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, rp->device);
     int64_t blocks = (k + 7) / 8;
@@ -476,7 +484,7 @@ int replay_flush(rpl_replay *rp)
             rp->err_dev, rp->ctrl_dev, q.new_size);
     }
     RPL_LAUNCHED();
-    return RPL_OK;
+    return replay_consumed(rp, zslot, rp->stream);
 }
 
 int launch_gather(rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t event,
@@ -605,6 +613,7 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
     rp->seed = o.seed;
     rp->rank = o.rank;
     if (const char *nd = getenv("RPL_NO_DEFER")) rp->no_defer = atoi(nd) != 0;
+    if (const char *nz = getenv("RPL_NO_ZC")) rp->zero_copy = atoi(nz) == 0;
     const bool u8 = o.state_dtype == RPL_U8;
     rp->max_host_add = o.max_host_add ? o.max_host_add : 65536;
     // pinned + device staging is two slots of max_host_add experiences: at most 256 MB each
@@ -654,6 +663,7 @@ extern "C" int replay_destroy(rpl_replay *rp)
     if (!rp) return RPL_OK;
     DeviceGuard g(rp->device);
     rp->pend.k = 0;   // a never-consumed deferred insert is dropped with the ring
+    rp->pend.slot = -1;
     cudaStreamSynchronize(rp->stream);
     for (int i = 0; i < 2; ++i) {
         if (rp->staged[i]) cudaEventDestroy(rp->staged[i]);
@@ -686,8 +696,10 @@ extern "C" int replay_add(rpl_replay *rp, int64_t k, const void *s, const int32_
     }
     DeviceGuard g(rp->device);
     if (int rc = replay_flush(rp)) return rc;   // inserts stay in call order
-    const void *ds = s, *ds2 = s_next;
+    const void *ds = s, *ds2 = nullptr;
+    if (mem != RPL_HOST) ds2 = s_next;
     const float *dr = r;
+    int zslot = -1;
     const int32_t *da = a;
     const uint8_t *dd = done;
     if (mem == RPL_HOST) {
@@ -717,9 +729,23 @@ extern "C" int replay_add(rpl_replay *rp, int64_t k, const void *s, const int32_
             memcpy(hp + off, s_next, bs); ds2 = dp + off; off += bs;
         }
         memcpy(hp + off, done, (size_t)k); dd = (const uint8_t *)(dp + off); off += (size_t)k;
-        RPL_CUDA(cudaMemcpyAsync(dp, hp, off, cudaMemcpyHostToDevice, rp->stream));
-        RPL_CUDA(cudaEventRecord(rp->staged[slot], rp->stream));
         rp->h2d_bytes += off;
+        if (rp->zero_copy && !rp->ring.u8 && !rp->no_defer && k <= kMaxDeferredRows) {
+            // zero-copy: the deferred insert's sources are the pinned slot itself -- the
+            // device reads them over PCIe (once, for the ring write) when it consumes the
+            // insert, so no copy op enters the stream; the slot's event is recorded then
+            const char *dev0 = (const char *)rp->dstage[slot];
+            auto host_of = [&](const void *d) { return (const void *)(hp + ((const char *)d - dev0)); };
+            ds = host_of(ds);
+            if (ds2) ds2 = host_of(ds2);
+            dr = (const float *)host_of(dr);
+            da = (const int32_t *)host_of(da);
+            dd = (const uint8_t *)host_of(dd);
+            zslot = slot;
+        } else {
+            RPL_CUDA(cudaMemcpyAsync(dp, hp, off, cudaMemcpyHostToDevice, rp->stream));
+            RPL_CUDA(cudaEventRecord(rp->staged[slot], rp->stream));
+        }
     }
     const int64_t new_size = rp->size + k < rp->ring.capacity ? rp->size + k : rp->ring.capacity;
     // Defer the ring write of a small insert into the next fast train step (its K1 reads
@@ -733,6 +759,7 @@ extern "C" int replay_add(rpl_replay *rp, int64_t k, const void *s, const int32_
     q.r = dr;
     q.a = da;
     q.done = dd;
+    q.slot = zslot;
     q.k = k;
     if (mem == RPL_DEVICE || k > kMaxDeferredRows || rp->no_defer) {
         if (int rc = replay_flush(rp)) return rc;

@@ -370,9 +370,11 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
         for (int e = tid; e < F_BT * D; e += F_NT1) {
             const int rr = e / D, d = e - rr * D, j = nxt ? pjs2[rr] : pjs[rr];
             const int64_t slot = nxt ? (idxs[rr] + 1) % p.capacity : idxs[rr];
-            const float *src = j < 0 ? p.ring + slot * p.rs + col0 + d
-                                     : (net == 0 || p.shared ? p.pend_s : p.pend_s2) + (int64_t)j * D + d;
-            cp_async4(Xs + rr * L.XP + d, src);
+            if (j < 0) {
+                cp_async4(Xs + rr * L.XP + d, p.ring + slot * p.rs + col0 + d);
+            } else {   // pending insert: its sources (possibly pinned host memory: plain loads)
+                Xs[rr * L.XP + d] = (net == 0 || p.shared ? p.pend_s : p.pend_s2)[(int64_t)j * D + d];
+            }
         }
         int32_t ra_ = 0;
         float rr_ = 0.0f;
@@ -389,16 +391,6 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
                 ra_ = p.pend_a[j];
                 rr_ = p.pend_r[j];
                 rd_ = p.pend_done[j];
-            }
-        }
-        // the deferred insert's ring rows (no sampled row of this step reads them from the
-        // ring), overlapped with this CTA's first operand loads
-        if (p.pend_k && task == (int)blockIdx.x) {
-            for (int j = blockIdx.x * NW + warp; j < p.pend_k; j += gridDim.x * NW) {
-                int64_t slot = p.pend_cur + j;
-                if (slot >= p.capacity) slot -= p.capacity;
-                ring_write_row(p.ring + slot * p.rs, p.rs, D, p.sw, lane, j, p.pend_s, p.pend_a,
-                               p.pend_r, p.pend_s2, p.pend_done, p.pend_err);
             }
         }
         trace_.mark(2);
@@ -783,6 +775,19 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
     const int hd_tasks = ((N1 + HD_U - 1) / HD_U) * hd_passes;
     const int n_hd = (hd_tasks + 1) * p.nsb;
     const int ntasks = n_w + n_h + n_hd;
+    // the deferred insert's ring rows (no sampled row of this step reads them from the ring;
+    // the next step's K1 follows K4): written by the first CTAs -- dW1 tasks, the shortest --
+    // after their task, so the (possibly PCIe) source loads stay off the critical path
+    auto write_pending = [&]() {
+        if (!p.pend_k) return;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = F_NT3 / 32;
+        for (int j = blockIdx.x * nw + warp; j < p.pend_k; j += gridDim.x * nw) {
+            int64_t slot = p.pend_cur + j;
+            if (slot >= p.capacity) slot -= p.capacity;
+            ring_write_row(p.ring + slot * p.rs, p.rs, p.D, p.sw, lane, j, p.pend_s, p.pend_a,
+                           p.pend_r, p.pend_s2, p.pend_done, p.pend_err);
+        }
+    };
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
         if (t < n_w) {
             // dW1[u][k] = sum_b dZ1[b][u] H0[b][k]  (+ db1[u] = sum_b dZ1[b][u])
@@ -939,6 +944,7 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             }
         }
     }
+    write_pending();
 }
 
 // ------------------------------------------------------------------------------------------
