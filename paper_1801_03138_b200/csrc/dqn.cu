@@ -764,6 +764,8 @@ struct rpl_dqn {
     bool k3_pdl = true;                    // K3 programmatic after K2
     bool k2_pdl = false, k4_pdl = false;   // experiments: RPL_K2PDL=1, RPL_K4PDL=1
     bool wide_tc = false;                  // byte-state wide inputs: layer 0 on tcgen05 (wide.cuh)
+    bool wide_fast = false;                // ... and the layers above it on the fast kernels
+    float *PdH0 = nullptr;                 // wide_fast: K3's dH0 partials [32][max_batch][N0]
     uint16_t *w0bf = nullptr;              // bf16 planes of W0 [online, target][3][N0 * D]
     uint16_t *dz0bf = nullptr;             // bf16 planes of dZ0 [3][max_batch][N0]
     bool w0bf_stale = true;                // planes to be re-split from the fp32 weights
@@ -875,9 +877,9 @@ static fwd_fn fast_fwd_fn(const rpl_dqn *d)
     if (ut == 64) return fast_fwd_kernel<64, 0, 0, 0>;
     return fast_fwd_kernel<32, 0, 0, 0>;
 }
-static size_t fast_fwd_smem(const rpl_dqn *d, int ut)
+static size_t fast_fwd_smem(const rpl_dqn *d, int ut, int D = -1)
 {
-    const FwdLayout L(d->cfg.state_dim, d->N[0], ut, d->J);
+    const FwdLayout L(D < 0 ? d->cfg.state_dim : D, d->N[0], ut, d->J);
     return (size_t)L.total * sizeof(float);
 }
 static size_t fast_td_smem(const rpl_dqn *d)
@@ -1005,6 +1007,27 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
     if (ok && tr && tr[0] == '1') {
         ok = dalloc(d, &d->trace, 4 * 2048 * 8);
         if (ok) cudaMemset(d->trace, 0, 4 * 2048 * 8 * sizeof(unsigned long long));
+    }
+    // wide byte-state inputs: the fast kernels run the layers above the tensor-core layer 0
+    {
+        const char *nf = getenv("RPL_NO_WIDE_FAST");
+        d->wide_fast = ok && d->wide_tc && d->T == 2 && d->N[0] % 4 == 0 && d->J <= F_MAXJ &&
+                       d->N[1] % 4 == 0 && (!cfg->dueling || cfg->stream % 4 == 0) &&
+                       fast_ut_cfg(*cfg, d->N[1]) > 0 && Bm <= WD_MAXN &&
+                       !(path && strcmp(path, "generic") == 0) && !(nf && nf[0] == '1');
+        if (d->wide_fast) {
+            const int ut = fast_ut(d);
+            const int nut = (d->N[1] + ut - 1) / ut;
+            d->part_elems = (int64_t)nets * nut * Bm * d->J;
+            ok = dalloc(d, &d->part, d->part_elems) && dalloc(d, &d->PdH0, (size_t)32 * Bm * d->N[0]);
+            ok = ok && cudaFuncSetAttribute(fast_fwd_fn(d), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            fast_fwd_smem(d, ut, 0)) == cudaSuccess &&
+                 cudaFuncSetAttribute(fast_bwd1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      K3_SMEM_FLOATS * sizeof(float)) == cudaSuccess &&
+                 fast_td_smem(d) <= 200 * 1024 &&
+                 cudaFuncSetAttribute(fast_td_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      fast_td_smem(d)) == cudaSuccess;
+        }
     }
     if (ok && d->fast) {
         const int ut = fast_ut(d);
@@ -1267,7 +1290,7 @@ static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
     const int ncombo = p.nets * p.nut;
     int g1 = std::min(k1_tasks, d->sms);
     if (k1_tasks > d->sms && ncombo <= d->sms) g1 = (d->sms / ncombo) * ncombo;
-    const size_t sm1 = fast_fwd_smem(d, p.UT);
+    const size_t sm1 = fast_fwd_smem(d, p.UT, p.D);
     const bool pdl = d->use_pdl;
     cudaError_t e;
     if (p.distinct) {   // distinct batch indices first (distinct.cuh)
@@ -1509,6 +1532,31 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                 return rc;
             }
         }
+        if (wide && d->wide_fast) {
+            // (3) layers above layer 0 on the fast kernels: H0 from the partials, then K1 (H0
+            // in), K2, K3 (dH0 partials out), K4 (dZ0 for step 4, every SGD but layer 0's)
+            wide_reduce_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->PF0, w.ks, p.nets, batch, d->N[0],
+                                                                   d->online, d->target, d->boff[0], d->H[0]);
+            FastArgs fp;
+            fill_fast(d, rp, batch, dp ? nullptr : loss_dev, dp ? 0 : 1, fp);
+            fp.D = 0;                 // K1 neither gathers nor computes layer 0
+            fp.distinct = 0;          // the batch was sampled by step (1)
+            fp.h0_in = d->H[0];       // [nets][B][N0] (the debug export's layer-0 activations)
+            fp.H0 = d->H[0];          // the online net's block [B][N0]
+            fp.PdH0 = d->PdH0;
+            fp.dZ0 = d->PF0;
+            fp.dZ0bf = d->dz0bf;
+            fp.NS = fast_ns(d, batch);
+            e = cudaGetLastError();
+            if (e == cudaSuccess) e = fast_enqueue(d, fp, d->stream);
+            if (e != cudaSuccess) {
+                if (prev >= 0) cudaSetDevice(prev);
+                return cuda_fail(e, "wide fast step");
+            }
+            g_launches.fetch_add(5);
+            w.do_db0 = 1;
+            w.b0 = d->boff[0];
+        } else {
         const int grid = grid_for(d, p);
         void *args[] = {&p};
         e = cudaLaunchCooperativeKernel((const void *)train_step_kernel, dim3(grid), dim3(NT), args,
@@ -1518,6 +1566,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             return cuda_fail(e, "cudaLaunchCooperativeKernel(train_step_kernel)");
         }
         g_launches.fetch_add(1);
+        }
         if (wide) {
             // (4) dW0 = dZ0^T x per 256-input tile, then its SGD / target sync
             wide_dw0_kernel<<<(unsigned)((p.D + WD_MAXN - 1) / WD_MAXN), WD_T, WD_SMEM, d->stream>>>(w);

@@ -23,6 +23,7 @@
 #include "mma_tf32.cuh"
 #include "ring_row.cuh"
 #include "distinct.cuh"
+#include "umma.cuh"
 
 namespace rpl {
 
@@ -80,6 +81,11 @@ struct FastArgs {
     int32_t *sync_flag;  // written by K2 (step t+1 is a sync step), read by K4 / sgd_kernel
     int apply_update;
     int distinct;        // 1: the batch indices come from distinct_fast_kernel (in idx)
+    // wide inputs (config 5): layer 0 runs in wide.cuh; the fast kernels run the layers above it
+    const float *h0_in;  // [nets][B][N0] layer-0 activations (K1 skips sample, gather, layer 0)
+    float *PdH0;         // [NS][B][N0] K3's dH0 split-K partials (no dW0 shares)
+    float *dZ0;          // [B][N0] dZ0 materialised by K4 for wide_dw0_kernel
+    uint16_t *dZ0bf;     // its bf16 hi / mid / lo planes [3][B][N0]
     uint32_t *err;
     unsigned long long *trace;   // optional per-CTA [kernel][cta][start, end] %globaltimer (ns)
 };
@@ -316,8 +322,10 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
                 if (u < nu) cp_async16(dst, theta + p.w1 + (int64_t)(u0 + u) * N0 + 4 * c);
                 else *reinterpret_cast<float4 *>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            cp_async_row(W0f, theta + p.w0, N0 * D, tid, F_NT1);
-            cp_async_row(b0s, theta + p.b0, N0, tid, F_NT1);
+            if (!p.h0_in) {
+                cp_async_row(W0f, theta + p.w0, N0 * D, tid, F_NT1);
+                cp_async_row(b0s, theta + p.b0, N0, tid, F_NT1);
+            }
             cp_async_row(b1s, theta + p.b1 + u0, nu, tid, F_NT1);
             for (int u = nu + tid; u < UT; u += F_NT1) b1s[u] = 0.0f;
         }
@@ -338,115 +346,131 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
                 else *reinterpret_cast<float4 *>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
-        // (2) Philox sample of the tile's rows (Q3)
-        if (tid < F_BT / 2) {
-            int32_t i0, i1;
-            if (p.distinct) {   // written by distinct_fast_kernel (rows past B: any valid slot)
-                i0 = rb + 2 * tid < B ? p.idx[rb + 2 * tid] : 0;
-                i1 = rb + 2 * tid + 1 < B ? p.idx[rb + 2 * tid + 1] : 0;
-            } else {
-                sample_pair(p.seed, p.rank, event, (uint32_t)(rb / 2 + tid), nvalid, i0, i1);
-                i0 = slot_of(i0, oldest, p.capacity);
-                i1 = slot_of(i1, oldest, p.capacity);
-            }
-            idxs[2 * tid] = i0;
-            idxs[2 * tid + 1] = i1;
-            // deferred-insert index of a slot (read-through), or -1
-            auto pend_j = [&](int64_t slot) {
-                int64_t j = slot - p.pend_cur;
-                if (j < 0) j += p.capacity;
-                return j < p.pend_k ? (int)j : -1;
-            };
-            pjs[2 * tid] = pend_j(i0);
-            pjs[2 * tid + 1] = pend_j(i1);
-            pjs2[2 * tid] = p.shared ? pend_j((i0 + 1) % p.capacity) : -1;
-            pjs2[2 * tid + 1] = p.shared ? pend_j((i1 + 1) % p.capacity) : -1;
-        }
-        __syncthreads();
-        // (3) gather the 16 sampled rows: s for online(s), s' for target(s') / online(s')
-        // shared states: s' is the old state of the next slot
-        const bool nxt = net != 0 && p.shared;
-        const int col0 = net == 0 || p.shared ? 0 : D;
-        for (int e = tid; e < F_BT * D; e += F_NT1) {
-            const int rr = e / D, d = e - rr * D, j = nxt ? pjs2[rr] : pjs[rr];
-            const int64_t slot = nxt ? (idxs[rr] + 1) % p.capacity : idxs[rr];
-            if (j < 0) {
-                cp_async4(Xs + rr * L.XP + d, p.ring + slot * p.rs + col0 + d);
-            } else {   // pending insert: its sources (possibly pinned host memory: plain loads)
-                Xs[rr * L.XP + d] = (net == 0 || p.shared ? p.pend_s : p.pend_s2)[(int64_t)j * D + d];
-            }
-        }
-        int32_t ra_ = 0;
-        float rr_ = 0.0f;
-        uint32_t rd_ = 0;
-        const bool unpack_scalars = net == 0 && ut == 0 && tid < F_BT && rb + tid < B;
-        if (unpack_scalars) {
-            const int j = pjs[tid];
-            if (j < 0) {
-                const float *row = p.ring + (int64_t)idxs[tid] * p.rs + p.sw;
-                ra_ = __float_as_int(__ldg(row));
-                rr_ = __ldg(row + 1);
-                rd_ = __float_as_uint(__ldg(row + 2));
-            } else {
-                ra_ = p.pend_a[j];
-                rr_ = p.pend_r[j];
-                rd_ = p.pend_done[j];
-            }
-        }
-        trace_.mark(2);
-        cp_async_wait_all();
-        __syncthreads();
-        trace_.mark(3);
-        // split X into tf32 hi / lo (zero beyond D); unpack the batch once for the backward
-        // pass and the debug export
-        for (int e = tid; e < F_BT * L.XP; e += F_NT1) {
-            const int rr = e / L.XP, d = e - rr * L.XP;
-            const float x = d < D ? Xs[e] : 0.0f;
-            uint32_t hi, lo;
-            tf32_split(x, hi, lo);
-            Xh[e] = hi;
-            Xl[e] = lo;
-            if (ut == 0 && net <= 1 && d < D && rb + rr < B)
-                (net == 0 ? p.Xs : p.Xs2)[(int64_t)(rb + rr) * D + d] = x;
-        }
-        if (unpack_scalars) {
-            p.idx[rb + tid] = idxs[tid];
-            p.a[rb + tid] = ra_;
-            p.r[rb + tid] = rr_;
-            p.done[rb + tid] = (uint8_t)(rd_ != 0u);
-        }
-        __syncthreads();
-        // (4) layer 0: H0[16][N0] = ReLU(X W0^T + b0)
-        for (int nt = warp; nt < N0 / 8; nt += NW) {
-            const int n = nt * 8 + g;
-            float c[4] = {0.f, 0.f, 0.f, 0.f};
-            for (int k0 = 0; k0 < D; k0 += 8) {
-                uint32_t ah[4], al[4], bh[2], bl[2];
-                ah[0] = Xh[g * L.XP + k0 + t];       al[0] = Xl[g * L.XP + k0 + t];
-                ah[1] = Xh[(g + 8) * L.XP + k0 + t]; al[1] = Xl[(g + 8) * L.XP + k0 + t];
-                ah[2] = Xh[g * L.XP + k0 + t + 4];   al[2] = Xl[g * L.XP + k0 + t + 4];
-                ah[3] = Xh[(g + 8) * L.XP + k0 + t + 4]; al[3] = Xl[(g + 8) * L.XP + k0 + t + 4];
-                const float w0 = k0 + t < D ? W0f[n * D + k0 + t] : 0.0f;
-                const float w1 = k0 + t + 4 < D ? W0f[n * D + k0 + t + 4] : 0.0f;
-                tf32_split(w0, bh[0], bl[0]);
-                tf32_split(w1, bh[1], bl[1]);
-                mma_3xtf32(c, ah, al, bh, bl);
-            }
-            const int col = nt * 8 + 2 * t;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int rr = g + (q >> 1) * 8, cc = col + (q & 1);
-                float h = c[q] + b0s[cc];
-                h = h > 0.0f ? h : 0.0f;
+        if (p.h0_in) {
+            // wide inputs: layer 0 came from the tensor-core kernels -- load the tile's H0 rows
+            // of this net and split them into tf32 hi / lo
+            const float *h0 = p.h0_in + ((int64_t)net * B + rb) * N0;
+            cp_async_wait_all();   // the weight tiles
+            for (int e = tid; e < F_BT * N0; e += F_NT1) {
+                const int rr = e / N0, cc = e - rr * N0;
+                const float h = rb + rr < B ? __ldcg(h0 + (int64_t)rr * N0 + cc) : 0.0f;
                 uint32_t hi, lo;
                 tf32_split(h, hi, lo);
                 H0h[rr * L.N0P + cc] = hi;
                 H0l[rr * L.N0P + cc] = lo;
-                if (net == 0 && ut == 0 && rb + rr < B) p.H0[(int64_t)(rb + rr) * N0 + cc] = h;
             }
+            __syncthreads();
+        } else {
+            // (2) Philox sample of the tile's rows (Q3)
+            if (tid < F_BT / 2) {
+                int32_t i0, i1;
+                if (p.distinct) {   // written by distinct_fast_kernel (rows past B: any valid slot)
+                    i0 = rb + 2 * tid < B ? p.idx[rb + 2 * tid] : 0;
+                    i1 = rb + 2 * tid + 1 < B ? p.idx[rb + 2 * tid + 1] : 0;
+                } else {
+                    sample_pair(p.seed, p.rank, event, (uint32_t)(rb / 2 + tid), nvalid, i0, i1);
+                    i0 = slot_of(i0, oldest, p.capacity);
+                    i1 = slot_of(i1, oldest, p.capacity);
+                }
+                idxs[2 * tid] = i0;
+                idxs[2 * tid + 1] = i1;
+                // deferred-insert index of a slot (read-through), or -1
+                auto pend_j = [&](int64_t slot) {
+                    int64_t j = slot - p.pend_cur;
+                    if (j < 0) j += p.capacity;
+                    return j < p.pend_k ? (int)j : -1;
+                };
+                pjs[2 * tid] = pend_j(i0);
+                pjs[2 * tid + 1] = pend_j(i1);
+                pjs2[2 * tid] = p.shared ? pend_j((i0 + 1) % p.capacity) : -1;
+                pjs2[2 * tid + 1] = p.shared ? pend_j((i1 + 1) % p.capacity) : -1;
+            }
+            __syncthreads();
+            // (3) gather the 16 sampled rows: s for online(s), s' for target(s') / online(s')
+            // shared states: s' is the old state of the next slot
+            const bool nxt = net != 0 && p.shared;
+            const int col0 = net == 0 || p.shared ? 0 : D;
+            for (int e = tid; e < F_BT * D; e += F_NT1) {
+                const int rr = e / D, d = e - rr * D, j = nxt ? pjs2[rr] : pjs[rr];
+                const int64_t slot = nxt ? (idxs[rr] + 1) % p.capacity : idxs[rr];
+                if (j < 0) {
+                    cp_async4(Xs + rr * L.XP + d, p.ring + slot * p.rs + col0 + d);
+                } else {   // pending insert: its sources (possibly pinned host memory: plain loads)
+                    Xs[rr * L.XP + d] = (net == 0 || p.shared ? p.pend_s : p.pend_s2)[(int64_t)j * D + d];
+                }
+            }
+            int32_t ra_ = 0;
+            float rr_ = 0.0f;
+            uint32_t rd_ = 0;
+            const bool unpack_scalars = net == 0 && ut == 0 && tid < F_BT && rb + tid < B;
+            if (unpack_scalars) {
+                const int j = pjs[tid];
+                if (j < 0) {
+                    const float *row = p.ring + (int64_t)idxs[tid] * p.rs + p.sw;
+                    ra_ = __float_as_int(__ldg(row));
+                    rr_ = __ldg(row + 1);
+                    rd_ = __float_as_uint(__ldg(row + 2));
+                } else {
+                    ra_ = p.pend_a[j];
+                    rr_ = p.pend_r[j];
+                    rd_ = p.pend_done[j];
+                }
+            }
+            trace_.mark(2);
+            cp_async_wait_all();
+            __syncthreads();
+            trace_.mark(3);
+            // split X into tf32 hi / lo (zero beyond D); unpack the batch once for the backward
+            // pass and the debug export
+            for (int e = tid; e < F_BT * L.XP; e += F_NT1) {
+                const int rr = e / L.XP, d = e - rr * L.XP;
+                const float x = d < D ? Xs[e] : 0.0f;
+                uint32_t hi, lo;
+                tf32_split(x, hi, lo);
+                Xh[e] = hi;
+                Xl[e] = lo;
+                if (ut == 0 && net <= 1 && d < D && rb + rr < B)
+                    (net == 0 ? p.Xs : p.Xs2)[(int64_t)(rb + rr) * D + d] = x;
+            }
+            if (unpack_scalars) {
+                p.idx[rb + tid] = idxs[tid];
+                p.a[rb + tid] = ra_;
+                p.r[rb + tid] = rr_;
+                p.done[rb + tid] = (uint8_t)(rd_ != 0u);
+            }
+            __syncthreads();
+            // (4) layer 0: H0[16][N0] = ReLU(X W0^T + b0)
+            for (int nt = warp; nt < N0 / 8; nt += NW) {
+                const int n = nt * 8 + g;
+                float c[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int k0 = 0; k0 < D; k0 += 8) {
+                    uint32_t ah[4], al[4], bh[2], bl[2];
+                    ah[0] = Xh[g * L.XP + k0 + t];       al[0] = Xl[g * L.XP + k0 + t];
+                    ah[1] = Xh[(g + 8) * L.XP + k0 + t]; al[1] = Xl[(g + 8) * L.XP + k0 + t];
+                    ah[2] = Xh[g * L.XP + k0 + t + 4];   al[2] = Xl[g * L.XP + k0 + t + 4];
+                    ah[3] = Xh[(g + 8) * L.XP + k0 + t + 4]; al[3] = Xl[(g + 8) * L.XP + k0 + t + 4];
+                    const float w0 = k0 + t < D ? W0f[n * D + k0 + t] : 0.0f;
+                    const float w1 = k0 + t + 4 < D ? W0f[n * D + k0 + t + 4] : 0.0f;
+                    tf32_split(w0, bh[0], bl[0]);
+                    tf32_split(w1, bh[1], bl[1]);
+                    mma_3xtf32(c, ah, al, bh, bl);
+                }
+                const int col = nt * 8 + 2 * t;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int rr = g + (q >> 1) * 8, cc = col + (q & 1);
+                    float h = c[q] + b0s[cc];
+                    h = h > 0.0f ? h : 0.0f;
+                    uint32_t hi, lo;
+                    tf32_split(h, hi, lo);
+                    H0h[rr * L.N0P + cc] = hi;
+                    H0l[rr * L.N0P + cc] = lo;
+                    if (net == 0 && ut == 0 && rb + rr < B) p.H0[(int64_t)(rb + rr) * N0 + cc] = h;
+                }
+            }
+            __syncthreads();
+            trace_.mark(4);
         }
-        __syncthreads();
-        trace_.mark(4);
         // (5) layer 1: H1[16][UT] = ReLU(H0 W1_tile^T + b1)
         for (int nt = warp; nt < UT / 8; nt += NW) {
             const float *wrow = W1s + (nt * 8 + g) * L.N0P;
@@ -810,6 +834,16 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             const int m0 = (rem / hnt) * BM, n0 = (rem % hnt) * K3N;
             const int chunk = (N1 + p.NS - 1) / p.NS;
             const int kb = s * chunk, ke = min(N1, kb + chunk);
+            if (p.PdH0) {
+                // wide inputs: the partial goes to memory; K4 forms dZ0, wide_dw0_kernel dW0
+                const Opnd a{p.dZ1, N1, B}, bo{p.online + p.w1, N0, N0};
+                float *out = p.PdH0 + (int64_t)s * B * N0;
+                auto epi = [&](int m, int n, float v) {
+                    if (m < B && n < N0) out[(int64_t)m * N0 + n] = v;
+                };
+                gemm_mma_tile<false, true>(a, bo, m0, n0, kb, ke, epi, false, NoRowsum{}, k3raw);
+                continue;
+            }
             // the partial dH0 tile stays in shared memory; masked by ReLU'(z0) it gives this
             // (split, batch tile)'s share of dW0 = dZ0^T X and db0 = sum_b dZ0 (the mask
             // distributes over the split-K sum), reduced in K4 in a fixed order
@@ -970,7 +1004,8 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
     // (2) W0, b0: the fixed-order sum of the (split, batch tile) partials written by K3.  A
     // CTA owns 32 consecutive elements; warp w sums partials q = w, w + 8, ... (compensated,
     // in order; coalesced 128-B loads), then the 8 warp sums are added in warp order.
-    const int64_t n0el = p.w1;                  // W0 and b0 lead the blob
+    // (wide inputs: W0 / b0 are wide_dw0_kernel's, which also gets dZ0 from here)
+    const int64_t n0el = p.PdH0 ? 0 : p.w1;     // W0 and b0 lead the blob
     const int nparts = p.NS * ((B + BM - 1) / BM);
     auto w0_partial = [&](int64_t i) {
         float g = 0.0f, comp = 0.0f;
@@ -1034,6 +1069,22 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
         __syncthreads();
         w0_finish(i0 + lane);
     }
+    if (p.PdH0) {
+        // wide inputs: dZ0 = ReLU'(z0) * (sum of K3's dH0 split-K partials, in split order)
+        // and its bf16 planes, for wide_dw0_kernel
+        const int64_t nz = (int64_t)B * p.N0;
+        for (int64_t i = (int64_t)blockIdx.x * NT + tid; i < nz; i += stride) {
+            float z = 0.0f;
+            for (int q = 0; q < p.NS; ++q) z += __ldcg(p.PdH0 + (int64_t)q * nz + i);
+            z = __ldcg(p.h0_in + i) > 0.0f ? z : 0.0f;
+            p.dZ0[i] = z;
+            uint16_t h, m, l;
+            umma::split3_bf16(z, h, m, l);
+            p.dZ0bf[i] = h;
+            p.dZ0bf[nz + i] = m;
+            p.dZ0bf[2 * nz + i] = l;
+        }
+    }
     trace_.mark(3);
     // (4) every other parameter: [w1, P), float4 where whole
     for (; e4 < n4; e4 += stride) {
@@ -1071,8 +1122,9 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
         p.grad[p.P] = loss;
         if (p.loss_out) *p.loss_out = loss;
         if (!ok) atomicOr(p.err, ERRBIT_NUMERIC);
-        // fire-and-forget reductions (no load round trip on the kernel's tail)
-        atomicAdd(reinterpret_cast<unsigned long long *>(p.rctrl), 1ull);   // sampler event consumed
+        // fire-and-forget reductions (no load round trip on the kernel's tail); with wide
+        // inputs the sampling gather has advanced the event already
+        if (!p.h0_in) atomicAdd(reinterpret_cast<unsigned long long *>(p.rctrl), 1ull);   // sampler event consumed
         atomicAdd(reinterpret_cast<unsigned long long *>(p.step_dev), 1ull); // executed train steps
     }
 }

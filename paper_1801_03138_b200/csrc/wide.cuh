@@ -53,6 +53,8 @@ struct WideArgs {
     float lr;
     int apply_update;
     const int32_t *sync_flag;
+    int64_t b0;                      // offset of b0 (the fast-path variant: db0 is this kernel's)
+    int do_db0;
 };
 
 // canonical no-swizzle offsets (umma.cuh): K-major rows x 64-deep slice, and MN-major
@@ -369,9 +371,47 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
             }
         }
     }
+    if (p.do_db0 && blockIdx.x * (WD_T / 32) < p.N0) {
+        // db0 = sum_b dZ0[b][u] (a warp per unit over the first CTAs, lanes stride the
+        // samples, fixed shuffle tree), and its SGD
+        const float loss = __ldcg(p.grad + p.P);
+        const bool upd = p.apply_update && isfinite(loss);
+        const bool sync = *p.sync_flag != 0;
+        for (int u = blockIdx.x * (WD_T / 32) + warp; u < p.N0 && u < (blockIdx.x + 1) * (WD_T / 32); u += WD_T / 32) {
+            float acc = 0.0f;
+            for (int bb = lane; bb < p.B; bb += 32) acc += __ldcg(p.dZ0 + (int64_t)bb * p.N0 + u);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+            if (lane == 0) {
+                p.grad[p.b0 + u] = acc;
+                if (upd) {
+                    const float w = p.online_w[p.b0 + u] - p.lr * acc;
+                    p.online_w[p.b0 + u] = w;
+                    if (sync) p.target_w[p.b0 + u] = w;
+                }
+            }
+        }
+    }
     umma::fence_before_sync();
     __syncthreads();
     if (warp == 0) umma::tmem_free(tmem, 256);
+}
+
+// wide inputs on the fast path: H0[net][b][u] = ReLU(b0_net[u] + sum of the wide_l0_kernel
+// partials in chunk order) for the fast kernels above layer 0
+__global__ void __launch_bounds__(256) wide_reduce_kernel(const float *__restrict__ PF0, int ks, int nets,
+                                                          int B, int N0, const float *online,
+                                                          const float *target, int64_t b0, float *H0)
+{
+    const int64_t per = (int64_t)B * N0, total = (int64_t)nets * per;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int net = (int)(i / per), u = (int)(i % N0);
+        float v = 0.0f;
+        for (int q = 0; q < ks; ++q) v += __ldcg(PF0 + (int64_t)q * total + i);
+        v += __ldg((net == 1 ? target : online) + b0 + u);
+        H0[i] = v > 0.0f ? v : 0.0f;
+    }
 }
 
 }  // namespace rpl

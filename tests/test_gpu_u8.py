@@ -64,14 +64,18 @@ def test_u8_insert_sample_gather_bit_exact(b, D):
     assert rp.check() == b.RPL_OK
 
 
-@pytest.mark.parametrize("path", ["tcgen05", "simt"])
+@pytest.mark.parametrize("path", ["tcgen05", "tcgen05-coop", "simt"])
 @pytest.mark.parametrize("ddqn", [False, True], ids=["dqn", "ddqn"])
 def test_u8_wide_input_train_step(b, ddqn, path, monkeypatch):
     # config 5 network: the paper's dueling MLP on an 84x84x4 byte input (28,224 -> 128 ->
     # V 512 / A 512 -> 1 + 8); layer 0 runs on the tensor cores (wide.cuh: bf16x3 split of
     # the fp32 operands, exact u8) or split-K on FP32 SIMT tiles (RPL_NO_WIDE_TC=1)
+    # tcgen05: layer 0 on the tensor cores, the layers above on the fast kernels;
+    # tcgen05-coop: the layers above on the cooperative kernel; simt: all on the cooperative kernel
     if path == "simt":
         monkeypatch.setenv("RPL_NO_WIDE_TC", "1")
+    if path == "tcgen05-coop":
+        monkeypatch.setenv("RPL_NO_WIDE_FAST", "1")
     D = ATARI_STATE_DIM
     cfg = b.DQNConfig(state_dim=D, n_actions=8, dueling=True, hidden=(128,), stream=512,
                       double_dqn=ddqn, gamma=0.99, lr=1e-3, huber_kappa=1.0, sync_period=2,
