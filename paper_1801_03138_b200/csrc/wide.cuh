@@ -371,13 +371,13 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
             }
         }
     }
-    if (p.do_db0 && blockIdx.x * (WD_T / 32) < p.N0) {
+    if (p.do_db0) {
         // db0 = sum_b dZ0[b][u] (a warp per unit over the first CTAs, lanes stride the
         // samples, fixed shuffle tree), and its SGD
         const float loss = __ldcg(p.grad + p.P);
         const bool upd = p.apply_update && isfinite(loss);
         const bool sync = *p.sync_flag != 0;
-        for (int u = blockIdx.x * (WD_T / 32) + warp; u < p.N0 && u < (blockIdx.x + 1) * (WD_T / 32); u += WD_T / 32) {
+        for (int u = blockIdx.x * (WD_T / 32) + warp; u < p.N0; u += gridDim.x * (WD_T / 32)) {
             float acc = 0.0f;
             for (int bb = lane; bb < p.B; bb += 32) acc += __ldcg(p.dZ0 + (int64_t)bb * p.N0 + u);
 #pragma unroll
