@@ -1569,7 +1569,9 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
         }
         if (wide) {
             // (4) dW0 = dZ0^T x per 256-input tile, then its SGD / target sync
-            wide_dw0_kernel<<<(unsigned)((p.D + WD_MAXN - 1) / WD_MAXN), WD_T, WD_SMEM, d->stream>>>(w);
+            // dW0 tiles: one wave over the SMs (28,224 inputs -> 147 tiles of 192)
+            w.ntile = (int)std::min<int64_t>(WD_MAXN, ((p.D + d->sms - 1) / d->sms + 15) / 16 * 16);
+            wide_dw0_kernel<<<(unsigned)((p.D + w.ntile - 1) / w.ntile), WD_T, WD_SMEM, d->stream>>>(w);
             e = cudaGetLastError();
             if (e != cudaSuccess) {
                 if (prev >= 0) cudaSetDevice(prev);

@@ -55,6 +55,7 @@ struct WideArgs {
     const int32_t *sync_flag;
     int64_t b0;                      // offset of b0 (the fast-path variant: db0 is this kernel's)
     int do_db0;
+    int ntile;                       // dW0 inputs per CTA (multiple of 16, <= 256)
 };
 
 // canonical no-swizzle offsets (umma.cuh): K-major rows x 64-deep slice, and MN-major
@@ -110,64 +111,81 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
     umma::fence_after_sync();
     const uint32_t tmem = tbase;
     const uint32_t idesc = umma::idesc_bf16(WD_M, N, false, false);
+    // software pipeline over the K slices: slice sl + 1's weight planes (cp.async group) and
+    // byte states (registers) are in flight while slice sl is converted and multiplied; a
+    // stage is refilled once the MMAs that read it two slices earlier have committed
+    const int64_t nd = (int64_t)p.N0 * p.D;
+    const uint16_t *Wp = p.W0bf + (net == 1 ? 3 * nd : 0);
+    auto issue_A = [&](int sl) {
+        // the hi / mid / lo planes of W0[u][k0 .. k0+63] (K-major), 16-byte copies of 8 k
+        uint8_t *A = sm + (sl & 1) * WD_STAGE;
+        const int64_t k0 = kb + (int64_t)sl * WD_KS;
+        for (int e = tid; e < 3 * WD_M * (WD_KS / 8); e += WD_T) {
+            const int pl = e / (WD_M * (WD_KS / 8)), r = e % (WD_M * (WD_KS / 8));
+            const int u = r / (WD_KS / 8), k = 8 * (r % (WD_KS / 8));
+            const bool v = u < p.N0 && k0 + k < ke;
+            wd_cp16(A + pl * WD_A_PLANE + wd_off_k(u, k), v ? Wp + pl * nd + (int64_t)u * p.D + k0 + k : Wp, v);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const int totalB = N * (WD_KS / 16);   // 16-byte pieces of a slice's states (<= 4 per thread)
+    auto load_B = [&](int sl, uint4 v[4]) {
+        const int64_t k0 = kb + (int64_t)sl * WD_KS;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = tid + q * WD_T;
+            v[q] = make_uint4(0u, 0u, 0u, 0u);
+            if (e >= totalB) continue;
+            const int b = e / (WD_KS / 16), k = 16 * (e % (WD_KS / 16));
+            if (b < p.B) {
+                const uint8_t *src = U + (int64_t)b * p.D + k0 + k;
+                if (k0 + k + 15 < ke && ((uintptr_t)src & 15) == 0) {
+                    v[q] = __ldg(reinterpret_cast<const uint4 *>(src));
+                } else {
+                    uint8_t t[16];
+                    for (int i = 0; i < 16; ++i) t[i] = (k0 + k + i < ke) ? src[i] : 0;
+                    v[q] = make_uint4(t[0] | t[1] << 8 | t[2] << 16 | (uint32_t)t[3] << 24,
+                                      t[4] | t[5] << 8 | t[6] << 16 | (uint32_t)t[7] << 24,
+                                      t[8] | t[9] << 8 | t[10] << 16 | (uint32_t)t[11] << 24,
+                                      t[12] | t[13] << 8 | t[14] << 16 | (uint32_t)t[15] << 24);
+                }
+            }
+        }
+    };
+    auto store_B = [&](int sl, const uint4 v[4]) {   // u8 -> bf16, K-major
+        uint8_t *Bs = sm + (sl & 1) * WD_STAGE + 3 * WD_A_PLANE;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = tid + q * WD_T;
+            if (e >= totalB) continue;
+            const int b = e / (WD_KS / 16), k = 16 * (e % (WD_KS / 16));
+            const uint32_t w4[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+            uint32_t o8[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                o8[2 * i] = pack2(u8_bf16(w4[i] & 0xFF), u8_bf16((w4[i] >> 8) & 0xFF));
+                o8[2 * i + 1] = pack2(u8_bf16((w4[i] >> 16) & 0xFF), u8_bf16(w4[i] >> 24));
+            }
+            *reinterpret_cast<uint4 *>(Bs + wd_off_k(b, k)) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
+            *reinterpret_cast<uint4 *>(Bs + wd_off_k(b, k + 8)) = make_uint4(o8[4], o8[5], o8[6], o8[7]);
+        }
+    };
+    uint4 vb[4], vn[4];
+    issue_A(0);
+    load_B(0, vb);
     for (int sl = 0; sl < nsl; ++sl) {
         const int st = sl & 1;
         uint8_t *A = sm + st * WD_STAGE, *Bs = A + 3 * WD_A_PLANE;
-        if (sl >= 2) umma::mbar_wait(&mbar[st], ((sl - 2) >> 1) & 1);   // MMAs of slice sl-2 done
-        const int64_t k0 = kb + (int64_t)sl * WD_KS;
-        // A: the hi / mid / lo planes of W0[u][k0 .. k0+63] (K-major), 16-byte copies of 8 k
-        {
-            const int64_t nd = (int64_t)p.N0 * p.D;
-            const uint16_t *Wp = p.W0bf + (net == 1 ? 3 * nd : 0);
-            for (int e = tid; e < 3 * WD_M * (WD_KS / 8); e += WD_T) {
-                const int pl = e / (WD_M * (WD_KS / 8)), r = e % (WD_M * (WD_KS / 8));
-                const int u = r / (WD_KS / 8), k = 8 * (r % (WD_KS / 8));
-                const bool v = u < p.N0 && k0 + k < ke;
-                wd_cp16(A + pl * WD_A_PLANE + wd_off_k(u, k), v ? Wp + pl * nd + (int64_t)u * p.D + k0 + k : Wp, v);
-            }
+        store_B(sl, vb);   // stage st was freed before A(sl) was issued
+        if (sl + 1 < nsl) {
+            // the other stage last fed the MMAs of slice sl - 1: wait for them, then refill it
+            if (sl >= 1) umma::mbar_wait(&mbar[st ^ 1], ((sl - 1) >> 1) & 1);
+            issue_A(sl + 1);
+            load_B(sl + 1, vn);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");   // A(sl) has landed
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-        // B: U[b][k0 .. k0+63] u8 -> bf16 (K-major), 16 bytes per thread-step; every load of
-        // the slice is issued before the first conversion (at most 4 per thread: N <= 256)
-        {
-            const int total = N * (WD_KS / 16);
-            uint4 v[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int e = tid + q * WD_T;
-                v[q] = make_uint4(0u, 0u, 0u, 0u);
-                if (e >= total) continue;
-                const int b = e / (WD_KS / 16), k = 16 * (e % (WD_KS / 16));
-                if (b < p.B) {
-                    const uint8_t *src = U + (int64_t)b * p.D + k0 + k;
-                    if (k0 + k + 15 < ke && ((uintptr_t)src & 15) == 0) {
-                        v[q] = __ldg(reinterpret_cast<const uint4 *>(src));
-                    } else {
-                        uint8_t t[16];
-                        for (int i = 0; i < 16; ++i) t[i] = (k0 + k + i < ke) ? src[i] : 0;
-                        v[q] = make_uint4(t[0] | t[1] << 8 | t[2] << 16 | (uint32_t)t[3] << 24,
-                                          t[4] | t[5] << 8 | t[6] << 16 | (uint32_t)t[7] << 24,
-                                          t[8] | t[9] << 8 | t[10] << 16 | (uint32_t)t[11] << 24,
-                                          t[12] | t[13] << 8 | t[14] << 16 | (uint32_t)t[15] << 24);
-                    }
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int e = tid + q * WD_T;
-                if (e >= total) continue;
-                const int b = e / (WD_KS / 16), k = 16 * (e % (WD_KS / 16));
-                const uint32_t w4[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
-                uint32_t o8[8];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    o8[2 * i] = pack2(u8_bf16(w4[i] & 0xFF), u8_bf16((w4[i] >> 8) & 0xFF));
-                    o8[2 * i + 1] = pack2(u8_bf16((w4[i] >> 16) & 0xFF), u8_bf16(w4[i] >> 24));
-                }
-                *reinterpret_cast<uint4 *>(Bs + wd_off_k(b, k)) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
-                *reinterpret_cast<uint4 *>(Bs + wd_off_k(b, k + 8)) = make_uint4(o8[4], o8[5], o8[6], o8[7]);
-            }
-        }
-        wd_cp_wait();
         umma::fence_async_smem();
         umma::fence_before_sync();
         __syncthreads();
@@ -182,6 +200,8 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
             }
             umma::commit(&mbar[st]);
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) vb[q] = vn[q];
     }
     // the last slice's commit covers every earlier MMA
     {
@@ -217,8 +237,8 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
     __shared__ uint64_t mbar[2];
     __shared__ uint32_t tbase;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t n0 = (int64_t)blockIdx.x * WD_MAXN;                  // first input of the tile
-    const int nn = (int)(p.D - n0 < WD_MAXN ? p.D - n0 : WD_MAXN);    // inputs in the tile
+    const int64_t n0 = (int64_t)blockIdx.x * p.ntile;                  // first input of the tile
+    const int nn = (int)(p.D - n0 < p.ntile ? p.D - n0 : p.ntile);    // inputs in the tile
     const int N = (nn + 15) & ~15;
     const int nsl = (p.B + WD_KS - 1) / WD_KS;
     if (warp == 0) umma::tmem_alloc(&tbase, 256);
