@@ -171,6 +171,12 @@ typedef struct {
     int64_t sync_period;  /* target <- online after step t when t % period == 0;
                              0 = only on sync_target()                                       */
     int32_t max_batch;    /* largest batch dqn_train_step accepts (sizes the workspaces)    */
+    int64_t avg_period;   /* data-parallel learners (dqn_attach_nccl): 0 = the gradient is
+                             averaged over ranks every step ("synchronized every train
+                             step"); K > 0 = each rank applies its own SGD and the online and
+                             target parameters are averaged over ranks after every K-th step
+                             (P:144's "synchronized periodically" / iterative parameter
+                             mixing, reading Q31)                                           */
 } rpl_dqn_config;
 
 /* Number of fp32 parameters of the blob layout:

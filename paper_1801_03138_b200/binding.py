@@ -61,7 +61,7 @@ class _DqnConfig(C.Structure):
                 ("n_actions", C.c_int32), ("dueling", C.c_int32), ("n_hidden", C.c_int32),
                 ("hidden", C.c_int32 * 4), ("stream", C.c_int32), ("double_dqn", C.c_int32),
                 ("gamma", C.c_float), ("lr", C.c_float), ("huber_kappa", C.c_float),
-                ("sync_period", C.c_int64), ("max_batch", C.c_int32)]
+                ("sync_period", C.c_int64), ("max_batch", C.c_int32), ("avg_period", C.c_int64)]
 
 
 def _load():
@@ -273,6 +273,7 @@ class DQNConfig:
     huber_kappa: float = 1.0
     sync_period: int = 10_000
     max_batch: int = 4096
+    avg_period: int = 0       # DP: 0 = gradient mean every step; K = parameter mean every K steps
 
     def _c(self, device=0, stream=None) -> _DqnConfig:
         c = _DqnConfig()
@@ -286,6 +287,7 @@ class DQNConfig:
         c.double_dqn = int(self.double_dqn)
         c.gamma, c.lr, c.huber_kappa = self.gamma, self.lr, self.huber_kappa
         c.sync_period, c.max_batch = self.sync_period, self.max_batch
+        c.avg_period = self.avg_period
         return c
 
     @property

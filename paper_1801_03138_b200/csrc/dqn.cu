@@ -1350,7 +1350,9 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
     cudaSetDevice(d->device);
     const int64_t t = d->steps + 1;
     const int do_sync = d->cfg.sync_period > 0 && t % d->cfg.sync_period == 0;
-    const bool dp = d->comm != nullptr && d->world > 1;
+    // data parallel: per-step gradient mean (dp), or local SGD + periodic parameter mean (avg)
+    const bool avg = d->comm != nullptr && d->world > 1 && d->cfg.avg_period > 0;
+    const bool dp = d->comm != nullptr && d->world > 1 && !avg;
     cudaError_t e = cudaSuccess;
     // a deferred insert is consumed by the fast path's K1 on the shared stream; otherwise it
     // is written now by the insert kernel
@@ -1598,6 +1600,18 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
         }
         g_launches.fetch_add(1);
         if (loss_dev) cudaMemcpyAsync(loss_dev, d->grad + d->P, sizeof(float), cudaMemcpyDeviceToDevice, d->stream);
+    }
+    if (avg && t % d->cfg.avg_period == 0) {
+        // iterative parameter mixing (reading Q31): online and target <- their mean over ranks
+        for (float *w : {d->online, d->target}) {
+            int nr = g_nccl.allreduce(w, w, (size_t)d->P, kNcclFloat, kNcclAvg, d->comm, d->stream);
+            if (nr != 0) {
+                set_error("ncclAllReduce failed: %s", g_nccl.errstr ? g_nccl.errstr(nr) : "?");
+                if (prev >= 0) cudaSetDevice(prev);
+                return RPL_ENCCL;
+            }
+        }
+        d->w0bf_stale = true;
     }
     (void)do_sync;
     if (prev >= 0) cudaSetDevice(prev);

@@ -104,3 +104,59 @@ def test_world2_distinct_shards_replicas_identical_and_mean_rule():
         gs.append(oracle.dqn_loss_grad(NET, w0, w0, batch, 0.99, 1.0, False)["grad"])
     assert not np.array_equal(gs[0], gs[1])      # the shards really differ
     assert not np.array_equal(out[0], _single(0))
+
+
+# ---- periodic parameter averaging ("each GPU could have its own model that is
+# synchronized periodically ... iterative parameter mixing"; avg_period, reading Q31) ----
+AVG_K = 2
+
+
+def _mixing_steps(rank, world, out):
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ring = oracle.Ring(500, 27)
+    ring.add(**experiences(500, seed=1, rank=rank))
+    w = init_params(27, 8, (64, 64), False, seed=3).astype(np.float32)
+    tg = w.copy()
+    hist, same = [], []
+    for step in range(1, STEPS + 1):
+        rc, batch = ring.sample(1, 2, rank, B)
+        o = oracle.dqn_loss_grad(NET, w, tg, batch, 0.99, 1.0, False)
+        w = oracle.sgd(w, o["grad"], 1e-2).astype(np.float32)          # local SGD
+        if step % AVG_K == 0:                                           # mean over ranks
+            for arr in (w, tg):
+                t = torch.from_numpy(arr)
+                dist.all_reduce(t, op=dist.ReduceOp.SUM)
+                arr[...] = (t / world).numpy()
+        gathered = [torch.zeros_like(torch.from_numpy(w)) for _ in range(world)]
+        dist.all_gather(gathered, torch.from_numpy(w))
+        same.append(all(np.array_equal(x.numpy(), w) for x in gathered))
+        hist.append(w.copy())
+    out[rank] = (hist, same)
+    dist.destroy_process_group()
+
+
+def test_world2_periodic_parameter_averaging():
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_mixing_steps, args=(2, out), nprocs=2, join=True)
+        res = {k: v for k, v in out.items()}
+    # replicas agree exactly right after every mixing step and differ in between
+    for step, same in enumerate(res[0][1], start=1):
+        assert same == (step % AVG_K == 0), step
+    # the first mixed weights are the mean of the two ranks' local trajectories
+    local = []
+    for r in (0, 1):
+        ring = oracle.Ring(500, 27)
+        ring.add(**experiences(500, seed=1, rank=r))
+        w = init_params(27, 8, (64, 64), False, seed=3).astype(np.float32)
+        tg = w.copy()
+        for _ in range(AVG_K):
+            rc, batch = ring.sample(1, 2, r, B)
+            w = oracle.sgd(w, oracle.dqn_loss_grad(NET, w, tg, batch, 0.99, 1.0, False)["grad"],
+                           1e-2).astype(np.float32)
+        local.append(w)
+    assert not np.array_equal(local[0], local[1])
+    np.testing.assert_array_equal(res[0][0][AVG_K - 1], (local[0] + local[1]) / np.float32(2))
