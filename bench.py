@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-gather", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--sweep", default="", help="comma list of batch sizes: one JSON line each")
+    ap.add_argument("--avg-period", type=int, default=0,
+                    help="N > 1: average parameters every K steps instead of gradients every step")
     ap.add_argument("--shared-state", action="store_true",
                     help="store one state per experience (P:141): s' = the next slot's s")
     ap.add_argument("--distinct", action="store_true",
@@ -76,10 +78,11 @@ def make_cfg(a, binding, batch):
     if a.net == "dueling":
         return binding.DQNConfig(state_dim=27, n_actions=8, dueling=True, hidden=(128,), stream=512,
                                  double_dqn=a.ddqn, gamma=0.99, lr=1e-4, huber_kappa=1.0,
-                                 sync_period=10_000, max_batch=max(batch, 128))
+                                 sync_period=10_000, max_batch=max(batch, 128),
+                                 avg_period=a.avg_period)
     return binding.DQNConfig(state_dim=27, n_actions=8, dueling=False, hidden=(64, 64),
                              double_dqn=a.ddqn, gamma=0.99, lr=1e-4, huber_kappa=1.0,
-                             sync_period=10_000, max_batch=max(batch, 128))
+                             sync_period=10_000, max_batch=max(batch, 128), avg_period=a.avg_period)
 
 
 def oracle_net_of(cfg):
@@ -465,7 +468,8 @@ def run_ours(a, batch, first_line=True):
                    "net": a.net, "double_dqn": a.ddqn, "adds_per_step": k,
                    "sampling": "distinct" if a.distinct else "uniform (with replacement, P:75)",
                    "state_storage": "shared (s' = next slot's s, P:141)" if a.shared_state else "s and s' per row",
-                   "parallelism": f"dp{world}",
+                   "parallelism": f"dp{world}" + (f", parameters averaged every {a.avg_period} steps"
+                                                  if a.avg_period and world > 1 else ""),
                    "l2": "inputs larger than L2: the 256 MB ring (> 126 MB L2) is sampled uniformly;"
                          " the 0.56 MB weights stay L2-resident as in steady-state training"},
         "samples_per_s": value * batch,
