@@ -1351,8 +1351,8 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
     const int64_t t = d->steps + 1;
     const int do_sync = d->cfg.sync_period > 0 && t % d->cfg.sync_period == 0;
     // data parallel: per-step gradient mean (dp), or local SGD + periodic parameter mean (avg)
-    const bool avg = d->comm != nullptr && d->world > 1 && d->cfg.avg_period > 0;
-    const bool dp = d->comm != nullptr && d->world > 1 && !avg;
+    const bool avg = d->comm != nullptr && d->cfg.avg_period > 0;
+    const bool dp = d->comm != nullptr && !avg;
     cudaError_t e = cudaSuccess;
     // a deferred insert is consumed by the fast path's K1 on the shared stream; otherwise it
     // is written now by the insert kernel
@@ -1744,7 +1744,11 @@ extern "C" int dqn_attach_nccl(rpl_dqn *d, int32_t rank, int32_t world, const vo
         set_error("dqn_attach_nccl: already attached");
         return RPL_ESTATE;
     }
-    if (world == 1) return RPL_OK;
+    // a world of one needs no communicator -- unless RPL_DP_FORCE=1 (tests run the whole NCCL
+    // path, all-reduces over a single rank included, on one GPU)
+    const char *ff = getenv("RPL_DP_FORCE");
+    const bool force = ff && ff[0] == '1';
+    if (world == 1 && !force) return RPL_OK;
     int rc = nccl_load();
     if (rc != RPL_OK) return rc;
     nccl_uid id;

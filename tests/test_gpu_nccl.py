@@ -1,0 +1,50 @@
+"""The NCCL data-parallel path of dqn_train_step on one GPU (RPL_DP_FORCE=1 builds a
+communicator of one rank): the library loads NCCL, creates the communicator from a unique id,
+all-reduces (mean) the gradient + loss word every step and applies the SGD after it
+(P:144), or averages the parameters every K steps (reading Q31).  Over a single rank the
+means are identities, so the parameters must equal an unattached learner's bit for bit.
+"""
+import numpy as np
+import pytest
+
+from inputs import experiences, init_params
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def b():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_1801_03138_b200.binding as binding
+    return binding
+
+
+@pytest.mark.parametrize("avg_period", [0, 3])
+@pytest.mark.parametrize("net", ["fast", "generic"])
+def test_nccl_single_rank_equals_local(b, monkeypatch, avg_period, net):
+    import torch
+    if net == "generic":
+        monkeypatch.setenv("RPL_PATH", "generic")
+    cfg = b.DQNConfig(max_batch=128, sync_period=4, avg_period=avg_period, double_dqn=True,
+                      lr=1e-3)
+    p0 = init_params(27, 8, (128,), True, 512, seed=3)
+    e = experiences(2000, seed=1)
+    runs = []
+    for attach in (False, True):
+        monkeypatch.setenv("RPL_DP_FORCE", "1" if attach else "0")
+        rp = b.Replay(2000, 27, seed=4)
+        rp.add_many(e)
+        dqn = b.DQN(cfg, p0)
+        if attach:
+            dqn.attach_nccl(0, 1, b.nccl_unique_id())
+        loss = torch.zeros(1, device="cuda")
+        for _ in range(7):
+            assert dqn.train_step(rp, 128, loss) == b.RPL_OK
+        torch.cuda.synchronize()
+        assert dqn.check() == b.RPL_OK and np.isfinite(loss.item())
+        runs.append((dqn.get_params(b.RPL_ONLINE), dqn.get_params(b.RPL_TARGET), loss.item()))
+    assert np.array_equal(runs[0][0], runs[1][0])
+    assert np.array_equal(runs[0][1], runs[1][1])
+    assert runs[0][2] == runs[1][2]
