@@ -77,6 +77,7 @@ struct TrainArgs {
     float *loss_out;
     int apply_update, do_sync;
     int wide_tc;           // layer 0 (forward partials, dW0 + its SGD) runs in wide.cuh kernels
+                           // (its partials are x 255: phase_l0_reduce divides the sum)
     int distinct;          // batch indices precomputed by distinct_kernel into idx
     uint16_t *dZ0bf;       // wide_tc: bf16 hi / mid / lo planes of dZ0 [3][B][N0]
     unsigned long long *trace;   // RPL_TRACE=1: per-phase %globaltimer of CTA 0 (else null)
@@ -329,6 +330,7 @@ __device__ void phase_l0_reduce(const TrainArgs &p)
         const int net = (int)(i / per_net), n = (int)(i % N);
         float v = 0.0f;
         for (int q = 0; q < p.ks0; ++q) v += __ldcg(p.PF0 + (int64_t)q * total + i);
+        if (p.wide_tc) v = v / 255.0f;   // tensor-core partials carry u, not u / 255
         v += __ldg(net_params(p, net) + p.boff[0] + n);
         p.H[0][i] = v > 0.0f ? v : 0.0f;
     }

@@ -10,8 +10,8 @@
 //
 //   wide_l0_kernel : Z0 partials.  CTA (net, k-chunk) computes D[128 units][B] =
 //                    W0_net[:, chunk] . U_net[:, chunk]^T (A = W0 K-major, B = U K-major) and
-//                    writes it to PF0[chunk][net][b][unit]; the cooperative train kernel adds
-//                    the chunks in order (+ bias, ReLU) -- the split-K layout of phase_l0_reduce.
+//                    writes it (still x 255) to PF0[chunk][net][b][unit]; the reduction adds the
+//                    chunks in order, divides by 255 once, adds the bias and applies the ReLU.
 //   wide_dw0_kernel: dW0 tile [128 units][256 inputs] = dZ0^T U over the batch (A = dZ0^T
 //                    MN-major, B = U^T MN-major), then g = D / 255 -> grad, SGD (and the target
 //                    sync) of those W0 entries: layer 0's gradient never makes a round trip.
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
             umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + c, v);
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-                if (c + i < p.B && u < p.N0) out[(int64_t)(c + i) * p.N0 + u] = v[i] / 255.0f;
+                if (c + i < p.B && u < p.N0) out[(int64_t)(c + i) * p.N0 + u] = v[i];   // x 255
         }
     }
     umma::fence_before_sync();
@@ -356,39 +356,57 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
         const bool upd = p.apply_update && isfinite(loss);
         const bool sync = *p.sync_flag != 0;
         const int64_t nd = (int64_t)p.N0 * p.D;
-        for (int u = warp; u < p.N0; u += WD_T / 32) {
-            for (int c = 4 * lane; c < nn; c += 128) {
-                const int64_t j = (int64_t)u * p.D + n0 + c;   // index within W0
-                const int64_t wi = p.w0 + j;
-                const float4 t = *reinterpret_cast<const float4 *>(T + u * TS + c);
-                const float4 g = make_float4(t.x / 255.0f, t.y / 255.0f, t.z / 255.0f, t.w / 255.0f);
-                *reinterpret_cast<float4 *>(p.grad + wi) = g;
-                if (!upd) continue;
-                float4 w = *reinterpret_cast<const float4 *>(p.online_w + wi);
-                w.x -= p.lr * g.x;
-                w.y -= p.lr * g.y;
-                w.z -= p.lr * g.z;
-                w.w -= p.lr * g.w;
-                *reinterpret_cast<float4 *>(p.online_w + wi) = w;
-                // the next step's forward operand: W0's bf16 planes, split once here
-                uint16_t h[4], m[4], l[4];
-                umma::split3_bf16(w.x, h[0], m[0], l[0]);
-                umma::split3_bf16(w.y, h[1], m[1], l[1]);
-                umma::split3_bf16(w.z, h[2], m[2], l[2]);
-                umma::split3_bf16(w.w, h[3], m[3], l[3]);
-                const uint2 ph = make_uint2(pack2(h[0], h[1]), pack2(h[2], h[3]));
-                const uint2 pm = make_uint2(pack2(m[0], m[1]), pack2(m[2], m[3]));
-                const uint2 pl = make_uint2(pack2(l[0], l[1]), pack2(l[2], l[3]));
-                *reinterpret_cast<uint2 *>(p.W0bf + j) = ph;
-                *reinterpret_cast<uint2 *>(p.W0bf + nd + j) = pm;
-                *reinterpret_cast<uint2 *>(p.W0bf + 2 * nd + j) = pl;
-                if (sync) {
-                    *reinterpret_cast<float4 *>(p.target_w + wi) = w;
-                    *reinterpret_cast<uint2 *>(p.W0bf + 3 * nd + j) = ph;
-                    *reinterpret_cast<uint2 *>(p.W0bf + 4 * nd + j) = pm;
-                    *reinterpret_cast<uint2 *>(p.W0bf + 5 * nd + j) = pl;
+        // a warp walks rows w, w + 8, ... four at a time: their weight loads (<= 8 float4 per
+        // lane) are all in flight before the first update
+        constexpr int NWE = WD_T / 32;
+        for (int ub = warp; ub < p.N0; ub += 4 * NWE) {
+            float4 wv[4][2];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int u = ub + r * NWE, c = 4 * lane + 128 * cc;
+                    wv[r][cc] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (upd && u < p.N0 && c < nn)
+                        wv[r][cc] = *reinterpret_cast<const float4 *>(p.online_w + p.w0 + (int64_t)u * p.D + n0 + c);
                 }
-            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int u = ub + r * NWE, c = 4 * lane + 128 * cc;
+                    if (u >= p.N0 || c >= nn) continue;
+                    const int64_t j = (int64_t)u * p.D + n0 + c;   // index within W0
+                    const int64_t wi = p.w0 + j;
+                    const float4 t = *reinterpret_cast<const float4 *>(T + u * TS + c);
+                    const float4 g = make_float4(t.x / 255.0f, t.y / 255.0f, t.z / 255.0f, t.w / 255.0f);
+                    *reinterpret_cast<float4 *>(p.grad + wi) = g;
+                    if (!upd) continue;
+                    float4 w = wv[r][cc];
+                    w.x -= p.lr * g.x;
+                    w.y -= p.lr * g.y;
+                    w.z -= p.lr * g.z;
+                    w.w -= p.lr * g.w;
+                    *reinterpret_cast<float4 *>(p.online_w + wi) = w;
+                    // the next step's forward operand: W0's bf16 planes, split once here
+                    uint16_t h[4], m[4], l[4];
+                    umma::split3_bf16(w.x, h[0], m[0], l[0]);
+                    umma::split3_bf16(w.y, h[1], m[1], l[1]);
+                    umma::split3_bf16(w.z, h[2], m[2], l[2]);
+                    umma::split3_bf16(w.w, h[3], m[3], l[3]);
+                    const uint2 ph = make_uint2(pack2(h[0], h[1]), pack2(h[2], h[3]));
+                    const uint2 pm = make_uint2(pack2(m[0], m[1]), pack2(m[2], m[3]));
+                    const uint2 pl = make_uint2(pack2(l[0], l[1]), pack2(l[2], l[3]));
+                    *reinterpret_cast<uint2 *>(p.W0bf + j) = ph;
+                    *reinterpret_cast<uint2 *>(p.W0bf + nd + j) = pm;
+                    *reinterpret_cast<uint2 *>(p.W0bf + 2 * nd + j) = pl;
+                    if (sync) {
+                        *reinterpret_cast<float4 *>(p.target_w + wi) = w;
+                        *reinterpret_cast<uint2 *>(p.W0bf + 3 * nd + j) = ph;
+                        *reinterpret_cast<uint2 *>(p.W0bf + 4 * nd + j) = pm;
+                        *reinterpret_cast<uint2 *>(p.W0bf + 5 * nd + j) = pl;
+                    }
+                }
         }
     }
     if (p.do_db0) {
@@ -429,7 +447,7 @@ __global__ void __launch_bounds__(256) wide_reduce_kernel(const float *__restric
         const int net = (int)(i / per), u = (int)(i % N0);
         float v = 0.0f;
         for (int q = 0; q < ks; ++q) v += __ldcg(PF0 + (int64_t)q * total + i);
-        v += __ldg((net == 1 ? target : online) + b0 + u);
+        v = v / 255.0f + __ldg((net == 1 ? target : online) + b0 + u);
         H0[i] = v > 0.0f ? v : 0.0f;
     }
 }
