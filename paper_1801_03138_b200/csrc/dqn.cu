@@ -761,6 +761,15 @@ struct rpl_dqn {
         FastArgs args;              // the args those nodes currently hold
     };
     std::vector<GraphEntry> graphs;
+    struct WideGraph {
+        const rpl_replay *rp;
+        int B, apply;
+        cudaGraph_t graph;
+        cudaGraphExec_t exec;
+        cudaGraphNode_t k4;        // the loss destination
+        FastArgs args;
+    };
+    std::vector<WideGraph> wide_graphs;
     bool use_graphs = true;
     bool use_pdl = false;                  // programmatic dependent launch inside the graph
     bool k3_pdl = true;                    // K3 programmatic after K2
@@ -910,6 +919,10 @@ extern "C" int dqn_destroy(rpl_dqn *d)
     cudaStreamSynchronize(d->stream);
     if (d->comm && g_nccl.destroy) g_nccl.destroy(d->comm);
     for (auto &g : d->graphs) {
+        cudaGraphExecDestroy(g.exec);
+        cudaGraphDestroy(g.graph);
+    }
+    for (auto &g : d->wide_graphs) {
         cudaGraphExecDestroy(g.exec);
         cudaGraphDestroy(g.graph);
     }
@@ -1332,6 +1345,96 @@ static int grid_for(const rpl_dqn *d, const TrainArgs &p)
     return (int)std::min<int64_t>(mx, d->sms);
 }
 
+// FastArgs of the fast kernels above a tensor-core layer 0 (byte-state wide inputs)
+static void wide_fast_args(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int apply, FastArgs &fp)
+{
+    fill_fast(d, rp, B, loss_dev, apply, fp);
+    fp.D = 0;                 // K1 neither gathers nor computes layer 0
+    fp.distinct = 0;          // the batch is sampled by the byte gather
+    fp.h0_in = d->H[0];       // [nets][B][N0] (the debug export's layer-0 activations)
+    fp.H0 = d->H[0];          // the online net's block [B][N0]
+    fp.PdH0 = d->PdH0;
+    fp.dZ0 = d->PF0;
+    fp.dZ0bf = d->dz0bf;
+    fp.NS = fast_ns(d, B);
+}
+
+// the byte-state wide step captured once per (replay, batch, mode) and replayed: gather
+// (event / size / cursor from the control block), tcgen05 layer 0, split-K reduction, the
+// fast kernels above it (K4 advances the event), dW0 + its SGD
+static cudaError_t wide_graph_step(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int apply,
+                                   const WideArgs &w)
+{
+    FastArgs fp;
+    wide_fast_args(d, rp, B, loss_dev, apply, fp);
+    fp.event_advanced = 0;
+    rpl_dqn::WideGraph *ge = nullptr;
+    for (auto &g : d->wide_graphs)
+        if (g.rp == rp && g.B == B && g.apply == apply) ge = &g;
+    cudaError_t e = cudaSuccess;
+    if (!ge) {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        cudaStream_t cs = d->cap_stream;
+        if (!cs && (e = cudaStreamCreateWithFlags(&d->cap_stream, cudaStreamNonBlocking)) != cudaSuccess)
+            return e;
+        cs = d->cap_stream;
+        e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) return e;
+        rpl_batch bt{d->Xs, d->Xs2, d->a, d->r, d->done, d->idx};
+        int rc = launch_gather_u8_dev(rp, B, &bt, cs);
+        wide_l0_kernel<<<w.nets * w.ks, WD_T, WD_SMEM, cs>>>(w);
+        wide_reduce_kernel<<<d->sms * 4, 256, 0, cs>>>(d->PF0, w.ks, w.nets, B, d->N[0], d->online,
+                                                       d->target, d->boff[0], d->H[0]);
+        cudaError_t e2 = rc == RPL_OK ? fast_enqueue(d, fp, cs) : cudaErrorUnknown;
+        wide_dw0_kernel<<<(unsigned)((w.D + w.ntile - 1) / w.ntile), WD_T, WD_SMEM, cs>>>(w);
+        e = cudaStreamEndCapture(cs, &graph);
+        if (e == cudaSuccess) e = e2;
+        if (e == cudaSuccess) e = cudaGetLastError();
+        cudaGraphNode_t k4 = nullptr;
+        if (e == cudaSuccess) {
+            size_t n = 0;
+            e = cudaGraphGetNodes(graph, nullptr, &n);
+            std::vector<cudaGraphNode_t> nodes(n);
+            if (e == cudaSuccess && n) e = cudaGraphGetNodes(graph, nodes.data(), &n);
+            for (size_t i = 0; e == cudaSuccess && i < n; ++i) {
+                cudaGraphNodeType ty;
+                cudaKernelNodeParams kp = {};
+                if (cudaGraphNodeGetType(nodes[i], &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel &&
+                    cudaGraphKernelNodeGetParams(nodes[i], &kp) == cudaSuccess &&
+                    kp.func == (void *)fast_bwd0_sgd_kernel)
+                    k4 = nodes[i];
+            }
+            if (e == cudaSuccess && !k4) e = cudaErrorInvalidValue;
+        }
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+        if (e != cudaSuccess) {
+            if (graph) cudaGraphDestroy(graph);
+            return e;
+        }
+        if (d->wide_graphs.size() >= 8) {
+            cudaGraphExecDestroy(d->wide_graphs.front().exec);
+            cudaGraphDestroy(d->wide_graphs.front().graph);
+            d->wide_graphs.erase(d->wide_graphs.begin());
+        }
+        d->wide_graphs.push_back({rp, B, apply, graph, exec, k4, fp});
+        ge = &d->wide_graphs.back();
+    } else if (memcmp(&ge->args, &fp, sizeof fp) != 0) {
+        // between replays only the loss destination may change (K4 writes it)
+        void *args[] = {&fp};
+        cudaKernelNodeParams kp = {};
+        e = cudaGraphKernelNodeGetParams(ge->k4, &kp);
+        kp.kernelParams = args;
+        kp.extra = nullptr;
+        if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(ge->exec, ge->k4, &kp);
+        if (e != cudaSuccess) return e;
+        ge->args = fp;
+    }
+    e = cudaGraphLaunch(ge->exec, d->stream);
+    if (e == cudaSuccess) g_launches.fetch_add(8);
+    return e;
+}
+
 extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *loss_dev)
 {
     if (!d || !rp || batch < 1 || batch > d->cfg.max_batch || rp->ring.D != d->cfg.state_dim ||
@@ -1516,6 +1619,18 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                 g_launches.fetch_add(2);
                 d->w0bf_stale = false;
             }
+            w.ntile = (int)std::min<int64_t>(WD_MAXN, ((p.D + d->sms - 1) / d->sms + 15) / 16 * 16);
+            w.do_db0 = d->wide_fast ? 1 : 0;
+            w.b0 = d->boff[0];
+            if (d->wide_fast && d->use_graphs && !rp->distinct) {
+                // the whole byte-state step as one CUDA graph (control block read on device)
+                e = wide_graph_step(d, rp, batch, dp ? nullptr : loss_dev, dp ? 0 : 1, w);
+                if (e != cudaSuccess) {
+                    if (prev >= 0) cudaSetDevice(prev);
+                    return cuda_fail(e, "wide graph step");
+                }
+                goto after_step;
+            }
             // (1) Philox sample + gather + unpack into the learner's batch buffers
             rpl_batch bt{d->Xs, d->Xs2, d->a, d->r, d->done, d->idx};
             if (int rc = launch_gather(rp, batch, nullptr, rp->events, 1, &bt)) {
@@ -1542,15 +1657,8 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             wide_reduce_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->PF0, w.ks, p.nets, batch, d->N[0],
                                                                    d->online, d->target, d->boff[0], d->H[0]);
             FastArgs fp;
-            fill_fast(d, rp, batch, dp ? nullptr : loss_dev, dp ? 0 : 1, fp);
-            fp.D = 0;                 // K1 neither gathers nor computes layer 0
-            fp.distinct = 0;          // the batch was sampled by step (1)
-            fp.h0_in = d->H[0];       // [nets][B][N0] (the debug export's layer-0 activations)
-            fp.H0 = d->H[0];          // the online net's block [B][N0]
-            fp.PdH0 = d->PdH0;
-            fp.dZ0 = d->PF0;
-            fp.dZ0bf = d->dz0bf;
-            fp.NS = fast_ns(d, batch);
+            wide_fast_args(d, rp, batch, dp ? nullptr : loss_dev, dp ? 0 : 1, fp);
+            fp.event_advanced = 1;    // the sampling gather advanced the event
             e = cudaGetLastError();
             if (e == cudaSuccess) e = fast_enqueue(d, fp, d->stream);
             if (e != cudaSuccess) {
@@ -1558,8 +1666,6 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                 return cuda_fail(e, "wide fast step");
             }
             g_launches.fetch_add(5);
-            w.do_db0 = 1;
-            w.b0 = d->boff[0];
         } else {
         const int grid = grid_for(d, p);
         void *args[] = {&p};
@@ -1574,7 +1680,6 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
         if (wide) {
             // (4) dW0 = dZ0^T x per 256-input tile, then its SGD / target sync
             // dW0 tiles: one wave over the SMs (28,224 inputs -> 147 tiles of 192)
-            w.ntile = (int)std::min<int64_t>(WD_MAXN, ((p.D + d->sms - 1) / d->sms + 15) / 16 * 16);
             wide_dw0_kernel<<<(unsigned)((p.D + w.ntile - 1) / w.ntile), WD_T, WD_SMEM, d->stream>>>(w);
             e = cudaGetLastError();
             if (e != cudaSuccess) {
@@ -1584,6 +1689,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             g_launches.fetch_add(2);
         }
     }
+after_step:
     if (dp) {
         int nr = g_nccl.allreduce(d->grad, d->grad, (size_t)d->P + 1, kNcclFloat, kNcclAvg,
                                   d->comm, d->stream);

@@ -122,6 +122,8 @@ int launch_distinct(const rpl_replay *rp, int B, int32_t *out, uint32_t *err, ui
 // slot of logical position 0 (shared states: the oldest experience; else 0, slot == u)
 int64_t sampleable(const rpl_replay *rp);
 uint64_t oldest_slot(const rpl_replay *rp);
+// the sampling gather of a graph-captured byte-state train step (control block read on device)
+int launch_gather_u8_dev(rpl_replay *rp, int64_t n, const rpl_batch *out, cudaStream_t st);
 // enqueue the pending deferred insert (if any) as an insert-kernel launch
 int replay_flush(rpl_replay *rp);
 // the pending insert was enqueued for consumption on `st`: a zero-copy staging slot may be

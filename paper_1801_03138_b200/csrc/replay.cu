@@ -379,9 +379,15 @@ __global__ void __launch_bounds__(256) gather_u8_kernel(const uint8_t *__restric
                                                         uint64_t seed, uint32_t rank, uint64_t event,
                                                         uint8_t *s, uint8_t *s2, int32_t *a, float *r,
                                                         uint8_t *done, int32_t *idx_out, uint32_t *err,
-                                                        uint64_t *ctrl)
+                                                        uint64_t *ctrl, const uint64_t *ctrl_in)
 {
     __shared__ int32_t ix_s;
+    if (ctrl_in) {   // graph-replayed train steps: event / size / cursor from the control block
+        event = ctrl_in[0];
+        size = (int64_t)ctrl_in[1];
+        nvalid = shared ? size - 1 : size;
+        oldest = (shared && size == capacity) ? ctrl_in[2] : 0;
+    }
     if (idx_in == nullptr && ctrl && blockIdx.x == 0 && threadIdx.x == 0) ctrl[0] = event + 1;
     for (int64_t e = blockIdx.x; e < n; e += gridDim.x) {
         if (threadIdx.x == 0) {
@@ -442,6 +448,24 @@ int launch_distinct(const rpl_replay *rp, int B, int32_t *out, uint32_t *err, ui
 }
 
 const void *insert_kernel_ptr() { return (const void *)insert_kernel; }
+
+// the sampling gather of a graph-captured byte-state step: event, size and cursor are read
+// from the control block on the device, the event is advanced by the step's last kernel
+int launch_gather_u8_dev(rpl_replay *rp, int64_t n, const rpl_batch *out, cudaStream_t st)
+{
+    const rpl::Ring &R = rp->ring;
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, rp->device);
+    int64_t nb = n < (int64_t)dev_sms * 8 ? n : (int64_t)dev_sms * 8;
+    if (nb < 1) nb = 1;
+    gather_u8_kernel<<<(unsigned)nb, 256, 0, st>>>(
+        reinterpret_cast<const uint8_t *>(R.rows), (int64_t)R.rs * 4, R.so, R.D, R.shared,
+        R.capacity, 0, 0, 0, n, nullptr, rp->seed, rp->rank, 0,
+        static_cast<uint8_t *>(out->s), static_cast<uint8_t *>(out->s_next), out->a, out->r,
+        out->done, out->idx, rp->err_dev, nullptr, rp->ctrl_dev);
+    RPL_LAUNCHED();
+    return RPL_OK;
+}
 
 int64_t sampleable(const rpl_replay *rp)
 {
@@ -530,7 +554,7 @@ int launch_gather(rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t ev
             R.capacity, oldest, nvalid, rp->size, n,
             use_sampler ? nullptr : idx_dev, rp->seed, rp->rank, event,
             static_cast<uint8_t *>(out->s), static_cast<uint8_t *>(out->s_next), out->a, out->r,
-            out->done, out->idx, rp->err_dev, rp->ctrl_dev);
+            out->done, out->idx, rp->err_dev, rp->ctrl_dev, nullptr);
     } else if (R.shared) {
         gather_shared_kernel<<<(unsigned)blocks, 256, 0, rp->stream>>>(
             R.rows, R.rs, R.D, R.sw, R.capacity, nvalid, oldest, rp->size, n,

@@ -86,6 +86,7 @@ struct FastArgs {
     float *PdH0;         // [NS][B][N0] K3's dH0 split-K partials (no dW0 shares)
     float *dZ0;          // [B][N0] dZ0 materialised by K4 for wide_dw0_kernel
     uint16_t *dZ0bf;     // its bf16 hi / mid / lo planes [3][B][N0]
+    int event_advanced;  // 1: the step's sampling kernel advanced rctrl[0] already
     uint32_t *err;
     unsigned long long *trace;   // optional per-CTA [kernel][cta][start, end] %globaltimer (ns)
 };
@@ -1124,7 +1125,7 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
         if (!ok) atomicOr(p.err, ERRBIT_NUMERIC);
         // fire-and-forget reductions (no load round trip on the kernel's tail); with wide
         // inputs the sampling gather has advanced the event already
-        if (!p.h0_in) atomicAdd(reinterpret_cast<unsigned long long *>(p.rctrl), 1ull);   // sampler event consumed
+        if (!p.event_advanced) atomicAdd(reinterpret_cast<unsigned long long *>(p.rctrl), 1ull);   // sampler event consumed
         atomicAdd(reinterpret_cast<unsigned long long *>(p.step_dev), 1ull); // executed train steps
     }
 }
