@@ -57,22 +57,25 @@ def test_shared_state_sample_wraps(b, distinct):
     assert rp.check() == b.RPL_OK
 
 
+@pytest.mark.parametrize("distinct", [False, True])
 @pytest.mark.parametrize("path", ["fast", "generic"])
-def test_shared_state_train_step(b, path, monkeypatch):
-    # a 96-slot ring that wraps during the run, 8 host inserts per step deferred into K1 (the
-    # s' of the newest committed slot is read through from the pending insert)
+def test_shared_state_train_step(b, path, distinct, monkeypatch):
+    # a 160-slot ring that wraps during the run, 8 host inserts per step deferred into the step
+    # (the s' of the newest committed slot is read through from the pending insert); with the
+    # distinct sampler the 128 distinct experiences come from the 159 sampleable ones
     if path == "generic":
         monkeypatch.setenv("RPL_PATH", "generic")
     cfg = b.DQNConfig(state_dim=27, n_actions=8, dueling=True, hidden=(128,), stream=512,
                       double_dqn=True, gamma=0.99, lr=1e-3, huber_kappa=1.0, sync_period=3,
                       max_batch=128)
-    rp = b.Replay(96, 27, seed=3, shared_state=True)
-    orc = oracle.Ring(96, 27, shared=True)
-    e = experiences(300, seed=6)
-    _add(rp, orc, {k: v[:80] for k, v in e.items()})
+    rp = b.Replay(160, 27, seed=3, shared_state=True,
+                  sampling="distinct" if distinct else "uniform")
+    orc = oracle.Ring(160, 27, shared=True, distinct=distinct)
+    e = experiences(400, seed=6)
+    _add(rp, orc, {k: v[:140] for k, v in e.items()})
     dqn = b.DQN(cfg, init_params(27, 8, (128,), True, 512, seed=7))
     for it in range(10):
-        _add(rp, orc, {k: v[80 + 8 * it:88 + 8 * it] for k, v in e.items()})
+        _add(rp, orc, {k: v[140 + 8 * it:148 + 8 * it] for k, v in e.items()})
         assert step_and_compare(b, cfg, dqn, rp, orc, 128, seed=3) is not None
     assert dqn.check() == b.RPL_OK and rp.check() == b.RPL_OK
 
