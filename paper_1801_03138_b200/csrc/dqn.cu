@@ -305,17 +305,23 @@ __device__ void phase_dz0(const TrainArgs &p)
     const int N = p.N[0];
     const int64_t total = (int64_t)p.B * N, stride = (int64_t)gridDim.x * NT;
     const int64_t pstride = (int64_t)p.B * N;
-    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < total; i += stride) {
-        float s = 0.0f;
-        for (int q = 0; q < p.nsplit_n[1]; ++q) s += __ldcg(p.PdH[1] + q * pstride + i);
-        const float z = __ldcg(p.H[0] + i) > 0.0f ? s : 0.0f;
-        p.PF0[i] = z;
-        if (p.wide_tc) {   // the dW0 kernel's tensor-core operand, split once
+    // wide_tc: the samples up to the next multiple of 16 get zero planes (wide_dw0_kernel)
+    const int64_t total16 = p.wide_tc ? (int64_t)((p.B + 15) & ~15) * N : total;
+    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < total16; i += stride) {
+        float z = 0.0f;
+        if (i < total) {
+            float s = 0.0f;
+            for (int q = 0; q < p.nsplit_n[1]; ++q) s += __ldcg(p.PdH[1] + q * pstride + i);
+            z = __ldcg(p.H[0] + i) > 0.0f ? s : 0.0f;
+            p.PF0[i] = z;
+        }
+        if (p.wide_tc) {   // the dW0 kernel's tensor-core operand, split once, pre-tiled
             uint16_t h, m, l;
             umma::split3_bf16(z, h, m, l);
-            p.dZ0bf[i] = h;
-            p.dZ0bf[total + i] = m;
-            p.dZ0bf[2 * total + i] = l;
+            const int64_t t = wd_tix_mn((int)(i % N), i / N), pz = wd_plane_elems(p.B);
+            p.dZ0bf[t] = h;
+            p.dZ0bf[pz + t] = m;
+            p.dZ0bf[2 * pz + t] = l;
         }
     }
 }
@@ -986,8 +992,11 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
         if (d->wide_tc) {
             ok = cudaFuncSetAttribute(wide_l0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WD_SMEM) == cudaSuccess &&
                  cudaFuncSetAttribute(wide_dw0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WD_SMEM) == cudaSuccess &&
-                 dalloc(d, &d->w0bf, (size_t)6 * d->N[0] * D) &&
-                 dalloc(d, &d->dz0bf, (size_t)3 * Bm * d->N[0]);
+                 dalloc(d, &d->w0bf, (size_t)6 * wd_plane_elems(D)) &&
+                 dalloc(d, &d->dz0bf, (size_t)3 * wd_plane_elems(Bm)) &&
+                 // the tiles' padding (inputs past D) is never written: zero once
+                 cudaMemset(d->w0bf, 0, (size_t)6 * wd_plane_elems(D) * 2) == cudaSuccess &&
+                 cudaMemset(d->dz0bf, 0, (size_t)3 * wd_plane_elems(Bm) * 2) == cudaSuccess;
         }
     }
     for (int l = 0; l < d->T && ok; ++l) {
@@ -1608,9 +1617,9 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             p.wide_tc = 1;
             p.ks0 = w.ks;
             if (d->w0bf_stale) {   // after create / set_params / sync_target / a DP step
-                const int64_t nd = (int64_t)d->N[0] * p.D;
-                wide_split_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->online + d->woff[0], d->w0bf, nd);
-                wide_split_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->target + d->woff[0], d->w0bf + 3 * nd, nd);
+                const int64_t pe = wd_plane_elems(p.D);
+                wide_split_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->online + d->woff[0], d->w0bf, d->N[0], p.D);
+                wide_split_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->target + d->woff[0], d->w0bf + 3 * pe, d->N[0], p.D);
                 e = cudaGetLastError();
                 if (e != cudaSuccess) {
                     if (prev >= 0) cudaSetDevice(prev);

@@ -24,6 +24,7 @@
 #include "ring_row.cuh"
 #include "distinct.cuh"
 #include "umma.cuh"
+#include "wide.cuh"
 
 namespace rpl {
 
@@ -1072,18 +1073,23 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
     }
     if (p.PdH0) {
         // wide inputs: dZ0 = ReLU'(z0) * (sum of K3's dH0 split-K partials, in split order)
-        // and its bf16 planes, for wide_dw0_kernel
-        const int64_t nz = (int64_t)B * p.N0;
-        for (int64_t i = (int64_t)blockIdx.x * NT + tid; i < nz; i += stride) {
+        // and its bf16 planes in wide_dw0_kernel's pre-tiled MN-major layout; the samples up
+        // to the next multiple of 16 (read by its last MMA) get zero planes
+        const int64_t nz = (int64_t)B * p.N0, pz = wd_plane_elems(B);
+        const int64_t nz16 = (int64_t)((B + 15) & ~15) * p.N0;
+        for (int64_t i = (int64_t)blockIdx.x * NT + tid; i < nz16; i += stride) {
             float z = 0.0f;
-            for (int q = 0; q < p.NS; ++q) z += __ldcg(p.PdH0 + (int64_t)q * nz + i);
-            z = __ldcg(p.h0_in + i) > 0.0f ? z : 0.0f;
-            p.dZ0[i] = z;
+            if (i < nz) {
+                for (int q = 0; q < p.NS; ++q) z += __ldcg(p.PdH0 + (int64_t)q * nz + i);
+                z = __ldcg(p.h0_in + i) > 0.0f ? z : 0.0f;
+                p.dZ0[i] = z;
+            }
             uint16_t h, m, l;
             umma::split3_bf16(z, h, m, l);
-            p.dZ0bf[i] = h;
-            p.dZ0bf[nz + i] = m;
-            p.dZ0bf[2 * nz + i] = l;
+            const int64_t t = wd_tix_mn((int)(i % p.N0), i / p.N0);
+            p.dZ0bf[t] = h;
+            p.dZ0bf[pz + t] = m;
+            p.dZ0bf[2 * pz + t] = l;
         }
     }
     trace_.mark(3);

@@ -78,6 +78,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase)
         :: "r"(smem_u32(mbar)), "r"(phase) : "memory");
 }
 
+// one thread arms the mbarrier with the bytes its bulk copies will deliver (its arrival)
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *mbar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(mbar)), "r"(bytes) : "memory");
+}
+
+// bulk (TMA engine) copy of `bytes` (multiple of 16, both ends 16-byte aligned) global ->
+// shared memory, completing as transaction bytes on `mbar`
+__device__ __forceinline__ void bulk_g2s(void *smem, const void *gmem, uint32_t bytes, uint64_t *mbar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(mbar)) : "memory");
+}
+
 // operands written with ordinary st.shared must be made visible to the tensor core (async proxy)
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }

@@ -17,9 +17,11 @@
 //                    sync) of those W0 entries: layer 0's gradient never makes a round trip.
 // The fp32 operands are split once, not per CTA: W0's planes live next to the fp32 master
 // weights (rewritten by the dW0 epilogue's SGD, re-split by wide_split_kernel after any host
-// write or target sync) and dZ0's planes are written by the train kernel; the CTAs copy them
-// with 16-byte cp.async straight into the canonical layout.  Both kernels stage 64-deep K
-// slices through two shared-memory buffers: the loads of slice i + 1 overlap the MMAs of
+// write or target sync) and dZ0's planes are written by the train kernel.  Both sets of planes
+// are stored PRE-TILED: each 64-deep K slice of a plane is the 16 KB canonical shared-memory
+// image of that slice (wd_tix_k / wd_tix_mn), so one bulk copy on the TMA engine
+// (cp.async.bulk, completing on an mbarrier) moves a slice plane.  Both kernels stage 64-deep
+// K slices through two shared-memory buffers: the loads of slice i + 1 overlap the MMAs of
 // slice i (tcgen05.commit -> mbarrier per buffer).
 #pragma once
 #include <stdint.h>
@@ -45,8 +47,8 @@ struct WideArgs {
     int64_t w0;                      // offset of W0 [N0][D] in the parameter blob
     float *PF0;                      // [ks][nets][B][N0]
     const float *dZ0;                // [B][N0] (materialised by the train kernel)
-    const uint16_t *dZ0bf;           // its bf16 hi / mid / lo planes [3][B][N0] (same kernel)
-    uint16_t *W0bf;                  // bf16 planes of W0: [net 0 online, 1 target][3][N0 * D]
+    const uint16_t *dZ0bf;           // its bf16 hi / mid / lo planes [3][wd_plane_elems(B)], MN-major tiles
+    uint16_t *W0bf;                  // bf16 planes of W0: [net 0 online, 1 target][3][wd_plane_elems(D)], K-major tiles
     float *grad;                     // [P + 1] (grad[P] = batch-mean loss, set by the train kernel)
     int64_t P;
     float *online_w, *target_w;      // SGD targets (== online / target)
@@ -62,24 +64,26 @@ struct WideArgs {
 __device__ __forceinline__ uint32_t wd_off_k(int r, int k) { return (r >> 3) * 1024 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2; }
 __device__ __forceinline__ uint32_t wd_off_mn(int r, int k, int R) { return (k >> 3) * (R / 8) * 128 + (r >> 3) * 128 + (k & 7) * 16 + (r & 7) * 2; }
 
+// pre-tiled global planes (128 rows, K padded to the 64-deep slice, padding zero): element
+// (row u, k) of a K-major plane (W0: u = unit, k = input) and of an MN-major one (dZ0^T:
+// u = unit, k = sample)
+__host__ __device__ inline int64_t wd_plane_elems(int64_t K) { return (int64_t)WD_M * ((K + WD_KS - 1) / WD_KS * WD_KS); }
+__device__ __forceinline__ int64_t wd_tix_k(int u, int64_t k) { return (k >> 6) * (WD_M * WD_KS) + wd_off_k(u, (int)(k & 63)) / 2; }
+__device__ __forceinline__ int64_t wd_tix_mn(int u, int64_t k) { return (k >> 6) * (WD_M * WD_KS) + wd_off_mn(u, (int)(k & 63), WD_M) / 2; }
+
 __device__ __forceinline__ uint32_t pack2(uint16_t a, uint16_t b) { return (uint32_t)a | ((uint32_t)b << 16); }
 
-__device__ __forceinline__ void wd_cp16(void *smem, const void *gmem, bool valid)
+// planes[p] = split3(W0)_p (p = hi, mid, lo) for W0 [N0][D] row-major, K-major tiles
+__global__ void __launch_bounds__(256) wide_split_kernel(const float *__restrict__ src, uint16_t *planes, int N0, int64_t D)
 {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
-}
-__device__ __forceinline__ void wd_cp_wait() { asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory"); }
-
-// planes[p][i] = split3(src[i])_p  (p = hi, mid, lo)
-__global__ void __launch_bounds__(256) wide_split_kernel(const float *__restrict__ src, uint16_t *planes, int64_t n)
-{
+    const int64_t n = (int64_t)N0 * D, pe = wd_plane_elems(D);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         uint16_t h, m, l;
         umma::split3_bf16(src[i], h, m, l);
-        planes[i] = h;
-        planes[n + i] = m;
-        planes[2 * n + i] = l;
+        const int64_t t = wd_tix_k((int)(i / D), i % D);
+        planes[t] = h;
+        planes[pe + t] = m;
+        planes[2 * pe + t] = l;
     }
 }
 __device__ __forceinline__ uint16_t u8_bf16(uint32_t v) { return __bfloat16_as_ushort(__uint2bfloat16_rn(v)); }
@@ -91,7 +95,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
 {
     extern __shared__ uint8_t wd_raw[];
     uint8_t *sm = reinterpret_cast<uint8_t *>(((uintptr_t)wd_raw + 1023) & ~(uintptr_t)1023);
-    __shared__ uint64_t mbar[2];
+    __shared__ uint64_t mbar[2], full[2];   // MMAs done with / weight planes landed in a stage
     __shared__ uint32_t tbase;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int net = blockIdx.x / p.ks, kq = blockIdx.x % p.ks;
@@ -104,6 +108,8 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
     if (tid == 0) {
         umma::mbar_init(&mbar[0], 1);
         umma::mbar_init(&mbar[1], 1);
+        umma::mbar_init(&full[0], 1);
+        umma::mbar_init(&full[1], 1);
         umma::fence_mbar_init();
     }
     umma::fence_before_sync();
@@ -114,19 +120,16 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
     // software pipeline over the K slices: slice sl + 1's weight planes (cp.async group) and
     // byte states (registers) are in flight while slice sl is converted and multiplied; a
     // stage is refilled once the MMAs that read it two slices earlier have committed
-    const int64_t nd = (int64_t)p.N0 * p.D;
-    const uint16_t *Wp = p.W0bf + (net == 1 ? 3 * nd : 0);
+    const int64_t pe = wd_plane_elems(p.D);
+    const uint16_t *Wp = p.W0bf + (net == 1 ? 3 * pe : 0);
     auto issue_A = [&](int sl) {
-        // the hi / mid / lo planes of W0[u][k0 .. k0+63] (K-major), 16-byte copies of 8 k
+        // thread 0: the hi / mid / lo tiles of W0[:, k0 .. k0+63], one 16 KB bulk copy each
+        if (tid != 0) return;
         uint8_t *A = sm + (sl & 1) * WD_STAGE;
-        const int64_t k0 = kb + (int64_t)sl * WD_KS;
-        for (int e = tid; e < 3 * WD_M * (WD_KS / 8); e += WD_T) {
-            const int pl = e / (WD_M * (WD_KS / 8)), r = e % (WD_M * (WD_KS / 8));
-            const int u = r / (WD_KS / 8), k = 8 * (r % (WD_KS / 8));
-            const bool v = u < p.N0 && k0 + k < ke;
-            wd_cp16(A + pl * WD_A_PLANE + wd_off_k(u, k), v ? Wp + pl * nd + (int64_t)u * p.D + k0 + k : Wp, v);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
+        const int64_t t0 = (kb + (int64_t)sl * WD_KS) / WD_KS * (WD_M * WD_KS);
+        umma::mbar_expect_tx(&full[sl & 1], 3 * WD_A_PLANE);
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl) umma::bulk_g2s(A + pl * WD_A_PLANE, Wp + pl * pe + t0, WD_A_PLANE, &full[sl & 1]);
     };
     const int totalB = N * (WD_KS / 16);   // 16-byte pieces of a slice's states (<= 4 per thread)
     auto load_B = [&](int sl, uint4 v[4]) {
@@ -182,15 +185,13 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
             if (sl >= 1) umma::mbar_wait(&mbar[st ^ 1], ((sl - 1) >> 1) & 1);
             issue_A(sl + 1);
             load_B(sl + 1, vn);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");   // A(sl) has landed
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         umma::fence_async_smem();
         umma::fence_before_sync();
         __syncthreads();
         if (tid == 0) {
             umma::fence_after_sync();
+            umma::mbar_wait(&full[st], (sl >> 1) & 1);   // A(sl) has landed
             for (int s = 0; s < WD_KS / 16; ++s) {
                 const uint64_t bd = umma::desc(Bs + 2 * s * 128, 128, 1024);
 #pragma unroll
@@ -241,10 +242,13 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
     const int nn = (int)(p.D - n0 < p.ntile ? p.D - n0 : p.ntile);    // inputs in the tile
     const int N = (nn + 15) & ~15;
     const int nsl = (p.B + WD_KS - 1) / WD_KS;
+    __shared__ uint64_t full[2];
     if (warp == 0) umma::tmem_alloc(&tbase, 256);
     if (tid == 0) {
         umma::mbar_init(&mbar[0], 1);
         umma::mbar_init(&mbar[1], 1);
+        umma::mbar_init(&full[0], 1);
+        umma::mbar_init(&full[1], 1);
         umma::fence_mbar_init();
     }
     umma::fence_before_sync();
@@ -257,17 +261,14 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
         uint8_t *A = sm + st * WD_STAGE, *Bs = A + 3 * WD_A_PLANE;
         if (sl >= 2) umma::mbar_wait(&mbar[st], ((sl - 2) >> 1) & 1);
         const int b0 = sl * WD_KS;
-        // A = dZ0^T slice: element (unit u, sample b) = dZ0[b][u], MN-major (contiguous in u):
-        // 16-byte copies of 8 units from the train kernel's bf16 planes
-        {
-            const int64_t pz = (int64_t)p.B * p.N0;
-            for (int e = tid; e < 3 * WD_KS * (WD_M / 8); e += WD_T) {
-                const int pl = e / (WD_KS * (WD_M / 8)), r = e % (WD_KS * (WD_M / 8));
-                const int bb = r / (WD_M / 8), u = 8 * (r % (WD_M / 8));
-                const bool v = b0 + bb < p.B && u < p.N0;
-                wd_cp16(A + pl * WD_A_PLANE + wd_off_mn(u, bb, WD_M),
-                        v ? p.dZ0bf + pl * pz + (int64_t)(b0 + bb) * p.N0 + u : p.dZ0bf, v);
-            }
+        // A = dZ0^T slice: element (unit u, sample b) = dZ0[b][u], MN-major: the train
+        // kernel's pre-tiled bf16 planes, one 16 KB bulk copy each (thread 0)
+        if (tid == 0) {
+            const int64_t pz = wd_plane_elems(p.B), t0 = (int64_t)sl * (WD_M * WD_KS);
+            umma::mbar_expect_tx(&full[st], 3 * WD_A_PLANE);
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl)
+                umma::bulk_g2s(A + pl * WD_A_PLANE, p.dZ0bf + pl * pz + t0, WD_A_PLANE, &full[st]);
         }
         // B = U^T slice: element (input n, sample b) = U[b][n0 + n], MN-major (contiguous in n);
         // all loads first (at most 4 per thread), then the conversions
@@ -310,12 +311,12 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
                 *reinterpret_cast<uint4 *>(Bs + wd_off_mn(n + 8, bb, N)) = make_uint4(o8[4], o8[5], o8[6], o8[7]);
             }
         }
-        wd_cp_wait();
         umma::fence_async_smem();
         umma::fence_before_sync();
         __syncthreads();
         if (tid == 0) {
             umma::fence_after_sync();
+            umma::mbar_wait(&full[st], (sl >> 1) & 1);
             const int ksteps = (min(WD_KS, p.B - b0) + 15) / 16;
             for (int s = 0; s < ksteps; ++s) {
                 const uint64_t bd = umma::desc(Bs + 2 * s * (N / 8) * 128, (N / 8) * 128, 128);
@@ -355,7 +356,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
         const float loss = __ldcg(p.grad + p.P);
         const bool upd = p.apply_update && isfinite(loss);
         const bool sync = *p.sync_flag != 0;
-        const int64_t nd = (int64_t)p.N0 * p.D;
+        const int64_t pe = wd_plane_elems(p.D);
         // a warp walks rows w, w + 8, ... four at a time: their weight loads (<= 8 float4 per
         // lane) are all in flight before the first update
         constexpr int NWE = WD_T / 32;
@@ -397,14 +398,15 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
                     const uint2 ph = make_uint2(pack2(h[0], h[1]), pack2(h[2], h[3]));
                     const uint2 pm = make_uint2(pack2(m[0], m[1]), pack2(m[2], m[3]));
                     const uint2 pl = make_uint2(pack2(l[0], l[1]), pack2(l[2], l[3]));
-                    *reinterpret_cast<uint2 *>(p.W0bf + j) = ph;
-                    *reinterpret_cast<uint2 *>(p.W0bf + nd + j) = pm;
-                    *reinterpret_cast<uint2 *>(p.W0bf + 2 * nd + j) = pl;
+                    const int64_t tx = wd_tix_k(u, n0 + c);   // 4 inputs of one core-matrix row
+                    *reinterpret_cast<uint2 *>(p.W0bf + tx) = ph;
+                    *reinterpret_cast<uint2 *>(p.W0bf + pe + tx) = pm;
+                    *reinterpret_cast<uint2 *>(p.W0bf + 2 * pe + tx) = pl;
                     if (sync) {
                         *reinterpret_cast<float4 *>(p.target_w + wi) = w;
-                        *reinterpret_cast<uint2 *>(p.W0bf + 3 * nd + j) = ph;
-                        *reinterpret_cast<uint2 *>(p.W0bf + 4 * nd + j) = pm;
-                        *reinterpret_cast<uint2 *>(p.W0bf + 5 * nd + j) = pl;
+                        *reinterpret_cast<uint2 *>(p.W0bf + 3 * pe + tx) = ph;
+                        *reinterpret_cast<uint2 *>(p.W0bf + 4 * pe + tx) = pm;
+                        *reinterpret_cast<uint2 *>(p.W0bf + 5 * pe + tx) = pl;
                     }
                 }
         }
