@@ -337,6 +337,8 @@ __device__ __forceinline__ void copy_bytes_cta(uint8_t *__restrict__ dst, const 
     }
 }
 
+constexpr int64_t kInsPiece = 4096;   // bytes of a byte-state row per insert CTA
+
 __global__ void __launch_bounds__(256) insert_u8_kernel(uint8_t *__restrict__ rows, int64_t rsb, int so,
                                                         int D, int shared, int64_t capacity, int64_t cursor,
                                                         int64_t k, const uint8_t *__restrict__ s,
@@ -350,12 +352,22 @@ __global__ void __launch_bounds__(256) insert_u8_kernel(uint8_t *__restrict__ ro
         ctrl[1] = (uint64_t)new_size;
         ctrl[2] = (uint64_t)((cursor + k) % capacity);
     }
-    for (int64_t j = blockIdx.x; j < k; j += gridDim.x) {
+    // a row's state bytes (s, then s' unless shared) are cut into kInsPiece-byte pieces, one
+    // CTA each: a few ~56 KB Atari rows are spread over many SMs instead of one CTA per row
+    const int64_t L = (int64_t)(shared ? 1 : 2) * D;
+    const int64_t np = (L + kInsPiece - 1) / kInsPiece;
+    for (int64_t w = blockIdx.x; w < k * np; w += gridDim.x) {
+        const int64_t j = w / np, q = w % np;
         int64_t slot = cursor + j;
         if (slot >= capacity) slot -= capacity;   // k <= capacity, cursor < capacity
         uint8_t *row = rows + slot * rsb;
-        copy_bytes_cta(row, s + j * D, D);
-        if (!shared) copy_bytes_cta(row + D, s2 + j * D, D);   // shared: s' is the next row's s
+        const int64_t b0 = q * kInsPiece, b1 = b0 + kInsPiece < L ? b0 + kInsPiece : L;
+        if (b0 < D) copy_bytes_cta(row + b0, s + j * D + b0, (b1 < D ? b1 : D) - b0);
+        if (b1 > D) {   // shared: s' is the next row's s (L == D, never taken)
+            const int64_t c0 = b0 > D ? b0 : D;
+            copy_bytes_cta(row + c0, s2 + j * D + (c0 - D), b1 - c0);
+        }
+        if (q != np - 1) continue;
         for (int b = (shared ? 1 : 2) * D + threadIdx.x; b < so; b += blockDim.x) row[b] = 0;
         if (threadIdx.x == 0) {
             uint32_t d = done[j];
@@ -495,8 +507,9 @@ int replay_flush(rpl_replay *rp)
     int64_t blocks = (k + 7) / 8;
     if (blocks > (int64_t)dev_sms * 8) blocks = (int64_t)dev_sms * 8;
     if (rp->ring.u8) {
-        // one CTA per experience row (rows are ~56 KB for Atari-shaped states)
-        const int64_t ublocks = k < (int64_t)dev_sms * 16 ? k : (int64_t)dev_sms * 16;
+        // one CTA per 4 KB piece of a row (rows are ~56 KB for Atari-shaped states)
+        const int64_t pieces = k * (((rp->ring.shared ? 1 : 2) * (int64_t)rp->ring.D + kInsPiece - 1) / kInsPiece);
+        const int64_t ublocks = pieces < (int64_t)dev_sms * 16 ? pieces : (int64_t)dev_sms * 16;
         insert_u8_kernel<<<(unsigned)ublocks, 256, 0, rp->stream>>>(
             reinterpret_cast<uint8_t *>(rp->ring.rows), (int64_t)rp->ring.rs * 4, rp->ring.so,
             rp->ring.D, rp->ring.shared, rp->ring.capacity, q.cursor, k, static_cast<const uint8_t *>(q.s), q.a, q.r,

@@ -256,60 +256,75 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
     umma::fence_after_sync();
     const uint32_t tmem = tbase;
     const uint32_t idesc = umma::idesc_bf16(WD_M, N, true, true);
-    for (int sl = 0; sl < nsl; ++sl) {
-        const int st = sl & 1;
-        uint8_t *A = sm + st * WD_STAGE, *Bs = A + 3 * WD_A_PLANE;
-        if (sl >= 2) umma::mbar_wait(&mbar[st], ((sl - 2) >> 1) & 1);
-        const int b0 = sl * WD_KS;
+    // software pipeline as in wide_l0_kernel: slice sl + 1's dZ0 planes (bulk copies) and byte
+    // states (registers) are in flight while slice sl is converted and multiplied
+    auto issue_A = [&](int sl) {
         // A = dZ0^T slice: element (unit u, sample b) = dZ0[b][u], MN-major: the train
         // kernel's pre-tiled bf16 planes, one 16 KB bulk copy each (thread 0)
-        if (tid == 0) {
-            const int64_t pz = wd_plane_elems(p.B), t0 = (int64_t)sl * (WD_M * WD_KS);
-            umma::mbar_expect_tx(&full[st], 3 * WD_A_PLANE);
+        if (tid != 0) return;
+        uint8_t *A = sm + (sl & 1) * WD_STAGE;
+        const int64_t pz = wd_plane_elems(p.B), t0 = (int64_t)sl * (WD_M * WD_KS);
+        umma::mbar_expect_tx(&full[sl & 1], 3 * WD_A_PLANE);
 #pragma unroll
-            for (int pl = 0; pl < 3; ++pl)
-                umma::bulk_g2s(A + pl * WD_A_PLANE, p.dZ0bf + pl * pz + t0, WD_A_PLANE, &full[st]);
+        for (int pl = 0; pl < 3; ++pl)
+            umma::bulk_g2s(A + pl * WD_A_PLANE, p.dZ0bf + pl * pz + t0, WD_A_PLANE, &full[sl & 1]);
+    };
+    // B = U^T slice: element (input n, sample b) = U[b][n0 + n], MN-major (contiguous in n);
+    // 16-byte pieces, at most 4 per thread
+    const int totalB = WD_KS * (N / 16);
+    auto load_B = [&](int sl, uint4 v[4]) {
+        const int b0 = sl * WD_KS;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = tid + q * WD_T;
+            v[q] = make_uint4(0u, 0u, 0u, 0u);
+            if (e >= totalB) continue;
+            const int bb = e / (N / 16), n = 16 * (e % (N / 16));
+            if (b0 + bb < p.B) {
+                const uint8_t *src = p.U0 + (int64_t)(b0 + bb) * p.D + n0 + n;
+                if (n + 15 < nn && ((uintptr_t)src & 15) == 0) {
+                    v[q] = __ldg(reinterpret_cast<const uint4 *>(src));
+                } else {
+                    uint8_t t[16];
+                    for (int i = 0; i < 16; ++i) t[i] = (n + i < nn) ? src[i] : 0;
+                    v[q] = make_uint4(t[0] | t[1] << 8 | t[2] << 16 | (uint32_t)t[3] << 24,
+                                      t[4] | t[5] << 8 | t[6] << 16 | (uint32_t)t[7] << 24,
+                                      t[8] | t[9] << 8 | t[10] << 16 | (uint32_t)t[11] << 24,
+                                      t[12] | t[13] << 8 | t[14] << 16 | (uint32_t)t[15] << 24);
+                }
+            }
         }
-        // B = U^T slice: element (input n, sample b) = U[b][n0 + n], MN-major (contiguous in n);
-        // all loads first (at most 4 per thread), then the conversions
-        {
-            const int total = WD_KS * (N / 16);
-            uint4 v[4];
+    };
+    auto store_B = [&](int sl, const uint4 v[4]) {
+        uint8_t *Bs = sm + (sl & 1) * WD_STAGE + 3 * WD_A_PLANE;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int e = tid + q * WD_T;
-                v[q] = make_uint4(0u, 0u, 0u, 0u);
-                if (e >= total) continue;
-                const int bb = e / (N / 16), n = 16 * (e % (N / 16));
-                if (b0 + bb < p.B) {
-                    const uint8_t *src = p.U0 + (int64_t)(b0 + bb) * p.D + n0 + n;
-                    if (n + 15 < nn && ((uintptr_t)src & 15) == 0) {
-                        v[q] = __ldg(reinterpret_cast<const uint4 *>(src));
-                    } else {
-                        uint8_t t[16];
-                        for (int i = 0; i < 16; ++i) t[i] = (n + i < nn) ? src[i] : 0;
-                        v[q] = make_uint4(t[0] | t[1] << 8 | t[2] << 16 | (uint32_t)t[3] << 24,
-                                          t[4] | t[5] << 8 | t[6] << 16 | (uint32_t)t[7] << 24,
-                                          t[8] | t[9] << 8 | t[10] << 16 | (uint32_t)t[11] << 24,
-                                          t[12] | t[13] << 8 | t[14] << 16 | (uint32_t)t[15] << 24);
-                    }
-                }
+        for (int q = 0; q < 4; ++q) {
+            const int e = tid + q * WD_T;
+            if (e >= totalB) continue;
+            const int bb = e / (N / 16), n = 16 * (e % (N / 16));
+            const uint32_t w4[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+            uint32_t o8[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                o8[2 * i] = pack2(u8_bf16(w4[i] & 0xFF), u8_bf16((w4[i] >> 8) & 0xFF));
+                o8[2 * i + 1] = pack2(u8_bf16((w4[i] >> 16) & 0xFF), u8_bf16(w4[i] >> 24));
             }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int e = tid + q * WD_T;
-                if (e >= total) continue;
-                const int bb = e / (N / 16), n = 16 * (e % (N / 16));
-                const uint32_t w4[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
-                uint32_t o8[8];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    o8[2 * i] = pack2(u8_bf16(w4[i] & 0xFF), u8_bf16((w4[i] >> 8) & 0xFF));
-                    o8[2 * i + 1] = pack2(u8_bf16((w4[i] >> 16) & 0xFF), u8_bf16(w4[i] >> 24));
-                }
-                *reinterpret_cast<uint4 *>(Bs + wd_off_mn(n, bb, N)) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
-                *reinterpret_cast<uint4 *>(Bs + wd_off_mn(n + 8, bb, N)) = make_uint4(o8[4], o8[5], o8[6], o8[7]);
-            }
+            *reinterpret_cast<uint4 *>(Bs + wd_off_mn(n, bb, N)) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
+            *reinterpret_cast<uint4 *>(Bs + wd_off_mn(n + 8, bb, N)) = make_uint4(o8[4], o8[5], o8[6], o8[7]);
+        }
+    };
+    uint4 vb[4], vn[4];
+    issue_A(0);
+    load_B(0, vb);
+    for (int sl = 0; sl < nsl; ++sl) {
+        const int st = sl & 1;
+        const uint8_t *A = sm + st * WD_STAGE, *Bs = A + 3 * WD_A_PLANE;
+        store_B(sl, vb);   // stage st was freed before A(sl) was issued
+        if (sl + 1 < nsl) {
+            // the other stage last fed the MMAs of slice sl - 1: wait for them, then refill it
+            if (sl >= 1) umma::mbar_wait(&mbar[st ^ 1], ((sl - 1) >> 1) & 1);
+            issue_A(sl + 1);
+            load_B(sl + 1, vn);
         }
         umma::fence_async_smem();
         umma::fence_before_sync();
@@ -317,7 +332,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
         if (tid == 0) {
             umma::fence_after_sync();
             umma::mbar_wait(&full[st], (sl >> 1) & 1);
-            const int ksteps = (min(WD_KS, p.B - b0) + 15) / 16;
+            const int ksteps = (min(WD_KS, p.B - sl * WD_KS) + 15) / 16;
             for (int s = 0; s < ksteps; ++s) {
                 const uint64_t bd = umma::desc(Bs + 2 * s * (N / 8) * 128, (N / 8) * 128, 128);
 #pragma unroll
@@ -328,6 +343,8 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
             }
             umma::commit(&mbar[st]);
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) vb[q] = vn[q];
     }
     {
         const int last = nsl - 1;
@@ -357,6 +374,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
         const bool upd = p.apply_update && isfinite(loss);
         const bool sync = *p.sync_flag != 0;
         const int64_t pe = wd_plane_elems(p.D);
+        const float k255 = 1.0f / 255.0f;
         // a warp walks rows w, w + 8, ... four at a time: their weight loads (<= 8 float4 per
         // lane) are all in flight before the first update
         constexpr int NWE = WD_T / 32;
@@ -380,7 +398,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
                     const int64_t j = (int64_t)u * p.D + n0 + c;   // index within W0
                     const int64_t wi = p.w0 + j;
                     const float4 t = *reinterpret_cast<const float4 *>(T + u * TS + c);
-                    const float4 g = make_float4(t.x / 255.0f, t.y / 255.0f, t.z / 255.0f, t.w / 255.0f);
+                    const float4 g = make_float4(t.x * k255, t.y * k255, t.z * k255, t.w * k255);
                     *reinterpret_cast<float4 *>(p.grad + wi) = g;
                     if (!upd) continue;
                     float4 w = wv[r][cc];
