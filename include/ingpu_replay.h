@@ -228,9 +228,10 @@ int dqn_step_count(const rpl_dqn *dqn, int64_t *steps);
  *   RPL_DBG_H        [B*H] f32 online-net activations on s over the hidden-unit space
  *                    (shared layers in order, then the stream units [V | A])
  *   RPL_DBG_LOSS     [1] f32
- *   RPL_DBG_TRACE    [4 x 2048 x 8] u64 per-CTA %globaltimer (ns) marks of the four fast-path
- *                    kernels of the last step: [0] start, [1] end, [2..7] phase marks (only
- *                    with env RPL_TRACE=1)
+ *   RPL_DBG_TRACE    [8 x 2048 x 8] u64 per-CTA marks of the last step's kernels (only with
+ *                    env RPL_TRACE=1): slots 0..3 the four fast-path kernels ([0] start and
+ *                    [1] end %globaltimer ns, [2..7] SM cycles since start), 4 / 5 the wide
+ *                    layer-0 forward / dW0 kernels ([0..7] %globaltimer ns)
  * `bytes` must equal the size of that array for the last step's batch. */
 enum { RPL_DBG_IDX = 0, RPL_DBG_S, RPL_DBG_S_NEXT, RPL_DBG_A, RPL_DBG_R, RPL_DBG_DONE,
        RPL_DBG_Q, RPL_DBG_QT_NEXT, RPL_DBG_QO_NEXT, RPL_DBG_Y, RPL_DBG_ASTAR, RPL_DBG_H,

@@ -361,7 +361,7 @@ class DQN:
                 RPL_DBG_ASTAR: (np.int32, (batch,)),
                 RPL_DBG_H: (np.float32, (batch, hidden_units)),
                 RPL_DBG_LOSS: (np.float32, (1,)),
-                RPL_DBG_TRACE: (np.uint64, (4, 2048, 8))}[what]
+                RPL_DBG_TRACE: (np.uint64, (8, 2048, 8))}[what]
         out = np.empty(spec[1], spec[0])
         _ok(_L.dqn_debug_export(self._h, what, out.ctypes.data_as(C.c_void_p), out.nbytes))
         return out

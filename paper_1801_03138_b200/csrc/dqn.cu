@@ -991,7 +991,7 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
                      !(nw && nw[0] == '1');
         if (d->wide_tc) {
             ok = cudaFuncSetAttribute(wide_l0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WD_SMEM) == cudaSuccess &&
-                 cudaFuncSetAttribute(wide_dw0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WD_SMEM) == cudaSuccess &&
+                 cudaFuncSetAttribute(wide_dw0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WD_SMEM_MAX) == cudaSuccess &&
                  dalloc(d, &d->w0bf, (size_t)6 * wd_plane_elems(D)) &&
                  dalloc(d, &d->dz0bf, (size_t)3 * wd_plane_elems(Bm)) &&
                  // the tiles' padding (inputs past D) is never written: zero once
@@ -1029,8 +1029,8 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
     ok = ok && dalloc(d, &d->step_dev, 1) && dalloc(d, &d->sync_flag, 1);
     const char *tr = getenv("RPL_TRACE");
     if (ok && tr && tr[0] == '1') {
-        ok = dalloc(d, &d->trace, 4 * 2048 * 8);
-        if (ok) cudaMemset(d->trace, 0, 4 * 2048 * 8 * sizeof(unsigned long long));
+        ok = dalloc(d, &d->trace, 8 * 2048 * 8);
+        if (ok) cudaMemset(d->trace, 0, 8 * 2048 * 8 * sizeof(unsigned long long));
     }
     // wide byte-state inputs: the fast kernels run the layers above the tensor-core layer 0
     {
@@ -1396,7 +1396,7 @@ static cudaError_t wide_graph_step(rpl_dqn *d, rpl_replay *rp, int B, float *los
         wide_reduce_kernel<<<d->sms * 4, 256, 0, cs>>>(d->PF0, w.ks, w.nets, B, d->N[0], d->online,
                                                        d->target, d->boff[0], d->H[0]);
         cudaError_t e2 = rc == RPL_OK ? fast_enqueue(d, fp, cs) : cudaErrorUnknown;
-        wide_dw0_kernel<<<(unsigned)((w.D + w.ntile - 1) / w.ntile), WD_T, WD_SMEM, cs>>>(w);
+        wide_dw0_kernel<<<(unsigned)((w.D + w.ntile - 1) / w.ntile), WD_T, wd_dw0_smem(w.ntile), cs>>>(w);
         e = cudaStreamEndCapture(cs, &graph);
         if (e == cudaSuccess) e = e2;
         if (e == cudaSuccess) e = cudaGetLastError();
@@ -1629,6 +1629,8 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                 d->w0bf_stale = false;
             }
             w.ntile = (int)std::min<int64_t>(WD_MAXN, ((p.D + d->sms - 1) / d->sms + 15) / 16 * 16);
+            w.wpre = wd_dw0_wpre(w.ntile) ? 1 : 0;
+            w.trace = d->trace;
             w.do_db0 = d->wide_fast ? 1 : 0;
             w.b0 = d->boff[0];
             if (d->wide_fast && d->use_graphs && !rp->distinct) {
@@ -1689,7 +1691,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
         if (wide) {
             // (4) dW0 = dZ0^T x per 256-input tile, then its SGD / target sync
             // dW0 tiles: one wave over the SMs (28,224 inputs -> 147 tiles of 192)
-            wide_dw0_kernel<<<(unsigned)((p.D + w.ntile - 1) / w.ntile), WD_T, WD_SMEM, d->stream>>>(w);
+            wide_dw0_kernel<<<(unsigned)((p.D + w.ntile - 1) / w.ntile), WD_T, wd_dw0_smem(w.ntile), d->stream>>>(w);
             e = cudaGetLastError();
             if (e != cudaSuccess) {
                 if (prev >= 0) cudaSetDevice(prev);
@@ -1811,7 +1813,7 @@ extern "C" int dqn_debug_export(rpl_dqn *d, int what, void *host_out, int64_t by
     case RPL_DBG_H: need = B * d->Htot * 4; break;
     case RPL_DBG_TRACE:
         if (!d->trace) { set_error("dqn_debug_export: tracing is off (set RPL_TRACE=1)"); return RPL_ESTATE; }
-        src = d->trace; need = 4 * 2048 * 8 * 8; break;
+        src = d->trace; need = 8 * 2048 * 8 * 8; break;
     default: set_error("dqn_debug_export: unknown item %d", what); return RPL_EINVAL;
     }
     if (bytes != need) {

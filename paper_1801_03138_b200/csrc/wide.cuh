@@ -38,6 +38,15 @@ constexpr int WD_A_PLANE = WD_M * WD_KS * 2;            // bytes of one bf16 A p
 constexpr int WD_B_BYTES = WD_MAXN * WD_KS * 2;         // bytes of the bf16 B slice
 constexpr int WD_STAGE = 3 * WD_A_PLANE + WD_B_BYTES;   // 80 KB
 constexpr int WD_SMEM = 2 * WD_STAGE + 1024;            // + alignment slack
+constexpr int WD_SMEM_MAX = 226 * 1024;                 // the per-CTA opt-in limit (227 KB) less static smem
+// wide_dw0_kernel's epilogue: the accumulator tile [128][N + 4] plus, when it fits, the tile's
+// fp32 weights [128][N + 4] prefetched with cp.async (one memory latency for the whole tile)
+__host__ __device__ inline int wd_dw0_need(int ntile) { return 1024 + 2 * WD_M * (ntile + 4) * 4; }
+__host__ __device__ inline bool wd_dw0_wpre(int ntile) { return wd_dw0_need(ntile) <= WD_SMEM_MAX; }
+__host__ __device__ inline int wd_dw0_smem(int ntile)
+{
+    return wd_dw0_wpre(ntile) && wd_dw0_need(ntile) > WD_SMEM ? wd_dw0_need(ntile) : WD_SMEM;
+}
 
 struct WideArgs {
     int D, B, N0, nets, ks;          // inputs, batch, layer-0 units (== 128), nets, k-chunks
@@ -58,6 +67,25 @@ struct WideArgs {
     int64_t b0;                      // offset of b0 (the fast-path variant: db0 is this kernel's)
     int do_db0;
     int ntile;                       // dW0 inputs per CTA (multiple of 16, <= 256)
+    int wpre;                        // wd_dw0_wpre(ntile): the launch has wd_dw0_smem(ntile) bytes
+    unsigned long long *trace;       // RPL_TRACE=1: per-CTA %globaltimer marks (kernel slots 4, 5)
+};
+
+// RPL_TRACE=1: thread 0 of each CTA stores %globaltimer at marks 0 .. 7 of its slot
+struct WdTrace {
+    unsigned long long *slot;
+    __device__ WdTrace(unsigned long long *tr, int kernel)
+        : slot(tr && threadIdx.x == 0 ? tr + 8 * ((size_t)kernel * 2048 + blockIdx.x) : nullptr)
+    {
+        mark(0);
+    }
+    __device__ void mark(int i)
+    {
+        if (!slot) return;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        slot[i] = t;
+    }
 };
 
 // canonical no-swizzle offsets (umma.cuh): K-major rows x 64-deep slice, and MN-major
@@ -70,6 +98,11 @@ __device__ __forceinline__ uint32_t wd_off_mn(int r, int k, int R) { return (k >
 __host__ __device__ inline int64_t wd_plane_elems(int64_t K) { return (int64_t)WD_M * ((K + WD_KS - 1) / WD_KS * WD_KS); }
 __device__ __forceinline__ int64_t wd_tix_k(int u, int64_t k) { return (k >> 6) * (WD_M * WD_KS) + wd_off_k(u, (int)(k & 63)) / 2; }
 __device__ __forceinline__ int64_t wd_tix_mn(int u, int64_t k) { return (k >> 6) * (WD_M * WD_KS) + wd_off_mn(u, (int)(k & 63), WD_M) / 2; }
+
+__device__ __forceinline__ void wd_cp16(void *smem, const void *gmem)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(umma::smem_u32(smem)), "l"(gmem) : "memory");
+}
 
 __device__ __forceinline__ uint32_t pack2(uint16_t a, uint16_t b) { return (uint32_t)a | ((uint32_t)b << 16); }
 
@@ -99,6 +132,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
     __shared__ uint32_t tbase;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int net = blockIdx.x / p.ks, kq = blockIdx.x % p.ks;
+    WdTrace tr(p.trace, 4);
     const int64_t kb = (int64_t)kq * p.kchunk;
     const int64_t ke = kb + p.kchunk < p.D ? kb + p.kchunk : p.D;
     const int nsl = (int)((ke - kb + WD_KS - 1) / WD_KS);
@@ -174,6 +208,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
         }
     };
     uint4 vb[4], vn[4];
+    tr.mark(1);
     issue_A(0);
     load_B(0, vb);
     for (int sl = 0; sl < nsl; ++sl) {
@@ -209,6 +244,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
         const int last = nsl - 1;
         umma::mbar_wait(&mbar[last & 1], (last >> 1) & 1);
     }
+    tr.mark(2);
     umma::fence_after_sync();
     // epilogue: warp w reads TMEM lanes (units) 32 (w % 4) .. + 31, columns (samples) of its half
     {
@@ -225,6 +261,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
     }
     umma::fence_before_sync();
     __syncthreads();
+    tr.mark(3);
     if (warp == 0) umma::tmem_free(tmem, 256);
 }
 
@@ -239,6 +276,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
     __shared__ uint32_t tbase;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t n0 = (int64_t)blockIdx.x * p.ntile;                  // first input of the tile
+    WdTrace tr(p.trace, 5);
     const int nn = (int)(p.D - n0 < p.ntile ? p.D - n0 : p.ntile);    // inputs in the tile
     const int N = (nn + 15) & ~15;
     const int nsl = (p.B + WD_KS - 1) / WD_KS;
@@ -256,6 +294,28 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
     umma::fence_after_sync();
     const uint32_t tmem = tbase;
     const uint32_t idesc = umma::idesc_bf16(WD_M, N, true, true);
+    const float loss = __ldcg(p.grad + p.P);
+    const bool upd = p.apply_update && isfinite(loss);
+    const bool sync = *p.sync_flag != 0;
+    if (p.do_db0 && warp == WD_T / 32 - 1) {
+        // db0 = sum_b dZ0[b][u] (the last warp of CTA u, lanes stride the samples, fixed
+        // shuffle tree) and its SGD, first thing: its loads overlap the first slice's
+        for (int u = blockIdx.x; u < p.N0; u += gridDim.x) {
+            float acc = 0.0f;
+#pragma unroll 8
+            for (int bb = lane; bb < p.B; bb += 32) acc += __ldcg(p.dZ0 + (int64_t)bb * p.N0 + u);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+            if (lane == 0) {
+                p.grad[p.b0 + u] = acc;
+                if (upd) {
+                    const float w = p.online_w[p.b0 + u] - p.lr * acc;
+                    p.online_w[p.b0 + u] = w;
+                    if (sync) p.target_w[p.b0 + u] = w;
+                }
+            }
+        }
+    }
     // software pipeline as in wide_l0_kernel: slice sl + 1's dZ0 planes (bulk copies) and byte
     // states (registers) are in flight while slice sl is converted and multiplied
     auto issue_A = [&](int sl) {
@@ -313,6 +373,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
             *reinterpret_cast<uint4 *>(Bs + wd_off_mn(n + 8, bb, N)) = make_uint4(o8[4], o8[5], o8[6], o8[7]);
         }
     };
+    tr.mark(1);
     uint4 vb[4], vn[4];
     issue_A(0);
     load_B(0, vb);
@@ -346,17 +407,30 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
 #pragma unroll
         for (int q = 0; q < 4; ++q) vb[q] = vn[q];
     }
+    tr.mark(2);
     {
         const int last = nsl - 1;
         umma::mbar_wait(&mbar[last & 1], (last >> 1) & 1);
     }
+    tr.mark(4);
     umma::fence_after_sync();
     // epilogue: the accumulator tile goes TMEM -> registers -> shared memory (the staging
-    // buffers are free: every MMA has completed), then each warp walks whole W0 rows so the
-    // weight, gradient and plane accesses are coalesced: g = D / 255 -> grad; w -= lr g
-    // (skipped on a non-finite loss); the target copy on sync steps
-    constexpr int TS = WD_MAXN + 4;                 // tile row stride (floats)
+    // buffers are free: every MMA has completed) while the tile's weights stream into shared
+    // memory behind it (wpre), then each warp walks whole W0 rows so the weight, gradient and
+    // plane accesses are coalesced: g = D / 255 -> grad; w -= lr g (skipped on a non-finite
+    // loss); the target copy on sync steps
+    const int TS = N + 4;                           // tile row stride (floats)
     float *T = reinterpret_cast<float *>(sm);       // [128][TS]
+    float *Wt = T + WD_M * TS;                      // [128][TS] (wpre)
+    const bool wpre = p.wpre && upd;
+    if (wpre) {
+        const int nq = nn / 4;
+        for (int e = tid; e < p.N0 * nq; e += WD_T) {
+            const int u = e / nq, c = 4 * (e % nq);
+            wd_cp16(Wt + u * TS + c, p.online_w + p.w0 + (int64_t)u * p.D + n0 + c);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     {
         const int q = warp & 3, half = warp >> 2, u = 32 * q + lane;
         const int c0 = half * (N / 2), c1 = c0 + N / 2;
@@ -367,41 +441,31 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
             *reinterpret_cast<float4 *>(T + u * TS + c + 4) = make_float4(v[4], v[5], v[6], v[7]);
         }
     }
+    if (wpre) asm volatile("cp.async.wait_group 0;" ::: "memory");
+    tr.mark(5);
     umma::fence_before_sync();
     __syncthreads();
     {
-        const float loss = __ldcg(p.grad + p.P);
-        const bool upd = p.apply_update && isfinite(loss);
-        const bool sync = *p.sync_flag != 0;
         const int64_t pe = wd_plane_elems(p.D);
         const float k255 = 1.0f / 255.0f;
-        // a warp walks rows w, w + 8, ... four at a time: their weight loads (<= 8 float4 per
-        // lane) are all in flight before the first update
+        // task (8-row group G, 16-input chunk): lane 4 r + q takes row 8 G + r, inputs
+        // 16 chunk + 4 q .. + 3, so the fp32 rows go out in 64-byte runs and the bf16 plane
+        // tiles in 256-byte runs (two whole core matrices): every store fills its sectors
         constexpr int NWE = WD_T / 32;
-        for (int ub = warp; ub < p.N0; ub += 4 * NWE) {
-            float4 wv[4][2];
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-                for (int cc = 0; cc < 2; ++cc) {
-                    const int u = ub + r * NWE, c = 4 * lane + 128 * cc;
-                    wv[r][cc] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (upd && u < p.N0 && c < nn)
-                        wv[r][cc] = *reinterpret_cast<const float4 *>(p.online_w + p.w0 + (int64_t)u * p.D + n0 + c);
-                }
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-                for (int cc = 0; cc < 2; ++cc) {
-                    const int u = ub + r * NWE, c = 4 * lane + 128 * cc;
-                    if (u >= p.N0 || c >= nn) continue;
+        const int r8 = lane >> 2, q4 = lane & 3;
+        const int nch = nn / 16, ntask = (p.N0 / 8) * nch;
+#pragma unroll 2
+        for (int task = warp; task < ntask; task += NWE) {
+                {
+                    const int u = 8 * (task / nch) + r8, c = 16 * (task % nch) + 4 * q4;
                     const int64_t j = (int64_t)u * p.D + n0 + c;   // index within W0
                     const int64_t wi = p.w0 + j;
                     const float4 t = *reinterpret_cast<const float4 *>(T + u * TS + c);
                     const float4 g = make_float4(t.x * k255, t.y * k255, t.z * k255, t.w * k255);
                     *reinterpret_cast<float4 *>(p.grad + wi) = g;
                     if (!upd) continue;
-                    float4 w = wv[r][cc];
+                    float4 w = wpre ? *reinterpret_cast<const float4 *>(Wt + u * TS + c)
+                                    : *reinterpret_cast<const float4 *>(p.online_w + wi);
                     w.x -= p.lr * g.x;
                     w.y -= p.lr * g.y;
                     w.z -= p.lr * g.z;
@@ -429,29 +493,9 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
                 }
         }
     }
-    if (p.do_db0) {
-        // db0 = sum_b dZ0[b][u] (a warp per unit over the first CTAs, lanes stride the
-        // samples, fixed shuffle tree), and its SGD
-        const float loss = __ldcg(p.grad + p.P);
-        const bool upd = p.apply_update && isfinite(loss);
-        const bool sync = *p.sync_flag != 0;
-        for (int u = blockIdx.x * (WD_T / 32) + warp; u < p.N0; u += gridDim.x * (WD_T / 32)) {
-            float acc = 0.0f;
-            for (int bb = lane; bb < p.B; bb += 32) acc += __ldcg(p.dZ0 + (int64_t)bb * p.N0 + u);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
-            if (lane == 0) {
-                p.grad[p.b0 + u] = acc;
-                if (upd) {
-                    const float w = p.online_w[p.b0 + u] - p.lr * acc;
-                    p.online_w[p.b0 + u] = w;
-                    if (sync) p.target_w[p.b0 + u] = w;
-                }
-            }
-        }
-    }
     umma::fence_before_sync();
     __syncthreads();
+    tr.mark(6);
     if (warp == 0) umma::tmem_free(tmem, 256);
 }
 
