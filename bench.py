@@ -55,6 +55,9 @@ def parse():
                     help="store one state per experience (P:141): s' = the next slot's s")
     ap.add_argument("--distinct", action="store_true",
                     help="sample distinct indices (RPL_SAMPLE_DISTINCT, P:75's planned switch)")
+    ap.add_argument("--ring", choices=["device", "host"], default="device",
+                    help="host: the in-RAM comparison mode (SURVEY NEXT-1): ring rows in pinned host "
+                         "memory, every batch read across PCIe by the same kernels")
     ap.add_argument("--config", choices=["c2", "c5"], default="c2",
                     help="c2: BASELINE configs[1] (default); c5: configs[4] 84x84x4 uint8 states, "
                          "batch 256 (other flags' defaults: --batch 256)")
@@ -70,8 +73,10 @@ def workload_name(a, batch):
     net = ("dueling DQN 27-128-[V512|A512]-1+8 (P:92-94)" if a.net == "dueling"
            else "2x64 MLP 27-64-64-8")
     tgt = "Double-DQN" if a.ddqn else "DQN"
+    where = (", ring rows in pinned host memory read across PCIe (in-RAM comparison mode)"
+             if a.ring == "host" else "")
     return (f"BASELINE configs[1]: {a.capacity:,}-slot replay of 27-float states, batch {batch}, "
-            f"{net}, {tgt} target, Huber, SGD, {a.adds_per_step} inserts/step")
+            f"{net}, {tgt} target, Huber, SGD, {a.adds_per_step} inserts/step{where}")
 
 
 def make_cfg(a, binding, batch):
@@ -261,7 +266,7 @@ def run_ours(a, batch, first_line=True):
     cfg = make_cfg(a, binding, batch)
     rp = binding.Replay(a.capacity, 27, device=local, burn_in=1, seed=2, rank=rank,
                         sampling="distinct" if a.distinct else "uniform",
-                        shared_state=a.shared_state)
+                        shared_state=a.shared_state, ring_memory=a.ring)
     # pre-fill the whole ring (startup excluded from timings); per-rank data stream
     rp.add_many(experiences(a.capacity, seed=1, rank=rank))
     dqn = binding.DQN(cfg, init_params(27, 8, cfg.hidden, cfg.dueling, cfg.stream, seed=3),
@@ -468,6 +473,7 @@ def run_ours(a, batch, first_line=True):
                    "net": a.net, "double_dqn": a.ddqn, "adds_per_step": k,
                    "sampling": "distinct" if a.distinct else "uniform (with replacement, P:75)",
                    "state_storage": "shared (s' = next slot's s, P:141)" if a.shared_state else "s and s' per row",
+                   "ring_memory": "host (pinned, read across PCIe: in-RAM comparison)" if a.ring == "host" else "device (HBM)",
                    "parallelism": f"dp{world}" + (f", parameters averaged every {a.avg_period} steps"
                                                   if a.avg_period and world > 1 else ""),
                    "l2": "inputs larger than L2: the 256 MB ring (> 126 MB L2) is sampled uniformly;"

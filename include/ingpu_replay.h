@@ -50,6 +50,7 @@ enum { RPL_HOST = 0, RPL_DEVICE = 1, RPL_DEVICE_DEFER = 2 };
 enum { RPL_ONLINE = 0, RPL_TARGET = 1, RPL_GRAD = 2 };  /* which parameter vector          */
 enum { RPL_F32 = 0, RPL_U8 = 1 };                        /* state element type of a replay  */
 enum { RPL_SAMPLE_UNIFORM = 0, RPL_SAMPLE_DISTINCT = 1 }; /* sampler of a replay            */
+enum { RPL_RING_DEVICE = 0, RPL_RING_HOST = 1 };          /* where a replay's rows live      */
 
 typedef struct rpl_replay rpl_replay;   /* opaque */
 typedef struct rpl_dqn rpl_dqn;         /* opaque */
@@ -78,6 +79,12 @@ typedef struct {
                              s_next (may be NULL); the sampler draws over the size - 1
                              experiences whose successor is stored (all but the newest), at
                              logical position u -> slot (oldest + u) mod capacity            */
+    int32_t ring_memory;  /* RPL_RING_DEVICE (default: the method, rows in HBM) or
+                             RPL_RING_HOST: the in-RAM comparison mode (
+                             P:50): the same rows in pinned, device-mapped host
+                             memory, so every sample / gather / train step reads its batch
+                             across PCIe -- the per-step transfer the in-GPU replay removes.
+                             The kernels, sampler and results are identical              */
 } rpl_replay_opts;
 
 /* Create an empty FIFO replay of `capacity` experiences whose states are `state_dim`

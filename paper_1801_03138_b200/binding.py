@@ -26,6 +26,7 @@ RPL_ECUDA, RPL_ENCCL, RPL_ESTATE = -5, -6, -7
 RPL_HOST, RPL_DEVICE, RPL_DEVICE_DEFER = 0, 1, 2
 RPL_ONLINE, RPL_TARGET, RPL_GRAD = 0, 1, 2
 RPL_F32, RPL_U8 = 0, 1
+RPL_RING_DEVICE, RPL_RING_HOST = 0, 1
 (RPL_DBG_IDX, RPL_DBG_S, RPL_DBG_S_NEXT, RPL_DBG_A, RPL_DBG_R, RPL_DBG_DONE, RPL_DBG_Q,
  RPL_DBG_QT_NEXT, RPL_DBG_QO_NEXT, RPL_DBG_Y, RPL_DBG_ASTAR, RPL_DBG_H, RPL_DBG_LOSS,
  RPL_DBG_TRACE) = range(14)
@@ -48,7 +49,8 @@ class RplError(RuntimeError):
 class _ReplayOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("cuda_stream", C.c_void_p), ("burn_in", C.c_int64),
                 ("seed", C.c_uint64), ("rank", C.c_uint32), ("max_host_add", C.c_int64),
-                ("state_dtype", C.c_int32), ("sampling", C.c_int32), ("state_sharing", C.c_int32)]
+                ("state_dtype", C.c_int32), ("sampling", C.c_int32), ("state_sharing", C.c_int32),
+                ("ring_memory", C.c_int32)]
 
 
 class _Batch(C.Structure):
@@ -146,7 +148,8 @@ class Replay:
 
     def __init__(self, capacity: int, state_dim: int, *, device: int = 0, stream=None,
                  burn_in: int = 1, seed: int = 2, rank: int = 0, max_host_add: int = 0,
-                 state_dtype: str = "f32", sampling: str = "uniform", shared_state: bool = False):
+                 state_dtype: str = "f32", sampling: str = "uniform", shared_state: bool = False,
+                 ring_memory: str = "device"):
         torch = _torch()
         if not torch.cuda.is_available():
             raise RplError(RPL_ECUDA, "no CUDA device (the in-GPU replay has no CPU fallback)")
@@ -158,8 +161,10 @@ class Replay:
             self._stream = _stream_handle(stream)
         o = _ReplayOpts(device, self._stream, burn_in, seed, rank, max_host_add,
                         RPL_U8 if self.u8 else RPL_F32, 1 if sampling == "distinct" else 0,
-                        1 if shared_state else 0)
+                        1 if shared_state else 0,
+                        RPL_RING_HOST if ring_memory == "host" else RPL_RING_DEVICE)
         self.shared_state = shared_state
+        self.ring_memory = ring_memory
         h = C.c_void_p()
         _ok(_L.replay_create(capacity, state_dim, C.byref(o), C.byref(h)))
         self._h = h

@@ -46,6 +46,7 @@ constexpr uint32_t TAG_SAMPLE = 1u;
 // a | r | done | pad], row stride a multiple of 128 B; `so` is the byte offset of a.
 struct Ring {
     float *rows = nullptr;     // capacity * rs words
+    int host = 0;              // RPL_RING_HOST: rows in pinned, mapped host memory
     int64_t capacity = 0;
     int32_t D = 0;
     int32_t rs = 0;            // row stride in 4-byte words

@@ -632,7 +632,8 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
         o.rank >= (1u << 24) || o.burn_in < 1 || o.max_host_add < 0 ||
         (o.state_dtype != RPL_F32 && o.state_dtype != RPL_U8) ||
         (o.sampling != RPL_SAMPLE_UNIFORM && o.sampling != RPL_SAMPLE_DISTINCT) ||
-        (o.state_sharing != 0 && o.state_sharing != 1)) {
+        (o.state_sharing != 0 && o.state_sharing != 1) ||
+        (o.ring_memory != RPL_RING_DEVICE && o.ring_memory != RPL_RING_HOST)) {
         set_error("replay_create: invalid argument (capacity=%lld state_dim=%d rank=%u burn_in=%lld)",
                   (long long)capacity, state_dim, o.rank, (long long)o.burn_in);
         return RPL_EINVAL;
@@ -668,13 +669,27 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
     if (u8) rp->no_defer = true;   // deferral is a fast-path (fp32 states) feature
     rp->distinct = o.sampling == RPL_SAMPLE_DISTINCT;
     const size_t ring_bytes = (size_t)capacity * rp->ring.rs * sizeof(float);
-    cudaError_t e = cudaMalloc(&rp->ring.rows, ring_bytes);
-    if (e != cudaSuccess) {
-        size_t fr = 0, tot = 0;
-        cudaMemGetInfo(&fr, &tot);
-        set_error("replay_create: cudaMalloc of %zu ring bytes failed (%zu free)", ring_bytes, fr);
-        delete rp;
-        return RPL_ENOMEM;
+    rp->ring.host = o.ring_memory == RPL_RING_HOST ? 1 : 0;
+    if (rp->ring.host) {
+        // in-RAM comparison mode: pinned host rows the kernels address directly (UVA)
+        if (cudaHostAlloc(&rp->ring.rows, ring_bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            rp->ring.rows = nullptr;
+            set_error("replay_create: cudaHostAlloc of %zu pinned ring bytes failed", ring_bytes);
+            delete rp;
+            return RPL_ENOMEM;
+        }
+        std::memset(rp->ring.rows, 0, ring_bytes);
+    } else {
+        cudaError_t e = cudaMalloc(&rp->ring.rows, ring_bytes);
+        if (e != cudaSuccess) {
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            set_error("replay_create: cudaMalloc of %zu ring bytes failed (%zu free)", ring_bytes, fr);
+            rp->ring.rows = nullptr;
+            delete rp;
+            return RPL_ENOMEM;
+        }
     }
     const size_t st = host_add_bytes(rp->max_host_add, state_dim, u8) + 64;
     bool ok = cudaMalloc(&rp->err_dev, sizeof(uint32_t)) == cudaSuccess &&
@@ -686,7 +701,7 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
              cudaEventCreateWithFlags(&rp->staged[i], cudaEventDisableTiming) == cudaSuccess;
     }
     if (!ok || cudaMemsetAsync(rp->err_dev, 0, sizeof(uint32_t), rp->stream) != cudaSuccess ||
-        cudaMemsetAsync(rp->ring.rows, 0, ring_bytes, rp->stream) != cudaSuccess) {
+        (!rp->ring.host && cudaMemsetAsync(rp->ring.rows, 0, ring_bytes, rp->stream) != cudaSuccess)) {
         set_error("replay_create: staging allocation of %zu bytes failed", st);
         replay_destroy(rp);
         return RPL_ENOMEM;
@@ -710,7 +725,10 @@ extern "C" int replay_destroy(rpl_replay *rp)
     if (rp->err_dev) cudaFree(rp->err_dev);
     if (rp->ctrl_dev) cudaFree(rp->ctrl_dev);
     if (rp->ds_idx) cudaFree(rp->ds_idx);
-    if (rp->ring.rows) cudaFree(rp->ring.rows);
+    if (rp->ring.rows) {
+        if (rp->ring.host) cudaFreeHost(rp->ring.rows);
+        else cudaFree(rp->ring.rows);
+    }
     delete rp;
     return RPL_OK;
 }
