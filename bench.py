@@ -455,6 +455,23 @@ def run_ours(a, batch, first_line=True):
             ins.append(row)
         gather["insert_sweep"] = ins
         rp.check()
+        # P:73 / Fig. 3 proper: single host experiences through the update-size queue
+        # (update_size U): wall time per replay_add call, block transfers included
+        upd = []
+        one = experiences(20_000, seed=14, rank=rank)
+        for U in (1, 10, 100, 2000, 10_000):
+            rq = binding.Replay(20_000, 27, device=local, update_size=U)
+            rows = [{kx: v[i:i + 1] for kx, v in one.items()} for i in range(20_000)]
+            for i in range(2000):
+                rq.add(**rows[i])
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for i in range(20_000):
+                rq.add(**rows[i])
+            torch.cuda.synchronize()
+            upd.append({"update_size": U, "us_per_add": (time.perf_counter() - t0) / 20_000 * 1e6})
+            rq.close()
+        gather["update_size_sweep"] = upd
 
     # ---- CPU oracle baseline (rank 0, N=1 only) ------------------------------------------
     cpu = None

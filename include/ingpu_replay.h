@@ -85,6 +85,16 @@ typedef struct {
                              memory, so every sample / gather / train step reads its batch
                              across PCIe -- the per-step transfer the in-GPU replay removes.
                              The kernels, sampler and results are identical              */
+    int64_t update_size;  /* 0 (default): every replay_add is one insert, visible at once.
+                             U > 0: P:73 block updates ("Experiences are queued in RAM until
+                             the queue has enough experiences to update the next block";
+                             P:119 uses U = 2,000): RPL_HOST experiences wait in a host queue
+                             and every U of them become one insert (one H2D transfer of
+                             U*(8*state_dim+9) bytes); queued experiences are not part of
+                             the replay (never sampled, not in size / cursor / total) until
+                             their block is written or replay_flush_queue writes a partial
+                             block.  Device-sourced adds are rejected (EINVAL) in this mode.
+                             U <= capacity; U > max_host_add raises max_host_add to U      */
 } rpl_replay_opts;
 
 /* Create an empty FIFO replay of `capacity` experiences whose states are `state_dim`
@@ -152,6 +162,11 @@ int replay_sample(rpl_replay *replay, int32_t batch, const rpl_batch *out);
  * in [0, size); out-of-range indices are clamped and raise the sticky EINVAL flag).
  * No sampler event is consumed.  Used for the gather-bandwidth measurement. */
 int replay_gather(rpl_replay *replay, int64_t n, const int32_t *idx_dev, const rpl_batch *out);
+
+/* update_size > 0 only: write the k < U queued experiences as a partial block (a no-op when
+ * none wait); *flushed (may be NULL) = k.  replay_queued reports how many wait. */
+int replay_flush_queue(rpl_replay *replay, int64_t *flushed);
+int replay_queued(const rpl_replay *replay, int64_t *queued);
 
 /* Host mirror of the ring state; no synchronisation. */
 int replay_size(const rpl_replay *replay, int64_t *size);

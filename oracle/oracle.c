@@ -175,6 +175,68 @@ int oracle_ring_add(oracle_ring *ring, int64_t k, const float *s, const int32_t 
     return ORACLE_OK;
 }
 
+/* ---- P:73 block-update queue ------------------------------------------------------------ */
+int oracle_queue_init(oracle_queue *q, int64_t update_size, int32_t state_dim)
+{
+    if (update_size < 1 || state_dim < 1) return ORACLE_EINVAL;
+    q->update_size = update_size;
+    q->queued = 0;
+    q->state_dim = state_dim;
+    q->s = (float *)calloc((size_t)update_size * state_dim, sizeof(float));
+    q->s_next = (float *)calloc((size_t)update_size * state_dim, sizeof(float));
+    q->r = (float *)calloc((size_t)update_size, sizeof(float));
+    q->a = (int32_t *)calloc((size_t)update_size, sizeof(int32_t));
+    q->done = (uint8_t *)calloc((size_t)update_size, 1);
+    if (!q->s || !q->s_next || !q->r || !q->a || !q->done) return ORACLE_ENOMEM;
+    return ORACLE_OK;
+}
+
+void oracle_queue_free(oracle_queue *q)
+{
+    free(q->s); free(q->s_next); free(q->r); free(q->a); free(q->done);
+    q->s = q->s_next = q->r = NULL;
+    q->a = NULL;
+    q->done = NULL;
+}
+
+/* append the k experiences one at a time; whenever U are waiting they become the next block
+ * (one oracle_ring_add of U).  done[j] > 1 anywhere rejects the whole call before any append;
+ * k > capacity is rejected as for oracle_ring_add.  s_next may be NULL for a shared ring. */
+int oracle_queue_add(oracle_queue *q, oracle_ring *ring, int64_t k, const float *s,
+                     const int32_t *a, const float *r, const float *s_next, const uint8_t *done)
+{
+    const int32_t D = q->state_dim;
+    if (k < 0 || k > ring->capacity || D != ring->state_dim) return ORACLE_EINVAL;
+    for (int64_t j = 0; j < k; ++j)
+        if (done[j] > 1) return ORACLE_ECORRUPT;
+    for (int64_t j = 0; j < k; ++j) {
+        const int64_t t = q->queued;
+        for (int32_t d = 0; d < D; ++d) q->s[t * D + d] = s[j * D + d];
+        for (int32_t d = 0; d < D; ++d) q->s_next[t * D + d] = s_next ? s_next[j * D + d] : 0.0f;
+        q->a[t] = a[j];
+        q->r[t] = r[j];
+        q->done[t] = done[j];
+        q->queued = t + 1;
+        if (q->queued == q->update_size) {
+            const int rc = oracle_ring_add(ring, q->update_size, q->s, q->a, q->r, q->s_next, q->done);
+            if (rc != ORACLE_OK) return rc;
+            q->queued = 0;
+        }
+    }
+    return ORACLE_OK;
+}
+
+/* write the k < U waiting experiences as a partial block; returns k (>= 0) or an error */
+int64_t oracle_queue_flush(oracle_queue *q, oracle_ring *ring)
+{
+    const int64_t k = q->queued;
+    if (k == 0) return 0;
+    const int rc = oracle_ring_add(ring, k, q->s, q->a, q->r, q->s_next, q->done);
+    if (rc != ORACLE_OK) return rc;
+    q->queued = 0;
+    return k;
+}
+
 /* gather the rows idx[0..B) and unpack them into five tensors ("the sampled
  * experiences are unpacked into old state, new state, action, reward and is_terminal").
  * Physical slot = logical index (reading Q4). */

@@ -47,6 +47,24 @@ int oracle_ring_sample(oracle_ring *ring, int64_t burn_in, uint64_t seed, uint32
                        int32_t batch, int32_t *idx, float *s, int32_t *a, float *r,
                        float *s_next, uint8_t *done);
 
+/* P:73 block updates: "Experiences are queued in RAM until the queue has enough experiences
+ * to update the next block" -- up to update_size experiences wait in front of a ring and are
+ * written to it as one block; queued experiences are not part of the replay */
+typedef struct {
+    int64_t update_size; /* U: block size */
+    int64_t queued;      /* experiences waiting, < U after every call */
+    int32_t state_dim;
+    float *s, *s_next, *r;
+    int32_t *a;
+    uint8_t *done;
+} oracle_queue;
+
+int oracle_queue_init(oracle_queue *q, int64_t update_size, int32_t state_dim);
+void oracle_queue_free(oracle_queue *q);
+int oracle_queue_add(oracle_queue *q, oracle_ring *ring, int64_t k, const float *s,
+                     const int32_t *a, const float *r, const float *s_next, const uint8_t *done);
+int64_t oracle_queue_flush(oracle_queue *q, oracle_ring *ring);
+
 /* byte-state replay (SURVEY config 5) */
 typedef struct {
     int64_t capacity;

@@ -119,6 +119,13 @@ def _declare(L):
     L.oracle_ring_set_shared.restype = C.c_int
     L.oracle_ring_add.argtypes = [C.POINTER(_Ring), C.c_int64, _P, _P, _P, _P, _P]
     L.oracle_ring_add.restype = C.c_int
+    L.oracle_queue_init.argtypes = [C.POINTER(_Queue), C.c_int64, C.c_int32]
+    L.oracle_queue_init.restype = C.c_int
+    L.oracle_queue_free.argtypes = [C.POINTER(_Queue)]
+    L.oracle_queue_add.argtypes = [C.POINTER(_Queue), C.POINTER(_Ring), C.c_int64, _P, _P, _P, _P, _P]
+    L.oracle_queue_add.restype = C.c_int
+    L.oracle_queue_flush.argtypes = [C.POINTER(_Queue), C.POINTER(_Ring)]
+    L.oracle_queue_flush.restype = C.c_int64
     L.oracle_ring_gather.argtypes = [C.POINTER(_Ring), C.c_int32, _P, _P, _P, _P, _P, _P]
     L.oracle_ring_gather.restype = C.c_int
     L.oracle_ring_sample.argtypes = [C.POINTER(_Ring), C.c_int64, C.c_uint64, C.c_uint32,
@@ -190,9 +197,28 @@ def sample_distinct(seed: int, rank: int, event: int, n: int, batch: int) -> np.
 # ------------------------------------------------------------------------------------
 # The replay ring (paper layout: packed 2D+3 floats per row)
 # ------------------------------------------------------------------------------------
+class _Queue(C.Structure):
+    _fields_ = [
+        ("update_size", C.c_int64),
+        ("queued", C.c_int64),
+        ("state_dim", C.c_int32),
+        ("s", C.POINTER(C.c_float)),
+        ("s_next", C.POINTER(C.c_float)),
+        ("r", C.POINTER(C.c_float)),
+        ("a", C.POINTER(C.c_int32)),
+        ("done", C.POINTER(C.c_uint8)),
+    ]
+
+
 class Ring:
     def __init__(self, capacity: int, state_dim: int, distinct: bool = False,
-                 shared: bool = False):
+                 shared: bool = False, update_size: int = 0):
+        self._q = None
+        if update_size:   # P:73 block updates through oracle_queue_*
+            self._q = _Queue()
+            rc = lib().oracle_queue_init(C.byref(self._q), update_size, state_dim)
+            if rc != OK:
+                raise ValueError(f"oracle_queue_init rc={rc}")
         self._r = _Ring()
         rc = lib().oracle_ring_init(C.byref(self._r), capacity, state_dim)
         if rc != OK:
@@ -205,10 +231,20 @@ class Ring:
     def __del__(self):
         if getattr(self, "_r", None) is not None and self._r.rows:
             lib().oracle_ring_free(C.byref(self._r))
+        if getattr(self, "_q", None) is not None and self._q.s:
+            lib().oracle_queue_free(C.byref(self._q))
 
     @property
     def capacity(self):
         return self._r.capacity
+
+    @property
+    def queued(self):
+        return self._q.queued if self._q is not None else 0
+
+    def flush_queue(self) -> int:
+        """Write the waiting experiences as a partial block; returns how many."""
+        return lib().oracle_queue_flush(C.byref(self._q), C.byref(self._r)) if self._q is not None else 0
 
     @property
     def cursor(self):
@@ -244,6 +280,9 @@ class Ring:
         r = _c(r, np.float32)
         s_next = _c(s_next, np.float32).reshape(-1, D) if s_next is not None else None
         done = _c(done, np.uint8)
+        if self._q is not None:
+            return lib().oracle_queue_add(C.byref(self._q), C.byref(self._r), k, _ptr(s), _ptr(a),
+                                          _ptr(r), _ptr(s_next), _ptr(done))
         return lib().oracle_ring_add(C.byref(self._r), k, _ptr(s), _ptr(a), _ptr(r),
                                      _ptr(s_next), _ptr(done))
 

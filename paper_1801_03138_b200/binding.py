@@ -33,7 +33,8 @@ RPL_RING_DEVICE, RPL_RING_HOST = 0, 1
 
 EXPORTS = [
     "replay_create", "replay_destroy", "replay_add", "replay_sample", "replay_gather",
-    "replay_size", "replay_state", "dqn_param_count", "dqn_create", "dqn_destroy",
+    "replay_size", "replay_state", "replay_flush_queue", "replay_queued", "dqn_param_count",
+    "dqn_create", "dqn_destroy",
     "dqn_train_step", "sync_target", "dqn_get_params", "dqn_set_params", "dqn_step_count",
     "dqn_debug_export", "rpl_nccl_unique_id", "dqn_attach_nccl", "rpl_check",
     "rpl_last_error", "rpl_kernel_launches",
@@ -50,7 +51,7 @@ class _ReplayOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("cuda_stream", C.c_void_p), ("burn_in", C.c_int64),
                 ("seed", C.c_uint64), ("rank", C.c_uint32), ("max_host_add", C.c_int64),
                 ("state_dtype", C.c_int32), ("sampling", C.c_int32), ("state_sharing", C.c_int32),
-                ("ring_memory", C.c_int32)]
+                ("ring_memory", C.c_int32), ("update_size", C.c_int64)]
 
 
 class _Batch(C.Structure):
@@ -80,6 +81,8 @@ def _load():
         "replay_sample": (C.c_int, [P, i32, C.POINTER(_Batch)]),
         "replay_gather": (C.c_int, [P, i64, P, C.POINTER(_Batch)]),
         "replay_size": (C.c_int, [P, C.POINTER(i64)]),
+        "replay_flush_queue": (C.c_int, [P, C.POINTER(i64)]),
+        "replay_queued": (C.c_int, [P, C.POINTER(i64)]),
         "replay_state": (C.c_int, [P, C.POINTER(i64), C.POINTER(i64), C.POINTER(u64),
                                    C.POINTER(u64), C.POINTER(u64)]),
         "dqn_param_count": (C.c_int, [C.POINTER(_DqnConfig), C.POINTER(i64)]),
@@ -149,7 +152,7 @@ class Replay:
     def __init__(self, capacity: int, state_dim: int, *, device: int = 0, stream=None,
                  burn_in: int = 1, seed: int = 2, rank: int = 0, max_host_add: int = 0,
                  state_dtype: str = "f32", sampling: str = "uniform", shared_state: bool = False,
-                 ring_memory: str = "device"):
+                 ring_memory: str = "device", update_size: int = 0):
         torch = _torch()
         if not torch.cuda.is_available():
             raise RplError(RPL_ECUDA, "no CUDA device (the in-GPU replay has no CPU fallback)")
@@ -162,7 +165,7 @@ class Replay:
         o = _ReplayOpts(device, self._stream, burn_in, seed, rank, max_host_add,
                         RPL_U8 if self.u8 else RPL_F32, 1 if sampling == "distinct" else 0,
                         1 if shared_state else 0,
-                        RPL_RING_HOST if ring_memory == "host" else RPL_RING_DEVICE)
+                        RPL_RING_HOST if ring_memory == "host" else RPL_RING_DEVICE, update_size)
         self.shared_state = shared_state
         self.ring_memory = ring_memory
         h = C.c_void_p()
@@ -249,6 +252,19 @@ class Replay:
     def size(self) -> int:
         v = C.c_int64()
         _ok(_L.replay_size(self._h, C.byref(v)))
+        return v.value
+
+    @property
+    def queued(self) -> int:
+        """Experiences waiting in the update-size queue (update_size > 0)."""
+        v = C.c_int64()
+        _ok(_L.replay_queued(self._h, C.byref(v)))
+        return v.value
+
+    def flush_queue(self) -> int:
+        """replay_flush_queue: write the queued experiences as a partial block."""
+        v = C.c_int64()
+        _ok(_L.replay_flush_queue(self._h, C.byref(v)))
         return v.value
 
     def state(self) -> dict:

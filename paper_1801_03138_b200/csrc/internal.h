@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/ingpu_replay.h"
 
@@ -78,6 +79,12 @@ struct rpl_replay {
     int64_t burn_in = 1;
     uint64_t seed = 2;
     uint32_t rank = 0;
+    // P:73 update-size queue (update_size > 0): host experiences waiting for their block,
+    // SoA like replay_add's inputs
+    int64_t qU = 0, qk = 0;
+    std::vector<uint8_t> qs, qs2, qdone;
+    std::vector<int32_t> qa;
+    std::vector<float> qr;
     // host mirror of the ring state (exact: every add is host-initiated with a known k)
     int64_t cursor = 0, size = 0;
     uint64_t total = 0, events = 0, h2d_bytes = 0;

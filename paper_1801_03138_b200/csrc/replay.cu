@@ -3,6 +3,7 @@
 //
 // Paper: P:71-75 [Methods] (packed 1,000,000 x 57 Variable, block inserts, uniform integer
 // sampling + gather + unpack), P:44 (FIFO, burn-in).  B200 design: DESIGN.md "Kernels".
+#include <algorithm>
 #include <cstdarg>
 #include <cstdlib>
 #include <cstring>
@@ -633,7 +634,8 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
         (o.state_dtype != RPL_F32 && o.state_dtype != RPL_U8) ||
         (o.sampling != RPL_SAMPLE_UNIFORM && o.sampling != RPL_SAMPLE_DISTINCT) ||
         (o.state_sharing != 0 && o.state_sharing != 1) ||
-        (o.ring_memory != RPL_RING_DEVICE && o.ring_memory != RPL_RING_HOST)) {
+        (o.ring_memory != RPL_RING_DEVICE && o.ring_memory != RPL_RING_HOST) ||
+        o.update_size < 0 || o.update_size > capacity) {
         set_error("replay_create: invalid argument (capacity=%lld state_dim=%d rank=%u burn_in=%lld)",
                   (long long)capacity, state_dim, o.rank, (long long)o.burn_in);
         return RPL_EINVAL;
@@ -658,6 +660,23 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
     const int64_t cap_rows = (int64_t)((256ull << 20) / host_add_bytes(1, state_dim, u8));
     if (rp->max_host_add > cap_rows) rp->max_host_add = cap_rows > 0 ? cap_rows : 1;
     if (rp->max_host_add > capacity) rp->max_host_add = capacity;
+    if (o.update_size > 0) {
+        // P:73 block updates: a block of U is one host add, so staging must hold U
+        if (o.update_size > cap_rows) {
+            set_error("replay_create: update_size %lld exceeds the %lld-experience staging",
+                      (long long)o.update_size, (long long)cap_rows);
+            delete rp;
+            return RPL_EINVAL;
+        }
+        if (rp->max_host_add < o.update_size) rp->max_host_add = o.update_size;
+        const size_t sb = (size_t)o.update_size * state_dim * (u8 ? 1 : 4);
+        rp->qU = o.update_size;
+        rp->qs.resize(sb);
+        rp->qs2.resize(o.state_sharing ? 0 : sb);
+        rp->qa.resize(o.update_size);
+        rp->qr.resize(o.update_size);
+        rp->qdone.resize(o.update_size);
+    }
     rp->ring.capacity = capacity;
     rp->ring.D = state_dim;
     rp->ring.u8 = u8 ? 1 : 0;
@@ -733,10 +752,77 @@ extern "C" int replay_destroy(rpl_replay *rp)
     return RPL_OK;
 }
 
+static int add_rows(rpl_replay *rp, int64_t k, const void *s, const int32_t *a, const float *r,
+                    const void *s_next, const uint8_t *done, int mem);
+
 extern "C" int replay_add(rpl_replay *rp, int64_t k, const void *s, const int32_t *a,
                           const float *r, const void *s_next, const uint8_t *done, int mem)
 {
     if (!rp) { set_error("replay_add: null handle"); return RPL_EINVAL; }
+    if (rp->qU == 0) return add_rows(rp, k, s, a, r, s_next, done, mem);
+    // P:73 block updates: append to the host queue; every U queued experiences are one insert
+    if (mem != RPL_HOST) {
+        set_error("replay_add: update_size > 0 queues host experiences only (mem=%d)", mem);
+        return RPL_EINVAL;
+    }
+    if (k < 0 || k > rp->ring.capacity) {
+        set_error("replay_add: invalid k=%lld (capacity %lld)", (long long)k, (long long)rp->ring.capacity);
+        return RPL_EINVAL;
+    }
+    if (k == 0) return RPL_OK;
+    if (!s || !a || !r || (!s_next && !rp->ring.shared) || !done) {
+        set_error("replay_add: null input pointer");
+        return RPL_EINVAL;
+    }
+    for (int64_t j = 0; j < k; ++j)
+        if (done[j] > 1) {
+            set_error("replay_add: done[%lld]=%u not in {0,1}", (long long)j, done[j]);
+            return RPL_ECORRUPT;
+        }
+    const size_t es = (size_t)rp->ring.D * (rp->ring.u8 ? 1 : 4);   // bytes of one state
+    int64_t j = 0;
+    while (j < k) {
+        const int64_t m = std::min(k - j, rp->qU - rp->qk);
+        std::memcpy(rp->qs.data() + rp->qk * es, (const char *)s + j * es, m * es);
+        if (!rp->ring.shared) std::memcpy(rp->qs2.data() + rp->qk * es, (const char *)s_next + j * es, m * es);
+        std::memcpy(rp->qa.data() + rp->qk, a + j, m * 4);
+        std::memcpy(rp->qr.data() + rp->qk, r + j, m * 4);
+        std::memcpy(rp->qdone.data() + rp->qk, done + j, m);
+        rp->qk += m;
+        j += m;
+        if (rp->qk == rp->qU) {
+            if (int rc = add_rows(rp, rp->qU, rp->qs.data(), rp->qa.data(), rp->qr.data(),
+                                  rp->ring.shared ? nullptr : rp->qs2.data(), rp->qdone.data(), RPL_HOST))
+                return rc;
+            rp->qk = 0;
+        }
+    }
+    return RPL_OK;
+}
+
+extern "C" int replay_flush_queue(rpl_replay *rp, int64_t *flushed)
+{
+    if (!rp) return RPL_EINVAL;
+    const int64_t k = rp->qk;
+    if (flushed) *flushed = k;
+    if (k == 0) return RPL_OK;
+    if (int rc = add_rows(rp, k, rp->qs.data(), rp->qa.data(), rp->qr.data(),
+                          rp->ring.shared ? nullptr : rp->qs2.data(), rp->qdone.data(), RPL_HOST))
+        return rc;
+    rp->qk = 0;
+    return RPL_OK;
+}
+
+extern "C" int replay_queued(const rpl_replay *rp, int64_t *queued)
+{
+    if (!rp || !queued) return RPL_EINVAL;
+    *queued = rp->qk;
+    return RPL_OK;
+}
+
+static int add_rows(rpl_replay *rp, int64_t k, const void *s, const int32_t *a, const float *r,
+                    const void *s_next, const uint8_t *done, int mem)
+{
     const int32_t D = rp->ring.D;
     if (k < 0 || k > rp->ring.capacity ||
         (mem != RPL_HOST && mem != RPL_DEVICE && mem != RPL_DEVICE_DEFER)) {

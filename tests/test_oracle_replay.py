@@ -191,3 +191,61 @@ def test_shared_state_sampler_brute_force(distinct):
             assert np.array_equal(b["s"][i], e["s"][src])
             assert np.array_equal(b["s_next"][i], e["s"][src + 1])   # the next experience's s
             assert b["a"][i] == e["a"][src] and b["done"][i] == e["done"][src]
+
+
+# ---- P:73 block updates (update-size queue) ---------------------------------------------------
+def test_queue_blocks_match_bounded_deque_brute_force():
+    # "Experiences are queued in RAM until the queue has enough experiences to update the
+    # next block"; brute force: a list queue in front of a bounded deque of written experiences,
+    # ragged add sizes (some spanning several blocks) and explicit partial flushes
+    import collections
+    C, D, U = 12, 5, 4
+    ring = oracle.Ring(C, D, update_size=U)
+    e = experiences(200, state_dim=D, seed=21)
+    queue, written = [], collections.deque(maxlen=C)
+    t = 0
+    for step, k in enumerate([1, 2, 3, 4, 9, 1, 12, 5, 3, 0, 7, 2, 11]):
+        part = {kk: v[t:t + k] for kk, v in e.items()}
+        assert ring.add(**part) == oracle.OK
+        for j in range(k):
+            queue.append(t + j)
+            if len(queue) == U:
+                written.extend(queue)
+                queue = []
+        t += k
+        if step % 4 == 3:   # explicit partial flush
+            n = ring.flush_queue()
+            assert n == len(queue)
+            written.extend(queue)
+            queue = []
+        assert ring.queued == len(queue) and ring.size == len(written)
+        # ring slots hold the written experiences in FIFO order from the cursor
+        g = ring.gather(np.arange(ring.size, dtype=np.int32))
+        for i in range(ring.size):
+            src = list(written)[(i - ring.cursor) % ring.size] if ring.size == C else list(written)[i]
+            assert np.array_equal(g["s"][i], e["s"][src]) and g["a"][i] == e["a"][src]
+
+
+def test_queue_2000_adds_make_exactly_one_block():
+    # P:119 update-size 2,000 with 27-float states: nothing is visible until the 2000th add
+    ring = oracle.Ring(10_000, 27, update_size=2000)
+    e = experiences(2000, seed=22)
+    for i in range(1999):
+        assert ring.add(**{k: v[i:i + 1] for k, v in e.items()}) == oracle.OK
+    assert ring.size == 0 and ring.queued == 1999 and ring.total == 0
+    assert ring.add(**{k: v[1999:] for k, v in e.items()}) == oracle.OK
+    assert ring.size == 2000 and ring.queued == 0 and ring.total == 2000 and ring.cursor == 2000
+
+
+def test_queue_staged_experiences_are_never_sampled():
+    # queued experiences are not part of the replay: the sampler draws over the written ones
+    ring = oracle.Ring(100, 3, update_size=10)
+    e = experiences(25, state_dim=3, seed=23)
+    ring.add(**e)   # 2 blocks written, 5 queued
+    assert ring.size == 20 and ring.queued == 5
+    rc, b = ring.sample(1, 2, 0, 512)
+    assert rc == oracle.OK and b["idx"].max() < 20
+    staged = {tuple(x) for x in e["s"][20:]}
+    assert not any(tuple(x) in staged for x in b["s"])
+    rc0 = ring.add(**{k: v[:1] for k, v in e.items()} | {"done": np.array([2], np.uint8)})
+    assert rc0 == oracle.ECORRUPT and ring.queued == 5   # nothing queued on a rejected add
