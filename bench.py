@@ -55,6 +55,9 @@ def parse():
                     help="store one state per experience (P:141): s' = the next slot's s")
     ap.add_argument("--distinct", action="store_true",
                     help="sample distinct indices (RPL_SAMPLE_DISTINCT, P:75's planned switch)")
+    ap.add_argument("--precision", choices=["fp32", "tf32", "bf16"], default="fp32",
+                    help="tensor-core products: fp32 (FP32-accurate splits, the default and the "
+                         "judged line) or one tf32 / bf16 product (reduced precision, parity 2e-2)")
     ap.add_argument("--ring", choices=["device", "host"], default="device",
                     help="host: the in-RAM comparison mode (SURVEY NEXT-1): ring rows in pinned host "
                          "memory, every batch read across PCIe by the same kernels")
@@ -62,6 +65,9 @@ def parse():
                     help="c2: BASELINE configs[1] (default); c5: configs[4] 84x84x4 uint8 states, "
                          "batch 256 (other flags' defaults: --batch 256)")
     return ap.parse_args()
+
+
+DTYPE = {"fp32": "f32", "tf32": "tf32", "bf16": "bf16"}
 
 
 def dist_env():
@@ -84,10 +90,11 @@ def make_cfg(a, binding, batch):
         return binding.DQNConfig(state_dim=27, n_actions=8, dueling=True, hidden=(128,), stream=512,
                                  double_dqn=a.ddqn, gamma=0.99, lr=1e-4, huber_kappa=1.0,
                                  sync_period=10_000, max_batch=max(batch, 128),
-                                 avg_period=a.avg_period)
+                                 avg_period=a.avg_period, precision=a.precision)
     return binding.DQNConfig(state_dim=27, n_actions=8, dueling=False, hidden=(64, 64),
                              double_dqn=a.ddqn, gamma=0.99, lr=1e-4, huber_kappa=1.0,
-                             sync_period=10_000, max_batch=max(batch, 128), avg_period=a.avg_period)
+                             sync_period=10_000, max_batch=max(batch, 128), avg_period=a.avg_period,
+                             precision=a.precision)
 
 
 def oracle_net_of(cfg):
@@ -485,7 +492,7 @@ def run_ours(a, batch, first_line=True):
     line = {
         "metric": METRIC, "value": value, "unit": "train_steps/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "vs_baseline": None, "dtype": DTYPE[a.precision], "data": "synthetic",
         "config": {"workload": workload_name(a, batch), "batch": batch, "capacity": a.capacity,
                    "net": a.net, "double_dqn": a.ddqn, "adds_per_step": k,
                    "sampling": "distinct" if a.distinct else "uniform (with replacement, P:75)",
@@ -518,10 +525,10 @@ C5_ROW_BYTES = 56576      # device row: round_up(round_up(2 * C5_D, 16) + 12, 12
 C5_ROW_BYTES_SHARED = 28288   # one state per row: round_up(round_up(C5_D, 16) + 12, 128)
 
 
-def c5_cfg(binding, batch, ddqn):
+def c5_cfg(binding, batch, ddqn, precision="fp32"):
     return binding.DQNConfig(state_dim=C5_D, n_actions=8, dueling=True, hidden=(128,), stream=512,
                              double_dqn=ddqn, gamma=0.99, lr=1e-4, huber_kappa=1.0,
-                             sync_period=10_000, max_batch=batch)
+                             sync_period=10_000, max_batch=batch, precision=precision)
 
 
 def time_oracle_c5(batch, ddqn, seconds, pool):
@@ -564,7 +571,7 @@ def run_c5(a):
     stream = torch.cuda.current_stream()
     peaks, peaks_kind = load_peaks()
     batch = a.batch if a.batch != 128 else 256
-    cfg = c5_cfg(binding, batch, a.ddqn)
+    cfg = c5_cfg(binding, batch, a.ddqn, a.precision)
     rp = binding.Replay(a.capacity, C5_D, device=local, burn_in=1, seed=2, rank=rank,
                         state_dtype="u8", shared_state=a.shared_state,
                         sampling="distinct" if a.distinct else "uniform")
@@ -714,7 +721,7 @@ def run_c5(a):
                   "(BASELINE configs[4]); gather GB/s vs HBM peak",
         "value": value, "unit": "train_steps/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "vs_baseline": None, "dtype": DTYPE[a.precision], "data": "synthetic",
         "config": {"workload": f"BASELINE configs[4]: {a.capacity:,}-slot replay of 84x84x4 uint8 "
                                f"states ({a.capacity * (C5_ROW_BYTES_SHARED if a.shared_state else C5_ROW_BYTES) / 1e9:.1f} GB ring"
                                f"{', shared states' if a.shared_state else ''}), "

@@ -51,6 +51,7 @@ enum { RPL_ONLINE = 0, RPL_TARGET = 1, RPL_GRAD = 2 };  /* which parameter vecto
 enum { RPL_F32 = 0, RPL_U8 = 1 };                        /* state element type of a replay  */
 enum { RPL_SAMPLE_UNIFORM = 0, RPL_SAMPLE_DISTINCT = 1 }; /* sampler of a replay            */
 enum { RPL_RING_DEVICE = 0, RPL_RING_HOST = 1 };          /* where a replay's rows live      */
+enum { RPL_PREC_FP32 = 0, RPL_PREC_TF32 = 1, RPL_PREC_BF16 = 2 };   /* learner precision   */
 
 typedef struct rpl_replay rpl_replay;   /* opaque */
 typedef struct rpl_dqn rpl_dqn;         /* opaque */
@@ -199,6 +200,13 @@ typedef struct {
                              target parameters are averaged over ranks after every K-th step
                              (P:144's "synchronized periodically" / iterative parameter
                              mixing, reading Q31)                                           */
+    int32_t precision;    /* tensor-core products of the fast path and of the wide layer 0:
+                             RPL_PREC_FP32 (default): FP32-accurate (3xTF32 / bf16x3 splits,
+                             the 1e-5 parity of the north star); RPL_PREC_TF32: one product
+                             of tf32-rounded operands (wide layer 0: two bf16 terms of the
+                             weights); RPL_PREC_BF16: one product of bf16-rounded operands
+                             (a BF16 MMA's numerics; parity 2e-2, north star).  The
+                             cooperative (generic) kernel computes in FP32 SIMT in every mode */
 } rpl_dqn_config;
 
 /* Number of fp32 parameters of the blob layout:

@@ -27,6 +27,7 @@ RPL_HOST, RPL_DEVICE, RPL_DEVICE_DEFER = 0, 1, 2
 RPL_ONLINE, RPL_TARGET, RPL_GRAD = 0, 1, 2
 RPL_F32, RPL_U8 = 0, 1
 RPL_RING_DEVICE, RPL_RING_HOST = 0, 1
+RPL_PREC_FP32, RPL_PREC_TF32, RPL_PREC_BF16 = 0, 1, 2
 (RPL_DBG_IDX, RPL_DBG_S, RPL_DBG_S_NEXT, RPL_DBG_A, RPL_DBG_R, RPL_DBG_DONE, RPL_DBG_Q,
  RPL_DBG_QT_NEXT, RPL_DBG_QO_NEXT, RPL_DBG_Y, RPL_DBG_ASTAR, RPL_DBG_H, RPL_DBG_LOSS,
  RPL_DBG_TRACE) = range(14)
@@ -64,7 +65,8 @@ class _DqnConfig(C.Structure):
                 ("n_actions", C.c_int32), ("dueling", C.c_int32), ("n_hidden", C.c_int32),
                 ("hidden", C.c_int32 * 4), ("stream", C.c_int32), ("double_dqn", C.c_int32),
                 ("gamma", C.c_float), ("lr", C.c_float), ("huber_kappa", C.c_float),
-                ("sync_period", C.c_int64), ("max_batch", C.c_int32), ("avg_period", C.c_int64)]
+                ("sync_period", C.c_int64), ("max_batch", C.c_int32), ("avg_period", C.c_int64),
+                ("precision", C.c_int32)]
 
 
 def _load():
@@ -295,6 +297,7 @@ class DQNConfig:
     sync_period: int = 10_000
     max_batch: int = 4096
     avg_period: int = 0       # DP: 0 = gradient mean every step; K = parameter mean every K steps
+    precision: str = "fp32"   # "fp32" (FP32-accurate, default) | "tf32" | "bf16" (tensor-core products)
 
     def _c(self, device=0, stream=None) -> _DqnConfig:
         c = _DqnConfig()
@@ -309,6 +312,7 @@ class DQNConfig:
         c.gamma, c.lr, c.huber_kappa = self.gamma, self.lr, self.huber_kappa
         c.sync_period, c.max_batch = self.sync_period, self.max_batch
         c.avg_period = self.avg_period
+        c.precision = {"fp32": RPL_PREC_FP32, "tf32": RPL_PREC_TF32, "bf16": RPL_PREC_BF16}[self.precision]
         return c
 
     @property

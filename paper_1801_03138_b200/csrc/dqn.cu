@@ -798,7 +798,8 @@ static int config_layout(const rpl_dqn_config *c, rpl_dqn *d)
     if (!c || c->state_dim < 1 || c->n_actions < 1 || c->n_actions > MAXA || c->n_hidden < 1 ||
         c->n_hidden > 4 || !(c->gamma >= 0.0f && c->gamma <= 1.0f) || !(c->lr >= 0.0f) ||
         !(c->huber_kappa > 0.0f) || c->sync_period < 0 || c->max_batch < 1 ||
-        c->max_batch > (1 << 20) || (c->dueling && (c->stream < 1 || c->stream > 4096)))
+        c->max_batch > (1 << 20) || (c->dueling && (c->stream < 1 || c->stream > 4096)) ||
+        c->precision < RPL_PREC_FP32 || c->precision > RPL_PREC_BF16)
         return RPL_EINVAL;
     for (int l = 0; l < c->n_hidden; ++l)
         if (c->hidden[l] < 1 || c->hidden[l] > 4096) return RPL_EINVAL;
@@ -1205,6 +1206,7 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
 {
     memset(&p, 0, sizeof p);
     const rpl_dqn_config &c = d->cfg;
+    p.prec = c.precision;
     p.ring = rp->ring.rows;
     p.rs = rp->ring.rs;
     p.D = rp->ring.D;
@@ -1630,6 +1632,8 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             }
             w.ntile = (int)std::min<int64_t>(WD_MAXN, ((p.D + d->sms - 1) / d->sms + 15) / 16 * 16);
             w.wpre = wd_dw0_wpre(w.ntile) ? 1 : 0;
+            // bf16 terms of the fp32 weights / dZ0 per product: 3 (FP32), 2 (TF32), 1 (BF16)
+            w.nplanes = d->cfg.precision == RPL_PREC_BF16 ? 1 : d->cfg.precision == RPL_PREC_TF32 ? 2 : 3;
             w.trace = d->trace;
             w.do_db0 = d->wide_fast ? 1 : 0;
             w.b0 = d->boff[0];

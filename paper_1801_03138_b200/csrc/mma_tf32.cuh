@@ -25,6 +25,20 @@ __device__ __forceinline__ void tf32_split(float x, uint32_t &hi, uint32_t &lo)
     lo = __float_as_uint(x - __uint_as_float(hi));
 }
 
+// precision of a learner's tensor-core products (rpl_dqn_config.precision): 0 = FP32 (the
+// 3xTF32 split above), 1 = TF32 (one product of tf32-rounded operands), 2 = BF16 (one product
+// of bf16-rounded operands: exact in the fp32 accumulator, i.e. a BF16 MMA's numerics).  The
+// reduced modes leave lo = 0 and skip the correction products.
+__device__ __forceinline__ void split_p(float x, uint32_t &hi, uint32_t &lo, int prec)
+{
+    if (prec == 0) {
+        tf32_split(x, hi, lo);
+        return;
+    }
+    hi = prec == 2 ? (__float_as_uint(x) + 0x8000u) & 0xffff0000u : (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
+    lo = 0u;
+}
+
 __device__ __forceinline__ void mma_tf32(float c[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1)
 {
@@ -37,10 +51,12 @@ __device__ __forceinline__ void mma_tf32(float c[4], uint32_t a0, uint32_t a1, u
 
 // c += A(16x8) B(8x8) with both operands given as hi/lo pairs
 __device__ __forceinline__ void mma_3xtf32(float c[4], const uint32_t ah[4], const uint32_t al[4],
-                                           const uint32_t bh[2], const uint32_t bl[2])
+                                           const uint32_t bh[2], const uint32_t bl[2], int prec = 0)
 {
-    mma_tf32(c, al[0], al[1], al[2], al[3], bh[0], bh[1]);
-    mma_tf32(c, ah[0], ah[1], ah[2], ah[3], bl[0], bl[1]);
+    if (prec == 0) {
+        mma_tf32(c, al[0], al[1], al[2], al[3], bh[0], bh[1]);
+        mma_tf32(c, ah[0], ah[1], ah[2], ah[3], bl[0], bl[1]);
+    }
     mma_tf32(c, ah[0], ah[1], ah[2], ah[3], bh[0], bh[1]);
 }
 
@@ -48,10 +64,12 @@ __device__ __forceinline__ void mma_3xtf32(float c[4], const uint32_t ah[4], con
 // k-step); combine small terms first with acc3_sum.
 __device__ __forceinline__ void mma_3xtf32_sep(float chh[4], float chl[4], float clh[4],
                                                const uint32_t ah[4], const uint32_t al[4],
-                                               const uint32_t bh[2], const uint32_t bl[2])
+                                               const uint32_t bh[2], const uint32_t bl[2], int prec = 0)
 {
-    mma_tf32(clh, al[0], al[1], al[2], al[3], bh[0], bh[1]);
-    mma_tf32(chl, ah[0], ah[1], ah[2], ah[3], bl[0], bl[1]);
+    if (prec == 0) {
+        mma_tf32(clh, al[0], al[1], al[2], al[3], bh[0], bh[1]);
+        mma_tf32(chl, ah[0], ah[1], ah[2], ah[3], bl[0], bl[1]);
+    }
     mma_tf32(chh, ah[0], ah[1], ah[2], ah[3], bh[0], bh[1]);
 }
 __device__ __forceinline__ float acc3_sum(float hh, float hl, float lh) { return (lh + hl) + hh; }

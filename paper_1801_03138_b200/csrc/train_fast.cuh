@@ -90,6 +90,7 @@ struct FastArgs {
     int event_advanced;  // 1: the step's sampling kernel advanced rctrl[0] already
     uint32_t *err;
     unsigned long long *trace;   // optional per-CTA [kernel][cta][start, end] %globaltimer (ns)
+    int prec;            // rpl_dqn_config.precision (split_p / mma_3xtf32, mma_tf32.cuh)
 };
 
 __device__ __forceinline__ unsigned long long gtimer()
@@ -357,7 +358,7 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
                 const int rr = e / N0, cc = e - rr * N0;
                 const float h = rb + rr < B ? __ldcg(h0 + (int64_t)rr * N0 + cc) : 0.0f;
                 uint32_t hi, lo;
-                tf32_split(h, hi, lo);
+                split_p(h, hi, lo, p.prec);
                 H0h[rr * L.N0P + cc] = hi;
                 H0l[rr * L.N0P + cc] = lo;
             }
@@ -428,7 +429,7 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
                 const int rr = e / L.XP, d = e - rr * L.XP;
                 const float x = d < D ? Xs[e] : 0.0f;
                 uint32_t hi, lo;
-                tf32_split(x, hi, lo);
+                split_p(x, hi, lo, p.prec);
                 Xh[e] = hi;
                 Xl[e] = lo;
                 if (ut == 0 && net <= 1 && d < D && rb + rr < B)
@@ -453,9 +454,9 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
                     ah[3] = Xh[(g + 8) * L.XP + k0 + t + 4]; al[3] = Xl[(g + 8) * L.XP + k0 + t + 4];
                     const float w0 = k0 + t < D ? W0f[n * D + k0 + t] : 0.0f;
                     const float w1 = k0 + t + 4 < D ? W0f[n * D + k0 + t + 4] : 0.0f;
-                    tf32_split(w0, bh[0], bl[0]);
-                    tf32_split(w1, bh[1], bl[1]);
-                    mma_3xtf32(c, ah, al, bh, bl);
+                    split_p(w0, bh[0], bl[0], p.prec);
+                    split_p(w1, bh[1], bl[1], p.prec);
+                    mma_3xtf32(c, ah, al, bh, bl, p.prec);
                 }
                 const int col = nt * 8 + 2 * t;
 #pragma unroll
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
                     float h = c[q] + b0s[cc];
                     h = h > 0.0f ? h : 0.0f;
                     uint32_t hi, lo;
-                    tf32_split(h, hi, lo);
+                    split_p(h, hi, lo, p.prec);
                     H0h[rr * L.N0P + cc] = hi;
                     H0l[rr * L.N0P + cc] = lo;
                     if (net == 0 && ut == 0 && rb + rr < B) p.H0[(int64_t)(rb + rr) * N0 + cc] = h;
@@ -484,9 +485,9 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
                 ah[1] = H0h[(g + 8) * L.N0P + k0 + t]; al[1] = H0l[(g + 8) * L.N0P + k0 + t];
                 ah[2] = H0h[g * L.N0P + k0 + t + 4];   al[2] = H0l[g * L.N0P + k0 + t + 4];
                 ah[3] = H0h[(g + 8) * L.N0P + k0 + t + 4]; al[3] = H0l[(g + 8) * L.N0P + k0 + t + 4];
-                tf32_split(wrow[k0 + t], bh[0], bl[0]);
-                tf32_split(wrow[k0 + t + 4], bh[1], bl[1]);
-                mma_3xtf32(c, ah, al, bh, bl);
+                split_p(wrow[k0 + t], bh[0], bl[0], p.prec);
+                split_p(wrow[k0 + t + 4], bh[1], bl[1], p.prec);
+                mma_3xtf32(c, ah, al, bh, bl, p.prec);
             }
             const int col = nt * 8 + 2 * t;
 #pragma unroll
@@ -511,16 +512,16 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
                 for (int q = 0; q < 4; ++q) c[jt][q] = 0.0f;
             for (int k0 = warp * 8; k0 < UT; k0 += NW * 8) {
                 uint32_t ah[4], al[4], bh[2], bl[2];
-                tf32_split(H1s[g * L.UTP + k0 + t], ah[0], al[0]);
-                tf32_split(H1s[(g + 8) * L.UTP + k0 + t], ah[1], al[1]);
-                tf32_split(H1s[g * L.UTP + k0 + t + 4], ah[2], al[2]);
-                tf32_split(H1s[(g + 8) * L.UTP + k0 + t + 4], ah[3], al[3]);
+                split_p(H1s[g * L.UTP + k0 + t], ah[0], al[0], p.prec);
+                split_p(H1s[(g + 8) * L.UTP + k0 + t], ah[1], al[1], p.prec);
+                split_p(H1s[g * L.UTP + k0 + t + 4], ah[2], al[2], p.prec);
+                split_p(H1s[(g + 8) * L.UTP + k0 + t + 4], ah[3], al[3], p.prec);
 #pragma unroll
                 for (int jt = 0; jt < F_JT; ++jt) {
                     if (jt < JT) {
-                        tf32_split(Whs[(8 * jt + g) * L.UTP + k0 + t], bh[0], bl[0]);
-                        tf32_split(Whs[(8 * jt + g) * L.UTP + k0 + t + 4], bh[1], bl[1]);
-                        mma_3xtf32(c[jt], ah, al, bh, bl);
+                        split_p(Whs[(8 * jt + g) * L.UTP + k0 + t], bh[0], bl[0], p.prec);
+                        split_p(Whs[(8 * jt + g) * L.UTP + k0 + t + 4], bh[1], bl[1], p.prec);
+                        mma_3xtf32(c[jt], ah, al, bh, bl, p.prec);
                     }
                 }
             }
@@ -698,7 +699,7 @@ __device__ __forceinline__ float mm_at(const float *S, int r, int kk)
 template <bool kARc, bool kBRc, class EPI, class RSUM>
 __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int m0, int n0, int kb, int ke,
                                               const EPI &epi, bool want_rowsum, const RSUM &rs, float *smf,
-                                              CtaTrace *tr = nullptr, int mk = 0)
+                                              int prec, CtaTrace *tr = nullptr, int mk = 0)
 {
     // 8 warps = 2 (m16 halves of the tile) x 4 (k-step residues): warp (wm, wk) computes rows
     // 16 wm .. 16 wm + 15 x all K3N columns over the k-steps ks == wk (mod 4) of every pass --
@@ -734,17 +735,17 @@ __device__ __forceinline__ void gemm_mma_tile(const Opnd &a, const Opnd &b, int 
         for (int ks = wk; ks < ksteps; ks += 4) {
             const int k = 8 * ks;
             uint32_t ah[4], al[4];
-            tf32_split(mm_at<kARc>(As, mr, k + t), ah[0], al[0]);
-            tf32_split(mm_at<kARc>(As, mr + 8, k + t), ah[1], al[1]);
-            tf32_split(mm_at<kARc>(As, mr, k + t + 4), ah[2], al[2]);
-            tf32_split(mm_at<kARc>(As, mr + 8, k + t + 4), ah[3], al[3]);
+            split_p(mm_at<kARc>(As, mr, k + t), ah[0], al[0], prec);
+            split_p(mm_at<kARc>(As, mr + 8, k + t), ah[1], al[1], prec);
+            split_p(mm_at<kARc>(As, mr, k + t + 4), ah[2], al[2], prec);
+            split_p(mm_at<kARc>(As, mr + 8, k + t + 4), ah[3], al[3], prec);
 #pragma unroll
             for (int nt = 0; nt < NT8; ++nt) {
                 const int nc = 8 * nt + g;
                 uint32_t bh[2], bl[2];
-                tf32_split(mm_at<kBRc>(Bs, nc, k + t), bh[0], bl[0]);
-                tf32_split(mm_at<kBRc>(Bs, nc, k + t + 4), bh[1], bl[1]);
-                mma_3xtf32_sep(c[nt], cl[nt], cm[nt], ah, al, bh, bl);
+                split_p(mm_at<kBRc>(Bs, nc, k + t), bh[0], bl[0], prec);
+                split_p(mm_at<kBRc>(Bs, nc, k + t + 4), bh[1], bl[1], prec);
+                mma_3xtf32_sep(c[nt], cl[nt], cm[nt], ah, al, bh, bl, prec);
             }
         }
 #pragma unroll
@@ -828,7 +829,7 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             auto rs = [&](int m, float v) {
                 if (m < N1) gp[p.b1 + m] = v;
             };
-            gemm_mma_tile<true, true>(a, bo, m0, n0, kb, ke, epi, n0 == 0, rs, k3raw);
+            gemm_mma_tile<true, true>(a, bo, m0, n0, kb, ke, epi, n0 == 0, rs, k3raw, p.prec);
         } else if (t < n_w + n_h) {
             // dH0 partial [s][b][k] = sum_{u in split s} dZ1[b][u] W1[u][k]
             const int u = t - n_w;
@@ -843,7 +844,7 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
                 auto epi = [&](int m, int n, float v) {
                     if (m < B && n < N0) out[(int64_t)m * N0 + n] = v;
                 };
-                gemm_mma_tile<false, true>(a, bo, m0, n0, kb, ke, epi, false, NoRowsum{}, k3raw);
+                gemm_mma_tile<false, true>(a, bo, m0, n0, kb, ke, epi, false, NoRowsum{}, k3raw, p.prec);
                 continue;
             }
             // the partial dH0 tile stays in shared memory; masked by ReLU'(z0) it gives this
@@ -872,7 +873,7 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             for (int e = threadIdx.x; e < (BM - nb) * K3N; e += F_NT3) h0t[nb * K3N + e] = 0.0f;
             const Opnd a{p.dZ1, N1, B}, bo{p.online + p.w1, N0, N0};
             auto epi = [&](int m, int n, float v) { tile[(m - m0) * (K3N + 4) + (n - n0)] = v; };
-            gemm_mma_tile<false, true>(a, bo, m0, n0, kb, ke, epi, false, NoRowsum{}, k3raw, &trace_, 2);
+            gemm_mma_tile<false, true>(a, bo, m0, n0, kb, ke, epi, false, NoRowsum{}, k3raw, p.prec, &trace_, 2);
             __syncthreads();
             trace_.mark(4);
             // dW0 / db0 share: C[unit k][d] = sum_b dZ0[b][k] xs[b][d] over the tile's rows with

@@ -69,6 +69,7 @@ struct WideArgs {
     int ntile;                       // dW0 inputs per CTA (multiple of 16, <= 256)
     int wpre;                        // wd_dw0_wpre(ntile): the launch has wd_dw0_smem(ntile) bytes
     unsigned long long *trace;       // RPL_TRACE=1: per-CTA %globaltimer marks (kernel slots 4, 5)
+    int nplanes;                     // bf16 terms per fp32 operand: 3 (FP32), 2 (TF32), 1 (BF16)
 };
 
 // RPL_TRACE=1: thread 0 of each CTA stores %globaltimer at marks 0 .. 7 of its slot
@@ -161,9 +162,8 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
         if (tid != 0) return;
         uint8_t *A = sm + (sl & 1) * WD_STAGE;
         const int64_t t0 = (kb + (int64_t)sl * WD_KS) / WD_KS * (WD_M * WD_KS);
-        umma::mbar_expect_tx(&full[sl & 1], 3 * WD_A_PLANE);
-#pragma unroll
-        for (int pl = 0; pl < 3; ++pl) umma::bulk_g2s(A + pl * WD_A_PLANE, Wp + pl * pe + t0, WD_A_PLANE, &full[sl & 1]);
+        umma::mbar_expect_tx(&full[sl & 1], p.nplanes * WD_A_PLANE);
+        for (int pl = 0; pl < p.nplanes; ++pl) umma::bulk_g2s(A + pl * WD_A_PLANE, Wp + pl * pe + t0, WD_A_PLANE, &full[sl & 1]);
     };
     const int totalB = N * (WD_KS / 16);   // 16-byte pieces of a slice's states (<= 4 per thread)
     auto load_B = [&](int sl, uint4 v[4]) {
@@ -229,8 +229,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
             umma::mbar_wait(&full[st], (sl >> 1) & 1);   // A(sl) has landed
             for (int s = 0; s < WD_KS / 16; ++s) {
                 const uint64_t bd = umma::desc(Bs + 2 * s * 128, 128, 1024);
-#pragma unroll
-                for (int pl = 0; pl < 3; ++pl)
+                for (int pl = 0; pl < p.nplanes; ++pl)
                     umma::mma_bf16(tmem, umma::desc(A + pl * WD_A_PLANE + 2 * s * 128, 128, 1024), bd,
                                    idesc, sl > 0 || s > 0 || pl > 0);
             }
@@ -324,9 +323,8 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
         if (tid != 0) return;
         uint8_t *A = sm + (sl & 1) * WD_STAGE;
         const int64_t pz = wd_plane_elems(p.B), t0 = (int64_t)sl * (WD_M * WD_KS);
-        umma::mbar_expect_tx(&full[sl & 1], 3 * WD_A_PLANE);
-#pragma unroll
-        for (int pl = 0; pl < 3; ++pl)
+        umma::mbar_expect_tx(&full[sl & 1], p.nplanes * WD_A_PLANE);
+        for (int pl = 0; pl < p.nplanes; ++pl)
             umma::bulk_g2s(A + pl * WD_A_PLANE, p.dZ0bf + pl * pz + t0, WD_A_PLANE, &full[sl & 1]);
     };
     // B = U^T slice: element (input n, sample b) = U[b][n0 + n], MN-major (contiguous in n);
@@ -396,8 +394,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
             const int ksteps = (min(WD_KS, p.B - sl * WD_KS) + 15) / 16;
             for (int s = 0; s < ksteps; ++s) {
                 const uint64_t bd = umma::desc(Bs + 2 * s * (N / 8) * 128, (N / 8) * 128, 128);
-#pragma unroll
-                for (int pl = 0; pl < 3; ++pl)
+                for (int pl = 0; pl < p.nplanes; ++pl)
                     umma::mma_bf16(tmem, umma::desc(A + pl * WD_A_PLANE + 2 * s * (WD_M / 8) * 128,
                                                     (WD_M / 8) * 128, 128),
                                    bd, idesc, sl > 0 || s > 0 || pl > 0);
@@ -482,13 +479,13 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
                     const uint2 pl = make_uint2(pack2(l[0], l[1]), pack2(l[2], l[3]));
                     const int64_t tx = wd_tix_k(u, n0 + c);   // 4 inputs of one core-matrix row
                     *reinterpret_cast<uint2 *>(p.W0bf + tx) = ph;
-                    *reinterpret_cast<uint2 *>(p.W0bf + pe + tx) = pm;
-                    *reinterpret_cast<uint2 *>(p.W0bf + 2 * pe + tx) = pl;
+                    if (p.nplanes > 1) *reinterpret_cast<uint2 *>(p.W0bf + pe + tx) = pm;
+                    if (p.nplanes > 2) *reinterpret_cast<uint2 *>(p.W0bf + 2 * pe + tx) = pl;
                     if (sync) {
                         *reinterpret_cast<float4 *>(p.target_w + wi) = w;
                         *reinterpret_cast<uint2 *>(p.W0bf + 3 * pe + tx) = ph;
-                        *reinterpret_cast<uint2 *>(p.W0bf + 4 * pe + tx) = pm;
-                        *reinterpret_cast<uint2 *>(p.W0bf + 5 * pe + tx) = pl;
+                        if (p.nplanes > 1) *reinterpret_cast<uint2 *>(p.W0bf + 4 * pe + tx) = pm;
+                        if (p.nplanes > 2) *reinterpret_cast<uint2 *>(p.W0bf + 5 * pe + tx) = pl;
                     }
                 }
         }

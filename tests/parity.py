@@ -83,7 +83,7 @@ def step_and_compare(b, cfg, dqn, rp, orc_ring, batch, *, seed, rank=0, burn_in=
             f = flips[:, sl]
             if f.any():
                 scale = np.max(np.abs(z), axis=1, keepdims=True)
-                bad = f & (np.abs(z) > 1e-5 * scale)
+                bad = f & (np.abs(z) > max(tol, 1e-5) * scale)
                 assert not bad.any(), f"ReLU decision differs beyond rounding: z={z[bad][:4]}"
         override = True
     astar = None
@@ -94,7 +94,7 @@ def step_and_compare(b, cfg, dqn, rp, orc_ring, batch, *, seed, rank=0, burn_in=
             rows = np.nonzero(ag != out["a_star"])[0]
             for i in rows:
                 margin = qo[i, out["a_star"][i]] - qo[i, ag[i]]
-                assert margin <= 1e-5 * max(1.0, np.max(np.abs(qo[i]))), "argmax beyond rounding"
+                assert margin <= max(tol, 1e-5) * max(1.0, np.max(np.abs(qo[i]))), "argmax beyond rounding"
             astar = ag
             override = True
     if override:
