@@ -786,6 +786,7 @@ struct rpl_dqn {
     uint16_t *w0bf = nullptr;              // bf16 planes of W0 [online, target][3][N0 * D]
     uint16_t *dz0bf = nullptr;             // bf16 planes of dZ0 [3][max_batch][N0]
     bool w0bf_stale = true;                // planes to be re-split from the fp32 weights
+    int wide_ks = 0, wide_cs = 1;          // wide_l0_kernel chunks and cluster size (wide_l0_plan)
     unsigned long long *trace = nullptr;   // RPL_TRACE=1: per-CTA timestamps of the fast kernels
     // data parallel
     void *comm = nullptr;
@@ -940,6 +941,8 @@ extern "C" int dqn_destroy(rpl_dqn *d)
     return RPL_OK;
 }
 
+static void wide_l0_plan(rpl_dqn *d, int nets, int64_t D);
+
 extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn **out)
 {
     if (!out || !init) {
@@ -998,6 +1001,7 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
                  // the tiles' padding (inputs past D) is never written: zero once
                  cudaMemset(d->w0bf, 0, (size_t)6 * wd_plane_elems(D) * 2) == cudaSuccess &&
                  cudaMemset(d->dz0bf, 0, (size_t)3 * wd_plane_elems(Bm) * 2) == cudaSuccess;
+            if (ok) wide_l0_plan(d, d->cfg.double_dqn ? 3 : 2, D);
         }
     }
     for (int l = 0; l < d->T && ok; ++l) {
@@ -1202,6 +1206,63 @@ static void fill_args(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.sync_flag = d->sync_flag;
 }
 
+// wide_l0_kernel launch: nets x ks CTAs in clusters of cs along the chunks (wide.cuh)
+static cudaError_t launch_wide_l0(const WideArgs &w, cudaStream_t st)
+{
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)(w.nets * w.ks));
+    lc.blockDim = dim3(WD_T);
+    lc.dynamicSmemBytes = WD_SMEM;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)w.cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, wide_l0_kernel, w);
+}
+
+// chunks (ks) and cluster size (cs) of wide_l0_kernel for `nets` nets: as many co-resident
+// clusters as the GPU holds (one CTA per SM; cudaOccupancyMaxActiveClusters), ks a multiple of
+// cs, ks <= kKs0Max.  Default cs = 1: the cluster sums measured slower than writing every
+// partial (cs = 2: epilogue 8.6 vs 5.0 us); RPL_WIDE_CS = 2..16 selects them
+static void wide_l0_plan(rpl_dqn *d, int nets, int64_t D)
+{
+    const int64_t S = (D + WD_KS - 1) / WD_KS;
+    int cs = 1;
+    if (const char *c = getenv("RPL_WIDE_CS")) cs = std::max(1, std::min(16, atoi(c)));
+    for (; cs >= 1; --cs) {
+        if (cs > 8) cudaFuncSetAttribute(wide_l0_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)(cs * nets));
+        lc.blockDim = dim3(WD_T);
+        lc.dynamicSmemBytes = WD_SMEM;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, wide_l0_kernel, &lc) != cudaSuccess) {
+            cudaGetLastError();
+            n = cs == 1 ? d->sms : 0;
+        }
+        int ks = (n / nets) * cs;
+        ks = (int)std::min<int64_t>(ks, std::min<int64_t>(S, kKs0Max) / cs * cs);
+        if (ks >= 2 * cs || (cs == 1 && ks >= 1)) {
+            d->wide_ks = ks;
+            d->wide_cs = cs;
+            return;
+        }
+    }
+    d->wide_ks = 1;
+    d->wide_cs = 1;
+}
+
 static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int apply, FastArgs &p)
 {
     memset(&p, 0, sizeof p);
@@ -1394,12 +1455,13 @@ static cudaError_t wide_graph_step(rpl_dqn *d, rpl_replay *rp, int B, float *los
         if (e != cudaSuccess) return e;
         rpl_batch bt{d->Xs, d->Xs2, d->a, d->r, d->done, d->idx};
         int rc = launch_gather_u8_dev(rp, B, &bt, cs);
-        wide_l0_kernel<<<w.nets * w.ks, WD_T, WD_SMEM, cs>>>(w);
-        wide_reduce_kernel<<<d->sms * 4, 256, 0, cs>>>(d->PF0, w.ks, w.nets, B, d->N[0], d->online,
+        cudaError_t el = launch_wide_l0(w, cs);
+        wide_reduce_kernel<<<d->sms * 4, 256, 0, cs>>>(d->PF0, wd_l0_partials(w.ks, w.cs, B), w.nets, B, d->N[0], d->online,
                                                        d->target, d->boff[0], d->H[0]);
         cudaError_t e2 = rc == RPL_OK ? fast_enqueue(d, fp, cs) : cudaErrorUnknown;
         wide_dw0_kernel<<<(unsigned)((w.D + w.ntile - 1) / w.ntile), WD_T, wd_dw0_smem(w.ntile), cs>>>(w);
         e = cudaStreamEndCapture(cs, &graph);
+        if (e == cudaSuccess) e = el;
         if (e == cudaSuccess) e = e2;
         if (e == cudaSuccess) e = cudaGetLastError();
         cudaGraphNode_t k4 = nullptr;
@@ -1593,13 +1655,12 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
         WideArgs w{};
         if (wide) {
             const int nets = p.nets;
-            const int ks_max = std::max(1, std::min(kKs0Max, d->sms / nets));
             w.D = p.D;
             w.B = batch;
             w.N0 = d->N[0];
             w.nets = nets;
-            w.kchunk = ((p.D + ks_max - 1) / ks_max + WD_KS - 1) / WD_KS * WD_KS;
-            w.ks = (int)((p.D + w.kchunk - 1) / w.kchunk);
+            w.ks = d->wide_ks;
+            w.cs = d->wide_cs;
             w.U0 = reinterpret_cast<const uint8_t *>(d->Xs);
             w.U1 = reinterpret_cast<const uint8_t *>(d->Xs2);
             w.online = d->online;
@@ -1617,7 +1678,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             w.apply_update = dp ? 0 : 1;
             w.sync_flag = d->sync_flag;
             p.wide_tc = 1;
-            p.ks0 = w.ks;
+            p.ks0 = wd_l0_partials(w.ks, w.cs, batch);   // partials left in PF0
             if (d->w0bf_stale) {   // after create / set_params / sync_target / a DP step
                 const int64_t pe = wd_plane_elems(p.D);
                 wide_split_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->online + d->woff[0], d->w0bf, d->N[0], p.D);
@@ -1653,8 +1714,8 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                 return rc;
             }
             // (2) layer-0 forward partials of every net
-            wide_l0_kernel<<<nets * w.ks, WD_T, WD_SMEM, d->stream>>>(w);
-            e = cudaGetLastError();
+            e = launch_wide_l0(w, d->stream);
+            if (e == cudaSuccess) e = cudaGetLastError();
             if (e != cudaSuccess) {
                 if (prev >= 0) cudaSetDevice(prev);
                 return cuda_fail(e, "wide_l0_kernel");
@@ -1669,7 +1730,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
         if (wide && d->wide_fast) {
             // (3) layers above layer 0 on the fast kernels: H0 from the partials, then K1 (H0
             // in), K2, K3 (dH0 partials out), K4 (dZ0 for step 4, every SGD but layer 0's)
-            wide_reduce_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->PF0, w.ks, p.nets, batch, d->N[0],
+            wide_reduce_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->PF0, wd_l0_partials(w.ks, w.cs, batch), p.nets, batch, d->N[0],
                                                                    d->online, d->target, d->boff[0], d->H[0]);
             FastArgs fp;
             wide_fast_args(d, rp, batch, dp ? nullptr : loss_dev, dp ? 0 : 1, fp);

@@ -24,6 +24,7 @@
 // K slices through two shared-memory buffers: the loads of slice i + 1 overlap the MMAs of
 // slice i (tcgen05.commit -> mbarrier per buffer).
 #pragma once
+#include <cooperative_groups.h>
 #include <stdint.h>
 
 #include "umma.cuh"
@@ -50,7 +51,9 @@ __host__ __device__ inline int wd_dw0_smem(int ntile)
 
 struct WideArgs {
     int D, B, N0, nets, ks;          // inputs, batch, layer-0 units (== 128), nets, k-chunks
-    int64_t kchunk;                  // inputs per chunk (multiple of WD_KS)
+    int64_t kchunk;                  // unused by wide_l0_kernel (chunks are slice ranges, wd_chunk)
+    int cs;                          // wide_l0_kernel cluster size: ks % cs == 0, the cs chunks of a
+                                     // cluster sum their partials over DSMEM (PF0 holds ks / cs)
     const uint8_t *U0, *U1;          // gathered byte states s, s' [B][D]
     const float *online, *target;
     int64_t w0;                      // offset of W0 [N0][D] in the parameter blob
@@ -88,6 +91,23 @@ struct WdTrace {
         slot[i] = t;
     }
 };
+
+// chunk q of ks: 64-deep slices [q S / ks, (q + 1) S / ks) of the S = ceil(D / 64) slices
+__host__ __device__ inline void wd_chunk(int64_t D, int ks, int q, int64_t &kb, int64_t &ke)
+{
+    const int64_t S = (D + WD_KS - 1) / WD_KS;
+    kb = q * S / ks * WD_KS;
+    ke = (q + 1) * S / ks * WD_KS;
+    if (ke > D) ke = D;
+}
+
+// layer-0 partials wide_l0_kernel leaves in PF0 for batch B: ks / cs when the cluster sums
+// apply (the rounded batch splits into 8-column pieces per owner), else ks
+__host__ __device__ inline int wd_l0_partials(int ks, int cs, int B)
+{
+    const int N = (B + 15) & ~15;
+    return cs > 1 && N % (8 * cs) == 0 ? ks / cs : ks;
+}
 
 // canonical no-swizzle offsets (umma.cuh): K-major rows x 64-deep slice, and MN-major
 __device__ __forceinline__ uint32_t wd_off_k(int r, int k) { return (r >> 3) * 1024 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2; }
@@ -134,8 +154,8 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int net = blockIdx.x / p.ks, kq = blockIdx.x % p.ks;
     WdTrace tr(p.trace, 4);
-    const int64_t kb = (int64_t)kq * p.kchunk;
-    const int64_t ke = kb + p.kchunk < p.D ? kb + p.kchunk : p.D;
+    int64_t kb, ke;
+    wd_chunk(p.D, p.ks, kq, kb, ke);
     const int nsl = (int)((ke - kb + WD_KS - 1) / WD_KS);
     const int N = (p.B + 15) & ~15;                  // UMMA N: the batch rounded up to 16
     const uint8_t *U = net == 0 ? p.U0 : p.U1;
@@ -246,7 +266,7 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
     tr.mark(2);
     umma::fence_after_sync();
     // epilogue: warp w reads TMEM lanes (units) 32 (w % 4) .. + 31, columns (samples) of its half
-    {
+    if (p.cs == 1 || N % (8 * p.cs) != 0) {   // (a batch that does not split: ks partials)
         const int q = warp & 3, half = warp >> 2, u = 32 * q + lane;
         const int c0 = half * (N / 2), c1 = c0 + N / 2;
         float *out = p.PF0 + ((int64_t)kq * p.nets + net) * p.B * p.N0;
@@ -256,6 +276,50 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
 #pragma unroll
             for (int i = 0; i < 8; ++i)
                 if (c + i < p.B && u < p.N0) out[(int64_t)(c + i) * p.N0 + u] = v[i];   // x 255
+        }
+    } else {
+        // cluster of cs consecutive chunks: CTA r owns sample columns [r Nc, (r + 1) Nc) of the
+        // cluster's sum.  Every CTA pushes each 8-column piece of its accumulator straight from
+        // TMEM into the owner's shared memory (distributed shared memory stores: no round
+        // trip), one slot per source rank; after one cluster barrier each owner adds its cs
+        // slots in rank order and writes the cluster's single partial -- PF0 traffic and
+        // wide_reduce_kernel's work drop cs-fold
+        namespace cg = cooperative_groups;
+        cg::cluster_group cl = cg::this_cluster();
+        const int rk = (int)cl.block_rank();
+        const int Nc = N / p.cs, RS = Nc + 4;               // columns per owner, slot row stride
+        float *R = reinterpret_cast<float *>(sm);            // [cs source ranks][128 units][RS]
+        {
+            const int q = warp & 3, half = warp >> 2, u = 32 * q + lane;
+            const int c0 = half * (N / 2), c1 = c0 + N / 2;
+            for (int c = c0; c < c1; c += 8) {
+                float v[8];
+                umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + c, v);
+                const int ow = c / Nc;
+                float *dst = cl.map_shared_rank(R, ow) + ((int64_t)rk * WD_M + u) * RS + (c - ow * Nc);
+                *reinterpret_cast<float4 *>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+                *reinterpret_cast<float4 *>(dst + 4) = make_float4(v[4], v[5], v[6], v[7]);
+            }
+        }
+        cl.sync();   // every slot of every owner is written
+        float *out = p.PF0 + ((int64_t)(kq / p.cs) * p.nets + net) * p.B * p.N0;
+        for (int f = tid; f < WD_M * (Nc / 4); f += WD_T) {
+            const int u = f % WD_M, c = 4 * (f / WD_M);     // consecutive threads: consecutive units
+            float4 acc = *reinterpret_cast<const float4 *>(R + (int64_t)u * RS + c);
+            for (int r = 1; r < p.cs; ++r) {
+                const float4 v = *reinterpret_cast<const float4 *>(R + ((int64_t)r * WD_M + u) * RS + c);
+                acc.x += v.x;
+                acc.y += v.y;
+                acc.z += v.z;
+                acc.w += v.w;
+            }
+            const int b = rk * Nc + c;
+            if (u < p.N0) {
+                const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+                for (int i2 = 0; i2 < 4; ++i2)
+                    if (b + i2 < p.B) out[(int64_t)(b + i2) * p.N0 + u] = a4[i2];   // x 255
+            }
         }
     }
     umma::fence_before_sync();

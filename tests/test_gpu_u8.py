@@ -64,7 +64,7 @@ def test_u8_insert_sample_gather_bit_exact(b, D):
     assert rp.check() == b.RPL_OK
 
 
-@pytest.mark.parametrize("path", ["tcgen05", "tcgen05-coop", "simt"])
+@pytest.mark.parametrize("path", ["tcgen05", "tcgen05-coop", "simt", "tcgen05-cluster"])
 @pytest.mark.parametrize("ddqn", [False, True], ids=["dqn", "ddqn"])
 def test_u8_wide_input_train_step(b, ddqn, path, monkeypatch):
     # config 5 network: the paper's dueling MLP on an 84x84x4 byte input (28,224 -> 128 ->
@@ -76,6 +76,8 @@ def test_u8_wide_input_train_step(b, ddqn, path, monkeypatch):
         monkeypatch.setenv("RPL_NO_WIDE_TC", "1")
     if path == "tcgen05-coop":
         monkeypatch.setenv("RPL_NO_WIDE_FAST", "1")
+    if path == "tcgen05-cluster":   # layer-0 partials summed in clusters of 2 over DSMEM
+        monkeypatch.setenv("RPL_WIDE_CS", "2")
     D = ATARI_STATE_DIM
     cfg = b.DQNConfig(state_dim=D, n_actions=8, dueling=True, hidden=(128,), stream=512,
                       double_dqn=ddqn, gamma=0.99, lr=1e-3, huber_kappa=1.0, sync_period=2,
