@@ -672,7 +672,8 @@ def run_c5(a):
     peak_emu = bf16 / 3.0
     achieved = flops / (kern_avg_ms / 1000.0) / 1e12
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_emu, "unit": "TFLOP/s",
-                "frac": achieved / peak_emu, "traffic": None,
+                "frac": achieved / peak_emu,
+                "traffic": load_traffic().get(f"c5_step_b{batch}_{'ddqn' if a.ddqn else 'dqn'}"),
                 "kernel": "the whole train step (Philox gather, wide_l0_kernel, the cooperative "
                           "train kernel for the layers above layer 0, wide_dw0_kernel + SGD) timed "
                           "with CUDA events around each dqn_train_step",
