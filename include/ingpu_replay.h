@@ -96,6 +96,12 @@ typedef struct {
                              their block is written or replay_flush_queue writes a partial
                              block.  Device-sourced adds are rejected (EINVAL) in this mode.
                              U <= capacity; U > max_host_add raises max_host_add to U      */
+    void *storage;        /* optional caller-owned DEVICE buffer for the ring rows (e.g. a
+                             torch tensor): at least replay_ring_bytes() bytes, 256-byte
+                             aligned, on opts.device, valid until replay_destroy (which does
+                             not free it); zeroed at create.  NULL: the library allocates.
+                             Ignored (must be NULL) with RPL_RING_HOST                      */
+    size_t storage_bytes; /* its size in bytes                                              */
 } rpl_replay_opts;
 
 /* Create an empty FIFO replay of `capacity` experiences whose states are `state_dim`
@@ -109,6 +115,10 @@ typedef struct {
  * ENOMEM, ECUDA.  *out owns the device ring until replay_destroy. */
 int replay_create(int64_t capacity, int32_t state_dim, const rpl_replay_opts *opts,
                   rpl_replay **out);
+/* Bytes of the ring rows replay_create would allocate for these arguments (the size an
+ * opts.storage buffer needs).  Errors: EINVAL as replay_create's argument checks. */
+int replay_ring_bytes(int64_t capacity, int32_t state_dim, const rpl_replay_opts *opts,
+                      size_t *bytes);
 int replay_destroy(rpl_replay *replay);
 
 /* Insert k experiences, oldest evicted first: experience j goes to slot

@@ -34,7 +34,8 @@ RPL_PREC_FP32, RPL_PREC_TF32, RPL_PREC_BF16 = 0, 1, 2
 
 EXPORTS = [
     "replay_create", "replay_destroy", "replay_add", "replay_sample", "replay_gather",
-    "replay_size", "replay_state", "replay_flush_queue", "replay_queued", "dqn_param_count",
+    "replay_size", "replay_state", "replay_flush_queue", "replay_queued", "replay_ring_bytes",
+    "dqn_param_count",
     "dqn_create", "dqn_destroy",
     "dqn_train_step", "sync_target", "dqn_get_params", "dqn_set_params", "dqn_step_count",
     "dqn_debug_export", "rpl_nccl_unique_id", "dqn_attach_nccl", "rpl_check",
@@ -52,7 +53,8 @@ class _ReplayOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("cuda_stream", C.c_void_p), ("burn_in", C.c_int64),
                 ("seed", C.c_uint64), ("rank", C.c_uint32), ("max_host_add", C.c_int64),
                 ("state_dtype", C.c_int32), ("sampling", C.c_int32), ("state_sharing", C.c_int32),
-                ("ring_memory", C.c_int32), ("update_size", C.c_int64)]
+                ("ring_memory", C.c_int32), ("update_size", C.c_int64), ("storage", C.c_void_p),
+                ("storage_bytes", C.c_size_t)]
 
 
 class _Batch(C.Structure):
@@ -84,6 +86,7 @@ def _load():
         "replay_gather": (C.c_int, [P, i64, P, C.POINTER(_Batch)]),
         "replay_size": (C.c_int, [P, C.POINTER(i64)]),
         "replay_flush_queue": (C.c_int, [P, C.POINTER(i64)]),
+        "replay_ring_bytes": (C.c_int, [i64, i32, C.POINTER(_ReplayOpts), C.POINTER(C.c_size_t)]),
         "replay_queued": (C.c_int, [P, C.POINTER(i64)]),
         "replay_state": (C.c_int, [P, C.POINTER(i64), C.POINTER(i64), C.POINTER(u64),
                                    C.POINTER(u64), C.POINTER(u64)]),
@@ -154,7 +157,9 @@ class Replay:
     def __init__(self, capacity: int, state_dim: int, *, device: int = 0, stream=None,
                  burn_in: int = 1, seed: int = 2, rank: int = 0, max_host_add: int = 0,
                  state_dtype: str = "f32", sampling: str = "uniform", shared_state: bool = False,
-                 ring_memory: str = "device", update_size: int = 0):
+                 ring_memory: str = "device", update_size: int = 0, storage=None):
+        """storage: optional caller-owned CUDA tensor holding the ring rows (at least
+        Replay.ring_bytes(...) bytes; kept referenced by this object)."""
         torch = _torch()
         if not torch.cuda.is_available():
             raise RplError(RPL_ECUDA, "no CUDA device (the in-GPU replay has no CPU fallback)")
@@ -167,7 +172,10 @@ class Replay:
         o = _ReplayOpts(device, self._stream, burn_in, seed, rank, max_host_add,
                         RPL_U8 if self.u8 else RPL_F32, 1 if sampling == "distinct" else 0,
                         1 if shared_state else 0,
-                        RPL_RING_HOST if ring_memory == "host" else RPL_RING_DEVICE, update_size)
+                        RPL_RING_HOST if ring_memory == "host" else RPL_RING_DEVICE, update_size,
+                        None if storage is None else storage.data_ptr(),
+                        0 if storage is None else storage.numel() * storage.element_size())
+        self._storage = storage
         self.shared_state = shared_state
         self.ring_memory = ring_memory
         h = C.c_void_p()
@@ -179,6 +187,17 @@ class Replay:
         if getattr(self, "_h", None):
             _L.replay_destroy(self._h)
             self._h = None
+        self._storage = None
+
+    @staticmethod
+    def ring_bytes(capacity: int, state_dim: int, state_dtype: str = "f32", shared_state: bool = False) -> int:
+        """replay_ring_bytes: the size a caller-provided `storage` tensor needs."""
+        o = _ReplayOpts()
+        o.state_dtype = RPL_U8 if state_dtype == "u8" else RPL_F32
+        o.state_sharing = 1 if shared_state else 0
+        n = C.c_size_t()
+        _ok(_L.replay_ring_bytes(capacity, state_dim, C.byref(o), C.byref(n)))
+        return n.value
 
     __del__ = close
 

@@ -443,8 +443,11 @@ __device__ void phase_head(const TrainArgs &p, TileSmem &sm)
         const float notdone = p.done[b] ? 0.0f : 1.0f;
         const float yb = rb + p.gamma * notdone * boot;
         // the enumerate-mask gather Q[i*A + a_i] is a register select here
-        const float qsel = __shfl_sync(0xffffffffu, q0, ab);
-        const float delta = qsel - yb;
+        const float qsel = __shfl_sync(0xffffffffu, q0, ab & 31);
+        // an action outside [0, A) poisons the loss (the update is skipped) and raises ECORRUPT
+        const bool bad = (unsigned)ab >= (unsigned)A;
+        if (bad && lane == 0) atomicOr(p.err, ERRBIT_CORRUPT);
+        const float delta = bad ? __int_as_float(0x7fc00000) : qsel - yb;
         const float g = (p.kappa_inf ? delta : fminf(fmaxf(delta, -p.kappa), p.kappa)) / (float)B;
         // dL/dhead: plain dO_j = [j==a]g ; dueling dV = g, dA_j = [j==a]g - g/|A|
         if (p.dueling) {
@@ -1969,7 +1972,11 @@ extern "C" int rpl_check(void *handle, int kind)
     uint32_t h = 0;
     RPL_CUDA(cudaMemcpy(&h, err, sizeof h, cudaMemcpyDeviceToHost));
     if (h) RPL_CUDA(cudaMemset(err, 0, sizeof h));
-    if (h & ERRBIT_CORRUPT) { set_error("corrupt terminal flag in a device-sourced add"); return RPL_ECORRUPT; }
+    if (h & ERRBIT_CORRUPT) {
+        set_error("corrupt experience: a device-sourced terminal flag > 1 or a sampled action outside [0, A) "
+                  "(that step's update was skipped)");
+        return RPL_ECORRUPT;
+    }
     if (h & ERRBIT_NUMERIC) { set_error("non-finite loss: update skipped"); return RPL_ENUMERIC; }
     if (h & ERRBIT_RANGE) { set_error("gather index out of range (clamped)"); return RPL_EINVAL; }
     return RPL_OK;

@@ -48,6 +48,7 @@ constexpr uint32_t TAG_SAMPLE = 1u;
 struct Ring {
     float *rows = nullptr;     // capacity * rs words
     int host = 0;              // RPL_RING_HOST: rows in pinned, mapped host memory
+    int owned = 1;             // 0: rows are the caller's opts.storage (not freed)
     int64_t capacity = 0;
     int32_t D = 0;
     int32_t rs = 0;            // row stride in 4-byte words

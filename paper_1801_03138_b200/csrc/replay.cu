@@ -620,6 +620,20 @@ static size_t host_add_bytes(int64_t k, int32_t D, bool u8)
     return (size_t)k * (2 * (size_t)D * (u8 ? 1 : 4) + 4 + 4 + 1);
 }
 
+extern "C" int replay_ring_bytes(int64_t capacity, int32_t state_dim, const rpl_replay_opts *opts,
+                                 size_t *bytes)
+{
+    if (!bytes || capacity < 1 || capacity >= (int64_t(1) << 31) || state_dim < 1 || state_dim > 1 << 20) {
+        set_error("replay_ring_bytes: invalid argument");
+        return RPL_EINVAL;
+    }
+    const bool u8 = opts && opts->state_dtype == RPL_U8;
+    const bool sh = opts && opts->state_sharing != 0;
+    const int64_t rs = u8 ? ring_u8_row_bytes(state_dim, sh) / 4 : ring_row_stride(state_dim, sh);
+    *bytes = (size_t)capacity * rs * sizeof(float);
+    return RPL_OK;
+}
+
 extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_replay_opts *opts,
                              rpl_replay **out)
 {
@@ -689,7 +703,21 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
     rp->distinct = o.sampling == RPL_SAMPLE_DISTINCT;
     const size_t ring_bytes = (size_t)capacity * rp->ring.rs * sizeof(float);
     rp->ring.host = o.ring_memory == RPL_RING_HOST ? 1 : 0;
-    if (rp->ring.host) {
+    if (o.storage) {
+        // caller-owned device rows (e.g. a torch tensor): checked, zeroed, never freed here
+        cudaPointerAttributes pa{};
+        const bool dev_ok = cudaPointerGetAttributes(&pa, o.storage) == cudaSuccess &&
+                            pa.type == cudaMemoryTypeDevice && pa.device == o.device;
+        cudaGetLastError();
+        if (rp->ring.host || o.storage_bytes < ring_bytes || ((uintptr_t)o.storage & 255) != 0 || !dev_ok) {
+            set_error("replay_create: opts.storage must be a 256-byte aligned device buffer of >= %zu bytes "
+                      "on device %d (got %zu bytes), and RPL_RING_DEVICE", ring_bytes, o.device, o.storage_bytes);
+            delete rp;
+            return RPL_EINVAL;
+        }
+        rp->ring.rows = (float *)o.storage;
+        rp->ring.owned = 0;
+    } else if (rp->ring.host) {
         // in-RAM comparison mode: pinned host rows the kernels address directly (UVA)
         if (cudaHostAlloc(&rp->ring.rows, ring_bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
             cudaGetLastError();
@@ -744,7 +772,7 @@ extern "C" int replay_destroy(rpl_replay *rp)
     if (rp->err_dev) cudaFree(rp->err_dev);
     if (rp->ctrl_dev) cudaFree(rp->ctrl_dev);
     if (rp->ds_idx) cudaFree(rp->ds_idx);
-    if (rp->ring.rows) {
+    if (rp->ring.rows && rp->ring.owned) {
         if (rp->ring.host) cudaFreeHost(rp->ring.rows);
         else cudaFree(rp->ring.rows);
     }

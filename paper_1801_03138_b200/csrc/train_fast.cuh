@@ -201,8 +201,12 @@ __device__ __forceinline__ void td_warp(const FastArgs &p, const float *hs, int 
     }
     const float notdone = db ? 0.0f : 1.0f;
     const float yb = rb + p.gamma * notdone * boot;
-    const float qsel = __shfl_sync(0xffffffffu, q[0], ab);   // Q[i*A + a_i]
-    const float delta = qsel - yb;
+    const float qsel = __shfl_sync(0xffffffffu, q[0], ab & 31);   // Q[i*A + a_i]
+    // an action outside [0, A) (a corrupt experience; the replay does not know A) poisons the
+    // loss, so the non-finite guard skips the whole update, and raises the sticky ECORRUPT
+    const bool bad = (unsigned)ab >= (unsigned)A;
+    if (bad && lane == 0) atomicOr(p.err, ERRBIT_CORRUPT);
+    const float delta = bad ? __int_as_float(0x7fc00000) : qsel - yb;
     const float g = (p.kinf ? delta : fminf(fmaxf(delta, -p.kappa), p.kappa)) / (float)B;
     if (p.dueling) {
         // dV = sum_a dQ_a = g ; dA_a = dQ_a - (1/|A|) sum_a' dQ_a'

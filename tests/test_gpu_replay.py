@@ -155,3 +155,32 @@ def test_full_1m_ring_sampled_rows(B):
     for k in ("s", "s_next", "a", "r", "done"):
         assert np.array_equal(g[k], e[k][t]), k
     assert rp.check() == B.RPL_OK
+
+
+def test_caller_provided_ring_storage(B):
+    # ring storage is library-allocated or caller-provided through opts.storage;
+    # a torch tensor holds the rows, sampling is bit-exact with the oracle, destroy leaves it
+    import torch
+    C = 3000
+    nbytes = B.Replay.ring_bytes(C, 27)
+    assert nbytes == C * 256   # 256-byte rows for 27-float states
+    buf = torch.full((nbytes,), 0xAB, dtype=torch.uint8, device="cuda")   # zeroed at create
+    rp = B.Replay(C, 27, seed=12, storage=buf)
+    orc = oracle.Ring(C, 27)
+    e = experiences(C + 500, seed=13)
+    for part in (slice(0, 2000), slice(2000, C + 500)):
+        rp.add(**{k: v[part] for k, v in e.items()})
+        orc.add(**{k: v[part] for k, v in e.items()})
+    for _ in range(2):
+        g = rp.sample(512)
+        rc, o = orc.sample(1, 12, 0, 512)
+        for k in ("idx", "s", "s_next", "a", "r", "done"):
+            assert np.array_equal(g[k].cpu().numpy(), o[k]), k
+    rows = buf.view(torch.float32).view(C, 64)[:, :27].cpu().numpy()
+    assert np.array_equal(rows, orc.rows()[:, :27])   # the rows really live in the tensor
+    rp.close()
+    assert buf.sum().item() != 0   # still allocated and intact after destroy
+    with pytest.raises(B.RplError):
+        B.Replay(C, 27, storage=buf[: nbytes - 256])   # too small
+    with pytest.raises(B.RplError):
+        B.Replay(C, 27, storage=buf[1:])               # misaligned

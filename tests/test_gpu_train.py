@@ -184,6 +184,28 @@ def test_nonfinite_loss_skips_update(b):
     assert np.array_equal(dqn.get_params(b.RPL_TARGET), t_before)
 
 
+@pytest.mark.parametrize("path", ["fast", "generic"])
+def test_action_outside_the_action_set_skips_update(b, path, monkeypatch):
+    # the oracle rejects a batch holding an action outside [0, A) (test_oracle_dqn.py); the
+    # device cannot return an argument error mid-stream, so the step skips its update and the
+    # sticky ECORRUPT reports it
+    if path == "generic":
+        monkeypatch.setenv("RPL_PATH", "generic")
+    import torch
+    cfg = _cfg(b, max_batch=64, sync_period=1)
+    rp = b.Replay(100, 27, seed=43)
+    e = experiences(100, seed=44)
+    e["a"][:] = 8   # A = 8
+    rp.add(**e)
+    dqn = b.DQN(cfg, _params(cfg))
+    p_before = dqn.get_params(b.RPL_ONLINE)
+    loss = torch.zeros(1, device="cuda")
+    assert dqn.train_step(rp, 64, loss) == b.RPL_OK
+    assert dqn.check() == b.RPL_ECORRUPT
+    assert not np.isfinite(loss.item())
+    assert np.array_equal(dqn.get_params(b.RPL_ONLINE), p_before)
+
+
 def test_explicit_sync_target_and_set_get(b):
     cfg = _cfg(b, max_batch=32)
     rp = b.Replay(500, 27, seed=51)

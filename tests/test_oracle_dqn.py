@@ -309,3 +309,17 @@ def test_dyadic_inputs_make_forward_exact_in_fp32():
             for k in ("q_s", "q_next_target", "y", "z"):
                 v = out[k]
                 assert np.array_equal(v.astype(np.float32).astype(np.float64), v), k
+
+
+def test_action_outside_the_action_set_is_rejected():
+    # the enumerate-mask select Q[i*A + a_i] is defined only for a_i in [0, A): a batch
+    # holding any other action is an argument error, not a silent out-of-bounds read
+    net = oracle.Net(state_dim=3, n_actions=4, dueling=True, hidden=(5,), stream=6)
+    th = init_params(3, 4, (5,), True, 6, seed=21)
+    e = experiences(8, 3, 4, seed=22)
+    assert oracle.dqn_loss_grad(net, th, th, e, 0.99, 1.0, False)["loss"] >= 0.0
+    for bad in (4, -1):
+        e2 = dict(e, a=e["a"].copy())
+        e2["a"][5] = bad
+        with pytest.raises(ValueError):
+            oracle.dqn_loss_grad(net, th, th, e2, 0.99, 1.0, False)
