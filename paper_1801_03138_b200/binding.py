@@ -136,6 +136,13 @@ def _dptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+def _host(x, dtype):
+    """x as a C-contiguous numpy array of dtype (no copy when it already is one)."""
+    if type(x) is np.ndarray and x.dtype == dtype and x.flags.c_contiguous:
+        return x
+    return np.ascontiguousarray(np.asarray(x), dtype)
+
+
 def _torch():
     import torch
     return torch
@@ -209,8 +216,8 @@ class Replay:
         """replay_add: numpy / CPU tensors -> RPL_HOST; CUDA tensors -> RPL_DEVICE, or
         RPL_DEVICE_DEFER with defer=True (the tensors must stay unchanged until the next
         call on this replay / the next train step on it; a reference is held until then)."""
-        torch = _torch()
-        if isinstance(s, torch.Tensor) and s.is_cuda:
+        if type(s) is not np.ndarray and isinstance(s, _torch().Tensor) and s.is_cuda:
+            torch = _torch()
             if s_next is None:   # shared-state replay: s' is the next experience's s
                 s_next = s[:0]
             ts = [s.contiguous(), a.contiguous(), r.contiguous(), s_next.contiguous(),
@@ -226,14 +233,13 @@ class Replay:
                                    RPL_DEVICE_DEFER if defer else RPL_DEVICE))
             self._deferred = ts if defer else None
             return rc
-        arrs = [np.ascontiguousarray(np.asarray(s), self.state_np),
-                np.ascontiguousarray(np.asarray(a), np.int32),
-                np.ascontiguousarray(np.asarray(r), np.float32),
-                None if s_next is None else np.ascontiguousarray(np.asarray(s_next), self.state_np),
-                np.ascontiguousarray(np.asarray(done), np.uint8)]
+        sn = self.state_np
+        arrs = (_host(s, sn), _host(a, np.int32), _host(r, np.float32),
+                None if s_next is None else _host(s_next, sn), _host(done, np.uint8))
         k = arrs[1].size
-        return _ok(_L.replay_add(self._h, k, *[None if x is None else x.ctypes.data_as(C.c_void_p)
-                                              for x in arrs], RPL_HOST))
+        st = _L.replay_add(self._h, k, arrs[0].ctypes.data, arrs[1].ctypes.data, arrs[2].ctypes.data,
+                           None if arrs[3] is None else arrs[3].ctypes.data, arrs[4].ctypes.data, RPL_HOST)
+        return st if st == RPL_OK else _ok(st)
 
     def add_many(self, e: dict, chunk: int = 65536):
         n = len(e["a"])
@@ -370,8 +376,9 @@ class DQN:
 
     def train_step(self, replay: Replay, batch: int, loss_out=None) -> int:
         """dqn_train_step; returns RPL_OK or RPL_NOT_READY (burn-in)."""
-        st = _ok(_L.dqn_train_step(self._h, replay._h, batch, _dptr(loss_out)),
-                 (RPL_OK, RPL_NOT_READY))
+        st = _L.dqn_train_step(self._h, replay._h, batch, None if loss_out is None else loss_out.data_ptr())
+        if st != RPL_OK:
+            _ok(st, (RPL_OK, RPL_NOT_READY))
         if st == RPL_OK:
             self._last_u8 = replay.u8
         return st

@@ -1641,7 +1641,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
         }
         if (e == cudaSuccess) {
             // the zero-copy staging slot may be rewritten once the stream passes this step
-            if (zslot >= 0 && cudaEventRecord(rp->staged[zslot], d->stream) != cudaSuccess)
+            if (zslot >= 0 && cudaEventRecord(rp->evs[zslot], d->stream) != cudaSuccess)
                 e = cudaGetLastError();
         }
         if (e != cudaSuccess) {

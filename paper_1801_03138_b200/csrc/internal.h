@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <string>
+#include <deque>
 #include <vector>
 
 #include "../../include/ingpu_replay.h"
@@ -89,12 +90,21 @@ struct rpl_replay {
     // host mirror of the ring state (exact: every add is host-initiated with a known k)
     int64_t cursor = 0, size = 0;
     uint64_t total = 0, events = 0, h2d_bytes = 0;
-    // pinned host staging + device staging for RPL_HOST adds (double-buffered)
+    // pinned host staging + device staging for RPL_HOST adds: one arena (room for two adds of
+    // max_host_add experiences) used as a ring of spans, one per add, so the host can run many
+    // small adds ahead of the device; a span is reused once its event -- recorded when the
+    // device has read it (H2D copy, or the step / insert kernel consuming a zero-copy insert)
+    // -- has fired (stage_alloc)
     int64_t max_host_add = 65536;
-    void *pinned[2] = {nullptr, nullptr};
-    void *dstage[2] = {nullptr, nullptr};
-    cudaEvent_t staged[2] = {nullptr, nullptr};
-    int stage_slot = 0;
+    char *pinned = nullptr, *dstage = nullptr;
+    size_t arena = 0, head = 0;
+    struct Span {
+        size_t off, len;
+        int ev;
+    };
+    std::deque<Span> live;                 // spans the device may still read, oldest first
+    std::vector<cudaEvent_t> evs;          // event pool (index = Pending::slot)
+    std::vector<int> free_evs;
     uint32_t *err_dev = nullptr;   // sticky device error word
     // device control block read by graph-replayed train steps: [0] sampler events consumed,
     // [1] filled size, [2] cursor (kept equal to the host mirror by the kernels that change them)

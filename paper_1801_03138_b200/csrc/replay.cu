@@ -491,7 +491,34 @@ uint64_t oldest_slot(const rpl_replay *rp)
 
 int replay_consumed(rpl_replay *rp, int slot, cudaStream_t st)
 {
-    if (slot >= 0) RPL_CUDA(cudaEventRecord(rp->staged[slot], st));
+    if (slot >= 0) RPL_CUDA(cudaEventRecord(rp->evs[slot], st));
+    return RPL_OK;
+}
+
+// the next staging span of `len` bytes (a multiple of 64): wraps to the arena start when the
+// tail is too short, and waits for the oldest live spans it would overwrite (their events were
+// all recorded: an add first flushes the previous deferred insert, which records its span's)
+static int stage_alloc(rpl_replay *rp, size_t len, size_t *off, int *ev)
+{
+    if (rp->head + len > rp->arena) rp->head = 0;
+    while (!rp->live.empty()) {
+        const rpl_replay::Span &f = rp->live.front();
+        if (!(f.off < rp->head + len && rp->head < f.off + f.len)) break;   // oldest first
+        RPL_CUDA(cudaEventSynchronize(rp->evs[f.ev]));
+        rp->free_evs.push_back(f.ev);
+        rp->live.pop_front();
+    }
+    if (rp->free_evs.empty()) {
+        cudaEvent_t e = nullptr;
+        RPL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        rp->evs.push_back(e);
+        rp->free_evs.push_back((int)rp->evs.size() - 1);
+    }
+    *ev = rp->free_evs.back();
+    rp->free_evs.pop_back();
+    *off = rp->head;
+    rp->live.push_back({rp->head, len, *ev});
+    rp->head += len;
     return RPL_OK;
 }
 
@@ -738,15 +765,13 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
             return RPL_ENOMEM;
         }
     }
-    const size_t st = host_add_bytes(rp->max_host_add, state_dim, u8) + 64;
+    const size_t st = host_add_bytes(rp->max_host_add, state_dim, u8) + 64 * 5;
+    rp->arena = 2 * st;
     bool ok = cudaMalloc(&rp->err_dev, sizeof(uint32_t)) == cudaSuccess &&
               cudaMalloc(&rp->ctrl_dev, 3 * sizeof(uint64_t)) == cudaSuccess &&
-              cudaMemsetAsync(rp->ctrl_dev, 0, 3 * sizeof(uint64_t), rp->stream) == cudaSuccess;
-    for (int i = 0; i < 2 && ok; ++i) {
-        ok = cudaHostAlloc(&rp->pinned[i], st, cudaHostAllocDefault) == cudaSuccess &&
-             cudaMalloc(&rp->dstage[i], st) == cudaSuccess &&
-             cudaEventCreateWithFlags(&rp->staged[i], cudaEventDisableTiming) == cudaSuccess;
-    }
+              cudaMemsetAsync(rp->ctrl_dev, 0, 3 * sizeof(uint64_t), rp->stream) == cudaSuccess &&
+              cudaHostAlloc((void **)&rp->pinned, rp->arena, cudaHostAllocDefault) == cudaSuccess &&
+              cudaMalloc((void **)&rp->dstage, rp->arena) == cudaSuccess;
     if (!ok || cudaMemsetAsync(rp->err_dev, 0, sizeof(uint32_t), rp->stream) != cudaSuccess ||
         (!rp->ring.host && cudaMemsetAsync(rp->ring.rows, 0, ring_bytes, rp->stream) != cudaSuccess)) {
         set_error("replay_create: staging allocation of %zu bytes failed", st);
@@ -764,11 +789,9 @@ extern "C" int replay_destroy(rpl_replay *rp)
     rp->pend.k = 0;   // a never-consumed deferred insert is dropped with the ring
     rp->pend.slot = -1;
     cudaStreamSynchronize(rp->stream);
-    for (int i = 0; i < 2; ++i) {
-        if (rp->staged[i]) cudaEventDestroy(rp->staged[i]);
-        if (rp->pinned[i]) cudaFreeHost(rp->pinned[i]);
-        if (rp->dstage[i]) cudaFree(rp->dstage[i]);
-    }
+    for (cudaEvent_t ev : rp->evs) cudaEventDestroy(ev);
+    if (rp->pinned) cudaFreeHost(rp->pinned);
+    if (rp->dstage) cudaFree(rp->dstage);
     if (rp->err_dev) cudaFree(rp->err_dev);
     if (rp->ctrl_dev) cudaFree(rp->ctrl_dev);
     if (rp->ds_idx) cudaFree(rp->ds_idx);
@@ -882,28 +905,32 @@ static int add_rows(rpl_replay *rp, int64_t k, const void *s, const int32_t *a, 
                 set_error("replay_add: done[%lld]=%u not in {0,1}", (long long)j, done[j]);
                 return RPL_ECORRUPT;
             }
-        const int slot = rp->stage_slot;
-        rp->stage_slot ^= 1;
-        // the pinned slot may still be read by the previous H2D copy from it
-        RPL_CUDA(cudaEventSynchronize(rp->staged[slot]));
-        char *hp = (char *)rp->pinned[slot];
-        char *dp = (char *)rp->dstage[slot];
-        // [r | a | s | s' | done]: the 4-byte fields first so every section stays aligned
+        // [r | a | s | s' | done], each section 64-byte aligned, in the next span of the arena
         const size_t bs = (size_t)k * D * (rp->ring.u8 ? 1 : sizeof(float));
-        size_t off = 0;
-        memcpy(hp + off, r, (size_t)k * 4); dr = (const float *)(dp + off); off += (size_t)k * 4;
-        memcpy(hp + off, a, (size_t)k * 4); da = (const int32_t *)(dp + off); off += (size_t)k * 4;
-        memcpy(hp + off, s, bs); ds = dp + off; off += bs;
+        auto up = [](size_t x) { return (x + 63) & ~(size_t)63; };
+        const size_t len = up((size_t)k * 4) * 2 + up(bs) * (rp->ring.shared ? 1 : 2) + up((size_t)k);
+        size_t base = 0;
+        int slot = -1;
+        if (int rc = stage_alloc(rp, len, &base, &slot)) return rc;
+        char *hp = rp->pinned + base;
+        char *dp = rp->dstage + base;
+        size_t off = 0, bytes = 0;
+        memcpy(hp + off, r, (size_t)k * 4); dr = (const float *)(dp + off); off += up((size_t)k * 4);
+        memcpy(hp + off, a, (size_t)k * 4); da = (const int32_t *)(dp + off); off += up((size_t)k * 4);
+        memcpy(hp + off, s, bs); ds = dp + off; off += up(bs);
+        bytes = (size_t)k * 8 + bs;
         if (!rp->ring.shared) {   // shared states: one state per experience crosses PCIe
-            memcpy(hp + off, s_next, bs); ds2 = dp + off; off += bs;
+            memcpy(hp + off, s_next, bs); ds2 = dp + off; off += up(bs);
+            bytes += bs;
         }
-        memcpy(hp + off, done, (size_t)k); dd = (const uint8_t *)(dp + off); off += (size_t)k;
-        rp->h2d_bytes += off;
+        memcpy(hp + off, done, (size_t)k); dd = (const uint8_t *)(dp + off); off += up((size_t)k);
+        bytes += (size_t)k;
+        rp->h2d_bytes += bytes;
         if (rp->zero_copy && !rp->ring.u8 && !rp->no_defer && k <= kMaxDeferredRows) {
             // zero-copy: the deferred insert's sources are the pinned slot itself -- the
             // device reads them over PCIe (once, for the ring write) when it consumes the
             // insert, so no copy op enters the stream; the slot's event is recorded then
-            const char *dev0 = (const char *)rp->dstage[slot];
+            const char *dev0 = dp;
             auto host_of = [&](const void *d) { return (const void *)(hp + ((const char *)d - dev0)); };
             ds = host_of(ds);
             if (ds2) ds2 = host_of(ds2);
@@ -913,7 +940,7 @@ static int add_rows(rpl_replay *rp, int64_t k, const void *s, const int32_t *a, 
             zslot = slot;
         } else {
             RPL_CUDA(cudaMemcpyAsync(dp, hp, off, cudaMemcpyHostToDevice, rp->stream));
-            RPL_CUDA(cudaEventRecord(rp->staged[slot], rp->stream));
+            RPL_CUDA(cudaEventRecord(rp->evs[slot], rp->stream));
         }
     }
     const int64_t new_size = rp->size + k < rp->ring.capacity ? rp->size + k : rp->ring.capacity;

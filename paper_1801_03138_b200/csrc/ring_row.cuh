@@ -48,4 +48,45 @@ __device__ __forceinline__ void ring_write_row(float *row, int rs, int D, int sw
     }
 }
 
+// the same row in two halves: every word of a row of <= 32 RW_PRE words into registers first
+// (all loads in flight at once: one round trip, e.g. over PCIe for a zero-copy source) ...
+constexpr int RW_PRE = 4;
+__device__ __forceinline__ void ring_load_row(float v[RW_PRE], int rs, int D, int sw, int lane, int64_t j,
+                                              const float *__restrict__ s, const int32_t *__restrict__ a,
+                                              const float *__restrict__ r, const float *__restrict__ s2,
+                                              const uint8_t *__restrict__ done, uint32_t *err)
+{
+#pragma unroll
+    for (int q = 0; q < RW_PRE; ++q) {
+        const int c = lane + 32 * q;
+        float x = 0.0f;
+        if (c < rs) {
+            if (c < D) {
+                x = s[j * D + c];
+            } else if (c < sw) {
+                x = s2[j * D + (c - D)];
+            } else if (c == sw) {
+                x = __int_as_float(a[j]);
+            } else if (c == sw + 1) {
+                x = r[j];
+            } else if (c == sw + 2) {
+                uint32_t d = done[j];
+                if (d > 1u) {
+                    atomicOr(err, ERRBIT_CORRUPT);
+                    d = 1u;
+                }
+                x = __uint_as_float(d);
+            }
+        }
+        v[q] = x;
+    }
+}
+// ... and stored later
+__device__ __forceinline__ void ring_store_row(float *row, const float v[RW_PRE], int rs, int lane)
+{
+#pragma unroll
+    for (int q = 0; q < RW_PRE; ++q)
+        if (lane + 32 * q < rs) row[lane + 32 * q] = v[q];
+}
+
 }  // namespace rpl

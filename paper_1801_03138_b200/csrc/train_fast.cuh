@@ -809,14 +809,25 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
     // the deferred insert's ring rows (no sampled row of this step reads them from the ring;
     // the next step's K1 follows K4): written by the first CTAs -- dW1 tasks, the shortest --
     // after their task, so the (possibly PCIe) source loads stay off the critical path
+    // A warp's first row (rows <= 128 words) is loaded into registers before the CTA's task, so
+    // a zero-copy source's PCIe round trip overlaps the task instead of following it
+    const int pw = threadIdx.x >> 5, plane = threadIdx.x & 31;
+    const int64_t pj0 = (int64_t)blockIdx.x * (F_NT3 / 32) + pw;
+    const bool pre = p.pend_k && pj0 < p.pend_k && p.rs <= 32 * RW_PRE;
+    float prow[RW_PRE];
+    if (pre) ring_load_row(prow, p.rs, p.D, p.sw, plane, pj0, p.pend_s, p.pend_a, p.pend_r, p.pend_s2,
+                           p.pend_done, p.pend_err);
     auto write_pending = [&]() {
         if (!p.pend_k) return;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = F_NT3 / 32;
-        for (int j = blockIdx.x * nw + warp; j < p.pend_k; j += gridDim.x * nw) {
+        for (int64_t j = blockIdx.x * nw + warp; j < p.pend_k; j += (int64_t)gridDim.x * nw) {
             int64_t slot = p.pend_cur + j;
             if (slot >= p.capacity) slot -= p.capacity;
-            ring_write_row(p.ring + slot * p.rs, p.rs, p.D, p.sw, lane, j, p.pend_s, p.pend_a,
-                           p.pend_r, p.pend_s2, p.pend_done, p.pend_err);
+            if (pre && j == pj0)
+                ring_store_row(p.ring + slot * p.rs, prow, p.rs, lane);
+            else
+                ring_write_row(p.ring + slot * p.rs, p.rs, p.D, p.sw, lane, j, p.pend_s, p.pend_a,
+                               p.pend_r, p.pend_s2, p.pend_done, p.pend_err);
         }
     };
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
@@ -1054,6 +1065,12 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
     const float loss = lsum / (float)B;
     const bool ok = isfinite(loss);
     const bool upd = p.apply_update && ok;
+    // the loss leaves first: a caller's loss_out may be pinned host memory, and that PCIe write
+    // then completes while the SGD below runs instead of at the kernel's end
+    if (blockIdx.x == 0 && tid == 0) {
+        p.grad[p.P] = loss;
+        if (p.loss_out) *p.loss_out = loss;
+    }
     const float lr = p.lr;
     trace_.mark(2);
     auto w0_finish = [&](int64_t i) {
@@ -1131,8 +1148,6 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
         }
     }
     if (blockIdx.x == 0 && tid == 0) {
-        p.grad[p.P] = loss;
-        if (p.loss_out) *p.loss_out = loss;
         if (!ok) atomicOr(p.err, ERRBIT_NUMERIC);
         // fire-and-forget reductions (no load round trip on the kernel's tail); with wide
         // inputs the sampling gather has advanced the event already
