@@ -663,8 +663,11 @@ def run_c5(a):
         e2e = {"value": world * K / (max(e2e_ms / 1000.0, wall)), "unit": "train_steps/s",
                "h2d_bytes_per_step": (rp.state()["h2d_bytes"] - h2d0) / K,
                "d2h_bytes_per_step": 4,
-               "note": "replay_add(RPL_HOST) of byte states -> pinned staging -> H2D, "
-                       "dqn_train_step, loss D2H every step; slower of CUDA-event and wall time"}
+               "us_per_step_device": e2e_ms * 1000.0 / K, "us_per_step_wall": wall * 1e6 / K,
+               "note": "replay_add(RPL_HOST) of byte states -> pinned staging -> H2D on the replay's "
+                       "copy stream (overlapping the previous step), insert kernel, dqn_train_step "
+                       "whose last kernel writes the loss into pinned host memory, every step; "
+                       "slower of CUDA-event and wall time"}
 
     flops = binding.step_flops(cfg, batch)
     kern_avg_ms = float(np.mean(kern_ms))

@@ -105,6 +105,8 @@ struct rpl_replay {
     std::deque<Span> live;                 // spans the device may still read, oldest first
     std::vector<cudaEvent_t> evs;          // event pool (index = Pending::slot)
     std::vector<int> free_evs;
+    cudaStream_t copy_stream = nullptr;    // H2D copies of host adds (overlap the work stream)
+    cudaEvent_t copy_done = nullptr;
     uint32_t *err_dev = nullptr;   // sticky device error word
     // device control block read by graph-replayed train steps: [0] sampler events consumed,
     // [1] filled size, [2] cursor (kept equal to the host mirror by the kernels that change them)

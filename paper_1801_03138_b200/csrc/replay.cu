@@ -771,7 +771,9 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
               cudaMalloc(&rp->ctrl_dev, 3 * sizeof(uint64_t)) == cudaSuccess &&
               cudaMemsetAsync(rp->ctrl_dev, 0, 3 * sizeof(uint64_t), rp->stream) == cudaSuccess &&
               cudaHostAlloc((void **)&rp->pinned, rp->arena, cudaHostAllocDefault) == cudaSuccess &&
-              cudaMalloc((void **)&rp->dstage, rp->arena) == cudaSuccess;
+              cudaMalloc((void **)&rp->dstage, rp->arena) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&rp->copy_stream, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&rp->copy_done, cudaEventDisableTiming) == cudaSuccess;
     if (!ok || cudaMemsetAsync(rp->err_dev, 0, sizeof(uint32_t), rp->stream) != cudaSuccess ||
         (!rp->ring.host && cudaMemsetAsync(rp->ring.rows, 0, ring_bytes, rp->stream) != cudaSuccess)) {
         set_error("replay_create: staging allocation of %zu bytes failed", st);
@@ -790,6 +792,11 @@ extern "C" int replay_destroy(rpl_replay *rp)
     rp->pend.slot = -1;
     cudaStreamSynchronize(rp->stream);
     for (cudaEvent_t ev : rp->evs) cudaEventDestroy(ev);
+    if (rp->copy_stream) {
+        cudaStreamSynchronize(rp->copy_stream);
+        cudaStreamDestroy(rp->copy_stream);
+    }
+    if (rp->copy_done) cudaEventDestroy(rp->copy_done);
     if (rp->pinned) cudaFreeHost(rp->pinned);
     if (rp->dstage) cudaFree(rp->dstage);
     if (rp->err_dev) cudaFree(rp->err_dev);
@@ -937,6 +944,15 @@ static int add_rows(rpl_replay *rp, int64_t k, const void *s, const int32_t *a, 
             dr = (const float *)host_of(dr);
             da = (const int32_t *)host_of(da);
             dd = (const uint8_t *)host_of(dd);
+            zslot = slot;
+        } else if (rp->copy_stream) {
+            // the H2D copy runs on the replay's copy stream, overlapping whatever the work
+            // stream is doing (typically the previous train step); the work stream waits for
+            // it before the insert reads the span, and the span's event is recorded once that
+            // consumer has run (its region is then free for a later add's copy)
+            RPL_CUDA(cudaMemcpyAsync(dp, hp, off, cudaMemcpyHostToDevice, rp->copy_stream));
+            RPL_CUDA(cudaEventRecord(rp->copy_done, rp->copy_stream));
+            RPL_CUDA(cudaStreamWaitEvent(rp->stream, rp->copy_done, 0));
             zslot = slot;
         } else {
             RPL_CUDA(cudaMemcpyAsync(dp, hp, off, cudaMemcpyHostToDevice, rp->stream));
