@@ -126,10 +126,14 @@ int replay_destroy(rpl_replay *replay);
  * capacity), total += k.  Inputs are SoA: s[k*state_dim], a[k], r[k],
  * s_next[k*state_dim] (fp32, or u8 for RPL_U8 replays), done[k] in {0,1}.
  * mem = RPL_HOST: host pointers, copied into
- * pinned staging before return (the caller may reuse them at once); one H2D copy of
- * k*(8*state_dim+9) bytes is counted in replay_state's h2d_bytes -- the only PCIe
- * traffic of the method; a deferred host add is read by the device straight from
- * the pinned staging (zero-copy) when the step consumes it.  mem = RPL_DEVICE: device pointers that must stay
+ * pinned staging before return (the caller may reuse them at once); one H2D transfer of
+ * k*(8*state_dim+9) bytes (fp32 states; k*(2*state_dim+9) for u8) is counted in replay_state's
+ * h2d_bytes -- the only PCIe traffic of the method.  A deferred host add is read by
+ * the device straight from the pinned staging (zero-copy) when the step consumes it; any other
+ * host add is copied on the replay's own copy stream, so the transfer overlaps work already
+ * queued on the replay's stream, which waits for it before the insert.  Staging is a ring of
+ * 2*max_host_add experiences: many small adds can be in flight; an add blocks only when it
+ * would overwrite a span the device has not consumed yet.  mem = RPL_DEVICE: device pointers that must stay
  * valid until the stream reaches the insert.  mem = RPL_DEVICE_DEFER: device pointers
  * whose contents must stay valid AND unchanged until the next call on this replay or the
  * next dqn_train_step on it has been reached by the stream.
