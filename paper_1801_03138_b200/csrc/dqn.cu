@@ -790,6 +790,7 @@ struct rpl_dqn {
     uint16_t *dz0bf = nullptr;             // bf16 planes of dZ0 [3][max_batch][N0]
     bool w0bf_stale = true;                // planes to be re-split from the fp32 weights
     int wide_ks = 0, wide_cs = 1;          // wide_l0_kernel chunks and cluster size (wide_l0_plan)
+    int k1_mc_clusters = 0;                // co-resident clusters of the multicast K1 (0: not used)
     unsigned long long *trace = nullptr;   // RPL_TRACE=1: per-CTA timestamps of the fast kernels
     // data parallel
     void *comm = nullptr;
@@ -898,6 +899,13 @@ static fwd_fn fast_fwd_fn(const rpl_dqn *d)
     if (ut == 128) return fast_fwd_kernel<128, 0, 0, 0>;
     if (ut == 64) return fast_fwd_kernel<64, 0, 0, 0>;
     return fast_fwd_kernel<32, 0, 0, 0>;
+}
+// the clustered K1 with multicast weight staging (paper net only), or null
+static fwd_fn fast_fwd_mc_fn(const rpl_dqn *d)
+{
+    const int ut = fast_ut(d), D = d->cfg.state_dim, N0 = d->N[0], J = d->J;
+    if (ut == 128 && D == 27 && N0 == 128 && J == 9) return fast_fwd_mc_kernel<128, 27, 128, 9>;
+    return nullptr;
 }
 static size_t fast_fwd_smem(const rpl_dqn *d, int ut, int D = -1)
 {
@@ -1074,6 +1082,22 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
         ok = ok && cudaStreamCreateWithFlags(&d->cap_stream, cudaStreamNonBlocking) == cudaSuccess;
         ok = ok && cudaFuncSetAttribute(fast_fwd_fn(d), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         fast_fwd_smem(d, ut)) == cudaSuccess;
+        // clustered K1 (multicast weights; opt-in RPL_K1MC=1: 9.6 vs 7.9 us per K1 measured,
+        // DESIGN.md §12): how many K1_MC-CTA clusters can be co-resident
+        if (ok && fast_fwd_mc_fn(d)) {
+            const char *nm = getenv("RPL_K1MC");
+            if ((nm && nm[0] == '1') &&
+                cudaFuncSetAttribute(fast_fwd_mc_fn(d), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     fast_fwd_smem(d, ut)) == cudaSuccess) {
+                cudaLaunchConfig_t lc = {};
+                lc.gridDim = dim3(K1_MC);
+                lc.blockDim = dim3(F_NT1);
+                lc.dynamicSmemBytes = fast_fwd_smem(d, ut);
+                int n = 0;
+                if (cudaOccupancyMaxActiveClusters(&n, fast_fwd_mc_fn(d), &lc) == cudaSuccess) d->k1_mc_clusters = n;
+            }
+            cudaGetLastError();
+        }
 
         ok = ok && cudaFuncSetAttribute(fast_bwd1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         K3_SMEM_FLOATS * sizeof(float)) == cudaSuccess;
@@ -1086,6 +1110,9 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
             for (const void *f : fns)
                 ok = ok && cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                                 cudaSharedmemCarveoutMaxShared) == cudaSuccess;
+            if (ok && fast_fwd_mc_fn(d))
+                ok = cudaFuncSetAttribute((const void *)fast_fwd_mc_fn(d), cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          cudaSharedmemCarveoutMaxShared) == cudaSuccess;
         }
         ok = ok && fast_td_smem(d) <= 200 * 1024 &&
              cudaFuncSetAttribute(fast_td_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1387,7 +1414,10 @@ static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
         e = launch_pdl(distinct_fast_kernel, 1, DS_T, ds_smem_bytes(p.B), st, false, p);
         if (e != cudaSuccess) return e;
     }
-    e = launch_pdl(fast_fwd_fn(d), g1, F_NT1, sm1, st, false, p);
+    // one task per CTA in whole co-resident clusters sharing a weight tile: the multicast K1
+    const bool mc = d->k1_mc_clusters > 0 && g1 == k1_tasks && nbt % K1_MC == 0 &&
+                    k1_tasks <= d->k1_mc_clusters * K1_MC && fast_fwd_mc_fn(d) && p.h0_in == nullptr;
+    e = launch_pdl(mc ? fast_fwd_mc_fn(d) : fast_fwd_fn(d), g1, F_NT1, sm1, st, false, p);
     if (e != cudaSuccess) return e;
     e = launch_pdl(fast_td_kernel, std::min(p.B, 4 * d->sms), NT, fast_td_smem(d), st,
                    pdl || d->k2_pdl, p);
@@ -1576,7 +1606,9 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                         if (cudaGraphNodeGetType(nodes[i], &ty) == cudaSuccess &&
                             ty == cudaGraphNodeTypeKernel &&
                             cudaGraphKernelNodeGetParams(nodes[i], &kp) == cudaSuccess) {
-                            if (kp.func == (void *)fast_fwd_fn(d)) k1 = nodes[i];
+                            if (kp.func == (void *)fast_fwd_fn(d) ||
+                                (fast_fwd_mc_fn(d) && kp.func == (void *)fast_fwd_mc_fn(d)))
+                                k1 = nodes[i];
                             if (kp.func == (void *)distinct_fast_kernel) ds = nodes[i];
                             if (kp.func == (void *)fast_bwd1_kernel) k3 = nodes[i];
                             if (kp.func == (void *)fast_bwd0_sgd_kernel) k4 = nodes[i];

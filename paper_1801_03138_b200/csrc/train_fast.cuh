@@ -277,10 +277,14 @@ struct FwdLayout {
 // w, w+16, ... of 8 output units.  Compile-time dims (KD, KN0, KJ) for the paper's /
 // configs[0] nets; 0 = read at run time.
 // ------------------------------------------------------------------------------------------
-template <int UT, int KD, int KN0, int KJ>
-__global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constant__ FastArgs p)
+// MC > 1: the kernel runs in clusters of MC CTAs that share one weight tile (consecutive
+// batch tiles of one (net, unit tile)); each CTA loads 1/MC of the tile's rows with TMA
+// multicast into every CTA of the cluster, so L2 serves the weights once per cluster
+template <int UT, int KD, int KN0, int KJ, int MC>
+__device__ __forceinline__ void fast_fwd_body(const FastArgs &p)
 {
     CtaTrace trace_(p.trace, 0);
+    __shared__ uint64_t wbar;   // MC > 1: the multicast weight bytes have landed
     pdl_trigger();
     extern __shared__ float4 smem4[];
     float *sm = reinterpret_cast<float *>(smem4);
@@ -308,11 +312,19 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
     }
     const int ntasks = p.nets * nbt * nut;
     // tasks are (net, unit tile)-major: with the grid a multiple of nets x nut (large batches),
-    // a CTA keeps one weight tile resident and walks batch tiles, loading the weights once
+    // a CTA keeps one weight tile resident and walks batch tiles, loading the weights once.
+    // MC > 1 (one task per CTA): batch tiles fastest, so a cluster shares its weight tile
     const int ncombo = p.nets * nut;
     int loaded = -1;
+    if (MC > 1) {
+        if (tid == 0) {
+            umma::mbar_init(&wbar, 1);
+            umma::fence_mbar_init();
+        }
+        cooperative_groups::this_cluster().sync();   // every peer's barrier exists before data lands
+    }
     for (int task = blockIdx.x; task < ntasks; task += gridDim.x) {
-        const int combo = task % ncombo, bt = task / ncombo;
+        const int combo = MC > 1 ? task / nbt : task % ncombo, bt = MC > 1 ? task % nbt : task / ncombo;
         const int net = combo / nut, ut = combo % nut;
         const int rb = bt * F_BT, u0 = ut * UT;
         const int nu = min(UT, N1 - u0);   // valid units in this tile (multiple of 4)
@@ -321,7 +333,33 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
         loaded = combo;
         __syncthreads();   // the previous task is done with shared memory
         // (1) weights -> shared memory, all 16-byte cp.async (no load waits on another)
-        if (reload) {
+        if (reload && MC > 1) {
+            // rows u = rank, rank + MC, ... of the W1 tile and 1/MC of W0 from this CTA, each
+            // bulk copy multicast to the whole cluster; the barrier expects the full tile
+            const int rk = (int)(blockIdx.x % MC);
+            const uint16_t all = (uint16_t)((1u << MC) - 1u);
+            const uint32_t w0b = (uint32_t)(N0 * D * 4), w0c = w0b / MC;
+            const bool w0split = !p.h0_in && w0c % 16 == 0;
+            if (tid == 0)
+                umma::mbar_expect_tx(&wbar, (uint32_t)(nu * N0 * 4) + (p.h0_in ? 0u : w0b));
+            if (warp == 0) {
+                for (int u = rk + MC * lane; u < nu; u += MC * 32)
+                    umma::bulk_g2s_mc(W1s + u * L.N0P, theta + p.w1 + (int64_t)(u0 + u) * N0, N0 * 4, &wbar, all);
+                if (lane == 0 && !p.h0_in) {
+                    if (w0split)
+                        umma::bulk_g2s_mc(reinterpret_cast<char *>(W0f) + rk * w0c,
+                                          reinterpret_cast<const char *>(theta + p.w0) + rk * w0c, w0c, &wbar, all);
+                    else if (rk == 0)
+                        umma::bulk_g2s_mc(W0f, theta + p.w0, w0b, &wbar, all);
+                }
+            }
+            const int c4 = N0 / 4;
+            for (int e = nu * c4 + tid; e < UT * c4; e += F_NT1) {
+                const int u = e / c4, c = e - u * c4;
+                *reinterpret_cast<float4 *>(W1s + u * L.N0P + 4 * c) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            if (!p.h0_in) cp_async_row(b0s, theta + p.b0, N0, tid, F_NT1);
+        } else if (reload) {
             const int c4 = N0 / 4;
             for (int e = tid; e < UT * c4; e += F_NT1) {
                 const int u = e / c4, c = e - u * c4;
@@ -333,6 +371,8 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
                 cp_async_row(W0f, theta + p.w0, N0 * D, tid, F_NT1);
                 cp_async_row(b0s, theta + p.b0, N0, tid, F_NT1);
             }
+        }
+        if (reload) {
             cp_async_row(b1s, theta + p.b1 + u0, nu, tid, F_NT1);
             for (int u = nu + tid; u < UT; u += F_NT1) b1s[u] = 0.0f;
         }
@@ -358,6 +398,7 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
             // of this net and split them into tf32 hi / lo
             const float *h0 = p.h0_in + ((int64_t)net * B + rb) * N0;
             cp_async_wait_all();   // the weight tiles
+            if (MC > 1 && reload) umma::mbar_wait(&wbar, 0);
             for (int e = tid; e < F_BT * N0; e += F_NT1) {
                 const int rr = e / N0, cc = e - rr * N0;
                 const float h = rb + rr < B ? __ldcg(h0 + (int64_t)rr * N0 + cc) : 0.0f;
@@ -425,6 +466,7 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
             }
             trace_.mark(2);
             cp_async_wait_all();
+            if (MC > 1 && reload) umma::mbar_wait(&wbar, 0);   // the multicast W1 / W0 tiles
             __syncthreads();
             trace_.mark(3);
             // split X into tf32 hi / lo (zero beyond D); unpack the batch once for the backward
@@ -550,6 +592,21 @@ __global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constan
             if (rb + rr < B) p.part[(((int64_t)net * nut + ut) * B + rb + rr) * J + j] = v;
         }
     }
+    if (MC > 1) cooperative_groups::this_cluster().sync();   // no CTA leaves while peers' copies fly
+}
+
+template <int UT, int KD, int KN0, int KJ>
+__global__ void __launch_bounds__(F_NT1, 1) fast_fwd_kernel(const __grid_constant__ FastArgs p)
+{
+    fast_fwd_body<UT, KD, KN0, KJ, 1>(p);
+}
+
+constexpr int K1_MC = 4;   // cluster size of the multicast K1 (co-residency: scripts/mb_cluster.cu)
+template <int UT, int KD, int KN0, int KJ>
+__global__ void __cluster_dims__(K1_MC, 1, 1) __launch_bounds__(F_NT1, 1)
+    fast_fwd_mc_kernel(const __grid_constant__ FastArgs p)
+{
+    fast_fwd_body<UT, KD, KN0, KJ, K1_MC>(p);
 }
 
 // ------------------------------------------------------------------------------------------

@@ -92,6 +92,16 @@ __device__ __forceinline__ void bulk_g2s(void *smem, const void *gmem, uint32_t 
                  :: "r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(mbar)) : "memory");
 }
 
+// the same copy delivered to the same shared-memory offset (data and mbarrier) of every CTA
+// of the cluster in ctaMask (TMA multicast)
+__device__ __forceinline__ void bulk_g2s_mc(void *smem, const void *gmem, uint32_t bytes, uint64_t *mbar,
+                                            uint16_t mask)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+                 "[%0], [%1], %2, [%3], %4;"
+                 :: "r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(mbar)), "h"(mask) : "memory");
+}
+
 // operands written with ordinary st.shared must be made visible to the tensor core (async proxy)
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
