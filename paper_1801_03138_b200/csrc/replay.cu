@@ -384,8 +384,7 @@ __global__ void __launch_bounds__(256) insert_u8_kernel(uint8_t *__restrict__ ro
     }
 }
 
-// Philox sample (or caller indices) + gather + unpack of byte-state rows: one CTA per piece
-constexpr int64_t kGatherPiece = 8192;   // bytes of an entry's states per gather CTA
+// Philox sample (or caller indices) + gather + unpack of byte-state rows: one CTA per entry
 __global__ void __launch_bounds__(256) gather_u8_kernel(const uint8_t *__restrict__ rows, int64_t rsb,
                                                         int so, int D, int shared, int64_t capacity,
                                                         uint64_t oldest, int64_t nvalid, int64_t size, int64_t n,
@@ -403,12 +402,7 @@ __global__ void __launch_bounds__(256) gather_u8_kernel(const uint8_t *__restric
         oldest = (shared && size == capacity) ? ctrl_in[2] : 0;
     }
     if (idx_in == nullptr && ctrl && blockIdx.x == 0 && threadIdx.x == 0) ctrl[0] = event + 1;
-    // an entry's state bytes (s, then s') are cut into kGatherPiece-byte pieces, one CTA each
-    // (every piece's CTA draws the entry's index itself; piece 0 writes the scalars)
-    const int64_t L2 = 2 * (int64_t)D;
-    const int64_t np = (L2 + kGatherPiece - 1) / kGatherPiece;
-    for (int64_t w = blockIdx.x; w < n * np; w += gridDim.x) {
-        const int64_t e = w / np, q = w % np;
+    for (int64_t e = blockIdx.x; e < n; e += gridDim.x) {
         if (threadIdx.x == 0) {
             int32_t ix;
             if (idx_in == nullptr) {
@@ -418,28 +412,21 @@ __global__ void __launch_bounds__(256) gather_u8_kernel(const uint8_t *__restric
             } else {
                 ix = idx_in[e];
                 if (ix < 0 || ix >= size) {
-                    if (q == 0) atomicOr(err, ERRBIT_RANGE);
+                    atomicOr(err, ERRBIT_RANGE);
                     ix = min(max(ix, 0), (int32_t)size - 1);
                 }
             }
             ix_s = ix;
-            if (q == 0) {
-                if (idx_out) idx_out[e] = ix;
-                const uint32_t *sc = reinterpret_cast<const uint32_t *>(rows + (int64_t)ix * rsb + so);
-                if (a) a[e] = (int32_t)__ldg(sc);
-                if (r) r[e] = __uint_as_float(__ldg(sc + 1));
-                if (done) done[e] = (uint8_t)(__ldg(sc + 2) != 0u);
-            }
+            if (idx_out) idx_out[e] = ix;
+            const uint32_t *sc = reinterpret_cast<const uint32_t *>(rows + (int64_t)ix * rsb + so);
+            if (a) a[e] = (int32_t)__ldg(sc);
+            if (r) r[e] = __uint_as_float(__ldg(sc + 1));
+            if (done) done[e] = (uint8_t)(__ldg(sc + 2) != 0u);
         }
         __syncthreads();
         const uint8_t *row = rows + (int64_t)ix_s * rsb;
-        const int64_t b0 = q * kGatherPiece, b1 = b0 + kGatherPiece < L2 ? b0 + kGatherPiece : L2;
-        if (s && b0 < D) copy_bytes_cta(s + e * D + b0, row + b0, (b1 < D ? b1 : D) - b0);
-        if (s2 && b1 > D) {
-            const int64_t c0 = b0 > D ? b0 : D;
-            const uint8_t *src2 = shared ? rows + (int64_t)((ix_s + 1) % capacity) * rsb : row + D;
-            copy_bytes_cta(s2 + e * D + (c0 - D), src2 + (c0 - D), b1 - c0);
-        }
+        if (s) copy_bytes_cta(s + e * D, row, D);
+        if (s2) copy_bytes_cta(s2 + e * D, shared ? rows + (int64_t)((ix_s + 1) % capacity) * rsb : row + D, D);
         __syncthreads();   // ix_s reuse
     }
 }
@@ -482,8 +469,7 @@ int launch_gather_u8_dev(rpl_replay *rp, int64_t n, const rpl_batch *out, cudaSt
     const rpl::Ring &R = rp->ring;
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, rp->device);
-    const int64_t pieces = n * ((2 * (int64_t)R.D + kGatherPiece - 1) / kGatherPiece);
-    int64_t nb = pieces < (int64_t)dev_sms * 8 ? pieces : (int64_t)dev_sms * 8;
+    int64_t nb = n < (int64_t)dev_sms * 8 ? n : (int64_t)dev_sms * 8;
     if (nb < 1) nb = 1;
     gather_u8_kernel<<<(unsigned)nb, 256, 0, st>>>(
         reinterpret_cast<const uint8_t *>(R.rows), (int64_t)R.rs * 4, R.so, R.D, R.shared,
@@ -602,8 +588,7 @@ int launch_gather(rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t ev
     const int64_t nvalid = sampleable(rp);
     const uint64_t oldest = oldest_slot(rp);
     if (R.u8) {
-        const int64_t pieces = n * ((2 * (int64_t)R.D + kGatherPiece - 1) / kGatherPiece);
-        int64_t nb = pieces < (int64_t)dev_sms * 8 ? pieces : (int64_t)dev_sms * 8;
+        int64_t nb = n < (int64_t)dev_sms * 8 ? n : (int64_t)dev_sms * 8;
         if (nb < 1) nb = 1;
         gather_u8_kernel<<<(unsigned)nb, 256, 0, rp->stream>>>(
             reinterpret_cast<const uint8_t *>(R.rows), (int64_t)R.rs * 4, R.so, R.D, R.shared,
