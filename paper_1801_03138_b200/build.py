@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libingpu_replay.so")
 SOURCES = ["replay.cu", "dqn.cu"]
-HEADERS = ["internal.h", "philox.cuh", "simt_gemm.cuh", "train_fast.cuh", "mma_tf32.cuh"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".h", ".cuh")))
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
@@ -23,7 +23,7 @@ FLAGS = [
     "-Xcompiler", "-fPIC,-O2,-Wall",
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
-]
+] + os.environ.get("RPL_NVCC_FLAGS", "").split()   # extra flags for A/B builds (e.g. -D...)
 
 
 def _stale() -> bool:
