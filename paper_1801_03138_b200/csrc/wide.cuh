@@ -51,7 +51,6 @@ __host__ __device__ inline int wd_dw0_smem(int ntile)
 
 struct WideArgs {
     int D, B, N0, nets, ks;          // inputs, batch, layer-0 units (== 128), nets, k-chunks
-    int64_t kchunk;                  // unused by wide_l0_kernel (chunks are slice ranges, wd_chunk)
     int cs;                          // wide_l0_kernel cluster size: ks % cs == 0, the cs chunks of a
                                      // cluster sum their partials over DSMEM (PF0 holds ks / cs)
     const uint8_t *U0, *U1;          // gathered byte states s, s' [B][D]
