@@ -559,20 +559,63 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
     if (warp == 0) umma::tmem_free(tmem, 256);
 }
 
-// wide inputs on the fast path: H0[net][b][u] = ReLU(b0_net[u] + sum of the wide_l0_kernel
-// partials in chunk order) for the fast kernels above layer 0
+// wide inputs on the fast path: H0[net][b][u] = ReLU(b0_net[u] + (sum of the wide_l0_kernel
+// partials) / 255) for the fast kernels above layer 0.  A CTA takes 32 float4 groups of 4
+// consecutive elements; its 8 warps take the chunks q = w, w + 8, ... (all <= ks / 8 + 1 loads
+// of a thread in flight at once), and warp 0 adds the 8 residue sums in warp order: a fixed
+// summation order, one memory round trip per thread
+constexpr int WR_G = 32, WR_S = 8, WR_MAXQ = 10;   // groups per CTA, residues, ks <= 80
 __global__ void __launch_bounds__(256) wide_reduce_kernel(const float *__restrict__ PF0, int ks, int nets,
                                                           int B, int N0, const float *online,
                                                           const float *target, int64_t b0, float *H0)
 {
-    const int64_t per = (int64_t)B * N0, total = (int64_t)nets * per;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int net = (int)(i / per), u = (int)(i % N0);
-        float v = 0.0f;
-        for (int q = 0; q < ks; ++q) v += __ldcg(PF0 + (int64_t)q * total + i);
-        v = v / 255.0f + __ldg((net == 1 ? target : online) + b0 + u);
-        H0[i] = v > 0.0f ? v : 0.0f;
+    __shared__ float4 part[WR_S][WR_G];
+    const int64_t per = (int64_t)B * N0, total = (int64_t)nets * per, G = total / 4;   // N0 % 4 == 0
+    const int gl = threadIdx.x % WR_G, res = threadIdx.x / WR_G;
+    for (int64_t gb = (int64_t)blockIdx.x * WR_G; gb < G; gb += (int64_t)gridDim.x * WR_G) {
+        const int64_t g = gb + gl;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (g < G) {
+            const float4 *src = reinterpret_cast<const float4 *>(PF0) + g;
+            float4 pv[WR_MAXQ];
+#pragma unroll
+            for (int r = 0; r < WR_MAXQ; ++r) {
+                const int q = res + WR_S * r;
+                pv[r] = q < ks ? __ldcg(src + (int64_t)q * G) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int r = 0; r < WR_MAXQ; ++r) {
+                acc.x += pv[r].x;
+                acc.y += pv[r].y;
+                acc.z += pv[r].z;
+                acc.w += pv[r].w;
+            }
+        }
+        part[res][gl] = acc;
+        __syncthreads();
+        if (res == 0 && g < G) {
+            float4 t = part[0][gl];
+#pragma unroll
+            for (int w = 1; w < WR_S; ++w) {
+                const float4 o = part[w][gl];
+                t.x += o.x;
+                t.y += o.y;
+                t.z += o.z;
+                t.w += o.w;
+            }
+            const float a4[4] = {t.x, t.y, t.z, t.w};
+            float4 h;
+            float *hv = reinterpret_cast<float *>(&h);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int64_t i = 4 * g + r;
+                const int net = (int)(i / per), u = (int)(i % N0);
+                const float v = a4[r] / 255.0f + __ldg((net == 1 ? target : online) + b0 + u);
+                hv[r] = v > 0.0f ? v : 0.0f;
+            }
+            reinterpret_cast<float4 *>(H0)[g] = h;
+        }
+        __syncthreads();
     }
 }
 
