@@ -102,7 +102,7 @@ struct rpl_replay {
         size_t off, len;
         int ev;
     };
-    std::deque<Span> live;                 // spans the device may still read, oldest first
+    std::deque<Span> live;                 // spans the device may still read
     std::vector<cudaEvent_t> evs;          // event pool (index = Pending::slot)
     std::vector<int> free_evs;
     cudaStream_t copy_stream = nullptr;    // H2D copies of host adds (overlap the work stream)

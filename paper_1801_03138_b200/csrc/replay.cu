@@ -496,17 +496,21 @@ int replay_consumed(rpl_replay *rp, int slot, cudaStream_t st)
 }
 
 // the next staging span of `len` bytes (a multiple of 64): wraps to the arena start when the
-// tail is too short, and waits for the oldest live spans it would overwrite (their events were
-// all recorded: an add first flushes the previous deferred insert, which records its span's)
+// tail is too short, and waits for every live span it would overwrite (their events were all
+// recorded: an add first flushes the previous deferred insert, which records its span's).
+// Every live span is checked, not only the oldest: a span left near the arena's end by an
+// earlier wrap can be older than the ones the new span overlaps.
 static int stage_alloc(rpl_replay *rp, size_t len, size_t *off, int *ev)
 {
     if (rp->head + len > rp->arena) rp->head = 0;
-    while (!rp->live.empty()) {
-        const rpl_replay::Span &f = rp->live.front();
-        if (!(f.off < rp->head + len && rp->head < f.off + f.len)) break;   // oldest first
-        RPL_CUDA(cudaEventSynchronize(rp->evs[f.ev]));
-        rp->free_evs.push_back(f.ev);
-        rp->live.pop_front();
+    for (auto it = rp->live.begin(); it != rp->live.end();) {
+        if (it->off < rp->head + len && rp->head < it->off + it->len) {
+            RPL_CUDA(cudaEventSynchronize(rp->evs[it->ev]));
+            rp->free_evs.push_back(it->ev);
+            it = rp->live.erase(it);
+        } else {
+            ++it;
+        }
     }
     if (rp->free_evs.empty()) {
         cudaEvent_t e = nullptr;

@@ -184,3 +184,38 @@ def test_caller_provided_ring_storage(B):
         B.Replay(C, 27, storage=buf[: nbytes - 256])   # too small
     with pytest.raises(B.RplError):
         B.Replay(C, 27, storage=buf[1:])               # misaligned
+
+
+def test_staging_arena_wraps_with_many_adds_in_flight(B):
+    # host adds take spans of a staging arena of 2 x max_host_add experiences (a ring): ragged
+    # adds wrap it many times, with and without train steps consuming deferred (zero-copy)
+    # inserts in between; the ring must hold exactly the oracle's rows
+    import torch
+    C = 5000
+    rp = B.Replay(C, 27, seed=14, max_host_add=64)
+    orc = oracle.Ring(C, 27)
+    e = experiences(9000, seed=15)
+    rng = np.random.default_rng(16)
+    cfg = B.DQNConfig(max_batch=64)
+    dqn = None
+    t = 0
+    for it in range(300):
+        k = int(rng.integers(1, 65))
+        part = {kk: v[t:t + k] for kk, v in e.items()}
+        t += k
+        rp.add(**part)
+        orc.add(**part)
+        if it == 100:
+            from inputs import init_params
+            dqn = B.DQN(cfg, init_params(27, 8, (128,), True, 512, seed=17))
+        if dqn is not None and it % 3 == 0:
+            assert dqn.train_step(rp, 64) == B.RPL_OK
+            orc.events += 1   # the step consumed a sampler event
+    st = rp.state()
+    assert (st["cursor"], st["size"], st["total"]) == (orc.cursor, orc.size, orc.total)
+    idx = torch.arange(orc.size, dtype=torch.int32, device="cuda")
+    g = _np(rp.gather(idx))
+    o = orc.gather(np.arange(orc.size, dtype=np.int32))
+    for k in ("s", "s_next", "a", "r", "done"):
+        assert np.array_equal(g[k], o[k]), k
+    assert rp.check() == B.RPL_OK
