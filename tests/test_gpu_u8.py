@@ -92,3 +92,35 @@ def test_u8_wide_input_train_step(b, ddqn, path, monkeypatch):
         step_and_compare(b, cfg, dqn, rp, orc, batch, seed=11)
     assert np.array_equal(dqn.get_params(b.RPL_TARGET), dqn.get_params(b.RPL_ONLINE)) == (True)
     assert dqn.check() == b.RPL_OK
+
+
+def test_u8_host_adds_through_a_small_staging_arena(b):
+    # byte-state host adds are copied on the replay's copy stream into spans of a staging
+    # arena of 2 x max_host_add experiences; ragged adds wrap it many times, interleaved with
+    # wide train steps, and the ring must hold exactly the oracle's rows
+    import torch
+    D = 4096   # wide enough for the tcgen05 layer 0, small enough for a fast test
+    C = 300
+    rp = b.Replay(C, D, seed=21, state_dtype="u8", max_host_add=16)
+    orc = oracle.RingU8(C, D)
+    e = experiences_u8(900, state_dim=D, seed=22)
+    cfg = b.DQNConfig(state_dim=D, n_actions=8, dueling=True, hidden=(128,), stream=512,
+                      max_batch=32, sync_period=4)
+    dqn = b.DQN(cfg, init_params(D, 8, (128,), True, 512, seed=23))
+    rng = np.random.default_rng(24)
+    t = 0
+    for it in range(60):
+        k = int(rng.integers(1, 17))
+        part = {kk: v[t:t + k] for kk, v in e.items()}
+        t += k
+        rp.add(**part)
+        orc.add(**part)
+        if it >= 10 and it % 2 == 0:
+            assert dqn.train_step(rp, 32) == b.RPL_OK
+            orc.events += 1
+    idx = torch.arange(orc.size, dtype=torch.int32, device="cuda")
+    g = {k: v.cpu().numpy() for k, v in rp.gather(idx).items()}
+    o = orc.gather(np.arange(orc.size, dtype=np.int32))
+    for k in ("s", "s_next", "a", "r", "done"):
+        assert np.array_equal(g[k], o[k]), k
+    assert rp.check() == b.RPL_OK and dqn.check() == b.RPL_OK
