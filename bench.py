@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--precision", choices=["fp32", "tf32", "bf16"], default="fp32",
                     help="tensor-core products: fp32 (FP32-accurate splits, the default and the "
                          "judged line) or one tf32 / bf16 product (reduced precision, parity 2e-2)")
+    ap.add_argument("--dp", choices=["nccl", "p2p"], default="nccl",
+                    help="N > 1: gradient mean by ncclAllReduce (default) or by the peer-memory "
+                         "mean + SGD kernel (dqn_attach_peers, one node)")
     ap.add_argument("--ring", choices=["device", "host"], default="device",
                     help="host: the in-RAM comparison mode (SURVEY NEXT-1): ring rows in pinned host "
                          "memory, every batch read across PCIe by the same kernels")
@@ -280,7 +283,10 @@ def run_ours(a, batch, first_line=True):
                       device=local)
     if world > 1:
         from paper_1801_03138_b200 import dp
-        dp.attach(dqn)   # NCCL gradient all-reduce inside every dqn_train_step
+        if a.dp == "p2p":
+            dp.attach_peers(dqn)   # gradient mean + SGD over peer memory inside every step
+        else:
+            dp.attach(dqn)   # NCCL gradient all-reduce inside every dqn_train_step
 
     K, W, k = a.steps, a.warmup, a.adds_per_step
     npool = max(k, 1) * 256
@@ -501,7 +507,8 @@ def run_ours(a, batch, first_line=True):
                    "state_storage": "shared (s' = next slot's s, P:141)" if a.shared_state else "s and s' per row",
                    "ring_memory": "host (pinned, read across PCIe: in-RAM comparison)" if a.ring == "host" else "device (HBM)",
                    "parallelism": f"dp{world}" + (f", parameters averaged every {a.avg_period} steps"
-                                                  if a.avg_period and world > 1 else ""),
+                                                  if a.avg_period and world > 1 else "")
+                                  + (", gradient mean over peer memory" if a.dp == "p2p" and world > 1 else ""),
                    "l2": "inputs larger than L2: the 256 MB ring (> 126 MB L2) is sampled uniformly;"
                          " the 0.56 MB weights stay L2-resident as in steady-state training"},
         "samples_per_s": value * batch,
@@ -588,7 +595,10 @@ def run_c5(a):
     dqn = binding.DQN(cfg, init_params(C5_D, 8, (128,), True, 512, seed=3), device=local)
     if world > 1:
         from paper_1801_03138_b200 import dp
-        dp.attach(dqn)
+        if a.dp == "p2p":
+            dp.attach_peers(dqn)
+        else:
+            dp.attach(dqn)
     K, W, k = a.steps, a.warmup, a.adds_per_step
     loss_dev = torch.zeros(1, device=dev)
 

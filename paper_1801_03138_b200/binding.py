@@ -38,7 +38,8 @@ EXPORTS = [
     "dqn_param_count",
     "dqn_create", "dqn_destroy",
     "dqn_train_step", "sync_target", "dqn_get_params", "dqn_set_params", "dqn_step_count",
-    "dqn_debug_export", "rpl_nccl_unique_id", "dqn_attach_nccl", "rpl_check",
+    "dqn_debug_export", "rpl_nccl_unique_id", "dqn_attach_nccl", "dqn_peer_handle",
+    "dqn_attach_peers", "rpl_dp_emulate", "rpl_check",
     "rpl_last_error", "rpl_kernel_launches",
 ]
 
@@ -101,6 +102,9 @@ def _load():
         "dqn_debug_export": (C.c_int, [P, C.c_int, P, i64]),
         "rpl_nccl_unique_id": (C.c_int, [P]),
         "dqn_attach_nccl": (C.c_int, [P, i32, i32, P]),
+        "dqn_peer_handle": (C.c_int, [P, P]),
+        "dqn_attach_peers": (C.c_int, [P, i32, i32, P]),
+        "rpl_dp_emulate": (C.c_int, [i32, i64, P, P, P, P, P, P, C.c_float, u64]),
         "rpl_check": (C.c_int, [P, C.c_int]),
         "rpl_last_error": (C.c_char_p, []),
         "rpl_kernel_launches": (C.c_uint64, []),
@@ -420,6 +424,18 @@ class DQN:
     def attach_nccl(self, rank: int, world: int, uid: bytes):
         buf = C.create_string_buffer(bytes(uid), 128)
         _ok(_L.dqn_attach_nccl(self._h, rank, world, buf))
+
+    def peer_handle(self) -> bytes:
+        """dqn_peer_handle: this learner's 64-byte exchange-buffer IPC handle."""
+        buf = C.create_string_buffer(64)
+        _ok(_L.dqn_peer_handle(self._h, buf))
+        return buf.raw
+
+    def attach_peers(self, rank: int, world: int, handles: bytes):
+        """dqn_attach_peers: `handles` = every rank's peer_handle(), concatenated in rank order."""
+        assert len(handles) == 64 * world
+        buf = C.create_string_buffer(bytes(handles), 64 * world)
+        _ok(_L.dqn_attach_peers(self._h, rank, world, buf))
 
     def check(self) -> int:
         return _L.rpl_check(self._h, 1)

@@ -1,0 +1,113 @@
+// dp_peer.cuh -- data-parallel gradient mean + SGD over peer memory (P:144
+// "synchronized every train step").  CUDA path only.
+//
+// Every rank exports one exchange buffer (cudaIpc): two gradient slots [2][P + 1] (slot t % 2
+// holds step t's gradient, loss in word P) and a flag word.  After its step's gradient is
+// complete, rank r's dp_peer_sgd_kernel publishes flag_r = t (release, system scope), waits until
+// every rank's flag reaches t (acquire), then every CTA reads its slice of all ranks' gradients
+// straight from their memory over NVLink, forms the mean in rank order (identical arithmetic on
+// every rank: replicas stay bit-identical), applies SGD / the target copy and writes the mean
+// (the API's RPL_GRAD).  Reuse of a slot two steps later is safe: a rank only passes step
+// t + 1's flag wait once every rank has started step t + 1, i.e. finished reading step t - 1.
+//
+// The same kernel emulates `nloc` ranks in one cooperative launch on one device (rank groups
+// of blocks, all buffers local): the multi-rank protocol is testable without more GPUs.
+#pragma once
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace rpl {
+
+constexpr int DP_MAXR = 8;   // ranks of one node
+
+struct DPArgs {
+    int nloc, world, rank0;              // ranks run by this launch: rank0 .. rank0 + nloc - 1
+    int64_t P;                           // parameters (the gradient slot holds P + 1 words)
+    unsigned long long t;                // step number (> 0), parity selects the slot
+    float lr;
+    const float *xbuf[DP_MAXR];          // rank q's exchange buffer (peer-mapped or local)
+    unsigned long long *flag[DP_MAXR];   // rank q's flag word
+    float *online[DP_MAXR], *target[DP_MAXR], *gmean[DP_MAXR];   // per local rank
+    const int32_t *sync_flag[DP_MAXR];
+    uint32_t *err[DP_MAXR];
+};
+
+// exchange buffer: [2][P + 1] floats, then the flag word on its own 256-byte line
+__host__ __device__ inline size_t dp_flag_offset(int64_t P) { return ((size_t)2 * (P + 1) * sizeof(float) + 255) / 256 * 256; }
+__host__ __device__ inline size_t dp_xbuf_bytes(int64_t P) { return dp_flag_offset(P) + 256; }
+__host__ __device__ inline unsigned long long *dp_flag_of(const float *xbuf, int64_t P)
+{
+    return (unsigned long long *)((char *)xbuf + dp_flag_offset(P));
+}
+
+// host: make `dev` current for a scope
+struct DeviceGuardDqn {
+    int prev = -1;
+    explicit DeviceGuardDqn(int dev)
+    {
+        cudaGetDevice(&prev);
+        cudaSetDevice(dev);
+    }
+    ~DeviceGuardDqn()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+__device__ __forceinline__ unsigned long long dp_ld_acquire(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void dp_st_release(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(256) dp_peer_sgd_kernel(const __grid_constant__ DPArgs a)
+{
+    const int bpr = gridDim.x / a.nloc;
+    const int rl = blockIdx.x / bpr, bi = blockIdx.x % bpr;
+    if (rl >= a.nloc) return;
+    const int rank = a.rank0 + rl;
+    const int64_t slot = (int64_t)(a.t & 1ull) * (a.P + 1);
+    // (1) this rank's step-t gradient is complete (written before this kernel): publish it
+    if (bi == 0 && threadIdx.x == 0) {
+        __threadfence_system();
+        dp_st_release(a.flag[rank], a.t);
+    }
+    // (2) wait for every rank's
+    if (threadIdx.x == 0)
+        for (int q = 0; q < a.world; ++q)
+            while (dp_ld_acquire(a.flag[q]) < a.t) {
+            }
+    __syncthreads();
+    __threadfence();
+    // (3) the mean loss decides the update for every CTA alike
+    float ls = 0.0f;
+    for (int q = 0; q < a.world; ++q) ls += __ldcv(a.xbuf[q] + slot + a.P);
+    const float loss = ls / (float)a.world;
+    const bool ok = isfinite(loss);
+    const int do_sync = *a.sync_flag[rl];
+    float *on = a.online[rl], *tg = a.target[rl], *gm = a.gmean[rl];
+    // (4) mean of the ranks' gradients in rank order, SGD, target copy on sync steps
+    for (int64_t i = (int64_t)bi * blockDim.x + threadIdx.x; i < a.P; i += (int64_t)bpr * blockDim.x) {
+        float g = 0.0f;
+        for (int q = 0; q < a.world; ++q) g += __ldcv(a.xbuf[q] + slot + i);
+        g = g / (float)a.world;
+        gm[i] = g;
+        if (ok) {
+            const float w = on[i] - a.lr * g;
+            on[i] = w;
+            if (do_sync) tg[i] = w;
+        }
+    }
+    if (bi == 0 && threadIdx.x == 0) {
+        gm[a.P] = loss;
+        if (!ok) atomicOr(a.err[rl], ERRBIT_NUMERIC);
+    }
+}
+
+}  // namespace rpl

@@ -29,6 +29,7 @@
 #include "simt_gemm.cuh"
 #include "train_fast.cuh"
 #include "wide.cuh"
+#include "dp_peer.cuh"
 
 namespace rpl {
 
@@ -795,6 +796,12 @@ struct rpl_dqn {
     // data parallel
     void *comm = nullptr;
     int rank = 0, world = 1;
+    // peer-memory data parallelism (dqn_attach_peers, dp_peer.cuh): this rank's exchange buffer
+    // [2][P + 1] gradient slots + a flag word, and every rank's, mapped through cudaIpc
+    float *xbuf = nullptr;
+    bool p2p = false;
+    float *peer_xbuf[DP_MAXR] = {};
+    bool peer_opened[DP_MAXR] = {};
     std::vector<void *> allocs;
 };
 
@@ -937,6 +944,9 @@ extern "C" int dqn_destroy(rpl_dqn *d)
     cudaSetDevice(d->device);
     cudaStreamSynchronize(d->stream);
     if (d->comm && g_nccl.destroy) g_nccl.destroy(d->comm);
+    for (int q = 0; q < DP_MAXR; ++q)
+        if (d->peer_opened[q]) cudaIpcCloseMemHandle(d->peer_xbuf[q]);
+    if (d->xbuf) cudaFree(d->xbuf);
     for (auto &g : d->graphs) {
         cudaGraphExecDestroy(g.exec);
         cudaGraphDestroy(g.graph);
@@ -1563,7 +1573,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
     const int do_sync = d->cfg.sync_period > 0 && t % d->cfg.sync_period == 0;
     // data parallel: per-step gradient mean (dp), or local SGD + periodic parameter mean (avg)
     const bool avg = d->comm != nullptr && d->cfg.avg_period > 0;
-    const bool dp = d->comm != nullptr && !avg;
+    const bool dp = (d->comm != nullptr || d->p2p) && !avg;
     cudaError_t e = cudaSuccess;
     // a deferred insert is consumed by the fast path's K1 on the shared stream; otherwise it
     // is written now by the insert kernel
@@ -1801,7 +1811,38 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
         }
     }
 after_step:
-    if (dp) {
+    if (dp && d->p2p) {
+        // gradient mean + SGD over peer memory (dp_peer.cuh): this step's gradient into its
+        // exchange slot, then one kernel publishes it, waits for every rank's and updates
+        float *mine = d->xbuf + (int64_t)(t & 1) * (d->P + 1);
+        e = cudaMemcpyAsync(mine, d->grad, (size_t)(d->P + 1) * sizeof(float), cudaMemcpyDeviceToDevice, d->stream);
+        DPArgs a{};
+        a.nloc = 1;
+        a.world = d->world;
+        a.rank0 = d->rank;
+        a.P = d->P;
+        a.t = (unsigned long long)t;
+        a.lr = d->cfg.lr;
+        for (int q = 0; q < d->world; ++q) {
+            a.xbuf[q] = d->peer_xbuf[q];
+            a.flag[q] = dp_flag_of(d->peer_xbuf[q], d->P);
+        }
+        a.online[0] = d->online;
+        a.target[0] = d->target;
+        a.gmean[0] = d->grad;
+        a.sync_flag[0] = d->sync_flag;
+        a.err[0] = d->err;
+        if (e == cudaSuccess) {
+            dp_peer_sgd_kernel<<<(unsigned)d->sms, 256, 0, d->stream>>>(a);
+            e = cudaGetLastError();
+        }
+        if (e != cudaSuccess) {
+            if (prev >= 0) cudaSetDevice(prev);
+            return cuda_fail(e, "dp_peer_sgd_kernel");
+        }
+        g_launches.fetch_add(1);
+        if (loss_dev) cudaMemcpyAsync(loss_dev, d->grad + d->P, sizeof(float), cudaMemcpyDeviceToDevice, d->stream);
+    } else if (dp) {
         int nr = g_nccl.allreduce(d->grad, d->grad, (size_t)d->P + 1, kNcclFloat, kNcclAvg,
                                   d->comm, d->stream);
         if (nr != 0) {
@@ -1984,6 +2025,87 @@ extern "C" int dqn_attach_nccl(rpl_dqn *d, int32_t rank, int32_t world, const vo
     }
     d->rank = rank;
     d->world = world;
+    return RPL_OK;
+}
+
+// ---- peer-memory data parallelism (dp_peer.cuh) ----------------------------------------------
+extern "C" int dqn_peer_handle(rpl_dqn *d, void *handle_out)
+{
+    if (!d || !handle_out) return RPL_EINVAL;
+    DeviceGuardDqn g(d->device);
+    if (!d->xbuf) {
+        const size_t bytes = dp_xbuf_bytes(d->P);
+        RPL_CUDA(cudaMalloc((void **)&d->xbuf, bytes));
+        RPL_CUDA(cudaMemset(d->xbuf, 0, bytes));
+    }
+    cudaIpcMemHandle_t h;
+    RPL_CUDA(cudaIpcGetMemHandle(&h, d->xbuf));
+    memcpy(handle_out, &h, sizeof h);
+    return RPL_OK;
+}
+
+extern "C" int dqn_attach_peers(rpl_dqn *d, int32_t rank, int32_t world, const void *handles)
+{
+    if (!d || !handles || world < 1 || world > DP_MAXR || rank < 0 || rank >= world) return RPL_EINVAL;
+    if (d->comm || d->p2p || !d->xbuf || d->cfg.avg_period > 0) {
+        set_error("dqn_attach_peers: needs dqn_peer_handle first, no NCCL attach, avg_period 0");
+        return RPL_ESTATE;
+    }
+    DeviceGuardDqn g(d->device);
+    const cudaIpcMemHandle_t *hs = static_cast<const cudaIpcMemHandle_t *>(handles);
+    for (int q = 0; q < world; ++q) {
+        if (q == rank) {
+            d->peer_xbuf[q] = d->xbuf;
+            continue;
+        }
+        void *ptr = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&ptr, hs[q], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            for (int r = 0; r < q; ++r)
+                if (d->peer_opened[r]) {
+                    cudaIpcCloseMemHandle(d->peer_xbuf[r]);
+                    d->peer_opened[r] = false;
+                }
+            return cuda_fail(e, "cudaIpcOpenMemHandle");
+        }
+        d->peer_xbuf[q] = (float *)ptr;
+        d->peer_opened[q] = true;
+    }
+    d->rank = rank;
+    d->world = world;
+    d->p2p = true;
+    return RPL_OK;
+}
+
+// test entry: `world` ranks emulated by one cooperative launch on this device (dp_peer.cuh)
+extern "C" int rpl_dp_emulate(int32_t world, int64_t P, float *xbufs, float *online, float *target,
+                              float *gmean, const int32_t *sync_flag, uint32_t *err, float lr,
+                              uint64_t t)
+{
+    if (world < 1 || world > DP_MAXR || P < 1 || !xbufs || !online || !target || !gmean ||
+        !sync_flag || !err || t == 0)
+        return RPL_EINVAL;
+    const size_t stride = dp_xbuf_bytes(P) / sizeof(float);
+    DPArgs a{};
+    a.nloc = world;
+    a.world = world;
+    a.rank0 = 0;
+    a.P = P;
+    a.t = t;
+    a.lr = lr;
+    for (int q = 0; q < world; ++q) {
+        a.xbuf[q] = xbufs + q * stride;
+        a.flag[q] = dp_flag_of(xbufs + q * stride, P);
+        a.online[q] = online + q * P;
+        a.target[q] = target + q * P;
+        a.gmean[q] = gmean + q * (P + 1);
+        a.sync_flag[q] = sync_flag;
+        a.err[q] = err;
+    }
+    const int bpr = 8;
+    void *args[] = {&a};
+    RPL_CUDA(cudaLaunchCooperativeKernel((const void *)dp_peer_sgd_kernel, dim3(world * bpr), dim3(256), args, 0, nullptr));
+    RPL_CUDA(cudaDeviceSynchronize());
     return RPL_OK;
 }
 

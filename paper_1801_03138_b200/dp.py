@@ -35,6 +35,25 @@ def attach(dqn) -> None:
     dqn.attach_nccl(rank, world, broadcast_bytes(uid, 0))
 
 
+def gather_bytes(payload: bytes, nbytes: int = 64) -> bytes:
+    """All-gather `nbytes` from every rank over the default process group; the result is the
+    ranks' payloads concatenated in rank order."""
+    backend = dist.get_backend()
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    assert len(payload) == nbytes
+    mine = torch.frombuffer(bytearray(payload), dtype=torch.uint8).to(dev)
+    out = [torch.zeros(nbytes, dtype=torch.uint8, device=dev) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, mine)
+    return b"".join(bytes(t.cpu().numpy().tobytes()) for t in out)
+
+
+def attach_peers(dqn) -> None:
+    """Attach a learner to its node's peers through peer memory (dqn_attach_peers): the
+    gradient mean and SGD then run in one kernel reading every rank's gradient over NVLink."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dqn.attach_peers(rank, world, gather_bytes(dqn.peer_handle(), 64))
+
+
 def shard_seed(base: int, rank: int) -> tuple[int, int]:
     """(data seed, sampler rank) of a learner: every rank draws its own experience stream and
     its own Philox sampler stream (the rank goes into counter word 3, Q3)."""

@@ -160,3 +160,31 @@ def test_world2_periodic_parameter_averaging():
         local.append(w)
     assert not np.array_equal(local[0], local[1])
     np.testing.assert_array_equal(res[0][0][AVG_K - 1], (local[0] + local[1]) / np.float32(2))
+
+
+def _gather_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1801_03138_b200 import dp
+    payload = bytes([rank * 16 + i % 16 for i in range(64)])
+    q.put((rank, dp.gather_bytes(payload, 64)))
+    dist.destroy_process_group()
+
+
+def test_world2_peer_handle_allgather():
+    # dqn_attach_peers' handle exchange: every rank receives all ranks' 64-byte handles,
+    # concatenated in rank order
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29000 + (os.getpid() % 1000)
+    ps = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    want = bytes([i % 16 for i in range(64)]) + bytes([16 + i % 16 for i in range(64)])
+    assert out[0] == want and out[1] == want

@@ -1,0 +1,118 @@
+"""Peer-memory data parallelism (dp_peer.cuh, dqn_attach_peers): the gradient mean + SGD in one
+kernel that reads every rank's gradient from its memory (P:144 per-step sync).
+
+* `rpl_dp_emulate` runs the kernel for 1 / 2 / 4 / 8 ranks emulated by one cooperative launch on
+  this GPU (the publish / wait / read protocol over rank-separate buffers, as the profiling
+  recipe prescribes for more ranks than GPUs): every rank's parameters equal the rank-order
+  mean-gradient SGD computed here in float32, the ranks stay bit-identical, the two exchange
+  slots alternate with the step parity, and a non-finite mean loss skips the update.
+* A learner attached to itself (world 1, a real cudaIpc handle) trains bit-identically to an
+  unattached one.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from inputs import experiences, init_params
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def b():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_1801_03138_b200.binding as binding
+    return binding
+
+
+def _xbuf_floats(P):
+    flag_off = ((2 * (P + 1) * 4 + 255) // 256) * 256
+    return (flag_off + 256) // 4, flag_off // 4
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_emulated_ranks_mean_sgd(b, world):
+    import torch
+    P, lr = 5003, np.float32(0.01)
+    stride, flag_at = _xbuf_floats(P)
+    rng = np.random.default_rng(world)
+    xb = torch.zeros(world * stride, dtype=torch.float32, device="cuda")
+    w0 = rng.standard_normal(P).astype(np.float32)
+    online = torch.from_numpy(np.tile(w0, world)).cuda()
+    target = torch.from_numpy(np.tile(w0, world)).cuda()
+    gmean = torch.zeros(world * (P + 1), dtype=torch.float32, device="cuda")
+    sync = torch.zeros(1, dtype=torch.int32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    w_ref = w0.copy()
+    for t in (1, 2, 3):
+        slot = (t & 1) * (P + 1)
+        grads = rng.standard_normal((world, P + 1)).astype(np.float32)
+        for q in range(world):
+            xb[q * stride + slot:q * stride + slot + P + 1] = torch.from_numpy(grads[q]).cuda()
+        sync.fill_(1 if t == 3 else 0)
+        st = b._L.rpl_dp_emulate(world, P, xb.data_ptr(), online.data_ptr(), target.data_ptr(),
+                                 gmean.data_ptr(), sync.data_ptr(), err.data_ptr(), C.c_float(lr), t)
+        assert st == b.RPL_OK, b.last_error()
+        # flags hold the step number
+        fl = xb.view(torch.int64)
+        for q in range(world):
+            assert fl[(q * stride + flag_at) // 2].item() == t
+        acc = grads[0].copy()
+        for q in range(1, world):
+            acc = (acc + grads[q]).astype(np.float32)
+        g = (acc / np.float32(world)).astype(np.float32)
+        on = online.view(world, P).cpu().numpy()
+        gm = gmean.view(world, P + 1).cpu().numpy()
+        for q in range(world):   # replicas bit-identical
+            assert np.array_equal(on[q], on[0]) and np.array_equal(gm[q], gm[0])
+        assert np.array_equal(gm[0], g)   # the mean, in rank order, exactly
+        w_ref = (w_ref - lr * g[:P]).astype(np.float32)
+        assert np.max(np.abs(on[0] - w_ref)) <= 1e-6 * max(1.0, np.max(np.abs(w_ref)))
+        w_ref = on[0].copy()
+    tg = target.view(world, P).cpu().numpy()
+    assert np.array_equal(tg[0], on[0])   # t = 3 was a sync step
+    assert err.item() == 0
+    # a non-finite mean loss skips the update and raises the sticky numeric bit
+    t = 4
+    slot = (t & 1) * (P + 1)
+    bad = rng.standard_normal((world, P + 1)).astype(np.float32)
+    bad[world - 1, P] = np.nan
+    for q in range(world):
+        xb[q * stride + slot:q * stride + slot + P + 1] = torch.from_numpy(bad[q]).cuda()
+    before = online.clone()
+    assert b._L.rpl_dp_emulate(world, P, xb.data_ptr(), online.data_ptr(), target.data_ptr(),
+                               gmean.data_ptr(), sync.data_ptr(), err.data_ptr(), C.c_float(lr), t) == b.RPL_OK
+    assert torch.equal(online, before) and err.item() == 2
+
+
+@pytest.mark.parametrize("net", ["fast", "generic"])
+def test_self_attached_learner_equals_local(b, monkeypatch, net):
+    import torch
+    if net == "generic":
+        monkeypatch.setenv("RPL_PATH", "generic")
+    cfg = b.DQNConfig(max_batch=128, sync_period=4, double_dqn=True, lr=1e-3)
+    p0 = init_params(27, 8, (128,), True, 512, seed=3)
+    e = experiences(2000, seed=1)
+    runs = []
+    for attach in (False, True):
+        rp = b.Replay(2000, 27, seed=4)
+        rp.add_many(e)
+        dqn = b.DQN(cfg, p0)
+        if attach:
+            h = dqn.peer_handle()
+            assert len(h) == 64
+            dqn.attach_peers(0, 1, h)
+        loss = torch.zeros(1, device="cuda")
+        for _ in range(7):
+            assert dqn.train_step(rp, 128, loss) == b.RPL_OK
+        torch.cuda.synchronize()
+        assert dqn.check() == b.RPL_OK and np.isfinite(loss.item())
+        runs.append((dqn.get_params(b.RPL_ONLINE), dqn.get_params(b.RPL_TARGET), loss.item(),
+                     dqn.get_params(b.RPL_GRAD)))
+    assert np.array_equal(runs[0][0], runs[1][0])
+    assert np.array_equal(runs[0][1], runs[1][1])
+    assert runs[0][2] == runs[1][2]
+    assert np.array_equal(runs[0][3], runs[1][3])
