@@ -1841,6 +1841,7 @@ after_step:
             return cuda_fail(e, "dp_peer_sgd_kernel");
         }
         g_launches.fetch_add(1);
+        d->w0bf_stale = true;   // the update rewrote W0 without its planes
         if (loss_dev) cudaMemcpyAsync(loss_dev, d->grad + d->P, sizeof(float), cudaMemcpyDeviceToDevice, d->stream);
     } else if (dp) {
         int nr = g_nccl.allreduce(d->grad, d->grad, (size_t)d->P + 1, kNcclFloat, kNcclAvg,

@@ -116,3 +116,27 @@ def test_self_attached_learner_equals_local(b, monkeypatch, net):
     assert np.array_equal(runs[0][1], runs[1][1])
     assert runs[0][2] == runs[1][2]
     assert np.array_equal(runs[0][3], runs[1][3])
+
+
+def test_self_attached_wide_learner_equals_local(b):
+    # config-5 network (tcgen05 layer 0): the peer-memory update also rewrites W0, whose bf16
+    # planes must be re-split before the next forward
+    import torch
+    D = 84 * 84 * 4
+    cfg = b.DQNConfig(state_dim=D, n_actions=8, dueling=True, hidden=(128,), stream=512,
+                      max_batch=32, sync_period=3, lr=1e-3)
+    from inputs import experiences_u8
+    p0 = init_params(D, 8, (128,), True, 512, seed=13)
+    e = experiences_u8(64, state_dim=D, seed=12)
+    runs = []
+    for attach in (False, True):
+        rp = b.Replay(64, D, seed=11, state_dtype="u8")
+        rp.add(**e)
+        dqn = b.DQN(cfg, p0)
+        if attach:
+            dqn.attach_peers(0, 1, dqn.peer_handle())
+        for _ in range(4):
+            assert dqn.train_step(rp, 32) == b.RPL_OK
+        assert dqn.check() == b.RPL_OK
+        runs.append(dqn.get_params(b.RPL_ONLINE))
+    assert np.array_equal(runs[0], runs[1])
