@@ -58,9 +58,10 @@ def parse():
     ap.add_argument("--precision", choices=["fp32", "tf32", "bf16"], default="fp32",
                     help="tensor-core products: fp32 (FP32-accurate splits, the default and the "
                          "judged line) or one tf32 / bf16 product (reduced precision, parity 2e-2)")
-    ap.add_argument("--dp", choices=["nccl", "p2p"], default="nccl",
-                    help="N > 1: gradient mean by ncclAllReduce (default) or by the peer-memory "
-                         "mean + SGD kernel (dqn_attach_peers, one node)")
+    ap.add_argument("--dp", choices=["auto", "nccl", "p2p"], default="auto",
+                    help="N > 1: gradient mean by the peer-memory mean + SGD kernel "
+                         "(dqn_attach_peers) when every rank's GPU can map every other's (auto, "
+                         "the default), or by ncclAllReduce")
     ap.add_argument("--ring", choices=["device", "host"], default="device",
                     help="host: the in-RAM comparison mode (SURVEY NEXT-1): ring rows in pinned host "
                          "memory, every batch read across PCIe by the same kernels")
@@ -283,10 +284,17 @@ def run_ours(a, batch, first_line=True):
                       device=local)
     if world > 1:
         from paper_1801_03138_b200 import dp
-        if a.dp == "p2p":
+        if a.avg_period:
+            dp.attach(dqn)   # parameter averaging runs on NCCL
+            a.dp_used = "nccl"
+        elif a.dp == "auto":
+            a.dp_used = dp.attach_auto(dqn)   # peer memory if possible, else NCCL
+        elif a.dp == "p2p":
             dp.attach_peers(dqn)   # gradient mean + SGD over peer memory inside every step
+            a.dp_used = "p2p"
         else:
             dp.attach(dqn)   # NCCL gradient all-reduce inside every dqn_train_step
+            a.dp_used = "nccl"
 
     K, W, k = a.steps, a.warmup, a.adds_per_step
     npool = max(k, 1) * 256
@@ -508,7 +516,8 @@ def run_ours(a, batch, first_line=True):
                    "ring_memory": "host (pinned, read across PCIe: in-RAM comparison)" if a.ring == "host" else "device (HBM)",
                    "parallelism": f"dp{world}" + (f", parameters averaged every {a.avg_period} steps"
                                                   if a.avg_period and world > 1 else "")
-                                  + (", gradient mean over peer memory" if a.dp == "p2p" and world > 1 else ""),
+                                  + (", gradient mean over peer memory" if getattr(a, "dp_used", "") == "p2p"
+                                     else ", NCCL gradient all-reduce" if world > 1 and not a.avg_period else ""),
                    "l2": "inputs larger than L2: the 256 MB ring (> 126 MB L2) is sampled uniformly;"
                          " the 0.56 MB weights stay L2-resident as in steady-state training"},
         "samples_per_s": value * batch,
@@ -595,10 +604,14 @@ def run_c5(a):
     dqn = binding.DQN(cfg, init_params(C5_D, 8, (128,), True, 512, seed=3), device=local)
     if world > 1:
         from paper_1801_03138_b200 import dp
-        if a.dp == "p2p":
+        if a.dp == "auto":
+            a.dp_used = dp.attach_auto(dqn)
+        elif a.dp == "p2p":
             dp.attach_peers(dqn)
+            a.dp_used = "p2p"
         else:
             dp.attach(dqn)
+            a.dp_used = "nccl"
     K, W, k = a.steps, a.warmup, a.adds_per_step
     loss_dev = torch.zeros(1, device=dev)
 
@@ -746,7 +759,9 @@ def run_c5(a):
                                f"{'Double-DQN' if a.ddqn else 'DQN'} target, Huber, SGD, {k} "
                                "inserts/step",
                    "batch": batch, "capacity": a.capacity, "double_dqn": a.ddqn,
-                   "adds_per_step": k, "parallelism": f"dp{world}",
+                   "adds_per_step": k, "parallelism": f"dp{world}" + (
+                       ", gradient mean over peer memory" if getattr(a, "dp_used", "") == "p2p"
+                       else ", NCCL gradient all-reduce" if world > 1 else ""),
                    "l2": "inputs larger than L2 (the byte ring is sampled uniformly)"},
         "samples_per_s": value * batch, "gpu_launches": launches, "roofline": roofline,
         "cpu_baseline": cpu, "e2e": e2e, "gather": gather, "clocks": clk.summary(),

@@ -304,6 +304,10 @@ int dqn_attach_nccl(rpl_dqn *dqn, int32_t rank, int32_t world, const void *id128
  * NCCL attached, or avg_period > 0), ECUDA (IPC mapping). */
 int dqn_peer_handle(rpl_dqn *dqn, void *handle_out);
 int dqn_attach_peers(rpl_dqn *dqn, int32_t rank, int32_t world, const void *handles);
+/* Undo dqn_attach_peers (synchronises; the exchange buffer stays for a later attach).  A rank
+ * whose peer did not arrive within ~10 s skips that step's update and reports RPL_ENCCL at the
+ * next synchronising call instead of hanging. */
+int dqn_detach_peers(rpl_dqn *dqn);
 
 /* Test entry: the peer-memory gradient mean + SGD for `world` ranks emulated by one
  * cooperative launch on the current device (all buffers device memory on it): xbufs[world]

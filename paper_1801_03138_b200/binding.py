@@ -39,7 +39,7 @@ EXPORTS = [
     "dqn_create", "dqn_destroy",
     "dqn_train_step", "sync_target", "dqn_get_params", "dqn_set_params", "dqn_step_count",
     "dqn_debug_export", "rpl_nccl_unique_id", "dqn_attach_nccl", "dqn_peer_handle",
-    "dqn_attach_peers", "rpl_dp_emulate", "rpl_check",
+    "dqn_attach_peers", "dqn_detach_peers", "rpl_dp_emulate", "rpl_check",
     "rpl_last_error", "rpl_kernel_launches",
 ]
 
@@ -104,6 +104,7 @@ def _load():
         "dqn_attach_nccl": (C.c_int, [P, i32, i32, P]),
         "dqn_peer_handle": (C.c_int, [P, P]),
         "dqn_attach_peers": (C.c_int, [P, i32, i32, P]),
+        "dqn_detach_peers": (C.c_int, [P]),
         "rpl_dp_emulate": (C.c_int, [i32, i64, P, P, P, P, P, P, C.c_float, u64]),
         "rpl_check": (C.c_int, [P, C.c_int]),
         "rpl_last_error": (C.c_char_p, []),
@@ -436,6 +437,9 @@ class DQN:
         assert len(handles) == 64 * world
         buf = C.create_string_buffer(bytes(handles), 64 * world)
         _ok(_L.dqn_attach_peers(self._h, rank, world, buf))
+
+    def detach_peers(self):
+        _ok(_L.dqn_detach_peers(self._h))
 
     def check(self) -> int:
         return _L.rpl_check(self._h, 1)

@@ -78,12 +78,23 @@ __global__ void __launch_bounds__(256) dp_peer_sgd_kernel(const __grid_constant_
         __threadfence_system();
         dp_st_release(a.flag[rank], a.t);
     }
-    // (2) wait for every rank's
-    if (threadIdx.x == 0)
-        for (int q = 0; q < a.world; ++q)
+    // (2) wait for every rank's; a rank that never arrives (a broken lockstep) ends the wait
+    // after ~10 s with the sticky ERRBIT_PEER and the update skipped, instead of a hang
+    __shared__ int timed_out;
+    if (threadIdx.x == 0) {
+        timed_out = 0;
+        const long long t0 = clock64();
+        for (int q = 0; q < a.world && !timed_out; ++q)
             while (dp_ld_acquire(a.flag[q]) < a.t) {
+                if (clock64() - t0 > 20000000000ll) {
+                    timed_out = 1;
+                    atomicOr(a.err[rl], ERRBIT_PEER);
+                    break;
+                }
             }
+    }
     __syncthreads();
+    if (timed_out) return;
     __threadfence();
     // (3) the mean loss decides the update for every CTA alike
     float ls = 0.0f;

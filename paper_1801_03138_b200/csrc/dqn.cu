@@ -2078,6 +2078,24 @@ extern "C" int dqn_attach_peers(rpl_dqn *d, int32_t rank, int32_t world, const v
     return RPL_OK;
 }
 
+extern "C" int dqn_detach_peers(rpl_dqn *d)
+{
+    if (!d) return RPL_EINVAL;
+    DeviceGuardDqn g(d->device);
+    cudaStreamSynchronize(d->stream);
+    for (int q = 0; q < DP_MAXR; ++q) {
+        if (d->peer_opened[q]) cudaIpcCloseMemHandle(d->peer_xbuf[q]);
+        d->peer_opened[q] = false;
+        d->peer_xbuf[q] = nullptr;
+    }
+    if (d->p2p) {
+        d->p2p = false;
+        d->rank = 0;
+        d->world = 1;
+    }
+    return RPL_OK;
+}
+
 // test entry: `world` ranks emulated by one cooperative launch on this device (dp_peer.cuh)
 extern "C" int rpl_dp_emulate(int32_t world, int64_t P, float *xbufs, float *online, float *target,
                               float *gmean, const int32_t *sync_flag, uint32_t *err, float lr,
@@ -2134,5 +2152,9 @@ extern "C" int rpl_check(void *handle, int kind)
     }
     if (h & ERRBIT_NUMERIC) { set_error("non-finite loss: update skipped"); return RPL_ENUMERIC; }
     if (h & ERRBIT_RANGE) { set_error("gather index out of range (clamped)"); return RPL_EINVAL; }
+    if (h & ERRBIT_PEER) {
+        set_error("peer-memory data parallelism: a rank did not publish its gradient (update skipped)");
+        return RPL_ENCCL;
+    }
     return RPL_OK;
 }

@@ -36,7 +36,7 @@ extern std::atomic<uint64_t> g_launches;            // kernels launched by this 
     } while (0)
 
 // sticky device-side error bits (written by kernels with atomicOr)
-enum : uint32_t { ERRBIT_CORRUPT = 1u, ERRBIT_NUMERIC = 2u, ERRBIT_RANGE = 4u };
+enum : uint32_t { ERRBIT_CORRUPT = 1u, ERRBIT_NUMERIC = 2u, ERRBIT_RANGE = 4u, ERRBIT_PEER = 8u };
 
 // Philox counter word 3 = (TAG << 24) | rank  (reading Q3)
 constexpr uint32_t TAG_SAMPLE = 1u;

@@ -54,6 +54,42 @@ def attach_peers(dqn) -> None:
     dqn.attach_peers(rank, world, gather_bytes(dqn.peer_handle(), 64))
 
 
+def attach_auto(dqn, peer_ok: bool | None = None) -> str:
+    """Peer memory when every rank can map every other rank's buffer (one node, peer access
+    between all the ranks' GPUs), else NCCL; every rank takes the same choice.  Returns
+    "p2p" or "nccl".  (peer_ok overrides the peer-access probe; tests.)"""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if world == 1:
+        return "none"
+    ok = world <= 8 if peer_ok is None else peer_ok
+    if ok and peer_ok is None:
+        dev = torch.cuda.current_device()
+        n = torch.cuda.device_count()
+        ok = n >= world and all(torch.cuda.can_device_access_peer(dev, o) for o in range(world) if o != dev)
+    agree = _all_min(1 if ok else 0)
+    attached = False
+    if agree:
+        try:
+            attach_peers(dqn)
+            attached = True
+        except Exception:
+            attached = False
+    if _all_min(1 if attached else 0):
+        return "p2p"
+    if attached:
+        dqn.detach_peers()
+    attach(dqn)
+    return "nccl"
+
+
+def _all_min(v: int) -> int:
+    backend = dist.get_backend()
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    t = torch.tensor([v], dtype=torch.int32, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return int(t.item())
+
+
 def shard_seed(base: int, rank: int) -> tuple[int, int]:
     """(data seed, sampler rank) of a learner: every rank draws its own experience stream and
     its own Philox sampler stream (the rank goes into counter word 3, Q3)."""

@@ -188,3 +188,57 @@ def test_world2_peer_handle_allgather():
         p.join(timeout=60)
     want = bytes([i % 16 for i in range(64)]) + bytes([16 + i % 16 for i in range(64)])
     assert out[0] == want and out[1] == want
+
+
+class _MockLearner:
+    def __init__(self, rank, fail):
+        self.rank, self.fail, self.calls = rank, fail, []
+
+    def peer_handle(self):
+        return bytes([self.rank]) * 64
+
+    def attach_peers(self, rank, world, handles):
+        self.calls.append(("attach_peers", handles))
+        if self.fail:
+            raise RuntimeError("IPC mapping failed")
+
+    def detach_peers(self):
+        self.calls.append(("detach_peers",))
+
+
+def _auto_worker(rank, world, port, fail_rank, peer_ok, q):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1801_03138_b200 import dp
+    m = _MockLearner(rank, rank == fail_rank)
+    dp.attach = lambda dqn: dqn.calls.append(("nccl",))   # no NCCL on this CPU box
+    q.put((rank, dp.attach_auto(m, peer_ok=peer_ok), [c[0] for c in m.calls]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank,peer_ok,want", [(-1, True, "p2p"), (1, True, "nccl"), (-1, False, "nccl")])
+def test_world2_attach_auto_agrees(fail_rank, peer_ok, want):
+    # every rank takes the same data-parallel path: peer memory only when all ranks can map all
+    # peers; one failed mapping sends everyone (the mapped ranks detaching first) to NCCL
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + (os.getpid() % 400) + 3 * (fail_rank + 1) + (0 if peer_ok else 1)
+    ps = [ctx.Process(target=_auto_worker, args=(r, 2, port, fail_rank, peer_ok, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, path, calls = q.get(timeout=120)
+        res[r] = (path, calls)
+    for p in ps:
+        p.join(timeout=60)
+    assert res[0][0] == res[1][0] == want
+    if want == "p2p":
+        assert res[0][1] == res[1][1] == ["attach_peers"]
+    elif peer_ok:
+        assert res[0][1] == ["attach_peers", "detach_peers", "nccl"] and res[1][1] == ["attach_peers", "nccl"]
+    else:
+        assert res[0][1] == res[1][1] == ["nccl"]
