@@ -79,19 +79,22 @@ __global__ void __launch_bounds__(256) dp_peer_sgd_kernel(const __grid_constant_
         dp_st_release(a.flag[rank], a.t);
     }
     // (2) wait for every rank's; a rank that never arrives (a broken lockstep) ends the wait
-    // after ~10 s with the sticky ERRBIT_PEER and the update skipped, instead of a hang
+    // after ~10 s with the sticky ERRBIT_PEER and the update skipped, and marks this rank's
+    // exchange broken so every later step skips at once (fail fast instead of a hang)
     __shared__ int timed_out;
+    unsigned *broken = reinterpret_cast<unsigned *>(a.flag[rank] + 8);
     if (threadIdx.x == 0) {
-        timed_out = 0;
+        timed_out = *reinterpret_cast<volatile unsigned *>(broken) != 0;
         const long long t0 = clock64();
         for (int q = 0; q < a.world && !timed_out; ++q)
             while (dp_ld_acquire(a.flag[q]) < a.t) {
                 if (clock64() - t0 > 20000000000ll) {
                     timed_out = 1;
-                    atomicOr(a.err[rl], ERRBIT_PEER);
+                    atomicExch(broken, 1u);
                     break;
                 }
             }
+        if (timed_out) atomicOr(a.err[rl], ERRBIT_PEER);
     }
     __syncthreads();
     if (timed_out) return;
