@@ -140,3 +140,40 @@ def test_self_attached_wide_learner_equals_local(b):
         assert dqn.check() == b.RPL_OK
         runs.append(dqn.get_params(b.RPL_ONLINE))
     assert np.array_equal(runs[0], runs[1])
+
+
+def _ipc_worker(rank, world, port, q):
+    # attach only: two processes on one GPU map each other's exchange buffers through cudaIpc
+    # (no train step: kernels that wait on one another must not share a GPU)
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1801_03138_b200.binding as b
+    from paper_1801_03138_b200 import dp
+    dqn = b.DQN(b.DQNConfig(max_batch=32), init_params(27, 8, (128,), True, 512, seed=3))
+    try:
+        dp.attach_peers(dqn)
+        dqn.detach_peers()
+        dp.attach_peers(dqn)   # re-attach after a detach
+        q.put((rank, "ok"))
+    except Exception as ex:   # reported to the parent
+        q.put((rank, repr(ex)))
+    dqn.detach_peers()
+    dist.destroy_process_group()
+
+
+def test_two_processes_map_each_others_exchange_buffers(b):
+    import multiprocessing as mp
+    import os
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 28000 + os.getpid() % 900
+    ps = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res
