@@ -299,7 +299,9 @@ int dqn_attach_nccl(rpl_dqn *dqn, int32_t rank, int32_t world, const void *id128
  * cudaIpcMemHandle to handle_out; after every rank has its peers' handles (e.g. all-gathered
  * with torch.distributed), dqn_attach_peers(rank, world, handles[world * 64 bytes]) maps them.
  * From then on dqn_train_step publishes its gradient, waits for every rank's (device-side
- * flags), averages them in rank order (replicas stay bit-identical) and updates.  Every rank
+ * flags), averages them in rank order (replicas stay bit-identical) and updates; gradients
+ * longer than 2^20 words are averaged reduce-scatter style (each rank averages 1/world of
+ * them and stores that slice into every rank's mean buffer) before the update.  Every rank
  * must call dqn_train_step the same number of times.  Errors: EINVAL, ESTATE (no handle yet,
  * NCCL attached, or avg_period > 0), ECUDA (IPC mapping). */
 int dqn_peer_handle(rpl_dqn *dqn, void *handle_out);
@@ -312,10 +314,12 @@ int dqn_detach_peers(rpl_dqn *dqn);
 /* Test entry: the peer-memory gradient mean + SGD for `world` ranks emulated by one
  * cooperative launch on the current device (all buffers device memory on it): xbufs[world]
  * exchange buffers of the layout above (stride = their byte size / 4 floats; slot t % 2 holds
- * rank q's gradient and loss), online / target [world][P], gmean [world][P + 1] outputs,
+ * rank q's gradient and loss, then the [P + 1] mean of the reduce-scatter variant, then the
+ * flag area), online / target [world][P], gmean [world][P + 1] outputs,
  * sync_flag (int32, 1 = copy to target), err (sticky word); t > 0.  Synchronises. */
 int rpl_dp_emulate(int32_t world, int64_t P, float *xbufs, float *online, float *target,
-                   float *gmean, const int32_t *sync_flag, uint32_t *err, float lr, uint64_t t);
+                   float *gmean, const int32_t *sync_flag, uint32_t *err, float lr, uint64_t t,
+                   int32_t reduce_scatter);
 
 /* Synchronise the handle's stream and report (then clear) its sticky device error:
  * RPL_OK, RPL_ECORRUPT, RPL_ENUMERIC or RPL_ECUDA.  handle = rpl_replay* or rpl_dqn*

@@ -105,7 +105,7 @@ def _load():
         "dqn_peer_handle": (C.c_int, [P, P]),
         "dqn_attach_peers": (C.c_int, [P, i32, i32, P]),
         "dqn_detach_peers": (C.c_int, [P]),
-        "rpl_dp_emulate": (C.c_int, [i32, i64, P, P, P, P, P, P, C.c_float, u64]),
+        "rpl_dp_emulate": (C.c_int, [i32, i64, P, P, P, P, P, P, C.c_float, u64, i32]),
         "rpl_check": (C.c_int, [P, C.c_int]),
         "rpl_last_error": (C.c_char_p, []),
         "rpl_kernel_launches": (C.c_uint64, []),

@@ -19,7 +19,8 @@
 
 namespace rpl {
 
-constexpr int DP_MAXR = 8;   // ranks of one node
+constexpr int DP_MAXR = 8;                  // ranks of one node
+constexpr int64_t kDpRsMin = 1 << 20;      // gradients longer than this use the reduce-scatter kernel
 
 struct DPArgs {
     int nloc, world, rank0;              // ranks run by this launch: rank0 .. rank0 + nloc - 1
@@ -33,8 +34,10 @@ struct DPArgs {
     uint32_t *err[DP_MAXR];
 };
 
-// exchange buffer: [2][P + 1] floats, then the flag word on its own 256-byte line
-__host__ __device__ inline size_t dp_flag_offset(int64_t P) { return ((size_t)2 * (P + 1) * sizeof(float) + 255) / 256 * 256; }
+// exchange buffer: [2][P + 1] gradient slots, [P + 1] mean (reduce-scatter variant), then a
+// 256-byte flag area: flag (u64) at +0, broken (u32) at +64, flag2 (u64) at +128, a block
+// counter (u32) at +192
+__host__ __device__ inline size_t dp_flag_offset(int64_t P) { return ((size_t)3 * (P + 1) * sizeof(float) + 255) / 256 * 256; }
 __host__ __device__ inline size_t dp_xbuf_bytes(int64_t P) { return dp_flag_offset(P) + 256; }
 __host__ __device__ inline unsigned long long *dp_flag_of(const float *xbuf, int64_t P)
 {
@@ -66,6 +69,90 @@ __device__ __forceinline__ void dp_st_release(unsigned long long *p, unsigned lo
     asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
 
+// thread 0: wait until every rank's flag word (at word offset `which` of its flag area) reaches
+// t; gives up after ~10 s or when this rank's exchange is already broken (returns true)
+__device__ inline bool dp_wait_all(const DPArgs &a, int rank, int rl, int which)
+{
+    unsigned *broken = reinterpret_cast<unsigned *>(a.flag[rank] + 8);
+    bool timed_out = *reinterpret_cast<volatile unsigned *>(broken) != 0;
+    const long long t0 = clock64();
+    for (int q = 0; q < a.world && !timed_out; ++q)
+        while (dp_ld_acquire(a.flag[q] + which) < a.t) {
+            if (clock64() - t0 > 20000000000ll) {
+                timed_out = true;
+                atomicExch(broken, 1u);
+                break;
+            }
+        }
+    if (timed_out) atomicOr(a.err[rl], ERRBIT_PEER);
+    return timed_out;
+}
+
+// Reduce-scatter variant for large P (config 5's 15 MB gradient): rank r averages only its
+// 1/world of the P + 1 words, reading them from every rank, and stores the mean into every
+// rank's mean buffer; its last block to finish publishes flag2; after every rank's flag2 each
+// rank applies SGD from its own mean buffer.  Each rank moves ~2 P words over NVLink instead of
+// world x P.  Cooperative launch: a rank's blocks wait for its own last block.  The mean buffer
+// needs no second slot: rank r writes rank q's again only after q's next flag, i.e. after q
+// finished reading it.
+__global__ void __launch_bounds__(256) dp_peer_rs_sgd_kernel(const __grid_constant__ DPArgs a)
+{
+    const int bpr = gridDim.x / a.nloc;
+    const int rl = blockIdx.x / bpr, bi = blockIdx.x % bpr;
+    if (rl >= a.nloc) return;
+    const int rank = a.rank0 + rl;
+    const int64_t slot = (int64_t)(a.t & 1ull) * (a.P + 1), n = a.P + 1;
+    __shared__ int timed_out;
+    if (bi == 0 && threadIdx.x == 0) {
+        __threadfence_system();
+        dp_st_release(a.flag[rank], a.t);
+    }
+    if (threadIdx.x == 0) timed_out = dp_wait_all(a, rank, rl, 0);
+    __syncthreads();
+    if (timed_out) return;
+    __threadfence();
+    // this rank's slice of the mean, into every rank's mean buffer
+    const int64_t lo = n * rank / a.world, hi = n * (rank + 1) / a.world;
+    for (int64_t i = lo + (int64_t)bi * blockDim.x + threadIdx.x; i < hi; i += (int64_t)bpr * blockDim.x) {
+        float g = 0.0f;
+        for (int q = 0; q < a.world; ++q) g += __ldcv(a.xbuf[q] + slot + i);
+        g = g / (float)a.world;
+        for (int q = 0; q < a.world; ++q) const_cast<float *>(a.xbuf[q])[2 * n + i] = g;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned *cnt = reinterpret_cast<unsigned *>(a.flag[rank] + 24);
+        if (atomicAdd(cnt, 1u) == (unsigned)bpr - 1) {   // this rank's last block: publish
+            atomicExch(cnt, 0u);
+            __threadfence_system();
+            dp_st_release(a.flag[rank] + 16, a.t);
+        }
+        timed_out = dp_wait_all(a, rank, rl, 16);
+    }
+    __syncthreads();
+    if (timed_out) return;
+    __threadfence();
+    const float *mean = a.xbuf[rank] + 2 * n;
+    const float loss = __ldcv(mean + a.P);
+    const bool ok = isfinite(loss);
+    const int do_sync = *a.sync_flag[rl];
+    float *on = a.online[rl], *tg = a.target[rl], *gm = a.gmean[rl];
+    for (int64_t i = (int64_t)bi * blockDim.x + threadIdx.x; i < a.P; i += (int64_t)bpr * blockDim.x) {
+        const float g = __ldcv(mean + i);
+        gm[i] = g;
+        if (ok) {
+            const float w = on[i] - a.lr * g;
+            on[i] = w;
+            if (do_sync) tg[i] = w;
+        }
+    }
+    if (bi == 0 && threadIdx.x == 0) {
+        gm[a.P] = loss;
+        if (!ok) atomicOr(a.err[rl], ERRBIT_NUMERIC);
+    }
+}
+
 __global__ void __launch_bounds__(256) dp_peer_sgd_kernel(const __grid_constant__ DPArgs a)
 {
     const int bpr = gridDim.x / a.nloc;
@@ -82,20 +169,7 @@ __global__ void __launch_bounds__(256) dp_peer_sgd_kernel(const __grid_constant_
     // after ~10 s with the sticky ERRBIT_PEER and the update skipped, and marks this rank's
     // exchange broken so every later step skips at once (fail fast instead of a hang)
     __shared__ int timed_out;
-    unsigned *broken = reinterpret_cast<unsigned *>(a.flag[rank] + 8);
-    if (threadIdx.x == 0) {
-        timed_out = *reinterpret_cast<volatile unsigned *>(broken) != 0;
-        const long long t0 = clock64();
-        for (int q = 0; q < a.world && !timed_out; ++q)
-            while (dp_ld_acquire(a.flag[q]) < a.t) {
-                if (clock64() - t0 > 20000000000ll) {
-                    timed_out = 1;
-                    atomicExch(broken, 1u);
-                    break;
-                }
-            }
-        if (timed_out) atomicOr(a.err[rl], ERRBIT_PEER);
-    }
+    if (threadIdx.x == 0) timed_out = dp_wait_all(a, rank, rl, 0);
     __syncthreads();
     if (timed_out) return;
     __threadfence();

@@ -1833,8 +1833,14 @@ after_step:
         a.sync_flag[0] = d->sync_flag;
         a.err[0] = d->err;
         if (e == cudaSuccess) {
-            dp_peer_sgd_kernel<<<(unsigned)d->sms, 256, 0, d->stream>>>(a);
-            e = cudaGetLastError();
+            if (d->P + 1 > kDpRsMin) {   // large gradients: the reduce-scatter variant
+                void *args[] = {&a};
+                e = cudaLaunchCooperativeKernel((const void *)dp_peer_rs_sgd_kernel, dim3(d->sms), dim3(256),
+                                                args, 0, d->stream);
+            } else {
+                dp_peer_sgd_kernel<<<(unsigned)d->sms, 256, 0, d->stream>>>(a);
+                e = cudaGetLastError();
+            }
         }
         if (e != cudaSuccess) {
             if (prev >= 0) cudaSetDevice(prev);
@@ -2099,7 +2105,7 @@ extern "C" int dqn_detach_peers(rpl_dqn *d)
 // test entry: `world` ranks emulated by one cooperative launch on this device (dp_peer.cuh)
 extern "C" int rpl_dp_emulate(int32_t world, int64_t P, float *xbufs, float *online, float *target,
                               float *gmean, const int32_t *sync_flag, uint32_t *err, float lr,
-                              uint64_t t)
+                              uint64_t t, int32_t reduce_scatter)
 {
     if (world < 1 || world > DP_MAXR || P < 1 || !xbufs || !online || !target || !gmean ||
         !sync_flag || !err || t == 0)
@@ -2123,7 +2129,9 @@ extern "C" int rpl_dp_emulate(int32_t world, int64_t P, float *xbufs, float *onl
     }
     const int bpr = 8;
     void *args[] = {&a};
-    RPL_CUDA(cudaLaunchCooperativeKernel((const void *)dp_peer_sgd_kernel, dim3(world * bpr), dim3(256), args, 0, nullptr));
+    RPL_CUDA(cudaLaunchCooperativeKernel(reduce_scatter ? (const void *)dp_peer_rs_sgd_kernel
+                                                        : (const void *)dp_peer_sgd_kernel,
+                                         dim3(world * bpr), dim3(256), args, 0, nullptr));
     RPL_CUDA(cudaDeviceSynchronize());
     return RPL_OK;
 }

@@ -29,12 +29,13 @@ def b():
 
 
 def _xbuf_floats(P):
-    flag_off = ((2 * (P + 1) * 4 + 255) // 256) * 256
+    flag_off = ((3 * (P + 1) * 4 + 255) // 256) * 256
     return (flag_off + 256) // 4, flag_off // 4
 
 
+@pytest.mark.parametrize("rs", [0, 1], ids=["all-read", "reduce-scatter"])
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
-def test_emulated_ranks_mean_sgd(b, world):
+def test_emulated_ranks_mean_sgd(b, world, rs):
     import torch
     P, lr = 5003, np.float32(0.01)
     stride, flag_at = _xbuf_floats(P)
@@ -54,7 +55,7 @@ def test_emulated_ranks_mean_sgd(b, world):
             xb[q * stride + slot:q * stride + slot + P + 1] = torch.from_numpy(grads[q]).cuda()
         sync.fill_(1 if t == 3 else 0)
         st = b._L.rpl_dp_emulate(world, P, xb.data_ptr(), online.data_ptr(), target.data_ptr(),
-                                 gmean.data_ptr(), sync.data_ptr(), err.data_ptr(), C.c_float(lr), t)
+                                 gmean.data_ptr(), sync.data_ptr(), err.data_ptr(), C.c_float(lr), t, rs)
         assert st == b.RPL_OK, b.last_error()
         # flags hold the step number
         fl = xb.view(torch.int64)
@@ -84,7 +85,7 @@ def test_emulated_ranks_mean_sgd(b, world):
         xb[q * stride + slot:q * stride + slot + P + 1] = torch.from_numpy(bad[q]).cuda()
     before = online.clone()
     assert b._L.rpl_dp_emulate(world, P, xb.data_ptr(), online.data_ptr(), target.data_ptr(),
-                               gmean.data_ptr(), sync.data_ptr(), err.data_ptr(), C.c_float(lr), t) == b.RPL_OK
+                               gmean.data_ptr(), sync.data_ptr(), err.data_ptr(), C.c_float(lr), t, rs) == b.RPL_OK
     assert torch.equal(online, before) and err.item() == 2
 
 
