@@ -1,6 +1,6 @@
 // ring_row.cuh -- the one definition of a packed ring row write (CUDA path only), shared by
-// the insert kernel (replay.cu) and the deferred insert that K1 of the fast train step
-// performs (train_fast.cuh).  Row layout: [s (D) | s' (D) | a (i32 bits) |
+// the insert kernel (replay.cu) and the deferred insert that K3 of the fast train step
+// performs (train_fast.cuh: rows loaded into registers at K3's start, stored at its end).  Row layout: [s (D) | s' (D) | a (i32 bits) |
 // r | done (u32 bits) | zero pad], rs words, or [s | a | r | done | pad] with shared states.
 // experience j goes to slot (cursor + j) mod capacity.
 

@@ -4,16 +4,19 @@
 // CUDA graph:
 //
 //   K1 fwd  : per (net, 16-row batch tile, unit tile of layer 1): Philox sample + gather the 16
-//             rows, layer 0 for those rows (recomputed per unit tile: 55 kMAC, cheaper than a
-//             grid-wide exchange), the tile's layer-1 units and its partial sums of the V/A
-//             heads.  All weights stream into shared memory with cp.async while the sampled
-//             rows are being gathered from HBM.
+//             rows (pending-insert slots read through from the insert's source), layer 0 for
+//             those rows (recomputed per unit tile: 55 kMAC, cheaper than a grid-wide
+//             exchange), the tile's layer-1 units and its partial sums of the V/A heads, all as
+//             3xTF32 mma.sync tiles (mma_tf32.cuh).  All weights stream into shared memory
+//             with cp.async while the sampled rows are being gathered from HBM.
 //   K2 td   : per sample: reduce head partials, dueling combine, max / argmax (warp shuffles),
 //             TD target, Huber, dQ, dV/dA, and dZ1 = dHead . W_head (*) ReLU'(z1).
-//   K3 bwd1 : dW1 = dZ1^T H0 (+ db1) and split-K partials of dH0 = dZ1 W1 as 32x64 FP32 SIMT
-//             GEMM tiles (4x4 register blocking, float4 operand staging), head gradients.
-//   K4 bwd0 : dZ0 = (sum of dH0 partials) (*) ReLU'(z0), dW0 = dZ0^T X, then SGD of every
-//             parameter (non-finite guard), target sync, counters.
+//   K3 bwd1 : (programmatic launch: stages K1's operands while K2 runs) dW1 = dZ1^T H0 (+ db1)
+//             32x32 tiles, split-K partials of dH0 = dZ1 W1 with their dW0 / db0 shares, head
+//             gradients -- 3xTF32 mma.sync; its first CTAs also write the deferred insert's
+//             ring rows.
+//   K4 bwd0 : W0 / b0 = fixed-order sum of K3's partials, then SGD of every parameter
+//             (non-finite guard), target sync, counters; the loss is stored first.
 //
 // Step-varying state (sampler event, ring size, step counter) lives in device memory so the
 // same graph replays every step with no host input.
