@@ -179,7 +179,7 @@ def test_world2_peer_handle_allgather():
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29000 + (os.getpid() % 1000)
+    port = _free_port()
     ps = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in ps:
         p.start()
@@ -225,7 +225,7 @@ def test_world2_attach_auto_agrees(fail_rank, peer_ok, want):
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + (os.getpid() % 400) + 3 * (fail_rank + 1) + (0 if peer_ok else 1)
+    port = _free_port()
     ps = [ctx.Process(target=_auto_worker, args=(r, 2, port, fail_rank, peer_ok, q)) for r in range(2)]
     for p in ps:
         p.start()

@@ -170,7 +170,10 @@ def test_two_processes_map_each_others_exchange_buffers(b):
     import os
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 28000 + os.getpid() % 900
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
     ps = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in ps:
         p.start()
