@@ -139,7 +139,9 @@ __global__ void __launch_bounds__(256) wide_split_kernel(const float *__restrict
         planes[2 * pe + t] = l;
     }
 }
-__device__ __forceinline__ uint16_t u8_bf16(uint32_t v) { return __bfloat16_as_ushort(__uint2bfloat16_rn(v)); }
+// a byte 0..255 as bf16: exact in fp32 and in bf16 (<= 8 significant bits), so the bf16 is the
+// fp32's upper half -- one I2F and a shift instead of the general rounding conversion
+__device__ __forceinline__ uint16_t u8_bf16(uint32_t v) { return (uint16_t)(__float_as_uint((float)v) >> 16); }
 
 // ------------------------------------------------------------------------------------------
 // layer-0 forward partials
