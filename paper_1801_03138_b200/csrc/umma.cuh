@@ -134,6 +134,16 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float v[8])
     for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// the same load without its wait: several loads in flight, then one tmem_wait_ld()
+__device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, uint32_t r[8])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                   "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 // fp32 -> three bf16 terms hi + mid + lo that carry all 24 significand bits (round-to-nearest
 // at each stage): x - (hi + mid + lo) is 0 for normal x outside the bf16 underflow range
 __device__ __forceinline__ void split3_bf16(float x, uint16_t &hi, uint16_t &mid, uint16_t &lo)

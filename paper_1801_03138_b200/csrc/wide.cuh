@@ -271,12 +271,21 @@ __global__ void __launch_bounds__(WD_T, 1) wide_l0_kernel(const __grid_constant_
         const int q = warp & 3, half = warp >> 2, u = 32 * q + lane;
         const int c0 = half * (N / 2), c1 = c0 + N / 2;
         float *out = p.PF0 + ((int64_t)kq * p.nets + net) * p.B * p.N0;
-        for (int c = c0; c < c1; c += 8) {
-            float v[8];
-            umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + c, v);
+        // 32 columns per round: four TMEM loads in flight, one wait, then the stores
+        for (int c = c0; c < c1; c += 32) {
+            uint32_t r[4][8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-                if (c + i < p.B && u < p.N0) out[(int64_t)(c + i) * p.N0 + u] = v[i];   // x 255
+            for (int j = 0; j < 4; ++j)
+                if (c + 8 * j < c1) umma::tmem_ld8_nowait(tmem + ((uint32_t)(32 * q) << 16) + c + 8 * j, r[j]);
+            umma::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int cc = c + 8 * j + i;
+                    if (cc < c1 && cc < p.B && u < p.N0)
+                        out[(int64_t)cc * p.N0 + u] = __uint_as_float(r[j][i]);   // x 255
+                }
         }
     } else {
         // cluster of cs consecutive chunks: CTA r owns sample columns [r Nc, (r + 1) Nc) of the
