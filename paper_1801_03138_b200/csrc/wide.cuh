@@ -505,11 +505,21 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
     {
         const int q = warp & 3, half = warp >> 2, u = 32 * q + lane;
         const int c0 = half * (N / 2), c1 = c0 + N / 2;
-        for (int c = c0; c < c1; c += 8) {
-            float v[8];
-            umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + c, v);
-            *reinterpret_cast<float4 *>(T + u * TS + c) = make_float4(v[0], v[1], v[2], v[3]);
-            *reinterpret_cast<float4 *>(T + u * TS + c + 4) = make_float4(v[4], v[5], v[6], v[7]);
+        for (int c = c0; c < c1; c += 32) {   // four TMEM loads in flight per wait
+            uint32_t r[4][8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (c + 8 * j < c1) umma::tmem_ld8_nowait(tmem + ((uint32_t)(32 * q) << 16) + c + 8 * j, r[j]);
+            umma::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (c + 8 * j < c1) {
+                    float *dst = T + u * TS + c + 8 * j;
+                    *reinterpret_cast<float4 *>(dst) = make_float4(__uint_as_float(r[j][0]), __uint_as_float(r[j][1]),
+                                                                   __uint_as_float(r[j][2]), __uint_as_float(r[j][3]));
+                    *reinterpret_cast<float4 *>(dst + 4) = make_float4(__uint_as_float(r[j][4]), __uint_as_float(r[j][5]),
+                                                                       __uint_as_float(r[j][6]), __uint_as_float(r[j][7]));
+                }
         }
     }
     if (wpre) asm volatile("cp.async.wait_group 0;" ::: "memory");
