@@ -496,9 +496,17 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
     const bool wpre = p.wpre && upd;
     if (wpre) {
         const int nq = nn / 4;
+        // e = pu * nq + pc, advanced by WD_T = du * nq + dc without divisions
+        const int du = WD_T / nq, dc = WD_T % nq;
+        int pu = tid / nq, pc = tid % nq;
         for (int e = tid; e < p.N0 * nq; e += WD_T) {
-            const int u = e / nq, c = 4 * (e % nq);
-            wd_cp16(Wt + u * TS + c, p.online_w + p.w0 + (int64_t)u * p.D + n0 + c);
+            wd_cp16(Wt + pu * TS + 4 * pc, p.online_w + p.w0 + (int64_t)pu * p.D + n0 + 4 * pc);
+            pu += du;
+            pc += dc;
+            if (pc >= nq) {
+                pc -= nq;
+                ++pu;
+            }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
@@ -536,9 +544,14 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
         const int r8 = lane >> 2, q4 = lane & 3;
         const int nch = nn / 16, ntask = (p.N0 / 8) * nch;
 #pragma unroll 2
-        for (int task = warp; task < ntask; task += NWE) {
+        int tg = warp / nch, tc = warp % nch;   // task = tg * nch + tc, advanced without divisions
+        for (int task = warp; task < ntask; task += NWE, tc += NWE) {
+                while (tc >= nch) {
+                    tc -= nch;
+                    ++tg;
+                }
                 {
-                    const int u = 8 * (task / nch) + r8, c = 16 * (task % nch) + 4 * q4;
+                    const int u = 8 * tg + r8, c = 16 * tc + 4 * q4;
                     const int64_t j = (int64_t)u * p.D + n0 + c;   // index within W0
                     const int64_t wi = p.w0 + j;
                     const float4 t = *reinterpret_cast<const float4 *>(T + u * TS + c);
