@@ -66,14 +66,25 @@ def attach_auto(dqn, peer_ok: bool | None = None) -> str:
         dev = torch.cuda.current_device()
         n = torch.cuda.device_count()
         ok = n >= world and all(torch.cuda.can_device_access_peer(dev, o) for o in range(world) if o != dev)
-    agree = _all_min(1 if ok else 0)
-    attached = False
-    if agree:
-        try:
-            attach_peers(dqn)
-            attached = True
-        except Exception:
-            attached = False
+    # every rank runs the same collectives whatever fails locally: agree on the probe, then on
+    # the exported handles, then on the mappings
+    if not _all_min(1 if ok else 0):
+        attach(dqn)
+        return "nccl"
+    handle, h_ok = bytes(64), True
+    try:
+        handle = dqn.peer_handle()
+    except Exception:
+        h_ok = False
+    if not _all_min(1 if h_ok else 0):
+        attach(dqn)
+        return "nccl"
+    handles = gather_bytes(handle, 64)
+    attached = True
+    try:
+        dqn.attach_peers(rank, world, handles)
+    except Exception:
+        attached = False
     if _all_min(1 if attached else 0):
         return "p2p"
     if attached:
