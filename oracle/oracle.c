@@ -702,6 +702,23 @@ void oracle_sgd(int64_t n, double *w, const double *g, double lr)
     for (int64_t i = 0; i < n; ++i) w[i] = w[i] - lr * g[i];
 }
 
+/* O6, data-parallel learners ("the model synchronized every train step"; reading
+ * Q22/Q23): every rank r evaluates its own batch mean gradient g_r; the ranks' gradients are
+ * summed in rank order 0..N-1, divided by N, and the same SGD step w <- w - alpha * mean is
+ * applied on every replica.  grads[r] points at rank r's P-word gradient.  mean_out
+ * (nullable) receives the mean. */
+void oracle_dp_mean_sgd(int32_t world, int64_t n, double *w, const double *const *grads,
+                        double lr, double *mean_out)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        double acc = 0.0;
+        for (int32_t r = 0; r < world; ++r) acc += grads[r][i];
+        const double g = acc / (double)world;
+        if (mean_out) mean_out[i] = g;
+        w[i] = w[i] - lr * g;
+    }
+}
+
 /* ------------------------------------------------------------------------------------
  * A complete learner: burn-in gate, sample, gather, loss/grad, SGD, step counter and the
  * periodic target sync ("updated to have the same weights as the online network once

@@ -111,6 +111,8 @@ int oracle_dqn_loss_grad(const oracle_net *net, const double *online, const doub
                          double *q_s, double *q_next_target, double *q_next_online, double *y,
                          int32_t *a_star, double *z_online, uint8_t *on_online);
 void oracle_sgd(int64_t n, double *w, const double *g, double lr);
+void oracle_dp_mean_sgd(int32_t world, int64_t n, double *w, const double *const *grads,
+                        double lr, double *mean_out);
 
 typedef struct {
     oracle_net net;

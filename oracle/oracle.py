@@ -155,6 +155,7 @@ def _declare(L):
                                        _P, _P, _P, _P, _P, _P, _P]
     L.oracle_dqn_loss_grad.restype = C.c_int
     L.oracle_sgd.argtypes = [C.c_int64, _P, _P, C.c_double]
+    L.oracle_dp_mean_sgd.argtypes = [C.c_int32, C.c_int64, _P, _P, C.c_double, _P]
     L.oracle_learner_step.argtypes = [C.POINTER(_Ring), C.POINTER(_Learner), C.c_int32, _P, _P]
     L.oracle_learner_step.restype = C.c_int
     L.oracle_sync_target.argtypes = [C.POINTER(_Learner)]
@@ -469,6 +470,18 @@ def sgd(w, g, lr: float) -> np.ndarray:
     g = _c(g, np.float64)
     lib().oracle_sgd(w.size, _ptr(w), _ptr(g), lr)
     return w
+
+
+def dp_mean_sgd(w, grads, lr: float):
+    """O6: rank-order sum of the ranks' gradients / N, then SGD on the replica.
+    Returns (new weights, mean gradient)."""
+    w = np.array(w, dtype=np.float64)
+    gs = [_c(g, np.float64) for g in grads]
+    assert all(g.size == w.size for g in gs)
+    arr = (C.c_void_p * len(gs))(*[g.ctypes.data for g in gs])
+    mean = np.zeros_like(w)
+    lib().oracle_dp_mean_sgd(len(gs), w.size, _ptr(w), C.cast(arr, C.c_void_p), lr, _ptr(mean))
+    return w, mean
 
 
 class Learner:
