@@ -20,6 +20,7 @@ import statistics
 import subprocess
 import sys
 import threading
+import types
 import time
 
 import numpy as np
@@ -58,10 +59,11 @@ def parse():
     ap.add_argument("--precision", choices=["fp32", "tf32", "bf16"], default="fp32",
                     help="tensor-core products: fp32 (FP32-accurate splits, the default and the "
                          "judged line) or one tf32 / bf16 product (reduced precision, parity 2e-2)")
-    ap.add_argument("--dp", choices=["auto", "nccl", "p2p"], default="auto",
-                    help="N > 1: gradient mean by the peer-memory mean + SGD kernel "
-                         "(dqn_attach_peers) when every rank's GPU can map every other's (auto, "
-                         "the default), or by ncclAllReduce")
+    ap.add_argument("--dp", choices=["nccl", "auto", "p2p"], default="nccl",
+                    help="N > 1: gradient mean by ncclAllReduce inside every step (nccl, the "
+                         "default: the north star's path), or by the peer-memory mean + SGD "
+                         "kernel (dqn_attach_peers) when every rank's GPU can map every other's "
+                         "(auto), or always (p2p)")
     ap.add_argument("--ring", choices=["device", "host"], default="device",
                     help="host: the in-RAM comparison mode (SURVEY NEXT-1): ring rows in pinned host "
                          "memory, every batch read across PCIe by the same kernels")
@@ -89,16 +91,19 @@ def workload_name(a, batch):
             f"{net}, {tgt} target, Huber, SGD, {a.adds_per_step} inserts/step{where}")
 
 
-def make_cfg(a, binding, batch):
+def cfg_fields(a, batch):
+    """The learner configuration of the run as plain fields (no library import: the oracle arm
+    uses these too)."""
+    common = dict(state_dim=27, n_actions=8, double_dqn=a.ddqn, gamma=0.99, lr=1e-4, huber_kappa=1.0,
+                  sync_period=10_000, max_batch=max(batch, 128), avg_period=a.avg_period,
+                  precision=a.precision)
     if a.net == "dueling":
-        return binding.DQNConfig(state_dim=27, n_actions=8, dueling=True, hidden=(128,), stream=512,
-                                 double_dqn=a.ddqn, gamma=0.99, lr=1e-4, huber_kappa=1.0,
-                                 sync_period=10_000, max_batch=max(batch, 128),
-                                 avg_period=a.avg_period, precision=a.precision)
-    return binding.DQNConfig(state_dim=27, n_actions=8, dueling=False, hidden=(64, 64),
-                             double_dqn=a.ddqn, gamma=0.99, lr=1e-4, huber_kappa=1.0,
-                             sync_period=10_000, max_batch=max(batch, 128), avg_period=a.avg_period,
-                             precision=a.precision)
+        return dict(common, dueling=True, hidden=(128,), stream=512)
+    return dict(common, dueling=False, hidden=(64, 64), stream=0)
+
+
+def make_cfg(a, binding, batch):
+    return binding.DQNConfig(**cfg_fields(a, batch))
 
 
 def oracle_net_of(cfg):
@@ -110,53 +115,85 @@ def oracle_net_of(cfg):
 # clocks during the timed region (B200_PROFILING.md clocks line)
 # ------------------------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and clock-event reasons sampled through NVML every `poll_ms` from before the
+    warm-up until after the extra passes; `mark_start` / `mark_end` bracket the timed region,
+    whose samples (if any) the summary reports, else those of the whole loaded phase."""
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, gpu_index):
-        self.gpu = gpu_index
-        self.rows = []
-        self.proc = None
+    def __init__(self, torch_device: int, poll_ms: float = 5.0):
+        self.dev = torch_device
+        self.poll = poll_ms / 1000.0
+        self.rows = []          # (t, sm_mhz, reasons bitmask)
+        self.win = [None, None]
+        self.max_mhz = None
+        self.err = None
+        self._stop = threading.Event()
+        self.t = None
 
-    def __enter__(self):
+    def _handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            pr = torch.cuda.get_device_properties(self.dev)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
         except Exception:
-            self.proc = None
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+
+    def start(self):
+        try:
+            nv, h = self._handle()
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        except Exception as e:   # no NVML: the line says so
+            self.err = f"{type(e).__name__}: {e}"
+            return self
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.rows.append((time.perf_counter(), float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                      int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))))
+                except Exception as e:
+                    self.err = f"{type(e).__name__}: {e}"
+                    return
+                time.sleep(self.poll)
+
+        self.t = threading.Thread(target=run, daemon=True)
+        self.t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+    def mark_start(self):
+        self.win[0] = time.perf_counter()
 
-    def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+    def mark_end(self):
+        self.win[1] = time.perf_counter()
+
+    def stop(self):
+        self._stop.set()
+        if self.t:
+            self.t.join(timeout=2)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for n, v in zip(names, r[5:9]):
-                if v.strip().lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"],
+                    "error": self.err}
+        t0, t1 = self.win
+        timed = [r for r in self.rows if t0 is not None and t1 is not None and t0 <= r[0] <= t1]
+        use = timed if timed else self.rows
+        import pynvml as nv
+        reasons = sorted({n for n, attr in self.REASONS for r in use
+                          if r[2] & int(getattr(nv, attr, 0))})
+        return {"sm_mhz": statistics.median(r[1] for r in use), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples_timed_region": len(timed), "samples": len(self.rows),
+                "window": "timed region" if timed else
+                          "warm-up + timed region + extra passes (the timed region was shorter than "
+                          "one poll)",
+                "poll_ms": self.poll * 1000.0, "source": "NVML"}
 
 
 def load_peaks():
@@ -178,14 +215,96 @@ def load_traffic():
     return {}
 
 
+def kernel_breakdown(step, n):
+    """Per-kernel device time of `n` calls of step(i), from CUPTI (torch.profiler): mean us per
+    launch, launches per step and share of the summed kernel time; run after the timed region."""
+    import collections
+    import torch
+    for i in range(3):
+        step(i)
+    torch.cuda.synchronize()
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+        for i in range(n):
+            step(3 + i)
+        torch.cuda.synchronize()
+    per = collections.defaultdict(list)
+    for e in prof.events():
+        if e.device_type == torch.autograd.DeviceType.CUDA:
+            per[e.name].append(e.time_range.end - e.time_range.start)
+    tot = sum(sum(v) for v in per.values()) or 1.0
+    out = [{"kernel": k, "mean_us": float(np.mean(v)), "launches_per_step": len(v) / n,
+            "share": sum(v) / tot} for k, v in per.items()]
+    out.sort(key=lambda d: -d["share"])
+    return {"steps": n, "busy_us_per_step": tot / n, "kernels": out}
+
+
+def flop_parts(cfg, batch):
+    """(forward, backward) FLOPs of one step (2 per multiply-add): forward = every net's pass
+    (online on s, target on s', online on s' for Double DQN); backward = dW of every layer + dX
+    of every layer but the first."""
+    layers, k = [], cfg.state_dim
+    for h in cfg.hidden:
+        layers.append((h, k))
+        k = h
+    if cfg.dueling:
+        layers += [(2 * cfg.stream, k), (1 + cfg.n_actions, cfg.stream)]
+    else:
+        layers.append((cfg.n_actions, k))
+    fwd = sum(o * i for o, i in layers)
+    dx = sum(o * i for o, i in layers[1:])
+    nets = 3 if cfg.double_dqn else 2
+    return 2 * batch * nets * fwd, 2 * batch * (fwd + dx)
+
+
+def tensor_peak(peaks, precision):
+    """The tensor-core roofline of the step's contractions: kind::tf32 tcgen05 MMAs (half the
+    measured bf16 dense rate, the nominal tf32 / bf16 ratio), three products per FP32-accurate
+    product (hi.hi + hi.lo + lo.hi) in the fp32 mode, one in the tf32 / bf16 modes; the
+    sustained bf16 figure since the kernels run inside a long step."""
+    bf16 = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1352.0)))
+    tf32 = bf16 * 0.5
+    return (tf32 / 3.0 if precision == "fp32" else tf32), bf16
+
+
+def step_roofline(cfg, binding, batch, flops, ms_per_step, kb, peaks, peaks_kind, traffic,
+                  precision="fp32"):
+    peak, bf16 = tensor_peak(peaks, precision)
+    achieved = flops / (ms_per_step / 1000.0) / 1e12
+    fwd, bwd = flop_parts(cfg, batch)
+    kernels = []
+    for d in kb["kernels"]:
+        row = dict(d)
+        name = d["kernel"]
+        f = fwd if "fwd" in name else bwd if "bwd1" in name else None
+        if f is not None and d["mean_us"] > 0:
+            row["flops"] = f
+            row["achieved_TFLOPs"] = f / (d["mean_us"] * 1e-6) / 1e12
+            row["frac"] = row["achieved_TFLOPs"] / peak
+        kernels.append(row)
+    return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "kernel": "the train step as one unit (one CUDA graph: fwd / td / bwd1 / bwd0+sgd "
+                      "kernels): its algorithmic FLOPs / the timed ms_per_step",
+            "kernel_avg_us": ms_per_step * 1000.0, "flops_per_launch": flops,
+            "peak_note": f"measured bf16 dense {bf16:.0f} TFLOP/s sustained ({peaks_kind}) x 0.5 "
+                         "(nominal tf32 / bf16 ratio)"
+                         + (" / 3 (three tf32 products per FP32-accurate product)" if precision == "fp32" else "")
+                         + ": the tensor-core ceiling of the step's contractions on this GPU, whichever "
+                           "MMA instructions the kernels of this batch size issue",
+            "kernels_cupti": {"steps": kb["steps"], "busy_us_per_step": kb["busy_us_per_step"],
+                              "kernels": kernels,
+                              "note": "per-kernel CUPTI durations from a separate pass after the "
+                                      "timed region; fwd = every net's forward FLOPs, bwd1 = the "
+                                      "backward FLOPs"}}
+
+
 # ------------------------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline and --impl reference)
 # ------------------------------------------------------------------------------------------
 def time_oracle(a, batch, seconds, max_steps=None, steps_wanted=None, warmup=0):
     import oracle
     from inputs import experiences, init_params
-    import paper_1801_03138_b200.binding as binding  # host-only: DQNConfig / param count
-    cfg = make_cfg(a, binding, batch)
+    cfg = types.SimpleNamespace(**cfg_fields(a, batch))
     net = oracle_net_of(cfg)
     ring = oracle.Ring(a.capacity, 27)
     ring.add_many(experiences(a.capacity, seed=1))
@@ -249,7 +368,8 @@ def run_reference(a):
         "data": "synthetic", "config": {"workload": workload_name(a, batch), "batch": batch,
                                         "capacity": a.capacity, "parallelism": "none (CPU oracle)"},
         "cpu_baseline": {"value": v, "unit": "train_steps/s", "cores": 1, "kind": "oracle",
-                         "sample": sample, "cpu": lscpu_model()},
+                         "sample": sample, "cpu": lscpu_model(), "host_nproc": os.cpu_count(),
+               "threads_used": 1},
         "e2e": {"value": v, "unit": "train_steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -307,7 +427,7 @@ def run_ours(a, batch, first_line=True):
             j = (i % 256) * k
             rp.add(**{kk: v[j:j + k] for kk, v in pool_d.items()}, defer=True)
 
-    launches0 = binding.kernel_launches()
+    clk = ClockSampler(local).start()   # before the warm-up, so a short timed region is covered
     for i in range(W):
         add_dev(i)
         dqn.train_step(rp, batch, loss_dev)
@@ -318,30 +438,23 @@ def run_ours(a, batch, first_line=True):
 
     # ---- device-resident timed region (nothing but the steps between the two events) ------
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        start.record(stream)
-        for i in range(K):
-            add_dev(W + i)
-            dqn.train_step(rp, batch, loss_dev)
-        end.record(stream)
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk.mark_start()
+    start.record(stream)
+    for i in range(K):
+        add_dev(W + i)
+        dqn.train_step(rp, batch, loss_dev)
+    end.record(stream)
+    torch.cuda.synchronize()
+    clk.mark_end()
     launches = binding.kernel_launches() - launches_w
     elapsed_ms = start.elapsed_time(end)
-    # per-launch duration of the step's kernels for the roofline: a separate pass with CUDA
-    # events around every dqn_train_step (the events add stream ops, so not the timed one)
-    kr = min(K, 1000)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(kr)]
-    for i in range(kr):
-        add_dev(W + K + i)
-        ev[i][0].record(stream)
-        dqn.train_step(rp, batch, loss_dev)
-        ev[i][1].record(stream)
-    torch.cuda.synchronize()
-    kern_ms = [s.elapsed_time(e) for s, e in ev]
+    # per-kernel device times (CUPTI through torch.profiler) in a separate pass after the timed
+    # region: the roofline's kernel shares, never the timed number
+    kb = kernel_breakdown(lambda i: (add_dev(W + K + i), dqn.train_step(rp, batch, loss_dev)),
+                          min(max(K, 50), 400))
     st = dqn.check()
     assert st == binding.RPL_OK, f"device error {st}: {binding.last_error()}"
     if world > 1:
@@ -388,22 +501,11 @@ def run_ours(a, batch, first_line=True):
                        "dqn_train_step whose last kernel writes the loss into pinned host memory, "
                        "every step; slower of CUDA-event and wall time"}
 
-    # ---- roofline of the dominant kernel (the fused train step) --------------------------
+    # ---- roofline: the train step as one unit (its FLOPs / the timed ms_per_step) and each
+    # tensor-core kernel on its own (its FLOPs / its CUPTI mean duration) ------------------
     flops = binding.step_flops(cfg, batch)
-    kern_avg_ms = float(np.mean(kern_ms))
-    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    peak_fp32 = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12   # FP32 FMA lanes x 2 x clock
-    achieved = flops / (kern_avg_ms / 1000.0) / 1e12
-    traffic = load_traffic().get(f"train_step_b{batch}_{a.net}_{'ddqn' if a.ddqn else 'dqn'}")
-    roofline = {"bound": "alu", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
-                "frac": achieved / peak_fp32, "traffic": traffic,
-                "kernel": "the train-step CUDA graph (fwd / td / bwd1 / bwd0+sgd kernels) timed as one "
-                          "unit with CUDA events around each dqn_train_step on the library stream",
-                "kernel_avg_us": kern_avg_ms * 1000.0, "flops_per_launch": flops,
-                "peak_note": "FP32 SIMT: 148 SMs x 128 FMA lanes x 2 FLOP x sm_max_mhz "
-                             f"{sm_mhz:.0f} MHz (derived, {peaks_kind} clock); the forward runs its "
-                             "products as 3xTF32 mma.sync, so this FP32 peak is the conservative "
-                             "denominator for an FP32-accurate step"}
+    roofline = step_roofline(cfg, binding, batch, flops, ms_per_step, kb, peaks, peaks_kind,
+                             load_traffic().get(f"train_step_b{batch}_{a.net}_{'ddqn' if a.ddqn else 'dqn'}"))
 
     # ---- gather bandwidth (metric part 2): explicit-index gather from the 1M ring --------
     gather = None
@@ -503,7 +605,13 @@ def run_ours(a, batch, first_line=True):
         cpu = {"value": n / el, "unit": "train_steps/s", "cores": 1, "kind": "oracle",
                "sample": f"{n} oracle steps ({a.adds_per_step} inserts + one B={batch} train step "
                          f"from a {a.capacity:,}-row host ring) in {el:.1f} s, single thread, fp64",
-               "cpu": lscpu_model()}
+               "cpu": lscpu_model(), "host_nproc": os.cpu_count(),
+               "threads_used": 1}
+
+    # ---- N > 1: the peer-memory exchange (dp_peer.cuh) as a second measured arm ----------
+    p2p_arm = None
+    if world > 1 and a.dp == "nccl" and not a.avg_period and first_line:
+        p2p_arm = time_p2p_arm(a, binding, cfg, rp, batch, add_dev, W + 2 * K + 400, stream, dev)
 
     line = {
         "metric": METRIC, "value": value, "unit": "train_steps/s", "n_gpus": world, "steps": K,
@@ -526,13 +634,59 @@ def run_ours(a, batch, first_line=True):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gather": gather,
-        "clocks": clk.summary(),
+        "dp_p2p_arm": p2p_arm,
+        "clocks": (clk.stop(), clk.summary())[1],
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
     dqn.close()
     rp.close()
     return line
+
+
+def time_p2p_arm(a, binding, cfg, rp, batch, add_dev, i0, stream, dev):
+    """A second learner on the same shards whose gradient mean + SGD runs in the peer-memory
+    kernel (dqn_attach_peers) instead of NCCL: the same K steps, timed the same way (max over
+    ranks).  Its failure mode is bounded: a missing peer ends the kernel's flag wait after ~10 s
+    with RPL_ENCCL at the check, reported here instead of a number."""
+    import torch
+    import torch.distributed as dist
+    from inputs import init_params
+    from paper_1801_03138_b200 import dp
+    K, W = a.steps, a.warmup
+    dqn = binding.DQN(cfg, init_params(27, 8, cfg.hidden, cfg.dueling, cfg.stream, seed=3),
+                      device=torch.cuda.current_device())
+    try:
+        used = dp.attach_auto(dqn)
+        if used != "p2p":
+            return {"unavailable": "peer mapping between the ranks' GPUs failed; NCCL used instead"}
+        for i in range(W):
+            add_dev(i0 + i)
+            dqn.train_step(rp, batch)
+        torch.cuda.synchronize()
+        dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for i in range(K):
+            add_dev(i0 + W + i)
+            dqn.train_step(rp, batch)
+        e.record(stream)
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e)
+        ok = dqn.check() == binding.RPL_OK
+        t = torch.tensor([ms, 0.0 if ok else 1.0], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, bad = t[0].item(), t[1].item()
+        if bad:
+            return {"error": "a rank's exchange failed (sticky RPL_ENCCL)"}
+        return {"value": dist.get_world_size() * K / (ms / 1000.0), "unit": "train_steps/s",
+                "ms_per_step": ms / K, "steps": K,
+                "note": "gradient mean + SGD over NVLink peer memory in one kernel per step "
+                        "(dp_peer.cuh), same shards and batch as the NCCL line"}
+    except Exception as ex:   # reported, never fatal to the NCCL line
+        return {"error": f"{type(ex).__name__}: {ex}"}
+    finally:
+        dqn.close()
 
 
 # ------------------------------------------------------------------------------------------
@@ -745,7 +899,8 @@ def run_c5(a):
         cpu = {"value": n / el, "unit": "train_steps/s", "cores": 1, "kind": "oracle",
                "sample": f"{n} oracle steps (sample + u8->x + loss/grad + SGD at B={batch}) from a "
                          f"1,024-row host byte ring in {el:.1f} s, single thread, fp64",
-               "cpu": lscpu_model()}
+               "cpu": lscpu_model(), "host_nproc": os.cpu_count(),
+               "threads_used": 1}
     line = {
         "metric": "DQN train steps/s at batch 256, 84x84x4 uint8 states, 1M replay per GPU "
                   "(BASELINE configs[4]); gather GB/s vs HBM peak",
@@ -772,11 +927,26 @@ def run_c5(a):
     rp.close()
 
 
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` without a torchrun environment: launch the N ranks here (one process per GPU,
+    torch.distributed.run on 127.0.0.1, the driver's own launch form) and return their exit
+    code; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     a = parse()
-    if a.impl == "reference":
+    if a.impl == "reference":   # rank 0 alone times the oracle (the other ranks exit at once)
         run_reference(a)
         return
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(a.gpus))
     if a.config == "c5":
         run_c5(a)
     elif a.sweep:

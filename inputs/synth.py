@@ -50,6 +50,52 @@ def experiences(n: int, state_dim: int = 27, n_actions: int = 8, seed: int = 1, 
 ATARI_STATE_DIM = 84 * 84 * 4   # SURVEY config 5: 84x84x4 uint8 frames stacked per state
 
 
+# ---- counter-based byte rows: experience t is a pure function of t (large rings) -----------
+# Rings too large to generate and keep on the host (configs[4]: 56 GB at 1M rows) are filled
+# from this hash on the device (torch) and checked on the host (numpy) for the sampled rows
+# only; both evaluate the same 32-bit integer arithmetic.
+_M = 0xFFFFFFFF
+
+
+def _h32(x, xp):
+    x = x & _M
+    x = (x ^ (x >> 16)) & _M
+    x = (x * 0x7FEB352D) & _M
+    x = (x ^ (x >> 15)) & _M
+    x = (x * 0x846CA68B) & _M
+    return (x ^ (x >> 16)) & _M
+
+
+def _u8_fields(t, D, n_actions, xp, arange):
+    j = arange(D)[None, :]
+    tt = t[:, None]
+    s = _h32(tt * 0x9E3779B1 + j * 0x85EBCA77 + 0x1000, xp) & 0xFF
+    s2 = _h32(tt * 0x9E3779B1 + j * 0x85EBCA77 + 0x2000, xp) & 0xFF
+    ha = _h32(t * 0x9E3779B1 + 0x3000, xp)
+    hr = _h32(t * 0x9E3779B1 + 0x4000, xp)
+    hd = _h32(t * 0x9E3779B1 + 0x5000, xp)
+    return s, s2, ha % n_actions, hr >> 8, (hd < (1 << 26))
+
+
+def u8_rows_np(t, state_dim: int = ATARI_STATE_DIM, n_actions: int = 8) -> dict:
+    """Experiences number t (int array) of the counter-based byte stream, as numpy arrays."""
+    t = np.asarray(t, dtype=np.int64)
+    s, s2, a, r24, d = _u8_fields(t, state_dim, n_actions, np, lambda n: np.arange(n, dtype=np.int64))
+    r = (r24.astype(np.float64) * 2.0 ** -23 - 1.0).astype(np.float32)
+    return dict(s=s.astype(np.uint8), a=a.astype(np.int32), r=r, s_next=s2.astype(np.uint8),
+                done=d.astype(np.uint8))
+
+
+def u8_rows_torch(t, state_dim: int = ATARI_STATE_DIM, n_actions: int = 8) -> dict:
+    """The same experiences as CUDA tensors (t: int64 tensor on the device)."""
+    import torch
+    s, s2, a, r24, d = _u8_fields(t, state_dim, n_actions, torch,
+                                  lambda n: torch.arange(n, dtype=torch.int64, device=t.device))
+    r = (r24.to(torch.float64) * 2.0 ** -23 - 1.0).to(torch.float32)
+    return dict(s=s.to(torch.uint8), a=a.to(torch.int32), r=r, s_next=s2.to(torch.uint8),
+                done=d.to(torch.uint8))
+
+
 def experiences_u8(n: int, state_dim: int = ATARI_STATE_DIM, n_actions: int = 8, seed: int = 1,
                    rank: int = 0, done_prob: float = 1.0 / 64.0) -> dict:
     """n synthetic Atari-shaped experiences (SURVEY config 5): uint8 states uniform over

@@ -69,23 +69,36 @@ __device__ __forceinline__ void dp_st_release(unsigned long long *p, unsigned lo
     asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
 
-// thread 0: wait until every rank's flag word (at word offset `which` of its flag area) reaches
-// t; gives up after ~10 s or when this rank's exchange is already broken (returns true)
-__device__ inline bool dp_wait_all(const DPArgs &a, int rank, int rl, int which)
+__device__ __forceinline__ unsigned *dp_broken_of(unsigned long long *flag) { return reinterpret_cast<unsigned *>(flag + 8); }
+__device__ __forceinline__ bool dp_is_broken(unsigned long long *flag)
 {
-    unsigned *broken = reinterpret_cast<unsigned *>(a.flag[rank] + 8);
-    bool timed_out = *reinterpret_cast<volatile unsigned *>(broken) != 0;
+    return *reinterpret_cast<volatile unsigned *>(dp_broken_of(flag)) != 0;
+}
+
+// thread 0: wait until every rank's flag word (at word offset `which` of its flag area) reaches
+// t (the own rank's only for `own`: its step-t gradient precedes the kernel in stream order).
+// Fails -- returns true, marks this rank's exchange broken and raises ERRBIT_PEER -- when this
+// rank's exchange is already broken, when a peer's is (a broken rank stops publishing, so every
+// rank of the group fails at the same step instead of averaging a frozen replica's gradient),
+// or after ~10 s without the flag.
+__device__ inline bool dp_wait_all(const DPArgs &a, int rank, int rl, int which, bool own)
+{
+    bool failed = dp_is_broken(a.flag[rank]);
     const long long t0 = clock64();
-    for (int q = 0; q < a.world && !timed_out; ++q)
+    for (int q = 0; q < a.world && !failed; ++q) {
+        if (q == rank && !own) continue;
         while (dp_ld_acquire(a.flag[q] + which) < a.t) {
-            if (clock64() - t0 > 20000000000ll) {
-                timed_out = true;
-                atomicExch(broken, 1u);
+            if (dp_is_broken(a.flag[q]) || clock64() - t0 > 20000000000ll) {
+                failed = true;
                 break;
             }
         }
-    if (timed_out) atomicOr(a.err[rl], ERRBIT_PEER);
-    return timed_out;
+    }
+    if (failed) {
+        atomicExch(dp_broken_of(a.flag[rank]), 1u);
+        atomicOr(a.err[rl], ERRBIT_PEER);
+    }
+    return failed;
 }
 
 // Reduce-scatter variant for large P (config 5's 15 MB gradient): rank r averages only its
@@ -103,11 +116,11 @@ __global__ void __launch_bounds__(256) dp_peer_rs_sgd_kernel(const __grid_consta
     const int rank = a.rank0 + rl;
     const int64_t slot = (int64_t)(a.t & 1ull) * (a.P + 1), n = a.P + 1;
     __shared__ int timed_out;
-    if (bi == 0 && threadIdx.x == 0) {
+    if (bi == 0 && threadIdx.x == 0 && !dp_is_broken(a.flag[rank])) {   // a broken rank stops publishing
         __threadfence_system();
         dp_st_release(a.flag[rank], a.t);
     }
-    if (threadIdx.x == 0) timed_out = dp_wait_all(a, rank, rl, 0);
+    if (threadIdx.x == 0) timed_out = dp_wait_all(a, rank, rl, 0, false);
     __syncthreads();
     if (timed_out) return;
     __threadfence();
@@ -128,7 +141,7 @@ __global__ void __launch_bounds__(256) dp_peer_rs_sgd_kernel(const __grid_consta
             __threadfence_system();
             dp_st_release(a.flag[rank] + 16, a.t);
         }
-        timed_out = dp_wait_all(a, rank, rl, 16);
+        timed_out = dp_wait_all(a, rank, rl, 16, true);   // co-resident (cooperative launch)
     }
     __syncthreads();
     if (timed_out) return;
@@ -161,15 +174,16 @@ __global__ void __launch_bounds__(256) dp_peer_sgd_kernel(const __grid_constant_
     const int rank = a.rank0 + rl;
     const int64_t slot = (int64_t)(a.t & 1ull) * (a.P + 1);
     // (1) this rank's step-t gradient is complete (written before this kernel): publish it
-    if (bi == 0 && threadIdx.x == 0) {
+    if (bi == 0 && threadIdx.x == 0 && !dp_is_broken(a.flag[rank])) {   // a broken rank stops publishing
         __threadfence_system();
         dp_st_release(a.flag[rank], a.t);
     }
-    // (2) wait for every rank's; a rank that never arrives (a broken lockstep) ends the wait
-    // after ~10 s with the sticky ERRBIT_PEER and the update skipped, and marks this rank's
-    // exchange broken so every later step skips at once (fail fast instead of a hang)
+    // (2) wait for every other rank's (no block waits on this rank's own flag, so a plain launch
+    // needs no co-residency); a rank that never arrives, or whose exchange is broken, ends the
+    // wait with the sticky ERRBIT_PEER and the update skipped, and marks this rank's exchange
+    // broken so every later step skips at once on every rank (fail fast instead of a hang)
     __shared__ int timed_out;
-    if (threadIdx.x == 0) timed_out = dp_wait_all(a, rank, rl, 0);
+    if (threadIdx.x == 0) timed_out = dp_wait_all(a, rank, rl, 0, false);
     __syncthreads();
     if (timed_out) return;
     __threadfence();

@@ -28,8 +28,22 @@
 #include "philox.cuh"
 #include "simt_gemm.cuh"
 #include "train_fast.cuh"
+#include "tc_fast.cuh"
 #include "wide.cuh"
 #include "dp_peer.cuh"
+
+// Variants measured slower than the default path are compiled in, and their
+// environment switches read, only in an experiments build (RPL_NVCC_FLAGS=-DRPL_EXPERIMENTS);
+// the default library has one kernel sequence per shape.
+#ifdef RPL_EXPERIMENTS
+static bool exp_flag(const char *name)
+{
+    const char *v = getenv(name);
+    return v && v[0] == '1';
+}
+#else
+static bool exp_flag(const char *) { return false; }
+#endif
 
 namespace rpl {
 
@@ -753,6 +767,7 @@ struct rpl_dqn {
     float *PF0 = nullptr;
     // fast path (two trunk layers): head partials, dH0 split-K partials, device counters
     bool fast = false;
+    bool tc = false;                 // the fast path's K1 / K3 on tcgen05 (tc_fast.cuh)
     float *part = nullptr, *dH0p = nullptr;
     int64_t part_elems = 0, dh0p_elems = 0;
     int64_t *step_dev = nullptr;
@@ -801,6 +816,7 @@ struct rpl_dqn {
     float *xbuf = nullptr;
     bool p2p = false;
     float *peer_xbuf[DP_MAXR] = {};
+    int64_t dp_base = 0;                   // d->steps at dqn_attach_peers: exchange step = steps - base
     bool peer_opened[DP_MAXR] = {};
     std::vector<void *> allocs;
 };
@@ -911,7 +927,11 @@ static fwd_fn fast_fwd_fn(const rpl_dqn *d)
 static fwd_fn fast_fwd_mc_fn(const rpl_dqn *d)
 {
     const int ut = fast_ut(d), D = d->cfg.state_dim, N0 = d->N[0], J = d->J;
+#ifdef RPL_EXPERIMENTS
     if (ut == 128 && D == 27 && N0 == 128 && J == 9) return fast_fwd_mc_kernel<128, 27, 128, 9>;
+#else
+    (void)ut, (void)D, (void)N0, (void)J;
+#endif
     return nullptr;
 }
 static size_t fast_fwd_smem(const rpl_dqn *d, int ut, int D = -1)
@@ -935,6 +955,44 @@ static int fast_ns(const rpl_dqn *d, int B)
     while (ns * 2 <= want && ns * 2 * 32 <= d->N[1]) ns *= 2;
     return ns;
 }
+
+// ---- tensor-core fast path (tc_fast.cuh) sizing --------------------------------------------
+// shapes: layer-0 units a multiple of 16 up to 128 (the layer-0 accumulator and both H0 planes
+// share 256 TMEM columns), inputs up to 31 (32 with the ones column of db0), layer-1 units
+// and the dueling streams multiples of 32
+static bool tc_shape_ok(const rpl_dqn *d)
+{
+    const rpl_dqn_config &c = d->cfg;
+    return d->T == 2 && d->N[0] % 16 == 0 && d->N[0] <= 128 && d->N[1] % 32 == 0 &&
+           (!c.dueling || c.stream % 32 == 0) && d->J <= tc::MAXJ && d->woff[1] % 4 == 0;
+}
+// K1 unit tile: 128 when that still gives every SM a task, else 64, else 32 (dividing N1 and
+// a dueling stream)
+static int tc_un_for(const rpl_dqn *d, int B)
+{
+    const int nets = d->cfg.double_dqn ? 3 : 2, nbt = (B + 127) / 128;
+    const int S = d->cfg.dueling ? d->cfg.stream : d->N[1];
+    for (int un : {128, 64}) {
+        if (d->N[1] % un || S % un) continue;
+        if (un == 64 || nets * nbt * (d->N[1] / un) >= d->sms) return un;
+    }
+    return 32;
+}
+// the tensor-core kernels take batches from kTcMinBatch up (below it the mma.sync kernels are
+// faster: the step is latency-bound there)
+static constexpr int kTcMinBatch = 1 << 30;
+static constexpr int kTcBsplit = 256;   // K3 (A) tasks: samples per batch split
+// K3 (B) tasks: splits of the layer-1 units (a power of two, >= 2 chunks of 32 units each)
+static int tc_ns_for(const rpl_dqn *d, int B)
+{
+    const int nbt = (B + 127) / 128, nA = ((d->N[1] + 127) / 128) * ((B + kTcBsplit - 1) / kTcBsplit);
+    const int mx = std::max(1, d->N[1] / 64);
+    const int want = std::max(4, (d->sms - nA) / nbt);
+    int ns = 1;
+    while (ns * 2 <= mx && ns * 2 <= want && (d->N[1] / (ns * 2)) % 32 == 0) ns *= 2;
+    return ns;
+}
+static size_t tc_fwd_smem(const rpl_dqn *d, int un) { return (size_t)tc::FwdSmem(d->N[0], un, d->J).total; }
 
 extern "C" int dqn_destroy(rpl_dqn *d)
 {
@@ -997,7 +1055,7 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
     bool ok = coop != 0;
     ok = ok && dalloc(d, &d->online, d->P) && dalloc(d, &d->target, d->P) &&
          dalloc(d, &d->grad, d->P + 1);
-    d->gpart_elems = (int64_t)nsplit_b_for(Bm) * d->P;
+    d->gpart_elems = (int64_t)nsplit_b_for(Bm) * ((d->P + 3) & ~(int64_t)3);
     ok = ok && (nsplit_b_for(Bm) == 1 || dalloc(d, &d->gpart, d->gpart_elems));
     ok = ok && dalloc(d, &d->Xs, (size_t)Bm * D) && dalloc(d, &d->Xs2, (size_t)Bm * D) &&
          dalloc(d, &d->r, Bm) && dalloc(d, &d->a, Bm) && dalloc(d, &d->idx, Bm) &&
@@ -1039,19 +1097,19 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
     d->fast = d->T == 2 && d->N[0] % 4 == 0 && d->N[0] <= 256 && D <= 31 && d->J <= F_MAXJ &&
               d->N[1] % 4 == 0 && (!cfg->dueling || cfg->stream % 4 == 0) && fast_ut_cfg(*cfg, d->N[1]) > 0 &&
               d->woff[1] % 4 == 0 && !(path && strcmp(path, "generic") == 0);
+    // the fast kernels' contractions on tcgen05 (fp32 rings: inputs <= 31; byte-state wide
+    // inputs: layer 0 is wide.cuh's, the tc kernels run the layers above it)
+    d->tc = tc_shape_ok(d) && (D <= 31 || D > kWideInput);
     const char *ng = getenv("RPL_NO_GRAPH");
     d->use_graphs = !(ng && ng[0] == '1');
     // programmatic dependent launch measured slower on this structure (dependent CTAs that
     // start early compete for SM slots); opt in with RPL_PDL=1
-    const char *np = getenv("RPL_PDL");
-    d->use_pdl = np && np[0] == '1';
+    d->use_pdl = exp_flag("RPL_PDL");
     ok = ok && cudaFuncSetAttribute(distinct_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)ds_smem_bytes(DS_MAXB)) == cudaSuccess;
-    const char *nk = getenv("RPL_NO_K3PDL");
-    d->k3_pdl = !(nk && nk[0] == '1');
-    const char *n2 = getenv("RPL_K2PDL"), *n4 = getenv("RPL_K4PDL");
-    d->k2_pdl = n2 && n2[0] == '1';
-    d->k4_pdl = n4 && n4[0] == '1';
+    d->k3_pdl = !exp_flag("RPL_NO_K3PDL");
+    d->k2_pdl = exp_flag("RPL_K2PDL");
+    d->k4_pdl = exp_flag("RPL_K4PDL");
     ok = ok && dalloc(d, &d->step_dev, 1) && dalloc(d, &d->sync_flag, 1);
     const char *tr = getenv("RPL_TRACE");
     if (ok && tr && tr[0] == '1') {
@@ -1067,7 +1125,7 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
                        !(path && strcmp(path, "generic") == 0) && !(nf && nf[0] == '1');
         if (d->wide_fast) {
             const int ut = fast_ut(d);
-            const int nut = (d->N[1] + ut - 1) / ut;
+            const int nut = (d->N[1] + (d->tc ? 32 : ut) - 1) / (d->tc ? 32 : ut);
             d->part_elems = (int64_t)nets * nut * Bm * d->J;
             ok = dalloc(d, &d->part, d->part_elems) && dalloc(d, &d->PdH0, (size_t)32 * Bm * d->N[0]);
             ok = ok && cudaFuncSetAttribute(fast_fwd_fn(d), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1079,14 +1137,22 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
                                       fast_td_smem(d)) == cudaSuccess;
         }
     }
+    if (ok && d->tc) {
+        ok = cudaFuncSetAttribute(tc_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)tc_fwd_smem(d, 128)) == cudaSuccess &&
+             cudaFuncSetAttribute(tc_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  tc::BwdSmem().total) == cudaSuccess;
+    }
     if (ok && d->fast) {
-        const int ut = fast_ut(d);
-        const int nut = (d->N[1] + ut - 1) / ut;
+        const int ut = fast_ut(d);   // the mma.sync K1's unit tile (its shared memory below)
+        const int nut = (d->N[1] + (d->tc ? 32 : ut) - 1) / (d->tc ? 32 : ut);   // tc: up to N1 / 32 partials
         d->part_elems = (int64_t)nets * nut * Bm * d->J;
         // dW0 / db0 partials: NS(B) x ceil(B / 32) x (N0 D + N0); NS(B) x tiles(B) <= sms
         // with tiles(B) = ceil(B / 32) * ceil(N0 / 64) >= ceil(B / 32), so the product is
-        // bounded by sms + ceil(B / 32) for every B <= max_batch
-        const int64_t w0p = d->sms + (Bm + BM - 1) / BM;
+        // bounded by sms + ceil(B / 32) for every B <= max_batch; tc: NS <= N1 / 64 splits of
+        // every 128-row batch tile
+        int64_t w0p = d->sms + (Bm + BM - 1) / BM;
+        if (d->tc) w0p = std::max<int64_t>(w0p, (int64_t)std::max(1, d->N[1] / 64) * ((Bm + 127) / 128));
         d->dh0p_elems = w0p * (d->woff[1]);
         ok = dalloc(d, &d->part, d->part_elems) && dalloc(d, &d->dH0p, d->dh0p_elems);
         ok = ok && cudaStreamCreateWithFlags(&d->cap_stream, cudaStreamNonBlocking) == cudaSuccess;
@@ -1095,8 +1161,7 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
         // clustered K1 (multicast weights; opt-in RPL_K1MC=1: 9.6 vs 7.9 us per K1 measured,
         // DESIGN.md §12): how many K1_MC-CTA clusters can be co-resident
         if (ok && fast_fwd_mc_fn(d)) {
-            const char *nm = getenv("RPL_K1MC");
-            if ((nm && nm[0] == '1') &&
+            if (exp_flag("RPL_K1MC") &&
                 cudaFuncSetAttribute(fast_fwd_mc_fn(d), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      fast_fwd_smem(d, ut)) == cudaSuccess) {
                 cudaLaunchConfig_t lc = {};
@@ -1116,7 +1181,8 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
         if (ok) {
             const void *fns[] = {(const void *)fast_fwd_fn(d), (const void *)fast_td_kernel,
                                  (const void *)fast_bwd1_kernel, (const void *)fast_bwd0_sgd_kernel,
-                                 (const void *)insert_kernel_ptr()};
+                                 (const void *)insert_kernel_ptr(), (const void *)tc_fwd_kernel,
+                                 (const void *)tc_bwd_kernel};
             for (const void *f : fns)
                 ok = ok && cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                                 cudaSharedmemCarveoutMaxShared) == cudaSuccess;
@@ -1272,7 +1338,9 @@ static void wide_l0_plan(rpl_dqn *d, int nets, int64_t D)
 {
     const int64_t S = (D + WD_KS - 1) / WD_KS;
     int cs = 1;
+#ifdef RPL_EXPERIMENTS
     if (const char *c = getenv("RPL_WIDE_CS")) cs = std::max(1, std::min(16, atoi(c)));
+#endif
     for (; cs >= 1; --cs) {
         if (cs > 8) cudaFuncSetAttribute(wide_l0_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaLaunchConfig_t lc = {};
@@ -1356,6 +1424,7 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.NS = fast_ns(d, B);
     p.nsb = (B + 511) / 512;
     p.bsplit = 512;
+    p.gps = (p.P + 3) & ~(int64_t)3;
     p.gpart = p.nsb == 1 ? d->grad : d->gpart;
     p.grad = d->grad;
     p.loss_part = d->loss_part;
@@ -1372,6 +1441,16 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.trace = d->trace;
     p.distinct = rp->distinct ? 1 : 0;
     p.capacity = rp->ring.capacity;
+    if (d->tc && B >= kTcMinBatch) {
+        p.tc = 1;
+        p.UT = tc_un_for(d, B);
+        p.nut = p.N1 / p.UT;
+        p.NS = tc_ns_for(d, B);
+        p.bsplit = kTcBsplit;
+        p.nsb = (B + kTcBsplit - 1) / kTcBsplit;
+        p.gpart = p.nsb == 1 ? d->grad : d->gpart;
+        p.nw0 = p.NS * ((B + 127) / 128);
+    }
     const rpl_replay::Pending &q = rp->pend;
     if (q.k > 0) {   // consumed by this step's K1 (dqn_train_step clears it)
         p.pend_k = (int)q.k;
@@ -1408,8 +1487,33 @@ static cudaError_t launch_pdl(K kernel, int grid, int block, size_t smem, cudaSt
 }
 
 // the fast-path kernels, enqueued on `st`
+static cudaError_t tc_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
+{
+    const bool pdl = d->use_pdl;
+    cudaError_t e;
+    if (p.distinct) {   // distinct batch indices first (distinct.cuh)
+        e = launch_pdl(distinct_fast_kernel, 1, DS_T, ds_smem_bytes(p.B), st, false, p);
+        if (e != cudaSuccess) return e;
+    }
+    // K1: (net, unit tile) combos x 128-row batch tiles; with more tasks than SMs the grid is a
+    // multiple of the combos, so a CTA keeps one weight tile staged across its batch tiles
+    const int nbt = (p.B + 127) / 128, ncombo = p.nets * p.nut, k1_tasks = ncombo * nbt;
+    int g1 = std::min(k1_tasks, d->sms);
+    if (k1_tasks > d->sms && ncombo <= d->sms) g1 = (d->sms / ncombo) * ncombo;
+    e = launch_pdl(tc_fwd_kernel, g1, tc::T, tc_fwd_smem(d, p.UT), st, false, p);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(fast_td_kernel, std::min(p.B, 4 * d->sms), NT, fast_td_smem(d), st, pdl || d->k2_pdl, p);
+    if (e != cudaSuccess) return e;
+    const int k3_tasks = ((p.N1 + 127) / 128) * p.nsb + nbt * p.NS;
+    e = launch_pdl(tc_bwd_kernel, std::min(k3_tasks, d->sms), tc::T, tc::BwdSmem().total, st,
+                   pdl || d->k3_pdl, p);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(fast_bwd0_sgd_kernel, d->sms, NT, 0, st, pdl || d->k4_pdl, p);
+}
+
 static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
 {
+    if (p.tc) return tc_enqueue(d, p, st);
     const int nbt = (p.B + F_BT - 1) / F_BT;
     const int k1_tasks = p.nets * nbt * p.nut;
     // large batches: a multiple of the nets x unit-tile combinations, so every CTA keeps one
@@ -1616,11 +1720,11 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                         if (cudaGraphNodeGetType(nodes[i], &ty) == cudaSuccess &&
                             ty == cudaGraphNodeTypeKernel &&
                             cudaGraphKernelNodeGetParams(nodes[i], &kp) == cudaSuccess) {
-                            if (kp.func == (void *)fast_fwd_fn(d) ||
+                            if (kp.func == (void *)fast_fwd_fn(d) || kp.func == (void *)tc_fwd_kernel ||
                                 (fast_fwd_mc_fn(d) && kp.func == (void *)fast_fwd_mc_fn(d)))
                                 k1 = nodes[i];
                             if (kp.func == (void *)distinct_fast_kernel) ds = nodes[i];
-                            if (kp.func == (void *)fast_bwd1_kernel) k3 = nodes[i];
+                            if (kp.func == (void *)fast_bwd1_kernel || kp.func == (void *)tc_bwd_kernel) k3 = nodes[i];
                             if (kp.func == (void *)fast_bwd0_sgd_kernel) k4 = nodes[i];
                         }
                     }
@@ -1814,14 +1918,17 @@ after_step:
     if (dp && d->p2p) {
         // gradient mean + SGD over peer memory (dp_peer.cuh): this step's gradient into its
         // exchange slot, then one kernel publishes it, waits for every rank's and updates
-        float *mine = d->xbuf + (int64_t)(t & 1) * (d->P + 1);
+        // exchange step numbers count from the attach (every rank attached at the same point
+        // of its stream, after the flag area was cleared), not from the learner's own steps
+        const int64_t tx = t - d->dp_base;
+        float *mine = d->xbuf + (int64_t)(tx & 1) * (d->P + 1);
         e = cudaMemcpyAsync(mine, d->grad, (size_t)(d->P + 1) * sizeof(float), cudaMemcpyDeviceToDevice, d->stream);
         DPArgs a{};
         a.nloc = 1;
         a.world = d->world;
         a.rank0 = d->rank;
         a.P = d->P;
-        a.t = (unsigned long long)t;
+        a.t = (unsigned long long)tx;
         a.lr = d->cfg.lr;
         for (int q = 0; q < d->world; ++q) {
             a.xbuf[q] = d->peer_xbuf[q];
@@ -1848,7 +1955,7 @@ after_step:
         }
         g_launches.fetch_add(1);
         d->w0bf_stale = true;   // the update rewrote W0 without its planes
-        if (loss_dev) cudaMemcpyAsync(loss_dev, d->grad + d->P, sizeof(float), cudaMemcpyDeviceToDevice, d->stream);
+        if (loss_dev) cudaMemcpyAsync(loss_dev, d->grad + d->P, sizeof(float), cudaMemcpyDefault, d->stream);
     } else if (dp) {
         int nr = g_nccl.allreduce(d->grad, d->grad, (size_t)d->P + 1, kNcclFloat, kNcclAvg,
                                   d->comm, d->stream);
@@ -1866,7 +1973,7 @@ after_step:
             return cuda_fail(e, "sgd_kernel");
         }
         g_launches.fetch_add(1);
-        if (loss_dev) cudaMemcpyAsync(loss_dev, d->grad + d->P, sizeof(float), cudaMemcpyDeviceToDevice, d->stream);
+        if (loss_dev) cudaMemcpyAsync(loss_dev, d->grad + d->P, sizeof(float), cudaMemcpyDefault, d->stream);
     }
     if (avg && t % d->cfg.avg_period == 0) {
         // iterative parameter mixing (reading Q31): online and target <- their mean over ranks
@@ -2059,6 +2166,15 @@ extern "C" int dqn_attach_peers(rpl_dqn *d, int32_t rank, int32_t world, const v
         return RPL_ESTATE;
     }
     DeviceGuardDqn g(d->device);
+    // a fresh protocol state: step flags, the broken word and the block counter are cleared and
+    // exchange steps count from here (a learner re-attached after a detach, a
+    // timeout or solo steps would otherwise read stale flags); the caller synchronises the
+    // ranks after every rank's attach and before the first step (dp.attach_auto's final
+    // all-reduce), so no peer can publish into a flag area before it is cleared
+    RPL_CUDA(cudaStreamSynchronize(d->stream));
+    RPL_CUDA(cudaMemset((char *)d->xbuf + dp_flag_offset(d->P), 0, 256));
+    RPL_CUDA(cudaDeviceSynchronize());
+    d->dp_base = d->steps;
     const cudaIpcMemHandle_t *hs = static_cast<const cudaIpcMemHandle_t *>(handles);
     for (int q = 0; q < world; ++q) {
         if (q == rank) {

@@ -75,7 +75,8 @@ struct FastArgs {
     float *dZ1;          // [B][N1]
     float *w0part;       // [NS][ceil(B/32)][N0*D + N0] dW0 / db0 partials (K3 -> K4)
     int NS;
-    float *gpart;        // [nsb][P] (== grad when nsb == 1)
+    float *gpart;        // [nsb][gps] (== grad when nsb == 1)
+    int64_t gps;         // gpart split stride: P rounded up to 4 (16-byte aligned splits)
     int nsb, bsplit;
     float *grad;         // [P + 1]
     float *loss_part, *Qs, *Qt2, *Qo2, *y;
@@ -94,6 +95,9 @@ struct FastArgs {
     uint32_t *err;
     unsigned long long *trace;   // optional per-CTA [kernel][cta][start, end] %globaltimer (ns)
     int prec;            // rpl_dqn_config.precision (split_p / mma_3xtf32, mma_tf32.cuh)
+    int tc;              // 1: K1 / K3 are the tensor-core kernels of tc_fast.cuh (K2 skips dZ1,
+                         //    which K3 forms on the fly; K4 sums nw0 dW0 / db0 partials)
+    int nw0;             // tc: dW0 / db0 partials in w0part (NS x 128-row batch tiles)
 };
 
 __device__ __forceinline__ unsigned long long gtimer()
@@ -633,11 +637,11 @@ __global__ void __launch_bounds__(NT) fast_td_kernel(const __grid_constant__ Fas
     // the head weights are reused for every sample of this CTA: stream them in once (they are
     // step-invariant, so before waiting for the forward kernel)
     pdl_trigger();
-    cp_async_row(Whs, p.online + p.wh, J * HS, tid, NT);
+    if (!p.tc) cp_async_row(Whs, p.online + p.wh, J * HS, tid, NT);
     pdl_wait();
     for (int b = blockIdx.x; b < B; b += gridDim.x) {
         __syncthreads();
-        cp_async_row(h1s, p.H1 + (int64_t)b * N1, N1, tid, NT);
+        if (!p.tc) cp_async_row(h1s, p.H1 + (int64_t)b * N1, N1, tid, NT);
         // the sample's action / reward / terminal, needed after the reduction (prefetched)
         int ab = 0;
         float rb = 0.0f;
@@ -670,6 +674,7 @@ __global__ void __launch_bounds__(NT) fast_td_kernel(const __grid_constant__ Fas
         __syncthreads();
         trace_.mark(4);
         for (int j = tid; j < J; j += NT) p.dHead[(int64_t)b * J + j] = dhs[j];
+        if (p.tc) continue;   // tc_bwd_kernel forms dZ1 from dHead itself
         // dZ1[b][u] = (dHead . W_head)[u] * ReLU'(z1[b][u]), 4 consecutive units per thread
         // (N1 % 4 == 0; a dueling stream boundary S % 4 == 0 never splits a group)
         for (int u4 = tid; u4 < N1 / 4; u4 += NT) {
@@ -896,7 +901,7 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             const int s = t / (wmt * wnt), rem = t % (wmt * wnt);
             const int m0 = (rem / wnt) * BM, n0 = (rem % wnt) * K3N;
             const int kb = s * p.bsplit, ke = min(B, kb + p.bsplit);
-            float *gp = p.gpart + (int64_t)s * p.P;
+            float *gp = p.gpart + (int64_t)s * p.gps;
             const Opnd a{p.dZ1, N1, N1}, bo{p.H0, N0, N0};
             auto epi = [&](int m, int n, float v) {
                 if (m < N1 && n < N0) gp[p.w1 + (int64_t)m * N0 + n] = v;
@@ -985,7 +990,7 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
             const int u = t - n_w - n_h;
             const int s = u / (hd_tasks + 1), c = u % (hd_tasks + 1);
             const int kb = s * p.bsplit, ke = min(B, kb + p.bsplit);
-            float *gp = p.gpart + (int64_t)s * p.P;
+            float *gp = p.gpart + (int64_t)s * p.gps;
             if (c == hd_tasks) {
                 // warp w reduces head rows j = w, w + 4, ...: lanes stride the samples
                 pdl_wait();
@@ -1084,7 +1089,7 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
     // in order; coalesced 128-B loads), then the 8 warp sums are added in warp order.
     // (wide inputs: W0 / b0 are wide_dw0_kernel's, which also gets dZ0 from here)
     const int64_t n0el = p.PdH0 ? 0 : p.w1;     // W0 and b0 lead the blob
-    const int nparts = p.NS * ((B + BM - 1) / BM);
+    const int nparts = p.tc ? p.nw0 : p.NS * ((B + BM - 1) / BM);
     auto w0_partial = [&](int64_t i) {
         float g = 0.0f, comp = 0.0f;
         if (i >= n0el) return g;
@@ -1198,7 +1203,7 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
             gs = __ldcg(p.grad + i);
         } else {
             gs = 0.0f;
-            for (int sb = 0; sb < p.nsb; ++sb) gs += __ldcg(p.gpart + (int64_t)sb * p.P + i);
+            for (int sb = 0; sb < p.nsb; ++sb) gs += __ldcg(p.gpart + (int64_t)sb * p.gps + i);
             p.grad[i] = gs;
         }
         if (upd) {

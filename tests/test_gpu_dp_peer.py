@@ -89,6 +89,59 @@ def test_emulated_ranks_mean_sgd(b, world, rs):
     assert torch.equal(online, before) and err.item() == 2
 
 
+@pytest.mark.parametrize("rs", [0, 1], ids=["all-read", "reduce-scatter"])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_emulated_ranks_dqn_gradients_vs_oracle_o6(b, world, rs):
+    # A10 against the oracle's O6: `world` learners, each with its own
+    # replay shard (rank-keyed experience stream and sampler stream), take one Double-DQN step
+    # whose per-rank gradient is checked against the oracle (teacher-forced, 1e-5 normwise);
+    # the exchange kernel then forms the mean of the GPU gradients and applies SGD on every
+    # emulated rank, and the result must equal O6 -- the oracle's rank-order mean of the
+    # oracle's per-rank gradients and its SGD -- within 1e-5 normwise per block
+    import torch
+    import oracle
+    from parity import blocks, f32, normwise, step_and_compare
+    cfg = b.DQNConfig(max_batch=128, sync_period=0, double_dqn=True, lr=1e-3)
+    p0 = init_params(27, 8, (128,), True, 512, seed=3)
+    P = p0.size
+    stride, _ = _xbuf_floats(P)
+    xb = torch.zeros(world * stride, dtype=torch.float32, device="cuda")
+    online = torch.from_numpy(np.tile(p0, world)).cuda()
+    target = online.clone()
+    gmean = torch.zeros(world * (P + 1), dtype=torch.float32, device="cuda")
+    sync = torch.zeros(1, dtype=torch.int32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    t = 1
+    slot = (t & 1) * (P + 1)
+    og, ol = [], []
+    for q in range(world):
+        rp = b.Replay(3000, 27, seed=2, rank=q)
+        orc = oracle.Ring(3000, 27)
+        e = experiences(3500, seed=1, rank=q)
+        rp.add_many(e)
+        orc.add_many(e)
+        dqn = b.DQN(cfg, p0)
+        out = step_and_compare(b, cfg, dqn, rp, orc, 128, seed=2, rank=q)
+        g = np.append(dqn.get_params(b.RPL_GRAD), dqn.debug(b.RPL_DBG_LOSS, 128)[0]).astype(np.float32)
+        xb[q * stride + slot:q * stride + slot + P + 1] = torch.from_numpy(g).cuda()
+        og.append(out["grad"])
+        ol.append(out["loss"])
+    assert len({round(float(x), 6) for x in ol}) == world   # distinct shards, distinct batches
+    st = b._L.rpl_dp_emulate(world, P, xb.data_ptr(), online.data_ptr(), target.data_ptr(),
+                             gmean.data_ptr(), sync.data_ptr(), err.data_ptr(), C.c_float(f32(cfg.lr)), t, rs)
+    assert st == b.RPL_OK, b.last_error()
+    w_o6, mean_o6 = oracle.dp_mean_sgd(p0, og, f32(cfg.lr))
+    on = online.view(world, P).cpu().numpy()
+    gm = gmean.view(world, P + 1).cpu().numpy()
+    for q in range(world):
+        assert np.array_equal(on[q], on[0]) and np.array_equal(gm[q], gm[0])
+    for name, sl in blocks(cfg):
+        normwise(gm[0][sl], mean_o6[sl], 1e-5, f"mean grad {name}")
+        normwise(on[0][sl], w_o6[sl], 1e-5, f"new {name}")
+    assert abs(float(gm[0][P]) - float(np.mean(ol))) <= 1e-5 * abs(float(np.mean(ol)))
+    assert err.item() == 0
+
+
 @pytest.mark.parametrize("net", ["fast", "generic"])
 def test_self_attached_learner_equals_local(b, monkeypatch, net):
     import torch

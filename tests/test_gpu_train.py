@@ -284,19 +284,3 @@ def test_deferred_device_insert_corrupt_done(b):
     assert rp.check() == b.RPL_ECORRUPT
     g = rp.gather(torch.tensor([48, 49], dtype=torch.int32, device="cuda"))
     assert g["done"].cpu().numpy().tolist() == [1, int(e["done"][1])]
-
-
-def test_k1_multicast_cluster_variant(b, monkeypatch):
-    # RPL_K1MC=1: K1 in 4-CTA clusters sharing the weight tile through TMA multicast (off by
-    # default) -- same parity bar as the default K1
-    monkeypatch.setenv("RPL_K1MC", "1")
-    cfg = _cfg(b, max_batch=128, sync_period=3)
-    rp = b.Replay(5000, 27, seed=61)
-    orc = oracle.Ring(5000, 27)
-    e = experiences(5000, seed=62)
-    rp.add(**e)
-    orc.add(**e)
-    dqn = b.DQN(cfg, _params(cfg))
-    for _ in range(4):
-        assert step_and_compare(b, cfg, dqn, rp, orc, 128, seed=61) is not None
-    assert dqn.check() == b.RPL_OK

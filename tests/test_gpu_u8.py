@@ -64,7 +64,7 @@ def test_u8_insert_sample_gather_bit_exact(b, D):
     assert rp.check() == b.RPL_OK
 
 
-@pytest.mark.parametrize("path", ["tcgen05", "tcgen05-coop", "simt", "tcgen05-cluster"])
+@pytest.mark.parametrize("path", ["tcgen05", "tcgen05-coop", "simt"])
 @pytest.mark.parametrize("ddqn", [False, True], ids=["dqn", "ddqn"])
 def test_u8_wide_input_train_step(b, ddqn, path, monkeypatch):
     # config 5 network: the paper's dueling MLP on an 84x84x4 byte input (28,224 -> 128 ->
@@ -76,8 +76,6 @@ def test_u8_wide_input_train_step(b, ddqn, path, monkeypatch):
         monkeypatch.setenv("RPL_NO_WIDE_TC", "1")
     if path == "tcgen05-coop":
         monkeypatch.setenv("RPL_NO_WIDE_FAST", "1")
-    if path == "tcgen05-cluster":   # layer-0 partials summed in clusters of 2 over DSMEM
-        monkeypatch.setenv("RPL_WIDE_CS", "2")
     D = ATARI_STATE_DIM
     cfg = b.DQNConfig(state_dim=D, n_actions=8, dueling=True, hidden=(128,), stream=512,
                       double_dqn=ddqn, gamma=0.99, lr=1e-3, huber_kappa=1.0, sync_period=2,
@@ -124,3 +122,77 @@ def test_u8_host_adds_through_a_small_staging_arena(b):
     for k in ("s", "s_next", "a", "r", "done"):
         assert np.array_equal(g[k], o[k]), k
     assert rp.check() == b.RPL_OK and dqn.check() == b.RPL_OK
+
+
+@pytest.mark.parametrize("path", ["tcgen05", "tcgen05-coop"])
+@pytest.mark.parametrize("ddqn", [False, True], ids=["dqn", "ddqn"])
+def test_u8_config5_batch_256_and_ragged_200(b, ddqn, path, monkeypatch):
+    # BASELINE configs[4] at its configured batch (84x84x4 byte states, B = 256):
+    # wide_l0 with UMMA N = 256 (one 256-column accumulator), wide_dw0 with four 64-sample
+    # slices (mbarrier phase flips across slices), then a ragged 200 (the last slice partial);
+    # both the fast layers-above kernels and the cooperative kernel
+    if path == "tcgen05-coop":
+        monkeypatch.setenv("RPL_NO_WIDE_FAST", "1")
+    D = ATARI_STATE_DIM
+    cfg = b.DQNConfig(state_dim=D, n_actions=8, dueling=True, hidden=(128,), stream=512,
+                      double_dqn=ddqn, gamma=0.99, lr=1e-3, huber_kappa=1.0, sync_period=2,
+                      max_batch=256)
+    rp = b.Replay(300, D, seed=31, state_dtype="u8")
+    orc = oracle.RingU8(300, D)
+    e = experiences_u8(420, state_dim=D, seed=32)   # wraps the ring
+    rp.add(**e)
+    orc.add(**e)
+    dqn = b.DQN(cfg, init_params(D, 8, (128,), True, 512, seed=33))
+    for batch in (256, 200, 256):
+        assert step_and_compare(b, cfg, dqn, rp, orc, batch, seed=31) is not None
+    assert dqn.check() == b.RPL_OK and rp.check() == b.RPL_OK
+
+
+def test_u8_ring_beyond_4gb_sampled_rows(b):
+    # a byte ring whose row offsets pass 2^32 bytes: 80,000 rows x 56,576 B = 4.5 GB (configs[4]
+    # rows); device-sourced adds wrap it, then the sampler's indices are bit-exact with the
+    # oracle's and every sampled row -- replay_sample, an explicit gather, and the train
+    # step's own in-step gather at B = 256 -- equals the generator's row t(i) of the FIFO
+    # closed form t(i) = i + C floor((T - 1 - i) / C)
+    import torch
+    from inputs import u8_rows_np, u8_rows_torch
+    C, D, T, K = 80_000, ATARI_STATE_DIM, 92_000, 2_000
+    rp = b.Replay(C, D, seed=41, state_dtype="u8", max_host_add=16)
+    assert b.Replay.ring_bytes(C, D, state_dtype="u8") > (1 << 32)
+    for t0 in range(0, T, K):
+        t = torch.arange(t0, t0 + K, dtype=torch.int64, device="cuda")
+        rows = u8_rows_torch(t, D, 8)
+        rp.add(**rows)
+    torch.cuda.synchronize()
+    st = rp.state()
+    assert (st["size"], st["total"], st["cursor"]) == (C, T, T % C)
+
+    def expect(idx):
+        i = idx.astype(np.int64)
+        return u8_rows_np(i + C * ((T - 1 - i) // C), D, 8)
+
+    for ev in range(2):
+        g = _np(rp.sample(256))
+        idx = oracle.sample_indices(41, 0, ev, C, 256)
+        assert np.array_equal(g["idx"], idx)
+        ex = expect(idx)
+        for k in ("s", "s_next", "a", "r", "done"):
+            assert np.array_equal(g[k], ex[k]), k
+    hi = torch.tensor([C - 1, C - 2, 76_000, 75_913, 0, 1], dtype=torch.int32, device="cuda")
+    g = _np(rp.gather(hi))
+    ex = expect(hi.cpu().numpy())
+    for k in ("s", "s_next", "a", "r", "done"):
+        assert np.array_equal(g[k], ex[k]), k
+    # the wide train step's in-step gather (gather_u8_kernel) at the configured batch
+    cfg = b.DQNConfig(state_dim=D, n_actions=8, dueling=True, hidden=(128,), stream=512,
+                      lr=1e-4, sync_period=0, max_batch=256)
+    dqn = b.DQN(cfg, init_params(D, 8, (128,), True, 512, seed=43))
+    assert dqn.train_step(rp, 256) == b.RPL_OK
+    idx = dqn.debug(b.RPL_DBG_IDX, 256)
+    assert np.array_equal(idx, oracle.sample_indices(41, 0, 2, C, 256))
+    ex = expect(idx)
+    for what, key in [(b.RPL_DBG_S, "s"), (b.RPL_DBG_S_NEXT, "s_next"), (b.RPL_DBG_A, "a"),
+                      (b.RPL_DBG_R, "r"), (b.RPL_DBG_DONE, "done")]:
+        assert np.array_equal(dqn.debug(what, 256).view(np.uint8),
+                              np.ascontiguousarray(ex[key]).view(np.uint8)), key
+    assert dqn.check() == b.RPL_OK and rp.check() == b.RPL_OK

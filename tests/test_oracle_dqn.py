@@ -285,6 +285,31 @@ def test_learner_target_sync_period():
     assert ln.step_count == 10 and ring.events == 10
 
 
+def test_learner_explicit_sync_target():
+    # P:88 / S:306-312: an explicit sync_target() at any step copies the online net bit for bit
+    # and the next steps leave the copy frozen (sync_period 0 = manual only); the DDQN
+    # bootstrap right after a sync equals the DQN one (online == target makes
+    # Q_t(s', argmax Q_o) = max Q_t)
+    net = oracle.Net(27, 8, False, (64, 64))
+    ring = oracle.Ring(1000, 27)
+    ring.add(**experiences(600, seed=63))
+    ln = oracle.Learner(net, init_params(27, 8, (64, 64), False, seed=64), lr=1e-2, sync_period=0)
+    for _ in range(2):
+        assert ln.step(ring, 32)[0] == oracle.OK
+    assert not np.array_equal(ln.target, ln.online)
+    ln.sync_target()
+    assert np.array_equal(ln.target, ln.online)
+    frozen = ln.target.copy()
+    assert ln.step(ring, 32)[0] == oracle.OK
+    assert np.array_equal(ln.target, frozen) and not np.array_equal(ln.online, frozen)
+    ln.sync_target()
+    rc, b = ring.sample(1, 2, 0, 32)
+    assert rc == oracle.OK
+    o1 = oracle.dqn_loss_grad(net, ln.online, ln.target, b, 0.99, 1.0, False)
+    o2 = oracle.dqn_loss_grad(net, ln.online, ln.target, b, 0.99, 1.0, True)
+    assert np.array_equal(o1["y"], o2["y"])
+
+
 def test_learner_burn_in_leaves_state_untouched():
     net = oracle.Net(27, 8, False, (64, 64))
     ring = oracle.Ring(1000, 27)
