@@ -64,9 +64,11 @@ def parse():
                          "default: the north star's path), or by the peer-memory mean + SGD "
                          "kernel (dqn_attach_peers) when every rank's GPU can map every other's "
                          "(auto), or always (p2p)")
-    ap.add_argument("--ring", choices=["device", "host"], default="device",
-                    help="host: the in-RAM comparison mode (SURVEY NEXT-1): ring rows in pinned host "
-                         "memory, every batch read across PCIe by the same kernels")
+    ap.add_argument("--ring", choices=["device", "host", "host_batch"], default="device",
+                    help="host_batch: the paper's in-RAM replay (SURVEY NEXT-1; P:15, P:50): CPU ring, "
+                         "CPU sampler and gather, one H2D batch copy per step into the same kernels; "
+                         "host: its zero-copy variant (ring rows in pinned host memory read across "
+                         "PCIe by the kernels)")
     ap.add_argument("--config", choices=["c2", "c5"], default="c2",
                     help="c2: BASELINE configs[1] (default); c5: configs[4] 84x84x4 uint8 states, "
                          "batch 256 (other flags' defaults: --batch 256)")
@@ -85,8 +87,9 @@ def workload_name(a, batch):
     net = ("dueling DQN 27-128-[V512|A512]-1+8 (P:92-94)" if a.net == "dueling"
            else "2x64 MLP 27-64-64-8")
     tgt = "Double-DQN" if a.ddqn else "DQN"
-    where = (", ring rows in pinned host memory read across PCIe (in-RAM comparison mode)"
-             if a.ring == "host" else "")
+    where = {"host": ", ring rows in pinned host memory read across PCIe (zero-copy in-RAM variant)",
+             "host_batch": ", the paper's in-RAM replay: CPU ring + CPU sampler/gather, one H2D batch "
+                           "copy per step (P:15, P:50)"}.get(a.ring, "")
     return (f"BASELINE configs[1]: {a.capacity:,}-slot replay of 27-float states, batch {batch}, "
             f"{net}, {tgt} target, Huber, SGD, {a.adds_per_step} inserts/step{where}")
 
@@ -425,7 +428,10 @@ def run_ours(a, batch, first_line=True):
     def add_dev(i):
         if k:
             j = (i % 256) * k
-            rp.add(**{kk: v[j:j + k] for kk, v in pool_d.items()}, defer=True)
+            if a.ring == "host_batch":   # the in-RAM replay takes host inputs (CPU-written rows)
+                rp.add(**{kk: v[j:j + k] for kk, v in pool_h.items()})
+            else:
+                rp.add(**{kk: v[j:j + k] for kk, v in pool_d.items()}, defer=True)
 
     clk = ClockSampler(local).start()   # before the warm-up, so a short timed region is covered
     for i in range(W):
@@ -509,7 +515,7 @@ def run_ours(a, batch, first_line=True):
 
     # ---- gather bandwidth (metric part 2): explicit-index gather from the 1M ring --------
     gather = None
-    if not a.no_gather and first_line:
+    if not a.no_gather and first_line and a.ring != "host_batch":
         n_idx = 1 << 22
         idx = torch.randint(0, a.capacity, (n_idx,), dtype=torch.int32, device=dev)
         out = {"s": torch.empty(n_idx, 27, device=dev), "s_next": torch.empty(n_idx, 27, device=dev),
@@ -553,48 +559,56 @@ def run_ours(a, batch, first_line=True):
                           "GBps": m * (ROW_READ_BYTES + ROW_WRITE_BYTES) / (t_ms / 1000.0) / 1e9})
         gather["sweep"] = sweep
         rp.check()
-        # insert cost vs block size k (the B200 version of P:119-125, Fig. 3),
-        # host-sourced (one pinned H2D copy inside replay_add) and device-sourced
+        # insert cost vs block size k (the B200 version of P:119-125, Fig. 3):
+        # replay_add timed inside the library (rpl_time_adds: no binding overhead per call),
+        # host-sourced from pageable numpy (copied into pinned staging), from pinned memory (the
+        # insert kernel reads it across PCIe, no staging copy, for k > 4096) and device-sourced;
+        # the device rows also give the insert kernel's HBM rate (CUDA events around the calls)
         ins = []
-        big = experiences(10_000, seed=13, rank=rank)
-        big_d = {kk: torch.from_numpy(v).to(dev) for kk, v in big.items()}
-        for kk_ in (1, 10, 100, 2000, 10_000):
+        kmax = min(1_000_000, a.capacity)
+        big = experiences(kmax, seed=13, rank=rank)
+        big_p = {kk: torch.from_numpy(v).pin_memory() for kk, v in big.items()}
+        big_d = {kk: v.to(dev) for kk, v in big_p.items()}
+        for kk_ in (1, 10, 100, 2000, 10_000, 100_000, kmax):
             row = {"k": kk_}
-            for src, pool in (("host", big), ("device", big_d)):
+            n_calls = max(3, min(2000, 2_000_000 // (kk_ * 10)))
+            for src, pool in (("host", big), ("pinned", big_p), ("device", big_d)):
+                if src == "host" and kk_ > 65_536:   # pageable adds go through the 64K staging
+                    continue
                 part = {kx: v[:kk_] for kx, v in pool.items()}
-                for _ in range(3):
-                    rp.add(**part)
-                reps_i = 20
+                rp.time_adds(part, 2)
                 torch.cuda.synchronize()
-                t0 = time.perf_counter()
                 gs.record(stream)
-                for _ in range(reps_i):
-                    rp.add(**part)
+                sec = rp.time_adds(part, n_calls)
                 ge.record(stream)
                 torch.cuda.synchronize()
-                wall = (time.perf_counter() - t0) / reps_i
-                dev_s = gs.elapsed_time(ge) / 1000.0 / reps_i
-                t = max(wall, dev_s)
+                t = max(sec, gs.elapsed_time(ge) / 1000.0) / n_calls
                 row[f"{src}_us_per_experience"] = t * 1e6 / kk_
                 row[f"{src}_GBps"] = kk_ * EXP_INPUT_BYTES / t / 1e9
+            # device-sourced: bytes the insert kernel moves (inputs read + 228 B algorithmic
+            # row written) over the per-call time, against the HBM peak
+            row["device_hbm_GBps"] = kk_ * (EXP_INPUT_BYTES + ROW_READ_BYTES) / (
+                row["device_us_per_experience"] * kk_ * 1e-6) / 1e9
+            row["device_hbm_frac"] = row["device_hbm_GBps"] / peaks["hbm_gbs"]
             ins.append(row)
         gather["insert_sweep"] = ins
+        gather["insert_note"] = ("per-call time of replay_add from rpl_time_adds (C loop + stream sync, "
+                                 "max of host wall and CUDA-event time); host = pageable numpy (memcpy "
+                                 "into pinned staging, then H2D / zero-copy), pinned = torch pinned "
+                                 "tensors (k > 4096: the insert kernel reads them across PCIe); GBps = "
+                                 f"{EXP_INPUT_BYTES} input bytes per experience / time; device_hbm = "
+                                 f"({EXP_INPUT_BYTES} read + {ROW_READ_BYTES} row bytes written) / time")
+        del big_p, big_d
         rp.check()
         # P:73 / Fig. 3 proper: single host experiences through the update-size queue
-        # (update_size U): wall time per replay_add call, block transfers included
+        # (update_size U): per replay_add call, block transfers included, timed in the library
         upd = []
-        one = experiences(20_000, seed=14, rank=rank)
+        one = experiences(1, seed=14, rank=rank)
         for U in (1, 10, 100, 2000, 10_000):
             rq = binding.Replay(20_000, 27, device=local, update_size=U)
-            rows = [{kx: v[i:i + 1] for kx, v in one.items()} for i in range(20_000)]
-            for i in range(2000):
-                rq.add(**rows[i])
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            for i in range(20_000):
-                rq.add(**rows[i])
-            torch.cuda.synchronize()
-            upd.append({"update_size": U, "us_per_add": (time.perf_counter() - t0) / 20_000 * 1e6})
+            rq.time_adds(one, 2000)
+            sec = rq.time_adds(one, 20_000)
+            upd.append({"update_size": U, "us_per_add": sec / 20_000 * 1e6})
             rq.close()
         gather["update_size_sweep"] = upd
 
@@ -621,7 +635,9 @@ def run_ours(a, batch, first_line=True):
                    "net": a.net, "double_dqn": a.ddqn, "adds_per_step": k,
                    "sampling": "distinct" if a.distinct else "uniform (with replacement, P:75)",
                    "state_storage": "shared (s' = next slot's s, P:141)" if a.shared_state else "s and s' per row",
-                   "ring_memory": "host (pinned, read across PCIe: in-RAM comparison)" if a.ring == "host" else "device (HBM)",
+                   "ring_memory": {"host": "host (pinned, read across PCIe: zero-copy in-RAM variant)",
+                                   "host_batch": "host (pageable; CPU sample + gather, one H2D batch copy "
+                                                 "per step: the paper's in-RAM replay)"}.get(a.ring, "device (HBM)"),
                    "parallelism": f"dp{world}" + (f", parameters averaged every {a.avg_period} steps"
                                                   if a.avg_period and world > 1 else "")
                                   + (", gradient mean over peer memory" if getattr(a, "dp_used", "") == "p2p"

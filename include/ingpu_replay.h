@@ -50,7 +50,7 @@ enum { RPL_HOST = 0, RPL_DEVICE = 1, RPL_DEVICE_DEFER = 2 };
 enum { RPL_ONLINE = 0, RPL_TARGET = 1, RPL_GRAD = 2 };  /* which parameter vector          */
 enum { RPL_F32 = 0, RPL_U8 = 1 };                        /* state element type of a replay  */
 enum { RPL_SAMPLE_UNIFORM = 0, RPL_SAMPLE_DISTINCT = 1 }; /* sampler of a replay            */
-enum { RPL_RING_DEVICE = 0, RPL_RING_HOST = 1 };          /* where a replay's rows live      */
+enum { RPL_RING_DEVICE = 0, RPL_RING_HOST = 1, RPL_RING_HOST_BATCH = 2 };  /* where rows live */
 enum { RPL_PREC_FP32 = 0, RPL_PREC_TF32 = 1, RPL_PREC_BF16 = 2 };   /* learner precision   */
 
 typedef struct rpl_replay rpl_replay;   /* opaque */
@@ -85,7 +85,18 @@ typedef struct {
                              P:50): the same rows in pinned, device-mapped host
                              memory, so every sample / gather / train step reads its batch
                              across PCIe -- the per-step transfer the in-GPU replay removes.
-                             The kernels, sampler and results are identical              */
+                             The kernels, sampler and results are identical.
+                             RPL_RING_HOST_BATCH: the paper's in-RAM replay itself ("the
+                             RAM variant ... copies sampled batches to the GPU"): rows
+                             in ordinary (pageable) host memory written by the CPU on
+                             replay_add (RPL_HOST inputs only), every replay_sample /
+                             dqn_train_step samples its indices on the CPU (the same Philox
+                             stream), gathers the rows on the CPU into pinned staging and
+                             copies the batch to the GPU in one H2D transfer of
+                             B*(row bytes + 4) bytes (counted in h2d_bytes) before the same
+                             train-step kernels run.  fp32 states, uniform sampling, one
+                             state pair per row, the fast path's net shapes; replay_gather
+                             returns RPL_ESTATE                                              */
     int64_t update_size;  /* 0 (default): every replay_add is one insert, visible at once.
                              U > 0: P:73 block updates ("Experiences are queued in RAM until
                              the queue has enough experiences to update the next block";
@@ -328,6 +339,14 @@ int rpl_check(void *handle, int kind);
 const char *rpl_last_error(void);
 /* Number of kernels this library launched in the calling process (launch accounting). */
 uint64_t rpl_kernel_launches(void);
+
+/* Measurement entry (the B200 version of P:119-125 / Fig. 3, cost per add vs update size):
+ * n_calls consecutive replay_add(replay, k, s, a, r, s_next, done, mem) calls with the same
+ * k-experience inputs, then a synchronisation of the replay's stream; *seconds = the host
+ * wall time of the whole loop (no per-call binding overhead).  Stops at the first non-OK
+ * status and returns it.  Inputs as replay_add's. */
+int rpl_time_adds(rpl_replay *replay, int64_t n_calls, int64_t k, const void *s, const int32_t *a,
+                  const float *r, const void *s_next, const uint8_t *done, int mem, double *seconds);
 
 #ifdef __cplusplus
 }

@@ -26,7 +26,7 @@ RPL_ECUDA, RPL_ENCCL, RPL_ESTATE = -5, -6, -7
 RPL_HOST, RPL_DEVICE, RPL_DEVICE_DEFER = 0, 1, 2
 RPL_ONLINE, RPL_TARGET, RPL_GRAD = 0, 1, 2
 RPL_F32, RPL_U8 = 0, 1
-RPL_RING_DEVICE, RPL_RING_HOST = 0, 1
+RPL_RING_DEVICE, RPL_RING_HOST, RPL_RING_HOST_BATCH = 0, 1, 2
 RPL_PREC_FP32, RPL_PREC_TF32, RPL_PREC_BF16 = 0, 1, 2
 (RPL_DBG_IDX, RPL_DBG_S, RPL_DBG_S_NEXT, RPL_DBG_A, RPL_DBG_R, RPL_DBG_DONE, RPL_DBG_Q,
  RPL_DBG_QT_NEXT, RPL_DBG_QO_NEXT, RPL_DBG_Y, RPL_DBG_ASTAR, RPL_DBG_H, RPL_DBG_LOSS,
@@ -40,7 +40,7 @@ EXPORTS = [
     "dqn_train_step", "sync_target", "dqn_get_params", "dqn_set_params", "dqn_step_count",
     "dqn_debug_export", "rpl_nccl_unique_id", "dqn_attach_nccl", "dqn_peer_handle",
     "dqn_attach_peers", "dqn_detach_peers", "rpl_dp_emulate", "rpl_check",
-    "rpl_last_error", "rpl_kernel_launches",
+    "rpl_last_error", "rpl_kernel_launches", "rpl_time_adds",
 ]
 
 
@@ -109,6 +109,7 @@ def _load():
         "rpl_check": (C.c_int, [P, C.c_int]),
         "rpl_last_error": (C.c_char_p, []),
         "rpl_kernel_launches": (C.c_uint64, []),
+        "rpl_time_adds": (C.c_int, [P, i64, i64, P, P, P, P, P, C.c_int, C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -184,7 +185,8 @@ class Replay:
         o = _ReplayOpts(device, self._stream, burn_in, seed, rank, max_host_add,
                         RPL_U8 if self.u8 else RPL_F32, 1 if sampling == "distinct" else 0,
                         1 if shared_state else 0,
-                        RPL_RING_HOST if ring_memory == "host" else RPL_RING_DEVICE, update_size,
+                        {"device": RPL_RING_DEVICE, "host": RPL_RING_HOST,
+                         "host_batch": RPL_RING_HOST_BATCH}[ring_memory], update_size,
                         None if storage is None else storage.data_ptr(),
                         0 if storage is None else storage.numel() * storage.element_size())
         self._storage = storage
@@ -245,6 +247,23 @@ class Replay:
         st = _L.replay_add(self._h, k, arrs[0].ctypes.data, arrs[1].ctypes.data, arrs[2].ctypes.data,
                            None if arrs[3] is None else arrs[3].ctypes.data, arrs[4].ctypes.data, RPL_HOST)
         return st if st == RPL_OK else _ok(st)
+
+    def time_adds(self, e: dict, n_calls: int) -> float:
+        """rpl_time_adds: wall seconds of n_calls replay_add calls of the experiences `e` (host
+        numpy arrays -> RPL_HOST, CUDA tensors -> RPL_DEVICE), timed inside the library."""
+        torch = _torch()
+        if isinstance(e["a"], torch.Tensor) and e["a"].is_cuda:
+            ts = [e[k].contiguous() for k in ("s", "a", "r", "s_next", "done")]
+            ptrs, mem, keep = [_dptr(t) for t in ts], RPL_DEVICE, ts
+        else:
+            sn = self.state_np
+            arrs = (_host(e["s"], sn), _host(e["a"], np.int32), _host(e["r"], np.float32),
+                    _host(e["s_next"], sn), _host(e["done"], np.uint8))
+            ptrs, mem, keep = [x.ctypes.data for x in arrs], RPL_HOST, arrs
+        sec = C.c_double(0.0)
+        _ok(_L.rpl_time_adds(self._h, n_calls, len(e["a"]), *ptrs, mem, C.byref(sec)))
+        del keep
+        return sec.value
 
     def add_many(self, e: dict, chunk: int = 65536):
         n = len(e["a"])

@@ -1682,6 +1682,11 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
     // a deferred insert is consumed by the fast path's K1 on the shared stream; otherwise it
     // is written now by the insert kernel
     const bool fast = d->fast && !rp->ring.u8;   // the fast kernels read fp32 rows
+    if (rp->ring.host == 2 && !fast) {
+        if (prev >= 0) cudaSetDevice(prev);
+        set_error("dqn_train_step: an RPL_RING_HOST_BATCH replay needs the fast path's net shape");
+        return RPL_ESTATE;
+    }
     if (!fast || rp->stream != d->stream) {
         if (int rc = replay_flush(rp)) {
             if (prev >= 0) cudaSetDevice(prev);
@@ -1691,6 +1696,18 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
     if (fast) {
         FastArgs fp;
         fill_fast(d, rp, batch, dp ? nullptr : loss_dev, dp ? 0 : 1, fp);
+        if (rp->ring.host == 2) {
+            // the paper's in-RAM replay: CPU sample + CPU gather into pinned
+            // staging, one H2D copy of the batch, then the same kernels on the copied rows
+            const float *rows = nullptr;
+            const int32_t *bidx = nullptr;
+            if (int rc = host_batch_stage(rp, batch, d->stream, &rows, &bidx)) {
+                if (prev >= 0) cudaSetDevice(prev);
+                return rc;
+            }
+            fp.ring = const_cast<float *>(rows);
+            fp.bidx = bidx;
+        }
         const int zslot = rp->pend.slot;   // zero-copy staging slot the insert reads (or -1)
         rp->pend.k = 0;
         rp->pend.slot = -1;

@@ -48,7 +48,8 @@ constexpr uint32_t TAG_SAMPLE = 1u;
 // a | r | done | pad], row stride a multiple of 128 B; `so` is the byte offset of a.
 struct Ring {
     float *rows = nullptr;     // capacity * rs words
-    int host = 0;              // RPL_RING_HOST: rows in pinned, mapped host memory
+    int host = 0;              // RPL_RING_HOST: rows in pinned, mapped host memory;
+                               // RPL_RING_HOST_BATCH (2): pageable host rows, CPU sampler
     int owned = 1;             // 0: rows are the caller's opts.storage (not freed)
     int64_t capacity = 0;
     int32_t D = 0;
@@ -128,6 +129,14 @@ struct rpl_replay {
     bool distinct = false;   // RPL_SAMPLE_DISTINCT (distinct.cuh)
     int32_t *ds_idx = nullptr;   // scratch indices of distinct replay_sample calls
     int64_t ds_cap = 0;
+    // RPL_RING_HOST_BATCH (the paper's in-RAM replay): per-step batch staging -- two pinned
+    // buffers [rows B x rs words | idx B] used alternately (an event per buffer marks its H2D
+    // copy done), and the device batch the step's kernels read
+    char *bpin[2] = {nullptr, nullptr};
+    cudaEvent_t bev[2] = {nullptr, nullptr};
+    int bcur = 0;
+    int64_t bcap = 0;          // rows the staging holds
+    float *bdev = nullptr;     // device rows [bcap x rs] then idx [bcap]
 };
 
 namespace rpl {
@@ -150,6 +159,10 @@ int replay_flush(rpl_replay *rp);
 // the pending insert was enqueued for consumption on `st`: a zero-copy staging slot may be
 // reused once the stream passes this point
 int replay_consumed(rpl_replay *rp, int slot, cudaStream_t st);
+// RPL_RING_HOST_BATCH: sample B indices of event rp->events on the CPU, gather their rows on
+// the CPU into pinned staging and enqueue one H2D copy on `st` into the device batch (rows
+// at *rows, indices at *idx); the caller advances the event
+int host_batch_stage(rpl_replay *rp, int B, cudaStream_t st, const float **rows, const int32_t **idx);
 // largest insert that may be deferred into K1 (K1's CTAs write its rows)
 constexpr int64_t kMaxDeferredRows = 4096;
 }  // namespace rpl

@@ -4,6 +4,7 @@
 // Paper: P:71-75 [Methods] (packed 1,000,000 x 57 Variable, block inserts, uniform integer
 // sampling + gather + unpack), P:44 (FIFO, burn-in).  B200 design: DESIGN.md "Kernels".
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdlib>
 #include <cstring>
@@ -54,6 +55,12 @@ struct DeviceGuard {
 // K1: insert.  One warp per experience; the warp writes the whole 128B-aligned row (one or
 // more fully coalesced 128-byte stores per 32 floats).  Slot = (cursor + j) mod capacity.
 // ------------------------------------------------------------------------------------------
+// One CTA inserts tiles of INS_R consecutive experiences: the tile's SoA sources (contiguous
+// runs of s / s' / a / r / done) are read with coalesced loads into shared memory, then the
+// packed rows (consecutive slots) leave as 16-byte stores, every warp writing whole 128-byte
+// lines -- all loads of a tile in flight at once (P:73 block insert).  Rows wider than
+// INS_RS words take one warp per row.
+constexpr int INS_R = 32, INS_RS = 64;
 __global__ void __launch_bounds__(256) insert_kernel(float *__restrict__ rows, int rs, int D, int sw,
                                                      int64_t capacity, int64_t cursor, int64_t k,
                                                      const float *__restrict__ s,
@@ -63,17 +70,56 @@ __global__ void __launch_bounds__(256) insert_kernel(float *__restrict__ rows, i
                                                      const uint8_t *__restrict__ done,
                                                      uint32_t *err, uint64_t *ctrl, int64_t new_size)
 {
-    const int lane = threadIdx.x & 31;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __shared__ __align__(16) float tile[INS_R * INS_RS];
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (blockIdx.x == 0 && tid == 0) {
         ctrl[1] = (uint64_t)new_size;
         ctrl[2] = (uint64_t)((cursor + k) % capacity);
     }
-    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k;
-         j += nwarps) {
-        int64_t slot = cursor + j;
-        if (slot >= capacity) slot -= capacity;   // k <= capacity, cursor < capacity
-        ring_write_row(rows + slot * rs, rs, D, sw, lane, j, s, a, r, s2, done, err);
+    if (rs > INS_RS) {
+        const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+        for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (tid >> 5); j < k; j += nwarps) {
+            int64_t slot = cursor + j;
+            if (slot >= capacity) slot -= capacity;   // k <= capacity, cursor < capacity
+            ring_write_row(rows + slot * rs, rs, D, sw, lane, j, s, a, r, s2, done, err);
+        }
+        return;
+    }
+    const int nq = rs / 4;   // 16-byte pieces per row (rs is a multiple of 32 words)
+    for (int64_t j0 = (int64_t)blockIdx.x * INS_R; j0 < k; j0 += (int64_t)gridDim.x * INS_R) {
+        const int nr = (int)(k - j0 < INS_R ? k - j0 : INS_R);
+        const int ns = nr * D;
+        for (int e = tid; e < ns; e += blockDim.x) {
+            const int rr = e / D, c = e - rr * D;
+            tile[rr * INS_RS + c] = s[j0 * D + e];
+            if (sw > D) tile[rr * INS_RS + D + c] = s2[j0 * D + e];
+        }
+        for (int e = tid; e < nr * (rs - sw); e += blockDim.x) {
+            const int rr = e / (rs - sw), c = sw + (e - rr * (rs - sw));
+            float v = 0.0f;
+            if (c == sw) {
+                v = __int_as_float(a[j0 + rr]);
+            } else if (c == sw + 1) {
+                v = r[j0 + rr];
+            } else if (c == sw + 2) {
+                uint32_t d = done[j0 + rr];
+                if (d > 1u) {   // a device-sourced done > 1 is stored as 1 and flagged
+                    atomicOr(err, ERRBIT_CORRUPT);
+                    d = 1u;
+                }
+                v = __uint_as_float(d);
+            }
+            tile[rr * INS_RS + c] = v;
+        }
+        __syncthreads();
+        for (int e = tid; e < nr * nq; e += blockDim.x) {
+            const int rr = e / nq, q = e - rr * nq;
+            int64_t slot = cursor + j0 + rr;
+            if (slot >= capacity) slot -= capacity;
+            *reinterpret_cast<float4 *>(rows + slot * rs + 4 * q) =
+                *reinterpret_cast<const float4 *>(tile + rr * INS_RS + 4 * q);
+        }
+        __syncthreads();
     }
 }
 
@@ -536,7 +582,7 @@ int replay_flush(rpl_replay *rp)
     q.slot = -1;
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, rp->device);
-    int64_t blocks = (k + 7) / 8;
+    int64_t blocks = rp->ring.rs > INS_RS ? (k + 7) / 8 : (k + INS_R - 1) / INS_R;
     if (blocks > (int64_t)dev_sms * 8) blocks = (int64_t)dev_sms * 8;
     if (rp->ring.u8) {
         // one CTA per 4 KB piece of a row (rows are ~56 KB for Atari-shaped states)
@@ -679,7 +725,10 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
         (o.state_dtype != RPL_F32 && o.state_dtype != RPL_U8) ||
         (o.sampling != RPL_SAMPLE_UNIFORM && o.sampling != RPL_SAMPLE_DISTINCT) ||
         (o.state_sharing != 0 && o.state_sharing != 1) ||
-        (o.ring_memory != RPL_RING_DEVICE && o.ring_memory != RPL_RING_HOST) ||
+        (o.ring_memory != RPL_RING_DEVICE && o.ring_memory != RPL_RING_HOST &&
+         o.ring_memory != RPL_RING_HOST_BATCH) ||
+        (o.ring_memory == RPL_RING_HOST_BATCH &&
+         (o.state_dtype != RPL_F32 || o.sampling != RPL_SAMPLE_UNIFORM || o.state_sharing)) ||
         o.update_size < 0 || o.update_size > capacity) {
         set_error("replay_create: invalid argument (capacity=%lld state_dim=%d rank=%u burn_in=%lld)",
                   (long long)capacity, state_dim, o.rank, (long long)o.burn_in);
@@ -733,7 +782,7 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
     if (u8) rp->no_defer = true;   // deferral is a fast-path (fp32 states) feature
     rp->distinct = o.sampling == RPL_SAMPLE_DISTINCT;
     const size_t ring_bytes = (size_t)capacity * rp->ring.rs * sizeof(float);
-    rp->ring.host = o.ring_memory == RPL_RING_HOST ? 1 : 0;
+    rp->ring.host = o.ring_memory == RPL_RING_HOST ? 1 : o.ring_memory == RPL_RING_HOST_BATCH ? 2 : 0;
     if (o.storage) {
         // caller-owned device rows (e.g. a torch tensor): checked, zeroed, never freed here
         cudaPointerAttributes pa{};
@@ -748,6 +797,16 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
         }
         rp->ring.rows = (float *)o.storage;
         rp->ring.owned = 0;
+    } else if (rp->ring.host == 2) {
+        // the paper's in-RAM replay: ordinary pageable host memory, written and read by the CPU
+        void *mem = nullptr;
+        if (posix_memalign(&mem, 4096, ring_bytes) != 0) {
+            set_error("replay_create: %zu bytes of host ring memory unavailable", ring_bytes);
+            delete rp;
+            return RPL_ENOMEM;
+        }
+        rp->ring.rows = (float *)mem;
+        std::memset(rp->ring.rows, 0, ring_bytes);
     } else if (rp->ring.host) {
         // in-RAM comparison mode: pinned host rows the kernels address directly (UVA)
         if (cudaHostAlloc(&rp->ring.rows, ring_bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
@@ -806,8 +865,14 @@ extern "C" int replay_destroy(rpl_replay *rp)
     if (rp->err_dev) cudaFree(rp->err_dev);
     if (rp->ctrl_dev) cudaFree(rp->ctrl_dev);
     if (rp->ds_idx) cudaFree(rp->ds_idx);
+    for (int i = 0; i < 2; ++i) {
+        if (rp->bev[i]) cudaEventDestroy(rp->bev[i]);
+        if (rp->bpin[i]) cudaFreeHost(rp->bpin[i]);
+    }
+    if (rp->bdev) cudaFree(rp->bdev);
     if (rp->ring.rows && rp->ring.owned) {
-        if (rp->ring.host) cudaFreeHost(rp->ring.rows);
+        if (rp->ring.host == 2) free(rp->ring.rows);
+        else if (rp->ring.host) cudaFreeHost(rp->ring.rows);
         else cudaFree(rp->ring.rows);
     }
     delete rp;
@@ -882,6 +947,105 @@ extern "C" int replay_queued(const rpl_replay *rp, int64_t *queued)
     return RPL_OK;
 }
 
+// RPL_RING_HOST_BATCH insert: the CPU writes the rows of the host ring (the paper's in-RAM
+// replay keeps its experiences in RAM; no transfer until a batch is sampled)
+static int host_ring_add(rpl_replay *rp, int64_t k, const float *s, const int32_t *a, const float *r,
+                         const float *s_next, const uint8_t *done, int mem)
+{
+    if (mem != RPL_HOST) {
+        set_error("replay_add: an RPL_RING_HOST_BATCH replay takes host inputs only (mem=%d)", mem);
+        return RPL_EINVAL;
+    }
+    for (int64_t j = 0; j < k; ++j)
+        if (done[j] > 1) {
+            set_error("replay_add: done[%lld]=%u not in {0,1}", (long long)j, done[j]);
+            return RPL_ECORRUPT;
+        }
+    const int32_t D = rp->ring.D, rs = rp->ring.rs;
+    for (int64_t j = 0; j < k; ++j) {
+        float *row = rp->ring.rows + ((rp->cursor + j) % rp->ring.capacity) * rs;
+        std::memcpy(row, s + j * D, (size_t)D * 4);
+        std::memcpy(row + D, s_next + j * D, (size_t)D * 4);
+        const uint32_t dn = done[j];
+        std::memcpy(row + 2 * D, a + j, 4);
+        std::memcpy(row + 2 * D + 1, r + j, 4);
+        std::memcpy(row + 2 * D + 2, &dn, 4);
+    }
+    rp->cursor = (rp->cursor + k) % rp->ring.capacity;
+    rp->size = std::min<int64_t>(rp->size + k, rp->ring.capacity);
+    rp->total += (uint64_t)k;
+    return RPL_OK;
+}
+
+// the CPU sampler of RPL_RING_HOST_BATCH: the device sampler's Philox stream (Q3)
+static void host_sample(const rpl_replay *rp, int B, uint64_t event, int32_t *idx)
+{
+    const uint64_t n = (uint64_t)rp->size;
+    for (int i = 0; i < B; i += 2) {
+        int32_t i0, i1;
+        sample_pair(rp->seed, rp->rank, event, (uint32_t)(i / 2), n, i0, i1);
+        idx[i] = i0;
+        if (i + 1 < B) idx[i + 1] = i1;
+    }
+}
+
+// grow the batch staging to B rows (waits for the copies in flight)
+static int host_batch_reserve(rpl_replay *rp, int64_t B)
+{
+    if (B <= rp->bcap) return RPL_OK;
+    const size_t rowb = (size_t)rp->ring.rs * 4, bytes = (size_t)B * (rowb + 4);
+    for (int i = 0; i < 2; ++i) {
+        if (rp->bev[i]) RPL_CUDA(cudaEventSynchronize(rp->bev[i]));
+        if (rp->bpin[i]) cudaFreeHost(rp->bpin[i]);
+        rp->bpin[i] = nullptr;
+        if (!rp->bev[i]) RPL_CUDA(cudaEventCreateWithFlags(&rp->bev[i], cudaEventDisableTiming));
+    }
+    if (rp->bdev) {
+        RPL_CUDA(cudaDeviceSynchronize());
+        cudaFree(rp->bdev);
+        rp->bdev = nullptr;
+    }
+    rp->bcap = 0;
+    for (int i = 0; i < 2; ++i)
+        if (cudaHostAlloc((void **)&rp->bpin[i], bytes, cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("in-RAM batch staging: %zu pinned bytes unavailable", bytes);
+            return RPL_ENOMEM;
+        }
+    if (cudaMalloc((void **)&rp->bdev, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("in-RAM batch staging: %zu device bytes unavailable", bytes);
+        return RPL_ENOMEM;
+    }
+    rp->bcap = B;
+    return RPL_OK;
+}
+
+namespace rpl {
+int host_batch_stage(rpl_replay *rp, int B, cudaStream_t st, const float **rows, const int32_t **idx)
+{
+    DeviceGuard g(rp->device);
+    if (int rc = host_batch_reserve(rp, B)) return rc;
+    const int c = rp->bcur;
+    rp->bcur ^= 1;
+    RPL_CUDA(cudaEventSynchronize(rp->bev[c]));   // the copy that last read this buffer is done
+    const size_t rowb = (size_t)rp->ring.rs * 4;
+    char *pin = rp->bpin[c];
+    int32_t *pidx = reinterpret_cast<int32_t *>(pin + (size_t)B * rowb);
+    host_sample(rp, B, rp->events, pidx);
+    for (int i = 0; i < B; ++i)
+        std::memcpy(pin + (size_t)i * rowb, rp->ring.rows + (int64_t)pidx[i] * rp->ring.rs, rowb);
+    // one transfer: the rows then the indices, packed at the front of the device batch
+    char *dst = reinterpret_cast<char *>(rp->bdev);
+    RPL_CUDA(cudaMemcpyAsync(dst, pin, (size_t)B * (rowb + 4), cudaMemcpyHostToDevice, st));
+    RPL_CUDA(cudaEventRecord(rp->bev[c], st));
+    rp->h2d_bytes += (uint64_t)B * (rowb + 4);
+    *rows = rp->bdev;
+    *idx = reinterpret_cast<const int32_t *>(dst + (size_t)B * rowb);
+    return RPL_OK;
+}
+}  // namespace rpl
+
 static int add_rows(rpl_replay *rp, int64_t k, const void *s, const int32_t *a, const float *r,
                     const void *s_next, const uint8_t *done, int mem)
 {
@@ -897,6 +1061,7 @@ static int add_rows(rpl_replay *rp, int64_t k, const void *s, const int32_t *a, 
         set_error("replay_add: null input pointer");
         return RPL_EINVAL;
     }
+    if (rp->ring.host == 2) return host_ring_add(rp, k, (const float *)s, a, r, (const float *)s_next, done, mem);
     DeviceGuard g(rp->device);
     if (int rc = replay_flush(rp)) return rc;   // inserts stay in call order
     const void *ds = s, *ds2 = nullptr;
@@ -905,7 +1070,37 @@ static int add_rows(rpl_replay *rp, int64_t k, const void *s, const int32_t *a, 
     int zslot = -1;
     const int32_t *da = a;
     const uint8_t *dd = done;
-    if (mem == RPL_HOST) {
+    bool direct = false;   // host inputs already in pinned memory: the insert kernel reads them
+    if (mem == RPL_HOST && k > kMaxDeferredRows) {
+        // large host blocks from pinned (page-locked, device-mapped) memory: no staging copy --
+        // the insert kernel reads the caller's arrays across PCIe once, and the call returns
+        // after it (the caller may reuse its buffers, as for any RPL_HOST add)
+        const void *ps[5] = {s, a, r, rp->ring.shared ? s : s_next, done};
+        const void *pd[5] = {};
+        direct = true;
+        for (int i = 0; i < 5 && direct; ++i) {
+            cudaPointerAttributes at{};
+            direct = cudaPointerGetAttributes(&at, ps[i]) == cudaSuccess &&
+                     at.type == cudaMemoryTypeHost && at.devicePointer != nullptr;
+            if (direct) pd[i] = at.devicePointer;
+        }
+        cudaGetLastError();
+        if (direct) {
+            for (int64_t j = 0; j < k; ++j)
+                if (done[j] > 1) {
+                    set_error("replay_add: done[%lld]=%u not in {0,1}", (long long)j, done[j]);
+                    return RPL_ECORRUPT;
+                }
+            ds = pd[0];
+            da = (const int32_t *)pd[1];
+            dr = (const float *)pd[2];
+            ds2 = rp->ring.shared ? nullptr : pd[3];
+            dd = (const uint8_t *)pd[4];
+            const size_t bs = (size_t)k * D * (rp->ring.u8 ? 1 : sizeof(float));
+            rp->h2d_bytes += bs * (rp->ring.shared ? 1 : 2) + (size_t)k * 9;
+        }
+    }
+    if (mem == RPL_HOST && !direct) {
         if (k > rp->max_host_add) {
             set_error("replay_add: k=%lld exceeds max_host_add=%lld", (long long)k,
                       (long long)rp->max_host_add);
@@ -980,6 +1175,7 @@ static int add_rows(rpl_replay *rp, int64_t k, const void *s, const int32_t *a, 
     if (mem == RPL_DEVICE || k > kMaxDeferredRows || rp->no_defer) {
         if (int rc = replay_flush(rp)) return rc;
     }
+    if (direct) RPL_CUDA(cudaStreamSynchronize(rp->stream));   // the caller's pinned arrays are read
     rp->cursor = (rp->cursor + k) % rp->ring.capacity;
     rp->size = new_size;
     rp->total += (uint64_t)k;
@@ -999,6 +1195,43 @@ extern "C" int replay_sample(rpl_replay *rp, int32_t batch, const rpl_batch *out
     const int64_t nvalid = sampleable(rp);
     if (rp->size < rp->burn_in || nvalid < 1 || (rp->distinct && nvalid < batch)) return RPL_NOT_READY;
     DeviceGuard g(rp->device);
+    if (rp->ring.host == 2) {
+        // in-RAM replay: CPU sample + CPU unpack into pinned staging, then the batch tensors
+        // cross PCIe (the paper's feed of sampled batches)
+        const int32_t D = rp->ring.D, rs = rp->ring.rs;
+        if (int rc = host_batch_reserve(rp, (int64_t)batch * 2)) return rc;
+        const int c = rp->bcur;
+        rp->bcur ^= 1;
+        RPL_CUDA(cudaEventSynchronize(rp->bev[c]));
+        char *pin = rp->bpin[c];
+        float *ps = reinterpret_cast<float *>(pin), *ps2 = ps + (size_t)batch * D;
+        int32_t *pa = reinterpret_cast<int32_t *>(ps2 + (size_t)batch * D);
+        float *pr = reinterpret_cast<float *>(pa + batch);
+        int32_t *pidx = reinterpret_cast<int32_t *>(pr + batch);
+        uint8_t *pd = reinterpret_cast<uint8_t *>(pidx + batch);
+        host_sample(rp, batch, rp->events, pidx);
+        for (int i = 0; i < batch; ++i) {
+            const float *row = rp->ring.rows + (int64_t)pidx[i] * rs;
+            std::memcpy(ps + (size_t)i * D, row, (size_t)D * 4);
+            std::memcpy(ps2 + (size_t)i * D, row + D, (size_t)D * 4);
+            std::memcpy(pa + i, row + 2 * D, 4);
+            std::memcpy(pr + i, row + 2 * D + 1, 4);
+            uint32_t dn;
+            std::memcpy(&dn, row + 2 * D + 2, 4);
+            pd[i] = (uint8_t)(dn != 0u);
+        }
+        const size_t sb = (size_t)batch * D * 4;
+        RPL_CUDA(cudaMemcpyAsync(out->s, ps, sb, cudaMemcpyHostToDevice, rp->stream));
+        RPL_CUDA(cudaMemcpyAsync(out->s_next, ps2, sb, cudaMemcpyHostToDevice, rp->stream));
+        RPL_CUDA(cudaMemcpyAsync(out->a, pa, (size_t)batch * 4, cudaMemcpyHostToDevice, rp->stream));
+        RPL_CUDA(cudaMemcpyAsync(out->r, pr, (size_t)batch * 4, cudaMemcpyHostToDevice, rp->stream));
+        RPL_CUDA(cudaMemcpyAsync(out->done, pd, (size_t)batch, cudaMemcpyHostToDevice, rp->stream));
+        if (out->idx) RPL_CUDA(cudaMemcpyAsync(out->idx, pidx, (size_t)batch * 4, cudaMemcpyHostToDevice, rp->stream));
+        RPL_CUDA(cudaEventRecord(rp->bev[c], rp->stream));
+        rp->h2d_bytes += 2 * sb + (size_t)batch * 9;
+        rp->events += 1;
+        return RPL_OK;
+    }
     int rc = launch_gather(rp, batch, nullptr, rp->events, 1, out);
     if (rc != RPL_OK) return rc;
     rp->events += 1;
@@ -1017,8 +1250,26 @@ extern "C" int replay_gather(rpl_replay *rp, int64_t n, const int32_t *idx_dev,
         set_error("replay_gather: empty replay");
         return RPL_ESTATE;
     }
+    if (rp->ring.host == 2) {
+        set_error("replay_gather: device-index gathers need device-addressable rows (not RPL_RING_HOST_BATCH)");
+        return RPL_ESTATE;
+    }
     DeviceGuard g(rp->device);
     return launch_gather(rp, n, idx_dev, 0, 0, out);
+}
+
+extern "C" int rpl_time_adds(rpl_replay *rp, int64_t n_calls, int64_t k, const void *s, const int32_t *a,
+                             const float *r, const void *s_next, const uint8_t *done, int mem, double *seconds)
+{
+    if (!rp || n_calls < 0 || !seconds) return RPL_EINVAL;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int64_t i = 0; i < n_calls; ++i)
+        if (int rc = replay_add(rp, k, s, a, r, s_next, done, mem)) return rc;
+    if (int rc = replay_flush(rp)) return rc;
+    DeviceGuard g(rp->device);
+    RPL_CUDA(cudaStreamSynchronize(rp->stream));
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return RPL_OK;
 }
 
 extern "C" int replay_size(const rpl_replay *rp, int64_t *size)

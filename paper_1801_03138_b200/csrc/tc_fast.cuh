@@ -276,7 +276,9 @@ __global__ void __launch_bounds__(tc::T, 1) tc_fwd_kernel(const __grid_constant_
             // (2) Philox sample of row rb + r (Q3): index 2j and 2j + 1 of call j
             const int row = rb + r;
             int32_t slot = 0;
-            if (p.distinct) {
+            if (p.bidx) {
+                slot = row < B ? p.bidx[row] : 0;
+            } else if (p.distinct) {
                 slot = row < B ? p.idx[row] : 0;
             } else {
                 int32_t i0, i1;
@@ -296,7 +298,8 @@ __global__ void __launch_bounds__(tc::T, 1) tc_fwd_kernel(const __grid_constant_
             // (3) gather the row's state into registers (pending slots read through from the
             // insert's sources, possibly pinned host memory)
             float x[KC];
-            const float *src = pjx < 0 ? p.ring + sslot * p.rs + col0
+            const int64_t rslot = p.bidx ? min(row, B - 1) : sslot;   // in-RAM: the copied batch
+            const float *src = pjx < 0 ? p.ring + rslot * p.rs + col0
                                        : (net == 0 || p.shared ? p.pend_s : p.pend_s2) + (int64_t)pjx * D;
 #pragma unroll
             for (int d = 0; d < KC; ++d) x[d] = (d < D && r < nb) ? src[d] : 0.0f;
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(tc::T, 1) tc_fwd_kernel(const __grid_constant_
                 float rr;
                 uint32_t rd;
                 if (pj < 0) {
-                    const float *sc = p.ring + (int64_t)slot * p.rs + p.sw;
+                    const float *sc = p.ring + (int64_t)(p.bidx ? row : slot) * p.rs + p.sw;
                     ra = __float_as_int(__ldg(sc));
                     rr = __ldg(sc + 1);
                     rd = __float_as_uint(__ldg(sc + 2));

@@ -86,6 +86,8 @@ struct FastArgs {
     int32_t *sync_flag;  // written by K2 (step t+1 is a sync step), read by K4 / sgd_kernel
     int apply_update;
     int distinct;        // 1: the batch indices come from distinct_fast_kernel (in idx)
+    const int32_t *bidx; // in-RAM replay (RPL_RING_HOST_BATCH): the CPU-sampled indices of the
+                         // batch copied to the device; then `ring` is that batch, row b = sample b
     // wide inputs (config 5): layer 0 runs in wide.cuh; the fast kernels run the layers above it
     const float *h0_in;  // [nets][B][N0] layer-0 activations (K1 skips sample, gather, layer 0)
     float *PdH0;         // [NS][B][N0] K3's dH0 split-K partials (no dW0 shares)
@@ -419,7 +421,10 @@ __device__ __forceinline__ void fast_fwd_body(const FastArgs &p)
             // (2) Philox sample of the tile's rows (Q3)
             if (tid < F_BT / 2) {
                 int32_t i0, i1;
-                if (p.distinct) {   // written by distinct_fast_kernel (rows past B: any valid slot)
+                if (p.bidx) {       // in-RAM replay: sampled on the CPU, rows already gathered
+                    i0 = rb + 2 * tid < B ? p.bidx[rb + 2 * tid] : 0;
+                    i1 = rb + 2 * tid + 1 < B ? p.bidx[rb + 2 * tid + 1] : 0;
+                } else if (p.distinct) {   // written by distinct_fast_kernel (rows past B: any valid slot)
                     i0 = rb + 2 * tid < B ? p.idx[rb + 2 * tid] : 0;
                     i1 = rb + 2 * tid + 1 < B ? p.idx[rb + 2 * tid + 1] : 0;
                 } else {
@@ -447,7 +452,7 @@ __device__ __forceinline__ void fast_fwd_body(const FastArgs &p)
             const int col0 = net == 0 || p.shared ? 0 : D;
             for (int e = tid; e < F_BT * D; e += F_NT1) {
                 const int rr = e / D, d = e - rr * D, j = nxt ? pjs2[rr] : pjs[rr];
-                const int64_t slot = nxt ? (idxs[rr] + 1) % p.capacity : idxs[rr];
+                const int64_t slot = p.bidx ? min(rb + rr, B - 1) : nxt ? (idxs[rr] + 1) % p.capacity : idxs[rr];
                 if (j < 0) {
                     cp_async4(Xs + rr * L.XP + d, p.ring + slot * p.rs + col0 + d);
                 } else {   // pending insert: its sources (possibly pinned host memory: plain loads)
@@ -461,7 +466,7 @@ __device__ __forceinline__ void fast_fwd_body(const FastArgs &p)
             if (unpack_scalars) {
                 const int j = pjs[tid];
                 if (j < 0) {
-                    const float *row = p.ring + (int64_t)idxs[tid] * p.rs + p.sw;
+                    const float *row = p.ring + (int64_t)(p.bidx ? rb + tid : idxs[tid]) * p.rs + p.sw;
                     ra_ = __float_as_int(__ldg(row));
                     rr_ = __ldg(row + 1);
                     rd_ = __float_as_uint(__ldg(row + 2));

@@ -219,3 +219,57 @@ def test_staging_arena_wraps_with_many_adds_in_flight(B):
     for k in ("s", "s_next", "a", "r", "done"):
         assert np.array_equal(g[k], o[k]), k
     assert rp.check() == B.RPL_OK
+
+
+@pytest.mark.parametrize("D,shared", [(27, False), (27, True), (40, False)])
+def test_block_inserts_pinned_device_and_tiles(B, D, shared):
+    # the tiled insert kernel (32 experiences per CTA iteration, 16-byte row stores; rows wider
+    # than 64 words one warp per row) on blocks that are not multiples of the tile and wrap the
+    # ring, from pinned host memory (k > 4096: read by the kernel across PCIe, no staging copy),
+    # pageable host memory and device memory; the ring equals the oracle's row for row
+    import torch
+    C = 9000
+    rp = B.Replay(C, D, seed=3, shared_state=shared)
+    orc = oracle.Ring(C, D, shared=shared) if shared else oracle.Ring(C, D)
+    e = experiences(30_000, state_dim=D, seed=21)
+    t = 0
+    h0 = rp.state()["h2d_bytes"]
+    for src, k in [("pinned", 5003), ("host", 4097), ("device", 6001), ("pinned", 8999),
+                   ("device", 33), ("pinned", 4100)]:
+        part = {kk: v[t:t + k] for kk, v in e.items()}
+        t += k
+        if src == "pinned":
+            rp.add(**{kk: torch.from_numpy(v).pin_memory() for kk, v in part.items()})
+        elif src == "device":
+            rp.add(**{kk: torch.from_numpy(v).cuda() for kk, v in part.items()})
+        else:
+            rp.add(**part)
+        orc.add(**part)
+        st = rp.state()
+        assert (st["cursor"], st["size"], st["total"]) == (orc.cursor, orc.size, orc.total)
+    per = (D if shared else 2 * D) * 4 + 9
+    assert rp.state()["h2d_bytes"] - h0 == (5003 + 4097 + 8999 + 4100) * per
+    idx = torch.arange(orc.size, dtype=torch.int32, device="cuda")
+    g = {k: v.cpu().numpy() for k, v in rp.gather(idx).items()}
+    o = orc.gather(np.arange(orc.size, dtype=np.int32))
+    for k in ("s", "s_next", "a", "r", "done"):
+        assert np.array_equal(g[k], o[k]), k
+    assert rp.check() == B.RPL_OK
+
+
+def test_time_adds_entry(B):
+    # rpl_time_adds runs replay_add n times inside the library: same ring state as n adds
+    rp = B.Replay(1000, 27, seed=3)
+    orc = oracle.Ring(1000, 27)
+    e = experiences(7, seed=5)
+    sec = rp.time_adds(e, 300)
+    for _ in range(300):
+        orc.add(**e)
+    assert sec > 0
+    st = rp.state()
+    assert (st["cursor"], st["size"], st["total"]) == (orc.cursor, orc.size, orc.total)
+    g = {k: v.cpu().numpy() for k, v in rp.gather(
+        __import__("torch").arange(1000, dtype=__import__("torch").int32, device="cuda")).items()}
+    o = orc.gather(np.arange(1000, dtype=np.int32))
+    for k in ("s", "s_next", "a", "r", "done"):
+        assert np.array_equal(g[k], o[k]), k

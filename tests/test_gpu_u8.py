@@ -140,8 +140,9 @@ def test_u8_config5_batch_256_and_ragged_200(b, ddqn, path, monkeypatch):
     rp = b.Replay(300, D, seed=31, state_dtype="u8")
     orc = oracle.RingU8(300, D)
     e = experiences_u8(420, state_dim=D, seed=32)   # wraps the ring
-    rp.add(**e)
-    orc.add(**e)
+    for part in (slice(0, 250), slice(250, 420)):
+        rp.add(**{k: v[part] for k, v in e.items()})
+        orc.add(**{k: v[part] for k, v in e.items()})
     dqn = b.DQN(cfg, init_params(D, 8, (128,), True, 512, seed=33))
     for batch in (256, 200, 256):
         assert step_and_compare(b, cfg, dqn, rp, orc, batch, seed=31) is not None
