@@ -790,6 +790,7 @@ def run_c5(a):
             j = (i * k) % (npool - k)
             rp.add(**{kk: v[j:j + k] for kk, v in pool_d.items()})
 
+    clk = ClockSampler(local).start()   # before the warm-up, so a short timed region is covered
     for i in range(W):
         add_dev(i)
         dqn.train_step(rp, batch, loss_dev)
@@ -798,28 +799,22 @@ def run_c5(a):
         dist.barrier()
     launches_w = binding.kernel_launches()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        start.record(stream)
-        for i in range(K):
-            add_dev(W + i)
-            dqn.train_step(rp, batch, loss_dev)
-        end.record(stream)
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk.mark_start()
+    start.record(stream)
+    for i in range(K):
+        add_dev(W + i)
+        dqn.train_step(rp, batch, loss_dev)
+    end.record(stream)
+    torch.cuda.synchronize()
+    clk.mark_end()
     launches = binding.kernel_launches() - launches_w
     elapsed_ms = start.elapsed_time(end)
-    kr = min(K, 200)   # per-step durations for the roofline, in a separate pass
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(kr)]
-    for i in range(kr):
-        add_dev(W + K + i)
-        ev[i][0].record(stream)
-        dqn.train_step(rp, batch, loss_dev)
-        ev[i][1].record(stream)
-    torch.cuda.synchronize()
-    kern_ms = [s_.elapsed_time(e_) for s_, e_ in ev]
+    # per-kernel CUPTI durations in a separate pass (the roofline's kernel shares)
+    kb = kernel_breakdown(lambda i: (add_dev(W + K + i), dqn.train_step(rp, batch, loss_dev)),
+                          min(max(K, 50), 200))
     assert dqn.check() == binding.RPL_OK, binding.last_error()
     if world > 1:
         t = torch.tensor([elapsed_ms], device=dev)
@@ -863,22 +858,24 @@ def run_c5(a):
                        "slower of CUDA-event and wall time"}
 
     flops = binding.step_flops(cfg, batch)
-    kern_avg_ms = float(np.mean(kern_ms))
+    ms_per_step = elapsed_ms / K
     # 97% of the step's FLOPs are layer 0, run as bf16 x3 tcgen05 MMAs (FP32-accurate): the
     # denominator is the measured bf16 dense peak / 3 (the FP32-emulation rate), the sustained
     # figure since the kernel runs inside a long step
     bf16 = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1352.0)))
-    peak_emu = bf16 / 3.0
-    achieved = flops / (kern_avg_ms / 1000.0) / 1e12
+    nterm = {"fp32": 3, "tf32": 2, "bf16": 1}[a.precision]
+    peak_emu = bf16 / nterm
+    achieved = flops / (ms_per_step / 1000.0) / 1e12
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_emu, "unit": "TFLOP/s",
                 "frac": achieved / peak_emu,
                 "traffic": load_traffic().get(f"c5_step_b{batch}_{'ddqn' if a.ddqn else 'dqn'}"),
-                "kernel": "the whole train step (Philox gather, wide_l0_kernel, the cooperative "
-                          "train kernel for the layers above layer 0, wide_dw0_kernel + SGD) timed "
-                          "with CUDA events around each dqn_train_step",
-                "kernel_avg_us": kern_avg_ms * 1000.0, "flops_per_launch": flops,
-                "peak_note": f"measured bf16 dense {bf16:.0f} TFLOP/s ({peaks_kind}) / 3: layer 0 runs "
-                             "three bf16 MMAs per FP32 product (hi/mid/lo split of the fp32 operand, "
+                "kernel": "the whole train step (one CUDA graph: Philox gather, wide_l0_kernel, "
+                          "wide_reduce, the fast kernels for the layers above layer 0, wide_dw0_kernel "
+                          "+ SGD): its algorithmic FLOPs / the timed ms_per_step",
+                "kernel_avg_us": ms_per_step * 1000.0, "flops_per_launch": flops,
+                "kernels_cupti": kb,
+                "peak_note": f"measured bf16 dense {bf16:.0f} TFLOP/s ({peaks_kind}) / {nterm}: layer 0 runs "
+                             f"{nterm} bf16 MMA(s) per product (hi/mid/lo split of the fp32 operand, "
                              "exact u8 input)"}
 
     gather = None
@@ -935,7 +932,7 @@ def run_c5(a):
                        else ", NCCL gradient all-reduce" if world > 1 else ""),
                    "l2": "inputs larger than L2 (the byte ring is sampled uniformly)"},
         "samples_per_s": value * batch, "gpu_launches": launches, "roofline": roofline,
-        "cpu_baseline": cpu, "e2e": e2e, "gather": gather, "clocks": clk.summary(),
+        "cpu_baseline": cpu, "e2e": e2e, "gather": gather, "clocks": (clk.stop(), clk.summary())[1],
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -966,21 +966,26 @@ static bool tc_shape_ok(const rpl_dqn *d)
     return d->T == 2 && d->N[0] % 16 == 0 && d->N[0] <= 128 && d->N[1] % 32 == 0 &&
            (!c.dueling || c.stream % 32 == 0) && d->J <= tc::MAXJ && d->woff[1] % 4 == 0;
 }
-// K1 unit tile: 128 when that still gives every SM a task, else 64, else 32 (dividing N1 and
-// a dueling stream)
+// K1 unit tile: the largest of 128 / 64 / 32 dividing N1 and a dueling stream (K1 CTAs are
+// persistent per (net, unit tile) and run that combo's batch tiles)
 static int tc_un_for(const rpl_dqn *d, int B)
 {
-    const int nets = d->cfg.double_dqn ? 3 : 2, nbt = (B + 127) / 128;
+    (void)B;
     const int S = d->cfg.dueling ? d->cfg.stream : d->N[1];
-    for (int un : {128, 64}) {
-        if (d->N[1] % un || S % un) continue;
-        if (un == 64 || nets * nbt * (d->N[1] / un) >= d->sms) return un;
-    }
+    for (int un : {128, 64})
+        if (d->N[1] % un == 0 && S % un == 0) return un;
     return 32;
 }
 // the tensor-core kernels take batches from kTcMinBatch up (below it the mma.sync kernels are
 // faster: the step is latency-bound there)
 static constexpr int kTcMinBatch = 1 << 30;
+static int tc_min_batch()
+{
+#ifdef RPL_EXPERIMENTS
+    if (const char *v = getenv("RPL_TC_MIN")) return atoi(v);
+#endif
+    return kTcMinBatch;
+}
 static constexpr int kTcBsplit = 256;   // K3 (A) tasks: samples per batch split
 // K3 (B) tasks: splits of the layer-1 units (a power of two, >= 2 chunks of 32 units each)
 static int tc_ns_for(const rpl_dqn *d, int B)
@@ -1441,7 +1446,7 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
     p.trace = d->trace;
     p.distinct = rp->distinct ? 1 : 0;
     p.capacity = rp->ring.capacity;
-    if (d->tc && B >= kTcMinBatch) {
+    if (d->tc && B >= tc_min_batch()) {
         p.tc = 1;
         p.UT = tc_un_for(d, B);
         p.nut = p.N1 / p.UT;
@@ -1497,10 +1502,10 @@ static cudaError_t tc_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
     }
     // K1: (net, unit tile) combos x 128-row batch tiles; with more tasks than SMs the grid is a
     // multiple of the combos, so a CTA keeps one weight tile staged across its batch tiles
-    const int nbt = (p.B + 127) / 128, ncombo = p.nets * p.nut, k1_tasks = ncombo * nbt;
-    int g1 = std::min(k1_tasks, d->sms);
-    if (k1_tasks > d->sms && ncombo <= d->sms) g1 = (d->sms / ncombo) * ncombo;
-    e = launch_pdl(tc_fwd_kernel, g1, tc::T, tc_fwd_smem(d, p.UT), st, false, p);
+    // one CTA per SM, persistent: cpc CTAs per (net, unit tile) combo split its batch tiles
+    const int nbt = (p.B + 127) / 128, ncombo = p.nets * p.nut;
+    const int cpc = std::max(1, std::min(nbt, d->sms / ncombo));
+    e = launch_pdl(tc_fwd_kernel, ncombo * cpc, tc::T1, tc_fwd_smem(d, p.UT), st, false, p);
     if (e != cudaSuccess) return e;
     e = launch_pdl(fast_td_kernel, std::min(p.B, 4 * d->sms), NT, fast_td_smem(d), st, pdl || d->k2_pdl, p);
     if (e != cudaSuccess) return e;

@@ -55,12 +55,12 @@ struct DeviceGuard {
 // K1: insert.  One warp per experience; the warp writes the whole 128B-aligned row (one or
 // more fully coalesced 128-byte stores per 32 floats).  Slot = (cursor + j) mod capacity.
 // ------------------------------------------------------------------------------------------
-// One CTA inserts tiles of INS_R consecutive experiences: the tile's SoA sources (contiguous
+// One CTA inserts tiles of INS_R (64) consecutive experiences: the tile's SoA sources (contiguous
 // runs of s / s' / a / r / done) are read with coalesced loads into shared memory, then the
 // packed rows (consecutive slots) leave as 16-byte stores, every warp writing whole 128-byte
 // lines -- all loads of a tile in flight at once (P:73 block insert).  Rows wider than
 // INS_RS words take one warp per row.
-constexpr int INS_R = 32, INS_RS = 64;
+constexpr int INS_R = 64, INS_RS = 64;
 __global__ void __launch_bounds__(256) insert_kernel(float *__restrict__ rows, int rs, int D, int sw,
                                                      int64_t capacity, int64_t cursor, int64_t k,
                                                      const float *__restrict__ s,
@@ -510,18 +510,107 @@ const void *insert_kernel_ptr() { return (const void *)insert_kernel; }
 
 // the sampling gather of a graph-captured byte-state step: event, size and cursor are read
 // from the control block on the device, the event is advanced by the step's last kernel
-int launch_gather_u8_dev(rpl_replay *rp, int64_t n, const rpl_batch *out, cudaStream_t st)
+// Byte-state gather with no CTA-wide barrier (states a multiple of 16 bytes): the 2D state
+// bytes of a sample ([s | s'], s' from the next slot's row with shared states) are cut into
+// GU_PIECE-byte pieces, one CTA task each; every thread draws the sample's index itself
+// (one Philox call) and moves GU_V 16-byte vectors with all loads in flight before its
+// stores.  Piece 0's thread 0 also writes the index and the scalars.
+constexpr int GU_V = 4, GU_T = 256;
+constexpr int64_t GU_PIECE = (int64_t)GU_T * GU_V * 16;   // 16 KB
+__global__ void __launch_bounds__(GU_T) gather_u8_pieces_kernel(
+    const uint8_t *__restrict__ rows, int64_t rsb, int so, int D, int shared, int64_t capacity,
+    uint64_t oldest, int64_t nvalid, int64_t size, int64_t n, const int32_t *__restrict__ idx_in,
+    uint64_t seed, uint32_t rank, uint64_t event, uint8_t *s, uint8_t *s2, int32_t *a, float *r,
+    uint8_t *done, int32_t *idx_out, uint32_t *err, uint64_t *ctrl, const uint64_t *ctrl_in)
 {
-    const rpl::Ring &R = rp->ring;
-    int dev_sms = 148;
-    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, rp->device);
+    if (ctrl_in) {   // graph-replayed train steps: event / size / cursor from the control block
+        event = ctrl_in[0];
+        size = (int64_t)ctrl_in[1];
+        nvalid = shared ? size - 1 : size;
+        oldest = (shared && size == capacity) ? ctrl_in[2] : 0;
+    }
+    if (idx_in == nullptr && ctrl && blockIdx.x == 0 && threadIdx.x == 0) ctrl[0] = event + 1;
+    const int64_t L = 2 * (int64_t)D, np = (L + GU_PIECE - 1) / GU_PIECE;
+    for (int64_t task = blockIdx.x; task < n * np; task += gridDim.x) {
+        const int64_t e = task / np, q = task - e * np;
+        // the sample's slot: lane 0 of every warp draws it (one Philox call), a shuffle shares it
+        int32_t ix = 0;
+        bool bad = false;
+        if ((threadIdx.x & 31) == 0) {
+            if (idx_in == nullptr) {
+                int32_t i0, i1;
+                sample_pair(seed, rank, event, (uint32_t)(e >> 1), (uint64_t)nvalid, i0, i1);
+                ix = slot_of((e & 1) ? i1 : i0, oldest, capacity);
+            } else {
+                ix = idx_in[e];
+                if (ix < 0 || ix >= size) {
+                    bad = true;
+                    ix = min(max(ix, 0), (int32_t)size - 1);
+                }
+            }
+        }
+        ix = __shfl_sync(0xffffffffu, ix, 0);
+        const uint8_t *row = rows + (int64_t)ix * rsb;
+        const uint8_t *row2 = shared ? rows + (int64_t)((ix + 1) % capacity) * rsb : row + D;
+        uint4 v[GU_V];
+        int64_t off[GU_V];
+#pragma unroll
+        for (int i = 0; i < GU_V; ++i) {
+            off[i] = q * GU_PIECE + (int64_t)(i * GU_T + threadIdx.x) * 16;
+            if (off[i] < L)
+                v[i] = __ldg(reinterpret_cast<const uint4 *>(off[i] < D ? row + off[i] : row2 + (off[i] - D)));
+        }
+#pragma unroll
+        for (int i = 0; i < GU_V; ++i) {
+            if (off[i] >= L) continue;
+            if (off[i] < D) {
+                if (s) *reinterpret_cast<uint4 *>(s + e * D + off[i]) = v[i];
+            } else if (s2) {
+                *reinterpret_cast<uint4 *>(s2 + e * D + (off[i] - D)) = v[i];
+            }
+        }
+        if (q == 0 && threadIdx.x == 0) {
+            if (bad) atomicOr(err, ERRBIT_RANGE);
+            if (idx_out) idx_out[e] = ix;
+            const uint32_t *sc = reinterpret_cast<const uint32_t *>(row + so);
+            if (a) a[e] = (int32_t)__ldg(sc);
+            if (r) r[e] = __uint_as_float(__ldg(sc + 1));
+            if (done) done[e] = (uint8_t)(__ldg(sc + 2) != 0u);
+        }
+    }
+}
+
+// the byte-state gather for n samples: the piece kernel when states are 16-byte multiples
+static void launch_gather_u8_any(const rpl::Ring &R, int dev_sms, uint64_t oldest, int64_t nvalid,
+                                 int64_t size, int64_t n, const int32_t *idx_in, uint64_t seed,
+                                 uint32_t rank, uint64_t event, const rpl_batch *out, uint32_t *err,
+                                 uint64_t *ctrl, const uint64_t *ctrl_in, cudaStream_t st)
+{
+    const uint8_t *rows = reinterpret_cast<const uint8_t *>(R.rows);
+    if (R.D % 16 == 0) {
+        const int64_t tasks = n * ((2 * (int64_t)R.D + GU_PIECE - 1) / GU_PIECE);
+        int64_t nb = tasks < (int64_t)dev_sms * 8 ? tasks : (int64_t)dev_sms * 8;
+        if (nb < 1) nb = 1;
+        gather_u8_pieces_kernel<<<(unsigned)nb, GU_T, 0, st>>>(
+            rows, (int64_t)R.rs * 4, R.so, R.D, R.shared, R.capacity, oldest, nvalid, size, n, idx_in,
+            seed, rank, event, static_cast<uint8_t *>(out->s), static_cast<uint8_t *>(out->s_next),
+            out->a, out->r, out->done, out->idx, err, ctrl, ctrl_in);
+        return;
+    }
     int64_t nb = n < (int64_t)dev_sms * 8 ? n : (int64_t)dev_sms * 8;
     if (nb < 1) nb = 1;
     gather_u8_kernel<<<(unsigned)nb, 256, 0, st>>>(
-        reinterpret_cast<const uint8_t *>(R.rows), (int64_t)R.rs * 4, R.so, R.D, R.shared,
-        R.capacity, 0, 0, 0, n, nullptr, rp->seed, rp->rank, 0,
-        static_cast<uint8_t *>(out->s), static_cast<uint8_t *>(out->s_next), out->a, out->r,
-        out->done, out->idx, rp->err_dev, nullptr, rp->ctrl_dev);
+        rows, (int64_t)R.rs * 4, R.so, R.D, R.shared, R.capacity, oldest, nvalid, size, n, idx_in, seed,
+        rank, event, static_cast<uint8_t *>(out->s), static_cast<uint8_t *>(out->s_next), out->a,
+        out->r, out->done, out->idx, err, ctrl, ctrl_in);
+}
+
+int launch_gather_u8_dev(rpl_replay *rp, int64_t n, const rpl_batch *out, cudaStream_t st)
+{
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, rp->device);
+    launch_gather_u8_any(rp->ring, dev_sms, 0, 0, 0, n, nullptr, rp->seed, rp->rank, 0, out,
+                         rp->err_dev, nullptr, rp->ctrl_dev, st);
     RPL_LAUNCHED();
     return RPL_OK;
 }
@@ -638,14 +727,8 @@ int launch_gather(rpl_replay *rp, int64_t n, const int32_t *idx_dev, uint64_t ev
     const int64_t nvalid = sampleable(rp);
     const uint64_t oldest = oldest_slot(rp);
     if (R.u8) {
-        int64_t nb = n < (int64_t)dev_sms * 8 ? n : (int64_t)dev_sms * 8;
-        if (nb < 1) nb = 1;
-        gather_u8_kernel<<<(unsigned)nb, 256, 0, rp->stream>>>(
-            reinterpret_cast<const uint8_t *>(R.rows), (int64_t)R.rs * 4, R.so, R.D, R.shared,
-            R.capacity, oldest, nvalid, rp->size, n,
-            use_sampler ? nullptr : idx_dev, rp->seed, rp->rank, event,
-            static_cast<uint8_t *>(out->s), static_cast<uint8_t *>(out->s_next), out->a, out->r,
-            out->done, out->idx, rp->err_dev, rp->ctrl_dev, nullptr);
+        launch_gather_u8_any(R, dev_sms, oldest, nvalid, rp->size, n, use_sampler ? nullptr : idx_dev,
+                             rp->seed, rp->rank, event, out, rp->err_dev, rp->ctrl_dev, nullptr, rp->stream);
     } else if (R.shared) {
         gather_shared_kernel<<<(unsigned)blocks, 256, 0, rp->stream>>>(
             R.rows, R.rs, R.D, R.sw, R.capacity, nvalid, oldest, rp->size, n,

@@ -8,7 +8,8 @@
 // experiences; with shared states the newest is excluded and u counts from the oldest
 __device__ __forceinline__ int32_t slot_of(int32_t u, uint64_t oldest, int64_t capacity)
 {
-    return (int32_t)((oldest + (uint64_t)u) % (uint64_t)capacity);
+    const uint64_t s = oldest + (uint64_t)u;   // u < capacity and oldest < capacity
+    return (int32_t)(s >= (uint64_t)capacity ? s - (uint64_t)capacity : s);
 }
 #pragma once
 #include <stdint.h>

@@ -150,6 +150,7 @@ __device__ __forceinline__ void operands_ready()
 }
 
 // ---- K1 shared-memory layout (bytes); the host sizes the launch with the same formula ----
+constexpr int T1 = 256;     // K1 threads: group 0 (warps 0-3) gather / layer 0, group 1 (warps 4-7) layer-1 epilogue
 struct FwdSmem {
     int oX, oW0, oW1, oWh, ob0, ob1, oidx, opj, opj2, obar, total;
     __host__ __device__ FwdSmem(int N0, int UN, int J)
@@ -163,18 +164,33 @@ struct FwdSmem {
         oidx = ob1 + UN * 4;                      // sampled slots [128]
         opj = oidx + 128 * 4;                     // deferred-insert index of a row, or -1 [128]
         opj2 = opj + 128 * 4;                     // the same for its s' row (shared states)
-        obar = (opj2 + 128 * 4 + 15) & ~15;       // mbarriers [2] + TMEM base
-        total = obar + 32;
+        obar = (opj2 + 128 * 4 + 15) & ~15;       // mbarriers f0, f1[2], free[2] + TMEM base
+        total = obar + 64;
     }
 };
+
+__device__ __forceinline__ void group0_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(umma::smem_u32(bar)) : "memory");
+}
 
 }  // namespace tc
 
 // ------------------------------------------------------------------------------------------
-// K1 (tensor cores).  TMEM columns: [0, 128) layer-0 accumulator, then the hi plane of H0;
-// [128, 256) the lo plane of H0; [256, 256 + UN) the layer-1 accumulator.
+// K1 (tensor cores), persistent per (net, unit tile of UN layer-1 units): a CTA stages its
+// weight tile once, then runs batch tiles bt = b0, b0 + cpc, ... (cpc CTAs per combo) as a
+// pipeline of two thread groups (TMEM lane = batch row; warp w owns lanes 32 (w % 4) ..):
+//   group 0 (warps 0-3): gather X(i) -> wait F1(i-1) (its A operand, H0, occupies TMEM
+//     [0, 256)) -> F0(i) = X W0^T (thread 0 issues) -> H0 = ReLU(+b0) split into TMEM hi / lo
+//     -> thread 0 issues F1(i) = H0 W1_tile^T into accumulator i % 2
+//   group 1 (warps 4-7): F1(i) done -> H1 = ReLU(+b1) (kept for the online net on s), head
+//     partial sums H1 . W_head -> releases accumulator i % 2
+// so the gather of tile i + 1 and the layer-1 epilogue of tile i overlap the MMAs of F1(i).
+// TMEM columns: [0, 128) layer-0 accumulator, then the hi plane of H0; [128, 256) its lo
+// plane; [256, 256 + UN) and [256 + UN, 256 + 2 UN) the two layer-1 accumulators.
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(tc::T, 1) tc_fwd_kernel(const __grid_constant__ FastArgs p)
+__global__ void __launch_bounds__(tc::T1, 1) tc_fwd_kernel(const __grid_constant__ FastArgs p)
 {
     using namespace tc;
     CtaTrace trace_(p.trace, 0);
@@ -187,22 +203,19 @@ __global__ void __launch_bounds__(tc::T, 1) tc_fwd_kernel(const __grid_constant_
     char *W1h = smc + L.oW1, *W1l = W1h + UN * N0 * 4;
     float *Whs = reinterpret_cast<float *>(smc + L.oWh);
     float *b0s = reinterpret_cast<float *>(smc + L.ob0), *b1s = reinterpret_cast<float *>(smc + L.ob1);
-    int *idxs = reinterpret_cast<int *>(smc + L.oidx), *pjs = reinterpret_cast<int *>(smc + L.opj);
-    int *pjs2 = reinterpret_cast<int *>(smc + L.opj2);
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smc + L.obar);
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(smc + L.obar + 16);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smc + L.obar);   // [0] f0, [1,2] f1, [3,4] free
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(smc + L.obar + 40);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, grp = tid >> 7, r = tid & 127;
+    const int wq = warp & 3;   // TMEM lane quarter of this warp
     if (warp == 0) umma::tmem_alloc(tslot, 512);
     if (tid == 0) {
         umma::mbar_init(&bar[0], 1);
         umma::mbar_init(&bar[1], 1);
+        umma::mbar_init(&bar[2], 1);
+        umma::mbar_init(&bar[3], 128);
+        umma::mbar_init(&bar[4], 128);
         umma::fence_mbar_init();
     }
-    umma::fence_before_sync();
-    __syncthreads();
-    umma::fence_after_sync();
-    const uint32_t tb = *tslot;
-    uint32_t ph0 = 0, ph1 = 0;
     const int nbt = (B + 127) / 128, nut = p.nut;
     const uint64_t event = p.rctrl[0];
     const uint64_t size = p.pend_k ? p.pend_size : p.rctrl[1];
@@ -213,207 +226,236 @@ __global__ void __launch_bounds__(tc::T, 1) tc_fwd_kernel(const __grid_constant_
         p.rctrl[1] = p.pend_size;
         p.rctrl[2] = cursor;
     }
-    const int ncombo = p.nets * nut, ntasks = ncombo * nbt;
-    int loaded = -1;
-    for (int task = blockIdx.x; task < ntasks; task += gridDim.x) {
-        // (net, unit tile)-major: a CTA whose tasks share the combo keeps the weights staged
-        const int combo = task % ncombo, bt = task / ncombo;
-        const int net = combo / nut, ut = combo % nut;
-        const int rb = bt * 128, u0 = ut * UN, nb = min(128, B - rb);
-        const float *theta = net == 1 ? p.target : p.online;
-        const bool reload = combo != loaded;
-        loaded = combo;
-        umma::fence_before_sync();
-        __syncthreads();   // the previous task is done with shared memory and TMEM
-        umma::fence_after_sync();
-        if (reload) {
-            // (1) weights -> tf32 planes.  W1 tile rows u < UN (K = N0): a warp stores 8 rows x
-            // 16 columns per instruction (rows fastest across lanes: conflict-free 16-byte
-            // stores into the core matrices, 64-byte global row pieces)
-            const int kq = N0 / 16, r8 = lane & 7, qq = lane >> 3;
-            for (int g = warp; g < (UN / 8) * kq; g += 4) {
-                const int u = (g / kq) * 8 + r8, k = (g % kq) * 16 + qq * 4;
-                const float4 w = __ldg(reinterpret_cast<const float4 *>(theta + p.w1 + (int64_t)(u0 + u) * N0 + k));
-                split_store4(W1h, W1l, off_k(u, k, N0), w.x, w.y, w.z, w.w, prec);
-            }
-            if (!p.h0_in && tid < N0p) {   // W0 row n = tid (K = D, zero past D)
-                float w[KC];
+    // this CTA's combo and first batch tile: CTAs c, c + ncombo, ... share combo c
+    const int ncombo = p.nets * nut;
+    const int combo = blockIdx.x % ncombo, cpc = gridDim.x / ncombo, bt0 = blockIdx.x / ncombo;
+    const int net = combo / nut, ut = combo % nut, u0 = ut * UN;
+    const float *theta = net == 1 ? p.target : p.online;
+    const bool vtile = p.dueling && u0 < p.S;
+    // (1) the weight tile -> tf32 planes, once.  W1 rows u < UN (K = N0): a warp stores 8 rows
+    // x 16 columns per instruction (conflict-free 16-byte stores, 64-byte global row pieces)
+    {
+        const int kq = N0 / 16, r8 = lane & 7, qq = lane >> 3;
+        for (int g = warp; g < (UN / 8) * kq; g += T1 / 32) {
+            const int u = (g / kq) * 8 + r8, k = (g % kq) * 16 + qq * 4;
+            const float4 w = __ldg(reinterpret_cast<const float4 *>(theta + p.w1 + (int64_t)(u0 + u) * N0 + k));
+            split_store4(W1h, W1l, off_k(u, k, N0), w.x, w.y, w.z, w.w, prec);
+        }
+        if (!p.h0_in) {   // W0 [N0p rows x 32] (K = D, zero past D): 4 consecutive inputs per item
+            for (int e = tid; e < N0p * (KC / 4); e += T1) {
+                const int n = e / (KC / 4), d4 = 4 * (e % (KC / 4));
+                float w[4];
 #pragma unroll
-                for (int d = 0; d < KC; ++d) w[d] = (tid < N0 && d < D) ? __ldg(theta + p.w0 + (int64_t)tid * D + d) : 0.0f;
-#pragma unroll
-                for (int q = 0; q < KC / 4; ++q)
-                    split_store4(W0h, W0l, off_k(tid, 4 * q, KC), w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3], prec);
-            }
-            for (int n = tid; n < N0; n += T) b0s[n] = __ldg(theta + p.b0 + n);
-            for (int u = tid; u < UN; u += T) b1s[u] = __ldg(theta + p.b1 + u0 + u);
-            // head weights of the tile's units: dueling V row (j = 0) over V units, A rows
-            // (j >= 1) over A units (a tile never straddles the streams: S % UN == 0)
-            const bool vtile = p.dueling && u0 < p.S;
-            for (int e = tid; e < J * UN; e += T) {
-                const int j = e / UN, c = e - j * UN;
-                float w = 0.0f;
-                if (!p.dueling) w = __ldg(theta + p.wh + (int64_t)j * N1 + u0 + c);
-                else if (vtile && j == 0) w = __ldg(theta + p.wh + u0 + c);
-                else if (!vtile && j > 0) w = __ldg(theta + p.wh + (int64_t)j * p.S + (u0 - p.S) + c);
-                Whs[e] = w;
+                for (int i = 0; i < 4; ++i)
+                    w[i] = (n < N0 && d4 + i < D) ? __ldg(theta + p.w0 + (int64_t)n * D + d4 + i) : 0.0f;
+                split_store4(W0h, W0l, off_k(n, d4, KC), w[0], w[1], w[2], w[3], prec);
             }
         }
-        const int r = tid;   // this thread's batch row / TMEM lane
-        if (p.h0_in) {
-            // wide inputs (config 5): layer 0 came from wide.cuh; its activations -> TMEM planes
-            const float *h0 = p.h0_in + ((int64_t)net * B + rb + r) * N0;
-            for (int c0 = 0; c0 < N0p; c0 += 16) {
-                uint32_t hh[16], hl[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const float h = (r < nb && c0 + i < N0) ? __ldcg(h0 + c0 + i) : 0.0f;
-                    split_p(h, hh[i], hl[i], prec);
+        for (int n = tid; n < N0; n += T1) b0s[n] = __ldg(theta + p.b0 + n);
+        for (int u = tid; u < UN; u += T1) b1s[u] = __ldg(theta + p.b1 + u0 + u);
+        // head weights of the tile's units: dueling V row (j = 0) over V units, A rows
+        // (j >= 1) over A units (a tile never straddles the streams: S % UN == 0)
+        for (int e = tid; e < J * UN; e += T1) {
+            const int j = e / UN, c = e - j * UN;
+            float w = 0.0f;
+            if (!p.dueling) w = __ldg(theta + p.wh + (int64_t)j * N1 + u0 + c);
+            else if (vtile && j == 0) w = __ldg(theta + p.wh + u0 + c);
+            else if (!vtile && j > 0) w = __ldg(theta + p.wh + (int64_t)j * p.S + (u0 - p.S) + c);
+            Whs[e] = w;
+        }
+    }
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tb = *tslot;
+    trace_.mark(2);
+    int it = 0;
+    for (int bt = bt0; bt < nbt; bt += cpc, ++it) {
+        const int rb = bt * 128, nb = min(128, B - rb);
+        const uint32_t accA = tb + 256 + (uint32_t)(UN * (it & 1));
+        if (grp == 0) {
+            // ---------------- group 0: gather, layer 0, issue layer 1 ----------------------
+            long long tg = trace_.now();
+            if (!p.h0_in) {
+                // (2) Philox sample of row rb + r (Q3): index 2j / 2j + 1 of call j
+                const int row = rb + r;
+                int32_t slot = 0;
+                if (p.bidx) {
+                    slot = row < B ? p.bidx[row] : 0;
+                } else if (p.distinct) {
+                    slot = row < B ? p.idx[row] : 0;
+                } else {
+                    int32_t i0, i1;
+                    sample_pair(p.seed, p.rank, event, (uint32_t)(row >> 1), nvalid, i0, i1);
+                    slot = slot_of((row & 1) ? i1 : i0, oldest, p.capacity);
                 }
-                st16(lane_addr(tb, warp, c0), hh);
-                if (prec == 0) st16(lane_addr(tb, warp, 128 + c0), hl);
+                auto pend_j = [&](int64_t sl) {
+                    int64_t j = sl - p.pend_cur;
+                    if (j < 0) j += p.capacity;
+                    return j < p.pend_k ? (int)j : -1;
+                };
+                const int pj = pend_j(slot);
+                const bool nxt = net != 0 && p.shared;    // shared states: s' = next slot's s
+                const int64_t sslot = nxt ? (slot + 1) % p.capacity : slot;
+                const int pjx = nxt ? pend_j(sslot) : pj;
+                const int col0 = net == 0 || p.shared ? 0 : D;
+                // (3) the row's state into registers (pending slots read through from the
+                // insert's sources, possibly pinned host memory)
+                float x[KC];
+                const int64_t rslot = p.bidx ? min(row, B - 1) : sslot;   // in-RAM: the copied batch
+                const float *src = pjx < 0 ? p.ring + rslot * p.rs + col0
+                                           : (net == 0 || p.shared ? p.pend_s : p.pend_s2) + (int64_t)pjx * D;
+#pragma unroll
+                for (int d = 0; d < KC; ++d) x[d] = (d < D && r < nb) ? src[d] : 0.0f;
+                if (net == 0 && ut == 0 && r < nb) {
+                    int32_t ra;
+                    float rr;
+                    uint32_t rd;
+                    if (pj < 0) {
+                        const float *sc = p.ring + (int64_t)(p.bidx ? row : slot) * p.rs + p.sw;
+                        ra = __float_as_int(__ldg(sc));
+                        rr = __ldg(sc + 1);
+                        rd = __float_as_uint(__ldg(sc + 2));
+                    } else {
+                        ra = p.pend_a[pj];
+                        rr = p.pend_r[pj];
+                        rd = p.pend_done[pj];
+                    }
+                    p.idx[row] = slot;
+                    p.a[row] = ra;
+                    p.r[row] = rr;
+                    p.done[row] = (uint8_t)(rd != 0u);
+                }
+                if (ut == 0 && net <= 1 && r < nb) {
+                    float *xo = (net == 0 ? p.Xs : p.Xs2) + (int64_t)row * D;
+                    for (int d = 0; d < D; ++d) xo[d] = x[d];
+                }
+#pragma unroll
+                for (int q = 0; q < KC / 4; ++q)
+                    split_store4(Xh, Xl, off_k(r, 4 * q, KC), x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3], prec);
+                umma::fence_async_smem();
+            }
+            trace_.acc(3, tg);   // phase 3: gather
+            tg = trace_.now();
+            // F1(it - 1) has finished reading H0 (TMEM [0, 256))
+            if (it > 0) umma::mbar_wait(&bar[1 + ((it - 1) & 1)], (uint32_t)(((it - 1) >> 1) & 1));
+            umma::fence_after_sync();
+            trace_.acc(4, tg);   // phase 4: wait for F1(it - 1)
+            tg = trace_.now();
+            if (p.h0_in) {
+                // wide inputs (config 5): layer 0 came from wide.cuh -> its activations into TMEM
+                const float *h0 = p.h0_in + ((int64_t)net * B + rb + r) * N0;
+                for (int c0 = 0; c0 < N0p; c0 += 16) {
+                    uint32_t hh[16], hl[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const float h = (r < nb && c0 + i < N0) ? __ldcg(h0 + c0 + i) : 0.0f;
+                        split_p(h, hh[i], hl[i], prec);
+                    }
+                    st16(lane_addr(tb, wq, c0), hh);
+                    if (prec == 0) st16(lane_addr(tb, wq, 128 + c0), hl);
+                }
+            } else {
+                group0_sync();   // every row of X is in shared memory
+                // (4) layer 0 on the tensor cores: D0[128][N0p] = X W0^T
+                if (tid == 0) {
+                    umma::fence_after_sync();
+                    const uint32_t id = idesc(128, N0p);
+#pragma unroll
+                    for (int s = 0; s < KC / 8; ++s)
+                        mma3_ss(tb, kdesc(Xh, s, KC), kdesc(Xl, s, KC), kdesc(W0h, s, KC), kdesc(W0l, s, KC), id,
+                                s > 0 ? 1u : 0u, prec);
+                    umma::commit(&bar[0]);
+                }
+                umma::mbar_wait(&bar[0], (uint32_t)(it & 1));
+                umma::fence_after_sync();
+                trace_.acc(5, tg);   // phase 5: layer-0 MMAs (issue + wait)
+                tg = trace_.now();
+                // H0 = ReLU(D0 + b0) -> hi plane over D0, lo plane at column 128
+                const bool keep = net == 0 && ut == 0 && r < nb;
+                for (int c0 = 0; c0 < N0p; c0 += 16) {
+                    uint32_t v[16], hl[16];
+                    ld16(lane_addr(tb, wq, c0), v);
+                    wait_ld();
+                    float h[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int c = c0 + i;
+                        h[i] = c < N0 ? fmaxf(__uint_as_float(v[i]) + b0s[c], 0.0f) : 0.0f;
+                        split_p(h[i], v[i], hl[i], prec);
+                    }
+                    if (keep) {
+                        float *ho = p.H0 + (int64_t)(rb + r) * N0 + c0;
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4)
+                            if (c0 + i < N0) *reinterpret_cast<float4 *>(ho + i) = make_float4(h[i], h[i + 1], h[i + 2], h[i + 3]);
+                    }
+                    st16(lane_addr(tb, wq, c0), v);
+                    if (prec == 0) st16(lane_addr(tb, wq, 128 + c0), hl);
+                }
+            }
+            wait_st();
+            umma::fence_before_sync();
+            group0_sync();   // H0 complete in TMEM
+            trace_.acc(6, tg);   // phase 6: layer-0 epilogue
+            // (5) layer 1: D1[128][UN] = H0 W1_tile^T into accumulator it % 2 (free once group 1
+            // has drained it for tile it - 2)
+            if (tid == 0) {
+                umma::fence_after_sync();
+                if (it >= 2) umma::mbar_wait(&bar[3 + (it & 1)], (uint32_t)(((it - 2) >> 1) & 1));
+                umma::fence_after_sync();
+                const uint32_t id = idesc(128, UN);
+                for (int s = 0; s < N0 / 8; ++s)
+                    mma3_ts(accA, tb + 8 * s, tb + 128 + 8 * s, kdesc(W1h, s, N0), kdesc(W1l, s, N0), id,
+                            s > 0 ? 1u : 0u, prec);
+                umma::commit(&bar[1 + (it & 1)]);
             }
         } else {
-            // (2) Philox sample of row rb + r (Q3): index 2j and 2j + 1 of call j
-            const int row = rb + r;
-            int32_t slot = 0;
-            if (p.bidx) {
-                slot = row < B ? p.bidx[row] : 0;
-            } else if (p.distinct) {
-                slot = row < B ? p.idx[row] : 0;
-            } else {
-                int32_t i0, i1;
-                sample_pair(p.seed, p.rank, event, (uint32_t)(row >> 1), nvalid, i0, i1);
-                slot = slot_of((row & 1) ? i1 : i0, oldest, p.capacity);
-            }
-            auto pend_j = [&](int64_t s) {
-                int64_t j = s - p.pend_cur;
-                if (j < 0) j += p.capacity;
-                return j < p.pend_k ? (int)j : -1;
-            };
-            const int pj = pend_j(slot);
-            const bool nxt = net != 0 && p.shared;    // shared states: s' = next slot's s
-            const int64_t sslot = nxt ? (slot + 1) % p.capacity : slot;
-            const int pjx = nxt ? pend_j(sslot) : pj;
-            const int col0 = net == 0 || p.shared ? 0 : D;
-            // (3) gather the row's state into registers (pending slots read through from the
-            // insert's sources, possibly pinned host memory)
-            float x[KC];
-            const int64_t rslot = p.bidx ? min(row, B - 1) : sslot;   // in-RAM: the copied batch
-            const float *src = pjx < 0 ? p.ring + rslot * p.rs + col0
-                                       : (net == 0 || p.shared ? p.pend_s : p.pend_s2) + (int64_t)pjx * D;
+            // ---------------- group 1: layer-1 epilogue of tile it ----------------------------
+            const long long tw = trace_.now_by(128);
+            umma::mbar_wait(&bar[1 + (it & 1)], (uint32_t)((it >> 1) & 1));
+            umma::fence_after_sync();
+            trace_.acc_by(128, 7, tw);   // phase 7: group 1 waiting for F1(it)
+            // (6) H1 = ReLU(D1 + b1) (kept for the online net on s) and the tile's head partials
+            float acc[MAXJ];
 #pragma unroll
-            for (int d = 0; d < KC; ++d) x[d] = (d < D && r < nb) ? src[d] : 0.0f;
-            if (net == 0 && ut == 0 && r < nb) {
-                int32_t ra;
-                float rr;
-                uint32_t rd;
-                if (pj < 0) {
-                    const float *sc = p.ring + (int64_t)(p.bidx ? row : slot) * p.rs + p.sw;
-                    ra = __float_as_int(__ldg(sc));
-                    rr = __ldg(sc + 1);
-                    rd = __float_as_uint(__ldg(sc + 2));
-                } else {
-                    ra = p.pend_a[pj];
-                    rr = p.pend_r[pj];
-                    rd = p.pend_done[pj];
-                }
-                p.idx[row] = slot;
-                p.a[row] = ra;
-                p.r[row] = rr;
-                p.done[row] = (uint8_t)(rd != 0u);
-            }
-            if (ut == 0 && net <= 1 && r < nb) {
-                float *xo = (net == 0 ? p.Xs : p.Xs2) + (int64_t)row * D;
-                for (int d = 0; d < D; ++d) xo[d] = x[d];
-            }
-#pragma unroll
-            for (int q = 0; q < KC / 4; ++q)
-                split_store4(Xh, Xl, off_k(r, 4 * q, KC), x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3], prec);
-            trace_.mark(2);
-            operands_ready();
-            // (4) layer 0 on the tensor cores: D0[128][N0p] = X W0^T
-            if (tid == 0) {
-                const uint32_t id = idesc(128, N0p);
-#pragma unroll
-                for (int s = 0; s < KC / 8; ++s)
-                    mma3_ss(tb, kdesc(Xh, s, KC), kdesc(Xl, s, KC), kdesc(W0h, s, KC), kdesc(W0l, s, KC), id,
-                            s > 0 ? 1u : 0u, prec);
-                umma::commit(&bar[0]);
-            }
-            wait_bar(&bar[0], ph0);
-            // H0 = ReLU(D0 + b0) -> hi plane over D0, lo plane at column 128
-            const bool keep = net == 0 && ut == 0 && r < nb;
-            for (int c0 = 0; c0 < N0p; c0 += 16) {
-                uint32_t v[16], hl[16];
-                ld16(lane_addr(tb, warp, c0), v);
+            for (int j = 0; j < MAXJ; ++j) acc[j] = 0.0f;
+            const bool keep1 = net == 0 && r < nb;
+            for (int c0 = 0; c0 < UN; c0 += 16) {
+                uint32_t v[16];
+                ld16(lane_addr(accA, wq, c0), v);
                 wait_ld();
                 float h[16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int c = c0 + i;
-                    h[i] = c < N0 ? fmaxf(__uint_as_float(v[i]) + b0s[c], 0.0f) : 0.0f;
-                    split_p(h[i], v[i], hl[i], prec);
+                for (int i = 0; i < 16; ++i) h[i] = fmaxf(__uint_as_float(v[i]) + b1s[c0 + i], 0.0f);
+                if (keep1) {
+                    float *ho = p.H1 + (int64_t)(rb + r) * N1 + u0 + c0;
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4 *>(ho + i) = make_float4(h[i], h[i + 1], h[i + 2], h[i + 3]);
                 }
-                if (keep) {
-                    float *ho = p.H0 + (int64_t)(rb + r) * N0 + c0;
+                if (vtile) {
 #pragma unroll
-                    for (int i = 0; i < 16; i += 4)
-                        if (c0 + i < N0) *reinterpret_cast<float4 *>(ho + i) = make_float4(h[i], h[i + 1], h[i + 2], h[i + 3]);
-                }
-                st16(lane_addr(tb, warp, c0), v);
-                if (prec == 0) st16(lane_addr(tb, warp, 128 + c0), hl);
-            }
-            trace_.mark(3);
-        }
-        operands_ready();
-        // (5) layer 1: D1[128][UN] = H0 W1_tile^T, A (H0 planes) from TMEM
-        if (tid == 0) {
-            const uint32_t id = idesc(128, UN);
-            for (int s = 0; s < N0 / 8; ++s)
-                mma3_ts(tb + 256, tb + 8 * s, tb + 128 + 8 * s, kdesc(W1h, s, N0), kdesc(W1l, s, N0), id,
-                        s > 0 ? 1u : 0u, prec);
-            umma::commit(&bar[1]);
-        }
-        wait_bar(&bar[1], ph1);
-        trace_.mark(4);
-        // (6) H1 = ReLU(D1 + b1) (kept for the online net on s) and the tile's head partials
-        const bool vtile = p.dueling && u0 < p.S;
-        float acc[MAXJ];
+                    for (int i = 0; i < 16; ++i) acc[0] = fmaf(h[i], Whs[c0 + i], acc[0]);
+                } else {
 #pragma unroll
-        for (int j = 0; j < MAXJ; ++j) acc[j] = 0.0f;
-        const bool keep1 = net == 0 && r < nb;
-        for (int c0 = 0; c0 < UN; c0 += 16) {
-            uint32_t v[16];
-            ld16(lane_addr(tb, warp, 256 + c0), v);
-            wait_ld();
-            float h[16];
+                    for (int j = 0; j < MAXJ; ++j) {
+                        if (j < J && (p.dueling ? j > 0 : true)) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) h[i] = fmaxf(__uint_as_float(v[i]) + b1s[c0 + i], 0.0f);
-            if (keep1) {
-                float *ho = p.H1 + (int64_t)(rb + r) * N1 + u0 + c0;
-#pragma unroll
-                for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4 *>(ho + i) = make_float4(h[i], h[i + 1], h[i + 2], h[i + 3]);
-            }
-            if (vtile) {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) acc[0] = fmaf(h[i], Whs[c0 + i], acc[0]);
-            } else {
-#pragma unroll
-                for (int j = 0; j < MAXJ; ++j) {
-                    if (j < J) {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) acc[j] = fmaf(h[i], Whs[j * UN + c0 + i], acc[j]);
+                            for (int i = 0; i < 16; ++i) acc[j] = fmaf(h[i], Whs[j * UN + c0 + i], acc[j]);
+                        }
                     }
                 }
             }
-        }
-        if (r < nb) {
-            float *po = p.part + (((int64_t)net * nut + ut) * B + rb + r) * J;
+            umma::fence_before_sync();
+            mbar_arrive(&bar[3 + (it & 1)]);   // accumulator it % 2 drained
+            if (r < nb) {
+                float *po = p.part + (((int64_t)net * nut + ut) * B + rb + r) * J;
 #pragma unroll
-            for (int j = 0; j < MAXJ; ++j)
-                if (j < J) po[j] = acc[j];
+                for (int j = 0; j < MAXJ; ++j)
+                    if (j < J) po[j] = acc[j];
+            }
         }
-        trace_.mark(5);
     }
     umma::fence_before_sync();
     __syncthreads();
@@ -490,10 +532,13 @@ __global__ void __launch_bounds__(tc::T, 1) tc_bwd_kernel(const __grid_constant_
             bool pend[2] = {false, false};
             for (int c = 0; c < nch; ++c) {
                 const int st = c & 1;
+                long long tw = trace_.now();
                 if (pend[st]) {   // the MMAs of chunk c - 2 are done with this stage
                     wait_bar(&bar[st], ph[st]);
                     pend[st] = false;
                 }
+                trace_.acc(3, tw);
+                const long long ts = trace_.now();
                 char *Sh = smc + (st ? L.oS1 : L.oS0), *Sl = Sh + 128 * KC * 4;
                 float *whs = reinterpret_cast<float *>(smc + L.owh) + st * MAXJ * KC;
                 const int uc = ua + KC * c;
@@ -546,6 +591,7 @@ __global__ void __launch_bounds__(tc::T, 1) tc_bwd_kernel(const __grid_constant_
                     split_store4(Sh, Sl, off_k(tid, 4 * q, KC), z[0], z[1], z[2], z[3], prec);
                 }
                 operands_ready();
+                trace_.acc(2, ts);
                 if (tid == 0) {
                     const uint32_t id = idesc(128, Nb);
 #pragma unroll
@@ -557,11 +603,14 @@ __global__ void __launch_bounds__(tc::T, 1) tc_bwd_kernel(const __grid_constant_
                 pend[st] = true;
             }
             // drain in chunk order
+            long long tw = trace_.now();
             for (int c = max(0, nch - 2); c < nch; ++c)
                 if (pend[c & 1]) {
                     wait_bar(&bar[c & 1], ph[c & 1]);
                     pend[c & 1] = false;
                 }
+            trace_.acc(3, tw);
+            const long long te = trace_.now();
             const int k = tid;   // TMEM lane = layer-0 unit
             if (p.PdH0) {
                 // wide inputs: the partial dH0 goes to memory; K4 forms dZ0 (wide.cuh dW0)
@@ -636,6 +685,7 @@ __global__ void __launch_bounds__(tc::T, 1) tc_bwd_kernel(const __grid_constant_
                     wait_ld();
                 }
             }
+            trace_.acc(5, te);
         } else {
             // ---------------- (A) dW1 and dWh for 128 units over one batch split ------------
             const int a = task - nB;
@@ -659,10 +709,13 @@ __global__ void __launch_bounds__(tc::T, 1) tc_bwd_kernel(const __grid_constant_
             bool pend[2] = {false, false};
             for (int c = 0; c < nch; ++c) {
                 const int st = c & 1;
+                long long tw = trace_.now();
                 if (pend[st]) {
                     wait_bar(&bar[st], ph[st]);
                     pend[st] = false;
                 }
+                trace_.acc(3, tw);
+                const long long ts = trace_.now();
                 char *Hh = smc + (st ? L.oS1 : L.oS0), *Hl = Hh + 128 * KC * 4;
                 char *Gh = Hl + 128 * KC * 4, *Gl = Gh + 32 * KC * 4;
                 float *dhs = reinterpret_cast<float *>(smc + L.owh) + st * MAXJ * KC;   // [i][J]
@@ -724,6 +777,7 @@ __global__ void __launch_bounds__(tc::T, 1) tc_bwd_kernel(const __grid_constant_
                 if (ut3 == 0 && tid < J)   // head-bias gradient sum_b dHead[b][j], by task ut3 = 0
                     for (int i = 0; i < KC; ++i) dbh += dhs[i * J + tid];
                 operands_ready();
+                trace_.acc(4, ts);
                 if (tid == 0) {
                     const uint32_t idw = idesc(128, N0p), idh = idesc(128, JP);
                     const uint32_t cb = tb + 256 + 128 * st;

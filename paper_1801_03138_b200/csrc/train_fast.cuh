@@ -112,9 +112,11 @@ __device__ __forceinline__ unsigned long long gtimer()
 // the CTA started when tracing is on (RPL_TRACE=1)
 struct CtaTrace {
     unsigned long long *slot;
+    unsigned long long *any;   // this CTA's trace words, for any thread (acc_by)
     long long c0;
     __device__ CtaTrace(unsigned long long *tr, int kernel)
-        : slot(tr && threadIdx.x == 0 ? tr + 8 * ((size_t)kernel * 2048 + blockIdx.x) : nullptr), c0(0)
+        : slot(tr && threadIdx.x == 0 ? tr + 8 * ((size_t)kernel * 2048 + blockIdx.x) : nullptr),
+          any(tr ? tr + 8 * ((size_t)kernel * 2048 + blockIdx.x) : nullptr), c0(0)
     {
         if (slot) {
             slot[0] = gtimer();
@@ -128,6 +130,18 @@ struct CtaTrace {
     __device__ void mark(int i)
     {
         if (slot) slot[i] = (unsigned long long)(clock64() - c0);
+    }
+    // accumulate the cycles since `t` into slot i (phase totals of a CTA)
+    __device__ void acc(int i, long long t)
+    {
+        if (slot) slot[i] += (unsigned long long)(clock64() - t);
+    }
+    __device__ long long now() const { return slot ? clock64() : 0; }
+    // the same from thread `who` of the CTA (e.g. the first thread of another warp group)
+    __device__ long long now_by(int who) const { return any && (int)threadIdx.x == who ? clock64() : 0; }
+    __device__ void acc_by(int who, int i, long long t)
+    {
+        if (any && (int)threadIdx.x == who) any[i] += (unsigned long long)(clock64() - t);
     }
 };
 

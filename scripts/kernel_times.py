@@ -76,19 +76,28 @@ def main():
 
 
 def trace_main():
-    """RPL_TRACE=1: per-CTA start/end of the four fast-path kernels of one step"""
+    """RPL_TRACE=1: per-CTA start/end of the four fast-path kernels of the last step, and the
+    per-CTA phase marks (cycles after CTA start; for the tensor-core K3, accumulated phase
+    cycles over all steps, printed per step)"""
     os.environ["RPL_TRACE"] = "1"
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--trace", action="store_true")
+    ap.add_argument("--batch", type=int, default=128)
+    ap.add_argument("--ddqn", action="store_true")
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--accum", action="store_true", help="marks are per-phase cycle totals (tc kernels)")
+    a = ap.parse_args()
     import paper_1801_03138_b200.binding as b
     from inputs import experiences, init_params
-    cfg = b.DQNConfig(max_batch=128)
+    cfg = b.DQNConfig(max_batch=a.batch, double_dqn=a.ddqn)
     rp = b.Replay(1_000_000, 27, seed=2)
     rp.add_many(experiences(1_000_000, seed=1))
     dqn = b.DQN(cfg, init_params(seed=3))
     loss = torch.zeros(1, device="cuda")
-    for i in range(100):
-        dqn.train_step(rp, 128, loss)
+    for i in range(a.steps):
+        dqn.train_step(rp, a.batch, loss)
     torch.cuda.synchronize()
-    tr = dqn.debug(b.RPL_DBG_TRACE, 128).astype(np.int64)
+    tr = dqn.debug(b.RPL_DBG_TRACE, a.batch).astype(np.int64)
     t0 = min(tr[k][tr[k][:, 0] > 0][:, 0].min() for k in range(4) if (tr[k][:, 0] > 0).any())
     names = ["K1 fwd", "K2 td", "K3 bwd1", "K4 bwd0+sgd"]
     for k in range(4):
@@ -104,7 +113,11 @@ def trace_main():
             mm = m & (tr[k][:, ph] > 0)
             if mm.any():
                 rel = tr[k][mm, ph] / 1965.0   # SM cycles -> us at the 1965 MHz max clock
-                print(f"    mark {ph}: {rel.mean():6.2f} us after CTA start (max {rel.max():6.2f}, n={mm.sum()})")
+                if a.accum and (k == 2 or (k == 0 and ph >= 3)):   # accumulated phase totals (tc kernels)
+                    rel = rel / a.steps
+                    print(f"    phase {ph}: {rel.mean():6.2f} us per step per CTA (max {rel.max():6.2f}, n={mm.sum()})")
+                else:
+                    print(f"    mark {ph}: {rel.mean():6.2f} us after CTA start (max {rel.max():6.2f}, n={mm.sum()})")
 
 
 if __name__ == "__main__":
