@@ -29,6 +29,7 @@
 #include "simt_gemm.cuh"
 #include "train_fast.cuh"
 #include "tc_fast.cuh"
+#include "tc_big.cuh"
 #include "wide.cuh"
 #include "dp_peer.cuh"
 
@@ -768,6 +769,10 @@ struct rpl_dqn {
     // fast path (two trunk layers): head partials, dH0 split-K partials, device counters
     bool fast = false;
     bool tc = false;                 // the fast path's K1 / K3 on tcgen05 (tc_fast.cuh)
+    bool tcb = false;                // large batches: tc_big.cuh's step (B >= kTcbMinBatch)
+    uint16_t *h0img = nullptr, *ximg = nullptr, *dz1img = nullptr, *w1img = nullptr;
+    float *dheadp = nullptr;
+    int64_t tcb_h0pl = 0, tcb_xpl = 0, tcb_dzpl = 0, tcb_w1pl = 0;
     float *part = nullptr, *dH0p = nullptr;
     int64_t part_elems = 0, dh0p_elems = 0;
     int64_t *step_dev = nullptr;
@@ -804,7 +809,8 @@ struct rpl_dqn {
     float *PdH0 = nullptr;                 // wide_fast: K3's dH0 partials [32][max_batch][N0]
     uint16_t *w0bf = nullptr;              // bf16 planes of W0 [online, target][3][N0 * D]
     uint16_t *dz0bf = nullptr;             // bf16 planes of dZ0 [3][max_batch][N0]
-    bool w0bf_stale = true;                // planes to be re-split from the fp32 weights
+    bool w0bf_stale = true;                // wide W0 bf16 planes to be re-split from the fp32 weights
+    bool w1img_stale = true;               // tcb: W1 images to be re-split (any update not K4's)
     int wide_ks = 0, wide_cs = 1;          // wide_l0_kernel chunks and cluster size (wide_l0_plan)
     int k1_mc_clusters = 0;                // co-resident clusters of the multicast K1 (0: not used)
     unsigned long long *trace = nullptr;   // RPL_TRACE=1: per-CTA timestamps of the fast kernels
@@ -998,6 +1004,44 @@ static int tc_ns_for(const rpl_dqn *d, int B)
     return ns;
 }
 static size_t tc_fwd_smem(const rpl_dqn *d, int un) { return (size_t)tc::FwdSmem(d->N[0], un, d->J).total; }
+
+// ---- large-batch tensor-core step (tc_big.cuh) ----------------------------------------------
+// shapes: 128 layer-0 units, fp32 states of <= 31 floats, layer-1 units and dueling streams in
+// 128-unit tiles, at most tcb::JW head outputs per tile (dueling |A| <= 8), FP32 or BF16
+// precision (TF32 keeps the mma.sync kernels)
+static bool tcb_shape_ok(const rpl_dqn *d)
+{
+    const rpl_dqn_config &c = d->cfg;
+    const int hw = c.dueling ? c.n_actions : d->J;
+    return d->T == 2 && d->N[0] == tcb::N0 && c.state_dim <= 31 && d->N[1] % 128 == 0 &&
+           (!c.dueling || c.stream % 128 == 0) && hw <= tcb::JW && d->J <= tcb::JPMAX &&
+           d->woff[1] % 4 == 0 && c.precision != RPL_PREC_TF32;
+}
+// batches from here up take the tensor-core step (below it the mma.sync kernels: the step is
+// latency-bound there)
+static constexpr int kTcbMinBatch = 512;
+static int tcb_min_batch()
+{
+#ifdef RPL_EXPERIMENTS
+    if (const char *v = getenv("RPL_TCB_MIN")) return atoi(v);
+#endif
+    return kTcbMinBatch;
+}
+// T3a chunk groups: one CTA per (unit tile, group), about one wave
+static int tcb_G(const rpl_dqn *d, int Bp)
+{
+    const int nch = Bp / 64, nut = d->N[1] / 128;
+    return std::max(1, std::min(nch, d->sms / nut));
+}
+// T3b splits of the layer-1 units (64-unit chunks): a power of two with splits x tiles <= sms
+static int tcb_NQ(const rpl_dqn *d, int Bp)
+{
+    const int nbt = Bp / 128, mx = d->N[1] / 64;
+    int q = 1;
+    while (q * 2 <= mx && q * 2 * nbt <= d->sms && d->N[1] % (q * 2 * 64) == 0) q *= 2;
+    return q;
+}
+static int tcb_t0_smem(const rpl_dqn *d) { return (2 * tcb::N0 * d->cfg.state_dim + 2 * tcb::N0 + tcb::T0_ROWS * 2 * 33) * 4; }
 
 extern "C" int dqn_destroy(rpl_dqn *d)
 {
@@ -1198,6 +1242,40 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
         ok = ok && fast_td_smem(d) <= 200 * 1024 &&
              cudaFuncSetAttribute(fast_td_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   fast_td_smem(d)) == cudaSuccess;
+    }
+    if (ok && d->fast && tcb_shape_ok(d) && Bm >= tcb_min_batch()) {
+        const int64_t Bpm = ((int64_t)Bm + 127) / 128 * 128;
+        d->tcb = true;
+        d->tcb_h0pl = Bpm * tcb::N0;
+        d->tcb_xpl = Bpm * tcb::XW;
+        d->tcb_dzpl = Bpm * d->N[1];
+        d->tcb_w1pl = (int64_t)d->N[1] * tcb::N0;
+        const int jp = (d->J + 3) & ~3;
+        ok = dalloc(d, &d->h0img, (size_t)3 * nets * d->tcb_h0pl) && dalloc(d, &d->ximg, (size_t)3 * d->tcb_xpl) &&
+             dalloc(d, &d->dz1img, (size_t)3 * d->tcb_dzpl) && dalloc(d, &d->w1img, (size_t)6 * d->tcb_w1pl) &&
+             dalloc(d, &d->dheadp, (size_t)Bpm * jp);
+        // T3a partial gradients [G][gps]; T3b dW0 | db0 partials [NQ * tiles][w1] with
+        // NQ * tiles <= max(sms, tiles)
+        const int64_t gps = (d->P + 3) & ~(int64_t)3;
+        const int64_t gneed = (int64_t)tcb_G(d, (int)Bpm) * gps;
+        if (ok && gneed > d->gpart_elems) {
+            ok = dalloc(d, &d->gpart, (size_t)gneed);
+            d->gpart_elems = gneed;
+        }
+        const int64_t wneed = (int64_t)std::max<int64_t>(d->sms, Bpm / 128) * d->woff[1];
+        if (ok && wneed > d->dh0p_elems) {
+            ok = dalloc(d, &d->dH0p, (size_t)wneed);
+            d->dh0p_elems = wneed;
+        }
+        const int64_t pneed = (int64_t)nets * (d->N[1] / 64) * Bm * d->J;
+        if (ok && pneed > d->part_elems) {
+            ok = dalloc(d, &d->part, (size_t)pneed);
+            d->part_elems = pneed;
+        }
+        ok = ok && cudaFuncSetAttribute(tcb_l0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tcb_t0_smem(d)) == cudaSuccess &&
+             cudaFuncSetAttribute(tcb_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tcb::T1Smem(d->J).total) == cudaSuccess &&
+             cudaFuncSetAttribute(tcb_dw1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tcb::T3aSmem(d->J).total) == cudaSuccess &&
+             cudaFuncSetAttribute(tcb_dh0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tcb::T3bSmem().total) == cudaSuccess;
     }
     if (!ok) {
         if (!coop) set_error("dqn_create: device %d lacks cooperative launch", d->device);
@@ -1456,6 +1534,25 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
         p.gpart = p.nsb == 1 ? d->grad : d->gpart;
         p.nw0 = p.NS * ((B + 127) / 128);
     }
+    if (d->tcb && B >= tcb_min_batch()) {
+        p.tc = 0;
+        p.tcb = 1;
+        p.Bp = (B + 127) / 128 * 128;
+        p.jp = (d->J + 3) & ~3;
+        p.h0img = d->h0img;
+        p.ximg = d->ximg;
+        p.dz1img = d->dz1img;
+        p.w1img = d->w1img;
+        p.h0pl = d->tcb_h0pl;
+        p.xpl = d->tcb_xpl;
+        p.dzpl = d->tcb_dzpl;
+        p.w1pl = d->tcb_w1pl;
+        p.dheadp = d->dheadp;
+        p.nsb = tcb_G(d, p.Bp);           // T3a chunk groups = K4's gradient splits
+        p.gpart = p.nsb == 1 ? d->grad : d->gpart;
+        p.NS = tcb_NQ(d, p.Bp);
+        p.nw0 = p.NS * (p.Bp / 128);
+    }
     const rpl_replay::Pending &q = rp->pend;
     if (q.k > 0) {   // consumed by this step's K1 (dqn_train_step clears it)
         p.pend_k = (int)q.k;
@@ -1516,8 +1613,32 @@ static cudaError_t tc_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
     return launch_pdl(fast_bwd0_sgd_kernel, d->sms, NT, 0, st, pdl || d->k4_pdl, p);
 }
 
+// the large-batch step (tc_big.cuh), enqueued on `st`
+static cudaError_t tcb_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
+{
+    cudaError_t e;
+    if (p.distinct) {   // distinct batch indices first (distinct.cuh)
+        e = launch_pdl(distinct_fast_kernel, 1, DS_T, ds_smem_bytes(p.B), st, false, p);
+        if (e != cudaSuccess) return e;
+    }
+    const int nbt = p.Bp / 128, nut = p.N1 / 128, ncombo = p.nets * nut;
+    e = launch_pdl(tcb_l0_kernel, p.Bp / tcb::T0_ROWS, tcb::T0_T, tcb_t0_smem(d), st, false, p);
+    if (e != cudaSuccess) return e;
+    const int cpc = std::max(1, std::min(nbt, d->sms / ncombo));
+    e = launch_pdl(tcb_fwd_kernel, ncombo * cpc, tcb::T1_T, tcb::T1Smem(p.J).total, st, false, p);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(tcb_td_kernel, (p.B + 7) / 8, 256, 0, st, false, p);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(tcb_dw1_kernel, nut * p.nsb, tcb::T3A_T, tcb::T3aSmem(p.J).total, st, false, p);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(tcb_dh0_kernel, nbt * p.NS, tcb::T3B_T, tcb::T3bSmem().total, st, false, p);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(fast_bwd0_sgd_kernel, d->sms, NT, 0, st, false, p);
+}
+
 static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
 {
+    if (p.tcb) return tcb_enqueue(d, p, st);
     if (p.tc) return tc_enqueue(d, p, st);
     const int nbt = (p.B + F_BT - 1) / F_BT;
     const int k1_tasks = p.nets * nbt * p.nut;
@@ -1713,6 +1834,19 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             fp.ring = const_cast<float *>(rows);
             fp.bidx = bidx;
         }
+        if (fp.tcb && d->w1img_stale) {   // after create / set_params / sync_target / a DP or small-batch update
+            tcb_w1_split_kernel<<<d->sms, 256, 0, d->stream>>>(d->online + d->woff[1], d->w1img, d->tcb_w1pl, d->N[1]);
+            tcb_w1_split_kernel<<<d->sms, 256, 0, d->stream>>>(d->target + d->woff[1], d->w1img + 3 * d->tcb_w1pl,
+                                                               d->tcb_w1pl, d->N[1]);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) {
+                if (prev >= 0) cudaSetDevice(prev);
+                return cuda_fail(e, "tcb_w1_split_kernel");
+            }
+            g_launches.fetch_add(2);
+            d->w1img_stale = false;
+        }
+        if (!fp.tcb && !dp) d->w1img_stale = true;   // the mma.sync step's K4 updates W1 without its image
         const int zslot = rp->pend.slot;   // zero-copy staging slot the insert reads (or -1)
         rp->pend.k = 0;
         rp->pend.slot = -1;
@@ -1748,6 +1882,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                             if (kp.func == (void *)distinct_fast_kernel) ds = nodes[i];
                             if (kp.func == (void *)fast_bwd1_kernel || kp.func == (void *)tc_bwd_kernel) k3 = nodes[i];
                             if (kp.func == (void *)fast_bwd0_sgd_kernel) k4 = nodes[i];
+                            if (kp.func == (void *)tcb_l0_kernel) k1 = k3 = nodes[i];   // T0 also writes the insert
                         }
                     }
                     if (e == cudaSuccess && (!k1 || !k3 || !k4)) e = cudaErrorInvalidValue;
@@ -1816,8 +1951,9 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             if (prev >= 0) cudaSetDevice(prev);
             return cuda_fail(e, "fast train step");
         }
-        g_launches.fetch_add(fp.distinct ? 5 : 4);
+        g_launches.fetch_add((fp.distinct ? 1 : 0) + (fp.tcb ? 6 : 4));
     } else {
+        d->w1img_stale = true;   // the generic kernels update W1 without the tcb image
         TrainArgs p;
         fill_args(d, rp, batch, loss_dev, dp ? 0 : 1, do_sync, p);
         // byte states with a wide input: layer 0 on the tensor cores (wide.cuh) around the
@@ -1977,6 +2113,7 @@ after_step:
         }
         g_launches.fetch_add(1);
         d->w0bf_stale = true;   // the update rewrote W0 without its planes
+        d->w1img_stale = true;
         if (loss_dev) cudaMemcpyAsync(loss_dev, d->grad + d->P, sizeof(float), cudaMemcpyDefault, d->stream);
     } else if (dp) {
         int nr = g_nccl.allreduce(d->grad, d->grad, (size_t)d->P + 1, kNcclFloat, kNcclAvg,
@@ -1987,6 +2124,7 @@ after_step:
             return RPL_ENCCL;
         }
         d->w0bf_stale = true;   // the all-reduced update rewrote W0 without its planes
+        d->w1img_stale = true;
         sgd_kernel<<<(unsigned)d->sms, 256, 0, d->stream>>>(d->online, d->target, d->grad, d->P,
                                                              d->cfg.lr, d->sync_flag, d->err);
         e = cudaGetLastError();
@@ -2008,6 +2146,7 @@ after_step:
             }
         }
         d->w0bf_stale = true;
+        d->w1img_stale = true;
     }
     (void)do_sync;
     if (prev >= 0) cudaSetDevice(prev);
@@ -2024,6 +2163,7 @@ extern "C" int sync_target(rpl_dqn *d)
     RPL_CUDA(cudaMemcpyAsync(d->target, d->online, (size_t)d->P * sizeof(float),
                              cudaMemcpyDeviceToDevice, d->stream));
     d->w0bf_stale = true;
+    d->w1img_stale = true;
     return RPL_OK;
 }
 
@@ -2055,6 +2195,7 @@ extern "C" int dqn_set_params(rpl_dqn *d, int which, const float *host_in, int64
                              cudaMemcpyHostToDevice, d->stream));
     RPL_CUDA(cudaStreamSynchronize(d->stream));
     d->w0bf_stale = true;
+    d->w1img_stale = true;
     return RPL_OK;
 }
 

@@ -99,7 +99,17 @@ struct FastArgs {
     int prec;            // rpl_dqn_config.precision (split_p / mma_3xtf32, mma_tf32.cuh)
     int tc;              // 1: K1 / K3 are the tensor-core kernels of tc_fast.cuh (K2 skips dZ1,
                          //    which K3 forms on the fly; K4 sums nw0 dW0 / db0 partials)
-    int nw0;             // tc: dW0 / db0 partials in w0part (NS x 128-row batch tiles)
+    int nw0;             // tc / tcb: dW0 / db0 partials in w0part
+    // large-batch tensor-core path (tc_big.cuh): bf16 hi / mid / lo images of the operands
+    int tcb;             // 1: the step runs tc_big.cuh's kernels (K4 writes the W1 image)
+    int Bp;              // B rounded up to 128 (rows past B are zero in every image)
+    int jp;              // dheadp row pitch (J rounded up to 4)
+    uint16_t *h0img;     // [nets][3][Bp * 128] H0 of every net
+    uint16_t *ximg;      // [3][Bp * 32] [x | 1] of s
+    uint16_t *dz1img;    // [3][Bp * N1] dZ1
+    uint16_t *w1img;     // [online, target][3][N1 * 128] W1
+    int64_t h0pl, xpl, dzpl, w1pl;   // plane strides (elements)
+    float *dheadp;       // [B][jp] dHead
 };
 
 __device__ __forceinline__ unsigned long long gtimer()
@@ -1108,7 +1118,7 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
     // in order; coalesced 128-B loads), then the 8 warp sums are added in warp order.
     // (wide inputs: W0 / b0 are wide_dw0_kernel's, which also gets dZ0 from here)
     const int64_t n0el = p.PdH0 ? 0 : p.w1;     // W0 and b0 lead the blob
-    const int nparts = p.tc ? p.nw0 : p.NS * ((B + BM - 1) / BM);
+    const int nparts = (p.tc || p.tcb) ? p.nw0 : p.NS * ((B + BM - 1) / BM);
     auto w0_partial = [&](int64_t i) {
         float g = 0.0f, comp = 0.0f;
         if (i >= n0el) return g;
@@ -1131,7 +1141,7 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
     };
     // (3) first float4 of the elementwise SGD over [w1, P)
     const int64_t lo = p.w1, n_el = p.P - p.w1;
-    const int64_t n4 = (p.nsb == 1) ? n_el / 4 : 0;
+    const int64_t n4 = (p.nsb == 1 && !p.w1img) ? n_el / 4 : 0;
     int64_t e4 = (int64_t)blockIdx.x * NT + tid;
     float4 g4 = make_float4(0.f, 0.f, 0.f, 0.f), w4 = g4;
     if (e4 < n4) {
@@ -1229,6 +1239,20 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
             const float w = p.online[i] - lr * gs;
             p.online[i] = w;
             if (do_sync) p.target[i] = w;
+            if (p.w1img && i < p.w1 + (int64_t)p.N1 * p.N0) {
+                // the large-batch path's bf16 image of W1 (tc_big.cuh) for the next step
+                const int64_t e = i - p.w1, u = e / p.N0;
+                const int k = (int)(e - u * p.N0);
+                const int64_t o = ((u >> 3) * (p.N0 >> 3) + (k >> 3)) * 64 + (u & 7) * 8 + (k & 7);
+                uint16_t h, m, l;
+                umma::split3_bf16(w, h, m, l);
+                for (int net = 0; net < (do_sync ? 2 : 1); ++net) {
+                    uint16_t *im = p.w1img + net * 3 * p.w1pl;
+                    im[o] = h;
+                    im[p.w1pl + o] = m;
+                    im[2 * p.w1pl + o] = l;
+                }
+            }
         }
     }
     if (blockIdx.x == 0 && tid == 0) {
