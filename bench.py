@@ -90,8 +90,25 @@ def workload_name(a, batch):
     where = {"host": ", ring rows in pinned host memory read across PCIe (zero-copy in-RAM variant)",
              "host_batch": ", the paper's in-RAM replay: CPU ring + CPU sampler/gather, one H2D batch "
                            "copy per step (P:15, P:50)"}.get(a.ring, "")
-    return (f"BASELINE configs[1]: {a.capacity:,}-slot replay of 27-float states, batch {batch}, "
+    cfgi = config_index(a, batch)
+    return (f"BASELINE configs[{cfgi}]: {a.capacity:,}-slot replay of 27-float states, batch {batch}, "
             f"{net}, {tgt} target, Huber, SGD, {a.adds_per_step} inserts/step{where}")
+
+
+def config_index(a, batch):
+    """Which BASELINE.json config a line measures: configs[1] is the paper setting (batch 128,
+    DQN); a Double-DQN or other-batch line belongs to the configs[2] sweep; N > 1 is configs[3]."""
+    if dist_env()[1] > 1:
+        return 3
+    return 1 if (batch == 128 and not a.ddqn) else 2
+
+
+def metric_name(a, batch):
+    """The headline metric string for the paper setting; sweep lines name their own batch."""
+    if config_index(a, batch) == 2:
+        tgt = "Double-DQN" if a.ddqn else "DQN"
+        return f"{tgt} train steps/s at batch {batch}, 1M replay (BASELINE configs[2] batch sweep)"
+    return METRIC
 
 
 def cfg_fields(a, batch):
@@ -365,7 +382,7 @@ def run_reference(a):
               f"B={batch} train step from a {a.capacity:,}-row host ring), time-capped at "
               f"{budget:.0f} s; single thread, fp64 arithmetic")
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "train_steps/s",
+        "impl": "reference", "metric": metric_name(a, batch), "value": v, "unit": "train_steps/s",
         "n_gpus": a.gpus, "steps": n, "warmup": min(a.warmup, 2), "ms_per_step": 1000 * el / n,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": workload_name(a, batch), "batch": batch,
@@ -628,7 +645,7 @@ def run_ours(a, batch, first_line=True):
         p2p_arm = time_p2p_arm(a, binding, cfg, rp, batch, add_dev, W + 2 * K + 400, stream, dev)
 
     line = {
-        "metric": METRIC, "value": value, "unit": "train_steps/s", "n_gpus": world, "steps": K,
+        "metric": metric_name(a, batch), "value": value, "unit": "train_steps/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": DTYPE[a.precision], "data": "synthetic",
         "config": {"workload": workload_name(a, batch), "batch": batch, "capacity": a.capacity,
@@ -723,10 +740,11 @@ def time_oracle_c5(batch, ddqn, seconds, pool):
     """The oracle on a bounded sample of config 5: a 1,024-row byte ring (the 56 GB ring does
     not fit in host RAM), its sampler + gather, u8 -> x, loss / gradient and SGD, composed
     as they stand (never tuned), single thread, fp64."""
+    import types
     import oracle
     from inputs import init_params
-    import paper_1801_03138_b200.binding as binding
-    cfg = c5_cfg(binding, batch, ddqn)
+    # plain fields (no product import on the oracle arm)
+    cfg = types.SimpleNamespace(state_dim=C5_D, n_actions=8, dueling=True, hidden=(128,), stream=512)
     net = oracle_net_of(cfg)
     ring = oracle.RingU8(1024, C5_D)
     ring.add(**pool)

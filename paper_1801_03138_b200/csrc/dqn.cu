@@ -809,8 +809,11 @@ struct rpl_dqn {
     float *PdH0 = nullptr;                 // wide_fast: K3's dH0 partials [32][max_batch][N0]
     uint16_t *w0bf = nullptr;              // bf16 planes of W0 [online, target][3][N0 * D]
     uint16_t *dz0bf = nullptr;             // bf16 planes of dZ0 [3][max_batch][N0]
-    bool w0bf_stale = true;                // wide W0 bf16 planes to be re-split from the fp32 weights
-    bool w1img_stale = true;               // tcb: W1 images to be re-split (any update not K4's)
+    // bf16 operand images to be re-split from the fp32 weights: bit 0 the online net's, bit 1
+    // the target net's (a data-parallel update rewrites the online weights, and the target
+    // only on a sync step)
+    int w0bf_stale = 3;                    // wide W0 planes
+    int w1img_stale = 3;                   // tcb: W1 images (any update not K4's)
     int wide_ks = 0, wide_cs = 1;          // wide_l0_kernel chunks and cluster size (wide_l0_plan)
     int k1_mc_clusters = 0;                // co-resident clusters of the multicast K1 (0: not used)
     unsigned long long *trace = nullptr;   // RPL_TRACE=1: per-CTA timestamps of the fast kernels
@@ -1019,7 +1022,7 @@ static bool tcb_shape_ok(const rpl_dqn *d)
 }
 // batches from here up take the tensor-core step (below it the mma.sync kernels: the step is
 // latency-bound there)
-static constexpr int kTcbMinBatch = 512;
+static constexpr int kTcbMinBatch = 640;
 static int tcb_min_batch()
 {
 #ifdef RPL_EXPERIMENTS
@@ -1251,7 +1254,7 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
         d->tcb_dzpl = Bpm * d->N[1];
         d->tcb_w1pl = (int64_t)d->N[1] * tcb::N0;
         const int jp = (d->J + 3) & ~3;
-        ok = dalloc(d, &d->h0img, (size_t)3 * nets * d->tcb_h0pl) && dalloc(d, &d->ximg, (size_t)3 * d->tcb_xpl) &&
+        ok = dalloc(d, &d->h0img, (size_t)3 * (nets + 1) * d->tcb_h0pl) && dalloc(d, &d->ximg, (size_t)3 * d->tcb_xpl) &&
              dalloc(d, &d->dz1img, (size_t)3 * d->tcb_dzpl) && dalloc(d, &d->w1img, (size_t)6 * d->tcb_w1pl) &&
              dalloc(d, &d->dheadp, (size_t)Bpm * jp);
         // T3a partial gradients [G][gps]; T3b dW0 | db0 partials [NQ * tiles][w1] with
@@ -1275,7 +1278,9 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
         ok = ok && cudaFuncSetAttribute(tcb_l0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tcb_t0_smem(d)) == cudaSuccess &&
              cudaFuncSetAttribute(tcb_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tcb::T1Smem(d->J).total) == cudaSuccess &&
              cudaFuncSetAttribute(tcb_dw1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tcb::T3aSmem(d->J).total) == cudaSuccess &&
-             cudaFuncSetAttribute(tcb_dh0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tcb::T3bSmem().total) == cudaSuccess;
+             cudaFuncSetAttribute(tcb_dh0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tcb::T3bSmem().total) == cudaSuccess &&
+             cudaFuncSetAttribute(tcb_td_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)tcb_td_smem(3, d->N[1], d->J)) == cudaSuccess;
     }
     if (!ok) {
         if (!coop) set_error("dqn_create: device %d lacks cooperative launch", d->device);
@@ -1627,7 +1632,7 @@ static cudaError_t tcb_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
     const int cpc = std::max(1, std::min(nbt, d->sms / ncombo));
     e = launch_pdl(tcb_fwd_kernel, ncombo * cpc, tcb::T1_T, tcb::T1Smem(p.J).total, st, false, p);
     if (e != cudaSuccess) return e;
-    e = launch_pdl(tcb_td_kernel, (p.B + 7) / 8, 256, 0, st, false, p);
+    e = launch_pdl(tcb_td_kernel, (p.B + 7) / 8, 256, tcb_td_smem(p.nets, p.N1, p.J), st, false, p);
     if (e != cudaSuccess) return e;
     e = launch_pdl(tcb_dw1_kernel, nut * p.nsb, tcb::T3A_T, tcb::T3aSmem(p.J).total, st, false, p);
     if (e != cudaSuccess) return e;
@@ -1835,18 +1840,23 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             fp.bidx = bidx;
         }
         if (fp.tcb && d->w1img_stale) {   // after create / set_params / sync_target / a DP or small-batch update
-            tcb_w1_split_kernel<<<d->sms, 256, 0, d->stream>>>(d->online + d->woff[1], d->w1img, d->tcb_w1pl, d->N[1]);
-            tcb_w1_split_kernel<<<d->sms, 256, 0, d->stream>>>(d->target + d->woff[1], d->w1img + 3 * d->tcb_w1pl,
-                                                               d->tcb_w1pl, d->N[1]);
+            if (d->w1img_stale & 1) {
+                tcb_w1_split_kernel<<<d->sms, 256, 0, d->stream>>>(d->online + d->woff[1], d->w1img, d->tcb_w1pl, d->N[1]);
+                g_launches.fetch_add(1);
+            }
+            if (d->w1img_stale & 2) {
+                tcb_w1_split_kernel<<<d->sms, 256, 0, d->stream>>>(d->target + d->woff[1], d->w1img + 3 * d->tcb_w1pl,
+                                                                   d->tcb_w1pl, d->N[1]);
+                g_launches.fetch_add(1);
+            }
             e = cudaGetLastError();
             if (e != cudaSuccess) {
                 if (prev >= 0) cudaSetDevice(prev);
                 return cuda_fail(e, "tcb_w1_split_kernel");
             }
-            g_launches.fetch_add(2);
-            d->w1img_stale = false;
+            d->w1img_stale = 0;
         }
-        if (!fp.tcb && !dp) d->w1img_stale = true;   // the mma.sync step's K4 updates W1 without its image
+        if (!fp.tcb && !dp) d->w1img_stale = 3;   // the mma.sync step's K4 updates W1 without its image
         const int zslot = rp->pend.slot;   // zero-copy staging slot the insert reads (or -1)
         rp->pend.k = 0;
         rp->pend.slot = -1;
@@ -1953,7 +1963,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
         }
         g_launches.fetch_add((fp.distinct ? 1 : 0) + (fp.tcb ? 6 : 4));
     } else {
-        d->w1img_stale = true;   // the generic kernels update W1 without the tcb image
+        d->w1img_stale = 3;   // the generic kernels update W1 without the tcb image
         TrainArgs p;
         fill_args(d, rp, batch, loss_dev, dp ? 0 : 1, do_sync, p);
         // byte states with a wide input: layer 0 on the tensor cores (wide.cuh) around the
@@ -1988,15 +1998,16 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             p.ks0 = wd_l0_partials(w.ks, w.cs, batch);   // partials left in PF0
             if (d->w0bf_stale) {   // after create / set_params / sync_target / a DP step
                 const int64_t pe = wd_plane_elems(p.D);
-                wide_split_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->online + d->woff[0], d->w0bf, d->N[0], p.D);
-                wide_split_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->target + d->woff[0], d->w0bf + 3 * pe, d->N[0], p.D);
+                if (d->w0bf_stale & 1) launch_wide_split(d->online + d->woff[0], d->w0bf, d->N[0], p.D, d->sms, d->stream);
+                if (d->w0bf_stale & 2)
+                    launch_wide_split(d->target + d->woff[0], d->w0bf + 3 * pe, d->N[0], p.D, d->sms, d->stream);
                 e = cudaGetLastError();
                 if (e != cudaSuccess) {
                     if (prev >= 0) cudaSetDevice(prev);
                     return cuda_fail(e, "wide_split_kernel");
                 }
-                g_launches.fetch_add(2);
-                d->w0bf_stale = false;
+                g_launches.fetch_add(d->w0bf_stale == 3 ? 2 : 1);
+                d->w0bf_stale = 0;
             }
             w.ntile = (int)std::min<int64_t>(WD_MAXN, ((p.D + d->sms - 1) / d->sms + 15) / 16 * 16);
             w.wpre = wd_dw0_wpre(w.ntile) ? 1 : 0;
@@ -2098,7 +2109,7 @@ after_step:
         a.sync_flag[0] = d->sync_flag;
         a.err[0] = d->err;
         if (e == cudaSuccess) {
-            if (d->P + 1 > kDpRsMin) {   // large gradients: the reduce-scatter variant
+            if (dp_use_rs(d->P, d->world)) {   // large gradients or >= 4 ranks: the reduce-scatter variant
                 void *args[] = {&a};
                 e = cudaLaunchCooperativeKernel((const void *)dp_peer_rs_sgd_kernel, dim3(d->sms), dim3(256),
                                                 args, 0, d->stream);
@@ -2112,8 +2123,9 @@ after_step:
             return cuda_fail(e, "dp_peer_sgd_kernel");
         }
         g_launches.fetch_add(1);
-        d->w0bf_stale = true;   // the update rewrote W0 without its planes
-        d->w1img_stale = true;
+        // the update rewrote the online W0 / W1 without their images (the target too on a sync step)
+        d->w0bf_stale |= do_sync ? 3 : 1;
+        d->w1img_stale |= do_sync ? 3 : 1;
         if (loss_dev) cudaMemcpyAsync(loss_dev, d->grad + d->P, sizeof(float), cudaMemcpyDefault, d->stream);
     } else if (dp) {
         int nr = g_nccl.allreduce(d->grad, d->grad, (size_t)d->P + 1, kNcclFloat, kNcclAvg,
@@ -2123,8 +2135,10 @@ after_step:
             if (prev >= 0) cudaSetDevice(prev);
             return RPL_ENCCL;
         }
-        d->w0bf_stale = true;   // the all-reduced update rewrote W0 without its planes
-        d->w1img_stale = true;
+        // the all-reduced update rewrote the online W0 / W1 without their images (the target
+        // too on a sync step)
+        d->w0bf_stale |= do_sync ? 3 : 1;
+        d->w1img_stale |= do_sync ? 3 : 1;
         sgd_kernel<<<(unsigned)d->sms, 256, 0, d->stream>>>(d->online, d->target, d->grad, d->P,
                                                              d->cfg.lr, d->sync_flag, d->err);
         e = cudaGetLastError();
@@ -2145,10 +2159,9 @@ after_step:
                 return RPL_ENCCL;
             }
         }
-        d->w0bf_stale = true;
-        d->w1img_stale = true;
+        d->w0bf_stale = 3;
+        d->w1img_stale = 3;
     }
-    (void)do_sync;
     if (prev >= 0) cudaSetDevice(prev);
     rp->events += 1;
     d->steps = t;
@@ -2162,8 +2175,8 @@ extern "C" int sync_target(rpl_dqn *d)
     if (!d) return RPL_EINVAL;
     RPL_CUDA(cudaMemcpyAsync(d->target, d->online, (size_t)d->P * sizeof(float),
                              cudaMemcpyDeviceToDevice, d->stream));
-    d->w0bf_stale = true;
-    d->w1img_stale = true;
+    d->w0bf_stale = 3;
+    d->w1img_stale = 3;
     return RPL_OK;
 }
 
@@ -2194,8 +2207,8 @@ extern "C" int dqn_set_params(rpl_dqn *d, int which, const float *host_in, int64
     RPL_CUDA(cudaMemcpyAsync(which_ptr(d, which), host_in, (size_t)n * sizeof(float),
                              cudaMemcpyHostToDevice, d->stream));
     RPL_CUDA(cudaStreamSynchronize(d->stream));
-    d->w0bf_stale = true;
-    d->w1img_stale = true;
+    d->w0bf_stale = 3;
+    d->w1img_stale = 3;
     return RPL_OK;
 }
 

@@ -54,7 +54,7 @@ namespace tcb {
 constexpr int N0 = 128;       // layer-0 units (the M of the dW0 MMA, the K of layer 1)
 constexpr int JW = 8;         // head outputs one unit tile contributes to (dueling A stream: |A|)
 constexpr int JPMAX = 16;     // padded head width of dHead rows (J <= 16)
-constexpr int T0_ROWS = 32, T0_T = 256;
+constexpr int T0_ROWS = 16, T0_T = 256;   // T0: 16 half-warps, one sampled row each
 constexpr int T1_T = 320;     // warps 0-7 epilogue, 8 producer, 9 MMA
 constexpr int T1_SLOTS = 4;   // H0 ring slots (one 32-deep K quarter of a 128-row tile each)
 constexpr int T1_SLOT = 3 * 128 * 32 * 2;   // bytes of one slot (three planes)
@@ -69,6 +69,20 @@ constexpr int XW = 32;                          // [x | 1] image width (state_di
 __host__ __device__ __forceinline__ int64_t img(int64_t r, int c, int C)
 {
     return ((r >> 3) * (C >> 3) + (c >> 3)) * 64 + (r & 7) * 8 + (c & 7);
+}
+
+// H0 image as T1 reads it: 128-row x 32-column (tile, K quarter) blocks of 8 KB, each block
+// row-group major with C = 32 (so one bulk copy per plane fills a T1 ring slot)
+__host__ __device__ __forceinline__ int64_t qimg(int64_t r, int c)
+{
+    return ((r >> 7) * (N0 / 32) + (c >> 5)) * (128 * 32) + (((r & 127) >> 3) * 4 + ((c & 31) >> 3)) * 64 + (r & 7) * 8 + (c & 7);
+}
+
+// dZ1 image as T3b reads it: 128-row x 64-unit (tile, unit chunk) blocks of 16 KB, each block
+// row-group major with C = 64 (one bulk copy per plane fills a T3b stage)
+__host__ __device__ __forceinline__ int64_t dzimg(int64_t r, int u, int N1)
+{
+    return ((r >> 7) * (N1 >> 6) + (u >> 6)) * (128 * 64) + (((r & 127) >> 3) * 8 + ((u & 63) >> 3)) * 64 + (r & 7) * 8 + (u & 7);
 }
 
 // eight consecutive fp32 values -> their hi / mid / lo bf16 terms, 16 bytes per plane
@@ -217,25 +231,42 @@ struct T3bSmem {
 }  // namespace tcb
 
 // ------------------------------------------------------------------------------------------
-// T0: sample, gather, deferred insert, layer 0 (FP32 FMA) -- 32 batch rows per CTA
+// T0: sample, gather, deferred insert, layer 0 (FP32 FMA) -- 16 batch rows per CTA.  Every
+// global load a phase needs is in flight at once: W0 / b0 by 16-byte cp.async (waited for only
+// before layer 0), a sampled row by one half-warp with 16-byte loads (the whole row, scalars
+// included, in one or two loads per lane)
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(tcb::T0_T) tcb_l0_kernel(const __grid_constant__ FastArgs p)
 {
     using namespace tcb;
-    extern __shared__ float sm0[];
-    const int D = p.D, B = p.B, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    extern __shared__ __align__(16) float sm0[];
+    const int D = p.D, B = p.B, tid = threadIdx.x, lane = tid & 31;
     constexpr int XS = 33;   // staged state pitch (>= D + 1, odd: conflict-free)
     float *W0s = sm0;                      // [online | target] [N0][D]
     float *b0s = W0s + 2 * N0 * D;         // [online | target] [N0]
-    float *xs = b0s + 2 * N0;              // [32 rows][s, s'][XS]
+    float *xs = b0s + 2 * N0;              // [T0_ROWS rows][s, s'][XS]
     __shared__ int32_t idxs[T0_ROWS], pjs[T0_ROWS], pjs2[T0_ROWS];
-    for (int e = tid; e < N0 * D; e += T0_T) {
-        W0s[e] = __ldg(p.online + p.w0 + e);
-        W0s[N0 * D + e] = __ldg(p.target + p.w0 + e);
-    }
-    for (int e = tid; e < N0; e += T0_T) {
-        b0s[e] = __ldg(p.online + p.b0 + e);
-        b0s[N0 + e] = __ldg(p.target + p.b0 + e);
+    // (0) W0 / b0 of both nets into shared memory, asynchronously (N0 * D and N0 are multiples
+    // of 4 floats; the blob offsets of W0 and b0 are 16-byte aligned when w0 % 4 == 0)
+    const bool wvec = (p.w0 & 3) == 0 && (p.b0 & 3) == 0;
+    if (wvec) {
+        for (int c = tid; c < N0 * D / 4; c += T0_T) {
+            cp_async16(W0s + 4 * c, p.online + p.w0 + 4 * c);
+            cp_async16(W0s + N0 * D + 4 * c, p.target + p.w0 + 4 * c);
+        }
+        for (int c = tid; c < N0 / 4; c += T0_T) {
+            cp_async16(b0s + 4 * c, p.online + p.b0 + 4 * c);
+            cp_async16(b0s + N0 + 4 * c, p.target + p.b0 + 4 * c);
+        }
+    } else {
+        for (int e = tid; e < N0 * D; e += T0_T) {
+            W0s[e] = __ldg(p.online + p.w0 + e);
+            W0s[N0 * D + e] = __ldg(p.target + p.w0 + e);
+        }
+        for (int e = tid; e < N0; e += T0_T) {
+            b0s[e] = __ldg(p.online + p.b0 + e);
+            b0s[N0 + e] = __ldg(p.target + p.b0 + e);
+        }
     }
     const uint64_t event = p.rctrl[0];
     const uint64_t size = p.pend_k ? p.pend_size : p.rctrl[1];
@@ -275,11 +306,47 @@ __global__ void __launch_bounds__(tcb::T0_T) tcb_l0_kernel(const __grid_constant
         pjs2[2 * tid + 1] = p.shared ? pend_j((i1 + 1) % p.capacity) : -1;
     }
     __syncthreads();
-    // (2) s and s' of the 32 rows (shared states: s' is the next slot's s); a sampled
-    // slot of the pending insert is read from the insert's sources
+    // (2) s and s' of the rows (shared states: s' is the next slot's s); a sampled slot
+    // of the pending insert is read from the insert's sources
+    const bool rvec = !p.shared && (p.rs & 3) == 0 && (reinterpret_cast<uintptr_t>(p.ring) & 15) == 0;
+    {
+        // half-warp h owns row h: lane l16 loads floats 4 (l16 + 16 i) .. + 3 of the row
+        const int r = tid >> 4, l16 = tid & 15, b = rb + r;
+        const bool mine = rvec && b < B && pjs[r] < 0;
+        const int nv = (p.sw + 3 + 3) >> 2;   // float4s up to the terminal flag
+        float4 v[2];
+        if (mine) {
+            const float4 *row = reinterpret_cast<const float4 *>(p.ring + (int64_t)(p.bidx ? b : idxs[r]) * p.rs);
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+                if (l16 + 16 * i < nv) v[i] = __ldg(row + l16 + 16 * i);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                if (l16 + 16 * i >= nv) continue;
+                const float f[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int c = 4 * (l16 + 16 * i) + q;
+                    if (c < D) {
+                        xs[(r * 2) * XS + c] = f[q];
+                    } else if (c < 2 * D) {
+                        xs[(r * 2 + 1) * XS + c - D] = f[q];
+                    } else if (c == p.sw) {
+                        p.a[b] = __float_as_int(f[q]);
+                    } else if (c == p.sw + 1) {
+                        p.r[b] = f[q];
+                    } else if (c == p.sw + 2) {
+                        p.done[b] = (uint8_t)(__float_as_uint(f[q]) != 0u);
+                    }
+                }
+            }
+        }
+    }
+    // rows the vector path does not take: shared-state rings, pending slots, rows past B
     for (int e = tid; e < T0_ROWS * 2 * D; e += T0_T) {
         const int r = e / (2 * D), rem = e - r * 2 * D, which = rem / D, dd = rem - which * D;
         const int b = rb + r;
+        if (rvec && b < B && pjs[r] < 0) continue;
         float v = 0.0f;
         if (b < B) {
             const bool nxt = which == 1 && p.shared;
@@ -288,31 +355,38 @@ __global__ void __launch_bounds__(tcb::T0_T) tcb_l0_kernel(const __grid_constant
             const int col0 = which == 0 || p.shared ? 0 : D;
             v = j < 0 ? __ldg(p.ring + slot * p.rs + col0 + dd)
                       : (which == 0 || p.shared ? p.pend_s : p.pend_s2)[(int64_t)j * D + dd];
-            (which == 0 ? p.Xs : p.Xs2)[(int64_t)b * D + dd] = v;
         }
         xs[(r * 2 + which) * XS + dd] = v;
     }
     if (tid < T0_ROWS && rb + tid < B) {
         const int b = rb + tid, j = pjs[tid];
-        int32_t ra;
-        float rr;
-        uint32_t rd;
-        if (j < 0) {
-            const float *row = p.ring + (int64_t)(p.bidx ? b : idxs[tid]) * p.rs + p.sw;
-            ra = __float_as_int(__ldg(row));
-            rr = __ldg(row + 1);
-            rd = __float_as_uint(__ldg(row + 2));
-        } else {
-            ra = p.pend_a[j];
-            rr = p.pend_r[j];
-            rd = p.pend_done[j];
+        if (!(rvec && j < 0)) {
+            int32_t ra;
+            float rr;
+            uint32_t rd;
+            if (j < 0) {
+                const float *row = p.ring + (int64_t)(p.bidx ? b : idxs[tid]) * p.rs + p.sw;
+                ra = __float_as_int(__ldg(row));
+                rr = __ldg(row + 1);
+                rd = __float_as_uint(__ldg(row + 2));
+            } else {
+                ra = p.pend_a[j];
+                rr = p.pend_r[j];
+                rd = p.pend_done[j];
+            }
+            p.a[b] = ra;
+            p.r[b] = rr;
+            p.done[b] = (uint8_t)(rd != 0u);
         }
         p.idx[b] = idxs[tid];
-        p.a[b] = ra;
-        p.r[b] = rr;
-        p.done[b] = (uint8_t)(rd != 0u);
     }
+    cp_async_wait_all();
     __syncthreads();
+    // the gathered states of the batch (the learner's batch tensors)
+    for (int e = tid; e < T0_ROWS * 2 * D; e += T0_T) {
+        const int which = e / (T0_ROWS * D), rem = e - which * T0_ROWS * D, r = rem / D, dd = rem - r * D;
+        if (rb + r < B) (which == 0 ? p.Xs : p.Xs2)[(int64_t)(rb + r) * D + dd] = xs[(r * 2 + which) * XS + dd];
+    }
     // (3) the [x | 1] image of s (the B operand of T3b's dW0 | db0 MMA), zero past D + 1 and
     // for rows past B
     if (tid < T0_ROWS * (XW / 8)) {
@@ -325,43 +399,38 @@ __global__ void __launch_bounds__(tcb::T0_T) tcb_l0_kernel(const __grid_constant
         }
         store8(p.ximg, p.xpl, img(b, 8 * cg, XW), x);
     }
-    // (4) layer 0 of every net: H0 = ReLU(x W0^T + b0); thread = (row, 16 units)
+    // (4) layer 0 of every net: H0 = ReLU(x W0^T + b0); thread = (row, 8 units)
     {
-        const int r = tid & 31, g = warp, b = rb + r, k0 = 16 * g;
+        const int r = tid % T0_ROWS, g = tid / T0_ROWS, b = rb + r, k0 = 8 * g;
         const bool ok = b < B;
         for (int net = 0; net < p.nets; ++net) {
             const float *x = xs + (r * 2 + (net == 0 ? 0 : 1)) * XS;
             const float *W = W0s + (net == 1 ? N0 * D : 0);
             const float *bb = b0s + (net == 1 ? N0 : 0);
-            float h[16];
+            float h[8];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) h[i] = bb[k0 + i];
+            for (int i = 0; i < 8; ++i) h[i] = bb[k0 + i];
             for (int dd = 0; dd < D; ++dd) {
                 const float xv = x[dd];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) h[i] = fmaf(W[(k0 + i) * D + dd], xv, h[i]);
+                for (int i = 0; i < 8; ++i) h[i] = fmaf(W[(k0 + i) * D + dd], xv, h[i]);
             }
 #pragma unroll
-            for (int i = 0; i < 16; ++i) h[i] = ok ? fmaxf(h[i], 0.0f) : 0.0f;
-            uint16_t *im = p.h0img + (int64_t)net * 3 * p.h0pl;
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                float v[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) v[i] = h[8 * hf + i];
-                store8(im, p.h0pl, img(b, k0 + 8 * hf, N0), v);
-            }
+            for (int i = 0; i < 8; ++i) h[i] = ok ? fmaxf(h[i], 0.0f) : 0.0f;
+            // T1's A operand (tile-quarter blocks), and T3a's B operand for the online net on s
+            store8(p.h0img + (int64_t)net * 3 * p.h0pl, p.h0pl, qimg(b, k0), h);
+            if (net == 0) store8(p.h0img + (int64_t)p.nets * 3 * p.h0pl, p.h0pl, img(b, k0, N0), h);
             if (net == 0 && ok) {
                 float *ho = p.H0 + (int64_t)b * N0 + k0;
-#pragma unroll
-                for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4 *>(ho + i) = make_float4(h[i], h[i + 1], h[i + 2], h[i + 3]);
+                *reinterpret_cast<float4 *>(ho) = make_float4(h[0], h[1], h[2], h[3]);
+                *reinterpret_cast<float4 *>(ho + 4) = make_float4(h[4], h[5], h[6], h[7]);
             }
         }
     }
     // (5) the deferred insert's rows into the ring: no sampled read of this step goes
     // to a pending slot's ring row (those read the insert's sources), so the order is free
     if (p.pend_k)
-        for (int64_t j = (int64_t)blockIdx.x * (T0_T / 32) + warp; j < p.pend_k; j += (int64_t)gridDim.x * (T0_T / 32))
+        for (int64_t j = (int64_t)blockIdx.x * (T0_T / 32) + (tid >> 5); j < p.pend_k; j += (int64_t)gridDim.x * (T0_T / 32))
             ring_write_row(p.ring + ((p.pend_cur + j) % p.capacity) * p.rs, p.rs, D, p.sw, lane, j, p.pend_s,
                            p.pend_a, p.pend_r, p.pend_s2, p.pend_done, p.pend_err);
 }
@@ -423,13 +492,10 @@ __global__ void __launch_bounds__(tcb::T1_T, 1) tcb_fwd_kernel(const __grid_cons
             if (lane == 0) umma::mbar_expect_tx(&full[slot], T1_SLOT);
             __syncwarp();
             char *dst = As + slot * T1_SLOT;
-            // 16 row groups x 3 planes: the 4 core matrices of a row group's K quarter are
-            // one 512-byte piece of the image
-            for (int c = lane; c < 48; c += 32) {
-                const int pl = c >> 4, rg = c & 15;
-                umma::bulk_g2s(dst + pl * (128 * 32 * 2) + rg * 512,
-                               h0 + pl * p.h0pl + img((int64_t)bt * 128 + 8 * rg, 32 * q, N0), 512, &full[slot]);
-            }
+            // a (tile, K quarter) block of the H0 image is one contiguous 8 KB piece per plane
+            if (lane < 3)
+                umma::bulk_g2s(dst + lane * (128 * 32 * 2), h0 + lane * p.h0pl + qimg((int64_t)bt * 128, 32 * q),
+                               128 * 32 * 2, &full[slot]);
         }
     } else if (warp == 9) {
         // ---- MMA issue ------------------------------------------------------------------------
@@ -527,6 +593,10 @@ __global__ void __launch_bounds__(tcb::T1_T, 1) tcb_fwd_kernel(const __grid_cons
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) tcb_td_kernel(const __grid_constant__ FastArgs p)
 {
+    // the partials of the CTA's 8 consecutive samples: for each (net, unit half-tile q) the
+    // 8 x J words are contiguous in p.part (T1 writes [net][q][b][j]), so the CTA loads them
+    // with coalesced loads, 8 in flight per thread, into raw[net][q][8][J]
+    extern __shared__ float raw[];
     __shared__ float hs[8][3 * (F_MAXJ + 1)];
     __shared__ float dhs[8][F_MAXJ + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -534,18 +604,26 @@ __global__ void __launch_bounds__(256) tcb_td_kernel(const __grid_constant__ Fas
         const int64_t t = *p.step_dev + 1;
         *p.sync_flag = (p.sync_period > 0 && t % p.sync_period == 0) ? 1 : 0;
     }
-    const int b = blockIdx.x * 8 + warp;
-    if (b >= p.B) return;
-    const int J = p.J, B = p.B, nut2 = p.N1 / 64;
+    const int J = p.J, B = p.B, nut2 = p.N1 / 64, b0 = blockIdx.x * 8;
+    const int nb = min(8, B - b0), span = nb * J, nseg = p.nets * nut2, n = nseg * span;
+#pragma unroll 8
+    for (int e = threadIdx.x; e < n; e += 256) {
+        const int seg = e / span, w = e - seg * span;
+        raw[seg * 8 * J + w] = __ldcg(p.part + ((int64_t)seg * B + b0) * J + w);
+    }
+    __syncthreads();
+    const int b = b0 + warp;
+    if (b >= B) return;
     const int ab = p.a[b];
     const float rb = p.r[b];
     const uint8_t db = p.done[b];
     for (int net = 0; net < p.nets; ++net) {
         const float *theta = net == 1 ? p.target : p.online;
         if (lane < J) {
-            const float *src = p.part + ((int64_t)net * nut2 * B + b) * J + lane;
+            // bias, then the partials in unit-tile order
+            const float *src = raw + (int64_t)net * nut2 * 8 * J + warp * J + lane;
             float v = __ldg(theta + p.bh + lane);
-            for (int q = 0; q < nut2; ++q) v += __ldcg(src + (int64_t)q * B * J);
+            for (int q = 0; q < nut2; ++q) v += src[q * 8 * J];
             hs[warp][net * (F_MAXJ + 1) + lane] = v;
         }
     }
@@ -554,11 +632,12 @@ __global__ void __launch_bounds__(256) tcb_td_kernel(const __grid_constant__ Fas
     __syncwarp();
     if (lane < p.jp) p.dheadp[(int64_t)b * p.jp + lane] = lane < J ? dhs[warp][lane] : 0.0f;
 }
+inline size_t tcb_td_smem(int nets, int N1, int J) { return (size_t)nets * (N1 / 64) * 8 * J * sizeof(float); }
 
 // ------------------------------------------------------------------------------------------
 // T3a: per (128-unit tile ut, chunk group g): 64-row chunks c = g, g + G, ... of the batch.
 // Per chunk: all threads form dZ1[b][u] (thread = 8 rows of one 8-unit column group per
-// pass) into the stage's A image; its 24 row-group pieces go to the global dZ1 image (T3b);
+// pass) into the stage's A image and straight into the global dZ1 image (T3b, dzimg blocks);
 // thread 0 issues dW1 += dZ1^T H0 (M = units, N = 128, K = 64 samples; both MN-major).
 // Partials -> gpart[g] (dW1, db1, dW_head of the tile; db_head from ut == 0).
 // ------------------------------------------------------------------------------------------
@@ -603,43 +682,54 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
     }
 #pragma unroll
     for (int j = 0; j < JPMAX; ++j) bha[j] = 0.0f;
-    const bool storer = warp == 7 && lane < 24;
+    // the H1 / dHead rows of pass (chunk c, pass ps) -- loaded one pass ahead, so the next
+    // pass's (and across chunks, the next chunk's first pass's) L2 loads are in flight while
+    // this pass computes
+    auto load_pass = [&](int c, int ps, float (&h1)[8], float (&dh)[JPMAX]) {
+        const int b = 64 * c + 16 * ps + 8 * rh + r8;
+        if (c < nch && b < B) {
+            const float4 *hp = reinterpret_cast<const float4 *>(p.H1 + (int64_t)b * N1 + u0 + 8 * cg);
+            const float4 x0 = __ldcg(hp), x1 = __ldcg(hp + 1);
+            h1[0] = x0.x; h1[1] = x0.y; h1[2] = x0.z; h1[3] = x0.w;
+            h1[4] = x1.x; h1[5] = x1.y; h1[6] = x1.z; h1[7] = x1.w;
+#pragma unroll
+            for (int q = 0; q < JPMAX / 4; ++q) {
+                float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (4 * q < jp) t = __ldcg(reinterpret_cast<const float4 *>(p.dheadp + (int64_t)b * jp) + q);
+                dh[4 * q] = t.x; dh[4 * q + 1] = t.y; dh[4 * q + 2] = t.z; dh[4 * q + 3] = t.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) h1[k] = 0.0f;
+#pragma unroll
+            for (int j = 0; j < JPMAX; ++j) dh[j] = 0.0f;
+        }
+    };
+    float h1n[8], dhn[JPMAX];
+    load_pass(g, 0, h1n, dhn);
     int i = 0;
     for (int c = g; c < nch; c += G, ++i) {
         const int s = i & 1;
         char *Ast = smc + L.oA + s * T3A_STAGE_A, *Bst = smc + L.oB + s * T3A_STAGE_B;
-        if (storer) bulk_wait_read1();    // chunk i - 2's dZ1 pieces have left stage s
-        if (i >= 2) umma::mbar_wait(&mfree[s], (uint32_t)(((i >> 1) - 1) & 1));   // and its MMAs
+        if (i >= 2) umma::mbar_wait(&mfree[s], (uint32_t)(((i >> 1) - 1) & 1));   // chunk i - 2's MMAs
         __syncthreads();
         umma::fence_after_sync();
         if (tid == 0) {
             umma::mbar_expect_tx(&full[s], T3A_STAGE_B);
             for (int pl = 0; pl < 3; ++pl)
-                umma::bulk_g2s(Bst + pl * (64 * N0 * 2), p.h0img + pl * p.h0pl + (int64_t)c * 64 * N0, 64 * N0 * 2,
+                umma::bulk_g2s(Bst + pl * (64 * N0 * 2), p.h0img + ((int64_t)p.nets * 3 + pl) * p.h0pl + (int64_t)c * 64 * N0, 64 * N0 * 2,
                                &full[s]);
         }
 #pragma unroll 1
         for (int ps = 0; ps < 4; ++ps) {
-            const int rr = 16 * ps + 8 * rh + r8, b = 64 * c + rr;
-            const bool ok = b < B;
+            const int rr = 16 * ps + 8 * rh + r8;
             float h1[8], dh[JPMAX];
-            if (ok) {
-                const float4 *hp = reinterpret_cast<const float4 *>(p.H1 + (int64_t)b * N1 + u0 + 8 * cg);
-                const float4 x0 = __ldcg(hp), x1 = __ldcg(hp + 1);
-                h1[0] = x0.x; h1[1] = x0.y; h1[2] = x0.z; h1[3] = x0.w;
-                h1[4] = x1.x; h1[5] = x1.y; h1[6] = x1.z; h1[7] = x1.w;
 #pragma unroll
-                for (int q = 0; q < JPMAX / 4; ++q) {
-                    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (4 * q < jp) t = __ldcg(reinterpret_cast<const float4 *>(p.dheadp + (int64_t)b * jp) + q);
-                    dh[4 * q] = t.x; dh[4 * q + 1] = t.y; dh[4 * q + 2] = t.z; dh[4 * q + 3] = t.w;
-                }
-            } else {
+            for (int k = 0; k < 8; ++k) h1[k] = h1n[k];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) h1[k] = 0.0f;
-#pragma unroll
-                for (int j = 0; j < JPMAX; ++j) dh[j] = 0.0f;
-            }
+            for (int j = 0; j < JPMAX; ++j) dh[j] = dhn[j];
+            if (ps < 3) load_pass(c, ps + 1, h1n, dhn);
+            else load_pass(c + G, 0, h1n, dhn);
             // the tile's head outputs start at jlo (0 or 1, head_range)
             float dsel[JW];
 #pragma unroll
@@ -662,15 +752,12 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
                 for (int j = 0; j < JPMAX; ++j) bha[j] += dh[j];
             }
             store8_smem(Ast, 64 * 128 * 2, (rr >> 3) * 2048 + cg * 128 + (rr & 7) * 16, dz);
+            // and straight into the global dZ1 image T3b reads (8 lanes write one 128-byte
+            // core matrix per plane)
+            store8(p.dz1img, p.dzpl, dzimg(64 * (int64_t)c + rr, u0 + 8 * cg, N1), dz);
         }
         umma::fence_async_smem();
         __syncthreads();
-        if (storer) {   // the chunk's dZ1 image rows -> global (read by T3b)
-            const int pl = lane >> 3, rg = lane & 7;
-            bulk_s2g(p.dz1img + pl * p.dzpl + img((int64_t)c * 64 + 8 * rg, u0, N1), Ast + pl * (64 * 128 * 2) + rg * 2048,
-                     2048);
-            bulk_commit();
-        }
         if (tid == 0) {
             tcb::wait(&full[s], (uint32_t)((i >> 1) & 1));
 #pragma unroll
@@ -753,7 +840,6 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
                     make_float4(__uint_as_float(v[c][k]), __uint_as_float(v[c][k + 1]), __uint_as_float(v[c][k + 2]),
                                 __uint_as_float(v[c][k + 3]));
     }
-    if (storer) bulk_wait_all();
     umma::fence_before_sync();
     __syncthreads();
     if (warp == 0) umma::tmem_free(tb, 128);
@@ -794,6 +880,15 @@ __global__ void __launch_bounds__(tcb::T3B_T, 1) tcb_dh0_kernel(const __grid_con
     const uint32_t tb = *tslot;
     const bool fp32 = p.prec != RPL_PREC_BF16;
     char *Xs = smc + L.oX;
+    // this thread's H0 row (sample bt * 128 + tid: the ReLU mask of dZ0), loaded now so the
+    // L2 round trips overlap the dH0 main loop
+    float4 h0r[N0 / 4];
+    {
+        const int b = bt * 128 + tid;
+        const float4 *h0 = reinterpret_cast<const float4 *>(p.H0 + (int64_t)b * N0);
+#pragma unroll
+        for (int i = 0; i < N0 / 4; ++i) h0r[i] = b < B ? __ldcg(h0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     if (warp == 1) {
         // ---- producer ------------------------------------------------------------------------
         if (lane == 0) {
@@ -807,16 +902,12 @@ __global__ void __launch_bounds__(tcb::T3B_T, 1) tcb_dh0_kernel(const __grid_con
             if (lane == 0) umma::mbar_expect_tx(&full[s], T3B_STAGE_A + T3B_STAGE_B);
             __syncwarp();
             char *A = smc + L.oA + s * T3B_STAGE_A, *Bq = smc + L.oB + s * T3B_STAGE_B;
-            for (int c = lane; c < 51; c += 32) {
-                if (c < 48) {   // dZ1 rows of the tile, units [uc, uc + 64): 1 KB per row group
-                    const int pl = c >> 4, rg = c & 15;
-                    umma::bulk_g2s(A + pl * (128 * 64 * 2) + rg * 1024,
-                                   p.dz1img + pl * p.dzpl + img((int64_t)bt * 128 + 8 * rg, uc, N1), 1024, &full[s]);
-                } else {        // W1 rows [uc, uc + 64) of the online net
-                    const int pl = c - 48;
-                    umma::bulk_g2s(Bq + pl * (64 * N0 * 2), p.w1img + pl * p.w1pl + (int64_t)uc * N0, 64 * N0 * 2,
-                                   &full[s]);
-                }
+            if (lane < 3) {   // the (tile, 64-unit chunk) block of dZ1: one 16 KB piece per plane
+                umma::bulk_g2s(A + lane * (128 * 64 * 2), p.dz1img + lane * p.dzpl + dzimg((int64_t)bt * 128, uc, N1),
+                               128 * 64 * 2, &full[s]);
+            } else if (lane < 6) {   // W1 rows [uc, uc + 64) of the online net
+                const int pl = lane - 3;
+                umma::bulk_g2s(Bq + pl * (64 * N0 * 2), p.w1img + pl * p.w1pl + (int64_t)uc * N0, 64 * N0 * 2, &full[s]);
             }
         }
     } else if (warp == 0 && lane == 0) {
@@ -845,18 +936,15 @@ __global__ void __launch_bounds__(tcb::T3B_T, 1) tcb_dh0_kernel(const __grid_con
     // ---- dZ0 of the tile (thread = sample row = TMEM lane) into an MN-major image ----------
     char *Z = smc + L.oA;   // stage 0 and 1 of A: 3 planes x [128 x 128]
     {
-        const int r = tid, b = bt * 128 + r;
-        const bool ok = b < B;
-        const float *h0 = p.H0 + (int64_t)b * N0;
-#pragma unroll 1
+        const int r = tid;
+#pragma unroll
         for (int c0 = 0; c0 < N0; c0 += 16) {
             uint32_t v[16];
             ld16(lane_addr(tb, warp, c0), v);
             float hm[16];
 #pragma unroll
             for (int i = 0; i < 16; i += 4) {
-                float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (ok) t = __ldcg(reinterpret_cast<const float4 *>(h0 + c0 + i));
+                const float4 t = h0r[(c0 + i) >> 2];
                 hm[i] = t.x; hm[i + 1] = t.y; hm[i + 2] = t.z; hm[i + 3] = t.w;
             }
             wait_ld();

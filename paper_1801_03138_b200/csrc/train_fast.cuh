@@ -104,7 +104,7 @@ struct FastArgs {
     int tcb;             // 1: the step runs tc_big.cuh's kernels (K4 writes the W1 image)
     int Bp;              // B rounded up to 128 (rows past B are zero in every image)
     int jp;              // dheadp row pitch (J rounded up to 4)
-    uint16_t *h0img;     // [nets][3][Bp * 128] H0 of every net
+    uint16_t *h0img;     // [nets + 1][3][Bp * 128] H0 of every net (tile-quarter blocks, T1), then the online net on s (row-group major, T3a)
     uint16_t *ximg;      // [3][Bp * 32] [x | 1] of s
     uint16_t *dz1img;    // [3][Bp * N1] dZ1
     uint16_t *w1img;     // [online, target][3][N1 * 128] W1
@@ -1141,10 +1141,13 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
     };
     // (3) first float4 of the elementwise SGD over [w1, P)
     const int64_t lo = p.w1, n_el = p.P - p.w1;
-    const int64_t n4 = (p.nsb == 1 && !p.w1img) ? n_el / 4 : 0;
+    // float4 groups: the single-split gradient, or (large-batch path, w1 % 4 == 0) the sum of
+    // the batch-split partials with W1's bf16 image written from the new weights
+    const bool split4 = p.nsb > 1 && (p.w1 & 3) == 0 && (p.gps & 3) == 0 && (!p.w1img || (p.N0 & 3) == 0);
+    const int64_t n4 = ((p.nsb == 1 && !p.w1img) || split4) ? n_el / 4 : 0;
     int64_t e4 = (int64_t)blockIdx.x * NT + tid;
     float4 g4 = make_float4(0.f, 0.f, 0.f, 0.f), w4 = g4;
-    if (e4 < n4) {
+    if (e4 < n4 && p.nsb == 1) {
         g4 = __ldcg(reinterpret_cast<const float4 *>(p.grad + lo + 4 * e4));
         w4 = *reinterpret_cast<const float4 *>(p.online + lo + 4 * e4);
     }
@@ -1212,7 +1215,26 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
     // (4) every other parameter: [w1, P), float4 where whole
     for (; e4 < n4; e4 += stride) {
         const int64_t i = lo + 4 * e4;
-        if (e4 != (int64_t)blockIdx.x * NT + tid) {
+        if (split4) {
+            // the partials in split order, 8 float4 loads in flight (the same per-element sums)
+            float4 t[8];
+            g4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int sb0 = 0; sb0 < p.nsb; sb0 += 8) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (sb0 + k < p.nsb) t[k] = __ldcg(reinterpret_cast<const float4 *>(p.gpart + (int64_t)(sb0 + k) * p.gps + i));
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (sb0 + k < p.nsb) {
+                        g4.x += t[k].x;
+                        g4.y += t[k].y;
+                        g4.z += t[k].z;
+                        g4.w += t[k].w;
+                    }
+            }
+            *reinterpret_cast<float4 *>(p.grad + i) = g4;
+            w4 = *reinterpret_cast<const float4 *>(p.online + i);
+        } else if (e4 != (int64_t)blockIdx.x * NT + tid) {
             g4 = __ldcg(reinterpret_cast<const float4 *>(p.grad + i));
             w4 = *reinterpret_cast<const float4 *>(p.online + i);
         }
@@ -1223,6 +1245,29 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
             w4.w -= lr * g4.w;
             *reinterpret_cast<float4 *>(p.online + i) = w4;
             if (do_sync) *reinterpret_cast<float4 *>(p.target + i) = w4;
+            if (p.w1img && i < p.w1 + (int64_t)p.N1 * p.N0) {
+                // four consecutive inputs of one W1 row: 8 bytes of one core-matrix row per plane
+                const int64_t e = i - p.w1, u = p.N0 == 128 ? e >> 7 : e / p.N0;
+                const int k = (int)(e - u * p.N0);
+                const int64_t o = ((u >> 3) * (p.N0 >> 3) + (k >> 3)) * 64 + (u & 7) * 8 + (k & 7);
+                const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+                uint32_t pk[3][2];
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    uint16_t a0, a1, a2, b0, b1, b2;
+                    umma::split3_bf16(wv[2 * h2], a0, a1, a2);
+                    umma::split3_bf16(wv[2 * h2 + 1], b0, b1, b2);
+                    pk[0][h2] = (uint32_t)a0 | ((uint32_t)b0 << 16);
+                    pk[1][h2] = (uint32_t)a1 | ((uint32_t)b1 << 16);
+                    pk[2][h2] = (uint32_t)a2 | ((uint32_t)b2 << 16);
+                }
+                for (int net = 0; net < (do_sync ? 2 : 1); ++net) {
+                    uint16_t *im = p.w1img + net * 3 * p.w1pl;
+#pragma unroll
+                    for (int pl = 0; pl < 3; ++pl)
+                        *reinterpret_cast<uint2 *>(im + pl * p.w1pl + o) = make_uint2(pk[pl][0], pk[pl][1]);
+                }
+            }
         }
     }
     for (int64_t e = 4 * n4 + (int64_t)blockIdx.x * NT + tid; e < n_el; e += stride) {
@@ -1241,7 +1286,7 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
             if (do_sync) p.target[i] = w;
             if (p.w1img && i < p.w1 + (int64_t)p.N1 * p.N0) {
                 // the large-batch path's bf16 image of W1 (tc_big.cuh) for the next step
-                const int64_t e = i - p.w1, u = e / p.N0;
+                const int64_t e = i - p.w1, u = p.N0 == 128 ? e >> 7 : e / p.N0;
                 const int k = (int)(e - u * p.N0);
                 const int64_t o = ((u >> 3) * (p.N0 >> 3) + (k >> 3)) * 64 + (u & 7) * 8 + (k & 7);
                 uint16_t h, m, l;

@@ -139,6 +139,44 @@ __global__ void __launch_bounds__(256) wide_split_kernel(const float *__restrict
         planes[2 * pe + t] = l;
     }
 }
+// the same for D % 8 == 0 and a 16-byte aligned source: a thread splits 8 consecutive inputs
+// of one unit row (two 16-byte loads) into one 16-byte core-matrix row per plane; the grid's
+// y dimension is the unit, so no 64-bit division per element
+__global__ void __launch_bounds__(256) wide_split8_kernel(const float *__restrict__ src, uint16_t *planes, int64_t D)
+{
+    const int u = blockIdx.y;
+    const int64_t pe = wd_plane_elems(D), G = D >> 3;
+    const float *row = src + (int64_t)u * D;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
+        const float4 x0 = __ldg(reinterpret_cast<const float4 *>(row) + 2 * g);
+        const float4 x1 = __ldg(reinterpret_cast<const float4 *>(row) + 2 * g + 1);
+        const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        uint32_t hw[4], mw[4], lw[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            uint16_t h0, m0, l0, h1, m1, l1;
+            umma::split3_bf16(x[2 * i], h0, m0, l0);
+            umma::split3_bf16(x[2 * i + 1], h1, m1, l1);
+            hw[i] = pack2(h0, h1);
+            mw[i] = pack2(m0, m1);
+            lw[i] = pack2(l0, l1);
+        }
+        const int64_t t = wd_tix_k(u, g << 3);   // 8 consecutive k of one row: 16 contiguous bytes
+        *reinterpret_cast<uint4 *>(planes + t) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4 *>(planes + pe + t) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+        *reinterpret_cast<uint4 *>(planes + 2 * pe + t) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+}
+inline void launch_wide_split(const float *src, uint16_t *planes, int N0, int64_t D, int sms, cudaStream_t st)
+{
+    if (D % 8 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && N0 <= 65535) {
+        const int64_t G = D / 8;
+        const unsigned gx = (unsigned)std::min<int64_t>((G + 255) / 256, std::max(1, 4 * sms / std::max(1, N0)) * 8);
+        wide_split8_kernel<<<dim3(gx, (unsigned)N0), 256, 0, st>>>(src, planes, D);
+    } else {
+        wide_split_kernel<<<sms * 4, 256, 0, st>>>(src, planes, N0, D);
+    }
+}
 // a byte 0..255 as bf16: exact in fp32 and in bf16 (<= 8 significant bits), so the bf16 is the
 // fp32's upper half -- one I2F and a shift instead of the general rounding conversion
 __device__ __forceinline__ uint16_t u8_bf16(uint32_t v) { return (uint16_t)(__float_as_uint((float)v) >> 16); }

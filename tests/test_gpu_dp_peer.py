@@ -142,12 +142,15 @@ def test_emulated_ranks_dqn_gradients_vs_oracle_o6(b, world, rs):
     assert err.item() == 0
 
 
-@pytest.mark.parametrize("net", ["fast", "generic"])
-def test_self_attached_learner_equals_local(b, monkeypatch, net):
+@pytest.mark.parametrize("net,B", [("fast", 128), ("fast", 640), ("generic", 128)])
+def test_self_attached_learner_equals_local(b, monkeypatch, net, B):
+    # B = 640 takes the tcgen05 step (tc_big.cuh): the peer-memory update rewrites W1 without
+    # its bf16 images, so the online images are re-split before the next step and the target's
+    # after a sync step
     import torch
     if net == "generic":
         monkeypatch.setenv("RPL_PATH", "generic")
-    cfg = b.DQNConfig(max_batch=128, sync_period=4, double_dqn=True, lr=1e-3)
+    cfg = b.DQNConfig(max_batch=B, sync_period=4, double_dqn=True, lr=1e-3)
     p0 = init_params(27, 8, (128,), True, 512, seed=3)
     e = experiences(2000, seed=1)
     runs = []
@@ -161,7 +164,7 @@ def test_self_attached_learner_equals_local(b, monkeypatch, net):
             dqn.attach_peers(0, 1, h)
         loss = torch.zeros(1, device="cuda")
         for _ in range(7):
-            assert dqn.train_step(rp, 128, loss) == b.RPL_OK
+            assert dqn.train_step(rp, B, loss) == b.RPL_OK
         torch.cuda.synchronize()
         assert dqn.check() == b.RPL_OK and np.isfinite(loss.item())
         runs.append((dqn.get_params(b.RPL_ONLINE), dqn.get_params(b.RPL_TARGET), loss.item(),
@@ -189,11 +192,12 @@ def test_self_attached_wide_learner_equals_local(b):
         dqn = b.DQN(cfg, p0)
         if attach:
             dqn.attach_peers(0, 1, dqn.peer_handle())
-        for _ in range(4):
+        for _ in range(7):   # syncs after steps 3 and 6: the target planes are re-split then only
             assert dqn.train_step(rp, 32) == b.RPL_OK
         assert dqn.check() == b.RPL_OK
-        runs.append(dqn.get_params(b.RPL_ONLINE))
-    assert np.array_equal(runs[0], runs[1])
+        runs.append((dqn.get_params(b.RPL_ONLINE), dqn.get_params(b.RPL_TARGET)))
+    assert np.array_equal(runs[0][0], runs[1][0])
+    assert np.array_equal(runs[0][1], runs[1][1])
 
 
 def _ipc_worker(rank, world, port, q):

@@ -1,4 +1,4 @@
-"""GPU parity of the large-batch tensor-core step (csrc/tc_big.cuh: batches >= kTcbMinBatch = 512)
+"""GPU parity of the large-batch tensor-core step (csrc/tc_big.cuh: batches >= kTcbMinBatch = 640)
 against the oracle, through the C-ABI (tests/parity.py: idx / batch bit-exact, Q / y / loss /
 gradients / new weights within 1e-5 normwise in FP32, 2e-2 at BF16 precision).
 
@@ -48,7 +48,7 @@ def _replay(b, cap=20_000, n=25_000, seed=6, **kw):
 
 
 @pytest.mark.parametrize("ddqn", [False, True], ids=["dqn", "ddqn"])
-@pytest.mark.parametrize("batch", [512, 600, 1000, 4096])
+@pytest.mark.parametrize("batch", [640, 700, 1000, 4096])
 def test_tcb_steps(b, batch, ddqn):
     cfg = _cfg(b, double_dqn=ddqn)
     rp, orc = _replay(b)
@@ -67,7 +67,7 @@ def test_tcb_plain_mlp(b):
 
 
 def test_tcb_switching_batch_sizes(b):
-    # mma.sync steps (B < 512) update W1 without its image; the next tensor-core step re-splits
+    # mma.sync steps (B < 640) update W1 without its image; the next tensor-core step re-splits
     cfg = _cfg(b, double_dqn=True, sync_period=3)
     rp, orc = _replay(b)
     dqn = b.DQN(cfg, _params(cfg, seed=11))

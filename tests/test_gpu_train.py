@@ -38,12 +38,16 @@ def _params(cfg, seed=3, dyadic=False):
                        seed=seed, dyadic=dyadic)
 
 
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
 @pytest.mark.parametrize("ddqn", [False, True], ids=["dqn", "ddqn"])
-def test_c1_200_steps_teacher_forced(b, ddqn):
+def test_c1_200_steps_teacher_forced(b, ddqn, precision):
     # BASELINE configs[0]: capacity 1000, D=27, 8 actions, B=32, 2x64 MLP, burn-in 100,
     # 200 executed train steps; 7 adds per iteration (the ring wraps in iteration 143);
-    # target sync every 50 steps
-    cfg = _cfg(b, dueling=False, hidden=(64, 64), double_dqn=ddqn, sync_period=50, max_batch=32)
+    # target sync every 50 steps.  BF16 (reading Q33): one bf16 product per tensor-core
+    # product, the north star's 2e-2 per step and for the 200-step drift
+    tol = 1e-5 if precision == "fp32" else 2e-2
+    cfg = _cfg(b, dueling=False, hidden=(64, 64), double_dqn=ddqn, sync_period=50, max_batch=32,
+               precision=precision)
     p0 = _params(cfg)
     rp = b.Replay(1000, 27, burn_in=100, seed=2)
     dqn = b.DQN(cfg, p0)
@@ -59,7 +63,7 @@ def test_c1_200_steps_teacher_forced(b, ddqn):
         rp.add(**part)
         orc.add(**part)
         free_ring.add(**part)
-        out = step_and_compare(b, cfg, dqn, rp, orc, 32, seed=2, burn_in=100, stats=stats)
+        out = step_and_compare(b, cfg, dqn, rp, orc, 32, seed=2, burn_in=100, stats=stats, tol=tol)
         ln.step(free_ring, 32)
         if out is None:
             assert it <= 14
@@ -73,8 +77,9 @@ def test_c1_200_steps_teacher_forced(b, ddqn):
             assert np.array_equal(tgt, out["target_before"])            # frozen
     assert executed == 200 and dqn.steps == 200
     # free-running drift of the fp32 device learner vs the fp64-arithmetic oracle learner
-    drift = normwise(dqn.get_params(b.RPL_ONLINE), ln.online, 1e-3, "200-step drift")
-    print(f"\nC1 {'DDQN' if ddqn else 'DQN'}: 200 steps, mask flips replayed {stats['mask_flips']},"
+    drift = normwise(dqn.get_params(b.RPL_ONLINE), ln.online, 1e-3 if precision == "fp32" else 2e-2,
+                     "200-step drift")
+    print(f"\nC1 {'DDQN' if ddqn else 'DQN'} {precision}: 200 steps, mask flips replayed {stats['mask_flips']},"
           f" free-running drift {drift:.2e}")
     assert dqn.check() == b.RPL_OK
 
