@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gather", action="store_true")
+    ap.add_argument("--no-c5", action="store_true",
+                    help="skip the config-5 (84x84x4 u8, 1M rows) measurement the default run embeds")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--sweep", default="", help="comma list of batch sizes: one JSON line each")
     ap.add_argument("--avg-period", type=int, default=0,
@@ -235,6 +237,12 @@ def load_traffic():
     return {}
 
 
+def step_traffic(key):
+    """(warm, cold) DRAM bytes per step for a bench shape, or None when not captured"""
+    t = load_traffic()
+    return (t[key], t.get(key + "_cold")) if key in t else None
+
+
 def kernel_breakdown(step, n):
     """Per-kernel device time of `n` calls of step(i), from CUPTI (torch.profiler): mean us per
     launch, launches per step and share of the summed kernel time; run after the timed region."""
@@ -292,19 +300,30 @@ def step_roofline(cfg, binding, batch, flops, ms_per_step, kb, peaks, peaks_kind
     achieved = flops / (ms_per_step / 1000.0) / 1e12
     fwd, bwd = flop_parts(cfg, batch)
     kernels = []
+    # the tensor-core kernels of the large-batch step (tc_big.cuh): their own contractions
+    nets = 3 if cfg.double_dqn else 2
+    n0, n1 = (cfg.hidden[0], 2 * cfg.stream) if cfg.dueling else (cfg.hidden[0], cfg.hidden[1] if len(cfg.hidden) > 1 else 0)
+    tcb_flops = {"tcb_fwd": 2 * batch * nets * n1 * n0, "tcb_dw1": 2 * batch * n1 * n0,
+                 "tcb_dh0": 2 * batch * n0 * n1 + 2 * batch * n0 * (cfg.state_dim + 1)}
     for d in kb["kernels"]:
         row = dict(d)
         name = d["kernel"]
-        f = fwd if "fwd" in name else bwd if "bwd1" in name else None
+        f = next((v for k, v in tcb_flops.items() if k in name), None)
+        if f is None:
+            f = fwd if "fast_fwd" in name else bwd if "bwd1" in name else None
         if f is not None and d["mean_us"] > 0:
             row["flops"] = f
             row["achieved_TFLOPs"] = f / (d["mean_us"] * 1e-6) / 1e12
             row["frac"] = row["achieved_TFLOPs"] / peak
         kernels.append(row)
     return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": traffic,
-            "kernel": "the train step as one unit (one CUDA graph: fwd / td / bwd1 / bwd0+sgd "
-                      "kernels): its algorithmic FLOPs / the timed ms_per_step",
+            "frac": achieved / peak, "traffic": traffic[0] if traffic else None,
+            "traffic_cold": traffic[1] if traffic else None,
+            "traffic_note": "DRAM bytes per step from ncu (profiles/traffic.json, profiles/r02/traffic/): "
+                            "traffic = warm (--cache-control none, the steady state), traffic_cold = "
+                            "ncu's default cache flush per kernel" if traffic else None,
+            "kernel": "the train step as one unit (one CUDA graph of the kernels listed in "
+                      "kernels_cupti): its algorithmic FLOPs / the timed ms_per_step",
             "kernel_avg_us": ms_per_step * 1000.0, "flops_per_launch": flops,
             "peak_note": f"measured bf16 dense {bf16:.0f} TFLOP/s sustained ({peaks_kind}) x 0.5 "
                          "(nominal tf32 / bf16 ratio)"
@@ -528,7 +547,7 @@ def run_ours(a, batch, first_line=True):
     # tensor-core kernel on its own (its FLOPs / its CUPTI mean duration) ------------------
     flops = binding.step_flops(cfg, batch)
     roofline = step_roofline(cfg, binding, batch, flops, ms_per_step, kb, peaks, peaks_kind,
-                             load_traffic().get(f"train_step_b{batch}_{a.net}_{'ddqn' if a.ddqn else 'dqn'}"))
+                             step_traffic(f"train_step_b{batch}_{a.net}_{'ddqn' if a.ddqn else 'dqn'}"))
 
     # ---- gather bandwidth (metric part 2): explicit-index gather from the 1M ring --------
     gather = None
@@ -670,11 +689,28 @@ def run_ours(a, batch, first_line=True):
         "dp_p2p_arm": p2p_arm,
         "clocks": (clk.stop(), clk.summary())[1],
     }
+    default_run = (batch == 128 and not a.ddqn and a.net == "dueling" and a.ring == "device" and
+                   not a.distinct and not a.shared_state and a.precision == "fp32" and not a.avg_period)
+    if first_line and not a.sweep and world == 1 and not a.no_c5 and default_run:
+        # BASELINE configs[4] measured in the same run (the driver's default invocation), on
+        # its full 1M-row, 56.6 GB byte ring: a compact copy of the --config c5 line
+        line["c5"] = c5_summary(a)
     if rank == 0:
         print(json.dumps(line), flush=True)
     dqn.close()
     rp.close()
     return line
+
+
+def c5_summary(a):
+    a5 = argparse.Namespace(**vars(a))
+    a5.steps, a5.warmup = min(a.steps, 1000), max(3, min(a.warmup, 50))
+    a5.batch, a5.capacity, a5.no_cpu_baseline, a5.no_gather = 256, 1_000_000, True, False
+    a5.ddqn = False
+    line = run_c5(a5, emit=False)
+    keep = ("metric", "value", "unit", "steps", "warmup", "ms_per_step", "dtype", "config",
+            "samples_per_s", "gpu_launches", "roofline", "e2e", "gather", "clocks")
+    return {k: line[k] for k in keep}
 
 
 def time_p2p_arm(a, binding, cfg, rp, batch, add_dev, i0, stream, dev):
@@ -762,7 +798,7 @@ def time_oracle_c5(batch, ddqn, seconds, pool):
             return n, el
 
 
-def run_c5(a):
+def run_c5(a, emit=True):
     import torch
     import torch.distributed as dist
     import paper_1801_03138_b200.binding as binding
@@ -952,10 +988,11 @@ def run_c5(a):
         "samples_per_s": value * batch, "gpu_launches": launches, "roofline": roofline,
         "cpu_baseline": cpu, "e2e": e2e, "gather": gather, "clocks": (clk.stop(), clk.summary())[1],
     }
-    if rank == 0:
+    if rank == 0 and emit:
         print(json.dumps(line), flush=True)
     dqn.close()
     rp.close()
+    return line
 
 
 def spawn_ranks(n: int) -> int:

@@ -1270,7 +1270,7 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
             ok = dalloc(d, &d->dH0p, (size_t)wneed);
             d->dh0p_elems = wneed;
         }
-        const int64_t pneed = (int64_t)nets * (d->N[1] / 64) * Bm * d->J;
+        const int64_t pneed = (int64_t)nets * (d->N[1] / 128) * tcb::T1_PSL * Bm * d->J;
         if (ok && pneed > d->part_elems) {
             ok = dalloc(d, &d->part, (size_t)pneed);
             d->part_elems = pneed;

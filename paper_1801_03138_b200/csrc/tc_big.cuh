@@ -12,10 +12,10 @@
 //                      [x | 1] image of s
 //   T1 tcb_fwd_kernel  layer 1 of every net: D1[b][u] = H0 W1^T (M = 128 samples, N = 128
 //                      units, K = 128), + b1, ReLU, the head's partial dot products per
-//                      64-unit half tile (FMA), H1 (fp32) of the online net on s.  Persistent
-//                      per (net, unit tile): the W1 tile stays in shared memory, the H0
-//                      tiles stream through a 4-slot ring; one producer warp (TMA), one MMA
-//                      warp, eight epilogue warps on a double-buffered accumulator
+//                      64-unit column group (FMA), H1 (fp32) of the online net on s.
+//                      Persistent per (net, unit tile): the W1 tile stays in shared memory,
+//                      the H0 tiles stream through a 4-slot ring; one producer warp (TMA),
+//                      one MMA warp, 8 epilogue warps on a double-buffered accumulator
 //   TD tcb_td_kernel   head sums, dueling combine, DQN / Double-DQN target, Huber,
 //                      dHead -- a warp per sample (train_fast.cuh td_warp)
 //   T3a tcb_dw1_kernel per (unit tile, batch chunk group): dZ1 = (dHead . W_head) * [H1 > 0]
@@ -55,7 +55,15 @@ constexpr int N0 = 128;       // layer-0 units (the M of the dW0 MMA, the K of l
 constexpr int JW = 8;         // head outputs one unit tile contributes to (dueling A stream: |A|)
 constexpr int JPMAX = 16;     // padded head width of dHead rows (J <= 16)
 constexpr int T0_ROWS = 16, T0_T = 256;   // T0: 16 half-warps, one sampled row each
-constexpr int T1_T = 320;     // warps 0-7 epilogue, 8 producer, 9 MMA
+constexpr int T1_EPW = 8;     // T1 epilogue warps: 2 per TMEM lane quarter (16 measured slower)
+constexpr int T1_PSL = 1;                   // head partial slots per 128-unit tile (TD sums N1 / 128)
+constexpr int T1_CPW = 128 / (T1_EPW / 4);  // accumulator columns per epilogue thread
+constexpr int T1_HN = 16;                   // head MMA N: the tile's head outputs, padded (J <= 16)
+// T1 tensor memory (512 columns): two layer-1 accumulators [0, 256), the head accumulator
+// [256, 272), the head MMA's A operand = H1 of the tile as 3 bf16 planes of 64 columns
+// (two bf16 per 32-bit column, even k in the low half) [320, 512)
+constexpr int T1_TM_DH = 256, T1_TM_AH = 320;
+constexpr int T1_T = (T1_EPW + 2) * 32;     // + producer warp, MMA warp
 constexpr int T1_SLOTS = 4;   // H0 ring slots (one 32-deep K quarter of a 128-row tile each)
 constexpr int T1_SLOT = 3 * 128 * 32 * 2;   // bytes of one slot (three planes)
 constexpr int T3A_T = 256;
@@ -145,6 +153,36 @@ __device__ __forceinline__ void ld16(uint32_t a, uint32_t (&r)[16])
                  : "r"(a));
 }
 __device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void st16(uint32_t a, const uint32_t *r)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                 :: "r"(a), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+                    "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+                 : "memory");
+}
+__device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// D[tmem] (+)= A[tmem] * B[smem]^T (kind::f16, A: M lanes x K packed two bf16 per column)
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t id, bool acc)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n"
+                 :: "r"(d), "r"(a), "l"(b), "r"(id), "r"((uint32_t)acc) : "memory");
+}
+// mma6 with the A terms in tensor memory (same product order)
+__device__ __forceinline__ void mma6_ts(uint32_t d, const uint32_t (&a)[3], const uint64_t (&b)[3], uint32_t id,
+                                        bool acc, bool fp32)
+{
+    if (fp32) {
+        mma_bf16_ts(d, a[2], b[0], id, acc);
+        mma_bf16_ts(d, a[0], b[2], id, true);
+        mma_bf16_ts(d, a[1], b[1], id, true);
+        mma_bf16_ts(d, a[1], b[0], id, true);
+        mma_bf16_ts(d, a[0], b[1], id, true);
+        mma_bf16_ts(d, a[0], b[0], id, true);
+    } else {
+        mma_bf16_ts(d, a[0], b[0], id, acc);
+    }
+}
 __device__ __forceinline__ uint32_t lane_addr(uint32_t base, int quarter, int col)
 {
     return base + ((uint32_t)(32 * quarter) << 16) + (uint32_t)col;
@@ -192,16 +230,34 @@ __device__ __forceinline__ float head_w(const FastArgs &p, const float *theta, i
     return j > 0 ? __ldg(theta + p.wh + (int64_t)j * p.S + (u - p.S)) : 0.0f;
 }
 
+// the head weights [J][128] of the unit tile at u0 into shared memory: every load of a thread
+// issued before the first store (J <= JPMAX, nt >= 256: at most 8 per thread)
+__device__ __forceinline__ void stage_head(const FastArgs &p, const float *theta, int u0, float *Whs, int tid, int nt)
+{
+    const int n = p.J * 128;
+    float v[JPMAX * 128 / 256];
+#pragma unroll
+    for (int i = 0; i < JPMAX * 128 / 256; ++i) {
+        const int e = tid + i * nt;
+        v[i] = e < n ? head_w(p, theta, e >> 7, u0 + (e & 127)) : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < JPMAX * 128 / 256; ++i) {
+        const int e = tid + i * nt;
+        if (e < n) Whs[e] = v[i];
+    }
+}
+
 struct T1Smem {
     int oW1, oA, oWh, ob1, obar, total;
-    __host__ __device__ T1Smem(int J)
+    __host__ __device__ T1Smem(int)
     {
         oW1 = 0;                               // W1 tile: 3 planes x [128 units x 128]
         oA = oW1 + 3 * 128 * N0 * 2;           // H0 ring: T1_SLOTS x 3 planes x [128 x 32]
-        oWh = oA + T1_SLOTS * T1_SLOT;         // the tile's head weights [J][128] fp32
-        ob1 = oWh + J * 128 * 4;               // b1 of the tile [128]
-        obar = (ob1 + 128 * 4 + 15) & ~15;     // 13 mbarriers + the TMEM base
-        total = obar + 14 * 8;
+        oWh = oA + T1_SLOTS * T1_SLOT;         // the tile's head weights: 3 planes x [16 x 128] bf16
+        ob1 = oWh + 3 * T1_HN * 128 * 2;       // b1 of the tile [128]
+        obar = (ob1 + 128 * 4 + 15) & ~15;     // 15 mbarriers + the TMEM base
+        total = obar + 16 * 8;
     }
 };
 struct T3aSmem {
@@ -448,19 +504,27 @@ __global__ void __launch_bounds__(tcb::T1_T, 1) tcb_fwd_kernel(const __grid_cons
     const int N1 = p.N1, B = p.B, J = p.J;
     const T1Smem L(J);
     char *W1s = smc + L.oW1, *As = smc + L.oA;
-    float *Whs = reinterpret_cast<float *>(smc + L.oWh), *b1s = reinterpret_cast<float *>(smc + L.ob1);
+    char *Whs = smc + L.oWh;
+    float *b1s = reinterpret_cast<float *>(smc + L.ob1);
     uint64_t *bar = reinterpret_cast<uint64_t *>(smc + L.obar);
     uint64_t *wbar = bar, *full = bar + 1, *empty = bar + 1 + T1_SLOTS, *accf = bar + 1 + 2 * T1_SLOTS,
-             *acce = accf + 2;
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(bar + 13);
+             *acce = accf + 2, *hready = acce + 2, *hdone = hready + 1;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(bar + 15);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nut = N1 / 128, ncombo = p.nets * nut;
     const int combo = blockIdx.x % ncombo, cpc = gridDim.x / ncombo, bt0 = blockIdx.x / ncombo;
     const int net = combo / nut, ut = combo % nut, u0 = ut * 128;
     const int nbt = p.Bp / 128, nq = N0 / 32;
     const int ntile = bt0 < nbt ? (nbt - bt0 + cpc - 1) / cpc : 0;
-    if (warp == 0) umma::tmem_alloc(tslot, 256);
+    // RPL_TRACE: per-CTA cycle totals (kernel slot 4): 2 MMA thread waiting for H0 slots, 3 MMA
+    // thread waiting for a drained accumulator, 4 epilogue waiting for an accumulator, 5
+    // epilogue work per tile, 6 producer waiting for a free slot
+    CtaTrace tr_(p.trace, 4);
+    const int mma_tid = 32 * (T1_EPW + 1), prod_tid = 32 * T1_EPW;
+    if (warp == 0) umma::tmem_alloc(tslot, 512);
     if (tid == 0) {
+        umma::mbar_init(hready, T1_EPW);
+        umma::mbar_init(hdone, 1);
         umma::mbar_init(wbar, 1);
         for (int i = 0; i < T1_SLOTS; ++i) {
             umma::mbar_init(&full[i], 1);
@@ -468,7 +532,7 @@ __global__ void __launch_bounds__(tcb::T1_T, 1) tcb_fwd_kernel(const __grid_cons
         }
         for (int i = 0; i < 2; ++i) {
             umma::mbar_init(&accf[i], 1);
-            umma::mbar_init(&acce[i], 8);
+            umma::mbar_init(&acce[i], T1_EPW);
         }
         umma::fence_mbar_init();
     }
@@ -479,7 +543,7 @@ __global__ void __launch_bounds__(tcb::T1_T, 1) tcb_fwd_kernel(const __grid_cons
     const uint16_t *h0 = p.h0img + (int64_t)net * 3 * p.h0pl;
     const uint16_t *w1 = p.w1img + (net == 1 ? 3 * p.w1pl : 0);   // the target's image for net 1
     const float *theta = net == 1 ? p.target : p.online;
-    if (warp == 8) {
+    if (warp == T1_EPW) {
         // ---- producer: the W1 tile once, then the H0 quarters through the ring -------------
         if (lane == 0) {
             umma::mbar_expect_tx(wbar, 3 * 128 * N0 * 2);
@@ -488,7 +552,9 @@ __global__ void __launch_bounds__(tcb::T1_T, 1) tcb_fwd_kernel(const __grid_cons
         }
         for (int n = 0; n < ntile * nq; ++n) {
             const int it = n / nq, q = n - it * nq, bt = bt0 + it * cpc, slot = n % T1_SLOTS;
+            long long t0 = tr_.now_by(prod_tid);
             if (n >= T1_SLOTS) umma::mbar_wait(&empty[slot], (uint32_t)(((n / T1_SLOTS) - 1) & 1));
+            tr_.acc_by(prod_tid, 6, t0);
             if (lane == 0) umma::mbar_expect_tx(&full[slot], T1_SLOT);
             __syncwarp();
             char *dst = As + slot * T1_SLOT;
@@ -497,19 +563,42 @@ __global__ void __launch_bounds__(tcb::T1_T, 1) tcb_fwd_kernel(const __grid_cons
                 umma::bulk_g2s(dst + lane * (128 * 32 * 2), h0 + lane * p.h0pl + qimg((int64_t)bt * 128, 32 * q),
                                128 * 32 * 2, &full[slot]);
         }
-    } else if (warp == 9) {
+    } else if (warp == T1_EPW + 1) {
         // ---- MMA issue ------------------------------------------------------------------------
         if (lane == 0) {
             const uint32_t id = umma::idesc_bf16(128, 128, false, false);
+            const uint32_t idh = umma::idesc_bf16(128, T1_HN, false, false);
             const bool fp32 = p.prec != RPL_PREC_BF16;
+            // the head contraction of tile t: D_head[b][j] = sum_u H1[b][u] W_head[j][u]
+            // (M = 128 samples, N = 16 outputs, K = 128 units; A = the H1 planes the epilogue
+            // wrote into tensor memory, B = the tile's head-weight image)
+            auto head = [&](int t) {
+                tcb::wait(hready, (uint32_t)(t & 1));
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    uint32_t ad[3];
+                    uint64_t bd[3];
+#pragma unroll
+                    for (int pl = 0; pl < 3; ++pl) {
+                        ad[pl] = tb + (uint32_t)(T1_TM_AH + 64 * pl + 8 * ks);
+                        bd[pl] = umma::desc(Whs + pl * (T1_HN * 128 * 2) + ks * 2 * 128, 128, (128 / 8) * 128);
+                    }
+                    mma6_ts(tb + T1_TM_DH, ad, bd, idh, ks > 0, fp32);
+                }
+                umma::commit(hdone);
+            };
             tcb::wait(wbar, 0);
             for (int it = 0; it < ntile; ++it) {
                 const int acc = it & 1;
+                long long t0 = tr_.now_by(mma_tid);
                 if (it >= 2) tcb::wait(&acce[acc], (uint32_t)(((it >> 1) - 1) & 1));
+                tr_.acc_by(mma_tid, 3, t0);
                 const uint32_t dcol = tb + (uint32_t)(acc * 128);
                 for (int q = 0; q < nq; ++q) {
                     const int n = it * nq + q, slot = n % T1_SLOTS;
+                    long long t1 = tr_.now_by(mma_tid);
                     tcb::wait(&full[slot], (uint32_t)((n / T1_SLOTS) & 1));
+                    tr_.acc_by(mma_tid, 2, t1);
                     const char *a = As + slot * T1_SLOT;
 #pragma unroll
                     for (int s = 0; s < 2; ++s) {
@@ -525,66 +614,104 @@ __global__ void __launch_bounds__(tcb::T1_T, 1) tcb_fwd_kernel(const __grid_cons
                     umma::commit(&empty[slot]);
                 }
                 umma::commit(&accf[acc]);
+                if (it >= 1) head(it - 1);
             }
+            if (ntile > 0) head(ntile - 1);
         }
     } else {
-        // ---- epilogue (warps 0-7): warp w reads TMEM lane quarter w % 4, columns 64 (w / 4) ...
-        for (int e = tid; e < J * 128; e += 256) {
-            const int j = e >> 7, c = e & 127;
-            Whs[e] = head_w(p, theta, j, u0 + c);
+        // ---- epilogue (warps 0 .. T1_EPW-1): warp w reads TMEM lane quarter w % 4, columns
+        // T1_CPW (w / 4) ...: bias, ReLU, H1 of the online net; H1's bf16 planes into tensor
+        // memory for the head MMA; the previous tile's head sums out as partials
+        {   // the tile's head-weight image (rows j < J of head_w, zero where unit u does not feed
+            // j and for the padding rows): thread = (output j, 8 consecutive units)
+            const int j = tid >> 4, ug = tid & 15;
+            float w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = j < J ? head_w(p, theta, j, u0 + 8 * ug + i) : 0.0f;
+            store8_smem(Whs, T1_HN * 128 * 2, (int)img(j, 8 * ug, 128) * 2, w);
         }
-        for (int c = tid; c < 128; c += 256) b1s[c] = __ldg(theta + p.b1 + u0 + c);
-        epi_sync(256);
-        int jlo, jhi;
-        head_range(p, u0, jlo, jhi);
-        const int quarter = warp & 3, half = warp >> 2, nut2 = N1 / 64;
+        for (int c = tid; c < 128; c += 32 * T1_EPW) b1s[c] = __ldg(theta + p.b1 + u0 + c);
+        umma::fence_async_smem();   // the head image is read by the tensor cores
+        epi_sync(32 * T1_EPW);
+        const int quarter = warp & 3, half = warp >> 2, nps = (N1 / 128) * T1_PSL;
+        // the head sums of tile t (its D_head, complete) -> this row's partials
+        auto head_out = [&](int t) {
+            tcb::wait(hdone, (uint32_t)(t & 1));
+            uint32_t dh[16];
+            ld16(lane_addr(tb + T1_TM_DH, quarter, 0), dh);
+            wait_ld();
+            const int b = (bt0 + t * cpc) * 128 + 32 * quarter + lane;
+            if (half == 0 && b < B) {
+                float *po = p.part + (((int64_t)net * nps + ut) * B + b) * J;
+#pragma unroll
+                for (int j = 0; j < T1_HN; ++j)
+                    if (j < J) po[j] = __uint_as_float(dh[j]);
+            }
+        };
         for (int it = 0; it < ntile; ++it) {
             const int acc = it & 1, bt = bt0 + it * cpc, b = bt * 128 + 32 * quarter + lane;
+            long long t0 = tr_.now();
             tcb::wait(&accf[acc], (uint32_t)((it >> 1) & 1));
-            float ha[JW];
+            tr_.acc(4, t0);
+            t0 = tr_.now();
+            uint32_t v[T1_CPW / 16][16];
 #pragma unroll
-            for (int j = 0; j < JW; ++j) ha[j] = 0.0f;
-            uint32_t v[4][16];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) ld16(lane_addr(tb + (uint32_t)(acc * 128), quarter, 64 * half + 16 * c), v[c]);
+            for (int c = 0; c < T1_CPW / 16; ++c) ld16(lane_addr(tb + (uint32_t)(acc * 128), quarter, T1_CPW * half + 16 * c), v[c]);
             wait_ld();
             umma::fence_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acce[acc]);   // accumulator drained into registers
+            uint32_t pk[3][T1_CPW / 2];               // H1 planes, two bf16 per word
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int c0 = 64 * half + 16 * c;
-                float h[16];
+            for (int c = 0; c < T1_CPW / 16; ++c) {
+                const int c0 = T1_CPW * half + 16 * c;
+                float h[16], bb[16];
+                // 16-byte shared loads (broadcast: every lane of the warp reads the same words)
 #pragma unroll
-                for (int i = 0; i < 16; ++i) h[i] = fmaxf(__uint_as_float(v[c][i]) + b1s[c0 + i], 0.0f);
+                for (int i = 0; i < 16; i += 4) {
+                    const float4 t = *reinterpret_cast<const float4 *>(b1s + c0 + i);
+                    bb[i] = t.x; bb[i + 1] = t.y; bb[i + 2] = t.z; bb[i + 3] = t.w;
+                }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) h[i] = fmaxf(__uint_as_float(v[c][i]) + bb[i], 0.0f);
+#ifndef RPL_T1_NOH1   // (timing experiment only: results invalid without H1)
                 if (net == 0 && b < B) {
+#else
+                if (net == 0 && b < 0) {
+#endif
                     float *ho = p.H1 + (int64_t)b * N1 + u0 + c0;
 #pragma unroll
                     for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4 *>(ho + i) = make_float4(h[i], h[i + 1], h[i + 2], h[i + 3]);
                 }
 #pragma unroll
-                for (int j = 0; j < JW; ++j)
-                    if (jlo + j < jhi) {
-                        const float *w = Whs + (jlo + j) * 128 + c0;
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) ha[j] = fmaf(h[i], w[i], ha[j]);
-                    }
-            }
-            if (b < B) {
-                float *po = p.part + (((int64_t)net * nut2 + ut * 2 + half) * B + b) * J;
-                for (int j = 0; j < J; ++j) {
-                    float v2 = 0.0f;
-#pragma unroll
-                    for (int q = 0; q < JW; ++q)
-                        if (j == jlo + q) v2 = ha[q];
-                    po[j] = (j >= jlo && j < jhi) ? v2 : 0.0f;
+                for (int i = 0; i < 16; i += 2) {
+                    uint16_t a0, a1, a2, b0, b1, b2;
+                    umma::split3_bf16(h[i], a0, a1, a2);
+                    umma::split3_bf16(h[i + 1], b0, b1, b2);
+                    pk[0][8 * c + i / 2] = (uint32_t)a0 | ((uint32_t)b0 << 16);
+                    pk[1][8 * c + i / 2] = (uint32_t)a1 | ((uint32_t)b1 << 16);
+                    pk[2][8 * c + i / 2] = (uint32_t)a2 | ((uint32_t)b2 << 16);
                 }
             }
+            // the previous tile's head MMAs have read the A planes and written D_head
+            if (it >= 1) head_out(it - 1);
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl)
+#pragma unroll
+                for (int c = 0; c < T1_CPW / 32; ++c)
+                    st16(lane_addr(tb + (uint32_t)(T1_TM_AH + 64 * pl), quarter, (T1_CPW / 2) * half + 16 * c),
+                         &pk[pl][16 * c]);
+            wait_st();
+            umma::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(hready);
+            tr_.acc(5, t0);
         }
+        if (ntile > 0) head_out(ntile - 1);
     }
     umma::fence_before_sync();
     __syncthreads();
-    if (warp == 0) umma::tmem_free(tb, 256);
+    if (warp == 0) umma::tmem_free(tb, 512);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -604,7 +731,7 @@ __global__ void __launch_bounds__(256) tcb_td_kernel(const __grid_constant__ Fas
         const int64_t t = *p.step_dev + 1;
         *p.sync_flag = (p.sync_period > 0 && t % p.sync_period == 0) ? 1 : 0;
     }
-    const int J = p.J, B = p.B, nut2 = p.N1 / 64, b0 = blockIdx.x * 8;
+    const int J = p.J, B = p.B, nut2 = (p.N1 / 128) * tcb::T1_PSL, b0 = blockIdx.x * 8;
     const int nb = min(8, B - b0), span = nb * J, nseg = p.nets * nut2, n = nseg * span;
 #pragma unroll 8
     for (int e = threadIdx.x; e < n; e += 256) {
@@ -632,7 +759,7 @@ __global__ void __launch_bounds__(256) tcb_td_kernel(const __grid_constant__ Fas
     __syncwarp();
     if (lane < p.jp) p.dheadp[(int64_t)b * p.jp + lane] = lane < J ? dhs[warp][lane] : 0.0f;
 }
-inline size_t tcb_td_smem(int nets, int N1, int J) { return (size_t)nets * (N1 / 64) * 8 * J * sizeof(float); }
+inline size_t tcb_td_smem(int nets, int N1, int J) { return (size_t)nets * (N1 / 128) * tcb::T1_PSL * 8 * J * sizeof(float); }
 
 // ------------------------------------------------------------------------------------------
 // T3a: per (128-unit tile ut, chunk group g): 64-row chunks c = g, g + G, ... of the batch.
@@ -663,7 +790,7 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
         umma::mbar_init(mdone, 1);
         umma::fence_mbar_init();
     }
-    for (int e = tid; e < J * 128; e += T3A_T) Whs[e] = head_w(p, p.online, e >> 7, u0 + (e & 127));
+    stage_head(p, p.online, u0, Whs, tid, T3A_T);
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
@@ -734,17 +861,25 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
             float dsel[JW];
 #pragma unroll
             for (int j = 0; j < JW; ++j) dsel[j] = jlo ? dh[j + 1] : dh[j];
-            float dz[8];
+            float dz[8], gs[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                float gs = 0.0f;
+            for (int k = 0; k < 8; ++k) gs[k] = 0.0f;
+            // head weights of the 8 units, two 16-byte shared loads per output
 #pragma unroll
-                for (int j = 0; j < JW; ++j)
-                    if (jlo + j < jhi) {
-                        gs = fmaf(dsel[j], Whs[(jlo + j) * 128 + 8 * cg + k], gs);
+            for (int j = 0; j < JW; ++j)
+                if (jlo + j < jhi) {
+                    const float4 *w4 = reinterpret_cast<const float4 *>(Whs + (jlo + j) * 128 + 8 * cg);
+                    const float4 wa = w4[0], wb = w4[1];
+                    const float w[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        gs[k] = fmaf(dsel[j], w[k], gs[k]);
                         wacc[j][k] = fmaf(dsel[j], h1[k], wacc[j][k]);
                     }
-                dz[k] = h1[k] > 0.0f ? gs : 0.0f;
+                }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                dz[k] = h1[k] > 0.0f ? gs[k] : 0.0f;
                 db1[k] += dz[k];
             }
             if (cg == 0) {

@@ -154,3 +154,21 @@ def test_host_batch_equals_device_ring_training(b):
         out.append((dqn.get_params(b.RPL_ONLINE), dqn.get_params(b.RPL_TARGET)))
         assert dqn.check() == b.RPL_OK
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+@pytest.mark.parametrize("ddqn", [False, True], ids=["dqn", "ddqn"])
+def test_host_batch_tcgen05_step(b, ddqn):
+    # the CPU-gathered batch into the large-batch tcgen05 step (tc_big.cuh T0 reads the copied
+    # rows): bit-exact batch, 1e-5 results at B = 700 (ragged) and 1024
+    cfg = b.DQNConfig(state_dim=27, n_actions=8, dueling=True, hidden=(128,), stream=512,
+                      double_dqn=ddqn, gamma=0.99, lr=1e-3, huber_kappa=1.0, sync_period=2,
+                      max_batch=1024)
+    rp = b.Replay(3000, 27, seed=7, ring_memory="host_batch")
+    orc = oracle.Ring(3000, 27)
+    e = experiences(3000, seed=15)
+    rp.add(**e)
+    orc.add(**e)
+    dqn = b.DQN(cfg, init_params(27, 8, (128,), True, 512, seed=16))
+    for B in (700, 1024, 700):
+        assert step_and_compare(b, cfg, dqn, rp, orc, B, seed=7) is not None
+    assert dqn.check() == b.RPL_OK and rp.check() == b.RPL_OK
