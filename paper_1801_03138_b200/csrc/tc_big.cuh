@@ -55,7 +55,13 @@ constexpr int N0 = 128;       // layer-0 units (the M of the dW0 MMA, the K of l
 constexpr int JW = 8;         // head outputs one unit tile contributes to (dueling A stream: |A|)
 constexpr int JPMAX = 16;     // padded head width of dHead rows (J <= 16)
 constexpr int T0_ROWS = 16, T0_T = 256;   // T0: 16 half-warps, one sampled row each
-constexpr int T1_EPW = 8;     // T1 epilogue warps: 2 per TMEM lane quarter (16 measured slower)
+#ifndef RPL_T1_EPW
+#define RPL_T1_EPW 8
+#endif
+#ifndef RPL_T1_SLOTS
+#define RPL_T1_SLOTS 4
+#endif
+constexpr int T1_EPW = RPL_T1_EPW;   // T1 epilogue warps (a multiple of 4: per TMEM lane quarter)
 constexpr int T1_PSL = 1;                   // head partial slots per 128-unit tile (TD sums N1 / 128)
 constexpr int T1_CPW = 128 / (T1_EPW / 4);  // accumulator columns per epilogue thread
 constexpr int T1_HN = 16;                   // head MMA N: the tile's head outputs, padded (J <= 16)
@@ -64,7 +70,7 @@ constexpr int T1_HN = 16;                   // head MMA N: the tile's head outpu
 // (two bf16 per 32-bit column, even k in the low half) [320, 512)
 constexpr int T1_TM_DH = 256, T1_TM_AH = 320;
 constexpr int T1_T = (T1_EPW + 2) * 32;     // + producer warp, MMA warp
-constexpr int T1_SLOTS = 4;   // H0 ring slots (one 32-deep K quarter of a 128-row tile each)
+constexpr int T1_SLOTS = RPL_T1_SLOTS;   // H0 ring slots (one 32-deep K quarter of a 128-row tile each)
 constexpr int T1_SLOT = 3 * 128 * 32 * 2;   // bytes of one slot (three planes)
 constexpr int T3A_T = 256;
 constexpr int T3A_STAGE_A = 3 * 64 * 128 * 2;   // dZ1 chunk: 64 samples x 128 units, 3 planes
@@ -98,14 +104,7 @@ __device__ __forceinline__ void split8(const float (&x)[8], uint4 &h, uint4 &m, 
 {
     uint32_t hw[4], mw[4], lw[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        uint16_t h0, m0, l0, h1, m1, l1;
-        umma::split3_bf16(x[2 * i], h0, m0, l0);
-        umma::split3_bf16(x[2 * i + 1], h1, m1, l1);
-        hw[i] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-        mw[i] = (uint32_t)m0 | ((uint32_t)m1 << 16);
-        lw[i] = (uint32_t)l0 | ((uint32_t)l1 << 16);
-    }
+    for (int i = 0; i < 4; ++i) umma::split3_pack2(x[2 * i], x[2 * i + 1], hw[i], mw[i], lw[i]);
     h = make_uint4(hw[0], hw[1], hw[2], hw[3]);
     m = make_uint4(mw[0], mw[1], mw[2], mw[3]);
     l = make_uint4(lw[0], lw[1], lw[2], lw[3]);
@@ -249,14 +248,15 @@ __device__ __forceinline__ void stage_head(const FastArgs &p, const float *theta
 }
 
 struct T1Smem {
-    int oW1, oA, oWh, ob1, obar, total;
+    int oW1, oA, oWh, ob1, oH, obar, total;
     __host__ __device__ T1Smem(int)
     {
         oW1 = 0;                               // W1 tile: 3 planes x [128 units x 128]
         oA = oW1 + 3 * 128 * N0 * 2;           // H0 ring: T1_SLOTS x 3 planes x [128 x 32]
         oWh = oA + T1_SLOTS * T1_SLOT;         // the tile's head weights: 3 planes x [16 x 128] bf16
         ob1 = oWh + 3 * T1_HN * 128 * 2;       // b1 of the tile [128]
-        obar = (ob1 + 128 * 4 + 15) & ~15;     // 15 mbarriers + the TMEM base
+        oH = ob1 + 128 * 4;                    // H1 store staging: per epilogue warp [32 rows][20]
+        obar = (oH + T1_EPW * 32 * 20 * 4 + 15) & ~15;   // 15 mbarriers + the TMEM base
         total = obar + 16 * 8;
     }
 };
@@ -622,8 +622,9 @@ __global__ void __launch_bounds__(tcb::T1_T, 1) tcb_fwd_kernel(const __grid_cons
         // ---- epilogue (warps 0 .. T1_EPW-1): warp w reads TMEM lane quarter w % 4, columns
         // T1_CPW (w / 4) ...: bias, ReLU, H1 of the online net; H1's bf16 planes into tensor
         // memory for the head MMA; the previous tile's head sums out as partials
-        {   // the tile's head-weight image (rows j < J of head_w, zero where unit u does not feed
-            // j and for the padding rows): thread = (output j, 8 consecutive units)
+        if (tid < T1_HN * 16) {   // the tile's head-weight image (rows j < J of head_w, zero
+            // where unit u does not feed j and for the padding rows): thread = (output j, 8
+            // consecutive units)
             const int j = tid >> 4, ug = tid & 15;
             float w[8];
 #pragma unroll
@@ -675,23 +676,30 @@ __global__ void __launch_bounds__(tcb::T1_T, 1) tcb_fwd_kernel(const __grid_cons
 #pragma unroll
                 for (int i = 0; i < 16; ++i) h[i] = fmaxf(__uint_as_float(v[c][i]) + bb[i], 0.0f);
 #ifndef RPL_T1_NOH1   // (timing experiment only: results invalid without H1)
-                if (net == 0 && b < B) {
+                if (net == 0) {
 #else
-                if (net == 0 && b < 0) {
+                if (net < 0) {
 #endif
-                    float *ho = p.H1 + (int64_t)b * N1 + u0 + c0;
+                    // H1 of the online net (T3a's input): the warp's 32 rows x 16 columns go
+                    // through shared memory so every global store is a whole 64-byte row
+                    // segment (8 rows per instruction) instead of a 16-byte piece of 32 rows
+                    float *st = reinterpret_cast<float *>(smc + L.oH) + warp * (32 * 20);
 #pragma unroll
-                    for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4 *>(ho + i) = make_float4(h[i], h[i + 1], h[i + 2], h[i + 3]);
+                    for (int i = 0; i < 16; i += 4)
+                        *reinterpret_cast<float4 *>(st + lane * 20 + i) = make_float4(h[i], h[i + 1], h[i + 2], h[i + 3]);
+                    __syncwarp();
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int rr = 8 * i + (lane >> 2), c4 = lane & 3;
+                        const int bb2 = bt * 128 + 32 * quarter + rr;
+                        const float4 t = *reinterpret_cast<const float4 *>(st + rr * 20 + 4 * c4);
+                        if (bb2 < B) *reinterpret_cast<float4 *>(p.H1 + (int64_t)bb2 * N1 + u0 + c0 + 4 * c4) = t;
+                    }
+                    __syncwarp();
                 }
 #pragma unroll
-                for (int i = 0; i < 16; i += 2) {
-                    uint16_t a0, a1, a2, b0, b1, b2;
-                    umma::split3_bf16(h[i], a0, a1, a2);
-                    umma::split3_bf16(h[i + 1], b0, b1, b2);
-                    pk[0][8 * c + i / 2] = (uint32_t)a0 | ((uint32_t)b0 << 16);
-                    pk[1][8 * c + i / 2] = (uint32_t)a1 | ((uint32_t)b1 << 16);
-                    pk[2][8 * c + i / 2] = (uint32_t)a2 | ((uint32_t)b2 << 16);
-                }
+                for (int i = 0; i < 16; i += 2)
+                    umma::split3_pack2(h[i], h[i + 1], pk[0][8 * c + i / 2], pk[1][8 * c + i / 2], pk[2][8 * c + i / 2]);
             }
             // the previous tile's head MMAs have read the A planes and written D_head
             if (it >= 1) head_out(it - 1);
@@ -780,6 +788,9 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
     uint32_t *tslot = reinterpret_cast<uint32_t *>(bar + 5);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nut = N1 / 128, ut = blockIdx.x % nut, g = blockIdx.x / nut, G = gridDim.x / nut;
+    // RPL_TRACE: thread 0's cycle totals (kernel slot 5): 2 chunk start (stage free + barrier),
+    // 3 the four dZ1 passes, 4 the barrier after them, 5 waiting for the H0 chunk (MMA issue)
+    CtaTrace tr_(p.trace, 5);
     const int u0 = ut * 128, nch = p.Bp / 64;
     if (warp == 0) umma::tmem_alloc(tslot, 128);
     if (tid == 0) {
@@ -838,8 +849,11 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
     for (int c = g; c < nch; c += G, ++i) {
         const int s = i & 1;
         char *Ast = smc + L.oA + s * T3A_STAGE_A, *Bst = smc + L.oB + s * T3A_STAGE_B;
+        long long t0 = tr_.now();
         if (i >= 2) umma::mbar_wait(&mfree[s], (uint32_t)(((i >> 1) - 1) & 1));   // chunk i - 2's MMAs
         __syncthreads();
+        tr_.acc(2, t0);
+        t0 = tr_.now();
         umma::fence_after_sync();
         if (tid == 0) {
             umma::mbar_expect_tx(&full[s], T3A_STAGE_B);
@@ -886,15 +900,30 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
 #pragma unroll
                 for (int j = 0; j < JPMAX; ++j) bha[j] += dh[j];
             }
-            store8_smem(Ast, 64 * 128 * 2, (rr >> 3) * 2048 + cg * 128 + (rr & 7) * 16, dz);
-            // and straight into the global dZ1 image T3b reads (8 lanes write one 128-byte
-            // core matrix per plane)
-            store8(p.dz1img, p.dzpl, dzimg(64 * (int64_t)c + rr, u0 + 8 * cg, N1), dz);
+            // the stage's A image, and straight into the global dZ1 image T3b reads (8 lanes
+            // write one 128-byte core matrix per plane); one split for both
+            {
+                uint4 zh, zm, zl;
+                split8(dz, zh, zm, zl);
+                char *sa = Ast + (rr >> 3) * 2048 + cg * 128 + (rr & 7) * 16;
+                *reinterpret_cast<uint4 *>(sa) = zh;
+                *reinterpret_cast<uint4 *>(sa + 64 * 128 * 2) = zm;
+                *reinterpret_cast<uint4 *>(sa + 2 * 64 * 128 * 2) = zl;
+                uint16_t *g = p.dz1img + dzimg(64 * (int64_t)c + rr, u0 + 8 * cg, N1);
+                *reinterpret_cast<uint4 *>(g) = zh;
+                *reinterpret_cast<uint4 *>(g + p.dzpl) = zm;
+                *reinterpret_cast<uint4 *>(g + 2 * p.dzpl) = zl;
+            }
         }
+        tr_.acc(3, t0);
+        t0 = tr_.now();
         umma::fence_async_smem();
         __syncthreads();
+        tr_.acc(4, t0);
         if (tid == 0) {
+            long long t1 = tr_.now();
             tcb::wait(&full[s], (uint32_t)((i >> 1) & 1));
+            tr_.acc(5, t1);
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {
                 uint64_t ad[3], bd[3];

@@ -1253,14 +1253,7 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
                 const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
                 uint32_t pk[3][2];
 #pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                    uint16_t a0, a1, a2, b0, b1, b2;
-                    umma::split3_bf16(wv[2 * h2], a0, a1, a2);
-                    umma::split3_bf16(wv[2 * h2 + 1], b0, b1, b2);
-                    pk[0][h2] = (uint32_t)a0 | ((uint32_t)b0 << 16);
-                    pk[1][h2] = (uint32_t)a1 | ((uint32_t)b1 << 16);
-                    pk[2][h2] = (uint32_t)a2 | ((uint32_t)b2 << 16);
-                }
+                for (int h2 = 0; h2 < 2; ++h2) umma::split3_pack2(wv[2 * h2], wv[2 * h2 + 1], pk[0][h2], pk[1][h2], pk[2][h2]);
                 for (int net = 0; net < (do_sync ? 2 : 1); ++net) {
                     uint16_t *im = p.w1img + net * 3 * p.w1pl;
 #pragma unroll

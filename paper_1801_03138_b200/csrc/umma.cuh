@@ -157,6 +157,17 @@ __device__ __forceinline__ void split3_bf16(float x, uint16_t &hi, uint16_t &mid
     mid = __bfloat16_as_ushort(m);
     lo = __bfloat16_as_ushort(l);
 }
+// the same for two consecutive values, packed two per word (x0 in the low half): one paired
+// conversion (F2FP ... PACK_AB) per term instead of two
+__device__ __forceinline__ void split3_pack2(float x0, float x1, uint32_t &h, uint32_t &m, uint32_t &l)
+{
+    auto bits = [](__nv_bfloat162 v) { return *reinterpret_cast<uint32_t *>(&v); };
+    h = bits(__floats2bfloat162_rn(x0, x1));
+    const float r0 = x0 - __uint_as_float(h << 16), r1 = x1 - __uint_as_float(h & 0xffff0000u);
+    m = bits(__floats2bfloat162_rn(r0, r1));
+    const float q0 = r0 - __uint_as_float(m << 16), q1 = r1 - __uint_as_float(m & 0xffff0000u);
+    l = bits(__floats2bfloat162_rn(q0, q1));
+}
 
 }  // namespace umma
 }  // namespace rpl

@@ -153,14 +153,7 @@ __global__ void __launch_bounds__(256) wide_split8_kernel(const float *__restric
         const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
         uint32_t hw[4], mw[4], lw[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            uint16_t h0, m0, l0, h1, m1, l1;
-            umma::split3_bf16(x[2 * i], h0, m0, l0);
-            umma::split3_bf16(x[2 * i + 1], h1, m1, l1);
-            hw[i] = pack2(h0, h1);
-            mw[i] = pack2(m0, m1);
-            lw[i] = pack2(l0, l1);
-        }
+        for (int i = 0; i < 4; ++i) umma::split3_pack2(x[2 * i], x[2 * i + 1], hw[i], mw[i], lw[i]);
         const int64_t t = wd_tix_k(u, g << 3);   // 8 consecutive k of one row: 16 contiguous bytes
         *reinterpret_cast<uint4 *>(planes + t) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
         *reinterpret_cast<uint4 *>(planes + pe + t) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
@@ -604,14 +597,9 @@ __global__ void __launch_bounds__(WD_T, 1) wide_dw0_kernel(const __grid_constant
                     w.w -= p.lr * g.w;
                     *reinterpret_cast<float4 *>(p.online_w + wi) = w;
                     // the next step's forward operand: W0's bf16 planes, split once here
-                    uint16_t h[4], m[4], l[4];
-                    umma::split3_bf16(w.x, h[0], m[0], l[0]);
-                    umma::split3_bf16(w.y, h[1], m[1], l[1]);
-                    umma::split3_bf16(w.z, h[2], m[2], l[2]);
-                    umma::split3_bf16(w.w, h[3], m[3], l[3]);
-                    const uint2 ph = make_uint2(pack2(h[0], h[1]), pack2(h[2], h[3]));
-                    const uint2 pm = make_uint2(pack2(m[0], m[1]), pack2(m[2], m[3]));
-                    const uint2 pl = make_uint2(pack2(l[0], l[1]), pack2(l[2], l[3]));
+                    uint2 ph, pm, pl;
+                    umma::split3_pack2(w.x, w.y, ph.x, pm.x, pl.x);
+                    umma::split3_pack2(w.z, w.w, ph.y, pm.y, pl.y);
                     const int64_t tx = wd_tix_k(u, n0 + c);   // 4 inputs of one core-matrix row
                     *reinterpret_cast<uint2 *>(p.W0bf + tx) = ph;
                     if (p.nplanes > 1) *reinterpret_cast<uint2 *>(p.W0bf + pe + tx) = pm;

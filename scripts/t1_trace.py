@@ -28,7 +28,8 @@ def main():
     for _ in range(a.steps):
         dqn.train_step(rp, a.batch, loss)
     torch.cuda.synchronize()
-    tr = dqn.debug(b.RPL_DBG_TRACE, a.batch).astype(np.int64)[4]
+    trall = dqn.debug(b.RPL_DBG_TRACE, a.batch).astype(np.int64)
+    tr = trall[4]
     m = tr[:, 0] > 0
     dur = (tr[m, 1] - tr[m, 0]) / 1000.0
     print(f"T1 B={a.batch} ddqn={a.ddqn}: {m.sum()} CTAs, last-step CTA duration mean {dur.mean():.2f} max {dur.max():.2f} us")
@@ -37,6 +38,15 @@ def main():
     for w, nm in names.items():
         v = tr[m, w] / a.steps / 1965.0
         print(f"  {nm:30s} {v.mean():7.2f} us per step per CTA (max {v.max():7.2f})")
+    tr = trall[5]
+    m = tr[:, 0] > 0
+    if m.any():
+        dur = (tr[m, 1] - tr[m, 0]) / 1000.0
+        print(f"T3a: {m.sum()} CTAs, last-step CTA duration mean {dur.mean():.2f} max {dur.max():.2f} us")
+        for w, nm in {2: "chunk start (stage free + barrier)", 3: "dZ1 passes", 4: "barrier after passes",
+                      5: "MMA issue waits for H0 chunk"}.items():
+            v = tr[m, w] / a.steps / 1965.0
+            print(f"  {nm:34s} {v.mean():7.2f} us per step per CTA (max {v.max():7.2f})")
 
 
 if __name__ == "__main__":
