@@ -771,6 +771,7 @@ struct rpl_dqn {
     bool tc = false;                 // the fast path's K1 / K3 on tcgen05 (tc_fast.cuh)
     bool tcb = false;                // large batches: tc_big.cuh's step (B >= kTcbMinBatch)
     uint16_t *h0img = nullptr, *ximg = nullptr, *dz1img = nullptr, *w1img = nullptr;
+    float *w0t = nullptr;                  // tcb: [online, target] W0^T [D][N0]
     float *dheadp = nullptr;
     int64_t tcb_h0pl = 0, tcb_xpl = 0, tcb_dzpl = 0, tcb_w1pl = 0;
     float *part = nullptr, *dH0p = nullptr;
@@ -1256,6 +1257,7 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
         const int jp = (d->J + 3) & ~3;
         ok = dalloc(d, &d->h0img, (size_t)3 * (nets + 1) * d->tcb_h0pl) && dalloc(d, &d->ximg, (size_t)3 * d->tcb_xpl) &&
              dalloc(d, &d->dz1img, (size_t)3 * d->tcb_dzpl) && dalloc(d, &d->w1img, (size_t)6 * d->tcb_w1pl) &&
+             dalloc(d, &d->w0t, (size_t)2 * tcb::N0 * d->cfg.state_dim) &&
              dalloc(d, &d->dheadp, (size_t)Bpm * jp);
         // T3a partial gradients [G][gps]; T3b dW0 | db0 partials [NQ * tiles][w1] with
         // NQ * tiles <= max(sms, tiles)
@@ -1548,6 +1550,7 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
         p.ximg = d->ximg;
         p.dz1img = d->dz1img;
         p.w1img = d->w1img;
+        p.w0t = d->w0t;
         p.h0pl = d->tcb_h0pl;
         p.xpl = d->tcb_xpl;
         p.dzpl = d->tcb_dzpl;
@@ -1841,12 +1844,15 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
         }
         if (fp.tcb && d->w1img_stale) {   // after create / set_params / sync_target / a DP or small-batch update
             if (d->w1img_stale & 1) {
-                tcb_w1_split_kernel<<<d->sms, 256, 0, d->stream>>>(d->online + d->woff[1], d->w1img, d->tcb_w1pl, d->N[1]);
+                tcb_w1_split_kernel<<<d->sms, 256, 0, d->stream>>>(d->online + d->woff[1], d->w1img, d->tcb_w1pl, d->N[1],
+                                                                   d->online + d->woff[0], d->w0t, d->cfg.state_dim);
                 g_launches.fetch_add(1);
             }
             if (d->w1img_stale & 2) {
                 tcb_w1_split_kernel<<<d->sms, 256, 0, d->stream>>>(d->target + d->woff[1], d->w1img + 3 * d->tcb_w1pl,
-                                                                   d->tcb_w1pl, d->N[1]);
+                                                                   d->tcb_w1pl, d->N[1], d->target + d->woff[0],
+                                                                   d->w0t + (int64_t)tcb::N0 * d->cfg.state_dim,
+                                                                   d->cfg.state_dim);
                 g_launches.fetch_add(1);
             }
             e = cudaGetLastError();

@@ -298,27 +298,20 @@ __global__ void __launch_bounds__(tcb::T0_T) tcb_l0_kernel(const __grid_constant
     extern __shared__ __align__(16) float sm0[];
     const int D = p.D, B = p.B, tid = threadIdx.x, lane = tid & 31;
     constexpr int XS = 33;   // staged state pitch (>= D + 1, odd: conflict-free)
-    float *W0s = sm0;                      // [online | target] [N0][D]
+    float *W0s = sm0;                      // [online | target] W0^T [D][N0]
     float *b0s = W0s + 2 * N0 * D;         // [online | target] [N0]
     float *xs = b0s + 2 * N0;              // [T0_ROWS rows][s, s'][XS]
     __shared__ int32_t idxs[T0_ROWS], pjs[T0_ROWS], pjs2[T0_ROWS];
-    // (0) W0 / b0 of both nets into shared memory, asynchronously (N0 * D and N0 are multiples
-    // of 4 floats; the blob offsets of W0 and b0 are 16-byte aligned when w0 % 4 == 0)
-    const bool wvec = (p.w0 & 3) == 0 && (p.b0 & 3) == 0;
-    if (wvec) {
-        for (int c = tid; c < N0 * D / 4; c += T0_T) {
-            cp_async16(W0s + 4 * c, p.online + p.w0 + 4 * c);
-            cp_async16(W0s + N0 * D + 4 * c, p.target + p.w0 + 4 * c);
-        }
+    // (0) W0^T [D][N0] (kept by K4 / tcb_w1_split_kernel) and b0 of both nets into shared
+    // memory, asynchronously (N0 * D and N0 are multiples of 4 floats; b0's blob offset is
+    // 16-byte aligned when b0 % 4 == 0)
+    for (int c = tid; c < 2 * N0 * D / 4; c += T0_T) cp_async16(W0s + 4 * c, p.w0t + 4 * c);
+    if ((p.b0 & 3) == 0) {
         for (int c = tid; c < N0 / 4; c += T0_T) {
             cp_async16(b0s + 4 * c, p.online + p.b0 + 4 * c);
             cp_async16(b0s + N0 + 4 * c, p.target + p.b0 + 4 * c);
         }
     } else {
-        for (int e = tid; e < N0 * D; e += T0_T) {
-            W0s[e] = __ldg(p.online + p.w0 + e);
-            W0s[N0 * D + e] = __ldg(p.target + p.w0 + e);
-        }
         for (int e = tid; e < N0; e += T0_T) {
             b0s[e] = __ldg(p.online + p.b0 + e);
             b0s[N0 + e] = __ldg(p.target + p.b0 + e);
@@ -461,15 +454,18 @@ __global__ void __launch_bounds__(tcb::T0_T) tcb_l0_kernel(const __grid_constant
         const bool ok = b < B;
         for (int net = 0; net < p.nets; ++net) {
             const float *x = xs + (r * 2 + (net == 0 ? 0 : 1)) * XS;
-            const float *W = W0s + (net == 1 ? N0 * D : 0);
+            const float *W = W0s + (net == 1 ? N0 * D : 0) + k0;
             const float *bb = b0s + (net == 1 ? N0 : 0);
             float h[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) h[i] = bb[k0 + i];
             for (int dd = 0; dd < D; ++dd) {
                 const float xv = x[dd];
+                const float4 wa = *reinterpret_cast<const float4 *>(W + dd * N0);
+                const float4 wb = *reinterpret_cast<const float4 *>(W + dd * N0 + 4);
+                const float w[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
 #pragma unroll
-                for (int i = 0; i < 8; ++i) h[i] = fmaf(W[(k0 + i) * D + dd], xv, h[i]);
+                for (int i = 0; i < 8; ++i) h[i] = fmaf(w[i], xv, h[i]);
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i) h[i] = ok ? fmaxf(h[i], 0.0f) : 0.0f;
@@ -843,8 +839,10 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
             for (int j = 0; j < JPMAX; ++j) dh[j] = 0.0f;
         }
     };
-    float h1n[8], dhn[JPMAX];
+    // two passes of loads in flight: (h1n, dhn) for the next pass, (h1m, dhm) for the one after
+    float h1n[8], dhn[JPMAX], h1m[8], dhm[JPMAX];
     load_pass(g, 0, h1n, dhn);
+    load_pass(g, 1, h1m, dhm);
     int i = 0;
     for (int c = g; c < nch; c += G, ++i) {
         const int s = i & 1;
@@ -866,11 +864,17 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
             const int rr = 16 * ps + 8 * rh + r8;
             float h1[8], dh[JPMAX];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) h1[k] = h1n[k];
+            for (int k = 0; k < 8; ++k) {
+                h1[k] = h1n[k];
+                h1n[k] = h1m[k];
+            }
 #pragma unroll
-            for (int j = 0; j < JPMAX; ++j) dh[j] = dhn[j];
-            if (ps < 3) load_pass(c, ps + 1, h1n, dhn);
-            else load_pass(c + G, 0, h1n, dhn);
+            for (int j = 0; j < JPMAX; ++j) {
+                dh[j] = dhn[j];
+                dhn[j] = dhm[j];
+            }
+            if (ps < 2) load_pass(c, ps + 2, h1m, dhm);
+            else load_pass(c + G, ps - 2, h1m, dhm);
             // the tile's head outputs start at jlo (0 or 1, head_range)
             float dsel[JW];
 #pragma unroll
@@ -1160,9 +1164,15 @@ __global__ void __launch_bounds__(tcb::T3B_T, 1) tcb_dh0_kernel(const __grid_con
 // the bf16 image of W1 (online and target) from the fp32 weights: after create, set_params,
 // sync_target and any update that is not K4's
 __global__ void __launch_bounds__(256) tcb_w1_split_kernel(const float *__restrict__ w1, uint16_t *__restrict__ im,
-                                                           int64_t plane, int N1)
+                                                           int64_t plane, int N1, const float *__restrict__ w0,
+                                                           float *__restrict__ w0t, int D)
 {
     using namespace tcb;
+    // W0 transposed ([D][N0], T0's layer-0 operand)
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)N0 * D; e += (int64_t)gridDim.x * blockDim.x) {
+        const int u = (int)(e / D), dd = (int)(e - (int64_t)u * D);
+        w0t[(int64_t)dd * N0 + u] = w0[e];
+    }
     const int64_t n8 = (int64_t)N1 * N0 / 8;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n8; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t u = e / (N0 / 8);

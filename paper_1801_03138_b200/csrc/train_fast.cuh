@@ -108,6 +108,7 @@ struct FastArgs {
     uint16_t *ximg;      // [3][Bp * 32] [x | 1] of s
     uint16_t *dz1img;    // [3][Bp * N1] dZ1
     uint16_t *w1img;     // [online, target][3][N1 * 128] W1
+    float *w0t;          // [online, target][D][N0] W0 transposed (T0's operand; K4 keeps it)
     int64_t h0pl, xpl, dzpl, w1pl;   // plane strides (elements)
     float *dheadp;       // [B][jp] dHead
 };
@@ -1180,6 +1181,11 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
             const float w = p.online[i] - lr * t;
             p.online[i] = w;
             if (do_sync) p.target[i] = w;
+            if (p.w0t && i < (int64_t)p.N0 * p.D) {   // the large-batch path's W0^T for T0
+                const int u = (int)(i / p.D), dd = (int)(i - (int64_t)u * p.D);
+                p.w0t[(int64_t)dd * p.N0 + u] = w;
+                if (do_sync) p.w0t[(int64_t)(p.D + dd) * p.N0 + u] = w;
+            }
         }
     };
     w0_finish(i0 + lane);
