@@ -844,6 +844,7 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
     load_pass(g, 0, h1n, dhn);
     load_pass(g, 1, h1m, dhm);
     int i = 0;
+    tr_.mark(6);   // setup done (cycles since the CTA started; overwritten per step)
     for (int c = g; c < nch; c += G, ++i) {
         const int s = i & 1;
         char *Ast = smc + L.oA + s * T3A_STAGE_A, *Bst = smc + L.oB + s * T3A_STAGE_B;
@@ -942,6 +943,7 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
         }
     }
     if (tid == 0) umma::commit(mdone);
+    tr_.mark(7);   // chunk loop done
     // the tile's db1 / dW_head / db_head: sums over the 8 rows of a lane group (shuffles), then
     // over the two row halves (shared memory), in a fixed order
 #pragma unroll

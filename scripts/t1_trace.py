@@ -47,6 +47,9 @@ def main():
                       5: "MMA issue waits for H0 chunk"}.items():
             v = tr[m, w] / a.steps / 1965.0
             print(f"  {nm:34s} {v.mean():7.2f} us per step per CTA (max {v.max():7.2f})")
+        su, lo = tr[m, 6] / 1965.0, (tr[m, 7] - tr[m, 6]) / 1965.0
+        print(f"  last step: setup {su.mean():6.2f} us (max {su.max():6.2f}), chunk loop {lo.mean():6.2f} (max {lo.max():6.2f}),"
+              f" epilogue {(dur - su - lo).mean():6.2f} (max {(dur - su - lo).max():6.2f})")
 
 
 if __name__ == "__main__":
