@@ -779,16 +779,22 @@ struct rpl_dqn {
     int64_t *step_dev = nullptr;
     int32_t *sync_flag = nullptr;
     cudaStream_t cap_stream = nullptr;
+    cudaStream_t loss_stream = nullptr;    // the step's side branch (loss_out_kernel)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    struct PtypeSlot { uint64_t page; bool host; };
+    PtypeSlot ptype_cache[64] = {};        // loss destinations: memory type per 4 KB page (+1)
     struct GraphEntry {
         const rpl_replay *rp;
         int B;
         int apply;                  // 0: data-parallel step (SGD after the all-reduce)
+        int le;                     // FastArgs.loss_early: the graph has the loss side branch
         cudaGraph_t graph;          // kept alive: its nodes are updated in place
         cudaGraphExec_t exec;
         // nodes whose args change between replays: K1 and the distinct sampler (deferred
         // insert read-through, control block), K3 (the deferred insert's ring write), K4
         // (the loss destination)
         cudaGraphNode_t k1, ds, k3, k4;
+        cudaGraphNode_t kl;         // loss_out_kernel (the loss side branch), or null
         FastArgs args;              // the args those nodes currently hold
     };
     std::vector<GraphEntry> graphs;
@@ -1067,6 +1073,9 @@ extern "C" int dqn_destroy(rpl_dqn *d)
         cudaGraphDestroy(g.graph);
     }
     if (d->cap_stream) cudaStreamDestroy(d->cap_stream);
+    if (d->loss_stream) cudaStreamDestroy(d->loss_stream);
+    if (d->ev_fork) cudaEventDestroy(d->ev_fork);
+    if (d->ev_join) cudaEventDestroy(d->ev_join);
     for (void *p : d->allocs) cudaFree(p);
     delete d;
     if (prev >= 0) cudaSetDevice(prev);
@@ -1208,7 +1217,10 @@ extern "C" int dqn_create(const rpl_dqn_config *cfg, const float *init, rpl_dqn 
         if (d->tc) w0p = std::max<int64_t>(w0p, (int64_t)std::max(1, d->N[1] / 64) * ((Bm + 127) / 128));
         d->dh0p_elems = w0p * (d->woff[1]);
         ok = dalloc(d, &d->part, d->part_elems) && dalloc(d, &d->dH0p, d->dh0p_elems);
-        ok = ok && cudaStreamCreateWithFlags(&d->cap_stream, cudaStreamNonBlocking) == cudaSuccess;
+        ok = ok && cudaStreamCreateWithFlags(&d->cap_stream, cudaStreamNonBlocking) == cudaSuccess &&
+             cudaStreamCreateWithFlags(&d->loss_stream, cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming) == cudaSuccess;
         ok = ok && cudaFuncSetAttribute(fast_fwd_fn(d), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         fast_fwd_smem(d, ut)) == cudaSuccess;
         // clustered K1 (multicast weights; opt-in RPL_K1MC=1: 9.6 vs 7.9 us per K1 measured,
@@ -1461,6 +1473,26 @@ static void wide_l0_plan(rpl_dqn *d, int nets, int64_t D)
     d->wide_cs = 1;
 }
 
+// a loss destination in (pinned / mapped) host memory: the step writes it from a side branch
+// (loss_out_kernel) so the PCIe write overlaps K3 / K4; device memory keeps the write in K4 (the
+// branch's fork / join costs ~1 us of graph time that only a host write wins back)
+// (the memory type is looked up once per 4 KB page: cudaPointerGetAttributes costs several us
+// of host time per call; host-pinned and device allocations never share a page of the unified
+// address space)
+static bool loss_in_host_memory(rpl_dqn *d, const void *ptr)
+{
+    const uint64_t page = reinterpret_cast<uintptr_t>(ptr) >> 12;
+    auto &slot = d->ptype_cache[page % 64];
+    if (slot.page == page + 1) return slot.host;
+    cudaPointerAttributes a{};
+    bool host = false;
+    if (cudaPointerGetAttributes(&a, ptr) == cudaSuccess) host = a.type == cudaMemoryTypeHost;
+    else cudaGetLastError();   // unregistered pageable memory: not a valid kernel destination anyway
+    slot.page = page + 1;
+    slot.host = host;
+    return host;
+}
+
 static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int apply, FastArgs &p)
 {
     memset(&p, 0, sizeof p);
@@ -1573,6 +1605,10 @@ static void fill_fast(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int ap
         p.pend_done = q.done;
         p.pend_err = rp->err_dev;
     }
+    // the loss leaves from a side branch of the step (loss_out_kernel after K2), so its
+    // possibly-PCIe write overlaps K3 / K4 (not in data-parallel steps: there the exchanged
+    // mean is the loss)
+    p.loss_early = (loss_dev && apply && !p.tc && loss_in_host_memory(d, loss_dev)) ? 1 : 0;
 }
 
 // the four fast-path kernels, enqueued on `st`
@@ -1594,6 +1630,35 @@ static cudaError_t launch_pdl(K kernel, int grid, int block, size_t smem, cudaSt
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, p);
+}
+
+// the loss side branch of a step (FastArgs.loss_early): fork after K3, join before the step ends
+static cudaError_t fork_loss(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
+{
+    if (!p.loss_early) return cudaSuccess;
+    cudaError_t e = cudaEventRecord(d->ev_fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(d->loss_stream, d->ev_fork, 0);
+    if (e == cudaSuccess) {
+        // highest launch priority: the scheduler places its one CTA ahead of K3's pending ones
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(1);
+        lc.blockDim = dim3(256);
+        lc.stream = d->loss_stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributePriority;
+        at[0].val.priority = hi;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        e = cudaLaunchKernelEx(&lc, loss_out_kernel, p);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(d->ev_join, d->loss_stream);
+    return e;
+}
+static cudaError_t join_loss(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
+{
+    return p.loss_early ? cudaStreamWaitEvent(st, d->ev_join, 0) : cudaSuccess;
 }
 
 // the fast-path kernels, enqueued on `st`
@@ -1618,7 +1683,8 @@ static cudaError_t tc_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
     e = launch_pdl(tc_bwd_kernel, std::min(k3_tasks, d->sms), tc::T, tc::BwdSmem().total, st,
                    pdl || d->k3_pdl, p);
     if (e != cudaSuccess) return e;
-    return launch_pdl(fast_bwd0_sgd_kernel, d->sms, NT, 0, st, pdl || d->k4_pdl, p);
+    e = launch_pdl(fast_bwd0_sgd_kernel, d->sms, NT, 0, st, pdl || d->k4_pdl, p);
+    return e == cudaSuccess ? join_loss(d, p, st) : e;
 }
 
 // the large-batch step (tc_big.cuh), enqueued on `st`
@@ -1640,8 +1706,10 @@ static cudaError_t tcb_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
     e = launch_pdl(tcb_dw1_kernel, nut * p.nsb, tcb::T3A_T, tcb::T3aSmem(p.J).total, st, false, p);
     if (e != cudaSuccess) return e;
     e = launch_pdl(tcb_dh0_kernel, nbt * p.NS, tcb::T3B_T, tcb::T3bSmem().total, st, false, p);
+    if (e == cudaSuccess) e = fork_loss(d, p, st);
     if (e != cudaSuccess) return e;
-    return launch_pdl(fast_bwd0_sgd_kernel, d->sms, NT, 0, st, false, p);
+    e = launch_pdl(fast_bwd0_sgd_kernel, d->sms, NT, 0, st, false, p);
+    return e == cudaSuccess ? join_loss(d, p, st) : e;
 }
 
 static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
@@ -1678,8 +1746,13 @@ static cudaError_t fast_enqueue(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
     // before K2's outputs); RPL_NO_K3PDL=1 serialises it
     e = launch_pdl(fast_bwd1_kernel, std::min(n_w + n_h + n_hd, 2 * d->sms), F_NT3,
                    K3_SMEM_FLOATS * sizeof(float), st, pdl || d->k3_pdl, p);
+    // the loss branch forks after K3: its PCIe write then runs beside K4, which reads no host
+    // memory (beside K3 it would hold up K3's zero-copy reads of a host-sourced insert: PCIe
+    // reads do not pass posted writes)
+    if (e == cudaSuccess) e = fork_loss(d, p, st);
     if (e != cudaSuccess) return e;
-    return launch_pdl(fast_bwd0_sgd_kernel, d->sms, NT, 0, st, pdl || d->k4_pdl, p);
+    e = launch_pdl(fast_bwd0_sgd_kernel, d->sms, NT, 0, st, pdl || d->k4_pdl, p);
+    return e == cudaSuccess ? join_loss(d, p, st) : e;
 }
 
 static int grid_for(const rpl_dqn *d, const TrainArgs &p)
@@ -1702,6 +1775,7 @@ static int grid_for(const rpl_dqn *d, const TrainArgs &p)
 static void wide_fast_args(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int apply, FastArgs &fp)
 {
     fill_fast(d, rp, B, loss_dev, apply, fp);
+    fp.loss_early = 0;        // the byte-state step ends with wide_dw0_kernel: K4's write overlaps it
     fp.D = 0;                 // K1 neither gathers nor computes layer 0
     fp.distinct = 0;          // the batch is sampled by the byte gather
     fp.h0_in = d->H[0];       // [nets][B][N0] (the debug export's layer-0 activations)
@@ -1870,11 +1944,11 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             rpl_dqn::GraphEntry *ge = nullptr;
             const int apply = dp ? 0 : 1;
             for (auto &g : d->graphs)
-                if (g.rp == rp && g.B == batch && g.apply == apply) ge = &g;
+                if (g.rp == rp && g.B == batch && g.apply == apply && g.le == fp.loss_early) ge = &g;
             if (!ge) {
                 cudaGraph_t graph = nullptr;
                 cudaGraphExec_t exec = nullptr;
-                cudaGraphNode_t k1 = nullptr, ds = nullptr, k3 = nullptr, k4 = nullptr;
+                cudaGraphNode_t k1 = nullptr, ds = nullptr, k3 = nullptr, k4 = nullptr, kl = nullptr;
                 e = cudaStreamBeginCapture(d->cap_stream, cudaStreamCaptureModeThreadLocal);
                 if (e == cudaSuccess) {
                     cudaError_t e2 = fast_enqueue(d, fp, d->cap_stream);
@@ -1898,6 +1972,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                             if (kp.func == (void *)distinct_fast_kernel) ds = nodes[i];
                             if (kp.func == (void *)fast_bwd1_kernel || kp.func == (void *)tc_bwd_kernel) k3 = nodes[i];
                             if (kp.func == (void *)fast_bwd0_sgd_kernel) k4 = nodes[i];
+                            if (kp.func == (void *)loss_out_kernel) kl = nodes[i];
                             if (kp.func == (void *)tcb_l0_kernel) k1 = k3 = nodes[i];   // T0 also writes the insert
                         }
                     }
@@ -1910,7 +1985,8 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                         cudaGraphDestroy(d->graphs.front().graph);
                         d->graphs.erase(d->graphs.begin());
                     }
-                    d->graphs.push_back({rp, batch, apply, graph, exec, k1, ds, k3, k4, fp});
+                    d->graphs.push_back({rp, batch, apply, fp.loss_early, graph, exec, k1, ds, k3, k4,
+                                         fp.loss_early ? kl : nullptr, fp});
                     ge = &d->graphs.back();
                 } else if (graph) {
                     cudaGraphDestroy(graph);
@@ -1950,7 +2026,10 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                         update(ge->ds);
                         update(ge->k3);
                     }
-                    if (loss_changed) update(ge->k4);
+                    if (loss_changed) {
+                        update(ge->k4);
+                        update(ge->kl);   // the loss side branch (null without it)
+                    }
                 }
                 if (e == cudaSuccess) ge->args = fp;
             }
@@ -1967,7 +2046,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             if (prev >= 0) cudaSetDevice(prev);
             return cuda_fail(e, "fast train step");
         }
-        g_launches.fetch_add((fp.distinct ? 1 : 0) + (fp.tcb ? 6 : 4));
+        g_launches.fetch_add((fp.distinct ? 1 : 0) + (fp.tcb ? 6 : 4) + (fp.loss_early ? 1 : 0));
     } else {
         d->w1img_stale = 3;   // the generic kernels update W1 without the tcb image
         TrainArgs p;

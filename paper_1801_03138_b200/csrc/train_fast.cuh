@@ -94,6 +94,7 @@ struct FastArgs {
     float *dZ0;          // [B][N0] dZ0 materialised by K4 for wide_dw0_kernel
     uint16_t *dZ0bf;     // its bf16 hi / mid / lo planes [3][B][N0]
     int event_advanced;  // 1: the step's sampling kernel advanced rctrl[0] already
+    int loss_early;      // 1: loss_out_kernel (a side branch after K2) writes *loss_out, K4 does not
     uint32_t *err;
     unsigned long long *trace;   // optional per-CTA [kernel][cta][start, end] %globaltimer (ns)
     int prec;            // rpl_dqn_config.precision (split_p / mma_3xtf32, mma_tf32.cuh)
@@ -883,6 +884,22 @@ constexpr int K3_GEMM_FLOATS = MM_FLOATS;
 constexpr int K3_DH_FLOATS = K3_GEMM_FLOATS + BM * (K3N + 4) + BM * 36 + BM * K3N;
 constexpr int K3_SMEM_FLOATS = K3_DH_FLOATS > K3_HD_FLOATS ? K3_DH_FLOATS : K3_HD_FLOATS;
 
+// the batch-mean loss exactly as K4 forms it (NT = 256 threads: thread t sums samples t, t + 256,
+// ... in order, warp sums, the 8 warp sums in warp order, / B): every thread of the CTA calls it
+__device__ __forceinline__ float block_batch_loss(const FastArgs &p, float *red8)
+{
+    const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+    float ls = 0.0f;
+    for (int b = tid; b < p.B; b += 256) ls += __ldcg(p.loss_part + b);
+    ls = warp_sum(ls);
+    if (lane == 0) red8[wq] = ls;
+    __syncthreads();
+    float lsum = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) lsum += red8[w];
+    return lsum / (float)p.B;
+}
+
 __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant__ FastArgs p)
 {
     // K3 is launched programmatically after K2: every operand K1 (or an earlier step) wrote
@@ -1094,6 +1111,16 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
     write_pending();
 }
 
+// the step's loss into the caller's slot (possibly pinned host memory) from a one-CTA kernel on
+// a side branch of the step graph that forks after K3 and joins after K4: the PCIe write and
+// its completion overlap K4 instead of delaying the end of the step's last kernel
+__global__ void __launch_bounds__(256) loss_out_kernel(const __grid_constant__ FastArgs p)
+{
+    __shared__ float red8[8];
+    const float loss = block_batch_loss(p, red8);
+    if (threadIdx.x == 0) *p.loss_out = loss;
+}
+
 // ------------------------------------------------------------------------------------------
 // K4: layer-0 backward + SGD of every parameter + target sync + counters
 // ------------------------------------------------------------------------------------------
@@ -1167,7 +1194,7 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
     // then completes while the SGD below runs instead of at the kernel's end
     if (blockIdx.x == 0 && tid == 0) {
         p.grad[p.P] = loss;
-        if (p.loss_out) *p.loss_out = loss;
+        if (p.loss_out && !p.loss_early) *p.loss_out = loss;
     }
     const float lr = p.lr;
     trace_.mark(2);
@@ -1182,7 +1209,7 @@ __global__ void __launch_bounds__(NT) fast_bwd0_sgd_kernel(const __grid_constant
             p.online[i] = w;
             if (do_sync) p.target[i] = w;
             if (p.w0t && i < (int64_t)p.N0 * p.D) {   // the large-batch path's W0^T for T0
-                const int u = (int)(i / p.D), dd = (int)(i - (int64_t)u * p.D);
+                const int ii = (int)i, u = ii / p.D, dd = ii - u * p.D;   // (W0 indices fit in 32 bits)
                 p.w0t[(int64_t)dd * p.N0 + u] = w;
                 if (do_sync) p.w0t[(int64_t)(p.D + dd) * p.N0 + u] = w;
             }

@@ -1,0 +1,6 @@
+#!/bin/bash
+set -u
+OUT=gpurun_out; mkdir -p $OUT
+timeout 1200 python -m pytest tests/test_gpu_train.py tests/test_gpu_tcb.py tests/test_gpu_ring_host.py tests/test_gpu_update_size.py tests/test_gpu_distinct.py tests/test_gpu_dp_peer.py tests/test_gpu_nccl.py -x -q > $OUT/pytest20.txt 2>&1; echo "pytest rc=$?"; tail -3 $OUT/pytest20.txt
+timeout 600 python bench.py --no-c5 --no-gather --no-cpu-baseline > $OUT/bench20.json 2> $OUT/bench20.err; echo "bench rc=$?"
+timeout 600 python bench.py --no-c5 --no-gather --no-cpu-baseline --batch 4096 --ddqn --steps 1000 > $OUT/bench20_4096.json 2> $OUT/bench20_4096.err; echo "bench rc=$?"

@@ -289,3 +289,31 @@ def test_deferred_device_insert_corrupt_done(b):
     assert rp.check() == b.RPL_ECORRUPT
     g = rp.gather(torch.tensor([48, 49], dtype=torch.int32, device="cuda"))
     assert g["done"].cpu().numpy().tolist() == [1, int(e["done"][1])]
+
+
+@pytest.mark.parametrize("batch", [128, 640])
+def test_loss_destination_device_and_pinned_host(b, batch):
+    # a pinned-host loss destination takes the step graph with the loss side branch
+    # (loss_out_kernel), a device one the graph whose K4 writes it: alternating the two on one
+    # learner must give, step for step, the loss of a learner that always writes to the device
+    import torch
+    cfg = _cfg(b, double_dqn=True, sync_period=3, max_batch=batch)
+    p0 = _params(cfg, seed=23)
+    e = experiences(3000, seed=24)
+    losses = []
+    for alternate in (False, True):
+        rp = b.Replay(3000, 27, seed=25)
+        rp.add(**e)
+        dqn = b.DQN(cfg, p0)
+        dev = torch.zeros(1, device="cuda")
+        host = torch.zeros(8, dtype=torch.float32, pin_memory=True)
+        out = []
+        for i in range(8):
+            dst = host[i:i + 1] if (alternate and i % 2 == 1) else dev
+            assert dqn.train_step(rp, batch, dst) == b.RPL_OK
+            torch.cuda.synchronize()
+            out.append(float(dst.cpu()[0]) if dst is dev else float(dst[0]))
+        assert dqn.check() == b.RPL_OK
+        losses.append(out)
+    assert losses[0] == losses[1]
+    assert all(np.isfinite(losses[0])) and all(v > 0 for v in losses[0])
