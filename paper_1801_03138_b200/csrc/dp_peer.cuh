@@ -36,12 +36,17 @@ struct DPArgs {
     float *online[DP_MAXR], *target[DP_MAXR], *gmean[DP_MAXR];   // per local rank
     const int32_t *sync_flag[DP_MAXR];
     uint32_t *err[DP_MAXR];
+    float *loss_out[DP_MAXR];            // the mean loss for the caller (or null), per local rank
 };
 
-// exchange buffer: [2][P + 1] gradient slots, [P + 1] mean (reduce-scatter variant), then a
+// exchange buffer: [2][S] gradient slots, [S] mean (reduce-scatter variant; S = P + 1 rounded to
+// 16 bytes: dp_slot_stride), then a
 // 256-byte flag area: flag (u64) at +0, broken (u32) at +64, flag2 (u64) at +128, a block
 // counter (u32) at +192
-__host__ __device__ inline size_t dp_flag_offset(int64_t P) { return ((size_t)3 * (P + 1) * sizeof(float) + 255) / 256 * 256; }
+// slot stride: P + 1 words rounded up to 16 bytes, so a step can write its gradient straight
+// into its slot with the same vector stores it uses for the learner's own gradient buffer
+__host__ __device__ inline int64_t dp_slot_stride(int64_t P) { return (P + 1 + 3) & ~(int64_t)3; }
+__host__ __device__ inline size_t dp_flag_offset(int64_t P) { return ((size_t)3 * dp_slot_stride(P) * sizeof(float) + 255) / 256 * 256; }
 __host__ __device__ inline size_t dp_xbuf_bytes(int64_t P) { return dp_flag_offset(P) + 256; }
 __host__ __device__ inline unsigned long long *dp_flag_of(const float *xbuf, int64_t P)
 {
@@ -118,7 +123,7 @@ __global__ void __launch_bounds__(256) dp_peer_rs_sgd_kernel(const __grid_consta
     const int rl = blockIdx.x / bpr, bi = blockIdx.x % bpr;
     if (rl >= a.nloc) return;
     const int rank = a.rank0 + rl;
-    const int64_t slot = (int64_t)(a.t & 1ull) * (a.P + 1), n = a.P + 1;
+    const int64_t n = a.P + 1, ss = dp_slot_stride(a.P), slot = (int64_t)(a.t & 1ull) * ss;
     __shared__ int timed_out;
     if (bi == 0 && threadIdx.x == 0 && !dp_is_broken(a.flag[rank])) {   // a broken rank stops publishing
         __threadfence_system();
@@ -134,7 +139,7 @@ __global__ void __launch_bounds__(256) dp_peer_rs_sgd_kernel(const __grid_consta
         float g = 0.0f;
         for (int q = 0; q < a.world; ++q) g += __ldcv(a.xbuf[q] + slot + i);
         g = g / (float)a.world;
-        for (int q = 0; q < a.world; ++q) const_cast<float *>(a.xbuf[q])[2 * n + i] = g;
+        for (int q = 0; q < a.world; ++q) const_cast<float *>(a.xbuf[q])[2 * ss + i] = g;
     }
     __threadfence_system();
     __syncthreads();
@@ -150,7 +155,7 @@ __global__ void __launch_bounds__(256) dp_peer_rs_sgd_kernel(const __grid_consta
     __syncthreads();
     if (timed_out) return;
     __threadfence();
-    const float *mean = a.xbuf[rank] + 2 * n;
+    const float *mean = a.xbuf[rank] + 2 * ss;
     const float loss = __ldcv(mean + a.P);
     const bool ok = isfinite(loss);
     const int do_sync = *a.sync_flag[rl];
@@ -166,6 +171,7 @@ __global__ void __launch_bounds__(256) dp_peer_rs_sgd_kernel(const __grid_consta
     }
     if (bi == 0 && threadIdx.x == 0) {
         gm[a.P] = loss;
+        if (a.loss_out[rl]) *a.loss_out[rl] = loss;
         if (!ok) atomicOr(a.err[rl], ERRBIT_NUMERIC);
     }
 }
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(256) dp_peer_sgd_kernel(const __grid_constant_
     const int rl = blockIdx.x / bpr, bi = blockIdx.x % bpr;
     if (rl >= a.nloc) return;
     const int rank = a.rank0 + rl;
-    const int64_t slot = (int64_t)(a.t & 1ull) * (a.P + 1);
+    const int64_t slot = (int64_t)(a.t & 1ull) * dp_slot_stride(a.P);
     // (1) this rank's step-t gradient is complete (written before this kernel): publish it
     if (bi == 0 && threadIdx.x == 0 && !dp_is_broken(a.flag[rank])) {   // a broken rank stops publishing
         __threadfence_system();
@@ -212,6 +218,7 @@ __global__ void __launch_bounds__(256) dp_peer_sgd_kernel(const __grid_constant_
     }
     if (bi == 0 && threadIdx.x == 0) {
         gm[a.P] = loss;
+        if (a.loss_out[rl]) *a.loss_out[rl] = loss;
         if (!ok) atomicOr(a.err[rl], ERRBIT_NUMERIC);
     }
 }

@@ -677,11 +677,12 @@ __global__ void __launch_bounds__(NT, 1) train_step_kernel(const __grid_constant
 // SGD after an NCCL all-reduce (world > 1): grad[P] holds the rank-averaged loss
 __global__ void __launch_bounds__(256) sgd_kernel(float *online, float *target, const float *grad,
                                                   int64_t P, float lr, const int32_t *sync_flag,
-                                                  uint32_t *err)
+                                                  uint32_t *err, float *loss_out)
 {
     const int do_sync = *sync_flag;
     const float loss = grad[P];
     const bool ok = isfinite(loss);
+    if (loss_out && blockIdx.x == 0 && threadIdx.x == 0) *loss_out = loss;   // the ranks' mean loss
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
          i += (int64_t)gridDim.x * blockDim.x) {
         if (ok) {
@@ -795,6 +796,10 @@ struct rpl_dqn {
         // (the loss destination)
         cudaGraphNode_t k1, ds, k3, k4;
         cudaGraphNode_t kl;         // loss_out_kernel (the loss side branch), or null
+        cudaGraphNode_t ksgd;       // NCCL data parallelism: the captured SGD after the all-reduce
+        float *sgd_loss;            // ... and the loss destination its node holds
+        int par;                    // peer-memory data parallelism: the exchange slot (step parity), else -1
+        cudaGraphNode_t kdp;        // ... and the captured exchange kernel (its DPArgs change every step)
         FastArgs args;              // the args those nodes currently hold
     };
     std::vector<GraphEntry> graphs;
@@ -1863,6 +1868,50 @@ static cudaError_t wide_graph_step(rpl_dqn *d, rpl_replay *rp, int B, float *los
     return e;
 }
 
+// the exchange kernel's arguments for exchange step tx (dp_peer.cuh)
+static void fill_dp(const rpl_dqn *d, int64_t tx, float *loss_out, DPArgs &a)
+{
+    a = DPArgs{};
+    a.nloc = 1;
+    a.world = d->world;
+    a.rank0 = d->rank;
+    a.P = d->P;
+    a.t = (unsigned long long)tx;
+    a.lr = d->cfg.lr;
+    for (int q = 0; q < d->world; ++q) {
+        a.xbuf[q] = d->peer_xbuf[q];
+        a.flag[q] = dp_flag_of(d->peer_xbuf[q], d->P);
+    }
+    a.online[0] = d->online;
+    a.target[0] = d->target;
+    a.gmean[0] = d->grad;
+    a.sync_flag[0] = d->sync_flag;
+    a.err[0] = d->err;
+    a.loss_out[0] = loss_out;
+}
+static cudaError_t launch_dp(const rpl_dqn *d, const DPArgs &a, cudaStream_t st)
+{
+    if (dp_use_rs(d->P, d->world)) {   // large gradients or >= 4 ranks: the reduce-scatter variant
+        void *args[] = {const_cast<DPArgs *>(&a)};
+        return cudaLaunchCooperativeKernel((const void *)dp_peer_rs_sgd_kernel, dim3(d->sms), dim3(256), args, 0, st);
+    }
+    dp_peer_sgd_kernel<<<(unsigned)d->sms, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+// cached step graphs that end in a data-parallel exchange: rebuilt after an attach / detach
+static void drop_dp_graphs(rpl_dqn *d)
+{
+    for (size_t i = 0; i < d->graphs.size();) {
+        if (d->graphs[i].apply == 0) {
+            cudaGraphExecDestroy(d->graphs[i].exec);
+            cudaGraphDestroy(d->graphs[i].graph);
+            d->graphs.erase(d->graphs.begin() + i);
+        } else {
+            ++i;
+        }
+    }
+}
+
 extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *loss_dev)
 {
     if (!d || !rp || batch < 1 || batch > d->cfg.max_batch || rp->ring.D != d->cfg.state_dim ||
@@ -1886,6 +1935,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
     // data parallel: per-step gradient mean (dp), or local SGD + periodic parameter mean (avg)
     const bool avg = d->comm != nullptr && d->cfg.avg_period > 0;
     const bool dp = (d->comm != nullptr || d->p2p) && !avg;
+    bool dp_graphed = false;   // the NCCL all-reduce + SGD captured in the fast step's graph
     cudaError_t e = cudaSuccess;
     // a deferred insert is consumed by the fast path's K1 on the shared stream; otherwise it
     // is written now by the insert kernel
@@ -1943,15 +1993,46 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
         if (d->use_graphs) {
             rpl_dqn::GraphEntry *ge = nullptr;
             const int apply = dp ? 0 : 1;
+            // NCCL data parallelism: the all-reduce (mean of gradient + loss word) and the SGD
+            // after it are captured into the same graph -- one launch per step, the loss written
+            // by the SGD kernel
+            const bool nccl_tail = dp && d->comm && !d->p2p;
+            float *sgd_loss = loss_dev ? loss_dev : d->loss_dev;
+            // peer-memory data parallelism: the step writes its gradient straight into the
+            // exchange slot of its parity (one graph per parity) and the exchange kernel is
+            // captured after K4 (its DPArgs -- step number, loss destination -- set per step)
+            const bool peer_tail = dp && d->p2p;
+            const int64_t tx = t - d->dp_base;
+            const int par = peer_tail ? (int)(tx & 1) : -1;
+            if (peer_tail) {
+                if (fp.gpart == fp.grad) fp.gpart = d->xbuf + (int64_t)par * dp_slot_stride(d->P);   // one batch split: K3 writes the gradient itself
+                fp.grad = d->xbuf + (int64_t)par * dp_slot_stride(d->P);
+            }
+            DPArgs dpa;
+            if (peer_tail) fill_dp(d, tx, loss_dev, dpa);
             for (auto &g : d->graphs)
-                if (g.rp == rp && g.B == batch && g.apply == apply && g.le == fp.loss_early) ge = &g;
+                if (g.rp == rp && g.B == batch && g.apply == apply && g.le == fp.loss_early && g.par == par) ge = &g;
             if (!ge) {
                 cudaGraph_t graph = nullptr;
                 cudaGraphExec_t exec = nullptr;
-                cudaGraphNode_t k1 = nullptr, ds = nullptr, k3 = nullptr, k4 = nullptr, kl = nullptr;
+                cudaGraphNode_t k1 = nullptr, ds = nullptr, k3 = nullptr, k4 = nullptr, kl = nullptr, ksgd = nullptr,
+                                kdp = nullptr;
                 e = cudaStreamBeginCapture(d->cap_stream, cudaStreamCaptureModeThreadLocal);
                 if (e == cudaSuccess) {
                     cudaError_t e2 = fast_enqueue(d, fp, d->cap_stream);
+                    if (e2 == cudaSuccess && nccl_tail) {
+                        const int nr = g_nccl.allreduce(d->grad, d->grad, (size_t)d->P + 1, kNcclFloat, kNcclAvg,
+                                                        d->comm, d->cap_stream);
+                        if (nr != 0) {
+                            set_error("ncclAllReduce (graph capture) failed: %s", g_nccl.errstr ? g_nccl.errstr(nr) : "?");
+                            e2 = cudaErrorUnknown;
+                        } else {
+                            sgd_kernel<<<(unsigned)d->sms, 256, 0, d->cap_stream>>>(d->online, d->target, d->grad, d->P,
+                                                                                   d->cfg.lr, d->sync_flag, d->err, sgd_loss);
+                            e2 = cudaGetLastError();
+                        }
+                    }
+                    if (e2 == cudaSuccess && peer_tail) e2 = launch_dp(d, dpa, d->cap_stream);
                     e = cudaStreamEndCapture(d->cap_stream, &graph);
                     if (e2 != cudaSuccess) e = e2;
                 }
@@ -1973,10 +2054,18 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                             if (kp.func == (void *)fast_bwd1_kernel || kp.func == (void *)tc_bwd_kernel) k3 = nodes[i];
                             if (kp.func == (void *)fast_bwd0_sgd_kernel) k4 = nodes[i];
                             if (kp.func == (void *)loss_out_kernel) kl = nodes[i];
+                            if (kp.func == (void *)sgd_kernel) ksgd = nodes[i];
+                            if (kp.func == (void *)dp_peer_sgd_kernel || kp.func == (void *)dp_peer_rs_sgd_kernel)
+                                kdp = nodes[i];
                             if (kp.func == (void *)tcb_l0_kernel) k1 = k3 = nodes[i];   // T0 also writes the insert
                         }
                     }
-                    if (e == cudaSuccess && (!k1 || !k3 || !k4)) e = cudaErrorInvalidValue;
+                    // NCCL's captured kernel nodes (a foreign module) fail the params query with
+                    // cudaErrorInvalidDeviceFunction: a non-sticky error, cleared here so the next
+                    // launch check does not report it
+                    cudaGetLastError();
+                    if (e == cudaSuccess && (!k1 || !k3 || !k4 || (nccl_tail && !ksgd) || (peer_tail && !kdp)))
+                        e = cudaErrorInvalidValue;
                 }
                 if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
                 if (e == cudaSuccess) {
@@ -1986,7 +2075,8 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                         d->graphs.erase(d->graphs.begin());
                     }
                     d->graphs.push_back({rp, batch, apply, fp.loss_early, graph, exec, k1, ds, k3, k4,
-                                         fp.loss_early ? kl : nullptr, fp});
+                                         fp.loss_early ? kl : nullptr, nccl_tail ? ksgd : nullptr, sgd_loss, par,
+                                         peer_tail ? kdp : nullptr, fp});
                     ge = &d->graphs.back();
                 } else if (graph) {
                     cudaGraphDestroy(graph);
@@ -2009,6 +2099,14 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                     if (!nd || e != cudaSuccess) return;
                     cudaKernelNodeParams kp = {};
                     e = cudaGraphKernelNodeGetParams(nd, &kp);
+                    if (e == cudaSuccess && (kp.func == (void *)sgd_kernel || kp.func == (void *)dp_peer_sgd_kernel ||
+                                             kp.func == (void *)dp_peer_rs_sgd_kernel))
+                        return;   // not a FastArgs kernel
+                    if (e == cudaErrorInvalidDeviceFunction) {   // a foreign (NCCL) kernel node: not ours
+                        cudaGetLastError();
+                        e = cudaSuccess;
+                        return;
+                    }
                     kp.kernelParams = args;
                     kp.extra = nullptr;
                     if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(ge->exec, nd, &kp);
@@ -2033,7 +2131,35 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                 }
                 if (e == cudaSuccess) ge->args = fp;
             }
+            if (e == cudaSuccess && ge && ge->ksgd && ge->sgd_loss != sgd_loss) {
+                // the SGD node's loss destination (its other arguments are fixed)
+                void *sargs[] = {&d->online, &d->target, &d->grad, &d->P, &d->cfg.lr, &d->sync_flag, &d->err,
+                                 &sgd_loss};
+                cudaKernelNodeParams kp = {};
+                e = cudaGraphKernelNodeGetParams(ge->ksgd, &kp);
+                kp.kernelParams = sargs;
+                kp.extra = nullptr;
+                if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(ge->exec, ge->ksgd, &kp);
+                if (e == cudaSuccess) ge->sgd_loss = sgd_loss;
+            }
+            if (e == cudaSuccess && ge && ge->kdp) {
+                // the exchange kernel's step number and loss destination
+                void *dargs[] = {&dpa};
+                cudaKernelNodeParams kp = {};
+                e = cudaGraphKernelNodeGetParams(ge->kdp, &kp);
+                kp.kernelParams = dargs;
+                kp.extra = nullptr;
+                if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(ge->exec, ge->kdp, &kp);
+            }
             if (e == cudaSuccess) e = cudaGraphLaunch(ge->exec, d->stream);
+            if (e == cudaSuccess && ge && ge->kdp) {
+                dp_graphed = true;
+                g_launches.fetch_add(1);   // the captured exchange kernel
+            }
+            if (e == cudaSuccess && ge && ge->ksgd) {
+                dp_graphed = true;
+                g_launches.fetch_add(1);   // the captured sgd_kernel (NCCL's own kernels not counted)
+            }
         } else {
             e = fast_enqueue(d, fp, d->stream);
         }
@@ -2174,44 +2300,27 @@ after_step:
         // exchange slot, then one kernel publishes it, waits for every rank's and updates
         // exchange step numbers count from the attach (every rank attached at the same point
         // of its stream, after the flag area was cleared), not from the learner's own steps
+        // (the byte-state and generic steps; the fast step captures all of this in its graph)
         const int64_t tx = t - d->dp_base;
-        float *mine = d->xbuf + (int64_t)(tx & 1) * (d->P + 1);
-        e = cudaMemcpyAsync(mine, d->grad, (size_t)(d->P + 1) * sizeof(float), cudaMemcpyDeviceToDevice, d->stream);
-        DPArgs a{};
-        a.nloc = 1;
-        a.world = d->world;
-        a.rank0 = d->rank;
-        a.P = d->P;
-        a.t = (unsigned long long)tx;
-        a.lr = d->cfg.lr;
-        for (int q = 0; q < d->world; ++q) {
-            a.xbuf[q] = d->peer_xbuf[q];
-            a.flag[q] = dp_flag_of(d->peer_xbuf[q], d->P);
-        }
-        a.online[0] = d->online;
-        a.target[0] = d->target;
-        a.gmean[0] = d->grad;
-        a.sync_flag[0] = d->sync_flag;
-        a.err[0] = d->err;
-        if (e == cudaSuccess) {
-            if (dp_use_rs(d->P, d->world)) {   // large gradients or >= 4 ranks: the reduce-scatter variant
-                void *args[] = {&a};
-                e = cudaLaunchCooperativeKernel((const void *)dp_peer_rs_sgd_kernel, dim3(d->sms), dim3(256),
-                                                args, 0, d->stream);
-            } else {
-                dp_peer_sgd_kernel<<<(unsigned)d->sms, 256, 0, d->stream>>>(a);
-                e = cudaGetLastError();
+        float *mine = d->xbuf + (int64_t)(tx & 1) * dp_slot_stride(d->P);
+        if (!dp_graphed) {
+            e = cudaMemcpyAsync(mine, d->grad, (size_t)(d->P + 1) * sizeof(float), cudaMemcpyDeviceToDevice, d->stream);
+            DPArgs a;
+            fill_dp(d, tx, loss_dev, a);
+            if (e == cudaSuccess) e = launch_dp(d, a, d->stream);
+            if (e != cudaSuccess) {
+                if (prev >= 0) cudaSetDevice(prev);
+                return cuda_fail(e, "dp_peer_sgd_kernel");
             }
+            g_launches.fetch_add(1);
         }
-        if (e != cudaSuccess) {
-            if (prev >= 0) cudaSetDevice(prev);
-            return cuda_fail(e, "dp_peer_sgd_kernel");
-        }
-        g_launches.fetch_add(1);
         // the update rewrote the online W0 / W1 without their images (the target too on a sync step)
         d->w0bf_stale |= do_sync ? 3 : 1;
         d->w1img_stale |= do_sync ? 3 : 1;
-        if (loss_dev) cudaMemcpyAsync(loss_dev, d->grad + d->P, sizeof(float), cudaMemcpyDefault, d->stream);
+    } else if (dp && dp_graphed) {
+        // the all-reduce and the SGD after it ran inside the step's graph (nccl_tail)
+        d->w0bf_stale |= do_sync ? 3 : 1;
+        d->w1img_stale |= do_sync ? 3 : 1;
     } else if (dp) {
         int nr = g_nccl.allreduce(d->grad, d->grad, (size_t)d->P + 1, kNcclFloat, kNcclAvg,
                                   d->comm, d->stream);
@@ -2225,14 +2334,13 @@ after_step:
         d->w0bf_stale |= do_sync ? 3 : 1;
         d->w1img_stale |= do_sync ? 3 : 1;
         sgd_kernel<<<(unsigned)d->sms, 256, 0, d->stream>>>(d->online, d->target, d->grad, d->P,
-                                                             d->cfg.lr, d->sync_flag, d->err);
+                                                             d->cfg.lr, d->sync_flag, d->err, loss_dev);
         e = cudaGetLastError();
         if (e != cudaSuccess) {
             if (prev >= 0) cudaSetDevice(prev);
             return cuda_fail(e, "sgd_kernel");
         }
         g_launches.fetch_add(1);
-        if (loss_dev) cudaMemcpyAsync(loss_dev, d->grad + d->P, sizeof(float), cudaMemcpyDefault, d->stream);
     }
     if (avg && t % d->cfg.avg_period == 0) {
         // iterative parameter mixing (reading Q31): online and target <- their mean over ranks
@@ -2436,6 +2544,7 @@ extern "C" int dqn_attach_peers(rpl_dqn *d, int32_t rank, int32_t world, const v
     RPL_CUDA(cudaMemset((char *)d->xbuf + dp_flag_offset(d->P), 0, 256));
     RPL_CUDA(cudaDeviceSynchronize());
     d->dp_base = d->steps;
+    drop_dp_graphs(d);   // their exchange kernels were captured for the previous attach
     const cudaIpcMemHandle_t *hs = static_cast<const cudaIpcMemHandle_t *>(handles);
     for (int q = 0; q < world; ++q) {
         if (q == rank) {
@@ -2476,6 +2585,7 @@ extern "C" int dqn_detach_peers(rpl_dqn *d)
         d->rank = 0;
         d->world = 1;
     }
+    drop_dp_graphs(d);
     return RPL_OK;
 }
 

@@ -28,8 +28,13 @@ def b():
     return binding
 
 
+def _slot_stride(P):
+    # dp_peer.cuh dp_slot_stride: P + 1 words rounded up to 16 bytes
+    return (P + 1 + 3) & ~3
+
+
 def _xbuf_floats(P):
-    flag_off = ((3 * (P + 1) * 4 + 255) // 256) * 256
+    flag_off = ((3 * _slot_stride(P) * 4 + 255) // 256) * 256
     return (flag_off + 256) // 4, flag_off // 4
 
 
@@ -49,7 +54,7 @@ def test_emulated_ranks_mean_sgd(b, world, rs):
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
     w_ref = w0.copy()
     for t in (1, 2, 3):
-        slot = (t & 1) * (P + 1)
+        slot = (t & 1) * _slot_stride(P)
         grads = rng.standard_normal((world, P + 1)).astype(np.float32)
         for q in range(world):
             xb[q * stride + slot:q * stride + slot + P + 1] = torch.from_numpy(grads[q]).cuda()
@@ -78,7 +83,7 @@ def test_emulated_ranks_mean_sgd(b, world, rs):
     assert err.item() == 0
     # a non-finite mean loss skips the update and raises the sticky numeric bit
     t = 4
-    slot = (t & 1) * (P + 1)
+    slot = (t & 1) * _slot_stride(P)
     bad = rng.standard_normal((world, P + 1)).astype(np.float32)
     bad[world - 1, P] = np.nan
     for q in range(world):
@@ -112,7 +117,7 @@ def test_emulated_ranks_dqn_gradients_vs_oracle_o6(b, world, rs):
     sync = torch.zeros(1, dtype=torch.int32, device="cuda")
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
     t = 1
-    slot = (t & 1) * (P + 1)
+    slot = (t & 1) * _slot_stride(P)
     og, ol = [], []
     for q in range(world):
         rp = b.Replay(3000, 27, seed=2, rank=q)

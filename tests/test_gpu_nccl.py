@@ -48,3 +48,34 @@ def test_nccl_single_rank_equals_local(b, monkeypatch, avg_period, net):
     assert np.array_equal(runs[0][0], runs[1][0])
     assert np.array_equal(runs[0][1], runs[1][1])
     assert runs[0][2] == runs[1][2]
+
+
+def test_nccl_graph_captured_exchange_loss_destinations(b, monkeypatch):
+    # the NCCL all-reduce and the SGD after it are captured in the step graph (one launch per
+    # step); the SGD kernel writes the mean loss to the caller's destination, which may change
+    # between steps (device, pinned host): a one-rank learner must equal an unattached one
+    import torch
+    cfg = b.DQNConfig(max_batch=128, sync_period=3, double_dqn=True, lr=1e-3)
+    p0 = init_params(27, 8, (128,), True, 512, seed=5)
+    e = experiences(2000, seed=6)
+    runs = []
+    for attach in (False, True):
+        monkeypatch.setenv("RPL_DP_FORCE", "1" if attach else "0")
+        rp = b.Replay(2000, 27, seed=7)
+        rp.add_many(e)
+        dqn = b.DQN(cfg, p0)
+        if attach:
+            dqn.attach_nccl(0, 1, b.nccl_unique_id())
+        dev = torch.zeros(1, device="cuda")
+        host = torch.zeros(6, dtype=torch.float32, pin_memory=True)
+        losses = []
+        for i in range(6):
+            dst = host[i:i + 1] if i % 2 else dev
+            assert dqn.train_step(rp, 128, dst) == b.RPL_OK
+            torch.cuda.synchronize()
+            losses.append(float(dst.cpu()[0]) if dst is dev else float(dst[0]))
+        assert dqn.check() == b.RPL_OK
+        runs.append((dqn.get_params(b.RPL_ONLINE), dqn.get_params(b.RPL_TARGET), losses))
+    assert np.array_equal(runs[0][0], runs[1][0])
+    assert np.array_equal(runs[0][1], runs[1][1])
+    assert runs[0][2] == runs[1][2]
