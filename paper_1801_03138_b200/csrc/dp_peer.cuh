@@ -22,6 +22,7 @@ namespace rpl {
 constexpr int DP_MAXR = 8;                  // ranks of one node
 constexpr int64_t kDpRsMin = 1 << 20;      // gradients longer than this use the reduce-scatter kernel
 constexpr int kDpRsWorld = 4;              // ... and so does every gradient from this many ranks up
+constexpr int DP_U = 8;                    // elements per thread and round (loads in flight)
 // all-read moves (world - 1) x P words into each rank per step, reduce-scatter about 2 x P plus
 // a second handshake: from 4 ranks up (C2 at 8 GPUs: 3.9 MB vs 1.1 MB per rank) the bytes win
 inline bool dp_use_rs(int64_t P, int world) { return P + 1 > kDpRsMin || world >= kDpRsWorld; }
@@ -37,7 +38,55 @@ struct DPArgs {
     const int32_t *sync_flag[DP_MAXR];
     uint32_t *err[DP_MAXR];
     float *loss_out[DP_MAXR];            // the mean loss for the caller (or null), per local rank
+    // byte-state learners (wide.cuh): W0's bf16 planes [online, target][3][pe], rewritten by the
+    // SGD for the W0 entries (the first n0 = N0 * D words of the blob), so the next step needs
+    // no re-split (null: no planes)
+    uint16_t *w0bf[DP_MAXR];
+    int64_t w0_n, w0_pe;
+    int w0_D, w0_planes;
 };
+
+// the SGD of blob word i (the new weight w) into W0's bf16 planes, when i is a W0 entry
+__device__ __forceinline__ void dp_w0_planes(const DPArgs &a, int rl, int64_t i, float w, int do_sync)
+{
+    if (!a.w0bf[rl] || i >= a.w0_n) return;
+    const int ii = (int)i, u = ii / a.w0_D, k = ii - u * a.w0_D;
+    const int64_t t = wd_tix_k(u, k);
+    uint16_t h, m, l;
+    umma::split3_bf16(w, h, m, l);
+    uint16_t *pl = a.w0bf[rl];
+    for (int net = 0; net < (do_sync ? 2 : 1); ++net, pl += 3 * a.w0_pe) {
+        pl[t] = h;
+        if (a.w0_planes > 1) pl[a.w0_pe + t] = m;
+        if (a.w0_planes > 2) pl[2 * a.w0_pe + t] = l;
+    }
+}
+
+// the same for the float4 group j (blob words 4j .. 4j + 3): with D % 4 == 0 the four words are
+// consecutive inputs of one unit row, i.e. 8 bytes of one core-matrix row per plane
+__device__ __forceinline__ void dp_w0_planes4(const DPArgs &a, int rl, int64_t j, float4 w, int do_sync)
+{
+    if (!a.w0bf[rl] || 4 * j >= a.w0_n) return;
+    if ((a.w0_D & 3) != 0) {
+        dp_w0_planes(a, rl, 4 * j, w.x, do_sync);
+        dp_w0_planes(a, rl, 4 * j + 1, w.y, do_sync);
+        dp_w0_planes(a, rl, 4 * j + 2, w.z, do_sync);
+        dp_w0_planes(a, rl, 4 * j + 3, w.w, do_sync);
+        return;
+    }
+    const int ii = (int)(4 * j), u = ii / a.w0_D, k = ii - u * a.w0_D;
+    const int64_t t = wd_tix_k(u, k);
+    uint2 h, m, l;
+    umma::split3_pack2(w.x, w.y, h.x, m.x, l.x);
+    umma::split3_pack2(w.z, w.w, h.y, m.y, l.y);
+    uint16_t *pl = a.w0bf[rl];
+    for (int net = 0; net < (do_sync ? 2 : 1); ++net, pl += 3 * a.w0_pe) {
+        *reinterpret_cast<uint2 *>(pl + t) = h;
+        if (a.w0_planes > 1) *reinterpret_cast<uint2 *>(pl + a.w0_pe + t) = m;
+        if (a.w0_planes > 2) *reinterpret_cast<uint2 *>(pl + 2 * a.w0_pe + t) = l;
+    }
+}
+
 
 // exchange buffer: [2][S] gradient slots, [S] mean (reduce-scatter variant; S = P + 1 rounded to
 // 16 bytes: dp_slot_stride), then a
@@ -134,12 +183,33 @@ __global__ void __launch_bounds__(256) dp_peer_rs_sgd_kernel(const __grid_consta
     if (timed_out) return;
     __threadfence();
     // this rank's slice of the mean, into every rank's mean buffer
-    const int64_t lo = n * rank / a.world, hi = n * (rank + 1) / a.world;
-    for (int64_t i = lo + (int64_t)bi * blockDim.x + threadIdx.x; i < hi; i += (int64_t)bpr * blockDim.x) {
-        float g = 0.0f;
-        for (int q = 0; q < a.world; ++q) g += __ldcv(a.xbuf[q] + slot + i);
-        g = g / (float)a.world;
-        for (int q = 0; q < a.world; ++q) const_cast<float *>(a.xbuf[q])[2 * ss + i] = g;
+    // this rank's slice (whole float4 groups: slots and the mean buffer are 16-byte aligned and
+    // padded) of the mean, into every rank's mean buffer; DP_U groups per thread and round with
+    // all their loads in flight (the same rank-order sums)
+    const int64_t n4 = (n + 3) / 4, lo4 = n4 * rank / a.world, hi4 = n4 * (rank + 1) / a.world;
+    const int64_t S = (int64_t)bpr * blockDim.x;
+    for (int64_t j0 = lo4 + (int64_t)bi * blockDim.x + threadIdx.x; j0 < hi4; j0 += DP_U * S) {
+        float4 g[DP_U];
+#pragma unroll
+        for (int u = 0; u < DP_U; ++u) g[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < a.world; ++q) {
+            float4 v[DP_U];
+            const float4 *src = reinterpret_cast<const float4 *>(a.xbuf[q] + slot);
+#pragma unroll
+            for (int u = 0; u < DP_U; ++u) v[u] = j0 + u * S < hi4 ? __ldcv(src + j0 + u * S) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < DP_U; ++u) {
+                g[u].x += v[u].x; g[u].y += v[u].y; g[u].z += v[u].z; g[u].w += v[u].w;
+            }
+        }
+        const float fw = (float)a.world;
+#pragma unroll
+        for (int u = 0; u < DP_U; ++u) {
+            if (j0 + u * S >= hi4) continue;
+            const float4 m = make_float4(g[u].x / fw, g[u].y / fw, g[u].z / fw, g[u].w / fw);
+            for (int q = 0; q < a.world; ++q)
+                reinterpret_cast<float4 *>(const_cast<float *>(a.xbuf[q]) + 2 * ss)[j0 + u * S] = m;
+        }
     }
     __threadfence_system();
     __syncthreads();
@@ -160,13 +230,52 @@ __global__ void __launch_bounds__(256) dp_peer_rs_sgd_kernel(const __grid_consta
     const bool ok = isfinite(loss);
     const int do_sync = *a.sync_flag[rl];
     float *on = a.online[rl], *tg = a.target[rl], *gm = a.gmean[rl];
-    for (int64_t i = (int64_t)bi * blockDim.x + threadIdx.x; i < a.P; i += (int64_t)bpr * blockDim.x) {
-        const float g = __ldcv(mean + i);
-        gm[i] = g;
-        if (ok) {
-            const float w = on[i] - a.lr * g;
-            on[i] = w;
-            if (do_sync) tg[i] = w;
+    // the learner's own arrays 16-byte aligned (the real learner; emulated ranks may not be):
+    // float4 groups, then the scalar tail
+    const bool vec = ((reinterpret_cast<uintptr_t>(on) | reinterpret_cast<uintptr_t>(tg) |
+                       reinterpret_cast<uintptr_t>(gm)) & 15) == 0;
+    const int64_t P4 = vec ? a.P / 4 : 0;
+    for (int64_t j0 = (int64_t)bi * blockDim.x + threadIdx.x; j0 < P4; j0 += DP_U * S) {
+        float4 g[DP_U], w[DP_U];
+#pragma unroll
+        for (int u = 0; u < DP_U; ++u) {
+            const bool in = j0 + u * S < P4;
+            g[u] = in ? __ldcv(reinterpret_cast<const float4 *>(mean) + j0 + u * S) : make_float4(0.f, 0.f, 0.f, 0.f);
+            w[u] = in ? reinterpret_cast<const float4 *>(on)[j0 + u * S] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < DP_U; ++u) {
+            const int64_t j = j0 + u * S;
+            if (j >= P4) continue;
+            reinterpret_cast<float4 *>(gm)[j] = g[u];
+            if (ok) {
+                const float4 nw = make_float4(w[u].x - a.lr * g[u].x, w[u].y - a.lr * g[u].y, w[u].z - a.lr * g[u].z,
+                                              w[u].w - a.lr * g[u].w);
+                reinterpret_cast<float4 *>(on)[j] = nw;
+                if (do_sync) reinterpret_cast<float4 *>(tg)[j] = nw;
+                dp_w0_planes4(a, rl, j, nw, do_sync);
+            }
+        }
+    }
+    for (int64_t i0 = 4 * P4 + (int64_t)bi * blockDim.x + threadIdx.x; i0 < a.P; i0 += DP_U * S) {
+        float g[DP_U], w[DP_U];
+#pragma unroll
+        for (int u = 0; u < DP_U; ++u) {
+            const bool in = i0 + u * S < a.P;
+            g[u] = in ? __ldcv(mean + i0 + u * S) : 0.0f;
+            w[u] = in ? on[i0 + u * S] : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < DP_U; ++u) {
+            const int64_t i = i0 + u * S;
+            if (i >= a.P) continue;
+            gm[i] = g[u];
+            if (ok) {
+                const float nw = w[u] - a.lr * g[u];
+                on[i] = nw;
+                if (do_sync) tg[i] = nw;
+                dp_w0_planes(a, rl, i, nw, do_sync);
+            }
         }
     }
     if (bi == 0 && threadIdx.x == 0) {
@@ -205,15 +314,33 @@ __global__ void __launch_bounds__(256) dp_peer_sgd_kernel(const __grid_constant_
     const int do_sync = *a.sync_flag[rl];
     float *on = a.online[rl], *tg = a.target[rl], *gm = a.gmean[rl];
     // (4) mean of the ranks' gradients in rank order, SGD, target copy on sync steps
-    for (int64_t i = (int64_t)bi * blockDim.x + threadIdx.x; i < a.P; i += (int64_t)bpr * blockDim.x) {
-        float g = 0.0f;
-        for (int q = 0; q < a.world; ++q) g += __ldcv(a.xbuf[q] + slot + i);
-        g = g / (float)a.world;
-        gm[i] = g;
-        if (ok) {
-            const float w = on[i] - a.lr * g;
-            on[i] = w;
-            if (do_sync) tg[i] = w;
+    const int64_t S = (int64_t)bpr * blockDim.x;
+    for (int64_t i0 = (int64_t)bi * blockDim.x + threadIdx.x; i0 < a.P; i0 += DP_U * S) {
+        float g[DP_U], w[DP_U];
+#pragma unroll
+        for (int u = 0; u < DP_U; ++u) {
+            g[u] = 0.0f;
+            w[u] = i0 + u * S < a.P ? on[i0 + u * S] : 0.0f;
+        }
+        for (int q = 0; q < a.world; ++q) {
+            float v[DP_U];
+#pragma unroll
+            for (int u = 0; u < DP_U; ++u) v[u] = i0 + u * S < a.P ? __ldcv(a.xbuf[q] + slot + i0 + u * S) : 0.0f;
+#pragma unroll
+            for (int u = 0; u < DP_U; ++u) g[u] += v[u];
+        }
+#pragma unroll
+        for (int u = 0; u < DP_U; ++u) {
+            const int64_t i = i0 + u * S;
+            if (i >= a.P) continue;
+            const float m = g[u] / (float)a.world;
+            gm[i] = m;
+            if (ok) {
+                const float nw = w[u] - a.lr * m;
+                on[i] = nw;
+                if (do_sync) tg[i] = nw;
+                dp_w0_planes(a, rl, i, nw, do_sync);
+            }
         }
     }
     if (bi == 0 && threadIdx.x == 0) {

@@ -806,6 +806,7 @@ struct rpl_dqn {
     struct WideGraph {
         const rpl_replay *rp;
         int B, apply;
+        int par;                   // peer-memory data parallelism: the exchange slot written, else -1
         cudaGraph_t graph;
         cudaGraphExec_t exec;
         cudaGraphNode_t k4;        // the loss destination
@@ -1795,14 +1796,21 @@ static void wide_fast_args(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, i
 // (event / size / cursor from the control block), tcgen05 layer 0, split-K reduction, the
 // fast kernels above it (K4 advances the event), dW0 + its SGD
 static cudaError_t wide_graph_step(rpl_dqn *d, rpl_replay *rp, int B, float *loss_dev, int apply,
-                                   const WideArgs &w)
+                                   const WideArgs &w0, int par)
 {
     FastArgs fp;
     wide_fast_args(d, rp, B, loss_dev, apply, fp);
     fp.event_advanced = 0;
+    WideArgs w = w0;
+    if (par >= 0) {   // peer-memory data parallelism: the gradient goes straight into its exchange slot
+        float *slot = d->xbuf + (int64_t)par * dp_slot_stride(d->P);
+        if (fp.gpart == fp.grad) fp.gpart = slot;
+        fp.grad = slot;
+        w.grad = slot;
+    }
     rpl_dqn::WideGraph *ge = nullptr;
     for (auto &g : d->wide_graphs)
-        if (g.rp == rp && g.B == B && g.apply == apply) ge = &g;
+        if (g.rp == rp && g.B == B && g.apply == apply && g.par == par) ge = &g;
     cudaError_t e = cudaSuccess;
     if (!ge) {
         cudaGraph_t graph = nullptr;
@@ -1850,7 +1858,7 @@ static cudaError_t wide_graph_step(rpl_dqn *d, rpl_replay *rp, int B, float *los
             cudaGraphDestroy(d->wide_graphs.front().graph);
             d->wide_graphs.erase(d->wide_graphs.begin());
         }
-        d->wide_graphs.push_back({rp, B, apply, graph, exec, k4, fp});
+        d->wide_graphs.push_back({rp, B, apply, par, graph, exec, k4, fp});
         ge = &d->wide_graphs.back();
     } else if (memcmp(&ge->args, &fp, sizeof fp) != 0) {
         // between replays only the loss destination may change (K4 writes it)
@@ -1901,6 +1909,15 @@ static cudaError_t launch_dp(const rpl_dqn *d, const DPArgs &a, cudaStream_t st)
 // cached step graphs that end in a data-parallel exchange: rebuilt after an attach / detach
 static void drop_dp_graphs(rpl_dqn *d)
 {
+    for (size_t i = 0; i < d->wide_graphs.size();) {
+        if (d->wide_graphs[i].apply == 0) {
+            cudaGraphExecDestroy(d->wide_graphs[i].exec);
+            cudaGraphDestroy(d->wide_graphs[i].graph);
+            d->wide_graphs.erase(d->wide_graphs.begin() + i);
+        } else {
+            ++i;
+        }
+    }
     for (size_t i = 0; i < d->graphs.size();) {
         if (d->graphs[i].apply == 0) {
             cudaGraphExecDestroy(d->graphs[i].exec);
@@ -1936,6 +1953,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
     const bool avg = d->comm != nullptr && d->cfg.avg_period > 0;
     const bool dp = (d->comm != nullptr || d->p2p) && !avg;
     bool dp_graphed = false;   // the NCCL all-reduce + SGD captured in the fast step's graph
+    int wide_par = -1;         // the byte-state graph wrote the gradient into this exchange slot
     cudaError_t e = cudaSuccess;
     // a deferred insert is consumed by the fast path's K1 on the shared stream; otherwise it
     // is written now by the insert kernel
@@ -2229,7 +2247,8 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             w.b0 = d->boff[0];
             if (d->wide_fast && d->use_graphs && !rp->distinct) {
                 // the whole byte-state step as one CUDA graph (control block read on device)
-                e = wide_graph_step(d, rp, batch, dp ? nullptr : loss_dev, dp ? 0 : 1, w);
+                wide_par = dp && d->p2p ? (int)((t - d->dp_base) & 1) : -1;
+                e = wide_graph_step(d, rp, batch, dp ? nullptr : loss_dev, dp ? 0 : 1, w, wide_par);
                 if (e != cudaSuccess) {
                     if (prev >= 0) cudaSetDevice(prev);
                     return cuda_fail(e, "wide graph step");
@@ -2303,10 +2322,24 @@ after_step:
         // (the byte-state and generic steps; the fast step captures all of this in its graph)
         const int64_t tx = t - d->dp_base;
         float *mine = d->xbuf + (int64_t)(tx & 1) * dp_slot_stride(d->P);
+        bool planes = false;   // the exchange's SGD rewrites W0's bf16 planes (byte-state learners)
         if (!dp_graphed) {
-            e = cudaMemcpyAsync(mine, d->grad, (size_t)(d->P + 1) * sizeof(float), cudaMemcpyDeviceToDevice, d->stream);
+            if (wide_par < 0)   // (the byte-state graph wrote it into the slot already)
+                e = cudaMemcpyAsync(mine, d->grad, (size_t)(d->P + 1) * sizeof(float), cudaMemcpyDeviceToDevice, d->stream);
             DPArgs a;
             fill_dp(d, tx, loss_dev, a);
+#ifndef RPL_NO_DP_PLANES   // (A/B timing builds only)
+            if (d->w0bf && rp->ring.u8 && d->wide_tc && d->woff[0] == 0 && !d->w0bf_stale) {
+#else
+            if (false) {
+#endif
+                a.w0bf[0] = d->w0bf;
+                a.w0_n = (int64_t)d->N[0] * d->cfg.state_dim;
+                a.w0_pe = wd_plane_elems(d->cfg.state_dim);
+                a.w0_D = d->cfg.state_dim;
+                a.w0_planes = d->cfg.precision == RPL_PREC_BF16 ? 1 : d->cfg.precision == RPL_PREC_TF32 ? 2 : 3;
+                planes = true;
+            }
             if (e == cudaSuccess) e = launch_dp(d, a, d->stream);
             if (e != cudaSuccess) {
                 if (prev >= 0) cudaSetDevice(prev);
@@ -2314,8 +2347,9 @@ after_step:
             }
             g_launches.fetch_add(1);
         }
-        // the update rewrote the online W0 / W1 without their images (the target too on a sync step)
-        d->w0bf_stale |= do_sync ? 3 : 1;
+        // the update rewrote the online W0 / W1 without their images (the target too on a sync
+        // step) -- except W0's planes when the exchange wrote them
+        if (!planes) d->w0bf_stale |= do_sync ? 3 : 1;
         d->w1img_stale |= do_sync ? 3 : 1;
     } else if (dp && dp_graphed) {
         // the all-reduce and the SGD after it ran inside the step's graph (nccl_tail)
