@@ -38,52 +38,55 @@ struct DPArgs {
     const int32_t *sync_flag[DP_MAXR];
     uint32_t *err[DP_MAXR];
     float *loss_out[DP_MAXR];            // the mean loss for the caller (or null), per local rank
-    // byte-state learners (wide.cuh): W0's bf16 planes [online, target][3][pe], rewritten by the
-    // SGD for the W0 entries (the first n0 = N0 * D words of the blob), so the next step needs
-    // no re-split (null: no planes)
-    uint16_t *w0bf[DP_MAXR];
-    int64_t w0_n, w0_pe;
-    int w0_D, w0_planes;
+    // byte-state learners (wide.cuh): W0's bf16 planes, rewritten by the SGD for the W0 entries,
+    // so the next step needs no re-split (.bf null: no planes); local rank 0 only
+    struct { uint16_t *bf; int64_t n, pe; int D, planes; } w0;
 };
 
+// W0's bf16 planes of a byte-state learner ([online, target][planes][pe], null: none): the first
+// n = N0 * D blob words are W0 [N0][D]
+struct W0Planes {
+    uint16_t *bf;
+    int64_t n, pe;
+    int D, planes;
+};
 // the SGD of blob word i (the new weight w) into W0's bf16 planes, when i is a W0 entry
-__device__ __forceinline__ void dp_w0_planes(const DPArgs &a, int rl, int64_t i, float w, int do_sync)
+__device__ __forceinline__ void dp_w0_planes(const W0Planes &q, int64_t i, float w, int do_sync)
 {
-    if (!a.w0bf[rl] || i >= a.w0_n) return;
-    const int ii = (int)i, u = ii / a.w0_D, k = ii - u * a.w0_D;
+    if (!q.bf || i >= q.n) return;
+    const int ii = (int)i, u = ii / q.D, k = ii - u * q.D;
     const int64_t t = wd_tix_k(u, k);
     uint16_t h, m, l;
     umma::split3_bf16(w, h, m, l);
-    uint16_t *pl = a.w0bf[rl];
-    for (int net = 0; net < (do_sync ? 2 : 1); ++net, pl += 3 * a.w0_pe) {
+    uint16_t *pl = q.bf;
+    for (int net = 0; net < (do_sync ? 2 : 1); ++net, pl += 3 * q.pe) {
         pl[t] = h;
-        if (a.w0_planes > 1) pl[a.w0_pe + t] = m;
-        if (a.w0_planes > 2) pl[2 * a.w0_pe + t] = l;
+        if (q.planes > 1) pl[q.pe + t] = m;
+        if (q.planes > 2) pl[2 * q.pe + t] = l;
     }
 }
-
 // the same for the float4 group j (blob words 4j .. 4j + 3): with D % 4 == 0 the four words are
 // consecutive inputs of one unit row, i.e. 8 bytes of one core-matrix row per plane
-__device__ __forceinline__ void dp_w0_planes4(const DPArgs &a, int rl, int64_t j, float4 w, int do_sync)
+__device__ __forceinline__ void dp_w0_planes4(const W0Planes &q, int64_t j, float4 w, int do_sync)
 {
-    if (!a.w0bf[rl] || 4 * j >= a.w0_n) return;
-    if ((a.w0_D & 3) != 0) {
-        dp_w0_planes(a, rl, 4 * j, w.x, do_sync);
-        dp_w0_planes(a, rl, 4 * j + 1, w.y, do_sync);
-        dp_w0_planes(a, rl, 4 * j + 2, w.z, do_sync);
-        dp_w0_planes(a, rl, 4 * j + 3, w.w, do_sync);
+    if (!q.bf || 4 * j >= q.n) return;
+    if ((q.D & 3) != 0) {
+        dp_w0_planes(q, 4 * j, w.x, do_sync);
+        dp_w0_planes(q, 4 * j + 1, w.y, do_sync);
+        dp_w0_planes(q, 4 * j + 2, w.z, do_sync);
+        dp_w0_planes(q, 4 * j + 3, w.w, do_sync);
         return;
     }
-    const int ii = (int)(4 * j), u = ii / a.w0_D, k = ii - u * a.w0_D;
+    const int ii = (int)(4 * j), u = ii / q.D, k = ii - u * q.D;
     const int64_t t = wd_tix_k(u, k);
     uint2 h, m, l;
     umma::split3_pack2(w.x, w.y, h.x, m.x, l.x);
     umma::split3_pack2(w.z, w.w, h.y, m.y, l.y);
-    uint16_t *pl = a.w0bf[rl];
-    for (int net = 0; net < (do_sync ? 2 : 1); ++net, pl += 3 * a.w0_pe) {
+    uint16_t *pl = q.bf;
+    for (int net = 0; net < (do_sync ? 2 : 1); ++net, pl += 3 * q.pe) {
         *reinterpret_cast<uint2 *>(pl + t) = h;
-        if (a.w0_planes > 1) *reinterpret_cast<uint2 *>(pl + a.w0_pe + t) = m;
-        if (a.w0_planes > 2) *reinterpret_cast<uint2 *>(pl + 2 * a.w0_pe + t) = l;
+        if (q.planes > 1) *reinterpret_cast<uint2 *>(pl + q.pe + t) = m;
+        if (q.planes > 2) *reinterpret_cast<uint2 *>(pl + 2 * q.pe + t) = l;
     }
 }
 
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(256) dp_peer_rs_sgd_kernel(const __grid_consta
                                               w[u].w - a.lr * g[u].w);
                 reinterpret_cast<float4 *>(on)[j] = nw;
                 if (do_sync) reinterpret_cast<float4 *>(tg)[j] = nw;
-                dp_w0_planes4(a, rl, j, nw, do_sync);
+                if (rl == 0) dp_w0_planes4(W0Planes{a.w0.bf, a.w0.n, a.w0.pe, a.w0.D, a.w0.planes}, j, nw, do_sync);
             }
         }
     }
@@ -274,7 +277,7 @@ __global__ void __launch_bounds__(256) dp_peer_rs_sgd_kernel(const __grid_consta
                 const float nw = w[u] - a.lr * g[u];
                 on[i] = nw;
                 if (do_sync) tg[i] = nw;
-                dp_w0_planes(a, rl, i, nw, do_sync);
+                if (rl == 0) dp_w0_planes(W0Planes{a.w0.bf, a.w0.n, a.w0.pe, a.w0.D, a.w0.planes}, i, nw, do_sync);
             }
         }
     }
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(256) dp_peer_sgd_kernel(const __grid_constant_
                 const float nw = w[u] - a.lr * m;
                 on[i] = nw;
                 if (do_sync) tg[i] = nw;
-                dp_w0_planes(a, rl, i, nw, do_sync);
+                if (rl == 0) dp_w0_planes(W0Planes{a.w0.bf, a.w0.n, a.w0.pe, a.w0.D, a.w0.planes}, i, nw, do_sync);
             }
         }
     }

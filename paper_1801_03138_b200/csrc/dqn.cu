@@ -675,23 +675,57 @@ __global__ void __launch_bounds__(NT, 1) train_step_kernel(const __grid_constant
 }
 
 // SGD after an NCCL all-reduce (world > 1): grad[P] holds the rank-averaged loss
-__global__ void __launch_bounds__(256) sgd_kernel(float *online, float *target, const float *grad,
-                                                  int64_t P, float lr, const int32_t *sync_flag,
-                                                  uint32_t *err, float *loss_out)
+// the SGD after an NCCL all-reduce (grad = the ranks' mean, word P = the mean loss): DP_U float4
+// groups per thread and round with their loads in flight, the scalar tail after; W0's bf16
+// planes rewritten for byte-state learners (as the peer-memory exchange does: DPArgs fields)
+struct SgdArgs {
+    float *online, *target;
+    const float *grad;
+    int64_t P;
+    float lr;
+    const int32_t *sync_flag;
+    uint32_t *err;
+    float *loss_out;      // the mean loss for the caller (or null)
+    W0Planes planes;      // byte-state learners: W0's bf16 planes rewritten with W0 (.bf null: none)
+};
+__global__ void __launch_bounds__(256) sgd_kernel(const __grid_constant__ SgdArgs a)
 {
-    const int do_sync = *sync_flag;
-    const float loss = grad[P];
+    const int do_sync = *a.sync_flag;
+    const float loss = a.grad[a.P];
     const bool ok = isfinite(loss);
-    if (loss_out && blockIdx.x == 0 && threadIdx.x == 0) *loss_out = loss;   // the ranks' mean loss
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        if (ok) {
-            const float w = online[i] - lr * grad[i];
-            online[i] = w;
-            if (do_sync) target[i] = w;
+    if (a.loss_out && blockIdx.x == 0 && threadIdx.x == 0) *a.loss_out = loss;   // the ranks' mean loss
+    const int64_t S = (int64_t)gridDim.x * blockDim.x, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(a.online) | reinterpret_cast<uintptr_t>(a.target) |
+                       reinterpret_cast<uintptr_t>(a.grad)) & 15) == 0;
+    const int64_t P4 = vec ? a.P / 4 : 0;
+    if (ok) {
+        for (int64_t j0 = t0; j0 < P4; j0 += DP_U * S) {
+            float4 g[DP_U], w[DP_U];
+#pragma unroll
+            for (int u = 0; u < DP_U; ++u) {
+                const bool in = j0 + u * S < P4;
+                g[u] = in ? __ldcg(reinterpret_cast<const float4 *>(a.grad) + j0 + u * S) : make_float4(0.f, 0.f, 0.f, 0.f);
+                w[u] = in ? reinterpret_cast<const float4 *>(a.online)[j0 + u * S] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < DP_U; ++u) {
+                const int64_t j = j0 + u * S;
+                if (j >= P4) continue;
+                const float4 nw = make_float4(w[u].x - a.lr * g[u].x, w[u].y - a.lr * g[u].y, w[u].z - a.lr * g[u].z,
+                                              w[u].w - a.lr * g[u].w);
+                reinterpret_cast<float4 *>(a.online)[j] = nw;
+                if (do_sync) reinterpret_cast<float4 *>(a.target)[j] = nw;
+                dp_w0_planes4(a.planes, j, nw, do_sync);
+            }
+        }
+        for (int64_t i = 4 * P4 + t0; i < a.P; i += S) {
+            const float w = a.online[i] - a.lr * a.grad[i];
+            a.online[i] = w;
+            if (do_sync) a.target[i] = w;
+            dp_w0_planes(a.planes, i, w, do_sync);
         }
     }
-    if (!ok && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(err, ERRBIT_NUMERIC);
+    if (!ok && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(a.err, ERRBIT_NUMERIC);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1876,6 +1910,28 @@ static cudaError_t wide_graph_step(rpl_dqn *d, rpl_replay *rp, int B, float *los
     return e;
 }
 
+// the SGD after an NCCL all-reduce; W0's planes for byte-state learners whose planes are current
+static SgdArgs sgd_args(const rpl_dqn *d, const rpl_replay *rp, float *loss_out)
+{
+    SgdArgs a{};
+    a.online = d->online;
+    a.target = d->target;
+    a.grad = d->grad;
+    a.P = d->P;
+    a.lr = d->cfg.lr;
+    a.sync_flag = d->sync_flag;
+    a.err = d->err;
+    a.loss_out = loss_out;
+    if (d->w0bf && rp->ring.u8 && d->wide_tc && d->woff[0] == 0 && !d->w0bf_stale) {
+        a.planes.bf = d->w0bf;
+        a.planes.n = (int64_t)d->N[0] * d->cfg.state_dim;
+        a.planes.pe = wd_plane_elems(d->cfg.state_dim);
+        a.planes.D = d->cfg.state_dim;
+        a.planes.planes = d->cfg.precision == RPL_PREC_BF16 ? 1 : d->cfg.precision == RPL_PREC_TF32 ? 2 : 3;
+    }
+    return a;
+}
+
 // the exchange kernel's arguments for exchange step tx (dp_peer.cuh)
 static void fill_dp(const rpl_dqn *d, int64_t tx, float *loss_out, DPArgs &a)
 {
@@ -2045,8 +2101,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                             set_error("ncclAllReduce (graph capture) failed: %s", g_nccl.errstr ? g_nccl.errstr(nr) : "?");
                             e2 = cudaErrorUnknown;
                         } else {
-                            sgd_kernel<<<(unsigned)d->sms, 256, 0, d->cap_stream>>>(d->online, d->target, d->grad, d->P,
-                                                                                   d->cfg.lr, d->sync_flag, d->err, sgd_loss);
+                            sgd_kernel<<<(unsigned)d->sms, 256, 0, d->cap_stream>>>(sgd_args(d, rp, sgd_loss));
                             e2 = cudaGetLastError();
                         }
                     }
@@ -2151,8 +2206,8 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             }
             if (e == cudaSuccess && ge && ge->ksgd && ge->sgd_loss != sgd_loss) {
                 // the SGD node's loss destination (its other arguments are fixed)
-                void *sargs[] = {&d->online, &d->target, &d->grad, &d->P, &d->cfg.lr, &d->sync_flag, &d->err,
-                                 &sgd_loss};
+                SgdArgs sa = sgd_args(d, rp, sgd_loss);
+                void *sargs[] = {&sa};
                 cudaKernelNodeParams kp = {};
                 e = cudaGraphKernelNodeGetParams(ge->ksgd, &kp);
                 kp.kernelParams = sargs;
@@ -2333,11 +2388,11 @@ after_step:
 #else
             if (false) {
 #endif
-                a.w0bf[0] = d->w0bf;
-                a.w0_n = (int64_t)d->N[0] * d->cfg.state_dim;
-                a.w0_pe = wd_plane_elems(d->cfg.state_dim);
-                a.w0_D = d->cfg.state_dim;
-                a.w0_planes = d->cfg.precision == RPL_PREC_BF16 ? 1 : d->cfg.precision == RPL_PREC_TF32 ? 2 : 3;
+                a.w0.bf = d->w0bf;
+                a.w0.n = (int64_t)d->N[0] * d->cfg.state_dim;
+                a.w0.pe = wd_plane_elems(d->cfg.state_dim);
+                a.w0.D = d->cfg.state_dim;
+                a.w0.planes = d->cfg.precision == RPL_PREC_BF16 ? 1 : d->cfg.precision == RPL_PREC_TF32 ? 2 : 3;
                 planes = true;
             }
             if (e == cudaSuccess) e = launch_dp(d, a, d->stream);
@@ -2363,12 +2418,12 @@ after_step:
             if (prev >= 0) cudaSetDevice(prev);
             return RPL_ENCCL;
         }
+        const SgdArgs sa = sgd_args(d, rp, loss_dev);
         // the all-reduced update rewrote the online W0 / W1 without their images (the target
-        // too on a sync step)
-        d->w0bf_stale |= do_sync ? 3 : 1;
+        // too on a sync step) -- except W0's planes when the SGD writes them
+        if (!sa.planes.bf) d->w0bf_stale |= do_sync ? 3 : 1;
         d->w1img_stale |= do_sync ? 3 : 1;
-        sgd_kernel<<<(unsigned)d->sms, 256, 0, d->stream>>>(d->online, d->target, d->grad, d->P,
-                                                             d->cfg.lr, d->sync_flag, d->err, loss_dev);
+        sgd_kernel<<<(unsigned)d->sms, 256, 0, d->stream>>>(sa);
         e = cudaGetLastError();
         if (e != cudaSuccess) {
             if (prev >= 0) cudaSetDevice(prev);

@@ -79,3 +79,28 @@ def test_nccl_graph_captured_exchange_loss_destinations(b, monkeypatch):
     assert np.array_equal(runs[0][0], runs[1][0])
     assert np.array_equal(runs[0][1], runs[1][1])
     assert runs[0][2] == runs[1][2]
+
+
+def test_nccl_single_rank_wide_learner_equals_local(b, monkeypatch):
+    # config-5 network (tcgen05 layer 0): the SGD after the all-reduce rewrites W0 and its bf16
+    # planes (the target's on sync steps), which the next step's layer 0 reads
+    from inputs import experiences_u8
+    D = 84 * 84 * 4
+    cfg = b.DQNConfig(state_dim=D, n_actions=8, dueling=True, hidden=(128,), stream=512,
+                      max_batch=32, sync_period=3, lr=1e-3)
+    p0 = init_params(D, 8, (128,), True, 512, seed=13)
+    e = experiences_u8(64, state_dim=D, seed=12)
+    runs = []
+    for attach in (False, True):
+        monkeypatch.setenv("RPL_DP_FORCE", "1" if attach else "0")
+        rp = b.Replay(64, D, seed=11, state_dtype="u8")
+        rp.add(**e)
+        dqn = b.DQN(cfg, p0)
+        if attach:
+            dqn.attach_nccl(0, 1, b.nccl_unique_id())
+        for _ in range(7):
+            assert dqn.train_step(rp, 32) == b.RPL_OK
+        assert dqn.check() == b.RPL_OK
+        runs.append((dqn.get_params(b.RPL_ONLINE), dqn.get_params(b.RPL_TARGET)))
+    assert np.array_equal(runs[0][0], runs[1][0])
+    assert np.array_equal(runs[0][1], runs[1][1])
