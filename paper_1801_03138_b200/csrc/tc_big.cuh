@@ -267,8 +267,8 @@ struct T3aSmem {
         oA = 0;                                  // dZ1 chunks: 2 stages
         oB = oA + 2 * T3A_STAGE_A;               // H0 chunks: 2 stages
         oWh = oB + 2 * T3A_STAGE_B;              // online head weights of the tile [J][128]
-        ored = oWh + J * 128 * 4;                // cross-warp sums [16 groups][8 + 8 JW] + [JPMAX]
-        obar = (ored + (16 * (8 + 8 * JW) + JPMAX) * 4 + 15) & ~15;
+        ored = oWh + J * 128 * 4;                // cross-warp sums [2 row halves][16 groups][8 + 8 JW] + [JPMAX]
+        obar = (ored + (2 * 16 * (8 + 8 * JW) + JPMAX) * 4 + 15) & ~15;
         total = obar + 6 * 8;
     }
 };
@@ -844,7 +844,9 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
     load_pass(g, 0, h1n, dhn);
     load_pass(g, 1, h1m, dhm);
     int i = 0;
+#ifndef RPL_T3A_EPI_TRACE
     tr_.mark(6);   // setup done (cycles since the CTA started; overwritten per step)
+#endif
     for (int c = g; c < nch; c += G, ++i) {
         const int s = i & 1;
         char *Ast = smc + L.oA + s * T3A_STAGE_A, *Bst = smc + L.oB + s * T3A_STAGE_B;
@@ -943,7 +945,11 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
         }
     }
     if (tid == 0) umma::commit(mdone);
+#ifndef RPL_T3A_EPI_TRACE
     tr_.mark(7);   // chunk loop done
+#else
+    tr_.mark(5);   // (epilogue trace build: 5 loop done, 6 shuffles done, 7 partial writes done)
+#endif
     // the tile's db1 / dW_head / db_head: sums over the 8 rows of a lane group (shuffles), then
     // over the two row halves (shared memory), in a fixed order
 #pragma unroll
@@ -957,42 +963,48 @@ __global__ void __launch_bounds__(tcb::T3A_T, 1) tcb_dw1_kernel(const __grid_con
 #pragma unroll
         for (int j = 0; j < JPMAX; ++j) bha[j] += __shfl_xor_sync(0xffffffffu, bha[j], o);
     }
+#ifdef RPL_T3A_EPI_TRACE
+    tr_.mark(6);
+#endif
+    // both row halves' lane-group sums into shared memory, then every thread writes whole
+    // coalesced runs of the tile's db1 / dW_head (row half 0 + row half 1, the former order)
     constexpr int RW = 8 + 8 * JW;
-    if (rh == 1 && r8 == 0) {
-        float *rp = red + cg * RW;
+    float *red1 = red + 16 * RW + JPMAX;   // row half 0 (red: row half 1, then db_head)
+    if (r8 == 0) {
+        float *rp = (rh == 1 ? red : red1) + cg * RW;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             rp[k] = db1[k];
 #pragma unroll
             for (int j = 0; j < JW; ++j) rp[8 + 8 * j + k] = wacc[j][k];
         }
-        if (cg == 0)
+        if (rh == 1 && cg == 0)
 #pragma unroll
             for (int j = 0; j < JPMAX; ++j) red[16 * RW + j] = bha[j];
     }
     __syncthreads();
     float *gp = p.gpart + (int64_t)g * p.gps;
-    if (rh == 0 && r8 == 0) {
-        const float *rp = red + cg * RW;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int u = u0 + 8 * cg + k;
-            gp[p.b1 + u] = db1[k] + rp[k];
-#pragma unroll
-            for (int j = 0; j < JW; ++j)
-                if (jlo + j < jhi) {
-                    const float v = wacc[j][k] + rp[8 + 8 * j + k];
-                    const int jj = jlo + j;
-                    int64_t o;
-                    if (!p.dueling) o = (int64_t)jj * N1 + u;
-                    else if (jj == 0) o = u;
-                    else o = (int64_t)jj * p.S + (u - p.S);
-                    gp[p.wh + o] = v;
-                }
+    for (int o = tid; o < 128 * (1 + JW); o += T3A_T) {
+        const int ul = o & 127, sl = o >> 7, cgo = ul >> 3, k = ul & 7, u = u0 + ul;
+        const int idx = sl == 0 ? k : 8 + 8 * (sl - 1) + k;
+        const float v = red1[cgo * RW + idx] + red[cgo * RW + idx];
+        if (sl == 0) {
+            gp[p.b1 + u] = v;
+        } else {
+            const int jj = jlo + sl - 1;
+            if (jj >= jhi) continue;
+            int64_t off;
+            if (!p.dueling) off = (int64_t)jj * N1 + u;
+            else if (jj == 0) off = u;
+            else off = (int64_t)jj * p.S + (u - p.S);
+            gp[p.wh + off] = v;
         }
-        if (cg == 0 && ut == 0)
-            for (int j = 0; j < J; ++j) gp[p.bh + j] = bha[j] + red[16 * RW + j];
     }
+    if (tid == 0 && ut == 0)   // db_head: row half 0's group 0 sums (registers of thread 0) + row half 1's
+        for (int j = 0; j < J; ++j) gp[p.bh + j] = bha[j] + red[16 * RW + j];
+#ifdef RPL_T3A_EPI_TRACE
+    tr_.mark(7);
+#endif
     // dW1 of the tile: TMEM lane = unit, column = layer-0 unit; warps w, w + 4 split the columns
     tcb::wait(mdone, 0);
     {
