@@ -94,9 +94,11 @@ typedef struct {
                              stream), gathers the rows on the CPU into pinned staging and
                              copies the batch to the GPU in one H2D transfer of
                              B*(row bytes + 4) bytes (counted in h2d_bytes) before the same
-                             train-step kernels run.  fp32 states, uniform sampling, one
-                             state pair per row, the fast path's net shapes; replay_gather
-                             returns RPL_ESTATE                                              */
+                             train-step kernels run.  fp32 states, uniform or distinct
+                             sampling (the CPU draws the same streams: the paper's in-RAM
+                             `random.sample` is the distinct rule, reading Q29), one state
+                             pair per row, the fast path's net shapes; replay_gather returns
+                             RPL_ESTATE                                                      */
     int64_t update_size;  /* 0 (default): every replay_add is one insert, visible at once.
                              U > 0: P:73 block updates ("Experiences are queued in RAM until
                              the queue has enough experiences to update the next block";

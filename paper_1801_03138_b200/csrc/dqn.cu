@@ -2039,6 +2039,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
             }
             fp.ring = const_cast<float *>(rows);
             fp.bidx = bidx;
+            fp.distinct = 0;   // (distinct batches are drawn by the CPU sampler too)
         }
         if (fp.tcb && d->w1img_stale) {   // after create / set_params / sync_target / a DP or small-batch update
             if (d->w1img_stale & 1) {

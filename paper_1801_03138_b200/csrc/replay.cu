@@ -14,6 +14,7 @@
 #include "philox.cuh"
 #include "ring_row.cuh"
 #include "distinct.cuh"
+#include <unordered_set>
 
 namespace rpl {
 
@@ -810,8 +811,7 @@ extern "C" int replay_create(int64_t capacity, int32_t state_dim, const rpl_repl
         (o.state_sharing != 0 && o.state_sharing != 1) ||
         (o.ring_memory != RPL_RING_DEVICE && o.ring_memory != RPL_RING_HOST &&
          o.ring_memory != RPL_RING_HOST_BATCH) ||
-        (o.ring_memory == RPL_RING_HOST_BATCH &&
-         (o.state_dtype != RPL_F32 || o.sampling != RPL_SAMPLE_UNIFORM || o.state_sharing)) ||
+        (o.ring_memory == RPL_RING_HOST_BATCH && (o.state_dtype != RPL_F32 || o.state_sharing)) ||
         o.update_size < 0 || o.update_size > capacity) {
         set_error("replay_create: invalid argument (capacity=%lld state_dim=%d rank=%u burn_in=%lld)",
                   (long long)capacity, state_dim, o.rank, (long long)o.burn_in);
@@ -1061,14 +1061,28 @@ static int host_ring_add(rpl_replay *rp, int64_t k, const float *s, const int32_
 }
 
 // the CPU sampler of RPL_RING_HOST_BATCH: the device sampler's Philox stream (Q3)
+// (distinct sampling, reading Q29 -- the paper's in-RAM `random.sample`: the first B distinct
+// values of the same uniform stream, in stream order; needs size >= B, checked by the callers)
 static void host_sample(const rpl_replay *rp, int B, uint64_t event, int32_t *idx)
 {
     const uint64_t n = (uint64_t)rp->size;
-    for (int i = 0; i < B; i += 2) {
-        int32_t i0, i1;
-        sample_pair(rp->seed, rp->rank, event, (uint32_t)(i / 2), n, i0, i1);
-        idx[i] = i0;
-        if (i + 1 < B) idx[i + 1] = i1;
+    if (!rp->distinct) {
+        for (int i = 0; i < B; i += 2) {
+            int32_t i0, i1;
+            sample_pair(rp->seed, rp->rank, event, (uint32_t)(i / 2), n, i0, i1);
+            idx[i] = i0;
+            if (i + 1 < B) idx[i + 1] = i1;
+        }
+        return;
+    }
+    std::unordered_set<int32_t> seen;
+    seen.reserve((size_t)2 * B);
+    int got = 0;
+    for (uint32_t j = 0; got < B; ++j) {   // stream positions 2j, 2j + 1
+        int32_t v[2];
+        sample_pair(rp->seed, rp->rank, event, j, n, v[0], v[1]);
+        for (int h = 0; h < 2 && got < B; ++h)
+            if (seen.insert(v[h]).second) idx[got++] = v[h];
     }
 }
 

@@ -172,3 +172,25 @@ def test_host_batch_tcgen05_step(b, ddqn):
     for B in (700, 1024, 700):
         assert step_and_compare(b, cfg, dqn, rp, orc, B, seed=7) is not None
     assert dqn.check() == b.RPL_OK and rp.check() == b.RPL_OK
+
+
+@pytest.mark.parametrize("B", [128, 700])
+def test_host_batch_distinct_sampling(b, B):
+    # the paper's in-RAM replay drew its batches with random.sample (without replacement):
+    # RPL_RING_HOST_BATCH with distinct sampling -- the CPU takes the first B distinct values of
+    # the uniform Philox stream (reading Q29), bit-exact against the oracle's distinct ring, and
+    # the train step (mma.sync at 128, tcgen05 at 700) within 1e-5
+    cfg = b.DQNConfig(state_dim=27, n_actions=8, dueling=True, hidden=(128,), stream=512,
+                      double_dqn=True, gamma=0.99, lr=1e-3, huber_kappa=1.0, sync_period=2,
+                      max_batch=1024)
+    rp = b.Replay(1500, 27, seed=9, ring_memory="host_batch", sampling="distinct")
+    orc = oracle.Ring(1500, 27, distinct=True)
+    e = experiences(1500, seed=17)
+    rp.add(**e)
+    orc.add(**e)
+    dqn = b.DQN(cfg, init_params(27, 8, (128,), True, 512, seed=18))
+    for _ in range(3):
+        assert step_and_compare(b, cfg, dqn, rp, orc, B, seed=9) is not None
+    idx = dqn.debug(b.RPL_DBG_IDX, B)
+    assert len(set(idx.tolist())) == B
+    assert dqn.check() == b.RPL_OK and rp.check() == b.RPL_OK
