@@ -1,3 +1,5 @@
+"""One-rank peer-memory learner vs an unattached one, step by step: indices of gradient / weight
+mismatches (debugging the graph-captured exchange; expects none)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch

@@ -1,3 +1,4 @@
+"""Per-phase RPL_TRACE marks of the config-5 wide kernels on a small byte ring (see wide_trace.py)."""
 import os, sys
 os.environ["RPL_TRACE"] = "1"
 sys.path.insert(0, "/root/repo")
