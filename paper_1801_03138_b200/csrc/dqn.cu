@@ -1691,7 +1691,8 @@ static cudaError_t fork_loss(rpl_dqn *d, const FastArgs &p, cudaStream_t st)
         at[0].val.priority = hi;
         lc.attrs = at;
         lc.numAttrs = 1;
-        e = cudaLaunchKernelEx(&lc, loss_out_kernel, p);
+        const LossArgs la{p.loss_part, p.B, p.loss_out};
+        e = cudaLaunchKernelEx(&lc, loss_out_kernel, la);
     }
     if (e == cudaSuccess) e = cudaEventRecord(d->ev_join, d->loss_stream);
     return e;
@@ -2174,7 +2175,7 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                     cudaKernelNodeParams kp = {};
                     e = cudaGraphKernelNodeGetParams(nd, &kp);
                     if (e == cudaSuccess && (kp.func == (void *)sgd_kernel || kp.func == (void *)dp_peer_sgd_kernel ||
-                                             kp.func == (void *)dp_peer_rs_sgd_kernel))
+                                             kp.func == (void *)dp_peer_rs_sgd_kernel || kp.func == (void *)loss_out_kernel))
                         return;   // not a FastArgs kernel
                     if (e == cudaErrorInvalidDeviceFunction) {   // a foreign (NCCL) kernel node: not ours
                         cudaGetLastError();
@@ -2198,10 +2199,17 @@ extern "C" int dqn_train_step(rpl_dqn *d, rpl_replay *rp, int32_t batch, float *
                         update(ge->ds);
                         update(ge->k3);
                     }
-                    if (loss_changed) {
-                        update(ge->k4);
-                        update(ge->kl);   // the loss side branch (null without it)
-                    }
+                    if (loss_changed && !ge->kl) update(ge->k4);
+                }
+                if (loss_changed && ge->kl && e == cudaSuccess) {
+                    // the loss side branch alone writes it (K4 skips it with loss_early)
+                    LossArgs la{fp.loss_part, fp.B, fp.loss_out};
+                    void *largs[] = {&la};
+                    cudaKernelNodeParams kp = {};
+                    e = cudaGraphKernelNodeGetParams(ge->kl, &kp);
+                    kp.kernelParams = largs;
+                    kp.extra = nullptr;
+                    if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(ge->exec, ge->kl, &kp);
                 }
                 if (e == cudaSuccess) ge->args = fp;
             }

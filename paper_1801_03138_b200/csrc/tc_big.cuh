@@ -737,23 +737,29 @@ __global__ void __launch_bounds__(256) tcb_td_kernel(const __grid_constant__ Fas
     }
     const int J = p.J, B = p.B, nut2 = (p.N1 / 128) * tcb::T1_PSL, b0 = blockIdx.x * 8;
     const int nb = min(8, B - b0), span = nb * J, nseg = p.nets * nut2, n = nseg * span;
+    // the sample's action / reward / terminal and the head biases, requested with the partials
+    const int b = b0 + warp;
+    const bool live = b < B;
+    const int ab = live ? p.a[b] : 0;
+    const float rb = live ? p.r[b] : 0.0f;
+    const uint8_t db = live ? p.done[b] : 0;
+    float bias[3];
+#pragma unroll
+    for (int net = 0; net < 3; ++net)
+        bias[net] = (net < p.nets && lane < J) ? __ldg((net == 1 ? p.target : p.online) + p.bh + lane) : 0.0f;
 #pragma unroll 8
     for (int e = threadIdx.x; e < n; e += 256) {
         const int seg = e / span, w = e - seg * span;
         raw[seg * 8 * J + w] = __ldcg(p.part + ((int64_t)seg * B + b0) * J + w);
     }
     __syncthreads();
-    const int b = b0 + warp;
-    if (b >= B) return;
-    const int ab = p.a[b];
-    const float rb = p.r[b];
-    const uint8_t db = p.done[b];
-    for (int net = 0; net < p.nets; ++net) {
-        const float *theta = net == 1 ? p.target : p.online;
-        if (lane < J) {
+    if (!live) return;
+#pragma unroll
+    for (int net = 0; net < 3; ++net) {
+        if (net < p.nets && lane < J) {
             // bias, then the partials in unit-tile order
             const float *src = raw + (int64_t)net * nut2 * 8 * J + warp * J + lane;
-            float v = __ldg(theta + p.bh + lane);
+            float v = bias[net];
             for (int q = 0; q < nut2; ++q) v += src[q * 8 * J];
             hs[warp][net * (F_MAXJ + 1) + lane] = v;
         }

@@ -94,7 +94,7 @@ struct FastArgs {
     float *dZ0;          // [B][N0] dZ0 materialised by K4 for wide_dw0_kernel
     uint16_t *dZ0bf;     // its bf16 hi / mid / lo planes [3][B][N0]
     int event_advanced;  // 1: the step's sampling kernel advanced rctrl[0] already
-    int loss_early;      // 1: loss_out_kernel (a side branch after K2) writes *loss_out, K4 does not
+    int loss_early;      // 1: loss_out_kernel (a side branch after K3) writes *loss_out, K4 does not
     uint32_t *err;
     unsigned long long *trace;   // optional per-CTA [kernel][cta][start, end] %globaltimer (ns)
     int prec;            // rpl_dqn_config.precision (split_p / mma_3xtf32, mma_tf32.cuh)
@@ -1114,11 +1114,27 @@ __global__ void __launch_bounds__(F_NT3) fast_bwd1_kernel(const __grid_constant_
 // the step's loss into the caller's slot (possibly pinned host memory) from a one-CTA kernel on
 // a side branch of the step graph that forks after K3 and joins after K4: the PCIe write and
 // its completion overlap K4 instead of delaying the end of the step's last kernel
-__global__ void __launch_bounds__(256) loss_out_kernel(const __grid_constant__ FastArgs p)
+// (its own small argument struct: the destination changes every step, and a graph node update
+// of a small parameter block is cheaper than one of FastArgs)
+struct LossArgs {
+    const float *loss_part;
+    int B;
+    float *loss_out;
+};
+__global__ void __launch_bounds__(256) loss_out_kernel(const __grid_constant__ LossArgs a)
 {
+    // the batch-mean loss exactly as K4 forms it (block_batch_loss's order)
     __shared__ float red8[8];
-    const float loss = block_batch_loss(p, red8);
-    if (threadIdx.x == 0) *p.loss_out = loss;
+    const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+    float ls = 0.0f;
+    for (int b = tid; b < a.B; b += 256) ls += __ldcg(a.loss_part + b);
+    ls = warp_sum(ls);
+    if (lane == 0) red8[wq] = ls;
+    __syncthreads();
+    float lsum = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) lsum += red8[w];
+    if (tid == 0) *a.loss_out = lsum / (float)a.B;
 }
 
 // ------------------------------------------------------------------------------------------
