@@ -522,7 +522,7 @@ def run_ours(a, batch, first_line=True):
             if k:
                 j = (i % 256) * k
                 rp.add(**{kk: v[j:j + k] for kk, v in pool_h.items()})
-            # the step's loss is stored by the last kernel straight into pinned host memory
+            # the step's loss is stored by a kernel of the step straight into pinned host memory
             # (a 4-byte device -> host write over PCIe; no copy op in the stream)
             dqn.train_step(rp, batch, loss_slots[i])
         e2.record(stream)
@@ -540,7 +540,8 @@ def run_ours(a, batch, first_line=True):
                "us_per_step_device": e2e_ms * 1000.0 / K, "us_per_step_wall": wall * 1e6 / K,
                "note": "replay_add(RPL_HOST) from pageable numpy -> library pinned staging (read "
                        "by the device over PCIe when the step consumes the insert: zero-copy), "
-                       "dqn_train_step whose last kernel writes the loss into pinned host memory, "
+                       "dqn_train_step whose loss side branch (loss_out_kernel, forked after K3 / T3b) "
+                       "writes the loss into pinned host memory, "
                        "every step; slower of CUDA-event and wall time"}
 
     # ---- roofline: the train step as one unit (its FLOPs / the timed ms_per_step) and each
