@@ -1,7 +1,7 @@
 #!/bin/bash
+# a quick GPU check of the large-batch path: parity tests, then per-kernel times and the sweep
 set -u
 OUT=gpurun_out; mkdir -p $OUT
-timeout 1200 python -m pytest tests/test_gpu_train.py tests/test_gpu_tcb.py tests/test_gpu_ring_host.py tests/test_gpu_update_size.py tests/test_gpu_distinct.py tests/test_gpu_nccl.py tests/test_gpu_dp_peer.py -x -q > $OUT/pytest52.txt 2>&1; echo "pytest rc=$?"; tail -2 $OUT/pytest52.txt
-python scripts/loss_branch_check.py > $OUT/lbc52.txt 2>&1
-timeout 600 python bench.py --no-c5 --no-gather --no-cpu-baseline > $OUT/bench52.json 2> $OUT/bench52.err
-timeout 300 python scripts/kernel_times.py --batch 4096 --ddqn > $OUT/kt52_4096.txt 2>&1
+timeout 1200 python -m pytest tests/test_gpu_tcb.py tests/test_gpu_train.py tests/test_gpu_ring_host.py tests/test_gpu_dp_peer.py -x -q > $OUT/pytest_chk.txt 2>&1; echo "pytest rc=$?"; tail -2 $OUT/pytest_chk.txt
+for B in 1024 4096; do timeout 300 python scripts/kernel_times.py --batch $B --ddqn > $OUT/kt_chk_$B.txt 2>&1; done
+timeout 600 python bench.py --ddqn --sweep 640,1024,2048,4096 --steps 1000 --warmup 50 --no-e2e --no-gather --no-cpu-baseline > $OUT/sw_chk.jsonl 2> /dev/null
