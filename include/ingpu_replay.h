@@ -255,12 +255,17 @@ int dqn_destroy(rpl_dqn *dqn);
  * -> gather -> Q_online(s), Q_target(s') [, Q_online(s')] -> TD target, Huber loss ->
  * backward through the online net -> SGD w -= lr * g -> step t += 1 -> target
  * sync when t % sync_period == 0.  One CUDA-graph launch of the fast path's kernels
- * (or one cooperative kernel for other shapes; byte-state wide inputs add their layer-0
- * tensor-core kernels), plus an NCCL all-reduce and an SGD launch when attached to world > 1.  loss_dev (nullable, fp32,
- * device memory or pinned host memory -- the latter is written by the device over PCIe, no
- * copy op) receives the batch-mean Huber loss.  Returns RPL_NOT_READY (nothing
- * enqueued, no counter advanced) while size < burn_in.  Errors: EINVAL (batch < 1 or >
- * max_batch, dims differ from the replay's, different device), ECUDA. */
+ * (four up to B = 512, six tcgen05-based ones from B = 640; one cooperative kernel for other
+ * shapes; byte-state wide inputs add their layer-0 tensor-core kernels).  Data-parallel
+ * learners (world > 1): the gradient mean -- NCCL all-reduce + SGD, or the
+ * peer-memory exchange kernel -- is captured in the same graph on the fast path (launched
+ * after the step's kernels otherwise).  loss_dev (nullable, fp32, device memory or pinned
+ * host memory -- the latter is written by the device over PCIe from a side branch of the
+ * step graph, no copy op; for data-parallel learners the ranks' mean loss) receives the
+ * batch-mean Huber loss.  Returns RPL_NOT_READY (nothing enqueued, no counter advanced)
+ * while size < burn_in.  Errors: EINVAL (batch < 1 or > max_batch, dims differ from the
+ * replay's, different device), ECUDA, ENCCL (an NCCL call failed, or a peer of the
+ * peer-memory exchange did not arrive: the update is skipped on every rank). */
 int dqn_train_step(rpl_dqn *dqn, rpl_replay *replay, int32_t batch, float *loss_dev);
 
 /* target <- online (bit copy), enqueued on the stream. */
