@@ -14,7 +14,7 @@
 #include "philox.cuh"
 #include "ring_row.cuh"
 #include "distinct.cuh"
-#include <unordered_set>
+#include <vector>
 
 namespace rpl {
 
@@ -1075,14 +1075,24 @@ static void host_sample(const rpl_replay *rp, int B, uint64_t event, int32_t *id
         }
         return;
     }
-    std::unordered_set<int32_t> seen;
-    seen.reserve((size_t)2 * B);
+    // an open-addressing set (power-of-two table of 4B slots, linear probing; -1 = empty)
+    static thread_local std::vector<int32_t> table;
+    size_t cap = 16;
+    while (cap < (size_t)4 * B) cap <<= 1;
+    table.assign(cap, -1);
+    const size_t mask = cap - 1;
     int got = 0;
     for (uint32_t j = 0; got < B; ++j) {   // stream positions 2j, 2j + 1
         int32_t v[2];
         sample_pair(rp->seed, rp->rank, event, j, n, v[0], v[1]);
-        for (int h = 0; h < 2 && got < B; ++h)
-            if (seen.insert(v[h]).second) idx[got++] = v[h];
+        for (int h = 0; h < 2 && got < B; ++h) {
+            size_t t = ((uint32_t)v[h] * 2654435761u) & mask;
+            while (table[t] != -1 && table[t] != v[h]) t = (t + 1) & mask;
+            if (table[t] == -1) {
+                table[t] = v[h];
+                idx[got++] = v[h];
+            }
+        }
     }
 }
 
